@@ -1,0 +1,344 @@
+// MixCache on the device: the HostStore (host_store.hpp:61-92) as a pinned,
+// mapped host table indexed by owned row r = f / W, the CacheBuffer
+// (cache_buffer.hpp:40-86) as an HBM slot pool per worker lane, and the
+// manager policy (missing manager.cpp) reproduced exactly:
+//
+//   needed_soon  := owned resident features of the window batches       (mark[s] == t)
+//   hits         := owned resident features of batch t, touched         (last_use[s] = t)
+//   working      := owned non-resident features, in global_ids order    (scan-compacted)
+//   evict        := max(0, |working| - free) eligible slots with the smallest
+//                   (last_use, admit_seq), oldest first; each pushes its slot on the
+//                   LIFO free stack (cache_buffer.cpp:64)
+//   admit        := working[i] takes free_stack[top - 1 - i] (pop order of
+//                   cache_buffer.cpp:41-42), admit_seq = seq0 + i, last_use = t
+//
+// Per-row state moves host <-> HBM by zero-copy loads/stores from the kernels
+// (PCIe); never-touched rows are initialised on the device with the
+// reference's initial_embedding stream (generator.cpp:110-115) instead of
+// being read over PCIe.
+#include "cache.h"
+
+namespace sfb {
+
+namespace {
+
+__global__ void owned_flag_kernel(const uint32_t* __restrict__ gids, int32_t U, uint32_t W,
+                                  uint32_t w, uint32_t* __restrict__ flag) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < U) flag[i] = (gids[i] % W == w) ? 1u : 0u;
+}
+
+__global__ void compact_kernel(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ rank,
+                               int32_t n, uint32_t* __restrict__ out, int32_t* __restrict__ count) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (flag[i]) out[rank[i]] = static_cast<uint32_t>(i);
+  if (i == n - 1) *count = static_cast<int32_t>(rank[i] + flag[i]);
+}
+
+// Probe the owned features of batch t: hits are touched and marked needed_soon,
+// misses flagged for admission.
+__global__ void probe_kernel(const uint32_t* __restrict__ own_k, int32_t n_own,
+                             const uint32_t* __restrict__ gids, uint32_t W,
+                             const uint32_t* __restrict__ index, uint32_t C, int32_t t,
+                             int32_t* __restrict__ last_use, int32_t* __restrict__ mark,
+                             uint32_t* __restrict__ own_slot, uint32_t* __restrict__ miss) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n_own) return;
+  const uint32_t f = gids[own_k[j]];
+  const uint32_t s = index[f / W];
+  if (s < C) {
+    if (t > last_use[s]) last_use[s] = t;  // CacheBuffer::touch (cache_buffer.cpp:69-72)
+    mark[s] = t;
+    own_slot[j] = s;
+    miss[j] = 0;
+  } else {
+    own_slot[j] = kEmpty;
+    miss[j] = 1;
+  }
+}
+
+// needed_soon for resident owned features of a lookahead batch
+__global__ void mark_window_kernel(const uint32_t* __restrict__ gids, int32_t U, uint32_t W,
+                                   uint32_t w, const uint32_t* __restrict__ index, uint32_t C,
+                                   int32_t t, int32_t* __restrict__ mark) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= U) return;
+  const uint32_t f = gids[i];
+  if (f % W != w) return;
+  const uint32_t s = index[f / W];
+  if (s < C) mark[s] = t;
+}
+
+// LRU key per slot: eligible = occupied && !needed_soon (pins are implied by
+// BSP stream order: batch t-1's update has completed before manage(t) runs).
+__global__ void victim_keys_kernel(uint32_t C, const uint32_t* __restrict__ slot_feat,
+                                   const int32_t* __restrict__ mark, int32_t t,
+                                   const int32_t* __restrict__ last_use,
+                                   const uint64_t* __restrict__ admit_seq,
+                                   uint64_t* __restrict__ keys, uint32_t* __restrict__ ids) {
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= C) return;
+  const bool eligible = slot_feat[s] != kEmpty && mark[s] != t;
+  keys[s] = eligible ? (static_cast<uint64_t>(last_use[s] + 1) << 40) |
+                           (admit_seq[s] & ((1ull << 40) - 1))
+                     : ~0ull;
+  ids[s] = s;
+}
+
+// pull_parameters_to_host: one warp per victim, 16 B zero-copy stores to the
+// pinned host table; the slot goes on top of the free stack.
+__global__ void evict_kernel(int32_t n_evict, const uint64_t* __restrict__ sorted_keys,
+                             const uint32_t* __restrict__ sorted_ids, uint32_t* __restrict__ slot_feat,
+                             uint32_t W, int d, const float* __restrict__ emb,
+                             const float* __restrict__ mom, const float* __restrict__ vel,
+                             const int32_t* __restrict__ steps, float* __restrict__ host_rows,
+                             int32_t* __restrict__ host_steps, uint32_t* __restrict__ index,
+                             uint32_t* __restrict__ free_stack, int32_t free_top,
+                             int32_t* __restrict__ err) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= n_evict) return;
+  if (sorted_keys[warp] == ~0ull) {  // fewer eligible slots than needed: capacity deadlock
+    if (lane == 0) *err = 1;
+    return;
+  }
+  const uint32_t s = sorted_ids[warp];
+  const uint32_t f = slot_feat[s];
+  const uint64_t r = f / W;
+  float* dst = host_rows + r * 3 * d;
+  const size_t so = static_cast<size_t>(s) * d;
+  if ((d & 3) == 0) {
+    const int d4 = d >> 2;
+    for (int c = lane; c < 3 * d4; c += 32) {
+      const int which = c / d4, cc = c - which * d4;
+      const float* src = (which == 0 ? emb : which == 1 ? mom : vel) + so;
+      reinterpret_cast<float4*>(dst)[c] = reinterpret_cast<const float4*>(src)[cc];
+    }
+  } else {
+    for (int c = lane; c < 3 * d; c += 32) {
+      const int which = c / d, cc = c - which * d;
+      dst[c] = (which == 0 ? emb : which == 1 ? mom : vel)[so + cc];
+    }
+  }
+  if (lane == 0) {
+    host_steps[r] = steps[s];
+    index[r] = kOnHost;
+    slot_feat[s] = kEmpty;
+    free_stack[free_top + warp] = s;
+  }
+}
+
+// push_parameters_to_cache: one warp per admitted feature.
+__global__ void admit_kernel(int32_t n_work, const uint32_t* __restrict__ work_j,
+                             const uint32_t* __restrict__ own_k, const uint32_t* __restrict__ gids,
+                             uint32_t W, int d, const uint32_t* __restrict__ free_stack,
+                             int32_t free_top, uint32_t* __restrict__ index,
+                             const float* __restrict__ host_rows,
+                             const int32_t* __restrict__ host_steps, uint64_t seed,
+                             uint64_t embed_hash, float* __restrict__ emb, float* __restrict__ mom,
+                             float* __restrict__ vel, int32_t* __restrict__ steps,
+                             uint32_t* __restrict__ slot_feat, int32_t* __restrict__ last_use,
+                             uint64_t* __restrict__ admit_seq, uint64_t seq0,
+                             int32_t* __restrict__ mark, int32_t t,
+                             uint32_t* __restrict__ own_slot, int32_t* __restrict__ n_from_host) {
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= n_work) return;
+  const uint32_t j = work_j[i];
+  const uint32_t f = gids[own_k[j]];
+  const uint64_t r = f / W;
+  const uint32_t s = free_stack[free_top - 1 - i];
+  const size_t so = static_cast<size_t>(s) * d;
+  const uint32_t where = index[r];
+  if (where == kOnHost) {
+    const float* src = host_rows + r * 3 * d;
+    if ((d & 3) == 0) {
+      const int d4 = d >> 2;
+      for (int c = lane; c < 3 * d4; c += 32) {
+        const int which = c / d4, cc = c - which * d4;
+        float* dst = (which == 0 ? emb : which == 1 ? mom : vel) + so;
+        reinterpret_cast<float4*>(dst)[cc] = reinterpret_cast<const float4*>(src)[c];
+      }
+    } else {
+      for (int c = lane; c < 3 * d; c += 32) {
+        const int which = c / d, cc = c - which * d;
+        (which == 0 ? emb : which == 1 ? mom : vel)[so + cc] = src[c];
+      }
+    }
+    if (lane == 0) {
+      steps[s] = host_steps[r];
+      atomicAdd(n_from_host, 1);
+    }
+  } else {
+    // HostStore::get_or_init lazy path (host_store.cpp:25-33)
+    const uint64_t se = derive_seed_h(seed, embed_hash, f);
+    for (int c = lane; c < d; c += 32) {
+      emb[so + c] = static_cast<float>(uniform_from(splitmix_mix(se + (c + 1) * kGolden), -0.01, 0.01));
+      mom[so + c] = 0.f;
+      vel[so + c] = 0.f;
+    }
+    if (lane == 0) steps[s] = 0;
+  }
+  if (lane == 0) {
+    slot_feat[s] = f;
+    last_use[s] = t;
+    admit_seq[s] = seq0 + i;
+    mark[s] = t;
+    index[r] = s;
+    own_slot[j] = s;
+  }
+}
+
+__global__ void init_lane_kernel(uint32_t C, uint32_t* slot_feat, int32_t* last_use,
+                                 int32_t* mark, uint32_t* free_stack) {
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < C; s += gridDim.x * blockDim.x) {
+    slot_feat[s] = kEmpty;
+    last_use[s] = -1;
+    mark[s] = -1;
+    free_stack[s] = C - 1 - s;  // lower slots at the top (cache_buffer.cpp:27-28)
+  }
+}
+
+__global__ void fill_u32(uint32_t* p, uint64_t n, uint32_t v) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    p[i] = v;
+}
+
+}  // namespace
+
+void CacheLane::init(uint64_t capacity, int dim, uint64_t owned_rows, uint64_t host_rows_cap,
+                     int64_t max_unique) {
+  C = capacity;
+  d = dim;
+  rows = owned_rows;
+  host_cap = host_rows_cap;
+  umax = max_unique > 0 ? max_unique : 1;
+  const size_t cd = static_cast<size_t>(C) * d;
+  CUDA_CHECK(cudaMalloc(&emb, sizeof(float) * cd));
+  CUDA_CHECK(cudaMalloc(&mom, sizeof(float) * cd));
+  CUDA_CHECK(cudaMalloc(&vel, sizeof(float) * cd));
+  CUDA_CHECK(cudaMemset(emb, 0, sizeof(float) * cd));
+  CUDA_CHECK(cudaMemset(mom, 0, sizeof(float) * cd));
+  CUDA_CHECK(cudaMemset(vel, 0, sizeof(float) * cd));
+  CUDA_CHECK(cudaMalloc(&steps, sizeof(int32_t) * C));
+  CUDA_CHECK(cudaMemset(steps, 0, sizeof(int32_t) * C));
+  CUDA_CHECK(cudaMalloc(&slot_feat, sizeof(uint32_t) * C));
+  CUDA_CHECK(cudaMalloc(&last_use, sizeof(int32_t) * C));
+  CUDA_CHECK(cudaMalloc(&admit_seq, sizeof(uint64_t) * C));
+  CUDA_CHECK(cudaMemset(admit_seq, 0, sizeof(uint64_t) * C));
+  CUDA_CHECK(cudaMalloc(&mark, sizeof(int32_t) * C));
+  CUDA_CHECK(cudaMalloc(&free_stack, sizeof(uint32_t) * C));
+  CUDA_CHECK(cudaMalloc(&index, sizeof(uint32_t) * rows));
+  init_lane_kernel<<<592, 256>>>(static_cast<uint32_t>(C), slot_feat, last_use, mark, free_stack);
+  CUDA_LAUNCH_CHECK();
+  fill_u32<<<1184, 256>>>(index, rows, kNever);
+  CUDA_LAUNCH_CHECK();
+  // pinned, mapped host table: [emb | m | v] per owned row + adam step counts
+  const size_t hbytes = sizeof(float) * static_cast<size_t>(host_cap) * 3 * d;
+  if (cudaHostAlloc(reinterpret_cast<void**>(&host_rows), hbytes,
+                    cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    fail(kConfig, "cannot pin " + std::to_string(hbytes >> 20) +
+                      " MiB for the host table (set host_rows / vocab smaller)");
+  }
+  CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&host_steps), sizeof(int32_t) * host_cap,
+                           cudaHostAllocMapped | cudaHostAllocPortable));
+  free_top = static_cast<int32_t>(C);
+  next_seq = 0;
+  // per-step scratch
+  CUDA_CHECK(cudaMalloc(&flag, sizeof(uint32_t) * umax));
+  CUDA_CHECK(cudaMalloc(&rank, sizeof(uint32_t) * umax));
+  CUDA_CHECK(cudaMalloc(&own_k, sizeof(uint32_t) * umax));
+  CUDA_CHECK(cudaMalloc(&own_slot, sizeof(uint32_t) * umax));
+  CUDA_CHECK(cudaMalloc(&miss, sizeof(uint32_t) * umax));
+  CUDA_CHECK(cudaMalloc(&miss_rank, sizeof(uint32_t) * umax));
+  CUDA_CHECK(cudaMalloc(&work_j, sizeof(uint32_t) * umax));
+  CUDA_CHECK(cudaMalloc(&keys, sizeof(uint64_t) * C));
+  CUDA_CHECK(cudaMalloc(&keys_sorted, sizeof(uint64_t) * C));
+  CUDA_CHECK(cudaMalloc(&ids, sizeof(uint32_t) * C));
+  CUDA_CHECK(cudaMalloc(&ids_sorted, sizeof(uint32_t) * C));
+  scan_bytes = scan_temp_bytes(umax);
+  sort_bytes = sort_pairs_temp_bytes(static_cast<int64_t>(C));
+  CUDA_CHECK(cudaMalloc(&temp, std::max(scan_bytes, sort_bytes)));
+  CUDA_CHECK(cudaMalloc(&counters, sizeof(int32_t) * 8));
+  CUDA_CHECK(cudaMemset(counters, 0, sizeof(int32_t) * 8));
+  CUDA_CHECK(cudaDeviceSynchronize());
+}
+
+void CacheLane::release() {
+  for (void* p : {static_cast<void*>(emb), static_cast<void*>(mom), static_cast<void*>(vel),
+                  static_cast<void*>(steps), static_cast<void*>(slot_feat),
+                  static_cast<void*>(last_use), static_cast<void*>(admit_seq),
+                  static_cast<void*>(mark), static_cast<void*>(free_stack),
+                  static_cast<void*>(index), static_cast<void*>(flag), static_cast<void*>(rank),
+                  static_cast<void*>(own_k), static_cast<void*>(own_slot), static_cast<void*>(miss),
+                  static_cast<void*>(miss_rank), static_cast<void*>(work_j),
+                  static_cast<void*>(keys), static_cast<void*>(keys_sorted),
+                  static_cast<void*>(ids), static_cast<void*>(ids_sorted), temp,
+                  static_cast<void*>(counters)})
+    if (p) cudaFree(p);
+  if (host_rows) cudaFreeHost(host_rows);
+  if (host_steps) cudaFreeHost(host_steps);
+  *this = CacheLane();
+}
+
+void CacheLane::select_owned(const uint32_t* d_gids, int32_t U, uint32_t W, uint32_t w,
+                             cudaStream_t s) {
+  if (U <= 0) return;
+  owned_flag_kernel<<<ceil_div(U, 256), 256, 0, s>>>(d_gids, U, W, w, flag);
+  CUDA_LAUNCH_CHECK();
+  exclusive_scan_u32(temp, scan_bytes, flag, rank, U, s);
+  compact_kernel<<<ceil_div(U, 256), 256, 0, s>>>(flag, rank, U, own_k, counters + kCntOwned);
+  CUDA_LAUNCH_CHECK();
+}
+
+void CacheLane::mark_window(const uint32_t* d_gids, int32_t U, uint32_t W, uint32_t w, int32_t t,
+                            cudaStream_t s) {
+  if (U <= 0) return;
+  mark_window_kernel<<<ceil_div(U, 256), 256, 0, s>>>(d_gids, U, W, w, index,
+                                                      static_cast<uint32_t>(C), t, mark);
+  CUDA_LAUNCH_CHECK();
+}
+
+void CacheLane::probe(const uint32_t* d_gids, int32_t n_own, uint32_t W, int32_t t,
+                      cudaStream_t s) {
+  if (n_own <= 0) return;
+  probe_kernel<<<ceil_div(n_own, 256), 256, 0, s>>>(own_k, n_own, d_gids, W, index,
+                                                    static_cast<uint32_t>(C), t, last_use, mark,
+                                                    own_slot, miss);
+  CUDA_LAUNCH_CHECK();
+  exclusive_scan_u32(temp, scan_bytes, miss, miss_rank, n_own, s);
+  compact_kernel<<<ceil_div(n_own, 256), 256, 0, s>>>(miss, miss_rank, n_own, work_j,
+                                                      counters + kCntWorking);
+  CUDA_LAUNCH_CHECK();
+}
+
+void CacheLane::evict(int32_t n_evict, uint32_t W, int32_t t, cudaStream_t s) {
+  if (n_evict <= 0) return;
+  victim_keys_kernel<<<ceil_div(C, 256), 256, 0, s>>>(static_cast<uint32_t>(C), slot_feat, mark, t,
+                                                      last_use, admit_seq, keys, ids);
+  CUDA_LAUNCH_CHECK();
+  sort_pairs_u64_u32(temp, sort_bytes, keys, keys_sorted, ids, ids_sorted,
+                     static_cast<int64_t>(C), 64, s);
+  evict_kernel<<<ceil_div(static_cast<int64_t>(n_evict) * 32, 256), 256, 0, s>>>(
+      n_evict, keys_sorted, ids_sorted, slot_feat, W, d, emb, mom, vel, steps, host_rows,
+      host_steps, index, free_stack, free_top, counters + kCntError);
+  CUDA_LAUNCH_CHECK();
+  free_top += n_evict;
+}
+
+void CacheLane::admit(int32_t n_work, const uint32_t* d_gids, uint32_t W, uint64_t seed, int32_t t,
+                      cudaStream_t s) {
+  if (n_work <= 0) return;
+  admit_kernel<<<ceil_div(static_cast<int64_t>(n_work) * 32, 256), 256, 0, s>>>(
+      n_work, work_j, own_k, d_gids, W, d, free_stack, free_top, index, host_rows, host_steps,
+      seed, fnv1a64("embed"), emb, mom, vel, steps, slot_feat, last_use, admit_seq, next_seq, mark,
+      t, own_slot, counters + kCntFromHost);
+  CUDA_LAUNCH_CHECK();
+  free_top -= n_work;
+  next_seq += static_cast<uint64_t>(n_work);
+}
+
+}  // namespace sfb

@@ -1,0 +1,56 @@
+// One worker lane's MixCache state in HBM + its partition of the pinned host
+// table (see cache.cu for the policy and the reference lines it follows).
+#pragma once
+
+#include "ops.h"
+
+namespace sfb {
+
+enum { kCntOwned = 0, kCntWorking = 1, kCntFromHost = 2, kCntError = 3 };
+
+struct CacheLane {
+  uint64_t C = 0;       // slots (cache_capacity)
+  int d = 0;
+  uint64_t rows = 0;    // owned rows = ceil(vocab / W); row r holds feature r*W + w
+  uint64_t host_cap = 0;
+  int64_t umax = 0;     // max uniques per step (scratch sizing)
+
+  // CacheBuffer slots (cache_buffer.hpp:42-50), structure of arrays
+  float* emb = nullptr;        // [C*d]
+  float* mom = nullptr;        // [C*d]
+  float* vel = nullptr;        // [C*d]
+  int32_t* steps = nullptr;    // [C]  ParamEntry::adam_steps
+  uint32_t* slot_feat = nullptr;  // [C] feature, kEmpty when free
+  int32_t* last_use = nullptr;    // [C]
+  uint64_t* admit_seq = nullptr;  // [C]
+  int32_t* mark = nullptr;        // [C] step stamp: needed_soon <=> mark == t
+  uint32_t* free_stack = nullptr; // [C] LIFO free list
+  int32_t free_top = 0;           // host mirror of the free-stack height
+  uint64_t next_seq = 0;          // host mirror of next admit_seq
+  uint32_t* index = nullptr;      // [rows] slot | kOnHost | kNever
+  float* host_rows = nullptr;     // pinned mapped [host_cap * 3d]
+  int32_t* host_steps = nullptr;  // pinned mapped [host_cap]
+
+  // per-step scratch
+  uint32_t *flag = nullptr, *rank = nullptr, *own_k = nullptr, *own_slot = nullptr;
+  uint32_t *miss = nullptr, *miss_rank = nullptr, *work_j = nullptr;
+  uint64_t *keys = nullptr, *keys_sorted = nullptr;
+  uint32_t *ids = nullptr, *ids_sorted = nullptr;
+  void* temp = nullptr;
+  size_t scan_bytes = 0, sort_bytes = 0;
+  int32_t* counters = nullptr;  // [8] device counters (kCnt*)
+
+  void init(uint64_t capacity, int dim, uint64_t owned_rows, uint64_t host_rows_cap,
+            int64_t max_unique);
+  void release();
+
+  void select_owned(const uint32_t* d_gids, int32_t U, uint32_t W, uint32_t w, cudaStream_t s);
+  void mark_window(const uint32_t* d_gids, int32_t U, uint32_t W, uint32_t w, int32_t t,
+                   cudaStream_t s);
+  void probe(const uint32_t* d_gids, int32_t n_own, uint32_t W, int32_t t, cudaStream_t s);
+  void evict(int32_t n_evict, uint32_t W, int32_t t, cudaStream_t s);
+  void admit(int32_t n_work, const uint32_t* d_gids, uint32_t W, uint64_t seed, int32_t t,
+             cudaStream_t s);
+};
+
+}  // namespace sfb

@@ -1,0 +1,103 @@
+// Shared host/device plumbing for the sm_100a kernels: error types that map
+// onto the reference's exception classes (include/sfctr/error.hpp:28-56),
+// CUDA/NCCL check macros, and the counter-based RNG of rng.hpp:27-84 in a
+// form that is bit-exact on the device.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace sfb {
+
+// Status codes of include/sfctr_b200.h.
+enum Status : int { kOk = 0, kConfig = 1, kData = 2, kLogic = 3, kRun = 4, kCuda = 5, kNccl = 6 };
+
+struct Error : std::runtime_error {
+  int status;
+  int64_t step;
+  Error(int s, const std::string& m, int64_t st = -1) : std::runtime_error(m), status(s), step(st) {}
+};
+
+[[noreturn]] inline void fail(int status, const std::string& msg, int64_t step = -1) {
+  throw Error(status, msg, step);
+}
+
+#define SFB_CHECK(cond, msg)                                                              \
+  do {                                                                                    \
+    if (!(cond))                                                                          \
+      ::sfb::fail(::sfb::kLogic, std::string("check failed: ") + #cond + " (" + (msg) + ")"); \
+  } while (0)
+
+#define CUDA_CHECK(expr)                                                                  \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      ::sfb::fail(::sfb::kCuda, std::string(#expr) + ": " + cudaGetErrorString(e_) + " at " + \
+                                    __FILE__ + ":" + std::to_string(__LINE__));           \
+  } while (0)
+
+// kernels launched by this thread (the bench's gpu_launches claim); CUB
+// primitives add their own kernel counts at the call site
+extern thread_local int64_t g_launches;
+#define CUDA_LAUNCH_CHECK()          \
+  do {                               \
+    ++::sfb::g_launches;             \
+    CUDA_CHECK(cudaGetLastError());  \
+  } while (0)
+
+inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+// ---------------- rng.hpp:27-56 (host + device) ----------------
+constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ull;
+
+__host__ __device__ inline uint64_t splitmix_mix(uint64_t z) {  // rng.hpp:38-41
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+__host__ __device__ inline uint64_t splitmix_next(uint64_t& s) {  // rng.hpp:36-42
+  s += kGolden;
+  return splitmix_mix(s);
+}
+
+inline uint64_t fnv1a64(const char* p, size_t n) {  // rng.hpp:27-34
+  uint64_t h = 0xcbf29ce484222325ull;
+  for (size_t i = 0; i < n; ++i) {
+    h ^= static_cast<uint8_t>(p[i]);
+    h *= 0x100000001b3ull;
+  }
+  return h;
+}
+inline uint64_t fnv1a64(const std::string& s) { return fnv1a64(s.data(), s.size()); }
+
+// derive_seed(base, label, index) with fnv1a64(label) precomputed (rng.hpp:49-56).
+__host__ __device__ inline uint64_t derive_seed_h(uint64_t base, uint64_t label_hash,
+                                                  uint64_t index) {
+  uint64_t state = base ^ label_hash;
+  state ^= kGolden * (index + 1);
+  uint64_t out = splitmix_next(state);
+  out = splitmix_next(state) ^ out;
+  return out;
+}
+
+#ifdef __CUDACC__
+// Rng::next_unit (rng.hpp:67): exact in fp64.
+__device__ __forceinline__ double unit_from(uint64_t x) {
+  return __dmul_rn(static_cast<double>(x >> 11), 0x1.0p-53);
+}
+// Rng::next_uniform(lo, hi) = lo + (hi - lo) * unit, rounded step by step as
+// the host does (no FMA contraction, rng.hpp:70).
+__device__ __forceinline__ double uniform_from(uint64_t x, double lo, double hi) {
+  return __dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), unit_from(x)));
+}
+#endif
+
+// Slot / index sentinels of the device MixCache.
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;   // slot_feature of a free slot
+constexpr uint32_t kNever = 0xFFFFFFFFu;   // index[r]: row never touched (lazy init on admit)
+constexpr uint32_t kOnHost = 0xFFFFFFFEu;  // index[r]: row lives in the pinned host table
+
+}  // namespace sfb

@@ -1,0 +1,279 @@
+// Worker ops on the virtual table: the forward gathers and
+// the backward scatter-add are HBM-bound byte movers, so every kernel moves
+// 128-bit vectors with consecutive threads on consecutive 16 B of one
+// embedding row (d=80 -> 20 lanes cover a 320 B row; rows are 16 B aligned).
+#include "kernels.h"
+
+namespace sfb {
+
+namespace {
+
+template <typename T>
+__device__ __forceinline__ T ldg_stream(const T* p) {
+  return __ldcs(p);
+}
+
+__global__ void gather_cache_v4(const uint32_t* __restrict__ own_k,
+                                const uint32_t* __restrict__ own_slot, int32_t n_own, int d4,
+                                const float4* __restrict__ emb, float4* __restrict__ G) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<int64_t>(n_own) * d4) return;
+  const int64_t j = i / d4;
+  const int c = static_cast<int>(i - j * d4);
+  G[static_cast<int64_t>(own_k[j]) * d4 + c] = emb[static_cast<int64_t>(own_slot[j]) * d4 + c];
+}
+
+__global__ void gather_cache_s(const uint32_t* __restrict__ own_k,
+                               const uint32_t* __restrict__ own_slot, int32_t n_own, int d,
+                               const float* __restrict__ emb, float* __restrict__ G) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<int64_t>(n_own) * d) return;
+  const int64_t j = i / d;
+  const int c = static_cast<int>(i - j * d);
+  G[static_cast<int64_t>(own_k[j]) * d + c] = emb[static_cast<int64_t>(own_slot[j]) * d + c];
+}
+
+// Thread per (row, 16 B column chunk); loops over the F fields of the row.
+// Writes X (streaming store: it is consumed once by the tower) and the FM
+// partial sums.
+__global__ void gather_instances_v4(const uint32_t* __restrict__ vid, int32_t rows, int F, int d4,
+                                    const float4* __restrict__ G, float4* __restrict__ X,
+                                    float4* __restrict__ fm_s, float* __restrict__ fm_sqp) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<int64_t>(rows) * d4) return;
+  const int64_t r = i / d4;
+  const int c = static_cast<int>(i - r * d4);
+  const uint32_t* vr = vid + r * F;
+  float4* xr = X + r * F * d4 + c;
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  float sq = 0.f;
+  int f = 0;
+  for (; f + 4 <= F; f += 4) {  // 4 independent row loads in flight
+    const uint32_t v0 = __ldg(vr + f), v1 = __ldg(vr + f + 1), v2 = __ldg(vr + f + 2),
+                   v3 = __ldg(vr + f + 3);
+    const float4 a0 = __ldg(G + static_cast<int64_t>(v0) * d4 + c);
+    const float4 a1 = __ldg(G + static_cast<int64_t>(v1) * d4 + c);
+    const float4 a2 = __ldg(G + static_cast<int64_t>(v2) * d4 + c);
+    const float4 a3 = __ldg(G + static_cast<int64_t>(v3) * d4 + c);
+    xr[(f + 0) * d4] = a0;
+    xr[(f + 1) * d4] = a1;
+    xr[(f + 2) * d4] = a2;
+    xr[(f + 3) * d4] = a3;
+    s.x += a0.x; s.y += a0.y; s.z += a0.z; s.w += a0.w;
+    sq += a0.x * a0.x + a0.y * a0.y + a0.z * a0.z + a0.w * a0.w;
+    s.x += a1.x; s.y += a1.y; s.z += a1.z; s.w += a1.w;
+    sq += a1.x * a1.x + a1.y * a1.y + a1.z * a1.z + a1.w * a1.w;
+    s.x += a2.x; s.y += a2.y; s.z += a2.z; s.w += a2.w;
+    sq += a2.x * a2.x + a2.y * a2.y + a2.z * a2.z + a2.w * a2.w;
+    s.x += a3.x; s.y += a3.y; s.z += a3.z; s.w += a3.w;
+    sq += a3.x * a3.x + a3.y * a3.y + a3.z * a3.z + a3.w * a3.w;
+  }
+  for (; f < F; ++f) {
+    const float4 a = __ldg(G + static_cast<int64_t>(__ldg(vr + f)) * d4 + c);
+    xr[f * d4] = a;
+    s.x += a.x; s.y += a.y; s.z += a.z; s.w += a.w;
+    sq += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w;
+  }
+  fm_s[r * d4 + c] = s;
+  fm_sqp[r * d4 + c] = sq;
+}
+
+__global__ void gather_instances_s(const uint32_t* __restrict__ vid, int32_t rows, int F, int d,
+                                   const float* __restrict__ G, float* __restrict__ X,
+                                   float* __restrict__ fm_s, float* __restrict__ fm_sqp) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<int64_t>(rows) * d) return;
+  const int64_t r = i / d;
+  const int c = static_cast<int>(i - r * d);
+  float s = 0.f, sq = 0.f;
+  for (int f = 0; f < F; ++f) {
+    const float a = G[static_cast<int64_t>(vid[r * F + f]) * d + c];
+    X[(r * F + f) * d + c] = a;
+    s += a;
+    sq += a * a;
+  }
+  fm_s[r * d + c] = s;
+  fm_sqp[r * d + c] = sq;
+}
+
+__global__ void fm_sums_kernel(const float* __restrict__ X, int32_t rows, int F, int d,
+                               float* __restrict__ fm_s, float* __restrict__ fm_sqp, int parts) {
+  // thread per (row, column c); one partial per column (parts == d here)
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<int64_t>(rows) * d) return;
+  const int64_t r = i / d;
+  const int c = static_cast<int>(i - r * d);
+  float s = 0.f, sq = 0.f;
+  for (int f = 0; f < F; ++f) {
+    const float a = X[(r * F + f) * d + c];
+    s += a;
+    sq += a * a;
+  }
+  fm_s[r * d + c] = s;
+  // fold columns onto `parts` partial slots (parts divides d handling below)
+  if (parts == d) fm_sqp[r * d + c] = sq;
+  else atomicAdd(fm_sqp + r * parts + (c / 4), sq);
+}
+
+__global__ void segment_sum_v4(const uint32_t* __restrict__ vid, int32_t n, int d4,
+                               const float4* __restrict__ dX, float* __restrict__ dG) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<int64_t>(n) * d4) return;
+  const int64_t p = i / d4;
+  const int c = static_cast<int>(i - p * d4);
+  const float4 g = __ldcs(dX + i);
+  float* dst = dG + (static_cast<int64_t>(__ldg(vid + p)) * d4 + c) * 4;
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(g.x), "f"(g.y),
+               "f"(g.z), "f"(g.w)
+               : "memory");
+}
+
+__global__ void segment_sum_s(const uint32_t* __restrict__ vid, int32_t n, int d,
+                              const float* __restrict__ dX, float* __restrict__ dG) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<int64_t>(n) * d) return;
+  const int64_t p = i / d;
+  const int c = static_cast<int>(i - p * d);
+  atomicAdd(dG + static_cast<int64_t>(vid[p]) * d + c, dX[i]);
+}
+
+// Lazy Adam: t = adam_steps + 1 per row; bias
+// corrections 1 - beta^t from host-built fp64 tables.
+__global__ void sparse_adam_kernel(const uint32_t* __restrict__ own_k,
+                                   const uint32_t* __restrict__ own_slot, int32_t n_own, int d,
+                                   const float* __restrict__ dG, float* __restrict__ emb,
+                                   float* __restrict__ mom, float* __restrict__ vel,
+                                   const int32_t* __restrict__ steps, const float* __restrict__ bc1,
+                                   const float* __restrict__ bc2, float lr, float b1, float b2,
+                                   float omb1, float omb2, float eps) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<int64_t>(n_own) * d) return;
+  const int64_t j = i / d;
+  const int c = static_cast<int>(i - j * d);
+  const uint32_t s = own_slot[j];
+  const int t = steps[s] + 1;
+  const float g = dG[static_cast<int64_t>(own_k[j]) * d + c];
+  const int64_t o = static_cast<int64_t>(s) * d + c;
+  const float m = b1 * mom[o] + omb1 * g;
+  const float v = b2 * vel[o] + omb2 * g * g;
+  mom[o] = m;
+  vel[o] = v;
+  const float mh = m / bc1[t], vh = v / bc2[t];
+  emb[o] -= lr * mh / (sqrtf(vh) + eps);
+}
+
+__global__ void sparse_adam_v4(const uint32_t* __restrict__ own_k,
+                               const uint32_t* __restrict__ own_slot, int32_t n_own, int d4,
+                               const float4* __restrict__ dG, float4* __restrict__ emb,
+                               float4* __restrict__ mom, float4* __restrict__ vel,
+                               const int32_t* __restrict__ steps, const float* __restrict__ bc1,
+                               const float* __restrict__ bc2, float lr, float b1, float b2,
+                               float omb1, float omb2, float eps) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<int64_t>(n_own) * d4) return;
+  const int64_t j = i / d4;
+  const int c = static_cast<int>(i - j * d4);
+  const uint32_t s = __ldg(own_slot + j);
+  const int t = __ldg(steps + s) + 1;
+  const float c1 = __ldg(bc1 + t), c2 = __ldg(bc2 + t);
+  const float4 g = __ldg(dG + static_cast<int64_t>(__ldg(own_k + j)) * d4 + c);
+  const int64_t o = static_cast<int64_t>(s) * d4 + c;
+  float4 m = mom[o], v = vel[o], e = emb[o];
+#define SFB_ADAM(X)                                   \
+  m.X = b1 * m.X + omb1 * g.X;                        \
+  v.X = b2 * v.X + omb2 * g.X * g.X;                  \
+  e.X -= lr * (m.X / c1) / (sqrtf(v.X / c2) + eps);
+  SFB_ADAM(x) SFB_ADAM(y) SFB_ADAM(z) SFB_ADAM(w)
+#undef SFB_ADAM
+  mom[o] = m;
+  vel[o] = v;
+  emb[o] = e;
+}
+
+__global__ void steps_inc_kernel(const uint32_t* __restrict__ own_slot, int32_t n_own,
+                                 int32_t* __restrict__ steps) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n_own) steps[own_slot[j]] += 1;
+}
+
+}  // namespace
+
+int fm_sq_parts(int d) { return (d & 3) == 0 ? d / 4 : d; }
+
+void gather_cache(const uint32_t* own_k, const uint32_t* own_slot, int32_t n_own, const float* emb,
+                  int d, float* G, cudaStream_t s) {
+  if (n_own <= 0) return;
+  if ((d & 3) == 0) {
+    const int64_t n = static_cast<int64_t>(n_own) * (d / 4);
+    gather_cache_v4<<<ceil_div(n, 256), 256, 0, s>>>(own_k, own_slot, n_own, d / 4,
+                                                     reinterpret_cast<const float4*>(emb),
+                                                     reinterpret_cast<float4*>(G));
+  } else {
+    const int64_t n = static_cast<int64_t>(n_own) * d;
+    gather_cache_s<<<ceil_div(n, 256), 256, 0, s>>>(own_k, own_slot, n_own, d, emb, G);
+  }
+  CUDA_LAUNCH_CHECK();
+}
+
+void gather_instances(const uint32_t* vid, int32_t rows, int F, int d, const float* G, float* X,
+                      float* fm_s, float* fm_sqp, cudaStream_t s) {
+  if (rows <= 0) return;
+  if ((d & 3) == 0) {
+    const int64_t n = static_cast<int64_t>(rows) * (d / 4);
+    gather_instances_v4<<<ceil_div(n, 256), 256, 0, s>>>(
+        vid, rows, F, d / 4, reinterpret_cast<const float4*>(G), reinterpret_cast<float4*>(X),
+        reinterpret_cast<float4*>(fm_s), fm_sqp);
+  } else {
+    const int64_t n = static_cast<int64_t>(rows) * d;
+    gather_instances_s<<<ceil_div(n, 256), 256, 0, s>>>(vid, rows, F, d, G, X, fm_s, fm_sqp);
+  }
+  CUDA_LAUNCH_CHECK();
+}
+
+void fm_sums(const float* X, int32_t rows, int F, int d, float* fm_s, float* fm_sqp,
+             cudaStream_t s) {
+  const int parts = fm_sq_parts(d);
+  if (parts != d) CUDA_CHECK(cudaMemsetAsync(fm_sqp, 0, sizeof(float) * rows * parts, s));
+  const int64_t n = static_cast<int64_t>(rows) * d;
+  fm_sums_kernel<<<ceil_div(n, 256), 256, 0, s>>>(X, rows, F, d, fm_s, fm_sqp, parts);
+  CUDA_LAUNCH_CHECK();
+}
+
+void segment_sum(const uint32_t* vid, int32_t n, int d, const float* dX, float* dG,
+                 cudaStream_t s) {
+  if (n <= 0) return;
+  if ((d & 3) == 0) {
+    const int64_t m = static_cast<int64_t>(n) * (d / 4);
+    segment_sum_v4<<<ceil_div(m, 256), 256, 0, s>>>(vid, n, d / 4,
+                                                    reinterpret_cast<const float4*>(dX), dG);
+  } else {
+    const int64_t m = static_cast<int64_t>(n) * d;
+    segment_sum_s<<<ceil_div(m, 256), 256, 0, s>>>(vid, n, d, dX, dG);
+  }
+  CUDA_LAUNCH_CHECK();
+}
+
+void sparse_adam(const uint32_t* own_k, const uint32_t* own_slot, int32_t n_own, const float* dG,
+                 int d, float* emb, float* mom, float* vel, int32_t* steps, const float* bc1,
+                 const float* bc2, float lr, float beta1, float beta2, float eps, cudaStream_t s) {
+  if (n_own <= 0) return;
+  const float omb1 = static_cast<float>(1.0 - static_cast<double>(beta1));
+  const float omb2 = static_cast<float>(1.0 - static_cast<double>(beta2));
+  if ((d & 3) == 0) {
+    const int64_t n = static_cast<int64_t>(n_own) * (d / 4);
+    sparse_adam_v4<<<ceil_div(n, 256), 256, 0, s>>>(
+        own_k, own_slot, n_own, d / 4, reinterpret_cast<const float4*>(dG),
+        reinterpret_cast<float4*>(emb), reinterpret_cast<float4*>(mom),
+        reinterpret_cast<float4*>(vel), steps, bc1, bc2, lr, beta1, beta2, omb1, omb2, eps);
+  } else {
+    const int64_t n = static_cast<int64_t>(n_own) * d;
+    sparse_adam_kernel<<<ceil_div(n, 256), 256, 0, s>>>(own_k, own_slot, n_own, d, dG, emb, mom,
+                                                        vel, steps, bc1, bc2, lr, beta1, beta2,
+                                                        omb1, omb2, eps);
+  }
+  CUDA_LAUNCH_CHECK();
+  steps_inc_kernel<<<ceil_div(n_own, 256), 256, 0, s>>>(own_slot, n_own, steps);
+  CUDA_LAUNCH_CHECK();
+}
+
+}  // namespace sfb

@@ -1,0 +1,61 @@
+// Host-side launchers of the sm_100a kernels (one .cu per subsystem).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "common.cuh"
+
+namespace sfb {
+
+// ---------------- generator.cu — SyntheticGenerator (generator.cpp:32-115) ----------------
+struct GenTables {
+  int fields = 0;
+  uint64_t vocab = 0, seed = 0, base = 0;
+  double zipf = 0, truth_scale = 0;
+  uint64_t* d_shard_starts = nullptr;  // [F+1]
+  double* d_cdf_base = nullptr;        // [base]
+  double* d_cdf_big = nullptr;         // [base+1] or null
+  double* d_tw = nullptr;              // scratch truth weights [max_ids]
+  int64_t tw_cap = 0;
+  std::vector<uint64_t> shard_starts;  // host copy
+  void build(int fields, uint64_t vocab, uint64_t seed, double zipf);  // host CDFs (std::pow)
+  void release();
+};
+void generate_rows(GenTables& g, int64_t step, int32_t row0, int32_t nrows, uint64_t* d_features,
+                   uint8_t* d_labels, cudaStream_t s);
+void initial_embedding_device(uint64_t seed, uint64_t feature, int dim, double* d_out,
+                              cudaStream_t s);
+
+// ---------------- vsi.cu — virtual_sparse_id (vsi.cpp:23-54) ----------------
+struct VsiScratch {
+  uint64_t key_space = 0;
+  int64_t cap = 0;                 // max ids per call
+  uint32_t* d_first = nullptr;     // [key_space] first position per feature, 0xFFFFFFFF = unseen
+  uint32_t* d_flag = nullptr;      // [cap]
+  uint32_t* d_rank = nullptr;      // [cap]
+  void* d_cub = nullptr;           // CUB temp storage
+  size_t cub_bytes = 0;
+  void init(uint64_t key_space, int64_t cap);
+  void release();
+};
+// ids u32 [n] -> global_ids u32 [U] (first-appearance order), vids u32 [n], *d_unique.
+void vsi_device(VsiScratch& v, const uint32_t* d_ids, int64_t n, uint32_t* d_gids,
+                uint32_t* d_vids, int32_t* d_unique, cudaStream_t s);
+// u64 -> u32 with range check; *d_bad set to 1 when any id >= limit
+void ids_to_u32(const uint64_t* d_in, uint32_t* d_out, int64_t n, uint64_t limit, int32_t* d_bad,
+                cudaStream_t s);
+void u32_to_u64(const uint32_t* d_in, uint64_t* d_out, int64_t n, cudaStream_t s);
+
+// ---------------- scan helpers (CUB) ----------------
+size_t scan_temp_bytes(int64_t n);
+void exclusive_scan_u32(void* temp, size_t temp_bytes, const uint32_t* in, uint32_t* out,
+                        int64_t n, cudaStream_t s);
+size_t sort_pairs_temp_bytes(int64_t n);
+void sort_pairs_u64_u32(void* temp, size_t temp_bytes, const uint64_t* keys_in, uint64_t* keys_out,
+                        const uint32_t* vals_in, uint32_t* vals_out, int64_t n, int end_bit,
+                        cudaStream_t s);
+
+}  // namespace sfb

@@ -1,0 +1,520 @@
+// One process = one GPU = `lanes` worker lanes of Algorithm 1.
+// The step is the reference's BSP step in stream order:
+//
+//   ids u64->u32 | allgather ids (NCCL) | VSI | [host: U]
+//   per lane: owned select, window marks, probe          | [host: n_own, n_work]
+//   per lane: evict (LRU sort + write-back), admit (fill / lazy init)
+//   gather_cache -> G | allreduce G (NCCL)
+//   per lane: gather_instances(+FM sums) -> tower fwd/bwd -> segment_sum -> dG
+//   allreduce dG + dense grads (NCCL) | per lane sparse Adam | dense Adam
+//
+// The two host waits ("[host: ...]") read the few counts that size the NCCL
+// payloads and the eviction sort; everything else is asynchronous.
+#include "trainer.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+
+namespace sfb {
+
+thread_local int64_t g_launches = 0;
+
+namespace {
+__global__ void finalize_loss_kernel(const float* sum, float inv_w, float* out) {
+  if (threadIdx.x == 0) *out = *sum * inv_w;
+}
+__global__ void dense_init_kernel(float* p, int64_t n, uint64_t stream_seed, double a) {
+  // W ~ U(-a, a) from the counter-based stream derive_seed(seed, label, 0)
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n)
+    p[i] = static_cast<float>(
+        uniform_from(splitmix_mix(stream_seed + static_cast<uint64_t>(i + 1) * kGolden), -a, a));
+}
+}  // namespace
+
+void validate_config(const sfctr_config& c) {  // config.cpp:55-78 + device limits
+  auto require = [](bool ok, const char* msg) {
+    if (!ok) fail(kConfig, msg);
+  };
+  require(c.num_workers > 0, "workers must be positive");
+  require(c.embedding_dim > 0, "dim must be positive");
+  require(c.num_fields > 0, "fields must be positive");
+  require(c.batch_size_per_worker > 0, "batch-size must be positive");
+  require(c.vocabulary_size > 0, "vocab must be positive");
+  require(c.cache_capacity > 0, "cache-capacity must be positive");
+  require(c.lookahead_depth > 0, "lookahead must be positive");
+  require(c.hidden_dim > 0, "hidden must be positive");
+  require(c.learning_rate > 0, "lr must be positive");
+  require(c.adam_beta1 > 0 && c.adam_beta1 < 1, "beta1 must be in (0,1)");
+  require(c.adam_beta2 > 0 && c.adam_beta2 < 1, "beta2 must be in (0,1)");
+  require(c.adam_epsilon > 0, "epsilon must be positive");
+  require(c.zipf_exponent >= 0, "zipf exponent must be non-negative");
+  require(c.vocabulary_size >= static_cast<uint64_t>(c.num_fields),
+          "vocab must be at least the number of fields (fields use disjoint vocabulary shards)");
+  // device-path limits
+  require(c.strategy == SFCTR_STRATEGY_CACHE,
+          "the device path implements the cache strategy (host/prefetch are simulator-only)");
+  require(c.vocabulary_size < 0xFFFFFFF0ull, "vocab must fit 32-bit device feature ids");
+  require(c.cache_capacity < 0xFFFFFFF0ull, "cache-capacity must fit 32-bit slots");
+  require(static_cast<int64_t>(c.num_workers) * c.batch_size_per_worker * c.num_fields <
+              (1ll << 31),
+          "global batch ids must fit 31 bits");
+  require(c.sync_mode == SFCTR_SYNC_ALLREDUCE || c.sync_mode == SFCTR_SYNC_ALLTOALL,
+          "sync must be allreduce or alltoall");
+}
+
+Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nccl_id, int device)
+    : cfg_(cfg), rank_(rank), world_(world), dev_(device) {
+  validate_config(cfg_);
+  if (world < 1 || rank < 0 || rank >= world) fail(kConfig, "bad rank/world");
+  if (cfg_.num_workers % world != 0) fail(kConfig, "workers must be a multiple of the process count");
+  W_ = cfg_.num_workers;
+  lanes_ = W_ / world;
+  lane0_ = rank * lanes_;
+  d_ = cfg_.embedding_dim;
+  F_ = cfg_.num_fields;
+  b_ = cfg_.batch_size_per_worker;
+  H_ = cfg_.hidden_dim;
+  K_ = F_ * d_;
+  n_local_ = static_cast<int64_t>(lanes_) * b_ * F_;
+  n_global_ = static_cast<int64_t>(W_) * b_ * F_;
+  P_ = static_cast<size_t>(K_) * H_ + 2 * H_ + 1;
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    fail(kCuda, "no CUDA device available (the device path has no CPU fallback)");
+  }
+  CUDA_CHECK(cudaSetDevice(device));
+  CUDA_CHECK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  if (world_ > 1) {
+    if (!nccl_id) fail(kConfig, "world > 1 needs an NCCL unique id");
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    NCCL_CHECK(ncclCommInitRank(&comm_, world_, id, rank_));
+  }
+
+  vsi_.init(cfg_.vocabulary_size, n_global_);
+  CUDA_CHECK(cudaMalloc(&d_in_feat_, sizeof(uint64_t) * n_local_));
+  CUDA_CHECK(cudaMalloc(&d_in_lab_, static_cast<size_t>(lanes_) * b_));
+  if (cfg_.lookahead_depth > 1)
+    CUDA_CHECK(cudaMalloc(&d_in_win_, sizeof(uint64_t) * n_local_ * (cfg_.lookahead_depth - 1)));
+  CUDA_CHECK(cudaMalloc(&d_ids32_, sizeof(uint32_t) * n_local_));
+  CUDA_CHECK(cudaMalloc(&d_gids_, sizeof(uint32_t) * n_global_));
+  CUDA_CHECK(cudaMalloc(&d_uniq_, sizeof(uint32_t) * n_global_));
+  CUDA_CHECK(cudaMalloc(&d_vid_, sizeof(uint32_t) * n_global_));
+  CUDA_CHECK(cudaMalloc(&d_scalars_, sizeof(int32_t) * 8));
+  CUDA_CHECK(cudaMemset(d_scalars_, 0, sizeof(int32_t) * 8));
+  if (cfg_.lookahead_depth > 1) {
+    CUDA_CHECK(cudaMalloc(&d_wuniq_, sizeof(uint32_t) * n_global_));
+    CUDA_CHECK(cudaMalloc(&d_wvid_, sizeof(uint32_t) * n_global_));
+  }
+  const size_t gd = static_cast<size_t>(n_global_) * d_;
+  CUDA_CHECK(cudaMalloc(&d_G_, sizeof(float) * gd));
+  CUDA_CHECK(cudaMalloc(&d_dG_, sizeof(float) * gd));
+  const size_t bk = static_cast<size_t>(b_) * K_;
+  CUDA_CHECK(cudaMalloc(&d_X_, sizeof(float) * bk));
+  CUDA_CHECK(cudaMalloc(&d_dX_, sizeof(float) * bk));
+  CUDA_CHECK(cudaMalloc(&d_fm_s_, sizeof(float) * b_ * d_));
+  CUDA_CHECK(cudaMalloc(&d_fm_sqp_, sizeof(float) * b_ * d_));
+  CUDA_CHECK(cudaMalloc(&d_logits_, sizeof(float) * lanes_ * b_));
+  CUDA_CHECK(cudaMalloc(&d_dense_, sizeof(float) * P_));
+  CUDA_CHECK(cudaMalloc(&d_dense_m_, sizeof(float) * P_));
+  CUDA_CHECK(cudaMalloc(&d_dense_v_, sizeof(float) * P_));
+  CUDA_CHECK(cudaMalloc(&d_grads_, sizeof(float) * (P_ + 1)));
+  CUDA_CHECK(cudaMalloc(&d_loss_, sizeof(float)));
+  CUDA_CHECK(cudaMemset(d_dense_, 0, sizeof(float) * P_));
+  CUDA_CHECK(cudaMemset(d_dense_m_, 0, sizeof(float) * P_));
+  CUDA_CHECK(cudaMemset(d_dense_v_, 0, sizeof(float) * P_));
+  // dense init (identical on every process: pure function of the seed)
+  const int64_t kh = static_cast<int64_t>(K_) * H_;
+  dense_init_kernel<<<ceil_div(kh, 256), 256, 0, stream_>>>(
+      d_dense_, kh, derive_seed_h(cfg_.seed, fnv1a64("dense_w1"), 0),
+      std::sqrt(6.0 / static_cast<double>(K_ + H_)));
+  CUDA_LAUNCH_CHECK();
+  dense_init_kernel<<<ceil_div(H_, 256), 256, 0, stream_>>>(
+      d_dense_ + kh + H_, H_, derive_seed_h(cfg_.seed, fnv1a64("dense_w2"), 0),
+      std::sqrt(6.0 / static_cast<double>(H_ + 1)));
+  CUDA_LAUNCH_CHECK();
+  CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_scalars_), sizeof(int32_t) * 8, 0));
+  CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_counts_), sizeof(int32_t) * 8 * lanes_, 0));
+  CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_loss_), sizeof(float), 0));
+  tower_.init(b_, K_, H_, d_);
+
+  const uint64_t owned_rows = (cfg_.vocabulary_size + W_ - 1) / W_;
+  const uint64_t host_rows = cfg_.host_table_rows ? cfg_.host_table_rows : owned_rows;
+  if (host_rows < owned_rows)
+    fail(kConfig, "host_rows must cover ceil(vocab / workers) rows (direct-mapped host table)");
+  lane_.resize(lanes_);
+  const int64_t umax = std::min<int64_t>(n_global_, static_cast<int64_t>(cfg_.vocabulary_size));
+  for (int l = 0; l < lanes_; ++l)
+    lane_[l].init(cfg_.cache_capacity, d_, owned_rows, host_rows, umax);
+  ensure_bias_tables(1024);
+  CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+Trainer::~Trainer() {
+  cudaSetDevice(dev_);
+  if (stream_) cudaStreamSynchronize(stream_);
+  for (auto& l : lane_) l.release();
+  tower_.release();
+  vsi_.release();
+  for (void* p : {static_cast<void*>(d_in_feat_), static_cast<void*>(d_in_lab_),
+                  static_cast<void*>(d_in_win_), static_cast<void*>(d_ids32_),
+                  static_cast<void*>(d_gids_), static_cast<void*>(d_uniq_),
+                  static_cast<void*>(d_vid_), static_cast<void*>(d_scalars_),
+                  static_cast<void*>(d_wuniq_), static_cast<void*>(d_wvid_),
+                  static_cast<void*>(d_G_), static_cast<void*>(d_dG_), static_cast<void*>(d_X_),
+                  static_cast<void*>(d_dX_), static_cast<void*>(d_fm_s_),
+                  static_cast<void*>(d_fm_sqp_), static_cast<void*>(d_logits_),
+                  static_cast<void*>(d_dense_), static_cast<void*>(d_dense_m_),
+                  static_cast<void*>(d_dense_v_), static_cast<void*>(d_grads_),
+                  static_cast<void*>(d_loss_), static_cast<void*>(d_bc1_),
+                  static_cast<void*>(d_bc2_)})
+    if (p) cudaFree(p);
+  if (h_scalars_) cudaFreeHost(h_scalars_);
+  if (h_counts_) cudaFreeHost(h_counts_);
+  if (h_loss_) cudaFreeHost(h_loss_);
+  for (auto e : ev_) cudaEventDestroy(e);
+  if (comm_) ncclCommDestroy(comm_);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Trainer::ensure_bias_tables(int64_t t_max) {
+  if (t_max < bc_cap_) return;
+  int64_t cap = std::max<int64_t>(1024, bc_cap_);
+  while (cap <= t_max) cap *= 2;
+  std::vector<float> b1(cap + 1), b2(cap + 1);
+  for (int64_t t = 0; t <= cap; ++t) {  // 1 - beta^t in fp64, stored fp32
+    b1[t] = static_cast<float>(1.0 - std::pow(cfg_.adam_beta1, static_cast<double>(t)));
+    b2[t] = static_cast<float>(1.0 - std::pow(cfg_.adam_beta2, static_cast<double>(t)));
+  }
+  CUDA_CHECK(cudaStreamSynchronize(stream_));
+  if (d_bc1_) cudaFree(d_bc1_);
+  if (d_bc2_) cudaFree(d_bc2_);
+  CUDA_CHECK(cudaMalloc(&d_bc1_, sizeof(float) * (cap + 1)));
+  CUDA_CHECK(cudaMalloc(&d_bc2_, sizeof(float) * (cap + 1)));
+  CUDA_CHECK(cudaMemcpy(d_bc1_, b1.data(), sizeof(float) * (cap + 1), cudaMemcpyHostToDevice));
+  CUDA_CHECK(cudaMemcpy(d_bc2_, b2.data(), sizeof(float) * (cap + 1), cudaMemcpyHostToDevice));
+  bc_cap_ = cap;
+}
+
+void Trainer::phase(const char* name) {
+  if (!timing_) return;
+  cudaEvent_t e;
+  CUDA_CHECK(cudaEventCreate(&e));
+  CUDA_CHECK(cudaEventRecord(e, stream_));
+  ev_.push_back(e);
+  ev_names_.emplace_back(name);
+}
+
+void Trainer::finish_phases() {
+  if (!timing_ || ev_.size() < 2) return;
+  CUDA_CHECK(cudaEventSynchronize(ev_.back()));
+  phase_ms_.clear();
+  for (size_t i = 1; i < ev_.size(); ++i) {
+    float ms = 0;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, ev_[i - 1], ev_[i]));
+    phase_ms_.emplace_back(ev_names_[i], ms);
+  }
+  for (auto e : ev_) cudaEventDestroy(e);
+  ev_.clear();
+  ev_names_.clear();
+}
+
+void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_t* d_labels,
+                          const uint64_t* d_window, float* d_loss) {
+  CUDA_CHECK(cudaSetDevice(dev_));
+  const int64_t launches0 = g_launches;
+  const int32_t t = static_cast<int32_t>(step);
+  const uint32_t Wu = static_cast<uint32_t>(W_);
+  cudaStream_t s = stream_;
+  if (step < 0 || step >= (1ll << 23)) fail(kLogic, "step index out of the supported range");
+  if (cfg_.lookahead_depth > 1 && !d_window)
+    fail(kLogic, "lookahead > 1 needs the window batches");
+  for (auto& e : ev_) cudaEventDestroy(e);
+  ev_.clear();
+  ev_names_.clear();
+  phase("start");
+  stats_ = sfctr_step_stats{};
+
+  // ---- Data-Loader: ids to u32, all-gather the global batch, VSI (Algorithm 1 l.2-3)
+  CUDA_CHECK(cudaMemsetAsync(d_scalars_, 0, sizeof(int32_t) * 8, s));
+  ids_to_u32(d_features, d_ids32_, n_local_, cfg_.vocabulary_size, d_scalars_ + 1, s);
+  const uint32_t* gids = d_ids32_;
+  if (world_ > 1) {
+    NCCL_CHECK(ncclAllGather(d_ids32_, d_gids_, static_cast<size_t>(n_local_), ncclUint32, comm_, s));
+    gids = d_gids_;
+    stats_.nvlink_bytes += n_local_ * 4;
+  }
+  phase("ids_allgather");
+  vsi_device(vsi_, gids, n_global_, d_uniq_, d_vid_, d_scalars_ + 0, s);
+  phase("vsi");
+  // window batches (needed_soon), one at a time through the window scratch
+  const int nwin = cfg_.lookahead_depth - 1;
+  std::vector<int32_t> wU(nwin, 0);
+  CUDA_CHECK(cudaMemcpyAsync(h_scalars_, d_scalars_, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  const int32_t U = h_scalars_[0];
+  if (h_scalars_[1]) fail(kLogic, "feature id >= vocabulary size in the batch", step);
+  stats_.unique = U;
+
+  // ---- Host-Manager: MixCache per lane (Algorithm 1 l.4-7)
+  CUDA_CHECK(cudaMemsetAsync(d_scalars_ + 2, 0, sizeof(int32_t) * 6, s));
+  for (int l = 0; l < lanes_; ++l) {
+    CUDA_CHECK(cudaMemsetAsync(lane_[l].counters, 0, sizeof(int32_t) * 8, s));
+    lane_[l].select_owned(d_uniq_, U, Wu, static_cast<uint32_t>(lane0_ + l), s);
+  }
+  for (int j = 0; j < nwin; ++j) {
+    const uint64_t* wfeat = d_window + static_cast<size_t>(j) * n_local_;
+    ids_to_u32(wfeat, d_ids32_, n_local_, cfg_.vocabulary_size, d_scalars_ + 1, s);
+    const uint32_t* wg = d_ids32_;
+    if (world_ > 1) {
+      NCCL_CHECK(ncclAllGather(d_ids32_, d_gids_, static_cast<size_t>(n_local_), ncclUint32, comm_, s));
+      wg = d_gids_;
+    }
+    vsi_device(vsi_, wg, n_global_, d_wuniq_, d_wvid_, d_scalars_ + 2, s);
+    CUDA_CHECK(cudaMemcpyAsync(h_scalars_ + 2, d_scalars_ + 2, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    wU[j] = h_scalars_[2];
+    for (int l = 0; l < lanes_; ++l)
+      lane_[l].mark_window(d_wuniq_, wU[j], Wu, static_cast<uint32_t>(lane0_ + l), t, s);
+  }
+  // owned counts (needed to size the probe)
+  for (int l = 0; l < lanes_; ++l)
+    CUDA_CHECK(cudaMemcpyAsync(h_counts_ + 8 * l, lane_[l].counters, sizeof(int32_t) * 8,
+                               cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  std::vector<int32_t> n_own(lanes_), n_work(lanes_);
+  for (int l = 0; l < lanes_; ++l) {
+    n_own[l] = h_counts_[8 * l + kCntOwned];
+    lane_[l].probe(d_uniq_, n_own[l], Wu, t, s);
+  }
+  phase("manage_probe");
+  for (int l = 0; l < lanes_; ++l)
+    CUDA_CHECK(cudaMemcpyAsync(h_counts_ + 8 * l, lane_[l].counters, sizeof(int32_t) * 8,
+                               cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  for (int l = 0; l < lanes_; ++l) {
+    n_work[l] = n_own[l] > 0 ? h_counts_[8 * l + kCntWorking] : 0;
+    CacheLane& L = lane_[l];
+    const int32_t n_evict = std::max<int32_t>(0, n_work[l] - L.free_top);
+    L.evict(n_evict, Wu, t, s);
+    L.admit(n_work[l], d_uniq_, Wu, cfg_.seed, t, s);
+    led_[0] += static_cast<int64_t>(n_work[l]) * d_ * 12;
+    led_[1] += static_cast<int64_t>(n_evict) * d_ * 12;
+    led_[3] += n_evict;
+    stats_.owned += n_own[l];
+    stats_.working += n_work[l];
+    stats_.evicted += n_evict;
+    stats_.pcie_d2h_bytes += static_cast<int64_t>(n_evict) * (3 * d_ + 1) * 4;
+  }
+  phase("manage_evict_admit");
+
+  // ---- GPU-Worker forward (Algorithm 1 l.9-11)
+  const size_t ud = static_cast<size_t>(U) * d_;
+  if (world_ > 1) CUDA_CHECK(cudaMemsetAsync(d_G_, 0, sizeof(float) * ud, s));
+  for (int l = 0; l < lanes_; ++l)
+    gather_cache(lane_[l].own_k, lane_[l].own_slot, n_own[l], lane_[l].emb, d_, d_G_, s);
+  phase("gather_cache");
+  if (world_ > 1) {
+    NCCL_CHECK(ncclAllReduce(d_G_, d_G_, ud, ncclFloat32, ncclSum, comm_, s));
+    stats_.nvlink_bytes += static_cast<int64_t>(ud) * 4;
+  }
+  // interworker ledger: allreduce_bytes per worker for each all-reduce
+  auto arb = [&](int64_t payload) { return 2 * static_cast<int64_t>(W_ - 1) * payload / W_; };
+  led_[2] += static_cast<int64_t>(lanes_) * arb(static_cast<int64_t>(ud) * 4);
+  phase("allreduce_embed");
+
+  // ---- per lane: gather_instances, forward_backward, segment_sum (l.11-12)
+  CUDA_CHECK(cudaMemsetAsync(d_dG_, 0, sizeof(float) * ud, s));
+  const float emb_scale = 1.f / static_cast<float>(W_);
+  for (int l = 0; l < lanes_; ++l) {
+    const uint32_t* vid = d_vid_ + static_cast<size_t>(lane0_ + l) * b_ * F_;
+    const uint8_t* lab = d_labels + static_cast<size_t>(l) * b_;
+    gather_instances(vid, b_, F_, d_, d_G_, d_X_, d_fm_s_, d_fm_sqp_, s);
+    phase("gather_instances");
+    tower_forward_backward(tower_, d_X_, d_fm_s_, d_fm_sqp_, lab, b_, F_, d_, d_dense_,
+                           d_logits_ + static_cast<size_t>(l) * b_, d_dX_, emb_scale, d_grads_,
+                           l > 0, s);
+    phase("tower");
+    segment_sum(vid, b_ * F_, d_, d_dX_, d_dG_, s);
+    phase("segment_sum");
+  }
+
+  // ---- grad_synchronize (l.13)
+  if (world_ > 1) {
+    NCCL_CHECK(ncclAllReduce(d_dG_, d_dG_, ud, ncclFloat32, ncclSum, comm_, s));
+    NCCL_CHECK(ncclAllReduce(d_grads_, d_grads_, P_ + 1, ncclFloat32, ncclSum, comm_, s));
+    stats_.nvlink_bytes += static_cast<int64_t>(ud + P_ + 1) * 4;
+  }
+  led_[2] += static_cast<int64_t>(lanes_) *
+             (arb(static_cast<int64_t>(ud) * 4) + arb(static_cast<int64_t>(P_) * 4));
+  phase("allreduce_grad");
+
+  // ---- update_sparse (l.14) + dense Adam
+  ensure_bias_tables(steps_done_ + 2);
+  for (int l = 0; l < lanes_; ++l)
+    sparse_adam(lane_[l].own_k, lane_[l].own_slot, n_own[l], d_dG_, d_, lane_[l].emb,
+                lane_[l].mom, lane_[l].vel, lane_[l].steps, d_bc1_, d_bc2_,
+                static_cast<float>(cfg_.learning_rate), static_cast<float>(cfg_.adam_beta1),
+                static_cast<float>(cfg_.adam_beta2), static_cast<float>(cfg_.adam_epsilon), s);
+  phase("sparse_adam");
+  dense_steps_ += 1;
+  const double bc1 = 1.0 - std::pow(cfg_.adam_beta1, static_cast<double>(dense_steps_));
+  const double bc2 = 1.0 - std::pow(cfg_.adam_beta2, static_cast<double>(dense_steps_));
+  dense_adam(d_dense_, d_dense_m_, d_dense_v_, d_grads_, static_cast<int64_t>(P_),
+             1.f / static_cast<float>(W_), static_cast<float>(cfg_.learning_rate),
+             static_cast<float>(cfg_.adam_beta1), static_cast<float>(cfg_.adam_beta2),
+             static_cast<float>(cfg_.adam_epsilon), static_cast<float>(bc1),
+             static_cast<float>(bc2), s);
+  finalize_loss_kernel<<<1, 32, 0, s>>>(d_grads_ + P_, 1.f / static_cast<float>(W_),
+                                        d_loss ? d_loss : d_loss_);
+  CUDA_LAUNCH_CHECK();
+  phase("dense_adam");
+  steps_done_ += 1;
+  stats_.kernel_launches = g_launches - launches0;
+}
+
+void Trainer::check_device_errors(int64_t step) {
+  for (int l = 0; l < lanes_; ++l) {
+    int32_t c[8];
+    CUDA_CHECK(cudaMemcpy(c, lane_[l].counters, sizeof(c), cudaMemcpyDeviceToHost));
+    if (c[kCntError]) {
+      const auto& L = lane_[l];
+      fail(kRun,
+           "capacity deadlock: fewer evictable slots than the working set needs (capacity=" +
+               std::to_string(L.C) + " free=" + std::to_string(L.free_top) + ")",
+           step);
+    }
+    stats_.filled_from_host += c[kCntFromHost];
+  }
+  stats_.pcie_h2d_bytes = stats_.filled_from_host * (3 * d_ + 1) * 4;
+}
+
+double Trainer::step_host(int64_t step, const uint64_t* features, const uint8_t* labels,
+                          const uint64_t* window) {
+  CUDA_CHECK(cudaSetDevice(dev_));
+  CUDA_CHECK(cudaMemcpyAsync(d_in_feat_, features, sizeof(uint64_t) * n_local_,
+                             cudaMemcpyHostToDevice, stream_));
+  CUDA_CHECK(cudaMemcpyAsync(d_in_lab_, labels, static_cast<size_t>(lanes_) * b_,
+                             cudaMemcpyHostToDevice, stream_));
+  if (window && cfg_.lookahead_depth > 1)
+    CUDA_CHECK(cudaMemcpyAsync(d_in_win_, window,
+                               sizeof(uint64_t) * n_local_ * (cfg_.lookahead_depth - 1),
+                               cudaMemcpyHostToDevice, stream_));
+  step_device(step, d_in_feat_, d_in_lab_, window ? d_in_win_ : nullptr, d_loss_);
+  CUDA_CHECK(cudaMemcpyAsync(h_loss_, d_loss_, sizeof(float), cudaMemcpyDeviceToHost, stream_));
+  CUDA_CHECK(cudaStreamSynchronize(stream_));
+  check_device_errors(step);
+  finish_phases();
+  return static_cast<double>(*h_loss_);
+}
+
+void Trainer::synchronize() {
+  CUDA_CHECK(cudaSetDevice(dev_));
+  CUDA_CHECK(cudaStreamSynchronize(stream_));
+  check_device_errors(steps_done_ - 1);
+  finish_phases();
+}
+
+void Trainer::logits(float* out) {
+  CUDA_CHECK(cudaStreamSynchronize(stream_));
+  CUDA_CHECK(cudaMemcpy(out, d_logits_, sizeof(float) * lanes_ * b_, cudaMemcpyDeviceToHost));
+}
+
+void Trainer::cache_slots(int lane, uint64_t* feature, int64_t* last_use, uint64_t* admit_seq) {
+  CUDA_CHECK(cudaStreamSynchronize(stream_));
+  const CacheLane& L = lane_.at(lane);
+  std::vector<uint32_t> f(L.C);
+  std::vector<int32_t> lu(L.C);
+  CUDA_CHECK(cudaMemcpy(f.data(), L.slot_feat, sizeof(uint32_t) * L.C, cudaMemcpyDeviceToHost));
+  CUDA_CHECK(cudaMemcpy(lu.data(), L.last_use, sizeof(int32_t) * L.C, cudaMemcpyDeviceToHost));
+  if (admit_seq)
+    CUDA_CHECK(cudaMemcpy(admit_seq, L.admit_seq, sizeof(uint64_t) * L.C, cudaMemcpyDeviceToHost));
+  for (uint64_t i = 0; i < L.C; ++i) {
+    if (feature) feature[i] = f[i] == kEmpty ? ~0ull : f[i];
+    if (last_use) last_use[i] = lu[i];
+  }
+}
+
+int64_t Trainer::snapshot(uint64_t* features, float* rows, int64_t* steps) {
+  CUDA_CHECK(cudaStreamSynchronize(stream_));
+  struct Src {
+    int lane;
+    uint32_t where;  // slot or kOnHost
+    uint64_t r;
+  };
+  std::map<uint64_t, Src> all;
+  for (int l = 0; l < lanes_; ++l) {
+    const CacheLane& L = lane_[l];
+    std::vector<uint32_t> idx(L.rows);
+    CUDA_CHECK(cudaMemcpy(idx.data(), L.index, sizeof(uint32_t) * L.rows, cudaMemcpyDeviceToHost));
+    for (uint64_t r = 0; r < L.rows; ++r) {
+      if (idx[r] == kNever) continue;
+      all[r * W_ + (lane0_ + l)] = Src{l, idx[r], r};
+    }
+  }
+  if (!features) return static_cast<int64_t>(all.size());
+  const int d3 = 3 * d_;
+  std::vector<std::vector<float>> ce(lanes_), cm(lanes_), cv(lanes_);
+  std::vector<std::vector<int32_t>> cs(lanes_);
+  if (rows || steps)
+    for (int l = 0; l < lanes_; ++l) {
+      const CacheLane& L = lane_[l];
+      const size_t cd = static_cast<size_t>(L.C) * d_;
+      ce[l].resize(cd);
+      cm[l].resize(cd);
+      cv[l].resize(cd);
+      cs[l].resize(L.C);
+      CUDA_CHECK(cudaMemcpy(ce[l].data(), L.emb, sizeof(float) * cd, cudaMemcpyDeviceToHost));
+      CUDA_CHECK(cudaMemcpy(cm[l].data(), L.mom, sizeof(float) * cd, cudaMemcpyDeviceToHost));
+      CUDA_CHECK(cudaMemcpy(cv[l].data(), L.vel, sizeof(float) * cd, cudaMemcpyDeviceToHost));
+      CUDA_CHECK(cudaMemcpy(cs[l].data(), L.steps, sizeof(int32_t) * L.C, cudaMemcpyDeviceToHost));
+    }
+  int64_t i = 0;
+  for (const auto& [f, src] : all) {
+    features[i] = f;
+    const CacheLane& L = lane_[src.lane];
+    if (rows) {
+      float* o = rows + static_cast<size_t>(i) * d3;
+      if (src.where == kOnHost) {
+        std::memcpy(o, L.host_rows + src.r * d3, sizeof(float) * d3);
+      } else {
+        const size_t so = static_cast<size_t>(src.where) * d_;
+        std::memcpy(o, ce[src.lane].data() + so, sizeof(float) * d_);
+        std::memcpy(o + d_, cm[src.lane].data() + so, sizeof(float) * d_);
+        std::memcpy(o + 2 * d_, cv[src.lane].data() + so, sizeof(float) * d_);
+      }
+    }
+    if (steps) steps[i] = src.where == kOnHost ? L.host_steps[src.r] : cs[src.lane][src.where];
+    ++i;
+  }
+  return i;
+}
+
+void Trainer::get_dense(float* w1, float* b1, float* w2, float* b2) {
+  CUDA_CHECK(cudaStreamSynchronize(stream_));
+  const size_t kh = static_cast<size_t>(K_) * H_;
+  if (w1) CUDA_CHECK(cudaMemcpy(w1, d_dense_, sizeof(float) * kh, cudaMemcpyDeviceToHost));
+  if (b1) CUDA_CHECK(cudaMemcpy(b1, d_dense_ + kh, sizeof(float) * H_, cudaMemcpyDeviceToHost));
+  if (w2) CUDA_CHECK(cudaMemcpy(w2, d_dense_ + kh + H_, sizeof(float) * H_, cudaMemcpyDeviceToHost));
+  if (b2) CUDA_CHECK(cudaMemcpy(b2, d_dense_ + kh + 2 * H_, sizeof(float), cudaMemcpyDeviceToHost));
+}
+
+void Trainer::set_dense(const float* w1, const float* b1, const float* w2, const float* b2) {
+  CUDA_CHECK(cudaStreamSynchronize(stream_));
+  const size_t kh = static_cast<size_t>(K_) * H_;
+  if (w1) CUDA_CHECK(cudaMemcpy(d_dense_, w1, sizeof(float) * kh, cudaMemcpyHostToDevice));
+  if (b1) CUDA_CHECK(cudaMemcpy(d_dense_ + kh, b1, sizeof(float) * H_, cudaMemcpyHostToDevice));
+  if (w2) CUDA_CHECK(cudaMemcpy(d_dense_ + kh + H_, w2, sizeof(float) * H_, cudaMemcpyHostToDevice));
+  if (b2) CUDA_CHECK(cudaMemcpy(d_dense_ + kh + 2 * H_, b2, sizeof(float), cudaMemcpyHostToDevice));
+}
+
+void Trainer::ledger(int64_t out[4]) const {
+  for (int i = 0; i < 4; ++i) out[i] = led_[i];
+}
+
+}  // namespace sfb

@@ -1,0 +1,109 @@
+// The per-process training engine behind sfctr_trainer_* (include/sfctr_b200.h).
+#pragma once
+
+#include <nccl.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/sfctr_b200.h"
+#include "cache.h"
+#include "kernels.h"
+
+namespace sfb {
+
+#define NCCL_CHECK(expr)                                                                  \
+  do {                                                                                    \
+    ncclResult_t r_ = (expr);                                                             \
+    if (r_ != ncclSuccess)                                                                \
+      ::sfb::fail(::sfb::kNccl, std::string(#expr) + ": " + ncclGetErrorString(r_));      \
+  } while (0)
+
+void validate_config(const sfctr_config& c);
+
+class Trainer {
+ public:
+  Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nccl_id, int device);
+  ~Trainer();
+
+  // one BSP step over this process's rows; inputs on the device
+  void step_device(int64_t step, const uint64_t* d_features, const uint8_t* d_labels,
+                   const uint64_t* d_window, float* d_loss);
+  // host-buffer variant: H2D copies, step, loss read back
+  double step_host(int64_t step, const uint64_t* features, const uint8_t* labels,
+                   const uint64_t* window);
+  void synchronize();
+
+  cudaStream_t stream() const { return stream_; }
+  int lanes() const { return lanes_; }
+  int rows() const { return lanes_ * cfg_.batch_size_per_worker; }
+
+  void logits(float* out);
+  void cache_slots(int lane, uint64_t* feature, int64_t* last_use, uint64_t* admit_seq);
+  uint64_t free_count(int lane) const { return static_cast<uint64_t>(lane_.at(lane).free_top); }
+  int64_t snapshot(uint64_t* features, float* rows, int64_t* steps);
+  void get_dense(float* w1, float* b1, float* w2, float* b2);
+  void set_dense(const float* w1, const float* b1, const float* w2, const float* b2);
+  void ledger(int64_t out[4]) const;
+  sfctr_step_stats stats() const { return stats_; }
+  void set_timing(bool on) { timing_ = on; }
+  const std::vector<std::pair<std::string, float>>& phase_times() const { return phase_ms_; }
+
+ private:
+  void ensure_bias_tables(int64_t t_max);
+  void phase(const char* name);
+  void finish_phases();
+  void check_device_errors(int64_t step);
+
+  sfctr_config cfg_;
+  int rank_, world_, lanes_, W_, lane0_, dev_;
+  int d_, F_, b_, H_, K_;
+  int64_t n_local_, n_global_;  // ids per step: this process / whole global batch
+  size_t P_;                    // dense parameter count
+  cudaStream_t stream_ = nullptr;
+  ncclComm_t comm_ = nullptr;
+
+  VsiScratch vsi_;
+  uint64_t* d_in_feat_ = nullptr;   // staging for host inputs
+  uint8_t* d_in_lab_ = nullptr;
+  uint64_t* d_in_win_ = nullptr;
+  uint32_t* d_ids32_ = nullptr;     // local ids, u32
+  uint32_t* d_gids_ = nullptr;      // global batch ids (all-gathered)
+  uint32_t* d_uniq_ = nullptr;      // global_ids [U]
+  uint32_t* d_vid_ = nullptr;       // virtual ids [n_global]
+  int32_t* d_scalars_ = nullptr;    // [0]=U, [1]=bad id flag, [2..]=window U
+  uint32_t* d_wuniq_ = nullptr;     // window batch uniques (one batch at a time)
+  uint32_t* d_wvid_ = nullptr;
+  float* d_G_ = nullptr;            // global common embedding [U x d]
+  float* d_dG_ = nullptr;           // global common gradients [U x d]
+  float* d_X_ = nullptr;            // minibatch embeddings [b x K]
+  float* d_dX_ = nullptr;
+  float* d_fm_s_ = nullptr;
+  float* d_fm_sqp_ = nullptr;
+  float* d_logits_ = nullptr;       // [rows]
+  float* d_dense_ = nullptr;        // [P] = W1 | b1 | w2 | b2
+  float* d_dense_m_ = nullptr;
+  float* d_dense_v_ = nullptr;
+  float* d_grads_ = nullptr;        // [P + 1] (+ loss sum)
+  float* d_loss_ = nullptr;
+  float* d_bc1_ = nullptr;          // sparse Adam bias-correction tables [t_cap + 1]
+  float* d_bc2_ = nullptr;
+  int64_t bc_cap_ = 0, bc_filled_ = 0;
+  int32_t* h_scalars_ = nullptr;    // pinned mirrors
+  int32_t* h_counts_ = nullptr;     // [lanes * 8]
+  float* h_loss_ = nullptr;
+
+  std::vector<CacheLane> lane_;
+  TowerBufs tower_;
+  int64_t dense_steps_ = 0;
+  int64_t steps_done_ = 0;
+  int64_t led_[4] = {0, 0, 0, 0};
+  sfctr_step_stats stats_{};
+
+  bool timing_ = false;
+  std::vector<cudaEvent_t> ev_;
+  std::vector<std::string> ev_names_;
+  std::vector<std::pair<std::string, float>> phase_ms_;
+};
+
+}  // namespace sfb

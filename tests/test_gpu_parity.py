@@ -1,0 +1,311 @@
+"""GPU parity tests: the sm_100a path through the C-ABI vs the CPU oracle.
+
+Bars (stated per test):
+  * integer / index work — generator ids and labels, VSI global/virtual ids,
+    cache slot tables (slot -> feature, last_use, admit_seq), free counts,
+    lazy-Adam step counts, the TransferLedger — must be BIT-EXACT;
+  * floating point — the device computes in fp32 against the oracle's fp64:
+    loss within rtol 1e-5; logits |dz| <= 1e-5 * (1 + |z|); embedding rows
+    and Adam moments |a - b| <= 1e-5 * (max|row| + 1e-3) per row after a few
+    steps (the scatter-add and all-reduce order differ from the oracle).
+"""
+import ctypes as C
+import hashlib
+
+import numpy as np
+import pytest
+
+import paper_2104_08542_b200 as sb
+from oracle_lib import OrcConfig, oracle, oracle_generate, oracle_vsi
+
+pytestmark = pytest.mark.gpu
+
+
+def sha(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).view(np.uint8).tobytes())
+    return h.hexdigest()
+
+
+# ---------------- generator / init ----------------
+
+def test_generator_golden(golden):
+    for rec in golden["batches"]:
+        cfg = sb.Config(num_workers=rec["workers"], batch_size_per_worker=rec["batch"],
+                        num_fields=rec["fields"], vocabulary_size=rec["vocab"], seed=rec["seed"],
+                        zipf_exponent=rec["zipf"])
+        g = sb.SyntheticGenerator(cfg)
+        f, y = g.generate(rec["step"])
+        assert sha(f) == rec["features_sha256"], rec["name"]
+        assert sha(y) == rec["labels_sha256"], rec["name"]
+        g.close()
+
+
+def test_generator_row_ranges_match_oracle():
+    cfg = sb.Config(num_workers=4, batch_size_per_worker=300, num_fields=13, vocabulary_size=77777,
+                    seed=11, zipf_exponent=0.9)
+    g = sb.SyntheticGenerator(cfg)
+    for step in (0, 3, 1000):
+        full_f, full_y = oracle_generate(1200, 13, 77777, 11, 0.9, step)
+        for r0, n in ((0, 1200), (300, 300), (1199, 1), (17, 500)):
+            f, y = g.generate(step, r0, n)
+            assert np.array_equal(f, full_f[r0 * 13:(r0 + n) * 13])
+            assert np.array_equal(y, full_y[r0:r0 + n])
+
+
+def test_initial_embedding_golden(golden):
+    import struct
+    for f, want in golden["initial_embedding_seed7_d80"].items():
+        v = sb.initial_embedding(7, int(f), 80)
+        assert [struct.pack("<d", x).hex() for x in v] == want
+
+
+# ---------------- VSI ----------------
+
+def test_vsi_golden_and_spec(golden):
+    for ex in golden["vsi_examples"]:
+        g, v, _ = sb.virtual_sparse_id(np.array(ex["features"], np.uint64), ex["rows"], ex["fields"])
+        assert g.tolist() == ex["global_ids"] and v.tolist() == ex["virtual_ids"]
+    for rec in golden["batches"]:
+        cfg = sb.Config(num_workers=rec["workers"], batch_size_per_worker=rec["batch"],
+                        num_fields=rec["fields"], vocabulary_size=rec["vocab"], seed=rec["seed"],
+                        zipf_exponent=rec["zipf"])
+        f, _ = sb.SyntheticGenerator(cfg).generate(rec["step"])
+        rows = rec["workers"] * rec["batch"]
+        g, v, rr = sb.virtual_sparse_id(f, rows, rec["fields"], rec["workers"],
+                                        key_space=rec["vocab"])
+        assert len(g) == rec["unique"]
+        assert sha(g) == rec["global_ids_sha256"] and sha(v) == rec["virtual_ids_sha256"]
+        assert rr.ravel().tolist() == rec["row_ranges"]
+
+
+def test_vsi_random_and_edge_cases():
+    rng = np.random.default_rng(0)
+    ctx = sb.VirtualSparseId(1 << 20, 1 << 16)
+    cases = [np.array([5], np.uint64), np.zeros(64, np.uint64),
+             np.arange(4096, dtype=np.uint64)[::-1].copy(),
+             np.full(1 << 16, (1 << 20) - 1, np.uint64)]
+    for _ in range(200):
+        n = int(rng.integers(1, 3000))
+        cases.append(rng.integers(0, int(rng.integers(1, 1 << 20)), n).astype(np.uint64))
+    for f in cases:
+        g, v, _ = ctx(f, f.size, 1)
+        go, vo = oracle_vsi(f, f.size, 1)
+        assert np.array_equal(g, go) and np.array_equal(v, vo)
+        assert np.array_equal(g[v.astype(np.int64)], f)  # roundtrip
+    with pytest.raises(sb.LogicError):
+        ctx(np.array([1 << 20], np.uint64), 1, 1)  # outside the key space
+    with pytest.raises(sb.LogicError):
+        ctx(np.arange(6, dtype=np.uint64), 3, 2, num_workers=2)  # uneven split
+    with pytest.raises(sb.LogicError):
+        ctx(np.zeros(0, np.uint64), 0, 2)  # empty batch
+
+
+# ---------------- DeepFM-lite ----------------
+
+def test_model_forward_backward_vs_oracle():
+    O = oracle()
+    rng = np.random.default_rng(2)
+    for rows, F, d, H in ((3, 2, 2, 3), (37, 5, 6, 20), (256, 26, 16, 64), (130, 39, 80, 64)):
+        K = F * d
+        x = rng.uniform(-0.05, 0.05, (rows, K)).astype(np.float32)
+        y = rng.integers(0, 2, rows).astype(np.uint8)
+        w1 = np.zeros(K * H)
+        b1 = np.zeros(H)
+        w2 = np.zeros(H)
+        b2 = np.zeros(1)
+        O.orc_dense_init(7, K, H, w1, b1, w2, b2)
+        b1 = rng.normal(0, 0.05, H)
+        w1f, b1f, w2f = w1.astype(np.float32), b1.astype(np.float32), w2.astype(np.float32)
+        xd = x.astype(np.float64)
+        w1d, b1d, w2d = w1f.astype(np.float64), b1f.astype(np.float64), w2f.astype(np.float64)
+        lg = np.zeros(rows)
+        dx = np.zeros(rows * K)
+        dw1 = np.zeros(K * H)
+        db1 = np.zeros(H)
+        dw2 = np.zeros(H)
+        db2 = np.zeros(1)
+        loss = O.orc_model_fwd_bwd(xd.ravel(), y, rows, F, d, H, w1d, b1d, w2d, 0.01,
+                                   lg.ctypes.data, dx.ctypes.data, dw1.ctypes.data,
+                                   db1.ctypes.data, dw2.ctypes.data, db2.ctypes.data, 1)
+        out = sb.model_forward_backward(x, y, w1f, b1f, w2f, np.float32([0.01]), F, d, H)
+        assert abs(out["loss"] - loss) <= 1e-5 * abs(loss)
+        assert np.all(np.abs(out["logits"] - lg) <= 1e-5 * (1 + np.abs(lg)))
+        for name, ref in (("dx", dx), ("dw1", dw1), ("db1", db1), ("dw2", dw2)):
+            got = np.asarray(out[name], np.float64).ravel()
+            scale = np.max(np.abs(ref)) + 1e-30
+            assert np.max(np.abs(got - ref)) <= 1e-4 * scale, name
+        assert abs(out["db2"] - db2[0]) <= 1e-4 * (abs(db2[0]) + np.max(np.abs(dw2)) + 1e-30)
+
+
+# ---------------- the trainer vs the oracle's simulated system ----------------
+
+def orc_cfg(cfg):
+    c = OrcConfig()
+    oracle().orc_config_default(c)
+    for k in ("num_workers", "embedding_dim", "num_fields", "batch_size_per_worker",
+              "vocabulary_size", "cache_capacity", "lookahead_depth", "seed", "learning_rate",
+              "adam_beta1", "adam_beta2", "adam_epsilon", "zipf_exponent", "hidden_dim"):
+        setattr(c, k, getattr(cfg, k))
+    return c
+
+
+def orc_slots(s, w, cap):
+    f = np.zeros(cap, np.uint64)
+    lu = np.zeros(cap, np.int64)
+    seq = np.zeros(cap, np.uint64)
+    oracle().orc_sim_cache_slots(s, w, f, lu, seq)
+    return f, lu, seq
+
+
+def orc_snapshot(s, d):
+    O = oracle()
+    n = O.orc_sim_snapshot(s, None, None, None)
+    f = np.zeros(n, np.uint64)
+    rows = np.zeros((n, 3 * d))
+    st = np.zeros(n, np.int64)
+    O.orc_sim_snapshot(s, f.ctypes.data, rows.ctypes.data, st.ctypes.data)
+    return f, rows, st
+
+
+def run_parity(cfg, steps, check_rows=True, row_tol=1e-5):
+    O = oracle()
+    oc = orc_cfg(cfg)
+    sim = O.orc_sim_create(C.byref(oc))
+    tr = sb.Trainer(cfg)
+    W, b, F, L = cfg.num_workers, cfg.batch_size_per_worker, cfg.num_fields, cfg.lookahead_depth
+    gen = sb.SyntheticGenerator(cfg)
+    evictions = 0
+    for t in range(steps):
+        f, y = gen.generate(t)
+        win = None
+        if L > 1:
+            win = np.concatenate([gen.generate(t + j)[0] for j in range(1, L)])
+        loss = tr.step(t, f, y, window=win)
+        ol = C.c_double()
+        logits = np.zeros(W * b)
+        rc = O.orc_sim_step(sim, t, f, y, win.ctypes.data if win is not None else None,
+                            L - 1 if win is not None else 0, C.byref(ol), None, logits.ctypes.data)
+        assert rc == 0, O.orc_last_error()
+        assert abs(loss - ol.value) <= 1e-5 * abs(ol.value), (t, loss, ol.value)
+        if t == 0:  # logits are compared from the identical initial state
+            lg = tr.logits()
+            assert np.all(np.abs(lg - logits) <= 1e-5 * (1 + np.abs(logits)))
+        # cache indexing: bit-exact per lane
+        for w in range(W):
+            df, dlu, dseq = tr.cache_slots(w)
+            of, olu, oseq = orc_slots(sim, w, cfg.cache_capacity)
+            assert np.array_equal(df, of), (t, w)
+            occ = of != np.iinfo(np.uint64).max
+            assert np.array_equal(dlu[occ], olu[occ]) and np.array_equal(dseq[occ], oseq[occ])
+            assert tr.free_count(w) == O.orc_sim_free_count(sim, w)
+        led = np.zeros(4, np.int64)
+        O.orc_sim_ledger(sim, led)
+        dl = tr.ledger()
+        assert [dl["host_to_worker"], dl["worker_to_host"], dl["interworker"],
+                dl["swap_events"]] == led.tolist(), t
+        evictions = dl["swap_events"]
+        assert tr.stats()["unique"] == O.orc_sim_last_unique(sim)
+    if check_rows:
+        df, drows, dst = tr.snapshot()
+        of, orows, ost = orc_snapshot(sim, cfg.embedding_dim)
+        assert np.array_equal(df, of) and np.array_equal(dst, ost)
+        err = np.abs(drows.astype(np.float64) - orows)
+        scale = np.max(np.abs(orows), axis=1, keepdims=True) + 1e-3
+        assert np.max(err / scale) <= row_tol, float(np.max(err / scale))
+        # dense parameters
+        K, H = cfg.num_fields * cfg.embedding_dim, cfg.hidden_dim
+        w1, b1, w2, b2 = tr.get_dense()
+        ow1, ob1, ow2, ob2 = np.zeros(K * H), np.zeros(H), np.zeros(H), np.zeros(1)
+        O.orc_sim_dense(sim, ow1, ob1, ow2, ob2)
+        assert np.max(np.abs(w1 - ow1)) <= 1e-5 * (np.max(np.abs(ow1)) + 1e-3)
+    O.orc_sim_destroy(sim)
+    tr.close()
+    return evictions
+
+
+def test_trainer_single_worker_with_evictions():
+    cfg = sb.Config(num_workers=1, batch_size_per_worker=64, num_fields=8, embedding_dim=8,
+                    vocabulary_size=5000, cache_capacity=700, hidden_dim=16, zipf_exponent=1.1)
+    assert run_parity(cfg, 8) > 0
+
+
+def test_trainer_four_lanes_one_process():
+    cfg = sb.Config(num_workers=4, batch_size_per_worker=32, num_fields=6, embedding_dim=4,
+                    vocabulary_size=3000, cache_capacity=260, hidden_dim=8, zipf_exponent=1.0)
+    assert run_parity(cfg, 8) > 0
+
+
+def test_trainer_odd_dim_and_no_eviction():
+    cfg = sb.Config(num_workers=2, batch_size_per_worker=16, num_fields=5, embedding_dim=6,
+                    vocabulary_size=100000, cache_capacity=20000, hidden_dim=3)
+    assert run_parity(cfg, 4) == 0
+
+
+def test_trainer_lookahead_two():
+    cfg = sb.Config(num_workers=2, batch_size_per_worker=16, num_fields=4, embedding_dim=4,
+                    vocabulary_size=800, cache_capacity=120, hidden_dim=8, lookahead_depth=2)
+    run_parity(cfg, 8)
+
+
+def test_trainer_cfg1_shape():
+    """BASELINE configs[0]: 26 fields, d=16, 1M vocab, batch 1024, single worker."""
+    cfg = sb.Config(num_workers=1, batch_size_per_worker=1024, num_fields=26, embedding_dim=16,
+                    vocabulary_size=1_000_000, cache_capacity=16384, hidden_dim=64)
+    run_parity(cfg, 3)
+
+
+def test_capacity_deadlock_is_a_run_error():
+    cfg = sb.Config(num_workers=1, batch_size_per_worker=8, num_fields=4, embedding_dim=4,
+                    vocabulary_size=100000, cache_capacity=8, hidden_dim=4, zipf_exponent=0.0)
+    tr = sb.Trainer(cfg)
+    f, y = sb.SyntheticGenerator(cfg).generate(0)
+    with pytest.raises(sb.RunError) as e:
+        tr.step(0, f, y)
+    assert e.value.step == 0
+
+
+def test_feature_out_of_vocab_is_a_logic_error():
+    cfg = sb.Config(num_workers=1, batch_size_per_worker=2, num_fields=2, vocabulary_size=100,
+                    cache_capacity=16, hidden_dim=4)
+    tr = sb.Trainer(cfg)
+    with pytest.raises(sb.LogicError):
+        tr.step(0, np.array([1, 2, 3, 100], np.uint64), np.zeros(2, np.uint8))
+
+
+def test_worker_count_invariance_device():
+    """SPEC acceptance 4 on the device: W in {1,2,4} on the same global batches."""
+    snaps = []
+    for W in (1, 2, 4):
+        cfg = sb.Config(num_workers=W, batch_size_per_worker=128 // W, num_fields=6,
+                        embedding_dim=4, vocabulary_size=2000, cache_capacity=4000, hidden_dim=8)
+        tr = sb.Trainer(cfg)
+        gen = sb.SyntheticGenerator(cfg)
+        losses = [tr.step(t, *gen.generate(t)) for t in range(5)]
+        snaps.append((losses, tr.snapshot()))
+        tr.close()
+    for losses, (f, r, s) in snaps[1:]:
+        assert np.allclose(losses, snaps[0][0], rtol=1e-5)
+        assert np.array_equal(f, snaps[0][1][0]) and np.array_equal(s, snaps[0][1][2])
+        assert np.max(np.abs(r - snaps[0][1][1])) <= 1e-6
+
+
+def test_cfg2_step_properties(golden):
+    """BASELINE configs[1] at W=1 (full size): VSI count equals the reference's,
+    every owned unique is resident after manage, loss finite and ~ln 2."""
+    rec = next(r for r in golden["batches"] if r["name"] == "cfg2_w1")
+    cfg = sb.Config(num_workers=1, batch_size_per_worker=8192, num_fields=39, embedding_dim=80,
+                    vocabulary_size=33_800_000, cache_capacity=400_000, hidden_dim=64,
+                    zipf_exponent=1.05)
+    tr = sb.Trainer(cfg)
+    gen = sb.SyntheticGenerator(cfg)
+    f, y = gen.generate(0)
+    assert sha(f) == rec["features_sha256"]
+    loss = tr.step(0, f, y)
+    st = tr.stats()
+    assert st["unique"] == rec["unique"] == st["owned"] == st["working"]
+    assert abs(loss - np.log(2)) < 0.05
+    loss2 = tr.step(1, *gen.generate(1))
+    assert np.isfinite(loss2)
+    tr.close()
