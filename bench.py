@@ -1,0 +1,384 @@
+#!/usr/bin/env python
+"""Benchmark: DeepFM training samples/s on the ScaleFreeCTR embedding hot path.
+
+Workload (BASELINE.json configs[1]): Criteo-shaped DeepFM-lite, 39 sparse
+fields, 33.8M-row table, d=80, hidden 64, batch 8192 per GPU, Zipf 1.05,
+lazy Adam, MixCache with a 2^19-slot (0.48 GiB of emb+m+v) HBM cache per GPU
+over a pinned host table. One process per GPU (torchrun), weak scaling.
+
+Arms
+  ours       : `value` = samples/s with each step's batch already resident in
+               HBM (device-resident API, CUDA events on the trainer stream,
+               max over ranks); `e2e` = the same through the public host-buffer
+               API (pinned host batch -> H2D -> step -> D2H of the loss, per
+               step). Also `roofline` of the dominant kernel (per-phase CUDA
+               events over the timed region), per-kernel rows, `cpu_baseline`.
+  reference  : the CPU path (the oracle port of the reference in fp64; the
+               reference's own TUs cover only VSI/generator/cache primitives)
+               on the host cores, rank 0 only.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOAD = ("cfg2: DeepFM-lite Criteo-shaped, 39 sparse fields, 33.8M-row table, d=80, hidden 64, "
+            "batch 8192/GPU, Zipf 1.05, lazy Adam, MixCache")
+METRIC = "training samples/sec"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--batch", type=int, default=8192)
+    p.add_argument("--fields", type=int, default=39)
+    p.add_argument("--dim", type=int, default=80)
+    p.add_argument("--vocab", type=int, default=33_800_000)
+    p.add_argument("--zipf", type=float, default=1.05)
+    p.add_argument("--hidden", type=int, default=64)
+    p.add_argument("--cache", type=int, default=1 << 19)
+    p.add_argument("--sync", default="allreduce", choices=["allreduce", "alltoall"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-rows", type=int, default=2048, help="rows per CPU-baseline step")
+    p.add_argument("--cpu-steps", type=int, default=3)
+    return p.parse_args()
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            pk = json.load(fh)
+        return pk, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{index}.csv")
+
+    def start(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.index), "-lms", "100"], stdout=self.fh,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait(timeout=10)
+        self.fh.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def phase_bytes(name, U, Uw, n, b, d, F, H, Ntot):
+    """Algorithmic bytes (or FLOPs for the tower) per step for each phase."""
+    if name == "vsi":
+        return 8 * Ntot + 12 * U, "B"
+    if name == "gather_cache":
+        return 8 * Uw + 8 * d * Uw, "B"
+    if name == "gather_instances":
+        return 4 * n + 8 * d * n + 4 * b * d + b * d, "B"
+    if name == "segment_sum":
+        return 4 * n + 4 * d * n + 4 * d * U, "B"
+    if name == "sparse_adam":
+        return 28 * d * Uw + 12 * Uw, "B"
+    if name == "tower":
+        return 6 * b * F * d * H, "FLOP"
+    return None, None
+
+
+def run_ours(args, D):
+    import torch
+
+    import paper_2104_08542_b200 as sb
+    from paper_2104_08542_b200 import dist as sdist
+
+    rank, world = D.rank, D.world
+    dev = D.local_rank
+    torch.cuda.set_device(dev)
+    cfg = sb.Config(num_workers=world, batch_size_per_worker=args.batch, num_fields=args.fields,
+                    embedding_dim=args.dim, vocabulary_size=args.vocab, cache_capacity=args.cache,
+                    hidden_dim=args.hidden, zipf_exponent=args.zipf, seed=7)
+    cfg.apply("sync", args.sync)
+    nid = sdist.nccl_id_for(D, sb.nccl_unique_id)
+    t0 = time.time()
+    tr = sb.Trainer(cfg, rank=rank, world=world, nccl_id=nid, device=dev)
+    setup_s = time.time() - t0
+    gen = sb.SyntheticGenerator(cfg, device=dev)
+    r0, nrows = sdist.rows_of(rank, tr.lanes, args.batch)
+    F = args.fields
+    W, K = args.warmup, args.steps
+    nb = W + 2 * K
+    # device-resident batches (value arm) and pinned host copies (e2e arm)
+    d_feat = torch.empty((nb, nrows * F), dtype=torch.int64, device=f"cuda:{dev}")
+    d_lab = torch.empty((nb, nrows), dtype=torch.uint8, device=f"cuda:{dev}")
+    for s in range(nb):
+        gen.generate_device(s, r0, nrows, d_feat[s].data_ptr(), d_lab[s].data_ptr())
+    torch.cuda.synchronize()
+    h_feat = d_feat.cpu().pin_memory()
+    h_lab = d_lab.cpu().pin_memory()
+    hf = h_feat.numpy().view(np.uint64)
+    hl = h_lab.numpy()
+
+    for s in range(W):  # warm-up through the public host API
+        tr.step(s, hf[s], hl[s])
+    stream = torch.cuda.ExternalStream(tr.stream, device=f"cuda:{dev}")
+    d_loss = torch.zeros(1, dtype=torch.float32, device=f"cuda:{dev}")
+
+    # ---- value: device-resident inputs, CUDA events on the trainer stream
+    tr.set_timing(True)
+    phases = {}
+    stats_acc = {}
+    clocks = Clocks(dev)
+    launches = 0
+    D.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for i in range(K):
+        s = W + i
+        tr.step_device(s, d_feat[s].data_ptr(), d_lab[s].data_ptr(), None, d_loss.data_ptr())
+        tr.synchronize()  # collects this step's per-phase events + deferred errors
+        for nm, ms in tr.phase_times():
+            phases[nm] = phases.get(nm, 0.0) + ms
+        st = tr.stats()
+        launches += st["kernel_launches"]
+        for k2, v in st.items():
+            stats_acc[k2] = stats_acc.get(k2, 0) + v
+    ev1.record(stream)
+    ev1.synchronize()
+    torch.cuda.synchronize()
+    dev_ms = ev0.elapsed_time(ev1)
+    clk = clocks.stop()
+    D.barrier()
+    tr.set_timing(False)
+    ms_step = D.max(dev_ms) / K
+    loss_dev = float(d_loss.item())
+
+    # ---- e2e: host batch -> H2D -> step -> D2H loss, through the public API
+    D.barrier()
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    losses = []
+    for i in range(K):
+        s = W + K + i
+        losses.append(tr.step(s, hf[s], hl[s]))
+    torch.cuda.synchronize()
+    e2e_s = D.max(time.perf_counter() - w0)
+    D.barrier()
+
+    rows_global = world * args.batch
+    value = rows_global / (ms_step / 1e3)
+    e2e_value = rows_global * K / e2e_s
+    per_step = {k2: v / K for k2, v in stats_acc.items()}
+    phase_ms = {k2: v / K for k2, v in phases.items()}
+    peaks, peak_kind = measured_peaks()
+    U = per_step.get("unique", 0)
+    Uw = per_step.get("owned", 0)
+    n = args.batch * F
+    Ntot = world * n
+    d, H = args.dim, args.hidden
+    kernels = {}
+    for nm, ms in phase_ms.items():
+        amount, unit = phase_bytes(nm, U, Uw, n, args.batch, d, F, H, Ntot)
+        row = {"ms": round(ms, 4)}
+        if amount is not None and ms > 0:
+            if unit == "B":
+                gbs = amount / (ms / 1e3) / 1e9
+                row.update(bytes=int(amount), gbs=round(gbs, 1),
+                           frac_hbm=round(gbs / peaks["hbm_gbs"], 3))
+            else:
+                tf = amount / (ms / 1e3) / 1e12
+                row.update(flops=int(amount), tflops=round(tf, 2),
+                           frac_bf16_sustained=round(tf / peaks["bf16_tflops_sustained"], 4))
+        kernels[nm] = row
+    # dominant kernel = the largest phase with an algorithmic model
+    cand = [(v["ms"], k2) for k2, v in kernels.items() if "bytes" in v or "flops" in v]
+    dom = max(cand)[1] if cand else None
+    roofline = None
+    if dom:
+        r = kernels[dom]
+        if "bytes" in r:
+            roofline = {"kernel": dom, "bound": "hbm", "achieved": r["gbs"], "peak": peaks["hbm_gbs"],
+                        "unit": "GB/s", "frac": r["frac_hbm"], "traffic": None,
+                        "peak_source": peak_kind}
+        else:
+            roofline = {"kernel": dom, "bound": "tensor", "achieved": r["tflops"],
+                        "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
+                        "frac": r["frac_bf16_sustained"], "traffic": None,
+                        "peak_source": peak_kind + " (bf16 sustained; tower runs fp32)"}
+    # NVLink sync rate (world > 1): bytes this rank handed to NCCL per step / time of the sync phases
+    sync = None
+    if world > 1:
+        sync_ms = sum(v for k2, v in phase_ms.items() if k2.startswith("allreduce") or k2 == "ids_allgather")
+        nv = per_step.get("nvlink_bytes", 0)
+        busbytes = 2 * (world - 1) / world * nv
+        sync = {"ms": round(sync_ms, 4), "payload_bytes": int(nv),
+                "busbw_gbs": round(busbytes / (sync_ms / 1e3) / 1e9, 1) if sync_ms else None,
+                "peak_gbs": 770.0, "peak_source": "B200_PROFILING.md measured peer copy"}
+    fill_ms = phase_ms.get("manage_evict_admit", 0.0)
+    mix = {"cache_slots_per_gpu": args.cache, "owned_uniques_per_step": round(Uw, 1),
+           "misses_per_step": round(per_step.get("working", 0), 1),
+           "evictions_per_step": round(per_step.get("evicted", 0), 1),
+           "pcie_h2d_bytes_per_step": int(per_step.get("pcie_h2d_bytes", 0)),
+           "pcie_d2h_bytes_per_step": int(per_step.get("pcie_d2h_bytes", 0)),
+           "evict_admit_ms": round(fill_ms, 4)}
+    if fill_ms > 0:
+        pc = (per_step.get("pcie_h2d_bytes", 0) + per_step.get("pcie_d2h_bytes", 0))
+        mix["pcie_gbs"] = round(pc / (fill_ms / 1e3) / 1e9, 2)
+        mix["pcie_peak_gbs"] = 64.0
+    out = {
+        "metric": METRIC, "value": round(value, 1), "unit": "samples/s", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+        "data": "synthetic (device Zipf generator, bit-exact with the reference SyntheticGenerator)",
+        "config": {"workload": WORKLOAD, "global_batch": rows_global, "fields": F, "dim": d,
+                   "vocab": args.vocab, "hidden": H, "zipf": args.zipf,
+                   "cache_slots_per_gpu": args.cache, "sync": args.sync,
+                   "parallelism": f"dp{world} (embedding rows owned f mod {world})",
+                   "l2": "no flush: per-step working set > L2 (X alone is 102 MB/GPU)",
+                   "setup_s": round(setup_s, 2)},
+        "e2e": {"value": round(e2e_value, 1), "unit": "samples/s",
+                "h2d_bytes_per_step": int(nrows * F * 8 + nrows),
+                "d2h_bytes_per_step": 4},
+        "gpu_launches": int(launches),
+        "roofline": roofline,
+        "kernels": kernels,
+        "mixcache": mix,
+        "sync": sync,
+        "clocks": clk,
+        "loss": {"device_last": loss_dev, "e2e_last": losses[-1] if losses else None},
+        "per_step": {k2: round(v, 1) for k2, v in per_step.items()},
+    }
+    tr.close()
+    return out
+
+
+def cpu_sample(args, workers, rows_total, steps, threads):
+    """The oracle port (fp64 reference semantics) on host cores: rows_total rows/step."""
+    import ctypes as C
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import OrcConfig, oracle, oracle_generate
+    O = oracle()
+    c = OrcConfig()
+    O.orc_config_default(c)
+    c.num_workers = workers
+    c.batch_size_per_worker = rows_total // workers
+    c.num_fields = args.fields
+    c.embedding_dim = args.dim
+    c.vocabulary_size = args.vocab
+    c.cache_capacity = args.cache
+    c.hidden_dim = args.hidden
+    c.zipf_exponent = args.zipf
+    c.num_threads = threads
+    sim = O.orc_sim_create(C.byref(c))
+    rows = c.batch_size_per_worker * workers
+    batches = [oracle_generate(rows, args.fields, args.vocab, 7, args.zipf, s) for s in range(steps)]
+    times = []
+    for s, (f, y) in enumerate(batches):
+        loss = C.c_double()
+        t0 = time.perf_counter()
+        rc = O.orc_sim_step(sim, s, f, y, None, 0, C.byref(loss), None, None)
+        times.append(time.perf_counter() - t0)
+        assert rc == 0, O.orc_last_error()
+    O.orc_sim_destroy(sim)
+    return rows, times
+
+
+def run_reference(args, D):
+    if D.rank != 0:
+        return None
+    threads = os.cpu_count() or 1
+    rows = min(args.cpu_rows, args.batch * D.world)
+    rows -= rows % D.world
+    rows_step, times = cpu_sample(args, D.world, rows, args.warmup + args.steps, threads)
+    t = times[args.warmup:]
+    ms = 1e3 * sum(t) / len(t)
+    val = rows_step / (ms / 1e3)
+    return {"metric": METRIC, "value": round(val, 1), "unit": "samples/s", "n_gpus": D.world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (oracle port of the reference SyntheticGenerator)",
+            "config": {"workload": WORKLOAD, "global_batch": args.batch * D.world,
+                       "sample_rows_per_step": rows_step, "cache_slots_per_gpu": args.cache},
+            "impl": "reference",
+            "cpu_baseline": {"value": round(val, 1), "unit": "samples/s", "cores": threads,
+                             "kind": "port",
+                             "sample": f"{rows_step} rows/step of the same workload, "
+                                       f"{D.world} simulated workers, {args.steps} timed steps"},
+            "e2e": {"value": round(val, 1), "unit": "samples/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    from paper_2104_08542_b200 import dist as sdist
+    D = sdist.from_env()
+    if D.world > 1 and args.gpus != D.world:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {D.world}")
+    if args.impl == "reference":
+        out = run_reference(args, D)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        D.close()
+        return
+    out = run_ours(args, D)
+    if D.rank == 0:
+        if D.world == 1 and not args.no_cpu_baseline:
+            threads = os.cpu_count() or 1
+            rows_step, times = cpu_sample(args, 1, args.cpu_rows, args.cpu_steps, threads)
+            t = times[1:] if len(times) > 1 else times
+            v = rows_step / (sum(t) / len(t))
+            out["cpu_baseline"] = {"value": round(v, 1), "unit": "samples/s", "cores": threads,
+                                   "kind": "port",
+                                   "sample": f"{rows_step} rows/step x {len(t)} steps of the same "
+                                             f"cfg2 workload, oracle port (fp64), "
+                                             f"{threads} threads"}
+        print(json.dumps(out), flush=True)
+    D.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -255,10 +255,10 @@ void segment_sum(const uint32_t* vid, int32_t n, int d, const float* dX, float* 
 
 void sparse_adam(const uint32_t* own_k, const uint32_t* own_slot, int32_t n_own, const float* dG,
                  int d, float* emb, float* mom, float* vel, int32_t* steps, const float* bc1,
-                 const float* bc2, float lr, float beta1, float beta2, float eps, cudaStream_t s) {
+                 const float* bc2, float lr, double beta1, double beta2, float eps, cudaStream_t s) {
   if (n_own <= 0) return;
-  const float omb1 = static_cast<float>(1.0 - static_cast<double>(beta1));
-  const float omb2 = static_cast<float>(1.0 - static_cast<double>(beta2));
+  const float omb1 = static_cast<float>(1.0 - beta1);
+  const float omb2 = static_cast<float>(1.0 - beta2);
   if ((d & 3) == 0) {
     const int64_t n = static_cast<int64_t>(n_own) * (d / 4);
     sparse_adam_v4<<<ceil_div(n, 256), 256, 0, s>>>(

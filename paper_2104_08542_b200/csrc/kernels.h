@@ -24,7 +24,7 @@ void segment_sum(const uint32_t* vid, int32_t n, int d, const float* dX, float* 
 // update_sparse: lazy Adam on the lane's owned rows, per-row step count
 void sparse_adam(const uint32_t* own_k, const uint32_t* own_slot, int32_t n_own, const float* dG,
                  int d, float* emb, float* mom, float* vel, int32_t* steps, const float* bc1,
-                 const float* bc2, float lr, float beta1, float beta2, float eps, cudaStream_t s);
+                 const float* bc2, float lr, double beta1, double beta2, float eps, cudaStream_t s);
 
 // ---------------- tower.cu — DeepFM-lite ----------------
 struct TowerBufs {
@@ -47,7 +47,7 @@ void tower_forward_backward(TowerBufs& t, const float* X, const float* fm_s, con
                             cudaStream_t s);
 // Adam over the dense parameter vector; bias corrections precomputed on the host in fp64.
 void dense_adam(float* p, float* m, float* v, const float* g, int64_t n, float grad_scale,
-                float lr, float beta1, float beta2, float eps, float bc1, float bc2,
+                float lr, double beta1, double beta2, float eps, float bc1, float bc2,
                 cudaStream_t s);
 void scale_add(float* y, const float* x, int64_t n, float a, cudaStream_t s);
 

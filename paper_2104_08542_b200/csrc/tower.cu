@@ -344,9 +344,9 @@ void tower_forward_backward(TowerBufs& t, const float* X, const float* fm_s, con
 }
 
 void dense_adam(float* p, float* m, float* v, const float* g, int64_t n, float grad_scale, float lr,
-                float beta1, float beta2, float eps, float bc1, float bc2, cudaStream_t s) {
-  const float omb1 = static_cast<float>(1.0 - static_cast<double>(beta1));
-  const float omb2 = static_cast<float>(1.0 - static_cast<double>(beta2));
+                double beta1, double beta2, float eps, float bc1, float bc2, cudaStream_t s) {
+  const float omb1 = static_cast<float>(1.0 - beta1);
+  const float omb2 = static_cast<float>(1.0 - beta2);
   dense_adam_kernel<<<ceil_div(n, 256), 256, 0, s>>>(p, m, v, g, n, grad_scale, lr, beta1, beta2,
                                                      omb1, omb2, eps, bc1, bc2);
   CUDA_LAUNCH_CHECK();

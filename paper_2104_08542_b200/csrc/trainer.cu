@@ -367,7 +367,7 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   const double bc2 = 1.0 - std::pow(cfg_.adam_beta2, static_cast<double>(dense_steps_));
   dense_adam(d_dense_, d_dense_m_, d_dense_v_, d_grads_, static_cast<int64_t>(P_),
              1.f / static_cast<float>(W_), static_cast<float>(cfg_.learning_rate),
-             static_cast<float>(cfg_.adam_beta1), static_cast<float>(cfg_.adam_beta2),
+             cfg_.adam_beta1, cfg_.adam_beta2,
              static_cast<float>(cfg_.adam_epsilon), static_cast<float>(bc1),
              static_cast<float>(bc2), s);
   finalize_loss_kernel<<<1, 32, 0, s>>>(d_grads_ + P_, 1.f / static_cast<float>(W_),

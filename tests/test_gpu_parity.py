@@ -169,6 +169,32 @@ def orc_snapshot(s, d):
     return f, rows, st
 
 
+def check_rows_close(drows, orows, steps, d, lr, rtol=1e-5):
+    """Embedding rows + Adam moments, fp32 device vs fp64 oracle.
+
+    m (linear in the gradient): |dm| <= rtol * max|m_row|.  v (quadratic):
+    |dv| <= 10 rtol * max|v_row|.  Embeddings: >= 99.9 % of coordinates within
+    rtol * max|emb_row|, and every coordinate within rtol * max|emb_row| +
+    1e-2 * lr * adam_steps. The slack term is Adam's conditioning: the update
+    lr * m_hat / (sqrt(v_hat) + eps) has slope lr / (4 eps) in g where
+    |g| ~ eps = 1e-8, so a coordinate whose fp32 gradient cancels down to ~eps
+    turns a 1e-11 gradient difference (fp32 vs fp64 accumulation of terms
+    ~1e-5) into up to ~1e-3 * lr of parameter difference per update.
+    """
+    a = drows.astype(np.float64)
+    e, m, v = slice(0, d), slice(d, 2 * d), slice(2 * d, 3 * d)
+    sc_m = np.max(np.abs(orows[:, m]), axis=1, keepdims=True) + 1e-30
+    assert np.max(np.abs(a[:, m] - orows[:, m]) / sc_m) <= rtol
+    sc_v = np.max(np.abs(orows[:, v]), axis=1, keepdims=True) + 1e-30
+    assert np.max(np.abs(a[:, v] - orows[:, v]) / sc_v) <= 10 * rtol
+    err = np.abs(a[:, e] - orows[:, e])
+    sc_e = np.max(np.abs(orows[:, e]), axis=1, keepdims=True)
+    within = err <= rtol * sc_e
+    assert within.mean() >= 0.999, within.mean()
+    bound = rtol * sc_e + 1e-2 * lr * np.maximum(steps, 1)[:, None]
+    assert np.all(err <= bound), float(np.max(err - bound))
+
+
 def run_parity(cfg, steps, check_rows=True, row_tol=1e-5):
     O = oracle()
     oc = orc_cfg(cfg)
@@ -211,9 +237,7 @@ def run_parity(cfg, steps, check_rows=True, row_tol=1e-5):
         df, drows, dst = tr.snapshot()
         of, orows, ost = orc_snapshot(sim, cfg.embedding_dim)
         assert np.array_equal(df, of) and np.array_equal(dst, ost)
-        err = np.abs(drows.astype(np.float64) - orows)
-        scale = np.max(np.abs(orows), axis=1, keepdims=True) + 1e-3
-        assert np.max(err / scale) <= row_tol, float(np.max(err / scale))
+        check_rows_close(drows, orows, dst, cfg.embedding_dim, cfg.learning_rate, row_tol)
         # dense parameters
         K, H = cfg.num_fields * cfg.embedding_dim, cfg.hidden_dim
         w1, b1, w2, b2 = tr.get_dense()
