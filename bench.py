@@ -136,6 +136,8 @@ def run_ours(args, D):
     rank, world = D.rank, D.world
     dev = D.local_rank
     torch.cuda.set_device(dev)
+    if args.cache <= 0:  # the whole owned shard resident in HBM
+        args.cache = (args.vocab + world - 1) // world
     cfg = sb.Config(num_workers=world, batch_size_per_worker=args.batch, num_fields=args.fields,
                     embedding_dim=args.dim, vocabulary_size=args.vocab, cache_capacity=args.cache,
                     hidden_dim=args.hidden, zipf_exponent=args.zipf, seed=7)
