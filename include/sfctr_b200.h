@@ -203,6 +203,13 @@ typedef struct sfctr_step_stats {
   int64_t pcie_d2h_bytes;  /* actual row bytes written back to the pinned host table */
   int64_t nvlink_bytes;    /* bytes this process handed to NCCL in the last step */
   int64_t kernel_launches; /* kernels launched by the last step */
+  /* running totals since creation (deferred device counters are folded in at
+   * every sfctr_trainer_synchronize / host-buffer step) */
+  int64_t total_steps;
+  int64_t total_working;
+  int64_t total_evicted;
+  int64_t total_filled_from_host;
+  int64_t total_kernel_launches;
 } sfctr_step_stats;
 int sfctr_trainer_stats(sfctr_trainer* t, sfctr_step_stats* out);
 

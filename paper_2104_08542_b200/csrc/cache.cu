@@ -42,14 +42,15 @@ __global__ void probe_kernel(const uint32_t* __restrict__ own_k, int32_t n_own,
                              const uint32_t* __restrict__ gids, uint32_t W,
                              const uint32_t* __restrict__ index, uint32_t C, int32_t t,
                              int32_t* __restrict__ last_use, int32_t* __restrict__ mark,
-                             uint32_t* __restrict__ own_slot, uint32_t* __restrict__ miss) {
+                             uint32_t* __restrict__ own_slot, uint32_t* __restrict__ miss,
+                             int32_t* __restrict__ marked) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n_own) return;
   const uint32_t f = gids[own_k[j]];
   const uint32_t s = index[f / W];
   if (s < C) {
     if (t > last_use[s]) last_use[s] = t;  // CacheBuffer::touch (cache_buffer.cpp:69-72)
-    mark[s] = t;
+    if (atomicExch(mark + s, t) != t) atomicAdd(marked, 1);
     own_slot[j] = s;
     miss[j] = 0;
   } else {
@@ -61,13 +62,14 @@ __global__ void probe_kernel(const uint32_t* __restrict__ own_k, int32_t n_own,
 // needed_soon for resident owned features of a lookahead batch
 __global__ void mark_window_kernel(const uint32_t* __restrict__ gids, int32_t U, uint32_t W,
                                    uint32_t w, const uint32_t* __restrict__ index, uint32_t C,
-                                   int32_t t, int32_t* __restrict__ mark) {
+                                   int32_t t, int32_t* __restrict__ mark,
+                                   int32_t* __restrict__ marked) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= U) return;
   const uint32_t f = gids[i];
   if (f % W != w) return;
   const uint32_t s = index[f / W];
-  if (s < C) mark[s] = t;
+  if (s < C && atomicExch(mark + s, t) != t) atomicAdd(marked, 1);
 }
 
 // LRU key per slot: eligible = occupied && !needed_soon (pins are implied by
@@ -298,7 +300,8 @@ void CacheLane::mark_window(const uint32_t* d_gids, int32_t U, uint32_t W, uint3
                             cudaStream_t s) {
   if (U <= 0) return;
   mark_window_kernel<<<ceil_div(U, 256), 256, 0, s>>>(d_gids, U, W, w, index,
-                                                      static_cast<uint32_t>(C), t, mark);
+                                                      static_cast<uint32_t>(C), t, mark,
+                                                      counters + kCntMarked);
   CUDA_LAUNCH_CHECK();
 }
 
@@ -307,7 +310,7 @@ void CacheLane::probe(const uint32_t* d_gids, int32_t n_own, uint32_t W, int32_t
   if (n_own <= 0) return;
   probe_kernel<<<ceil_div(n_own, 256), 256, 0, s>>>(own_k, n_own, d_gids, W, index,
                                                     static_cast<uint32_t>(C), t, last_use, mark,
-                                                    own_slot, miss);
+                                                    own_slot, miss, counters + kCntMarked);
   CUDA_LAUNCH_CHECK();
   exclusive_scan_u32(temp, scan_bytes, miss, miss_rank, n_own, s);
   compact_kernel<<<ceil_div(n_own, 256), 256, 0, s>>>(miss, miss_rank, n_own, work_j,

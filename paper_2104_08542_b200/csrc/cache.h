@@ -6,7 +6,8 @@
 
 namespace sfb {
 
-enum { kCntOwned = 0, kCntWorking = 1, kCntFromHost = 2, kCntError = 3 };
+// device counters per lane; kCntMarked = resident slots stamped needed_soon this step
+enum { kCntOwned = 0, kCntWorking = 1, kCntFromHost = 2, kCntError = 3, kCntMarked = 4 };
 
 struct CacheLane {
   uint64_t C = 0;       // slots (cache_capacity)

@@ -210,14 +210,20 @@ void Trainer::phase(const char* name) {
   ev_names_.emplace_back(name);
 }
 
+// Sums, per phase name, the device time between consecutive phase events of
+// every step recorded since the last call (events accumulate across steps so
+// a timed region needs no extra host synchronisation).
 void Trainer::finish_phases() {
-  if (!timing_ || ev_.size() < 2) return;
+  if (ev_.size() < 2) return;
   CUDA_CHECK(cudaEventSynchronize(ev_.back()));
-  phase_ms_.clear();
   for (size_t i = 1; i < ev_.size(); ++i) {
+    if (ev_names_[i] == "start") continue;
     float ms = 0;
     CUDA_CHECK(cudaEventElapsedTime(&ms, ev_[i - 1], ev_[i]));
-    phase_ms_.emplace_back(ev_names_[i], ms);
+    auto it = std::find_if(phase_ms_.begin(), phase_ms_.end(),
+                           [&](const auto& p) { return p.first == ev_names_[i]; });
+    if (it == phase_ms_.end()) phase_ms_.emplace_back(ev_names_[i], ms);
+    else it->second += ms;
   }
   for (auto e : ev_) cudaEventDestroy(e);
   ev_.clear();
@@ -234,11 +240,16 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   if (step < 0 || step >= (1ll << 23)) fail(kLogic, "step index out of the supported range");
   if (cfg_.lookahead_depth > 1 && !d_window)
     fail(kLogic, "lookahead > 1 needs the window batches");
-  for (auto& e : ev_) cudaEventDestroy(e);
-  ev_.clear();
-  ev_names_.clear();
   phase("start");
-  stats_ = sfctr_step_stats{};
+  {  // per-step fields restart, running totals carry over
+    sfctr_step_stats next{};
+    next.total_steps = stats_.total_steps;
+    next.total_working = stats_.total_working;
+    next.total_evicted = stats_.total_evicted;
+    next.total_filled_from_host = stats_.total_filled_from_host;
+    next.total_kernel_launches = stats_.total_kernel_launches;
+    stats_ = next;
+  }
 
   // ---- Data-Loader: ids to u32, all-gather the global batch, VSI (Algorithm 1 l.2-3)
   CUDA_CHECK(cudaMemsetAsync(d_scalars_, 0, sizeof(int32_t) * 8, s));
@@ -264,7 +275,9 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   // ---- Host-Manager: MixCache per lane (Algorithm 1 l.4-7)
   CUDA_CHECK(cudaMemsetAsync(d_scalars_ + 2, 0, sizeof(int32_t) * 6, s));
   for (int l = 0; l < lanes_; ++l) {
-    CUDA_CHECK(cudaMemsetAsync(lane_[l].counters, 0, sizeof(int32_t) * 8, s));
+    // per-step counters; kCntFromHost (index 2) stays cumulative
+    CUDA_CHECK(cudaMemsetAsync(lane_[l].counters, 0, sizeof(int32_t) * 2, s));
+    CUDA_CHECK(cudaMemsetAsync(lane_[l].counters + 3, 0, sizeof(int32_t) * 5, s));
     lane_[l].select_owned(d_uniq_, U, Wu, static_cast<uint32_t>(lane0_ + l), s);
   }
   for (int j = 0; j < nwin; ++j) {
@@ -297,8 +310,23 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
     CUDA_CHECK(cudaMemcpyAsync(h_counts_ + 8 * l, lane_[l].counters, sizeof(int32_t) * 8,
                                cudaMemcpyDeviceToHost, s));
   CUDA_CHECK(cudaStreamSynchronize(s));
+  // capacity check before any state moves (push_parameters_to_cache deadlock)
   for (int l = 0; l < lanes_; ++l) {
     n_work[l] = n_own[l] > 0 ? h_counts_[8 * l + kCntWorking] : 0;
+    const CacheLane& L = lane_[l];
+    const int64_t occupied = static_cast<int64_t>(L.C) - L.free_top;
+    const int64_t marked = h_counts_[8 * l + kCntMarked];
+    const int64_t evictable = occupied - marked;
+    if (n_work[l] > L.free_top + evictable)
+      fail(kRun,
+           "capacity deadlock on worker " + std::to_string(lane0_ + l) + ": need " +
+               std::to_string(n_work[l]) + " slots, " + std::to_string(L.free_top + evictable) +
+               " free or evictable (capacity=" + std::to_string(L.C) +
+               " occupied=" + std::to_string(occupied) + " free=" + std::to_string(L.free_top) +
+               " pinned=0 needed_soon=" + std::to_string(marked) + ")",
+           step);
+  }
+  for (int l = 0; l < lanes_; ++l) {
     CacheLane& L = lane_[l];
     const int32_t n_evict = std::max<int32_t>(0, n_work[l] - L.free_top);
     L.evict(n_evict, Wu, t, s);
@@ -376,9 +404,17 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   phase("dense_adam");
   steps_done_ += 1;
   stats_.kernel_launches = g_launches - launches0;
+  stats_.total_steps += 1;
+  stats_.total_working += stats_.working;
+  stats_.total_evicted += stats_.evicted;
+  stats_.total_kernel_launches += stats_.kernel_launches;
 }
 
+// Folds the deferred device counters in: capacity errors flagged by kernels
+// and the number of admissions that read a row back from the host table
+// (cumulative on the device; the delta covers every step since the last call).
 void Trainer::check_device_errors(int64_t step) {
+  int64_t cum = 0;
   for (int l = 0; l < lanes_; ++l) {
     int32_t c[8];
     CUDA_CHECK(cudaMemcpy(c, lane_[l].counters, sizeof(c), cudaMemcpyDeviceToHost));
@@ -389,9 +425,13 @@ void Trainer::check_device_errors(int64_t step) {
                std::to_string(L.C) + " free=" + std::to_string(L.free_top) + ")",
            step);
     }
-    stats_.filled_from_host += c[kCntFromHost];
+    cum += c[kCntFromHost];
   }
-  stats_.pcie_h2d_bytes = stats_.filled_from_host * (3 * d_ + 1) * 4;
+  const int64_t delta = cum - from_host_seen_;
+  from_host_seen_ = cum;
+  stats_.filled_from_host = delta;
+  stats_.total_filled_from_host += delta;
+  stats_.pcie_h2d_bytes = delta * (3 * d_ + 1) * 4;
 }
 
 double Trainer::step_host(int64_t step, const uint64_t* features, const uint8_t* labels,

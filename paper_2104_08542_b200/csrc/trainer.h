@@ -46,8 +46,16 @@ class Trainer {
   void set_dense(const float* w1, const float* b1, const float* w2, const float* b2);
   void ledger(int64_t out[4]) const;
   sfctr_step_stats stats() const { return stats_; }
-  void set_timing(bool on) { timing_ = on; }
-  const std::vector<std::pair<std::string, float>>& phase_times() const { return phase_ms_; }
+  // enabling (re)starts the per-phase accumulation; phase_times() returns the
+  // per-phase device-time sums over the steps run since
+  void set_timing(bool on) {
+    timing_ = on;
+    if (on) phase_ms_.clear();
+  }
+  const std::vector<std::pair<std::string, float>>& phase_times() {
+    finish_phases();
+    return phase_ms_;
+  }
 
  private:
   void ensure_bias_tables(int64_t t_max);
@@ -98,6 +106,7 @@ class Trainer {
   int64_t dense_steps_ = 0;
   int64_t steps_done_ = 0;
   int64_t led_[4] = {0, 0, 0, 0};
+  int64_t from_host_seen_ = 0;
   sfctr_step_stats stats_{};
 
   bool timing_ = false;

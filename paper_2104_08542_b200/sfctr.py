@@ -106,7 +106,8 @@ class Config(C.Structure):
 class StepStats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in (
         "unique", "owned", "working", "evicted", "filled_from_host", "pcie_h2d_bytes",
-        "pcie_d2h_bytes", "nvlink_bytes", "kernel_launches")]
+        "pcie_d2h_bytes", "nvlink_bytes", "kernel_launches", "total_steps", "total_working",
+        "total_evicted", "total_filled_from_host", "total_kernel_launches")]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
