@@ -486,7 +486,8 @@ int sfctr_model_forward_backward(int device, int32_t rows, int32_t fields, int32
     SFB_CHECK(rows > 0 && fields > 0 && dim > 0 && hidden > 0, "bad model shape");
     const int K = fields * dim, H = hidden;
     const size_t P = static_cast<size_t>(K) * H + 2 * H + 1;
-    const size_t rk = static_cast<size_t>(rows) * K;
+    const int ldx = sfb::tower_ldx(K);
+    const size_t rk = static_cast<size_t>(rows) * ldx;
     float *d_x, *d_dx, *d_dense, *d_g, *d_s, *d_sq, *d_lg;
     uint8_t* d_y;
     CUDA_CHECK(cudaMalloc(&d_x, sizeof(float) * rk));
@@ -497,7 +498,9 @@ int sfctr_model_forward_backward(int device, int32_t rows, int32_t fields, int32
     CUDA_CHECK(cudaMalloc(&d_sq, sizeof(float) * rows * dim));
     CUDA_CHECK(cudaMalloc(&d_lg, sizeof(float) * rows));
     CUDA_CHECK(cudaMalloc(&d_y, rows));
-    CUDA_CHECK(cudaMemcpy(d_x, x, sizeof(float) * rk, cudaMemcpyHostToDevice));
+    CUDA_CHECK(cudaMemset(d_x, 0, sizeof(float) * rk));
+    CUDA_CHECK(cudaMemcpy2D(d_x, sizeof(float) * ldx, x, sizeof(float) * K, sizeof(float) * K, rows,
+                            cudaMemcpyHostToDevice));
     CUDA_CHECK(cudaMemcpy(d_y, labels, rows, cudaMemcpyHostToDevice));
     const size_t kh = static_cast<size_t>(K) * H;
     CUDA_CHECK(cudaMemcpy(d_dense, w1, sizeof(float) * kh, cudaMemcpyHostToDevice));
@@ -505,20 +508,25 @@ int sfctr_model_forward_backward(int device, int32_t rows, int32_t fields, int32
     CUDA_CHECK(cudaMemcpy(d_dense + kh + H, w2, sizeof(float) * H, cudaMemcpyHostToDevice));
     CUDA_CHECK(cudaMemcpy(d_dense + kh + 2 * H, b2, sizeof(float), cudaMemcpyHostToDevice));
     sfb::TowerBufs tb;
+    sfb::TowerTC tt;
     tb.init(rows, K, H, dim);
-    sfb::fm_sums(d_x, rows, fields, dim, d_s, d_sq, nullptr);
-    sfb::tower_forward_backward(tb, d_x, d_s, d_sq, d_y, rows, fields, dim, d_dense, d_lg, d_dx,
-                                1.f, d_g, false, nullptr);
+    tt.init(rows, K, H, dim);
+    sfb::fm_sums(d_x, rows, fields, dim, ldx, d_s, d_sq, nullptr);
+    sfb::tower_forward_backward_tc(tb, tt, d_x, ldx, d_s, d_sq, d_y, rows, fields, dim, d_dense,
+                                   d_lg, d_dx, 1.f, d_g, false, nullptr);
     CUDA_CHECK(cudaDeviceSynchronize());
     std::vector<float> g(P + 1);
     CUDA_CHECK(cudaMemcpy(g.data(), d_g, sizeof(float) * (P + 1), cudaMemcpyDeviceToHost));
     if (loss) *loss = g[P];
     if (logits) CUDA_CHECK(cudaMemcpy(logits, d_lg, sizeof(float) * rows, cudaMemcpyDeviceToHost));
-    if (dx) CUDA_CHECK(cudaMemcpy(dx, d_dx, sizeof(float) * rk, cudaMemcpyDeviceToHost));
+    if (dx)
+      CUDA_CHECK(cudaMemcpy2D(dx, sizeof(float) * K, d_dx, sizeof(float) * ldx, sizeof(float) * K,
+                              rows, cudaMemcpyDeviceToHost));
     if (dw1) std::memcpy(dw1, g.data(), sizeof(float) * kh);
     if (db1) std::memcpy(db1, g.data() + kh, sizeof(float) * H);
     if (dw2) std::memcpy(dw2, g.data() + kh + H, sizeof(float) * H);
     if (db2) *db2 = g[kh + 2 * H];
+    tt.release();
     tb.release();
     for (void* p : {static_cast<void*>(d_x), static_cast<void*>(d_dx), static_cast<void*>(d_dense),
                     static_cast<void*>(d_g), static_cast<void*>(d_s), static_cast<void*>(d_sq),

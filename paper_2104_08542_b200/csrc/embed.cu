@@ -79,7 +79,7 @@ __global__ void gather_instances_v4(const uint32_t* __restrict__ vid, int32_t ro
 }
 
 __global__ void gather_instances_s(const uint32_t* __restrict__ vid, int32_t rows, int F, int d,
-                                   const float* __restrict__ G, float* __restrict__ X,
+                                   int ldx, const float* __restrict__ G, float* __restrict__ X,
                                    float* __restrict__ fm_s, float* __restrict__ fm_sqp) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= static_cast<int64_t>(rows) * d) return;
@@ -88,7 +88,7 @@ __global__ void gather_instances_s(const uint32_t* __restrict__ vid, int32_t row
   float s = 0.f, sq = 0.f;
   for (int f = 0; f < F; ++f) {
     const float a = G[static_cast<int64_t>(vid[r * F + f]) * d + c];
-    X[(r * F + f) * d + c] = a;
+    X[r * ldx + f * d + c] = a;
     s += a;
     sq += a * a;
   }
@@ -96,7 +96,7 @@ __global__ void gather_instances_s(const uint32_t* __restrict__ vid, int32_t row
   fm_sqp[r * d + c] = sq;
 }
 
-__global__ void fm_sums_kernel(const float* __restrict__ X, int32_t rows, int F, int d,
+__global__ void fm_sums_kernel(const float* __restrict__ X, int32_t rows, int F, int d, int ldx,
                                float* __restrict__ fm_s, float* __restrict__ fm_sqp, int parts) {
   // thread per (row, column c); one partial per column (parts == d here)
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -105,7 +105,7 @@ __global__ void fm_sums_kernel(const float* __restrict__ X, int32_t rows, int F,
   const int c = static_cast<int>(i - r * d);
   float s = 0.f, sq = 0.f;
   for (int f = 0; f < F; ++f) {
-    const float a = X[(r * F + f) * d + c];
+    const float a = X[r * ldx + f * d + c];
     s += a;
     sq += a * a;
   }
@@ -128,13 +128,15 @@ __global__ void segment_sum_v4(const uint32_t* __restrict__ vid, int32_t n, int 
                : "memory");
 }
 
-__global__ void segment_sum_s(const uint32_t* __restrict__ vid, int32_t n, int d,
+__global__ void segment_sum_s(const uint32_t* __restrict__ vid, int32_t n, int F, int d, int ldx,
                               const float* __restrict__ dX, float* __restrict__ dG) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= static_cast<int64_t>(n) * d) return;
-  const int64_t p = i / d;
+  const int64_t p = i / d;  // position = row * F + field
   const int c = static_cast<int>(i - p * d);
-  atomicAdd(dG + static_cast<int64_t>(vid[p]) * d + c, dX[i]);
+  const int64_t r = p / F;
+  const int f = static_cast<int>(p - r * F);
+  atomicAdd(dG + static_cast<int64_t>(vid[p]) * d + c, dX[r * ldx + f * d + c]);
 }
 
 // Lazy Adam: t = adam_steps + 1 per row; bias
@@ -215,8 +217,8 @@ void gather_cache(const uint32_t* own_k, const uint32_t* own_slot, int32_t n_own
   CUDA_LAUNCH_CHECK();
 }
 
-void gather_instances(const uint32_t* vid, int32_t rows, int F, int d, const float* G, float* X,
-                      float* fm_s, float* fm_sqp, cudaStream_t s) {
+void gather_instances(const uint32_t* vid, int32_t rows, int F, int d, int ldx, const float* G,
+                      float* X, float* fm_s, float* fm_sqp, cudaStream_t s) {
   if (rows <= 0) return;
   if ((d & 3) == 0) {
     const int64_t n = static_cast<int64_t>(rows) * (d / 4);
@@ -225,30 +227,30 @@ void gather_instances(const uint32_t* vid, int32_t rows, int F, int d, const flo
         reinterpret_cast<float4*>(fm_s), fm_sqp);
   } else {
     const int64_t n = static_cast<int64_t>(rows) * d;
-    gather_instances_s<<<ceil_div(n, 256), 256, 0, s>>>(vid, rows, F, d, G, X, fm_s, fm_sqp);
+    gather_instances_s<<<ceil_div(n, 256), 256, 0, s>>>(vid, rows, F, d, ldx, G, X, fm_s, fm_sqp);
   }
   CUDA_LAUNCH_CHECK();
 }
 
-void fm_sums(const float* X, int32_t rows, int F, int d, float* fm_s, float* fm_sqp,
+void fm_sums(const float* X, int32_t rows, int F, int d, int ldx, float* fm_s, float* fm_sqp,
              cudaStream_t s) {
   const int parts = fm_sq_parts(d);
   if (parts != d) CUDA_CHECK(cudaMemsetAsync(fm_sqp, 0, sizeof(float) * rows * parts, s));
   const int64_t n = static_cast<int64_t>(rows) * d;
-  fm_sums_kernel<<<ceil_div(n, 256), 256, 0, s>>>(X, rows, F, d, fm_s, fm_sqp, parts);
+  fm_sums_kernel<<<ceil_div(n, 256), 256, 0, s>>>(X, rows, F, d, ldx, fm_s, fm_sqp, parts);
   CUDA_LAUNCH_CHECK();
 }
 
-void segment_sum(const uint32_t* vid, int32_t n, int d, const float* dX, float* dG,
+void segment_sum(const uint32_t* vid, int32_t n, int F, int d, int ldx, const float* dX, float* dG,
                  cudaStream_t s) {
   if (n <= 0) return;
-  if ((d & 3) == 0) {
+  if ((d & 3) == 0 && ldx == F * d) {
     const int64_t m = static_cast<int64_t>(n) * (d / 4);
     segment_sum_v4<<<ceil_div(m, 256), 256, 0, s>>>(vid, n, d / 4,
                                                     reinterpret_cast<const float4*>(dX), dG);
   } else {
     const int64_t m = static_cast<int64_t>(n) * d;
-    segment_sum_s<<<ceil_div(m, 256), 256, 0, s>>>(vid, n, d, dX, dG);
+    segment_sum_s<<<ceil_div(m, 256), 256, 0, s>>>(vid, n, F, d, ldx, dX, dG);
   }
   CUDA_LAUNCH_CHECK();
 }

@@ -12,14 +12,14 @@ void gather_cache(const uint32_t* own_k, const uint32_t* own_slot, int32_t n_own
                   const float* emb, int d, float* G, cudaStream_t s);
 // gather_instances + FM sums: X[i] = G[vid[i]] for the lane's rows; s[r] = sum_f X[r,f];
 // sqp[r, c4] = partial sum of squares
-void gather_instances(const uint32_t* vid, int32_t rows, int F, int d, const float* G, float* X,
-                      float* fm_s, float* fm_sqp, cudaStream_t s);
+void gather_instances(const uint32_t* vid, int32_t rows, int F, int d, int ldx, const float* G,
+                      float* X, float* fm_s, float* fm_sqp, cudaStream_t s);
 int fm_sq_parts(int d);  // columns of fm_sqp per row
 // FM sums of a materialised X (standalone model op)
-void fm_sums(const float* X, int32_t rows, int F, int d, float* fm_s, float* fm_sqp,
+void fm_sums(const float* X, int32_t rows, int F, int d, int ldx, float* fm_s, float* fm_sqp,
              cudaStream_t s);
 // segment_sum: dG[vid[i]] += dX[i] (vector red.global.add.v4.f32)
-void segment_sum(const uint32_t* vid, int32_t n, int d, const float* dX, float* dG,
+void segment_sum(const uint32_t* vid, int32_t n, int F, int d, int ldx, const float* dX, float* dG,
                  cudaStream_t s);
 // update_sparse: lazy Adam on the lane's owned rows, per-row step count
 void sparse_adam(const uint32_t* own_k, const uint32_t* own_slot, int32_t n_own, const float* dG,
@@ -39,12 +39,41 @@ struct TowerBufs {
   void init(int rows_cap, int K, int H, int d);
   void release();
 };
-// forward GEMM + head + backward (dX scaled by emb_scale, dense grads accumulated into
-// grads = [dW1 | db1 | dw2 | db2 | loss_sum] when accumulate, else overwritten).
-void tower_forward_backward(TowerBufs& t, const float* X, const float* fm_s, const float* fm_sqp,
-                            const uint8_t* labels, int32_t rows, int F, int d, const float* dense,
-                            float* logits, float* dX, float emb_scale, float* grads, bool accumulate,
-                            cudaStream_t s);
+// Operand buffers of the tensor-core tower (tc_tower.cu): 3xTF32 hi/lo parts of
+// W1 (both layouts) and dh (both layouts), split-K partials. Leading dims are
+// padded to 16 B for TMA.
+struct TowerTC {
+  int rows_cap = 0, K = 0, H = 0, d = 0;
+  int ldk = 0, ldh = 0, ldr = 0;  // padded K, H, rows
+  int s1_max = 1, s3_max = 1;     // split-K factors of GEMM1 / GEMM3
+  float *w_hi = nullptr, *w_lo = nullptr;    // [K x ldh]
+  float *wt_hi = nullptr, *wt_lo = nullptr;  // [H x ldk]
+  float *dh_hi = nullptr, *dh_lo = nullptr;  // [rows x ldh]
+  float *dht_hi = nullptr, *dht_lo = nullptr;  // [H x ldr]
+  float* part1 = nullptr;  // [s1, rows, H]
+  float* part3 = nullptr;  // [s3, K, H]
+  void init(int rows_cap, int K, int H, int d);
+  void release();
+};
+int tower_ldx(int K);  // row stride of X / dX (K rounded up to 4 floats)
+
+// Forward + head + backward of one lane's rows on the tensor cores. X and dX
+// have row stride ldx = tower_ldx(K); dX is scaled by emb_scale; dense grads go
+// to grads = [dW1 | db1 | dw2 | db2 | loss_sum] (accumulated when accumulate).
+void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc, const float* X, int ldx,
+                               const float* fm_s, const float* fm_sqp, const uint8_t* labels,
+                               int32_t rows, int F, int d, const float* dense, float* logits,
+                               float* dX, float emb_scale, float* grads, bool accumulate,
+                               cudaStream_t s);
+// fp32 SIMT reference tiles of the same tower (validation only; needs ldx == K)
+void tower_forward_backward_simt(TowerBufs& t, const float* X, const float* fm_s,
+                                 const float* fm_sqp, const uint8_t* labels, int32_t rows, int F,
+                                 int d, const float* dense, float* logits, float* dX,
+                                 float emb_scale, float* grads, bool accumulate, cudaStream_t s);
+void dw1_reduce(const float* part, int splits, int64_t n, float* out, bool accumulate,
+                cudaStream_t s);
+void small_grads(TowerBufs& t, int rows, int H, float* g_b1, float* g_w2, float* g_b2,
+                 float* g_loss, bool accumulate, cudaStream_t s);
 // Adam over the dense parameter vector; bias corrections precomputed on the host in fp64.
 void dense_adam(float* p, float* m, float* v, const float* g, int64_t n, float grad_scale,
                 float lr, double beta1, double beta2, float eps, float bc1, float bc2,

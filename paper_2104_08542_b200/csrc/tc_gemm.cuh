@@ -1,0 +1,328 @@
+// Blackwell (sm_100a) tensor-core GEMM for the DeepFM-lite tower:
+// tcgen05.mma kind::tf32 with TMEM accumulators, TMA-fed shared-memory
+// stages, and the 3xTF32 split (a*b ~= ah*bh + ah*bl + al*bh, each part
+// rounded to tf32) so that fp32-level accuracy is kept against the fp64
+// oracle.
+//
+// One CTA = 6 warps:
+//   warp 0     : TMA producer (one elected lane) into a ring of smem stages
+//   warp 1     : TMEM allocator + MMA issuer (one elected lane)
+//   warps 2..5 : split the A tile in place into (hi, lo) tf32 parts when A is
+//                not pre-split, then run the epilogue (tcgen05.ld TMEM ->
+//                registers -> global)
+// M tile = 128 rows (TMEM lane = row), N tile = BN columns, K block = 32 fp32
+// (one 128 B swizzle span). Operands use the canonical SWIZZLE_128B layouts
+// that TMA writes: K-major (8-row x 128 B atoms) or MN-major (32-element x
+// 8-row atoms, A only).
+#pragma once
+
+#include <cuda.h>
+
+#include "common.cuh"
+
+namespace sfb {
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int BKE = 32;                  // K elements per block (128 B)
+constexpr int A_BYTES = BM * BKE * 4;    // 16 KB
+
+enum Epi : int { kEpiStore = 0, kEpiDx = 1 };
+
+struct Params {
+  int M, N, K;            // logical GEMM sizes
+  int num_k_blocks;       // ceil(K / 32)
+  int k_blocks_per_split; // blockIdx.z covers [z*kps, (z+1)*kps)
+  // kEpiStore: out[z][m][n] with leading dim ldo, split stride split_stride
+  float* out;
+  int ldo;
+  long long split_stride;
+  // kEpiDx: dX[m][n] = scale * (acc + gz[m] * (fm_s[m][n % d] - X[m][n])), ld = ldx
+  const float* gz;
+  const float* fm_s;
+  const float* X;
+  int ldx;
+  int d;
+  float scale;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst,
+                                            int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+
+// sm_100 shared-memory matrix descriptor (cute::UMMA::SmemDescriptor):
+// start>>4 [0,14), LBO>>4 [16,30), SBO>>4 [32,46), version=1 [46,48),
+// base offset 0, layout type [61,64) = 2 (SWIZZLE_128B).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((addr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+  d |= 1ull << 46;
+  d |= 2ull << 61;
+  return d;
+}
+
+// Instruction descriptor for kind::tf32 (cute::UMMA::InstrDescriptor):
+// c_format F32 (1) at [4,6), a/b format TF32 (2) at [7,10)/[10,13),
+// a_major [15], b_major [16], N>>3 at [17,23), M>>4 at [24,29).
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int a_mn, int b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(a_mn) << 15) |
+         (static_cast<uint32_t>(b_mn) << 16) | (static_cast<uint32_t>(N >> 3) << 17) |
+         (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+template <int BN>
+struct Layout {
+  static constexpr int B_BYTES = BN * BKE * 4;  // K-major B tile, 128 B per row
+  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 6 ? 6 : (STAGES_RAW < 2 ? 2 : STAGES_RAW);
+  static constexpr int TMEM_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
+  // dynamic smem: 1 KB alignment slack + stages + barriers
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 256;
+};
+
+// A_MN: A is MN-major (4 TMA boxes of 32 m x 32 k); otherwise K-major (box 32 k x 128 m).
+// SPLIT_A: A arrives as raw fp32 and is split in smem; otherwise tmAlo supplies the lo part.
+template <int BN, bool A_MN, bool SPLIT_A, int EPI>
+__global__ void __launch_bounds__(192, 1)
+    gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap tmA,
+                       const __grid_constant__ CUtensorMap tmAlo,
+                       const __grid_constant__ CUtensorMap tmBhi,
+                       const __grid_constant__ CUtensorMap tmBlo, const Params p) {
+  using L = Layout<BN>;
+  constexpr int ST = L::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * L::STAGE_BYTES);
+  uint64_t* ready = full + ST;
+  uint64_t* empty = ready + ST;
+  uint64_t* tmem_full = empty + ST;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  auto a_hi = [&](int s) { return smem + s * L::STAGE_BYTES; };
+  auto a_lo = [&](int s) { return smem + s * L::STAGE_BYTES + A_BYTES; };
+  auto b_hi = [&](int s) { return smem + s * L::STAGE_BYTES + 2 * A_BYTES; };
+  auto b_lo = [&](int s) { return smem + s * L::STAGE_BYTES + 2 * A_BYTES + L::B_BYTES; };
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int kb0 = blockIdx.z * p.k_blocks_per_split;
+  const int kb1 = min(p.num_k_blocks, kb0 + p.k_blocks_per_split);
+  const int nkb = kb1 - kb0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(ready + s, 128);
+      mbar_init(empty + s, 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmBhi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmBlo)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_holder)),
+                 "n"(L::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      constexpr uint32_t bytes = (SPLIT_A ? A_BYTES : 2 * A_BYTES) + 2 * L::B_BYTES;
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % ST;
+        const uint32_t ph = (i / ST) & 1;
+        mbar_wait(empty + s, ph ^ 1);
+        mbar_expect_tx(full + s, bytes);
+        const int kc = (kb0 + i) * BKE;
+        if constexpr (A_MN) {
+#pragma unroll
+          for (int a = 0; a < 4; ++a) tma_load_2d(&tmA, full + s, a_hi(s) + a * 4096, m0 + a * 32, kc);
+        } else {
+          tma_load_2d(&tmA, full + s, a_hi(s), kc, m0);
+          if constexpr (!SPLIT_A) tma_load_2d(&tmAlo, full + s, a_lo(s), kc, m0);
+        }
+        tma_load_2d(&tmBhi, full + s, b_hi(s), kc, n0);
+        tma_load_2d(&tmBlo, full + s, b_lo(s), kc, n0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      constexpr uint32_t idesc = idesc_tf32(BM, BN, A_MN ? 1 : 0, 0);
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % ST;
+        const uint32_t ph = (i / ST) & 1;
+        if constexpr (SPLIT_A) mbar_wait(ready + s, ph);
+        else mbar_wait(full + s, ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+        for (int kk = 0; kk < BKE / 8; ++kk) {
+          uint64_t ah, al;
+          if constexpr (A_MN) {  // 8 k-rows = one 1 KB K-group; MN atoms 4 KB apart
+            ah = smem_desc(smem_u32(a_hi(s)) + kk * 1024, 4096, 1024);
+            al = smem_desc(smem_u32(a_lo(s)) + kk * 1024, 4096, 1024);
+          } else {  // K-major: advance 32 B inside the 128 B swizzle row
+            ah = smem_desc(smem_u32(a_hi(s)) + kk * 32, 16, 1024);
+            al = smem_desc(smem_u32(a_lo(s)) + kk * 32, 16, 1024);
+          }
+          const uint64_t bh = smem_desc(smem_u32(b_hi(s)) + kk * 32, 16, 1024);
+          const uint64_t bl = smem_desc(smem_u32(b_lo(s)) + kk * 32, 16, 1024);
+          mma_tf32(tmem, ah, bh, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+          mma_tf32(tmem, ah, bl, idesc, 1u);
+          mma_tf32(tmem, al, bh, idesc, 1u);
+        }
+        mma_commit(empty + s);  // frees the stage once these MMAs have read it
+      }
+      mma_commit(tmem_full);
+    }
+  } else {
+    const int t = threadIdx.x - 64;  // 0..127
+    if constexpr (SPLIT_A) {         // ---------------- in-place 3xTF32 split of A
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % ST;
+        const uint32_t ph = (i / ST) & 1;
+        mbar_wait(full + s, ph);
+        float4* hi = reinterpret_cast<float4*>(a_hi(s));
+        float4* lo = reinterpret_cast<float4*>(a_lo(s));
+#pragma unroll 4
+        for (int e = t; e < A_BYTES / 16; e += 128) {
+          const float4 v = hi[e];
+          float4 h, l;
+          h.x = tf32_rna(v.x); l.x = tf32_rna(v.x - h.x);
+          h.y = tf32_rna(v.y); l.y = tf32_rna(v.y - h.y);
+          h.z = tf32_rna(v.z); l.z = tf32_rna(v.z - h.z);
+          h.w = tf32_rna(v.w); l.w = tf32_rna(v.w - h.w);
+          hi[e] = h;
+          lo[e] = l;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(ready + s);
+      }
+    }
+    // ---------------- epilogue: TMEM lane quarter = warp % 4
+    mbar_wait(tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int m = m0 + row;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 8) {
+      float v[8];
+      tmem_ld8(trow + c0, v);
+      if (m >= p.M || nkb <= 0) continue;
+      const int nb = n0 + c0;
+      if constexpr (EPI == kEpiStore) {
+        float* o = p.out + blockIdx.z * p.split_stride + static_cast<long long>(m) * p.ldo + nb;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (nb + j < p.N) o[j] = v[j];
+      } else {
+        const float g = p.gz[m];
+        const float* xr = p.X + static_cast<long long>(m) * p.ldx;
+        const float* sr = p.fm_s + static_cast<long long>(m) * p.d;
+        float* o = const_cast<float*>(p.out) + static_cast<long long>(m) * p.ldo;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int n = nb + j;
+          if (n < p.N) o[n] = p.scale * (v[j] + g * (sr[n % p.d] - xr[n]));
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(L::TMEM_COLS));
+  }
+}
+
+}  // namespace tc
+}  // namespace sfb

@@ -1,0 +1,295 @@
+// Tensor-core path of the DeepFM-lite tower (tcgen05 3xTF32, see tc_gemm.cuh).
+//
+//   prep   : W1 -> (hi, lo) tf32 parts in both layouts (W1 [K x H] for dX,
+//            W1^T [H x K] for the forward), once per step
+//   GEMM1  : hpre_part[z] = X W1          A = X (K-major, split in smem), split-K z
+//   head   : hpre = b1 + sum_z part; z, p, BCE, gz; dh (+ its hi/lo parts in
+//            row-major and transposed layouts)
+//   GEMM2  : dX = s * (dh W1^T + gz (S - x))   A = dh (pre-split), B = W1
+//   GEMM3  : dW1_part[z] = X^T dh         A = X (MN-major, split in smem), split-K z
+//   reduce : dW1 = sum_z part (fixed order); db1, dw2, db2, loss (fixed order)
+#include <cuda.h>
+
+#include <cstring>
+#include <mutex>
+
+#include "kernels.h"
+#include "tc_gemm.cuh"
+
+namespace sfb {
+
+namespace {
+
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                 const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                 const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                 CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled encoder() {
+  static EncodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiled>(p);
+  });
+  if (!fn) fail(kCuda, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// 2D fp32 tensor [outer][inner] with row stride ld (elements), SWIZZLE_128B box.
+CUtensorMap tmap(const float* base, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_in,
+                 uint32_t box_out) {
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof(m));
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {ld * sizeof(float)};
+  const cuuint32_t box[2] = {box_in, box_out};
+  const cuuint32_t es[2] = {1, 1};
+  const CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base),
+                               dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    fail(kCuda, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+  return m;
+}
+
+__device__ __forceinline__ float rna(float x) { return tc::tf32_rna(x); }
+
+// W1 [K x H] packed -> hi/lo of W1 [K x ldh] and W1^T [H x ldk]
+__global__ void prep_w1_kernel(const float* __restrict__ w1, int K, int H, int ldh, int ldk,
+                               float* __restrict__ w_hi, float* __restrict__ w_lo,
+                               float* __restrict__ wt_hi, float* __restrict__ wt_lo) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<int64_t>(K) * H) return;
+  const int k = static_cast<int>(i / H), j = static_cast<int>(i % H);
+  const float v = w1[i];
+  const float h = rna(v), l = rna(v - h);
+  w_hi[static_cast<int64_t>(k) * ldh + j] = h;
+  w_lo[static_cast<int64_t>(k) * ldh + j] = l;
+  wt_hi[static_cast<int64_t>(j) * ldk + k] = h;
+  wt_lo[static_cast<int64_t>(j) * ldk + k] = l;
+}
+
+// Warp per row: sums the split-K partials of GEMM1, then the DeepFM-lite head.
+__global__ void head_tc_kernel(int rows, int H, int d, int sq_parts, const float* __restrict__ part,
+                               int splits, long long split_stride, const float* __restrict__ b1,
+                               const float* __restrict__ w2, const float* __restrict__ b2p,
+                               const float* __restrict__ fm_s, const float* __restrict__ fm_sqp,
+                               const uint8_t* __restrict__ labels, float inv_rows,
+                               float* __restrict__ logits, float* __restrict__ act,
+                               float* __restrict__ dh, float* __restrict__ gz,
+                               float* __restrict__ lossr, float* __restrict__ dh_hi,
+                               float* __restrict__ dh_lo, int ldh, float* __restrict__ dht_hi,
+                               float* __restrict__ dht_lo, int ldr) {
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  float mlp = 0.f;
+  for (int j = lane; j < H; j += 32) {
+    float h = b1[j];
+    for (int z = 0; z < splits; ++z) h += part[z * split_stride + static_cast<long long>(r) * H + j];
+    act[static_cast<int64_t>(r) * H + j] = h;  // pre-activation for now
+    mlp += fmaxf(h, 0.f) * w2[j];
+  }
+  float ss = 0.f, sq = 0.f;
+  for (int c = lane; c < d; c += 32) {
+    const float v = fm_s[static_cast<int64_t>(r) * d + c];
+    ss += v * v;
+  }
+  for (int c = lane; c < sq_parts; c += 32) sq += fm_sqp[static_cast<int64_t>(r) * sq_parts + c];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mlp += __shfl_xor_sync(0xFFFFFFFFu, mlp, o);
+    ss += __shfl_xor_sync(0xFFFFFFFFu, ss, o);
+    sq += __shfl_xor_sync(0xFFFFFFFFu, sq, o);
+  }
+  const float z = 0.5f * (ss - sq) + (mlp + __ldg(b2p));
+  const float p = 1.f / (1.f + expf(-z));
+  const float y = labels[r] ? 1.f : 0.f;
+  constexpr float kClamp = 1e-7f;
+  const bool clamped = (p < kClamp) || (p > 1.f - kClamp);
+  const float pc = fminf(fmaxf(p, kClamp), 1.f - kClamp);
+  const float g = clamped ? 0.f : (p - y) * inv_rows;
+  for (int j = lane; j < H; j += 32) {
+    const int64_t o = static_cast<int64_t>(r) * H + j;
+    const float hv = act[o];
+    act[o] = fmaxf(hv, 0.f);
+    const float dv = hv > 0.f ? g * w2[j] : 0.f;
+    dh[o] = dv;
+    const float h = rna(dv), l = rna(dv - h);
+    dh_hi[static_cast<int64_t>(r) * ldh + j] = h;
+    dh_lo[static_cast<int64_t>(r) * ldh + j] = l;
+    dht_hi[static_cast<int64_t>(j) * ldr + r] = h;
+    dht_lo[static_cast<int64_t>(j) * ldr + r] = l;
+  }
+  if (lane == 0) {
+    logits[r] = z;
+    gz[r] = g;
+    lossr[r] = -(y * logf(pc) + (1.f - y) * log1pf(-pc));
+  }
+}
+
+int round_up(int a, int b) { return (a + b - 1) / b * b; }
+
+template <int BN, bool A_MN, bool SPLIT_A, int EPI>
+void launch_gemm(dim3 grid, const CUtensorMap& a, const CUtensorMap& alo, const CUtensorMap& bhi,
+                 const CUtensorMap& blo, const tc::Params& p, cudaStream_t s) {
+  auto kern = tc::gemm_tf32x3_kernel<BN, A_MN, SPLIT_A, EPI>;
+  constexpr int smem = tc::Layout<BN>::SMEM;
+  static bool configured = false;  // per instantiation
+  if (!configured) {
+    CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = true;
+  }
+  kern<<<grid, 192, smem, s>>>(a, alo, bhi, blo, p);
+  CUDA_LAUNCH_CHECK();
+}
+
+// split-K factor so that tiles * splits ~ one wave of 148 SMs, no empty split
+void split_k(int tiles, int nkb, int* splits, int* kps) {
+  int s = std::max(1, std::min(nkb, 148 / std::max(1, tiles)));
+  *kps = (nkb + s - 1) / s;
+  *splits = (nkb + *kps - 1) / *kps;
+}
+
+}  // namespace
+
+void TowerTC::init(int rc, int k, int h, int d_) {
+  release();
+  rows_cap = rc;
+  K = k;
+  H = h;
+  d = d_;
+  ldk = round_up(K, 4);
+  ldh = round_up(H, 4);
+  ldr = round_up(rc, 4);
+  const int nkb1 = (K + tc::BKE - 1) / tc::BKE;
+  int kps;
+  split_k(((rc + 127) / 128) * ((H + 63) / 64), nkb1, &s1_max, &kps);
+  const int nkb3 = (rc + tc::BKE - 1) / tc::BKE;
+  split_k(((K + 127) / 128) * ((H + 63) / 64), nkb3, &s3_max, &kps);
+  auto alloc = [](float** p, size_t n) { CUDA_CHECK(cudaMalloc(p, sizeof(float) * std::max<size_t>(n, 1))); };
+  alloc(&w_hi, static_cast<size_t>(K) * ldh);
+  alloc(&w_lo, static_cast<size_t>(K) * ldh);
+  alloc(&wt_hi, static_cast<size_t>(H) * ldk);
+  alloc(&wt_lo, static_cast<size_t>(H) * ldk);
+  alloc(&dh_hi, static_cast<size_t>(rc) * ldh);
+  alloc(&dh_lo, static_cast<size_t>(rc) * ldh);
+  alloc(&dht_hi, static_cast<size_t>(H) * ldr);
+  alloc(&dht_lo, static_cast<size_t>(H) * ldr);
+  alloc(&part1, static_cast<size_t>(s1_max) * rc * H);
+  alloc(&part3, static_cast<size_t>(s3_max) * K * H);
+  CUDA_CHECK(cudaMemset(w_hi, 0, sizeof(float) * K * ldh));
+  CUDA_CHECK(cudaMemset(w_lo, 0, sizeof(float) * K * ldh));
+}
+
+void TowerTC::release() {
+  for (float* p : {w_hi, w_lo, wt_hi, wt_lo, dh_hi, dh_lo, dht_hi, dht_lo, part1, part3})
+    if (p) cudaFree(p);
+  w_hi = w_lo = wt_hi = wt_lo = dh_hi = dh_lo = dht_hi = dht_lo = part1 = part3 = nullptr;
+}
+
+int tower_ldx(int K) { return round_up(K, 4); }
+
+void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc_, const float* X, int ldx,
+                               const float* fm_s, const float* fm_sqp, const uint8_t* labels,
+                               int32_t rows, int F, int d, const float* dense, float* logits,
+                               float* dX, float emb_scale, float* grads, bool accumulate,
+                               cudaStream_t s) {
+  const int K = F * d, H = t.H;
+  SFB_CHECK(rows <= t.rows_cap && rows <= tc_.rows_cap && K == tc_.K && ldx == tc_.ldk,
+            "tower buffers too small");
+  const float* w1 = dense;
+  const float* b1 = dense + static_cast<size_t>(K) * H;
+  const float* w2 = b1 + H;
+  const float* b2p = w2 + H;
+  float* g_w1 = grads;
+  float* g_b1 = grads + static_cast<size_t>(K) * H;
+  float* g_w2 = g_b1 + H;
+  float* g_b2 = g_w2 + H;
+  float* g_loss = g_b2 + 1;
+
+  // W1 hi/lo in both layouts
+  prep_w1_kernel<<<ceil_div(static_cast<int64_t>(K) * H, 256), 256, 0, s>>>(
+      w1, K, H, tc_.ldh, tc_.ldk, tc_.w_hi, tc_.w_lo, tc_.wt_hi, tc_.wt_lo);
+  CUDA_LAUNCH_CHECK();
+
+  // ---- GEMM1: hpre partials = X W1 (A = X K-major, B = W1^T)
+  const int nkb1 = (K + tc::BKE - 1) / tc::BKE;
+  const int mt = (rows + 127) / 128, nt = (H + 63) / 64;
+  int s1, kps1;
+  split_k(mt * nt, nkb1, &s1, &kps1);
+  {
+    const CUtensorMap a = tmap(X, K, rows, ldx, 32, 128);
+    const CUtensorMap bh = tmap(tc_.wt_hi, K, H, tc_.ldk, 32, 64);
+    const CUtensorMap bl = tmap(tc_.wt_lo, K, H, tc_.ldk, 32, 64);
+    tc::Params p{};
+    p.M = rows;
+    p.N = H;
+    p.K = K;
+    p.num_k_blocks = nkb1;
+    p.k_blocks_per_split = kps1;
+    p.out = tc_.part1;
+    p.ldo = H;
+    p.split_stride = static_cast<long long>(rows) * H;
+    launch_gemm<64, false, true, tc::kEpiStore>(dim3(mt, nt, s1), a, a, bh, bl, p, s);
+  }
+  // ---- head
+  head_tc_kernel<<<ceil_div(static_cast<int64_t>(rows) * 32, 256), 256, 0, s>>>(
+      rows, H, d, fm_sq_parts(d), tc_.part1, s1, static_cast<long long>(rows) * H, b1, w2, b2p,
+      fm_s, fm_sqp, labels, 1.f / rows, logits, t.act, t.dh, t.gz, t.lossr, tc_.dh_hi, tc_.dh_lo,
+      tc_.ldh, tc_.dht_hi, tc_.dht_lo, tc_.ldr);
+  CUDA_LAUNCH_CHECK();
+  // ---- GEMM2: dX = scale (dh W1^T + gz (S - x)) (A = dh hi/lo, B = W1 hi/lo, both K-major)
+  {
+    const CUtensorMap ah = tmap(tc_.dh_hi, H, rows, tc_.ldh, 32, 128);
+    const CUtensorMap al = tmap(tc_.dh_lo, H, rows, tc_.ldh, 32, 128);
+    const CUtensorMap bh = tmap(tc_.w_hi, H, K, tc_.ldh, 32, 128);
+    const CUtensorMap bl = tmap(tc_.w_lo, H, K, tc_.ldh, 32, 128);
+    tc::Params p{};
+    p.M = rows;
+    p.N = K;
+    p.K = H;
+    p.num_k_blocks = (H + tc::BKE - 1) / tc::BKE;
+    p.k_blocks_per_split = p.num_k_blocks;
+    p.out = dX;
+    p.ldo = ldx;
+    p.gz = t.gz;
+    p.fm_s = fm_s;
+    p.X = X;
+    p.ldx = ldx;
+    p.d = d;
+    p.scale = emb_scale;
+    launch_gemm<128, false, false, tc::kEpiDx>(dim3(mt, (K + 127) / 128, 1), ah, al, bh, bl, p, s);
+  }
+  // ---- GEMM3: dW1 partials = X^T dh (A = X MN-major, B = dh^T hi/lo K-major)
+  const int nkb3 = (rows + tc::BKE - 1) / tc::BKE;
+  const int mt3 = (K + 127) / 128;
+  int s3, kps3;
+  split_k(mt3 * nt, nkb3, &s3, &kps3);
+  {
+    const CUtensorMap a = tmap(X, K, rows, ldx, 32, 32);
+    const CUtensorMap bh = tmap(tc_.dht_hi, rows, H, tc_.ldr, 32, 64);
+    const CUtensorMap bl = tmap(tc_.dht_lo, rows, H, tc_.ldr, 32, 64);
+    tc::Params p{};
+    p.M = K;
+    p.N = H;
+    p.K = rows;
+    p.num_k_blocks = nkb3;
+    p.k_blocks_per_split = kps3;
+    p.out = tc_.part3;
+    p.ldo = H;
+    p.split_stride = static_cast<long long>(K) * H;
+    launch_gemm<64, true, true, tc::kEpiStore>(dim3(mt3, nt, s3), a, a, bh, bl, p, s);
+  }
+  const int64_t kh = static_cast<int64_t>(K) * H;
+  dw1_reduce(tc_.part3, s3, kh, g_w1, accumulate, s);
+  small_grads(t, rows, H, g_b1, g_w2, g_b2, g_loss, accumulate, s);
+}
+
+}  // namespace sfb

@@ -305,10 +305,23 @@ void TowerBufs::release() {
   hpre = act = dh = gz = lossr = part = nullptr;
 }
 
-void tower_forward_backward(TowerBufs& t, const float* X, const float* fm_s, const float* fm_sqp,
-                            const uint8_t* labels, int32_t rows, int F, int d, const float* dense,
-                            float* logits, float* dX, float emb_scale, float* grads,
-                            bool accumulate, cudaStream_t s) {
+void dw1_reduce(const float* part, int splits, int64_t n, float* out, bool accumulate,
+                cudaStream_t s) {
+  dw1_reduce_kernel<<<ceil_div(n, 256), 256, 0, s>>>(part, splits, n, out, accumulate ? 1 : 0);
+  CUDA_LAUNCH_CHECK();
+}
+
+void small_grads(TowerBufs& t, int rows, int H, float* g_b1, float* g_w2, float* g_b2,
+                 float* g_loss, bool accumulate, cudaStream_t s) {
+  small_grads_kernel<<<H + 2, 256, 0, s>>>(t.dh, t.act, t.gz, t.lossr, rows, H, 1.f / rows, g_b1,
+                                           g_w2, g_b2, g_loss, accumulate ? 1 : 0);
+  CUDA_LAUNCH_CHECK();
+}
+
+void tower_forward_backward_simt(TowerBufs& t, const float* X, const float* fm_s,
+                                 const float* fm_sqp, const uint8_t* labels, int32_t rows, int F,
+                                 int d, const float* dense, float* logits, float* dX,
+                                 float emb_scale, float* grads, bool accumulate, cudaStream_t s) {
   const int K = F * d, H = t.H;
   SFB_CHECK(rows <= t.rows_cap && K == t.K, "tower buffers too small");
   const float* w1 = dense;

@@ -114,7 +114,8 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
   const size_t gd = static_cast<size_t>(n_global_) * d_;
   CUDA_CHECK(cudaMalloc(&d_G_, sizeof(float) * gd));
   CUDA_CHECK(cudaMalloc(&d_dG_, sizeof(float) * gd));
-  const size_t bk = static_cast<size_t>(b_) * K_;
+  ldx_ = tower_ldx(K_);
+  const size_t bk = static_cast<size_t>(b_) * ldx_;
   CUDA_CHECK(cudaMalloc(&d_X_, sizeof(float) * bk));
   CUDA_CHECK(cudaMalloc(&d_dX_, sizeof(float) * bk));
   CUDA_CHECK(cudaMalloc(&d_fm_s_, sizeof(float) * b_ * d_));
@@ -142,6 +143,10 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
   CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_counts_), sizeof(int32_t) * 8 * lanes_, 0));
   CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_loss_), sizeof(float), 0));
   tower_.init(b_, K_, H_, d_);
+  towertc_.init(b_, K_, H_, d_);
+  // validation switch: the fp32 SIMT tiles instead of tcgen05 (only when rows are unpadded)
+  const char* ts = std::getenv("SFCTR_TOWER_SIMT");
+  tower_simt_ = ts && ts[0] == '1' && ldx_ == K_;
 
   const uint64_t owned_rows = (cfg_.vocabulary_size + W_ - 1) / W_;
   const uint64_t host_rows = cfg_.host_table_rows ? cfg_.host_table_rows : owned_rows;
@@ -160,6 +165,7 @@ Trainer::~Trainer() {
   if (stream_) cudaStreamSynchronize(stream_);
   for (auto& l : lane_) l.release();
   tower_.release();
+  towertc_.release();
   vsi_.release();
   for (void* p : {static_cast<void*>(d_in_feat_), static_cast<void*>(d_in_lab_),
                   static_cast<void*>(d_in_win_), static_cast<void*>(d_ids32_),
@@ -362,13 +368,18 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   for (int l = 0; l < lanes_; ++l) {
     const uint32_t* vid = d_vid_ + static_cast<size_t>(lane0_ + l) * b_ * F_;
     const uint8_t* lab = d_labels + static_cast<size_t>(l) * b_;
-    gather_instances(vid, b_, F_, d_, d_G_, d_X_, d_fm_s_, d_fm_sqp_, s);
+    gather_instances(vid, b_, F_, d_, ldx_, d_G_, d_X_, d_fm_s_, d_fm_sqp_, s);
     phase("gather_instances");
-    tower_forward_backward(tower_, d_X_, d_fm_s_, d_fm_sqp_, lab, b_, F_, d_, d_dense_,
-                           d_logits_ + static_cast<size_t>(l) * b_, d_dX_, emb_scale, d_grads_,
-                           l > 0, s);
+    if (tower_simt_)
+      tower_forward_backward_simt(tower_, d_X_, d_fm_s_, d_fm_sqp_, lab, b_, F_, d_, d_dense_,
+                                  d_logits_ + static_cast<size_t>(l) * b_, d_dX_, emb_scale,
+                                  d_grads_, l > 0, s);
+    else
+      tower_forward_backward_tc(tower_, towertc_, d_X_, ldx_, d_fm_s_, d_fm_sqp_, lab, b_, F_, d_,
+                                d_dense_, d_logits_ + static_cast<size_t>(l) * b_, d_dX_,
+                                emb_scale, d_grads_, l > 0, s);
     phase("tower");
-    segment_sum(vid, b_ * F_, d_, d_dX_, d_dG_, s);
+    segment_sum(vid, b_ * F_, F_, d_, ldx_, d_dX_, d_dG_, s);
     phase("segment_sum");
   }
 

@@ -103,6 +103,9 @@ class Trainer {
 
   std::vector<CacheLane> lane_;
   TowerBufs tower_;
+  TowerTC towertc_;
+  int ldx_ = 0;
+  bool tower_simt_ = false;
   int64_t dense_steps_ = 0;
   int64_t steps_done_ = 0;
   int64_t led_[4] = {0, 0, 0, 0};
