@@ -44,6 +44,10 @@ struct Params {
   int ldx;
   int d;
   float scale;
+  // MN-major A descriptor strides (bytes): between 32-element MN atoms, between
+  // 4-row K groups of the SWIZZLE_128B_BASE32B layout
+  uint32_t mn_lbo = 4096;
+  uint32_t mn_sbo = 512;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -82,14 +86,17 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
 
 // sm_100 shared-memory matrix descriptor (cute::UMMA::SmemDescriptor):
 // start>>4 [0,14), LBO>>4 [16,30), SBO>>4 [32,46), version=1 [46,48),
-// base offset 0, layout type [61,64) = 2 (SWIZZLE_128B).
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+// base offset 0, layout type [61,64): 2 = SWIZZLE_128B (16 B chunks, 8-row
+// atoms; K-major operands), 1 = SWIZZLE_128B_BASE32B (32 B chunks, 4-row
+// atoms; the only layout tcgen05 accepts for MN-major tf32 operands).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo,
+                                              uint32_t layout = 2) {
   uint64_t d = 0;
   d |= static_cast<uint64_t>((addr >> 4) & 0x3FFF);
   d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
   d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
   d |= 1ull << 46;
-  d |= 2ull << 61;
+  d |= static_cast<uint64_t>(layout) << 61;
   return d;
 }
 
@@ -243,9 +250,9 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
         for (int kk = 0; kk < BKE / 8; ++kk) {
           uint64_t ah, al;
-          if constexpr (A_MN) {  // 8 k-rows = one 1 KB K-group; MN atoms 4 KB apart
-            ah = smem_desc(smem_u32(a_hi(s)) + kk * 1024, 4096, 1024);
-            al = smem_desc(smem_u32(a_lo(s)) + kk * 1024, 4096, 1024);
+          if constexpr (A_MN) {  // 8 k-rows = two 512 B K-groups; MN atoms 4 KB apart
+            ah = smem_desc(smem_u32(a_hi(s)) + kk * 1024, p.mn_lbo, p.mn_sbo, 1);
+            al = smem_desc(smem_u32(a_lo(s)) + kk * 1024, p.mn_lbo, p.mn_sbo, 1);
           } else {  // K-major: advance 32 B inside the 128 B swizzle row
             ah = smem_desc(smem_u32(a_hi(s)) + kk * 32, 16, 1024);
             al = smem_desc(smem_u32(a_lo(s)) + kk * 32, 16, 1024);

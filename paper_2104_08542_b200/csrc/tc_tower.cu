@@ -40,9 +40,12 @@ EncodeTiled encoder() {
   return fn;
 }
 
-// 2D fp32 tensor [outer][inner] with row stride ld (elements), SWIZZLE_128B box.
+// 2D fp32 tensor [outer][inner] with row stride ld (elements). SWIZZLE_128B
+// boxes for K-major operands; SWIZZLE_128B_ATOM_32B (32 B chunks) for the
+// MN-major tf32 operand (tcgen05's SWIZZLE_128B_BASE32B smem layout).
 CUtensorMap tmap(const float* base, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_in,
-                 uint32_t box_out) {
+                 uint32_t box_out,
+                 CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   CUtensorMap m;
   std::memset(&m, 0, sizeof(m));
   const cuuint64_t dims[2] = {inner, outer};
@@ -50,8 +53,8 @@ CUtensorMap tmap(const float* base, uint64_t inner, uint64_t outer, uint64_t ld,
   const cuuint32_t box[2] = {box_in, box_out};
   const cuuint32_t es[2] = {1, 1};
   const CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base),
-                               dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     fail(kCuda, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
@@ -273,7 +276,7 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc_, const float* X, int l
   int s3, kps3;
   split_k(mt3 * nt, nkb3, &s3, &kps3);
   {
-    const CUtensorMap a = tmap(X, K, rows, ldx, 32, 32);
+    const CUtensorMap a = tmap(X, K, rows, ldx, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     const CUtensorMap bh = tmap(tc_.dht_hi, rows, H, tc_.ldr, 32, 64);
     const CUtensorMap bl = tmap(tc_.dht_lo, rows, H, tc_.ldr, 32, 64);
     tc::Params p{};
