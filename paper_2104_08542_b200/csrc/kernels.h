@@ -35,6 +35,7 @@ struct TowerBufs {
   float* gz = nullptr;     // [rows]    d(mean loss)/dz
   float* lossr = nullptr;  // [rows]    per-row BCE
   float* part = nullptr;   // [splits, K, H] dW1 partials
+  float* sg_part = nullptr;  // [128, 2H+2] small-gradient chunk partials
   int splits = 0;
   void init(int rows_cap, int K, int H, int d);
   void release();
@@ -49,7 +50,6 @@ struct TowerTC {
   float *w_hi = nullptr, *w_lo = nullptr;    // [K x ldh]
   float *wt_hi = nullptr, *wt_lo = nullptr;  // [H x ldk]
   float *dh_hi = nullptr, *dh_lo = nullptr;  // [rows x ldh]
-  float *dht_hi = nullptr, *dht_lo = nullptr;  // [H x ldr]
   float* part1 = nullptr;  // [s1, rows, H]
   float* part3 = nullptr;  // [s3, K, H]
   void init(int rows_cap, int K, int H, int d);

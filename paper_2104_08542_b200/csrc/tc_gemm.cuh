@@ -168,7 +168,8 @@ struct Layout {
 
 // A_MN: A is MN-major (4 TMA boxes of 32 m x 32 k); otherwise K-major (box 32 k x 128 m).
 // SPLIT_A: A arrives as raw fp32 and is split in smem; otherwise tmAlo supplies the lo part.
-template <int BN, bool A_MN, bool SPLIT_A, int EPI>
+// B_MN: B is MN-major (BN/32 TMA boxes of 32 n x 32 k, BASE32B layout); otherwise K-major.
+template <int BN, bool A_MN, bool SPLIT_A, int EPI, bool B_MN = false>
 __global__ void __launch_bounds__(192, 1)
     gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmAlo,
@@ -234,13 +235,22 @@ __global__ void __launch_bounds__(192, 1)
           tma_load_2d(&tmA, full + s, a_hi(s), kc, m0);
           if constexpr (!SPLIT_A) tma_load_2d(&tmAlo, full + s, a_lo(s), kc, m0);
         }
-        tma_load_2d(&tmBhi, full + s, b_hi(s), kc, n0);
-        tma_load_2d(&tmBlo, full + s, b_lo(s), kc, n0);
+        if constexpr (B_MN) {
+#pragma unroll
+          for (int b = 0; b < BN / 32; ++b) {
+            tma_load_2d(&tmBhi, full + s, b_hi(s) + b * 4096, n0 + b * 32, kc);
+            tma_load_2d(&tmBlo, full + s, b_lo(s) + b * 4096, n0 + b * 32, kc);
+          }
+        } else {
+          tma_load_2d(&tmBhi, full + s, b_hi(s), kc, n0);
+          tma_load_2d(&tmBlo, full + s, b_lo(s), kc, n0);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer
-      constexpr uint32_t idesc = idesc_tf32(BM, BN, A_MN ? 1 : 0, 0);
+      static_assert(!B_MN || BN % 32 == 0, "MN-major B needs whole 32-column atoms");
+      constexpr uint32_t idesc = idesc_tf32(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
       for (int i = 0; i < nkb; ++i) {
         const int s = i % ST;
         const uint32_t ph = (i / ST) & 1;
@@ -257,8 +267,14 @@ __global__ void __launch_bounds__(192, 1)
             ah = smem_desc(smem_u32(a_hi(s)) + kk * 32, 16, 1024);
             al = smem_desc(smem_u32(a_lo(s)) + kk * 32, 16, 1024);
           }
-          const uint64_t bh = smem_desc(smem_u32(b_hi(s)) + kk * 32, 16, 1024);
-          const uint64_t bl = smem_desc(smem_u32(b_lo(s)) + kk * 32, 16, 1024);
+          uint64_t bh, bl;
+          if constexpr (B_MN) {
+            bh = smem_desc(smem_u32(b_hi(s)) + kk * 1024, 4096, 512, 1);
+            bl = smem_desc(smem_u32(b_lo(s)) + kk * 1024, 4096, 512, 1);
+          } else {
+            bh = smem_desc(smem_u32(b_hi(s)) + kk * 32, 16, 1024);
+            bl = smem_desc(smem_u32(b_lo(s)) + kk * 32, 16, 1024);
+          }
           mma_tf32(tmem, ah, bh, idesc, (i > 0 || kk > 0) ? 1u : 0u);
           mma_tf32(tmem, ah, bl, idesc, 1u);
           mma_tf32(tmem, al, bh, idesc, 1u);
@@ -294,30 +310,44 @@ __global__ void __launch_bounds__(192, 1)
     // ---------------- epilogue: TMEM lane quarter = warp % 4
     mbar_wait(tmem_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // (1) TMEM -> smem tile [128][BN+1] (one row per thread; the +1 pad makes
+    //     the row-per-thread stores bank-conflict free). All MMAs have
+    //     completed, so the stage ring is free to reuse.
     const int q = warp & 3;
     const int row = q * 32 + lane;
-    const int m = m0 + row;
     const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
+    float* tile = reinterpret_cast<float*>(smem);
+    constexpr int TS = BN + 1;
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 8) {
       float v[8];
       tmem_ld8(trow + c0, v);
-      if (m >= p.M || nkb <= 0) continue;
-      const int nb = n0 + c0;
-      if constexpr (EPI == kEpiStore) {
-        float* o = p.out + blockIdx.z * p.split_stride + static_cast<long long>(m) * p.ldo + nb;
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (nb + j < p.N) o[j] = v[j];
-      } else {
-        const float g = p.gz[m];
-        const float* xr = p.X + static_cast<long long>(m) * p.ldx;
-        const float* sr = p.fm_s + static_cast<long long>(m) * p.d;
-        float* o = const_cast<float*>(p.out) + static_cast<long long>(m) * p.ldo;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int n = nb + j;
-          if (n < p.N) o[n] = p.scale * (v[j] + g * (sr[n % p.d] - xr[n]));
+      for (int j = 0; j < 8; ++j) tile[row * TS + c0 + j] = v[j];
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    // (2) coalesced write-out: warp w2 takes rows w2, w2+4, ...; lanes sweep columns
+    const int w2 = t >> 5;
+    if (nkb > 0) {
+#pragma unroll 1
+      for (int r = w2; r < BM; r += 4) {
+        const int m = m0 + r;
+        if (m >= p.M) break;
+        if constexpr (EPI == kEpiStore) {
+          float* o = p.out + blockIdx.z * p.split_stride + static_cast<long long>(m) * p.ldo;
+          for (int c = lane; c < BN; c += 32) {
+            const int n = n0 + c;
+            if (n < p.N) o[n] = tile[r * TS + c];
+          }
+        } else {
+          const float g = p.gz[m];
+          const float* xr = p.X + static_cast<long long>(m) * p.ldx;
+          const float* sr = p.fm_s + static_cast<long long>(m) * p.d;
+          float* o = p.out + static_cast<long long>(m) * p.ldo;
+          for (int c = lane; c < BN; c += 32) {
+            const int n = n0 + c;
+            if (n < p.N) o[n] = p.scale * (tile[r * TS + c] + g * (sr[n % p.d] - __ldg(xr + n)));
+          }
         }
       }
     }

@@ -87,8 +87,7 @@ __global__ void head_tc_kernel(int rows, int H, int d, int sq_parts, const float
                                float* __restrict__ logits, float* __restrict__ act,
                                float* __restrict__ dh, float* __restrict__ gz,
                                float* __restrict__ lossr, float* __restrict__ dh_hi,
-                               float* __restrict__ dh_lo, int ldh, float* __restrict__ dht_hi,
-                               float* __restrict__ dht_lo, int ldr) {
+                               float* __restrict__ dh_lo, int ldh) {
   const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (r >= rows) return;
@@ -127,8 +126,6 @@ __global__ void head_tc_kernel(int rows, int H, int d, int sq_parts, const float
     const float h = rna(dv), l = rna(dv - h);
     dh_hi[static_cast<int64_t>(r) * ldh + j] = h;
     dh_lo[static_cast<int64_t>(r) * ldh + j] = l;
-    dht_hi[static_cast<int64_t>(j) * ldr + r] = h;
-    dht_lo[static_cast<int64_t>(j) * ldr + r] = l;
   }
   if (lane == 0) {
     logits[r] = z;
@@ -139,10 +136,10 @@ __global__ void head_tc_kernel(int rows, int H, int d, int sq_parts, const float
 
 int round_up(int a, int b) { return (a + b - 1) / b * b; }
 
-template <int BN, bool A_MN, bool SPLIT_A, int EPI>
+template <int BN, bool A_MN, bool SPLIT_A, int EPI, bool B_MN = false>
 void launch_gemm(dim3 grid, const CUtensorMap& a, const CUtensorMap& alo, const CUtensorMap& bhi,
                  const CUtensorMap& blo, const tc::Params& p, cudaStream_t s) {
-  auto kern = tc::gemm_tf32x3_kernel<BN, A_MN, SPLIT_A, EPI>;
+  auto kern = tc::gemm_tf32x3_kernel<BN, A_MN, SPLIT_A, EPI, B_MN>;
   constexpr int smem = tc::Layout<BN>::SMEM;
   static bool configured = false;  // per instantiation
   if (!configured) {
@@ -183,8 +180,6 @@ void TowerTC::init(int rc, int k, int h, int d_) {
   alloc(&wt_lo, static_cast<size_t>(H) * ldk);
   alloc(&dh_hi, static_cast<size_t>(rc) * ldh);
   alloc(&dh_lo, static_cast<size_t>(rc) * ldh);
-  alloc(&dht_hi, static_cast<size_t>(H) * ldr);
-  alloc(&dht_lo, static_cast<size_t>(H) * ldr);
   alloc(&part1, static_cast<size_t>(s1_max) * rc * H);
   alloc(&part3, static_cast<size_t>(s3_max) * K * H);
   CUDA_CHECK(cudaMemset(w_hi, 0, sizeof(float) * K * ldh));
@@ -192,9 +187,9 @@ void TowerTC::init(int rc, int k, int h, int d_) {
 }
 
 void TowerTC::release() {
-  for (float* p : {w_hi, w_lo, wt_hi, wt_lo, dh_hi, dh_lo, dht_hi, dht_lo, part1, part3})
+  for (float* p : {w_hi, w_lo, wt_hi, wt_lo, dh_hi, dh_lo, part1, part3})
     if (p) cudaFree(p);
-  w_hi = w_lo = wt_hi = wt_lo = dh_hi = dh_lo = dht_hi = dht_lo = part1 = part3 = nullptr;
+  w_hi = w_lo = wt_hi = wt_lo = dh_hi = dh_lo = part1 = part3 = nullptr;
 }
 
 int tower_ldx(int K) { return round_up(K, 4); }
@@ -246,7 +241,7 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc_, const float* X, int l
   head_tc_kernel<<<ceil_div(static_cast<int64_t>(rows) * 32, 256), 256, 0, s>>>(
       rows, H, d, fm_sq_parts(d), tc_.part1, s1, static_cast<long long>(rows) * H, b1, w2, b2p,
       fm_s, fm_sqp, labels, 1.f / rows, logits, t.act, t.dh, t.gz, t.lossr, tc_.dh_hi, tc_.dh_lo,
-      tc_.ldh, tc_.dht_hi, tc_.dht_lo, tc_.ldr);
+      tc_.ldh);
   CUDA_LAUNCH_CHECK();
   // ---- GEMM2: dX = scale (dh W1^T + gz (S - x)) (A = dh hi/lo, B = W1 hi/lo, both K-major)
   {
@@ -270,15 +265,15 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc_, const float* X, int l
     p.scale = emb_scale;
     launch_gemm<128, false, false, tc::kEpiDx>(dim3(mt, (K + 127) / 128, 1), ah, al, bh, bl, p, s);
   }
-  // ---- GEMM3: dW1 partials = X^T dh (A = X MN-major, B = dh^T hi/lo K-major)
+  // ---- GEMM3: dW1 partials = X^T dh (A = X MN-major, B = dh hi/lo MN-major)
   const int nkb3 = (rows + tc::BKE - 1) / tc::BKE;
   const int mt3 = (K + 127) / 128;
   int s3, kps3;
   split_k(mt3 * nt, nkb3, &s3, &kps3);
   {
     const CUtensorMap a = tmap(X, K, rows, ldx, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-    const CUtensorMap bh = tmap(tc_.dht_hi, rows, H, tc_.ldr, 32, 64);
-    const CUtensorMap bl = tmap(tc_.dht_lo, rows, H, tc_.ldr, 32, 64);
+    const CUtensorMap bh = tmap(tc_.dh_hi, H, rows, tc_.ldh, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    const CUtensorMap bl = tmap(tc_.dh_lo, H, rows, tc_.ldh, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     tc::Params p{};
     p.M = K;
     p.N = H;
@@ -288,7 +283,7 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc_, const float* X, int l
     p.out = tc_.part3;
     p.ldo = H;
     p.split_stride = static_cast<long long>(K) * H;
-    launch_gemm<64, true, true, tc::kEpiStore>(dim3(mt3, nt, s3), a, a, bh, bl, p, s);
+    launch_gemm<64, true, true, tc::kEpiStore, true>(dim3(mt3, nt, s3), a, a, bh, bl, p, s);
   }
   const int64_t kh = static_cast<int64_t>(K) * H;
   dw1_reduce(tc_.part3, s3, kh, g_w1, accumulate, s);

@@ -297,11 +297,13 @@ void TowerBufs::init(int rc, int k, int h, int dim) {
   const int kt = ceil_div(K, TB), ht = ceil_div(H, TB);
   splits = std::max(1, std::min(ceil_div(rc, BK), (2 * 148 + kt * ht - 1) / (kt * ht)));
   CUDA_CHECK(cudaMalloc(&part, sizeof(float) * static_cast<size_t>(splits) * K * H));
+  CUDA_CHECK(cudaMalloc(&sg_part, sizeof(float) * 128 * (2 * h + 2)));
 }
 
 void TowerBufs::release() {
-  for (float* p : {hpre, act, dh, gz, lossr, part})
+  for (float* p : {hpre, act, dh, gz, lossr, part, sg_part})
     if (p) cudaFree(p);
+  sg_part = nullptr;
   hpre = act = dh = gz = lossr = part = nullptr;
 }
 
@@ -311,10 +313,71 @@ void dw1_reduce(const float* part, int splits, int64_t n, float* out, bool accum
   CUDA_LAUNCH_CHECK();
 }
 
+namespace {
+// Phase 1: block c reduces rows [c*R, (c+1)*R) with column-coalesced reads of
+// dh/act (thread j <-> column j), writing partials [c][2H+2] =
+// (db1[0..H) | dw2[0..H) | db2 | loss). Phase 2 sums the chunks in order.
+constexpr int kSgChunks = 128;
+__global__ void small_grads_p1(const float* __restrict__ dh, const float* __restrict__ act,
+                               const float* __restrict__ gz, const float* __restrict__ lossr,
+                               int rows, int H, float* __restrict__ part) {
+  const int c = blockIdx.x, tid = threadIdx.x;
+  const int R = (rows + gridDim.x - 1) / gridDim.x;
+  const int r0 = c * R, r1 = min(rows, r0 + R);
+  float* out = part + static_cast<int64_t>(c) * (2 * H + 2);
+  for (int j = tid; j < H; j += blockDim.x) {
+    float a = 0.f, b = 0.f;
+    for (int r = r0; r < r1; ++r) {
+      const int64_t o = static_cast<int64_t>(r) * H + j;
+      a += dh[o];
+      b += gz[r] * act[o];
+    }
+    out[j] = a;
+    out[H + j] = b;
+  }
+  __shared__ float red[2][256];
+  float s0 = 0.f, s1 = 0.f;
+  for (int r = r0 + tid; r < r1; r += blockDim.x) {
+    s0 += gz[r];
+    s1 += lossr[r];
+  }
+  red[0][tid] = s0;
+  red[1][tid] = s1;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (tid < o) {
+      red[0][tid] += red[0][tid + o];
+      red[1][tid] += red[1][tid + o];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    out[2 * H] = red[0][0];
+    out[2 * H + 1] = red[1][0];
+  }
+}
+__global__ void small_grads_p2(const float* __restrict__ part, int chunks, int H, float inv_rows,
+                               float* __restrict__ g_db1, float* __restrict__ g_dw2,
+                               float* __restrict__ g_db2, float* __restrict__ g_loss,
+                               int accumulate) {
+  const int n = 2 * H + 2;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    float s = 0.f;
+    for (int c = 0; c < chunks; ++c) s += part[static_cast<int64_t>(c) * n + i];
+    float* dst = i < H ? g_db1 + i : (i < 2 * H ? g_dw2 + (i - H) : (i == 2 * H ? g_db2 : g_loss));
+    if (i == 2 * H + 1) s *= inv_rows;
+    *dst = accumulate ? *dst + s : s;
+  }
+}
+}  // namespace
+
 void small_grads(TowerBufs& t, int rows, int H, float* g_b1, float* g_w2, float* g_b2,
                  float* g_loss, bool accumulate, cudaStream_t s) {
-  small_grads_kernel<<<H + 2, 256, 0, s>>>(t.dh, t.act, t.gz, t.lossr, rows, H, 1.f / rows, g_b1,
-                                           g_w2, g_b2, g_loss, accumulate ? 1 : 0);
+  const int chunks = std::max(1, std::min(kSgChunks, rows));
+  small_grads_p1<<<chunks, 256, 0, s>>>(t.dh, t.act, t.gz, t.lossr, rows, H, t.sg_part);
+  CUDA_LAUNCH_CHECK();
+  small_grads_p2<<<1, 256, 0, s>>>(t.sg_part, chunks, H, 1.f / rows, g_b1, g_w2, g_b2, g_loss,
+                                   accumulate ? 1 : 0);
   CUDA_LAUNCH_CHECK();
 }
 

