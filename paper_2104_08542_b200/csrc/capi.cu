@@ -514,6 +514,7 @@ int sfctr_model_forward_backward(int device, int32_t rows, int32_t fields, int32
     sfb::fm_sums(d_x, rows, fields, dim, ldx, d_s, d_sq, nullptr);
     sfb::tower_forward_backward_tc(tb, tt, d_x, ldx, d_s, d_sq, d_y, rows, fields, dim, d_dense,
                                    d_lg, d_dx, 1.f, d_g, false, nullptr);
+    sfb::fm_grad_add(d_x, rows, fields, dim, ldx, d_s, tb.gz, 1.f, d_dx, nullptr);
     CUDA_CHECK(cudaDeviceSynchronize());
     std::vector<float> g(P + 1);
     CUDA_CHECK(cudaMemcpy(g.data(), d_g, sizeof(float) * (P + 1), cudaMemcpyDeviceToHost));

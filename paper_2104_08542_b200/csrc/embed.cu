@@ -115,28 +115,56 @@ __global__ void fm_sums_kernel(const float* __restrict__ X, int32_t rows, int F,
   else atomicAdd(fm_sqp + r * parts + (c / 4), sq);
 }
 
-__global__ void segment_sum_v4(const uint32_t* __restrict__ vid, int32_t n, int d4,
-                               const float4* __restrict__ dX, float* __restrict__ dG) {
+// The embedding gradient of position p = (row r, field f) is
+//   dX_mlp[p] + scale * gz[r] * (S_r - v_p)          (FM: d/dv_f sum_{i<j}<v_i,v_j>)
+// The tower writes the MLP part; the FM part is added here, where v_p = G[vid[p]]
+// is an L2-resident re-read of the row being scattered to.
+__global__ void segment_sum_v4(const uint32_t* __restrict__ vid, int32_t n, int F, int d4,
+                               const float4* __restrict__ dX, const float4* __restrict__ G,
+                               const float4* __restrict__ fm_s, const float* __restrict__ gz,
+                               float scale, float* __restrict__ dG) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= static_cast<int64_t>(n) * d4) return;
   const int64_t p = i / d4;
   const int c = static_cast<int>(i - p * d4);
-  const float4 g = __ldcs(dX + i);
-  float* dst = dG + (static_cast<int64_t>(__ldg(vid + p)) * d4 + c) * 4;
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(g.x), "f"(g.y),
-               "f"(g.z), "f"(g.w)
+  const int64_t r = p / F;
+  const uint32_t v = __ldg(vid + p);
+  const float4 a = __ldcs(dX + i);
+  const float4 e = __ldg(G + static_cast<int64_t>(v) * d4 + c);
+  const float4 s = __ldg(fm_s + r * d4 + c);
+  const float k = scale * __ldg(gz + r);
+  float* dst = dG + (static_cast<int64_t>(v) * d4 + c) * 4;
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst),
+               "f"(a.x + k * (s.x - e.x)), "f"(a.y + k * (s.y - e.y)), "f"(a.z + k * (s.z - e.z)),
+               "f"(a.w + k * (s.w - e.w))
                : "memory");
 }
 
 __global__ void segment_sum_s(const uint32_t* __restrict__ vid, int32_t n, int F, int d, int ldx,
-                              const float* __restrict__ dX, float* __restrict__ dG) {
+                              const float* __restrict__ dX, const float* __restrict__ G,
+                              const float* __restrict__ fm_s, const float* __restrict__ gz,
+                              float scale, float* __restrict__ dG) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= static_cast<int64_t>(n) * d) return;
   const int64_t p = i / d;  // position = row * F + field
   const int c = static_cast<int>(i - p * d);
   const int64_t r = p / F;
   const int f = static_cast<int>(p - r * F);
-  atomicAdd(dG + static_cast<int64_t>(vid[p]) * d + c, dX[r * ldx + f * d + c]);
+  const int64_t v = vid[p];
+  const float g = dX[r * ldx + f * d + c] + scale * gz[r] * (fm_s[r * d + c] - G[v * d + c]);
+  atomicAdd(dG + v * d + c, g);
+}
+
+// dx[r, k] += scale * gz[r] * (fm_s[r, k % d] - x[r, k])  (standalone model op)
+__global__ void fm_grad_add_kernel(const float* __restrict__ X, int32_t rows, int K, int d, int ldx,
+                                   const float* __restrict__ fm_s, const float* __restrict__ gz,
+                                   float scale, float* __restrict__ dX) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<int64_t>(rows) * K) return;
+  const int64_t r = i / K;
+  const int k = static_cast<int>(i - r * K);
+  const int64_t o = r * ldx + k;
+  dX[o] += scale * gz[r] * (fm_s[r * d + (k % d)] - X[o]);
 }
 
 // Lazy Adam: t = adam_steps + 1 per row; bias
@@ -241,16 +269,26 @@ void fm_sums(const float* X, int32_t rows, int F, int d, int ldx, float* fm_s, f
   CUDA_LAUNCH_CHECK();
 }
 
-void segment_sum(const uint32_t* vid, int32_t n, int F, int d, int ldx, const float* dX, float* dG,
+void fm_grad_add(const float* X, int32_t rows, int F, int d, int ldx, const float* fm_s,
+                 const float* gz, float scale, float* dX, cudaStream_t s) {
+  const int64_t n = static_cast<int64_t>(rows) * F * d;
+  if (n <= 0) return;
+  fm_grad_add_kernel<<<ceil_div(n, 256), 256, 0, s>>>(X, rows, F * d, d, ldx, fm_s, gz, scale, dX);
+  CUDA_LAUNCH_CHECK();
+}
+
+void segment_sum(const uint32_t* vid, int32_t n, int F, int d, int ldx, const float* dX,
+                 const float* G, const float* fm_s, const float* gz, float scale, float* dG,
                  cudaStream_t s) {
   if (n <= 0) return;
   if ((d & 3) == 0 && ldx == F * d) {
     const int64_t m = static_cast<int64_t>(n) * (d / 4);
-    segment_sum_v4<<<ceil_div(m, 256), 256, 0, s>>>(vid, n, d / 4,
-                                                    reinterpret_cast<const float4*>(dX), dG);
+    segment_sum_v4<<<ceil_div(m, 256), 256, 0, s>>>(
+        vid, n, F, d / 4, reinterpret_cast<const float4*>(dX), reinterpret_cast<const float4*>(G),
+        reinterpret_cast<const float4*>(fm_s), gz, scale, dG);
   } else {
     const int64_t m = static_cast<int64_t>(n) * d;
-    segment_sum_s<<<ceil_div(m, 256), 256, 0, s>>>(vid, n, F, d, ldx, dX, dG);
+    segment_sum_s<<<ceil_div(m, 256), 256, 0, s>>>(vid, n, F, d, ldx, dX, G, fm_s, gz, scale, dG);
   }
   CUDA_LAUNCH_CHECK();
 }

@@ -18,9 +18,14 @@ int fm_sq_parts(int d);  // columns of fm_sqp per row
 // FM sums of a materialised X (standalone model op)
 void fm_sums(const float* X, int32_t rows, int F, int d, int ldx, float* fm_s, float* fm_sqp,
              cudaStream_t s);
-// segment_sum: dG[vid[i]] += dX[i] (vector red.global.add.v4.f32)
-void segment_sum(const uint32_t* vid, int32_t n, int F, int d, int ldx, const float* dX, float* dG,
+// segment_sum: dG[vid[p]] += dX_mlp[p] + scale*gz[r]*(fm_s[r] - G[vid[p]]) for the lane's
+// positions p = (r, f) (vector red.global.add.v4.f32)
+void segment_sum(const uint32_t* vid, int32_t n, int F, int d, int ldx, const float* dX,
+                 const float* G, const float* fm_s, const float* gz, float scale, float* dG,
                  cudaStream_t s);
+// dX[r, k] += scale * gz[r] * (fm_s[r, k % d] - X[r, k]) (FM part, standalone model op)
+void fm_grad_add(const float* X, int32_t rows, int F, int d, int ldx, const float* fm_s,
+                 const float* gz, float scale, float* dX, cudaStream_t s);
 // update_sparse: lazy Adam on the lane's owned rows, per-row step count
 void sparse_adam(const uint32_t* own_k, const uint32_t* own_slot, int32_t n_own, const float* dG,
                  int d, float* emb, float* mom, float* vel, int32_t* steps, const float* bc1,

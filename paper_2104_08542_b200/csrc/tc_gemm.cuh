@@ -333,21 +333,13 @@ __global__ void __launch_bounds__(192, 1)
       for (int r = w2; r < BM; r += 4) {
         const int m = m0 + r;
         if (m >= p.M) break;
-        if constexpr (EPI == kEpiStore) {
-          float* o = p.out + blockIdx.z * p.split_stride + static_cast<long long>(m) * p.ldo;
-          for (int c = lane; c < BN; c += 32) {
-            const int n = n0 + c;
-            if (n < p.N) o[n] = tile[r * TS + c];
-          }
-        } else {
-          const float g = p.gz[m];
-          const float* xr = p.X + static_cast<long long>(m) * p.ldx;
-          const float* sr = p.fm_s + static_cast<long long>(m) * p.d;
-          float* o = p.out + static_cast<long long>(m) * p.ldo;
-          for (int c = lane; c < BN; c += 32) {
-            const int n = n0 + c;
-            if (n < p.N) o[n] = p.scale * (tile[r * TS + c] + g * (sr[n % p.d] - __ldg(xr + n)));
-          }
+        // store-only epilogue: no global loads, so nothing serialises on DRAM latency
+        float* o = p.out + blockIdx.z * p.split_stride + static_cast<long long>(m) * p.ldo;
+        const float sc = EPI == kEpiStore ? 1.f : p.scale;
+#pragma unroll
+        for (int c = lane; c < BN; c += 32) {
+          const int n = n0 + c;
+          if (n < p.N) o[n] = sc * tile[r * TS + c];
         }
       }
     }

@@ -156,7 +156,8 @@ __global__ void __launch_bounds__(256) dx_kernel(const float* __restrict__ x,
       const int k = k0 + tx * 4 + v;
       if (k >= K) continue;
       const int64_t o = static_cast<int64_t>(r) * K + k;
-      dX[o] = scale * (acc[u][v] + g * (fm_s[static_cast<int64_t>(r) * d + (k % d)] - x[o]));
+      (void)g;  // the FM part is added by segment_sum / fm_grad_add
+      dX[o] = scale * acc[u][v];
     }
   }
 }
@@ -297,7 +298,7 @@ void TowerBufs::init(int rc, int k, int h, int dim) {
   const int kt = ceil_div(K, TB), ht = ceil_div(H, TB);
   splits = std::max(1, std::min(ceil_div(rc, BK), (2 * 148 + kt * ht - 1) / (kt * ht)));
   CUDA_CHECK(cudaMalloc(&part, sizeof(float) * static_cast<size_t>(splits) * K * H));
-  CUDA_CHECK(cudaMalloc(&sg_part, sizeof(float) * 128 * (2 * h + 2)));
+  CUDA_CHECK(cudaMalloc(&sg_part, sizeof(float) * 256 * (2 * h + 2)));  // kSgChunks rows
 }
 
 void TowerBufs::release() {
@@ -317,7 +318,7 @@ namespace {
 // Phase 1: block c reduces rows [c*R, (c+1)*R) with column-coalesced reads of
 // dh/act (thread j <-> column j), writing partials [c][2H+2] =
 // (db1[0..H) | dw2[0..H) | db2 | loss). Phase 2 sums the chunks in order.
-constexpr int kSgChunks = 128;
+constexpr int kSgChunks = 256;
 __global__ void small_grads_p1(const float* __restrict__ dh, const float* __restrict__ act,
                                const float* __restrict__ gz, const float* __restrict__ lossr,
                                int rows, int H, float* __restrict__ part) {
@@ -326,14 +327,23 @@ __global__ void small_grads_p1(const float* __restrict__ dh, const float* __rest
   const int r0 = c * R, r1 = min(rows, r0 + R);
   float* out = part + static_cast<int64_t>(c) * (2 * H + 2);
   for (int j = tid; j < H; j += blockDim.x) {
-    float a = 0.f, b = 0.f;
-    for (int r = r0; r < r1; ++r) {
-      const int64_t o = static_cast<int64_t>(r) * H + j;
-      a += dh[o];
-      b += gz[r] * act[o];
+    float a[4] = {0.f, 0.f, 0.f, 0.f}, b[4] = {0.f, 0.f, 0.f, 0.f};
+    int r = r0;
+    for (; r + 4 <= r1; r += 4) {  // 4 independent row streams in flight
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t o = static_cast<int64_t>(r + u) * H + j;
+        a[u] += dh[o];
+        b[u] += gz[r + u] * act[o];
+      }
     }
-    out[j] = a;
-    out[H + j] = b;
+    for (; r < r1; ++r) {
+      const int64_t o = static_cast<int64_t>(r) * H + j;
+      a[0] += dh[o];
+      b[0] += gz[r] * act[o];
+    }
+    out[j] = (a[0] + a[1]) + (a[2] + a[3]);
+    out[H + j] = (b[0] + b[1]) + (b[2] + b[3]);
   }
   __shared__ float red[2][256];
   float s0 = 0.f, s1 = 0.f;
@@ -360,14 +370,19 @@ __global__ void small_grads_p2(const float* __restrict__ part, int chunks, int H
                                float* __restrict__ g_db1, float* __restrict__ g_dw2,
                                float* __restrict__ g_db2, float* __restrict__ g_loss,
                                int accumulate) {
+  // warp per output; lanes take chunks lane, lane+32, ...; fixed shuffle tree (deterministic)
   const int n = 2 * H + 2;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    float s = 0.f;
-    for (int c = 0; c < chunks; ++c) s += part[static_cast<int64_t>(c) * n + i];
-    float* dst = i < H ? g_db1 + i : (i < 2 * H ? g_dw2 + (i - H) : (i == 2 * H ? g_db2 : g_loss));
-    if (i == 2 * H + 1) s *= inv_rows;
-    *dst = accumulate ? *dst + s : s;
-  }
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  float s = 0.f;
+  for (int c = lane; c < chunks; c += 32) s += part[static_cast<int64_t>(c) * n + i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+  if (lane) return;
+  float* dst = i < H ? g_db1 + i : (i < 2 * H ? g_dw2 + (i - H) : (i == 2 * H ? g_db2 : g_loss));
+  if (i == 2 * H + 1) s *= inv_rows;
+  *dst = accumulate ? *dst + s : s;
 }
 }  // namespace
 
@@ -376,8 +391,8 @@ void small_grads(TowerBufs& t, int rows, int H, float* g_b1, float* g_w2, float*
   const int chunks = std::max(1, std::min(kSgChunks, rows));
   small_grads_p1<<<chunks, 256, 0, s>>>(t.dh, t.act, t.gz, t.lossr, rows, H, t.sg_part);
   CUDA_LAUNCH_CHECK();
-  small_grads_p2<<<1, 256, 0, s>>>(t.sg_part, chunks, H, 1.f / rows, g_b1, g_w2, g_b2, g_loss,
-                                   accumulate ? 1 : 0);
+  small_grads_p2<<<ceil_div(2 * H + 2, 8), 256, 0, s>>>(t.sg_part, chunks, H, 1.f / rows, g_b1,
+                                                         g_w2, g_b2, g_loss, accumulate ? 1 : 0);
   CUDA_LAUNCH_CHECK();
 }
 

@@ -379,7 +379,7 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
                                 d_dense_, d_logits_ + static_cast<size_t>(l) * b_, d_dX_,
                                 emb_scale, d_grads_, l > 0, s);
     phase("tower");
-    segment_sum(vid, b_ * F_, F_, d_, ldx_, d_dX_, d_dG_, s);
+    segment_sum(vid, b_ * F_, F_, d_, ldx_, d_dX_, d_G_, d_fm_s_, tower_.gz, emb_scale, d_dG_, s);
     phase("segment_sum");
   }
 
