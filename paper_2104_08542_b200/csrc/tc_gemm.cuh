@@ -155,12 +155,16 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-template <int BN>
+// MAXST caps the ring depth: a short-K GEMM needs few stages, and a smaller
+// footprint lets several CTAs share an SM to overlap each other's latencies.
+template <int BN, int MAXST = 6>
 struct Layout {
   static constexpr int B_BYTES = BN * BKE * 4;  // K-major B tile, 128 B per row
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
-  static constexpr int STAGES = STAGES_RAW > 6 ? 6 : (STAGES_RAW < 2 ? 2 : STAGES_RAW);
+  static constexpr int STAGES_FIT = STAGES_RAW > 6 ? 6 : (STAGES_RAW < 2 ? 2 : STAGES_RAW);
+  static constexpr int STAGES = STAGES_FIT < MAXST ? STAGES_FIT : MAXST;
+  static_assert(STAGES * STAGE_BYTES >= BM * (BN + 1) * 4, "epilogue tile must fit the ring");
   static constexpr int TMEM_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
   // dynamic smem: 1 KB alignment slack + stages + barriers
   static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 256;
@@ -169,13 +173,13 @@ struct Layout {
 // A_MN: A is MN-major (4 TMA boxes of 32 m x 32 k); otherwise K-major (box 32 k x 128 m).
 // SPLIT_A: A arrives as raw fp32 and is split in smem; otherwise tmAlo supplies the lo part.
 // B_MN: B is MN-major (BN/32 TMA boxes of 32 n x 32 k, BASE32B layout); otherwise K-major.
-template <int BN, bool A_MN, bool SPLIT_A, int EPI, bool B_MN = false>
+template <int BN, bool A_MN, bool SPLIT_A, int EPI, bool B_MN = false, int MAXST = 6>
 __global__ void __launch_bounds__(192, 1)
     gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmAlo,
                        const __grid_constant__ CUtensorMap tmBhi,
                        const __grid_constant__ CUtensorMap tmBlo, const Params p) {
-  using L = Layout<BN>;
+  using L = Layout<BN, MAXST>;
   constexpr int ST = L::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &

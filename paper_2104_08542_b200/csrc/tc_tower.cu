@@ -136,11 +136,11 @@ __global__ void head_tc_kernel(int rows, int H, int d, int sq_parts, const float
 
 int round_up(int a, int b) { return (a + b - 1) / b * b; }
 
-template <int BN, bool A_MN, bool SPLIT_A, int EPI, bool B_MN = false>
+template <int BN, bool A_MN, bool SPLIT_A, int EPI, bool B_MN = false, int MAXST = 6>
 void launch_gemm(dim3 grid, const CUtensorMap& a, const CUtensorMap& alo, const CUtensorMap& bhi,
                  const CUtensorMap& blo, const tc::Params& p, cudaStream_t s) {
-  auto kern = tc::gemm_tf32x3_kernel<BN, A_MN, SPLIT_A, EPI, B_MN>;
-  constexpr int smem = tc::Layout<BN>::SMEM;
+  auto kern = tc::gemm_tf32x3_kernel<BN, A_MN, SPLIT_A, EPI, B_MN, MAXST>;
+  constexpr int smem = tc::Layout<BN, MAXST>::SMEM;
   static bool configured = false;  // per instantiation
   if (!configured) {
     CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -247,8 +247,8 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc_, const float* X, int l
   {
     const CUtensorMap ah = tmap(tc_.dh_hi, H, rows, tc_.ldh, 32, 128);
     const CUtensorMap al = tmap(tc_.dh_lo, H, rows, tc_.ldh, 32, 128);
-    const CUtensorMap bh = tmap(tc_.w_hi, H, K, tc_.ldh, 32, 128);
-    const CUtensorMap bl = tmap(tc_.w_lo, H, K, tc_.ldh, 32, 128);
+    const CUtensorMap bh = tmap(tc_.w_hi, H, K, tc_.ldh, 32, 64);
+    const CUtensorMap bl = tmap(tc_.w_lo, H, K, tc_.ldh, 32, 64);
     tc::Params p{};
     p.M = rows;
     p.N = K;
@@ -263,7 +263,10 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc_, const float* X, int l
     p.ldx = ldx;
     p.d = d;
     p.scale = emb_scale;
-    launch_gemm<128, false, false, tc::kEpiDx>(dim3(mt, (K + 127) / 128, 1), ah, al, bh, bl, p, s);
+    // K = H is short (2 k-blocks at H = 64): a 2-stage, BN = 64 footprint (~97 KB)
+    // puts two CTAs on every SM so one's epilogue overlaps the other's loads
+    launch_gemm<64, false, false, tc::kEpiDx, false, 2>(dim3(mt, (K + 63) / 64, 1), ah, al, bh, bl,
+                                                       p, s);
   }
   // ---- GEMM3: dW1 partials = X^T dh (A = X MN-major, B = dh hi/lo MN-major)
   const int nkb3 = (rows + tc::BKE - 1) / tc::BKE;
