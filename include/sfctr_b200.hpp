@@ -1,0 +1,171 @@
+// sfctr_b200.hpp — header-only C++ façade over the C-ABI (sfctr_b200.h) that
+// keeps the reference's C++ vocabulary: it consumes and produces the
+// reference's own types (sfctr::RawBatch / DedupBatch / FeatureId,
+// include/sfctr/batch.hpp, types.hpp) and throws the reference's exception
+// classes (include/sfctr/error.hpp:28-56). Build with
+// -I/path/to/reference/proj/core/include and link libsfctr_b200.so.
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "sfctr/batch.hpp"
+#include "sfctr/error.hpp"
+#include "sfctr_b200.h"
+
+namespace sfctr {
+namespace b200 {
+
+class CudaError : public std::runtime_error {
+ public:
+  explicit CudaError(const std::string& m) : std::runtime_error(m) {}
+};
+
+// status code -> the reference's exception class (error.hpp:28-56)
+inline void check(int status) {
+  if (status == SFCTR_OK) return;
+  const std::string msg = sfctr_last_error();
+  switch (status) {
+    case SFCTR_ERR_CONFIG: throw ConfigError(msg);
+    case SFCTR_ERR_DATA: throw DataError(msg);
+    case SFCTR_ERR_LOGIC: throw LogicError(msg);
+    case SFCTR_ERR_RUN: throw RunError(sfctr_last_error_step(), msg);
+    default: throw CudaError(msg);
+  }
+}
+
+struct Config {  // SimConfig (config.hpp:42-71) + B200 keys
+  sfctr_config c;
+  Config() { sfctr_config_default(&c); }
+  Config& set(const std::string& key, const std::string& value) {  // apply_config_entry
+    check(sfctr_config_apply(&c, key.c_str(), value.c_str()));
+    return *this;
+  }
+  Config& load(const std::string& path) {  // load_config_file
+    check(sfctr_config_load(&c, path.c_str()));
+    return *this;
+  }
+  void validate() const { check(sfctr_config_validate(&c)); }
+};
+
+// SyntheticGenerator (generator.hpp:35-62) on the device
+class Generator {
+ public:
+  explicit Generator(const Config& cfg, int device = 0) : cfg_(cfg) {
+    check(sfctr_generator_create(&cfg_.c, device, &g_));
+  }
+  ~Generator() { sfctr_generator_destroy(g_); }
+  Generator(const Generator&) = delete;
+  Generator& operator=(const Generator&) = delete;
+
+  RawBatch generate(std::int64_t step) const {  // generator.cpp:82-108
+    RawBatch b;
+    b.rows = cfg_.c.num_workers * cfg_.c.batch_size_per_worker;
+    b.fields = cfg_.c.num_fields;
+    std::vector<std::uint64_t> f(static_cast<std::size_t>(b.rows) * b.fields);
+    b.labels.resize(b.rows);
+    check(sfctr_generator_generate(g_, step, 0, b.rows, f.data(), b.labels.data()));
+    b.features.reserve(f.size());
+    for (auto v : f) b.features.emplace_back(v);
+    return b;
+  }
+  std::uint64_t shard_start(int field) const { return sfctr_generator_shard_start(g_, field); }
+
+ private:
+  Config cfg_;
+  sfctr_generator* g_ = nullptr;
+};
+
+inline std::vector<double> initial_embedding(std::uint64_t seed, FeatureId f, int dim,
+                                             int device = 0) {  // generator.hpp:62
+  std::vector<double> out(dim);
+  check(sfctr_initial_embedding(seed, f.value, dim, device, out.data()));
+  return out;
+}
+
+// DedupBatch virtual_sparse_id(const RawBatch&, int) (vsi.hpp:29), on the device.
+// key_space defaults to max id + 1.
+inline DedupBatch virtual_sparse_id(const RawBatch& batch, int num_workers, int device = 0,
+                                    std::uint64_t key_space = 0) {
+  const std::size_t n = batch.features.size();
+  std::vector<std::uint64_t> ids(n);
+  std::uint64_t mx = 0;
+  for (std::size_t i = 0; i < n; ++i) {
+    ids[i] = batch.features[i].value;
+    mx = ids[i] > mx ? ids[i] : mx;
+  }
+  if (!key_space) key_space = mx + 1;
+  sfctr_vsi* v = nullptr;
+  check(sfctr_vsi_create(device, key_space, static_cast<std::int64_t>(n ? n : 1), &v));
+  std::vector<std::uint64_t> g(n ? n : 1), vid(n ? n : 1);
+  std::vector<std::int32_t> rr(2 * (num_workers > 0 ? num_workers : 1));
+  std::int64_t u = 0;
+  const int st = sfctr_virtual_sparse_id(v, ids.data(), batch.rows, batch.fields, num_workers,
+                                         g.data(), vid.data(), &u, rr.data());
+  sfctr_vsi_destroy(v);
+  check(st);
+  DedupBatch d;
+  d.rows = batch.rows;
+  d.fields = batch.fields;
+  d.labels = batch.labels;
+  d.global_ids.reserve(u);
+  for (std::int64_t k = 0; k < u; ++k) d.global_ids.emplace_back(g[k]);
+  d.virtual_ids.reserve(n);
+  for (std::size_t i = 0; i < n; ++i) d.virtual_ids.emplace_back(vid[i]);
+  for (int w = 0; w < num_workers; ++w) d.worker_row_ranges.push_back({rr[2 * w], rr[2 * w + 1]});
+  return d;
+}
+
+// HostStore + CacheBuffer per worker + worker ops: one BSP step per call.
+class Trainer {
+ public:
+  Trainer(const Config& cfg, int rank = 0, int world = 1, const std::uint8_t* nccl_id = nullptr,
+          int device = 0)
+      : cfg_(cfg) {
+    check(sfctr_trainer_create(&cfg_.c, rank, world, nccl_id, device, &t_));
+  }
+  ~Trainer() { sfctr_trainer_destroy(t_); }
+  Trainer(const Trainer&) = delete;
+  Trainer& operator=(const Trainer&) = delete;
+
+  // this process's rows of global batch `step`
+  double step(std::int64_t step, const RawBatch& rows) {
+    std::vector<std::uint64_t> f(rows.features.size());
+    for (std::size_t i = 0; i < f.size(); ++i) f[i] = rows.features[i].value;
+    double loss = 0;
+    check(sfctr_trainer_step(t_, step, f.data(), rows.labels.data(), nullptr, &loss));
+    return loss;
+  }
+  // HostStore::snapshot_sorted (host_store.hpp:85-86): feature -> (emb|m|v fp32, adam_steps)
+  std::map<std::uint64_t, std::pair<std::vector<float>, std::int64_t>> snapshot() {
+    std::int64_t n = 0;
+    check(sfctr_trainer_snapshot(t_, &n, nullptr, nullptr, nullptr));
+    const int d3 = 3 * cfg_.c.embedding_dim;
+    std::vector<std::uint64_t> f(n ? n : 1);
+    std::vector<float> rows(static_cast<std::size_t>(n ? n : 1) * d3);
+    std::vector<std::int64_t> st(n ? n : 1);
+    check(sfctr_trainer_snapshot(t_, &n, f.data(), rows.data(), st.data()));
+    std::map<std::uint64_t, std::pair<std::vector<float>, std::int64_t>> out;
+    for (std::int64_t i = 0; i < n; ++i)
+      out.emplace(f[i], std::make_pair(std::vector<float>(rows.begin() + i * d3,
+                                                          rows.begin() + (i + 1) * d3),
+                                       st[i]));
+    return out;
+  }
+  // TransferLedger (ledger.hpp:60-63): h2w, w2h, interworker, swap_events
+  std::vector<std::int64_t> ledger() {
+    std::vector<std::int64_t> out(4);
+    check(sfctr_trainer_ledger(t_, out.data()));
+    return out;
+  }
+  sfctr_trainer* handle() { return t_; }
+
+ private:
+  Config cfg_;
+  sfctr_trainer* t_ = nullptr;
+};
+
+}  // namespace b200
+}  // namespace sfctr

@@ -75,6 +75,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// TMA prefetch of a box into L2 (no smem, no barrier): lets the producer run
+// far ahead of the smem ring so DRAM latency overlaps the stages in flight.
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int x, int y) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y)
+               : "memory");
+}
+
 __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst,
                                             int x, int y) {
   asm volatile(
@@ -226,9 +235,23 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer
       constexpr uint32_t bytes = (SPLIT_A ? A_BYTES : 2 * A_BYTES) + 2 * L::B_BYTES;
+      constexpr int PD = 2 * ST;  // L2 prefetch distance (k-blocks) for the streamed A operand
+      auto prefetch_a = [&](int i) {
+        const int kc = (kb0 + i) * BKE;
+        if constexpr (A_MN) {
+#pragma unroll
+          for (int a = 0; a < 4; ++a) tma_prefetch_2d(&tmA, m0 + a * 32, kc);
+        } else {
+          tma_prefetch_2d(&tmA, kc, m0);
+        }
+      };
+      if constexpr (SPLIT_A)
+        for (int i = 0; i < PD && i < nkb; ++i) prefetch_a(i);
       for (int i = 0; i < nkb; ++i) {
         const int s = i % ST;
         const uint32_t ph = (i / ST) & 1;
+        if constexpr (SPLIT_A)
+          if (i + PD < nkb) prefetch_a(i + PD);
         mbar_wait(empty + s, ph ^ 1);
         mbar_expect_tx(full + s, bytes);
         const int kc = (kb0 + i) * BKE;

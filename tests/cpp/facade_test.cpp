@@ -1,0 +1,60 @@
+// Drop-in check of include/sfctr_b200.hpp: the reference's own C++ types go in,
+// and the device path must agree with the reference's own functions
+// (sfctr::SyntheticGenerator::generate, sfctr::virtual_sparse_id from the
+// reference TUs in oracle/_ref/libsfctr_ref.so). Exit 0 = identical.
+#include <cstdio>
+
+#include "sfctr/generator.hpp"
+#include "sfctr/vsi.hpp"
+#include "sfctr_b200.hpp"
+
+int main() {
+  sfctr::SimConfig rc;  // the reference's config type
+  rc.num_workers = 2;
+  rc.batch_size_per_worker = 512;
+  rc.num_fields = 26;
+  rc.vocabulary_size = 1000000;
+  rc.zipf_exponent = 1.2;
+  sfctr::b200::Config bc;
+  bc.set("workers", "2").set("batch_size", "512").set("fields", "26").set("vocab", "1000000");
+  bc.set("zipf", "1.2");
+  sfctr::SyntheticGenerator ref_gen(rc);
+  sfctr::b200::Generator dev_gen(bc);
+  for (int step = 0; step < 3; ++step) {
+    const sfctr::RawBatch a = ref_gen.generate(step);
+    const sfctr::RawBatch b = dev_gen.generate(step);
+    if (a.features != b.features || a.labels != b.labels) {
+      std::printf("generator mismatch at step %d\n", step);
+      return 1;
+    }
+    const sfctr::DedupBatch da = sfctr::virtual_sparse_id(a, 2);
+    const sfctr::DedupBatch db = sfctr::b200::virtual_sparse_id(b, 2, 0, rc.vocabulary_size);
+    if (da.global_ids != db.global_ids || da.virtual_ids != db.virtual_ids ||
+        da.labels != db.labels || da.worker_row_ranges.size() != db.worker_row_ranges.size()) {
+      std::printf("vsi mismatch at step %d\n", step);
+      return 1;
+    }
+  }
+  // the reference exception classes come through the façade
+  try {
+    sfctr::RawBatch bad;
+    bad.rows = 3;
+    bad.fields = 1;
+    bad.features = {sfctr::FeatureId{1}, sfctr::FeatureId{2}, sfctr::FeatureId{3}};
+    bad.labels = {0, 0, 0};
+    sfctr::b200::virtual_sparse_id(bad, 2);
+    std::printf("expected LogicError\n");
+    return 1;
+  } catch (const sfctr::LogicError&) {
+  }
+  try {
+    sfctr::b200::Config c;
+    c.set("workers", "0").validate();
+    return 1;
+  } catch (const sfctr::ConfigError&) {
+  }
+  sfctr::b200::Trainer tr(bc);
+  const double loss = tr.step(0, dev_gen.generate(0));
+  std::printf("facade ok: loss %.6f\n", loss);
+  return 0;
+}
