@@ -22,10 +22,14 @@ namespace sfb {
 
 namespace {
 
-__global__ void owned_flag_kernel(const uint32_t* __restrict__ gids, int32_t U, uint32_t W,
+// Counts live on the device (U, n_own): grids cover the upper bound `cap`
+// and entries past the live count are flagged 0, so no host round trip is
+// needed to size the manage kernels.
+__global__ void owned_flag_kernel(const uint32_t* __restrict__ gids,
+                                  const int32_t* __restrict__ U_ptr, int32_t cap, uint32_t W,
                                   uint32_t w, uint32_t* __restrict__ flag) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < U) flag[i] = (gids[i] % W == w) ? 1u : 0u;
+  if (i < cap) flag[i] = (i < *U_ptr && gids[i] % W == w) ? 1u : 0u;
 }
 
 __global__ void compact_kernel(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ rank,
@@ -38,14 +42,19 @@ __global__ void compact_kernel(const uint32_t* __restrict__ flag, const uint32_t
 
 // Probe the owned features of batch t: hits are touched and marked needed_soon,
 // misses flagged for admission.
-__global__ void probe_kernel(const uint32_t* __restrict__ own_k, int32_t n_own,
+__global__ void probe_kernel(const uint32_t* __restrict__ own_k,
+                             const int32_t* __restrict__ n_own_ptr, int32_t cap,
                              const uint32_t* __restrict__ gids, uint32_t W,
                              const uint32_t* __restrict__ index, uint32_t C, int32_t t,
                              int32_t* __restrict__ last_use, int32_t* __restrict__ mark,
                              uint32_t* __restrict__ own_slot, uint32_t* __restrict__ miss,
                              int32_t* __restrict__ marked) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n_own) return;
+  if (j >= cap) return;
+  if (j >= *n_own_ptr) {
+    miss[j] = 0;
+    return;
+  }
   const uint32_t f = gids[own_k[j]];
   const uint32_t s = index[f / W];
   if (s < C) {
@@ -60,12 +69,13 @@ __global__ void probe_kernel(const uint32_t* __restrict__ own_k, int32_t n_own,
 }
 
 // needed_soon for resident owned features of a lookahead batch
-__global__ void mark_window_kernel(const uint32_t* __restrict__ gids, int32_t U, uint32_t W,
+__global__ void mark_window_kernel(const uint32_t* __restrict__ gids,
+                                   const int32_t* __restrict__ U_ptr, int32_t cap, uint32_t W,
                                    uint32_t w, const uint32_t* __restrict__ index, uint32_t C,
                                    int32_t t, int32_t* __restrict__ mark,
                                    int32_t* __restrict__ marked) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= U) return;
+  if (i >= cap || i >= *U_ptr) return;
   const uint32_t f = gids[i];
   if (f % W != w) return;
   const uint32_t s = index[f / W];
@@ -286,35 +296,34 @@ void CacheLane::release() {
   *this = CacheLane();
 }
 
-void CacheLane::select_owned(const uint32_t* d_gids, int32_t U, uint32_t W, uint32_t w,
-                             cudaStream_t s) {
-  if (U <= 0) return;
-  owned_flag_kernel<<<ceil_div(U, 256), 256, 0, s>>>(d_gids, U, W, w, flag);
+void CacheLane::select_owned(const uint32_t* d_gids, const int32_t* d_U, int32_t cap, uint32_t W,
+                             uint32_t w, cudaStream_t s) {
+  if (cap <= 0) return;
+  owned_flag_kernel<<<ceil_div(cap, 256), 256, 0, s>>>(d_gids, d_U, cap, W, w, flag);
   CUDA_LAUNCH_CHECK();
-  exclusive_scan_u32(temp, scan_bytes, flag, rank, U, s);
-  compact_kernel<<<ceil_div(U, 256), 256, 0, s>>>(flag, rank, U, own_k, counters + kCntOwned);
-  CUDA_LAUNCH_CHECK();
-}
-
-void CacheLane::mark_window(const uint32_t* d_gids, int32_t U, uint32_t W, uint32_t w, int32_t t,
-                            cudaStream_t s) {
-  if (U <= 0) return;
-  mark_window_kernel<<<ceil_div(U, 256), 256, 0, s>>>(d_gids, U, W, w, index,
-                                                      static_cast<uint32_t>(C), t, mark,
-                                                      counters + kCntMarked);
+  exclusive_scan_u32(temp, scan_bytes, flag, rank, cap, s);
+  compact_kernel<<<ceil_div(cap, 256), 256, 0, s>>>(flag, rank, cap, own_k, counters + kCntOwned);
   CUDA_LAUNCH_CHECK();
 }
 
-void CacheLane::probe(const uint32_t* d_gids, int32_t n_own, uint32_t W, int32_t t,
-                      cudaStream_t s) {
-  if (n_own <= 0) return;
-  probe_kernel<<<ceil_div(n_own, 256), 256, 0, s>>>(own_k, n_own, d_gids, W, index,
-                                                    static_cast<uint32_t>(C), t, last_use, mark,
-                                                    own_slot, miss, counters + kCntMarked);
+void CacheLane::mark_window(const uint32_t* d_gids, const int32_t* d_U, int32_t cap, uint32_t W,
+                            uint32_t w, int32_t t, cudaStream_t s) {
+  if (cap <= 0) return;
+  mark_window_kernel<<<ceil_div(cap, 256), 256, 0, s>>>(d_gids, d_U, cap, W, w, index,
+                                                        static_cast<uint32_t>(C), t, mark,
+                                                        counters + kCntMarked);
   CUDA_LAUNCH_CHECK();
-  exclusive_scan_u32(temp, scan_bytes, miss, miss_rank, n_own, s);
-  compact_kernel<<<ceil_div(n_own, 256), 256, 0, s>>>(miss, miss_rank, n_own, work_j,
-                                                      counters + kCntWorking);
+}
+
+void CacheLane::probe(const uint32_t* d_gids, int32_t cap, uint32_t W, int32_t t, cudaStream_t s) {
+  if (cap <= 0) return;
+  probe_kernel<<<ceil_div(cap, 256), 256, 0, s>>>(own_k, counters + kCntOwned, cap, d_gids, W,
+                                                  index, static_cast<uint32_t>(C), t, last_use,
+                                                  mark, own_slot, miss, counters + kCntMarked);
+  CUDA_LAUNCH_CHECK();
+  exclusive_scan_u32(temp, scan_bytes, miss, miss_rank, cap, s);
+  compact_kernel<<<ceil_div(cap, 256), 256, 0, s>>>(miss, miss_rank, cap, work_j,
+                                                    counters + kCntWorking);
   CUDA_LAUNCH_CHECK();
 }
 

@@ -45,10 +45,12 @@ struct CacheLane {
             int64_t max_unique);
   void release();
 
-  void select_owned(const uint32_t* d_gids, int32_t U, uint32_t W, uint32_t w, cudaStream_t s);
-  void mark_window(const uint32_t* d_gids, int32_t U, uint32_t W, uint32_t w, int32_t t,
-                   cudaStream_t s);
-  void probe(const uint32_t* d_gids, int32_t n_own, uint32_t W, int32_t t, cudaStream_t s);
+  // U / n_own are device counts; `cap` bounds the grids (the global batch size)
+  void select_owned(const uint32_t* d_gids, const int32_t* d_U, int32_t cap, uint32_t W,
+                    uint32_t w, cudaStream_t s);
+  void mark_window(const uint32_t* d_gids, const int32_t* d_U, int32_t cap, uint32_t W, uint32_t w,
+                   int32_t t, cudaStream_t s);
+  void probe(const uint32_t* d_gids, int32_t cap, uint32_t W, int32_t t, cudaStream_t s);
   void evict(int32_t n_evict, uint32_t W, int32_t t, cudaStream_t s);
   void admit(int32_t n_work, const uint32_t* d_gids, uint32_t W, uint64_t seed, int32_t t,
              cudaStream_t s);

@@ -269,23 +269,18 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   phase("ids_allgather");
   vsi_device(vsi_, gids, n_global_, d_uniq_, d_vid_, d_scalars_ + 0, s);
   phase("vsi");
-  // window batches (needed_soon), one at a time through the window scratch
-  const int nwin = cfg_.lookahead_depth - 1;
-  std::vector<int32_t> wU(nwin, 0);
-  CUDA_CHECK(cudaMemcpyAsync(h_scalars_, d_scalars_, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost, s));
-  CUDA_CHECK(cudaStreamSynchronize(s));
-  const int32_t U = h_scalars_[0];
-  if (h_scalars_[1]) fail(kLogic, "feature id >= vocabulary size in the batch", step);
-  stats_.unique = U;
-
-  // ---- Host-Manager: MixCache per lane (Algorithm 1 l.4-7)
-  CUDA_CHECK(cudaMemsetAsync(d_scalars_ + 2, 0, sizeof(int32_t) * 6, s));
+  // ---- Host-Manager: MixCache per lane (Algorithm 1 l.4-7). The unique and
+  // owned counts stay on the device (grids cover the batch-size bound), so the
+  // step waits on the host only once, after the probe.
+  const int32_t cap = static_cast<int32_t>(lane_[0].umax);
   for (int l = 0; l < lanes_; ++l) {
     // per-step counters; kCntFromHost (index 2) stays cumulative
     CUDA_CHECK(cudaMemsetAsync(lane_[l].counters, 0, sizeof(int32_t) * 2, s));
     CUDA_CHECK(cudaMemsetAsync(lane_[l].counters + 3, 0, sizeof(int32_t) * 5, s));
-    lane_[l].select_owned(d_uniq_, U, Wu, static_cast<uint32_t>(lane0_ + l), s);
+    lane_[l].select_owned(d_uniq_, d_scalars_ + 0, cap, Wu, static_cast<uint32_t>(lane0_ + l), s);
   }
+  // window batches t+1..t+L-1 (needed_soon), one at a time through the window scratch
+  const int nwin = cfg_.lookahead_depth - 1;
   for (int j = 0; j < nwin; ++j) {
     const uint64_t* wfeat = d_window + static_cast<size_t>(j) * n_local_;
     ids_to_u32(wfeat, d_ids32_, n_local_, cfg_.vocabulary_size, d_scalars_ + 1, s);
@@ -295,27 +290,22 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
       wg = d_gids_;
     }
     vsi_device(vsi_, wg, n_global_, d_wuniq_, d_wvid_, d_scalars_ + 2, s);
-    CUDA_CHECK(cudaMemcpyAsync(h_scalars_ + 2, d_scalars_ + 2, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    CUDA_CHECK(cudaStreamSynchronize(s));
-    wU[j] = h_scalars_[2];
     for (int l = 0; l < lanes_; ++l)
-      lane_[l].mark_window(d_wuniq_, wU[j], Wu, static_cast<uint32_t>(lane0_ + l), t, s);
+      lane_[l].mark_window(d_wuniq_, d_scalars_ + 2, cap, Wu, static_cast<uint32_t>(lane0_ + l), t,
+                           s);
   }
-  // owned counts (needed to size the probe)
-  for (int l = 0; l < lanes_; ++l)
-    CUDA_CHECK(cudaMemcpyAsync(h_counts_ + 8 * l, lane_[l].counters, sizeof(int32_t) * 8,
-                               cudaMemcpyDeviceToHost, s));
-  CUDA_CHECK(cudaStreamSynchronize(s));
-  std::vector<int32_t> n_own(lanes_), n_work(lanes_);
-  for (int l = 0; l < lanes_; ++l) {
-    n_own[l] = h_counts_[8 * l + kCntOwned];
-    lane_[l].probe(d_uniq_, n_own[l], Wu, t, s);
-  }
+  for (int l = 0; l < lanes_; ++l) lane_[l].probe(d_uniq_, cap, Wu, t, s);
   phase("manage_probe");
+  CUDA_CHECK(cudaMemcpyAsync(h_scalars_, d_scalars_, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost, s));
   for (int l = 0; l < lanes_; ++l)
     CUDA_CHECK(cudaMemcpyAsync(h_counts_ + 8 * l, lane_[l].counters, sizeof(int32_t) * 8,
                                cudaMemcpyDeviceToHost, s));
   CUDA_CHECK(cudaStreamSynchronize(s));
+  const int32_t U = h_scalars_[0];
+  if (h_scalars_[1]) fail(kLogic, "feature id >= vocabulary size in the batch", step);
+  stats_.unique = U;
+  std::vector<int32_t> n_own(lanes_), n_work(lanes_);
+  for (int l = 0; l < lanes_; ++l) n_own[l] = h_counts_[8 * l + kCntOwned];
   // capacity check before any state moves (push_parameters_to_cache deadlock)
   for (int l = 0; l < lanes_; ++l) {
     n_work[l] = n_own[l] > 0 ? h_counts_[8 * l + kCntWorking] : 0;
