@@ -182,7 +182,7 @@ __global__ void sparse_adam_kernel(const uint32_t* __restrict__ own_k,
   const int c = static_cast<int>(i - j * d);
   const uint32_t s = own_slot[j];
   const int t = steps[s] + 1;
-  const float g = dG[static_cast<int64_t>(own_k[j]) * d + c];
+  const float g = dG[static_cast<int64_t>(own_k ? own_k[j] : j) * d + c];
   const int64_t o = static_cast<int64_t>(s) * d + c;
   const float m = b1 * mom[o] + omb1 * g;
   const float v = b2 * vel[o] + omb2 * g * g;
@@ -206,7 +206,7 @@ __global__ void sparse_adam_v4(const uint32_t* __restrict__ own_k,
   const uint32_t s = __ldg(own_slot + j);
   const int t = __ldg(steps + s) + 1;
   const float c1 = __ldg(bc1 + t), c2 = __ldg(bc2 + t);
-  const float4 g = __ldg(dG + static_cast<int64_t>(__ldg(own_k + j)) * d4 + c);
+  const float4 g = __ldg(dG + static_cast<int64_t>(own_k ? __ldg(own_k + j) : j) * d4 + c);
   const int64_t o = static_cast<int64_t>(s) * d4 + c;
   float4 m = mom[o], v = vel[o], e = emb[o];
 #define SFB_ADAM(X)                                   \
@@ -293,7 +293,8 @@ void segment_sum(const uint32_t* vid, int32_t n, int F, int d, int ldx, const fl
   CUDA_LAUNCH_CHECK();
 }
 
-void sparse_adam(const uint32_t* own_k, const uint32_t* own_slot, int32_t n_own, const float* dG,
+void sparse_adam(const uint32_t* own_k /* gradient row index, or null = j */,
+                 const uint32_t* own_slot, int32_t n_own, const float* dG,
                  int d, float* emb, float* mom, float* vel, int32_t* steps, const float* bc1,
                  const float* bc2, float lr, double beta1, double beta2, float eps, cudaStream_t s) {
   if (n_own <= 0) return;

@@ -1,0 +1,281 @@
+// Owner-routed embedding exchange (sync = alltoall; SURVEY §8f rank 2,
+// PAPER.md:535 "All2All"): instead of all-reducing the zero-padded U x d
+// common embedding and common gradients, every rank moves
+// only the rows its own minibatch touches, straight from / to the row's owner.
+//
+// All ranks run the same VSI, so every rank can derive, without any request
+// round, the touched mask tm[k] (bit w <=> worker w's rows contain unique k):
+//   receive plan (me)  : R_o = [k : owner(k) = o, bit me]      -> local row lpos[k]
+//   send plan (me = o) : S_w = [k owned by me : bit w]        -> send slot spos[j][w]
+// Forward: owner packs S_w rows, grouped ncclSend/ncclRecv, rows land in the
+// local table E (owner-major blocks). Backward: the local gradient table dE is
+// sent back block by block; the owner sums the contributions of workers
+// 0..W-1 in that fixed order (the reference's ordered sum).
+#include <cub/device/device_scan.cuh>
+
+#include "exchange.h"
+
+namespace sfb {
+
+namespace {
+
+struct Cnt8Sum {
+  __host__ __device__ Cnt8 operator()(const Cnt8& a, const Cnt8& b) const {
+    Cnt8 r;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r.c[i] = a.c[i] + b.c[i];
+    return r;
+  }
+};
+
+// tm[vid[i]] |= 1 << worker(i); warp peers with the same vid pre-combine
+__global__ void touch_mask_kernel(const uint32_t* __restrict__ vid, int64_t n, int64_t per_worker,
+                                  uint32_t* __restrict__ tm) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const bool valid = i < n;
+  const uint32_t v = valid ? vid[i] : 0xFFFFFFFFu;
+  const unsigned active = __ballot_sync(0xFFFFFFFFu, valid);
+  if (!valid) return;
+  const uint32_t bit = 1u << static_cast<uint32_t>(i / per_worker);
+  const unsigned peers = __match_any_sync(active, v);
+  const uint32_t bits = __reduce_or_sync(peers, bit);
+  if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicOr(tm + v, bits);
+}
+
+// receive plan input: one-hot(owner) for uniques touched by `me`
+__global__ void recv_onehot_kernel(const uint32_t* __restrict__ uniq, const int32_t* __restrict__ U,
+                                   int32_t cap, const uint32_t* __restrict__ tm, uint32_t W,
+                                   uint32_t me, Cnt8* __restrict__ out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= cap) return;
+  Cnt8 c{};
+  if (k < *U && ((tm[k] >> me) & 1u)) c.c[uniq[k] % W] = 1;
+  out[k] = c;
+}
+
+// send plan input: for owned j, bit w of the touched mask for every w
+__global__ void send_onehot_kernel(const uint32_t* __restrict__ own_k,
+                                   const int32_t* __restrict__ n_own, int32_t cap,
+                                   const uint32_t* __restrict__ tm, uint32_t W,
+                                   Cnt8* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= cap) return;
+  Cnt8 c{};
+  if (j < *n_own) {
+    const uint32_t m = tm[own_k[j]];
+#pragma unroll
+    for (uint32_t w = 0; w < 8; ++w) c.c[w] = (w < W) ? ((m >> w) & 1u) : 0u;
+  }
+  out[j] = c;
+}
+
+// totals[0..8) = receive counts per owner, totals[8..16) = send counts per destination
+__global__ void plan_totals_kernel(const Cnt8* __restrict__ rscan, const Cnt8* __restrict__ rin,
+                                   const Cnt8* __restrict__ sscan, const Cnt8* __restrict__ sin,
+                                   int32_t cap, int32_t* __restrict__ totals) {
+  const int i = threadIdx.x;
+  if (i < 8) totals[i] = static_cast<int32_t>(rscan[cap - 1].c[i] + rin[cap - 1].c[i]);
+  else if (i < 16) totals[i] = static_cast<int32_t>(sscan[cap - 1].c[i - 8] + sin[cap - 1].c[i - 8]);
+}
+
+// lpos[k] = roff[owner] + rank of k among the uniques of that owner I touch
+__global__ void lpos_kernel(const uint32_t* __restrict__ uniq, const int32_t* __restrict__ U,
+                            int32_t cap, const uint32_t* __restrict__ tm, uint32_t W, uint32_t me,
+                            const Cnt8* __restrict__ rscan, const int32_t* __restrict__ totals,
+                            uint32_t* __restrict__ lpos) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= cap) return;
+  if (k >= *U || !((tm[k] >> me) & 1u)) {
+    lpos[k] = 0xFFFFFFFFu;
+    return;
+  }
+  const uint32_t o = uniq[k] % W;
+  uint32_t off = 0;
+  for (uint32_t q = 0; q < o; ++q) off += static_cast<uint32_t>(totals[q]);
+  lpos[k] = off + rscan[k].c[o];
+}
+
+__global__ void lvid_kernel(const uint32_t* __restrict__ vid, int64_t n,
+                            const uint32_t* __restrict__ lpos, uint32_t* __restrict__ lvid) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) lvid[i] = lpos[vid[i]];
+}
+
+// Forward pack: owned row j goes to sendbuf[soff[w] + spos[j][w]] for every
+// remote worker w that touches it, and to E[lpos] when I touch it myself.
+// One warp per owned row, 16 B lanes.
+__global__ void pack_rows_kernel(const uint32_t* __restrict__ own_k,
+                                 const uint32_t* __restrict__ own_slot, int32_t n_own,
+                                 const uint32_t* __restrict__ tm, const Cnt8* __restrict__ sscan,
+                                 const int32_t* __restrict__ totals, uint32_t W, uint32_t me,
+                                 const uint32_t* __restrict__ lpos, const float4* __restrict__ emb,
+                                 int d4, float4* __restrict__ sendbuf, float4* __restrict__ E) {
+  const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= n_own) return;
+  const uint32_t k = own_k[j];
+  const uint32_t m = tm[k];
+  const float4* src = emb + static_cast<int64_t>(own_slot[j]) * d4;
+  uint32_t soff = 0;
+  for (uint32_t w = 0; w < W; ++w) {
+    if ((m >> w) & 1u) {
+      float4* dst = (w == me) ? E + static_cast<int64_t>(lpos[k]) * d4
+                              : sendbuf + static_cast<int64_t>(soff + sscan[j].c[w]) * d4;
+      for (int c = lane; c < d4; c += 32) dst[c] = src[c];
+    }
+    if (w != me) soff += static_cast<uint32_t>(totals[8 + w]);
+  }
+}
+
+// Backward: g[j] = sum over w = 0..W-1 (fixed order) of worker w's partial
+// gradient of owned row j (mine from dE, the others from recvbuf).
+__global__ void owner_reduce_kernel(const uint32_t* __restrict__ own_k, int32_t n_own,
+                                    const uint32_t* __restrict__ tm, const Cnt8* __restrict__ sscan,
+                                    const int32_t* __restrict__ totals, uint32_t W, uint32_t me,
+                                    const uint32_t* __restrict__ lpos, const float4* __restrict__ dE,
+                                    const float4* __restrict__ recvbuf, int d4,
+                                    float4* __restrict__ g) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<int64_t>(n_own) * d4) return;
+  const int64_t j = i / d4;
+  const int c = static_cast<int>(i - j * d4);
+  const uint32_t k = own_k[j];
+  const uint32_t m = tm[k];
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  uint32_t soff = 0;
+  for (uint32_t w = 0; w < W; ++w) {
+    if ((m >> w) & 1u) {
+      const float4 v = (w == me) ? dE[static_cast<int64_t>(lpos[k]) * d4 + c]
+                                 : recvbuf[static_cast<int64_t>(soff + sscan[j].c[w]) * d4 + c];
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    if (w != me) soff += static_cast<uint32_t>(totals[8 + w]);
+  }
+  g[i] = acc;
+}
+
+}  // namespace
+
+void Exchange::init(int W_, int me_, int64_t cap_, int d_) {
+  release();
+  W = W_;
+  me = me_;
+  cap = cap_;
+  d = d_;
+  SFB_CHECK(W <= 8, "alltoall sync supports at most 8 workers");
+  SFB_CHECK((d & 3) == 0, "alltoall sync needs embedding_dim % 4 == 0");
+  CUDA_CHECK(cudaMalloc(&tm, sizeof(uint32_t) * cap));
+  CUDA_CHECK(cudaMalloc(&lpos, sizeof(uint32_t) * cap));
+  CUDA_CHECK(cudaMalloc(&rin, sizeof(Cnt8) * cap));
+  CUDA_CHECK(cudaMalloc(&rscan, sizeof(Cnt8) * cap));
+  CUDA_CHECK(cudaMalloc(&sin, sizeof(Cnt8) * cap));
+  CUDA_CHECK(cudaMalloc(&sscan, sizeof(Cnt8) * cap));
+  CUDA_CHECK(cudaMalloc(&totals, sizeof(int32_t) * 16));
+  CUDA_CHECK(cudaMalloc(&buf, sizeof(float) * cap * d));
+  CUDA_CHECK(cudaMalloc(&gown, sizeof(float) * cap * d));
+  CUDA_CHECK(cub::DeviceScan::ExclusiveScan(nullptr, scan_bytes, rin, rscan, Cnt8Sum{}, Cnt8{},
+                                            static_cast<int>(cap)));
+  CUDA_CHECK(cudaMalloc(&temp, scan_bytes));
+}
+
+void Exchange::release() {
+  for (void* p : {static_cast<void*>(tm), static_cast<void*>(lpos), static_cast<void*>(rin),
+                  static_cast<void*>(rscan), static_cast<void*>(sin), static_cast<void*>(sscan),
+                  static_cast<void*>(totals), static_cast<void*>(buf), static_cast<void*>(gown),
+                  temp})
+    if (p) cudaFree(p);
+  *this = Exchange();
+}
+
+void Exchange::plan(const uint32_t* d_vid, int64_t n_global, int64_t per_worker,
+                    const uint32_t* d_uniq, const int32_t* d_U, const uint32_t* d_own_k,
+                    const int32_t* d_n_own, cudaStream_t s) {
+  const int c = static_cast<int>(cap);
+  CUDA_CHECK(cudaMemsetAsync(tm, 0, sizeof(uint32_t) * cap, s));
+  touch_mask_kernel<<<ceil_div(n_global, 256), 256, 0, s>>>(d_vid, n_global, per_worker, tm);
+  CUDA_LAUNCH_CHECK();
+  recv_onehot_kernel<<<ceil_div(c, 256), 256, 0, s>>>(d_uniq, d_U, c, tm, W, me, rin);
+  CUDA_LAUNCH_CHECK();
+  CUDA_CHECK(cub::DeviceScan::ExclusiveScan(temp, scan_bytes, rin, rscan, Cnt8Sum{}, Cnt8{}, c, s));
+  g_launches += 2;
+  send_onehot_kernel<<<ceil_div(c, 256), 256, 0, s>>>(d_own_k, d_n_own, c, tm, W, sin);
+  CUDA_LAUNCH_CHECK();
+  CUDA_CHECK(cub::DeviceScan::ExclusiveScan(temp, scan_bytes, sin, sscan, Cnt8Sum{}, Cnt8{}, c, s));
+  g_launches += 2;
+  plan_totals_kernel<<<1, 32, 0, s>>>(rscan, rin, sscan, sin, c, totals);
+  CUDA_LAUNCH_CHECK();
+  lpos_kernel<<<ceil_div(c, 256), 256, 0, s>>>(d_uniq, d_U, c, tm, W, me, rscan, totals, lpos);
+  CUDA_LAUNCH_CHECK();
+}
+
+void Exchange::local_vids(const uint32_t* d_vid_mine, int64_t n, uint32_t* d_lvid, cudaStream_t s) {
+  lvid_kernel<<<ceil_div(n, 256), 256, 0, s>>>(d_vid_mine, n, lpos, d_lvid);
+  CUDA_LAUNCH_CHECK();
+}
+
+void Exchange::set_counts(const int32_t* h_totals) {
+  recv_rows.assign(h_totals, h_totals + 8);
+  send_rows.assign(h_totals + 8, h_totals + 16);
+  recv_off.assign(9, 0);
+  for (int o = 0; o < 8; ++o) recv_off[o + 1] = recv_off[o] + recv_rows[o];
+  send_off.assign(9, 0);
+  for (int w = 0; w < 8; ++w) send_off[w + 1] = send_off[w] + (w == me ? 0 : send_rows[w]);
+}
+
+int64_t Exchange::forward(const uint32_t* d_own_k, const uint32_t* d_own_slot, int32_t n_own,
+                          const float* emb, float* E, ncclComm_t comm, cudaStream_t s) {
+  const int d4 = d / 4;
+  if (n_own > 0) {
+    pack_rows_kernel<<<ceil_div(static_cast<int64_t>(n_own) * 32, 256), 256, 0, s>>>(
+        d_own_k, d_own_slot, n_own, tm, sscan, totals, W, me, lpos,
+        reinterpret_cast<const float4*>(emb), d4, reinterpret_cast<float4*>(buf),
+        reinterpret_cast<float4*>(E));
+    CUDA_LAUNCH_CHECK();
+  }
+  int64_t bytes = 0;
+  NCCL_CHECK(ncclGroupStart());
+  for (int w = 0; w < W; ++w) {
+    if (w == me) continue;
+    if (send_rows[w] > 0) {
+      NCCL_CHECK(ncclSend(buf + static_cast<size_t>(send_off[w]) * d,
+                          static_cast<size_t>(send_rows[w]) * d, ncclFloat32, w, comm, s));
+      bytes += static_cast<int64_t>(send_rows[w]) * d * 4;
+    }
+    if (recv_rows[w] > 0)
+      NCCL_CHECK(ncclRecv(E + static_cast<size_t>(recv_off[w]) * d,
+                          static_cast<size_t>(recv_rows[w]) * d, ncclFloat32, w, comm, s));
+  }
+  NCCL_CHECK(ncclGroupEnd());
+  return bytes;
+}
+
+int64_t Exchange::backward(const uint32_t* d_own_k, int32_t n_own, const float* dE, ncclComm_t comm,
+                           cudaStream_t s) {
+  int64_t bytes = 0;
+  NCCL_CHECK(ncclGroupStart());
+  for (int w = 0; w < W; ++w) {
+    if (w == me) continue;
+    if (recv_rows[w] > 0) {  // my partial gradients of rows owned by w
+      NCCL_CHECK(ncclSend(dE + static_cast<size_t>(recv_off[w]) * d,
+                          static_cast<size_t>(recv_rows[w]) * d, ncclFloat32, w, comm, s));
+      bytes += static_cast<int64_t>(recv_rows[w]) * d * 4;
+    }
+    if (send_rows[w] > 0)  // worker w's partial gradients of rows I own
+      NCCL_CHECK(ncclRecv(buf + static_cast<size_t>(send_off[w]) * d,
+                          static_cast<size_t>(send_rows[w]) * d, ncclFloat32, w, comm, s));
+  }
+  NCCL_CHECK(ncclGroupEnd());
+  const int d4 = d / 4;
+  if (n_own > 0) {
+    owner_reduce_kernel<<<ceil_div(static_cast<int64_t>(n_own) * d4, 256), 256, 0, s>>>(
+        d_own_k, n_own, tm, sscan, totals, W, me, lpos, reinterpret_cast<const float4*>(dE),
+        reinterpret_cast<const float4*>(buf), d4, reinterpret_cast<float4*>(gown));
+    CUDA_LAUNCH_CHECK();
+  }
+  return bytes;
+}
+
+}  // namespace sfb

@@ -1,0 +1,55 @@
+// Owner-routed all-to-all exchange of embedding rows / gradients (exchange.cu).
+#pragma once
+
+#include <nccl.h>
+
+#include <string>
+#include <vector>
+
+#include "ops.h"
+
+namespace sfb {
+
+#ifndef NCCL_CHECK
+#define NCCL_CHECK(expr)                                                                  \
+  do {                                                                                    \
+    ncclResult_t r_ = (expr);                                                             \
+    if (r_ != ncclSuccess)                                                                \
+      ::sfb::fail(::sfb::kNccl, std::string(#expr) + ": " + ncclGetErrorString(r_));      \
+  } while (0)
+#endif
+
+struct Cnt8 {  // per-worker counters (at most 8 workers on one NVSwitch box)
+  uint32_t c[8];
+};
+
+struct Exchange {
+  int W = 0, me = 0, d = 0;
+  int64_t cap = 0;               // bound on uniques per step
+  uint32_t* tm = nullptr;        // [cap] touched-by-worker bitmask per unique
+  uint32_t* lpos = nullptr;      // [cap] row in the local table E (or ~0)
+  Cnt8 *rin = nullptr, *rscan = nullptr;  // receive plan (one-hot owner, scan)
+  Cnt8 *sin = nullptr, *sscan = nullptr;  // send plan (mask bits of owned rows, scan)
+  int32_t* totals = nullptr;     // [16] recv rows per owner | send rows per destination
+  float* buf = nullptr;          // [cap x d] forward send / backward receive rows
+  float* gown = nullptr;         // [cap x d] owner-summed gradients, owned order
+  void* temp = nullptr;
+  size_t scan_bytes = 0;
+  std::vector<int64_t> recv_rows, send_rows, recv_off, send_off;  // host copies
+
+  void init(int W, int me, int64_t cap, int d);
+  void release();
+  // device-only planning (no host wait); totals land in `totals`
+  void plan(const uint32_t* d_vid, int64_t n_global, int64_t per_worker, const uint32_t* d_uniq,
+            const int32_t* d_U, const uint32_t* d_own_k, const int32_t* d_n_own, cudaStream_t s);
+  void set_counts(const int32_t* h_totals);  // after the step's host wait
+  void local_vids(const uint32_t* d_vid_mine, int64_t n, uint32_t* d_lvid, cudaStream_t s);
+  int64_t local_rows() const { return recv_off.empty() ? 0 : recv_off[8]; }
+  // returns the bytes this rank sent
+  int64_t forward(const uint32_t* d_own_k, const uint32_t* d_own_slot, int32_t n_own,
+                  const float* emb, float* E, ncclComm_t comm, cudaStream_t s);
+  int64_t backward(const uint32_t* d_own_k, int32_t n_own, const float* dE, ncclComm_t comm,
+                   cudaStream_t s);
+};
+
+}  // namespace sfb

@@ -26,8 +26,9 @@ void segment_sum(const uint32_t* vid, int32_t n, int F, int d, int ldx, const fl
 // dX[r, k] += scale * gz[r] * (fm_s[r, k % d] - X[r, k]) (FM part, standalone model op)
 void fm_grad_add(const float* X, int32_t rows, int F, int d, int ldx, const float* fm_s,
                  const float* gz, float scale, float* dX, cudaStream_t s);
-// update_sparse: lazy Adam on the lane's owned rows, per-row step count
-void sparse_adam(const uint32_t* own_k, const uint32_t* own_slot, int32_t n_own, const float* dG,
+// update_sparse: lazy Adam on the lane's owned rows, per-row step count.
+// The gradient of owned row j is dG[grad_idx[j]] (grad_idx == nullptr: dG[j]).
+void sparse_adam(const uint32_t* grad_idx, const uint32_t* own_slot, int32_t n_own, const float* dG,
                  int d, float* emb, float* mom, float* vel, int32_t* steps, const float* bc1,
                  const float* bc2, float lr, double beta1, double beta2, float eps, cudaStream_t s);
 

@@ -156,6 +156,15 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
   const int64_t umax = std::min<int64_t>(n_global_, static_cast<int64_t>(cfg_.vocabulary_size));
   for (int l = 0; l < lanes_; ++l)
     lane_[l].init(cfg_.cache_capacity, d_, owned_rows, host_rows, umax);
+  if (world_ > 1 && cfg_.sync_mode == SFCTR_SYNC_ALLTOALL) {
+    if (lanes_ != 1) fail(kConfig, "sync=alltoall needs one worker per process");
+    if (W_ > 8) fail(kConfig, "sync=alltoall supports at most 8 workers (one NVSwitch box)");
+    if (d_ % 4) fail(kConfig, "sync=alltoall needs dim % 4 == 0");
+    a2a_ = true;
+    xch_.init(W_, rank_, umax, d_);
+    CUDA_CHECK(cudaMalloc(&d_lvid_, sizeof(uint32_t) * n_local_));
+    CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_totals_), sizeof(int32_t) * 16, 0));
+  }
   ensure_bias_tables(1024);
   CUDA_CHECK(cudaStreamSynchronize(stream_));
 }
@@ -166,6 +175,9 @@ Trainer::~Trainer() {
   for (auto& l : lane_) l.release();
   tower_.release();
   towertc_.release();
+  xch_.release();
+  if (d_lvid_) cudaFree(d_lvid_);
+  if (h_totals_) cudaFreeHost(h_totals_);
   vsi_.release();
   for (void* p : {static_cast<void*>(d_in_feat_), static_cast<void*>(d_in_lab_),
                   static_cast<void*>(d_in_win_), static_cast<void*>(d_ids32_),
@@ -295,6 +307,12 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
                            s);
   }
   for (int l = 0; l < lanes_; ++l) lane_[l].probe(d_uniq_, cap, Wu, t, s);
+  if (a2a_) {  // exchange plan (touched masks, send/receive positions), device only
+    xch_.plan(d_vid_, n_global_, static_cast<int64_t>(b_) * F_, d_uniq_, d_scalars_ + 0,
+              lane_[0].own_k, lane_[0].counters + kCntOwned, s);
+    CUDA_CHECK(cudaMemcpyAsync(h_totals_, xch_.totals, sizeof(int32_t) * 16,
+                               cudaMemcpyDeviceToHost, s));
+  }
   phase("manage_probe");
   CUDA_CHECK(cudaMemcpyAsync(h_scalars_, d_scalars_, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost, s));
   for (int l = 0; l < lanes_; ++l)
@@ -339,24 +357,38 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
 
   // ---- GPU-Worker forward (Algorithm 1 l.9-11)
   const size_t ud = static_cast<size_t>(U) * d_;
-  if (world_ > 1) CUDA_CHECK(cudaMemsetAsync(d_G_, 0, sizeof(float) * ud, s));
-  for (int l = 0; l < lanes_; ++l)
-    gather_cache(lane_[l].own_k, lane_[l].own_slot, n_own[l], lane_[l].emb, d_, d_G_, s);
-  phase("gather_cache");
-  if (world_ > 1) {
-    NCCL_CHECK(ncclAllReduce(d_G_, d_G_, ud, ncclFloat32, ncclSum, comm_, s));
-    stats_.nvlink_bytes += static_cast<int64_t>(ud) * 4;
+  // rows of the table the lanes gather from: all U uniques (all-reduce scheme) or
+  // only the ones this rank touches (owner-routed all-to-all)
+  size_t table_rows = static_cast<size_t>(U);
+  if (a2a_) {
+    xch_.set_counts(h_totals_);
+    stats_.nvlink_bytes +=
+        xch_.forward(lane_[0].own_k, lane_[0].own_slot, n_own[0], lane_[0].emb, d_G_, comm_, s);
+    table_rows = static_cast<size_t>(xch_.local_rows());
+    xch_.local_vids(d_vid_ + static_cast<size_t>(lane0_) * b_ * F_, n_local_, d_lvid_, s);
+    phase("exchange_embed");
+  } else {
+    if (world_ > 1) CUDA_CHECK(cudaMemsetAsync(d_G_, 0, sizeof(float) * ud, s));
+    for (int l = 0; l < lanes_; ++l)
+      gather_cache(lane_[l].own_k, lane_[l].own_slot, n_own[l], lane_[l].emb, d_, d_G_, s);
+    phase("gather_cache");
+    if (world_ > 1) {
+      NCCL_CHECK(ncclAllReduce(d_G_, d_G_, ud, ncclFloat32, ncclSum, comm_, s));
+      stats_.nvlink_bytes += static_cast<int64_t>(ud) * 4;
+    }
+    phase("allreduce_embed");
   }
-  // interworker ledger: allreduce_bytes per worker for each all-reduce
+  // interworker ledger: the reference's accounting model, allreduce_bytes per
+  // worker for each all-reduce, whatever the device scheme
   auto arb = [&](int64_t payload) { return 2 * static_cast<int64_t>(W_ - 1) * payload / W_; };
   led_[2] += static_cast<int64_t>(lanes_) * arb(static_cast<int64_t>(ud) * 4);
-  phase("allreduce_embed");
 
   // ---- per lane: gather_instances, forward_backward, segment_sum (l.11-12)
-  CUDA_CHECK(cudaMemsetAsync(d_dG_, 0, sizeof(float) * ud, s));
+  CUDA_CHECK(cudaMemsetAsync(d_dG_, 0, sizeof(float) * table_rows * d_, s));
   const float emb_scale = 1.f / static_cast<float>(W_);
   for (int l = 0; l < lanes_; ++l) {
-    const uint32_t* vid = d_vid_ + static_cast<size_t>(lane0_ + l) * b_ * F_;
+    const uint32_t* vid =
+        a2a_ ? d_lvid_ : d_vid_ + static_cast<size_t>(lane0_ + l) * b_ * F_;
     const uint8_t* lab = d_labels + static_cast<size_t>(l) * b_;
     gather_instances(vid, b_, F_, d_, ldx_, d_G_, d_X_, d_fm_s_, d_fm_sqp_, s);
     phase("gather_instances");
@@ -374,19 +406,27 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   }
 
   // ---- grad_synchronize (l.13)
-  if (world_ > 1) {
+  const float* grad_rows = d_dG_;
+  if (a2a_) {
+    stats_.nvlink_bytes += xch_.backward(lane_[0].own_k, n_own[0], d_dG_, comm_, s);
+    grad_rows = xch_.gown;
+  } else if (world_ > 1) {
     NCCL_CHECK(ncclAllReduce(d_dG_, d_dG_, ud, ncclFloat32, ncclSum, comm_, s));
+    stats_.nvlink_bytes += static_cast<int64_t>(ud) * 4;
+  }
+  if (world_ > 1) {
     NCCL_CHECK(ncclAllReduce(d_grads_, d_grads_, P_ + 1, ncclFloat32, ncclSum, comm_, s));
-    stats_.nvlink_bytes += static_cast<int64_t>(ud + P_ + 1) * 4;
+    stats_.nvlink_bytes += static_cast<int64_t>(P_ + 1) * 4;
   }
   led_[2] += static_cast<int64_t>(lanes_) *
              (arb(static_cast<int64_t>(ud) * 4) + arb(static_cast<int64_t>(P_) * 4));
-  phase("allreduce_grad");
+  phase(a2a_ ? "exchange_grad" : "allreduce_grad");
 
   // ---- update_sparse (l.14) + dense Adam
   ensure_bias_tables(steps_done_ + 2);
   for (int l = 0; l < lanes_; ++l)
-    sparse_adam(lane_[l].own_k, lane_[l].own_slot, n_own[l], d_dG_, d_, lane_[l].emb,
+    sparse_adam(a2a_ ? nullptr : lane_[l].own_k, lane_[l].own_slot, n_own[l], grad_rows, d_,
+                lane_[l].emb,
                 lane_[l].mom, lane_[l].vel, lane_[l].steps, d_bc1_, d_bc2_,
                 static_cast<float>(cfg_.learning_rate), static_cast<float>(cfg_.adam_beta1),
                 static_cast<float>(cfg_.adam_beta2), static_cast<float>(cfg_.adam_epsilon), s);

@@ -8,16 +8,10 @@
 
 #include "../../include/sfctr_b200.h"
 #include "cache.h"
+#include "exchange.h"
 #include "kernels.h"
 
 namespace sfb {
-
-#define NCCL_CHECK(expr)                                                                  \
-  do {                                                                                    \
-    ncclResult_t r_ = (expr);                                                             \
-    if (r_ != ncclSuccess)                                                                \
-      ::sfb::fail(::sfb::kNccl, std::string(#expr) + ": " + ncclGetErrorString(r_));      \
-  } while (0)
 
 void validate_config(const sfctr_config& c);
 
@@ -104,6 +98,10 @@ class Trainer {
   std::vector<CacheLane> lane_;
   TowerBufs tower_;
   TowerTC towertc_;
+  bool a2a_ = false;              // owner-routed all-to-all sync (world > 1)
+  Exchange xch_;
+  uint32_t* d_lvid_ = nullptr;    // [n_local] local-table rows of this process's positions
+  int32_t* h_totals_ = nullptr;   // pinned [16] exchange plan totals
   int ldx_ = 0;
   bool tower_simt_ = false;
   int64_t dense_steps_ = 0;
