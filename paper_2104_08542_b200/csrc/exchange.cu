@@ -11,22 +11,11 @@
 // local table E (owner-major blocks). Backward: the local gradient table dE is
 // sent back block by block; the owner sums the contributions of workers
 // 0..W-1 in that fixed order (the reference's ordered sum).
-#include <cub/device/device_scan.cuh>
-
 #include "exchange.h"
 
 namespace sfb {
 
 namespace {
-
-struct Cnt8Sum {
-  __host__ __device__ Cnt8 operator()(const Cnt8& a, const Cnt8& b) const {
-    Cnt8 r;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) r.c[i] = a.c[i] + b.c[i];
-    return r;
-  }
-};
 
 // tm[vid[i]] |= 1 << worker(i); warp peers with the same vid pre-combine
 __global__ void touch_mask_kernel(const uint32_t* __restrict__ vid, int64_t n, int64_t per_worker,
@@ -40,59 +29,6 @@ __global__ void touch_mask_kernel(const uint32_t* __restrict__ vid, int64_t n, i
   const unsigned peers = __match_any_sync(active, v);
   const uint32_t bits = __reduce_or_sync(peers, bit);
   if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicOr(tm + v, bits);
-}
-
-// receive plan input: one-hot(owner) for uniques touched by `me`
-__global__ void recv_onehot_kernel(const uint32_t* __restrict__ uniq, const int32_t* __restrict__ U,
-                                   int32_t cap, const uint32_t* __restrict__ tm, uint32_t W,
-                                   uint32_t me, Cnt8* __restrict__ out) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= cap) return;
-  Cnt8 c{};
-  if (k < *U && ((tm[k] >> me) & 1u)) c.c[uniq[k] % W] = 1;
-  out[k] = c;
-}
-
-// send plan input: for owned j, bit w of the touched mask for every w
-__global__ void send_onehot_kernel(const uint32_t* __restrict__ own_k,
-                                   const int32_t* __restrict__ n_own, int32_t cap,
-                                   const uint32_t* __restrict__ tm, uint32_t W,
-                                   Cnt8* __restrict__ out) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= cap) return;
-  Cnt8 c{};
-  if (j < *n_own) {
-    const uint32_t m = tm[own_k[j]];
-#pragma unroll
-    for (uint32_t w = 0; w < 8; ++w) c.c[w] = (w < W) ? ((m >> w) & 1u) : 0u;
-  }
-  out[j] = c;
-}
-
-// totals[0..8) = receive counts per owner, totals[8..16) = send counts per destination
-__global__ void plan_totals_kernel(const Cnt8* __restrict__ rscan, const Cnt8* __restrict__ rin,
-                                   const Cnt8* __restrict__ sscan, const Cnt8* __restrict__ sin,
-                                   int32_t cap, int32_t* __restrict__ totals) {
-  const int i = threadIdx.x;
-  if (i < 8) totals[i] = static_cast<int32_t>(rscan[cap - 1].c[i] + rin[cap - 1].c[i]);
-  else if (i < 16) totals[i] = static_cast<int32_t>(sscan[cap - 1].c[i - 8] + sin[cap - 1].c[i - 8]);
-}
-
-// lpos[k] = roff[owner] + rank of k among the uniques of that owner I touch
-__global__ void lpos_kernel(const uint32_t* __restrict__ uniq, const int32_t* __restrict__ U,
-                            int32_t cap, const uint32_t* __restrict__ tm, uint32_t W, uint32_t me,
-                            const Cnt8* __restrict__ rscan, const int32_t* __restrict__ totals,
-                            uint32_t* __restrict__ lpos) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= cap) return;
-  if (k >= *U || !((tm[k] >> me) & 1u)) {
-    lpos[k] = 0xFFFFFFFFu;
-    return;
-  }
-  const uint32_t o = uniq[k] % W;
-  uint32_t off = 0;
-  for (uint32_t q = 0; q < o; ++q) off += static_cast<uint32_t>(totals[q]);
-  lpos[k] = off + rscan[k].c[o];
 }
 
 __global__ void lvid_kernel(const uint32_t* __restrict__ vid, int64_t n,
@@ -169,45 +105,163 @@ void Exchange::init(int W_, int me_, int64_t cap_, int d_) {
   SFB_CHECK((d & 3) == 0, "alltoall sync needs embedding_dim % 4 == 0");
   CUDA_CHECK(cudaMalloc(&tm, sizeof(uint32_t) * cap));
   CUDA_CHECK(cudaMalloc(&lpos, sizeof(uint32_t) * cap));
-  CUDA_CHECK(cudaMalloc(&rin, sizeof(Cnt8) * cap));
-  CUDA_CHECK(cudaMalloc(&rscan, sizeof(Cnt8) * cap));
-  CUDA_CHECK(cudaMalloc(&sin, sizeof(Cnt8) * cap));
   CUDA_CHECK(cudaMalloc(&sscan, sizeof(Cnt8) * cap));
+  const int ntiles = ceil_div(cap, 1024);
+  CUDA_CHECK(cudaMalloc(&tile_cnt, sizeof(uint32_t) * 8 * ntiles));
+  CUDA_CHECK(cudaMalloc(&tile_off, sizeof(uint32_t) * 8 * ntiles));
   CUDA_CHECK(cudaMalloc(&totals, sizeof(int32_t) * 16));
   CUDA_CHECK(cudaMalloc(&buf, sizeof(float) * cap * d));
   CUDA_CHECK(cudaMalloc(&gown, sizeof(float) * cap * d));
-  CUDA_CHECK(cub::DeviceScan::ExclusiveScan(nullptr, scan_bytes, rin, rscan, Cnt8Sum{}, Cnt8{},
-                                            static_cast<int>(cap)));
-  CUDA_CHECK(cudaMalloc(&temp, scan_bytes));
 }
 
 void Exchange::release() {
-  for (void* p : {static_cast<void*>(tm), static_cast<void*>(lpos), static_cast<void*>(rin),
-                  static_cast<void*>(rscan), static_cast<void*>(sin), static_cast<void*>(sscan),
-                  static_cast<void*>(totals), static_cast<void*>(buf), static_cast<void*>(gown),
-                  temp})
+  for (void* p : {static_cast<void*>(tm), static_cast<void*>(lpos), static_cast<void*>(sscan),
+                  static_cast<void*>(tile_cnt), static_cast<void*>(tile_off),
+                  static_cast<void*>(totals), static_cast<void*>(buf), static_cast<void*>(gown)})
     if (p) cudaFree(p);
   *this = Exchange();
 }
+
+namespace {
+
+// ---- multi-plane ranking: for every element with mask bits p, its rank among
+// the earlier elements that have bit p (8 planes at once, ballot + popc). A
+// tile is 4 rounds x 256 threads = 1024 elements.
+constexpr int kTile = 1024;
+
+// element mask: receive plan = bit(owner) if I touch unique k; send plan = touched mask
+template <bool SEND>
+__device__ __forceinline__ uint32_t plan_mask(int i, const uint32_t* __restrict__ keys,
+                                              const int32_t* __restrict__ live,
+                                              const uint32_t* __restrict__ tm, uint32_t W,
+                                              uint32_t me) {
+  if (i >= *live) return 0u;
+  if (SEND) return tm[keys[i]] & ((1u << W) - 1u);  // keys = own_k
+  return ((tm[i] >> me) & 1u) ? (1u << (keys[i] % W)) : 0u;  // keys = uniq
+}
+
+template <bool SEND>
+__global__ void __launch_bounds__(256) plan_count_kernel(const uint32_t* __restrict__ keys,
+                                                         const int32_t* __restrict__ live, int cap,
+                                                         const uint32_t* __restrict__ tm,
+                                                         uint32_t W, uint32_t me,
+                                                         uint32_t* __restrict__ tile_cnt) {
+  __shared__ uint32_t wc[8][8];  // [warp][plane]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int r = 0; r < 4; ++r) {
+    const int i = blockIdx.x * kTile + r * 256 + threadIdx.x;
+    const uint32_t m = i < cap ? plan_mask<SEND>(i, keys, live, tm, W, me) : 0u;
+#pragma unroll
+    for (int p = 0; p < 8; ++p) acc[p] += __popc(__ballot_sync(0xFFFFFFFFu, (m >> p) & 1u));
+  }
+  if (lane == 0)
+#pragma unroll
+    for (int p = 0; p < 8; ++p) wc[warp][p] = acc[p];
+  __syncthreads();
+  if (threadIdx.x < 8) {
+    uint32_t s = 0;
+    for (int w = 0; w < 8; ++w) s += wc[w][threadIdx.x];
+    tile_cnt[blockIdx.x * 8 + threadIdx.x] = s;
+  }
+}
+
+// warp p scans plane p over the tiles (exclusive), totals[p] = plane total
+__global__ void plan_scan_tiles_kernel(const uint32_t* __restrict__ tile_cnt, int ntiles,
+                                       uint32_t* __restrict__ tile_off,
+                                       int32_t* __restrict__ totals) {
+  const int p = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (p >= 8) return;
+  uint32_t carry = 0;
+  for (int t0 = 0; t0 < ntiles; t0 += 32) {
+    const int t = t0 + lane;
+    const uint32_t v = t < ntiles ? tile_cnt[t * 8 + p] : 0u;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (t < ntiles) tile_off[t * 8 + p] = carry + x - v;
+    carry += __shfl_sync(0xFFFFFFFFu, x, 31);
+  }
+  if (lane == 0) totals[p] = static_cast<int32_t>(carry);
+}
+
+template <bool SEND>
+__global__ void __launch_bounds__(256) plan_rank_kernel(const uint32_t* __restrict__ keys,
+                                                        const int32_t* __restrict__ live, int cap,
+                                                        const uint32_t* __restrict__ tm,
+                                                        uint32_t W, uint32_t me,
+                                                        const uint32_t* __restrict__ tile_off,
+                                                        const int32_t* __restrict__ totals,
+                                                        Cnt8* __restrict__ ranks,
+                                                        uint32_t* __restrict__ lpos) {
+  __shared__ uint32_t wc[4][8][8];  // [round][warp][plane]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  uint32_t m[4], pre[4][8];
+  for (int r = 0; r < 4; ++r) {
+    const int i = blockIdx.x * kTile + r * 256 + threadIdx.x;
+    m[r] = i < cap ? plan_mask<SEND>(i, keys, live, tm, W, me) : 0u;
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      const unsigned b = __ballot_sync(0xFFFFFFFFu, (m[r] >> p) & 1u);
+      pre[r][p] = __popc(b & lt);
+      if (lane == 0) wc[r][warp][p] = __popc(b);
+    }
+  }
+  __syncthreads();
+  for (int r = 0; r < 4; ++r) {
+    const int i = blockIdx.x * kTile + r * 256 + threadIdx.x;
+    if (i >= cap) continue;
+    Cnt8 out{};
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      uint32_t off = tile_off[blockIdx.x * 8 + p];
+      for (int rr = 0; rr < r; ++rr)
+        for (int w = 0; w < 8; ++w) off += wc[rr][w][p];
+      for (int w = 0; w < warp; ++w) off += wc[r][w][p];
+      out.c[p] = off + pre[r][p];
+    }
+    if (SEND) {
+      ranks[i] = out;
+    } else if (m[r]) {  // lpos = owner block offset + rank within the owner's block
+      const uint32_t o = __ffs(m[r]) - 1;
+      uint32_t base = 0;
+      for (uint32_t q = 0; q < o; ++q) base += static_cast<uint32_t>(totals[q]);
+      lpos[i] = base + out.c[o];
+    } else {
+      lpos[i] = 0xFFFFFFFFu;
+    }
+  }
+}
+
+}  // namespace
 
 void Exchange::plan(const uint32_t* d_vid, int64_t n_global, int64_t per_worker,
                     const uint32_t* d_uniq, const int32_t* d_U, const uint32_t* d_own_k,
                     const int32_t* d_n_own, cudaStream_t s) {
   const int c = static_cast<int>(cap);
+  const int ntiles = ceil_div(c, kTile);
   CUDA_CHECK(cudaMemsetAsync(tm, 0, sizeof(uint32_t) * cap, s));
   touch_mask_kernel<<<ceil_div(n_global, 256), 256, 0, s>>>(d_vid, n_global, per_worker, tm);
   CUDA_LAUNCH_CHECK();
-  recv_onehot_kernel<<<ceil_div(c, 256), 256, 0, s>>>(d_uniq, d_U, c, tm, W, me, rin);
+  // receive plan over the uniques
+  plan_count_kernel<false><<<ntiles, 256, 0, s>>>(d_uniq, d_U, c, tm, W, me, tile_cnt);
   CUDA_LAUNCH_CHECK();
-  CUDA_CHECK(cub::DeviceScan::ExclusiveScan(temp, scan_bytes, rin, rscan, Cnt8Sum{}, Cnt8{}, c, s));
-  g_launches += 2;
-  send_onehot_kernel<<<ceil_div(c, 256), 256, 0, s>>>(d_own_k, d_n_own, c, tm, W, sin);
+  plan_scan_tiles_kernel<<<1, 256, 0, s>>>(tile_cnt, ntiles, tile_off, totals);
   CUDA_LAUNCH_CHECK();
-  CUDA_CHECK(cub::DeviceScan::ExclusiveScan(temp, scan_bytes, sin, sscan, Cnt8Sum{}, Cnt8{}, c, s));
-  g_launches += 2;
-  plan_totals_kernel<<<1, 32, 0, s>>>(rscan, rin, sscan, sin, c, totals);
+  plan_rank_kernel<false><<<ntiles, 256, 0, s>>>(d_uniq, d_U, c, tm, W, me, tile_off, totals,
+                                                 nullptr, lpos);
   CUDA_LAUNCH_CHECK();
-  lpos_kernel<<<ceil_div(c, 256), 256, 0, s>>>(d_uniq, d_U, c, tm, W, me, rscan, totals, lpos);
+  // send plan over my owned uniques
+  plan_count_kernel<true><<<ntiles, 256, 0, s>>>(d_own_k, d_n_own, c, tm, W, me, tile_cnt);
+  CUDA_LAUNCH_CHECK();
+  plan_scan_tiles_kernel<<<1, 256, 0, s>>>(tile_cnt, ntiles, tile_off, totals + 8);
+  CUDA_LAUNCH_CHECK();
+  plan_rank_kernel<true><<<ntiles, 256, 0, s>>>(d_own_k, d_n_own, c, tm, W, me, tile_off,
+                                                totals, sscan, nullptr);
   CUDA_LAUNCH_CHECK();
 }
 

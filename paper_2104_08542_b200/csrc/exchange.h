@@ -28,13 +28,12 @@ struct Exchange {
   int64_t cap = 0;               // bound on uniques per step
   uint32_t* tm = nullptr;        // [cap] touched-by-worker bitmask per unique
   uint32_t* lpos = nullptr;      // [cap] row in the local table E (or ~0)
-  Cnt8 *rin = nullptr, *rscan = nullptr;  // receive plan (one-hot owner, scan)
-  Cnt8 *sin = nullptr, *sscan = nullptr;  // send plan (mask bits of owned rows, scan)
+  Cnt8* sscan = nullptr;         // [cap] send slot of owned row j for each destination
+  uint32_t* tile_cnt = nullptr;  // [tiles x 8] per-tile plane counts (planning scratch)
+  uint32_t* tile_off = nullptr;  // [tiles x 8] exclusive tile offsets
   int32_t* totals = nullptr;     // [16] recv rows per owner | send rows per destination
   float* buf = nullptr;          // [cap x d] forward send / backward receive rows
   float* gown = nullptr;         // [cap x d] owner-summed gradients, owned order
-  void* temp = nullptr;
-  size_t scan_bytes = 0;
   std::vector<int64_t> recv_rows, send_rows, recv_off, send_off;  // host copies
 
   void init(int W, int me, int64_t cap, int d);
