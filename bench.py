@@ -258,12 +258,16 @@ def run_ours(args, D):
     # NVLink sync rate (world > 1): bytes this rank handed to NCCL per step / time of the sync phases
     sync = None
     if world > 1:
-        sync_ms = sum(v for k2, v in phase_ms.items() if k2.startswith("allreduce") or k2 == "ids_allgather")
+        sync_ms = sum(v for k2, v in phase_ms.items()
+                      if k2.startswith(("allreduce", "exchange")) or k2 == "ids_allgather")
         nv = per_step.get("nvlink_bytes", 0)
-        busbytes = 2 * (world - 1) / world * nv
-        sync = {"ms": round(sync_ms, 4), "payload_bytes": int(nv),
+        # all-reduce: NCCL bus bytes = 2(W-1)/W x payload; all-to-all: every byte
+        # this rank sends crosses NVLink once
+        busbytes = nv if args.sync == "alltoall" else 2 * (world - 1) / world * nv
+        sync = {"ms": round(sync_ms, 4), "bytes_per_step": int(nv), "scheme": args.sync,
                 "busbw_gbs": round(busbytes / (sync_ms / 1e3) / 1e9, 1) if sync_ms else None,
-                "peak_gbs": 770.0, "peak_source": "B200_PROFILING.md measured peer copy"}
+                "peak_gbs": 770.0, "peak_source": "B200_PROFILING.md measured peer copy",
+                "note": "time includes the exchange planning-free phases only"}
     fill_ms = phase_ms.get("manage_evict_admit", 0.0)
     mix = {"cache_slots_per_gpu": args.cache, "owned_uniques_per_step": round(Uw, 1),
            "misses_per_step": round(per_step.get("working", 0), 1),

@@ -109,12 +109,19 @@ void Exchange::init(int W_, int me_, int64_t cap_, int d_) {
   const int ntiles = ceil_div(cap, 1024);
   CUDA_CHECK(cudaMalloc(&tile_cnt, sizeof(uint32_t) * 8 * ntiles));
   CUDA_CHECK(cudaMalloc(&tile_off, sizeof(uint32_t) * 8 * ntiles));
-  CUDA_CHECK(cudaMalloc(&totals, sizeof(int32_t) * 16));
+  CUDA_CHECK(cudaMalloc(&totals, sizeof(int32_t) * kTotals));
   CUDA_CHECK(cudaMalloc(&buf, sizeof(float) * cap * d));
   CUDA_CHECK(cudaMalloc(&gown, sizeof(float) * cap * d));
 }
 
 void Exchange::release() {
+  if (p2p)
+    for (int w = 0; w < W; ++w) {
+      if (w == me) continue;
+      if (peer_E[w]) cudaIpcCloseMemHandle(peer_E[w]);
+      if (peer_buf[w]) cudaIpcCloseMemHandle(peer_buf[w]);
+    }
+  if (bar) cudaFree(bar);
   for (void* p : {static_cast<void*>(tm), static_cast<void*>(lpos), static_cast<void*>(sscan),
                   static_cast<void*>(tile_cnt), static_cast<void*>(tile_off),
                   static_cast<void*>(totals), static_cast<void*>(buf), static_cast<void*>(gown)})
@@ -123,6 +130,11 @@ void Exchange::release() {
 }
 
 namespace {
+
+__global__ void count_matrix_kernel(const uint32_t* __restrict__ uniq,
+                                    const int32_t* __restrict__ U, int cap,
+                                    const uint32_t* __restrict__ tm, uint32_t W,
+                                    int32_t* __restrict__ cnt);
 
 // ---- multi-plane ranking: for every element with mask bits p, its rank among
 // the earlier elements that have bit p (8 planes at once, ballot + popc). A
@@ -263,6 +275,11 @@ void Exchange::plan(const uint32_t* d_vid, int64_t n_global, int64_t per_worker,
   plan_rank_kernel<true><<<ntiles, 256, 0, s>>>(d_own_k, d_n_own, c, tm, W, me, tile_off,
                                                 totals, sscan, nullptr);
   CUDA_LAUNCH_CHECK();
+  // every peer's layout (peer-store transport)
+  CUDA_CHECK(cudaMemsetAsync(totals + 16, 0, sizeof(int32_t) * 64, s));
+  count_matrix_kernel<<<std::min(ceil_div(c, 256), 148 * 4), 256, 0, s>>>(d_uniq, d_U, c, tm, W,
+                                                                           totals + 16);
+  CUDA_LAUNCH_CHECK();
 }
 
 void Exchange::local_vids(const uint32_t* d_vid_mine, int64_t n, uint32_t* d_lvid, cudaStream_t s) {
@@ -277,11 +294,166 @@ void Exchange::set_counts(const int32_t* h_totals) {
   for (int o = 0; o < 8; ++o) recv_off[o + 1] = recv_off[o] + recv_rows[o];
   send_off.assign(9, 0);
   for (int w = 0; w < 8; ++w) send_off[w + 1] = send_off[w] + (w == me ? 0 : send_rows[w]);
+  // cnt[w][o] = h_totals[16 + w*8 + o]
+  roff_all.assign(64, 0);
+  boff_all.assign(64, 0);
+  for (int w = 0; w < 8; ++w)
+    for (int o = 1; o < 8; ++o)
+      roff_all[w * 8 + o] = roff_all[w * 8 + o - 1] + h_totals[16 + w * 8 + o - 1];
+  for (int o = 0; o < 8; ++o)
+    for (int w = 1; w < 8; ++w)
+      boff_all[o * 8 + w] =
+          boff_all[o * 8 + w - 1] + (w - 1 == o ? 0 : h_totals[16 + (w - 1) * 8 + o]);
+}
+
+namespace {
+
+// count matrix cnt[w][o] = #uniques owned by o that worker w touches (every
+// rank computes all of it, so each knows every peer's receive layout)
+__global__ void count_matrix_kernel(const uint32_t* __restrict__ uniq,
+                                    const int32_t* __restrict__ U, int cap,
+                                    const uint32_t* __restrict__ tm, uint32_t W,
+                                    int32_t* __restrict__ cnt) {
+  __shared__ int32_t c[64];
+  if (threadIdx.x < 64) c[threadIdx.x] = 0;
+  __syncthreads();
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < cap; k += gridDim.x * blockDim.x) {
+    if (k >= *U) break;
+    const uint32_t o = uniq[k] % W;
+    uint32_t m = tm[k];
+    while (m) {
+      const uint32_t w = __ffs(m) - 1;
+      m &= m - 1;
+      atomicAdd(c + w * 8 + o, 1);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 64 && c[threadIdx.x]) atomicAdd(cnt + threadIdx.x, c[threadIdx.x]);
+}
+
+struct PeerRows {
+  float4* E[8];        // every rank's local table E (mine included)
+  float4* buf[8];      // every rank's gradient receive buffer
+  uint32_t e_off[8];   // row where my owner block starts in rank w's E
+  uint32_t b_off[8];   // row where my block starts in owner o's receive buffer
+};
+
+// Forward over NVLink: owned row j is stored straight into the E of every
+// worker that touches it (one warp per row, 16 B lanes, peer stores).
+__global__ void push_rows_p2p_kernel(const uint32_t* __restrict__ own_k,
+                                     const uint32_t* __restrict__ own_slot, int32_t n_own,
+                                     const uint32_t* __restrict__ tm,
+                                     const Cnt8* __restrict__ sscan, uint32_t W,
+                                     const float4* __restrict__ emb, int d4, PeerRows pr) {
+  const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j < n_own) {
+    const uint32_t m = tm[own_k[j]];
+    const float4* src = emb + static_cast<int64_t>(own_slot[j]) * d4;
+    for (uint32_t w = 0; w < W; ++w) {
+      if (!((m >> w) & 1u)) continue;
+      float4* dst = pr.E[w] + static_cast<int64_t>(pr.e_off[w] + sscan[j].c[w]) * d4;
+      for (int c = lane; c < d4; c += 32) dst[c] = src[c];
+    }
+  }
+  __threadfence_system();
+}
+
+// Backward over NVLink: my partial-gradient block for owner o (rows
+// [src_row, src_row + n)) goes to o's receive buffer at dst_row.
+__global__ void push_block_p2p_kernel(const float4* __restrict__ dE, int64_t src_row, int64_t n,
+                                      int d4, float4* __restrict__ dst) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n * d4) dst[i] = dE[src_row * d4 + i];
+  __threadfence_system();
+}
+
+}  // namespace
+
+void Exchange::setup_p2p(float* E, ncclComm_t comm, cudaStream_t s) {
+  int dev = 0;
+  CUDA_CHECK(cudaGetDevice(&dev));
+  // every rank must reach every peer over NVLink; otherwise keep NCCL send/recv
+  std::vector<int> devs(W, -1);
+  int* d_dev = nullptr;
+  CUDA_CHECK(cudaMalloc(&d_dev, sizeof(int) * W));
+  CUDA_CHECK(cudaMemcpyAsync(d_dev + me, &dev, sizeof(int), cudaMemcpyHostToDevice, s));
+  NCCL_CHECK(ncclAllGather(d_dev + me, d_dev, 1, ncclInt32, comm, s));
+  CUDA_CHECK(cudaMemcpyAsync(devs.data(), d_dev, sizeof(int) * W, cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  cudaFree(d_dev);
+  int ok = 1;
+  for (int w = 0; w < W; ++w) {
+    if (w == me) continue;
+    int can = 0;
+    if (cudaDeviceCanAccessPeer(&can, dev, devs[w]) != cudaSuccess || !can) ok = 0;
+  }
+  cudaGetLastError();
+  // agree on the transport (min over ranks)
+  int* d_ok = nullptr;
+  CUDA_CHECK(cudaMalloc(&d_ok, sizeof(int)));
+  CUDA_CHECK(cudaMemcpyAsync(d_ok, &ok, sizeof(int), cudaMemcpyHostToDevice, s));
+  NCCL_CHECK(ncclAllReduce(d_ok, d_ok, 1, ncclInt32, ncclMin, comm, s));
+  CUDA_CHECK(cudaMemcpyAsync(&ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  cudaFree(d_ok);
+  if (!ok) return;
+  // exchange IPC handles of E and buf
+  cudaIpcMemHandle_t mine[2];
+  CUDA_CHECK(cudaIpcGetMemHandle(&mine[0], E));
+  CUDA_CHECK(cudaIpcGetMemHandle(&mine[1], buf));
+  const size_t hb = sizeof(mine);
+  uint8_t* d_h = nullptr;
+  CUDA_CHECK(cudaMalloc(&d_h, hb * W));
+  CUDA_CHECK(cudaMemcpyAsync(d_h + hb * me, mine, hb, cudaMemcpyHostToDevice, s));
+  NCCL_CHECK(ncclAllGather(d_h + hb * me, d_h, hb, ncclUint8, comm, s));
+  std::vector<cudaIpcMemHandle_t> all(2 * W);
+  CUDA_CHECK(cudaMemcpyAsync(all.data(), d_h, hb * W, cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  cudaFree(d_h);
+  for (int w = 0; w < W; ++w) {
+    if (w == me) {
+      peer_E[w] = E;
+      peer_buf[w] = buf;
+      continue;
+    }
+    void* pe = nullptr;
+    void* pb = nullptr;
+    CUDA_CHECK(cudaIpcOpenMemHandle(&pe, all[2 * w], cudaIpcMemLazyEnablePeerAccess));
+    CUDA_CHECK(cudaIpcOpenMemHandle(&pb, all[2 * w + 1], cudaIpcMemLazyEnablePeerAccess));
+    peer_E[w] = static_cast<float*>(pe);
+    peer_buf[w] = static_cast<float*>(pb);
+  }
+  CUDA_CHECK(cudaMalloc(&bar, sizeof(float)));
+  CUDA_CHECK(cudaMemset(bar, 0, sizeof(float)));
+  p2p = true;
+}
+
+void Exchange::barrier(ncclComm_t comm, cudaStream_t s) {
+  // stream-ordered rendezvous: every rank's peer stores (kernel complete +
+  // system fence) precede its contribution, so after this all are visible
+  NCCL_CHECK(ncclAllReduce(bar, bar, 1, ncclFloat32, ncclSum, comm, s));
 }
 
 int64_t Exchange::forward(const uint32_t* d_own_k, const uint32_t* d_own_slot, int32_t n_own,
                           const float* emb, float* E, ncclComm_t comm, cudaStream_t s) {
   const int d4 = d / 4;
+  if (p2p) {
+    PeerRows pr{};
+    int64_t bytes = 0;
+    for (int w = 0; w < W; ++w) {
+      pr.E[w] = reinterpret_cast<float4*>(peer_E[w]);
+      pr.e_off[w] = static_cast<uint32_t>(roff_all[w * 8 + me]);
+      if (w != me) bytes += static_cast<int64_t>(send_rows[w]) * d * 4;
+    }
+    if (n_own > 0) {
+      push_rows_p2p_kernel<<<ceil_div(static_cast<int64_t>(n_own) * 32, 256), 256, 0, s>>>(
+          d_own_k, d_own_slot, n_own, tm, sscan, W, reinterpret_cast<const float4*>(emb), d4, pr);
+      CUDA_LAUNCH_CHECK();
+    }
+    barrier(comm, s);
+    return bytes;
+  }
   if (n_own > 0) {
     pack_rows_kernel<<<ceil_div(static_cast<int64_t>(n_own) * 32, 256), 256, 0, s>>>(
         d_own_k, d_own_slot, n_own, tm, sscan, totals, W, me, lpos,
@@ -309,6 +481,19 @@ int64_t Exchange::forward(const uint32_t* d_own_k, const uint32_t* d_own_slot, i
 int64_t Exchange::backward(const uint32_t* d_own_k, int32_t n_own, const float* dE, ncclComm_t comm,
                            cudaStream_t s) {
   int64_t bytes = 0;
+  if (p2p) {
+    const int d4 = d / 4;
+    for (int o = 0; o < W; ++o) {
+      if (o == me || recv_rows[o] == 0) continue;
+      const int64_t n = recv_rows[o];
+      push_block_p2p_kernel<<<ceil_div(n * d4, 256), 256, 0, s>>>(
+          reinterpret_cast<const float4*>(dE), recv_off[o], n, d4,
+          reinterpret_cast<float4*>(peer_buf[o]) + boff_all[o * 8 + me] * d4);
+      CUDA_LAUNCH_CHECK();
+      bytes += n * d * 4;
+    }
+    barrier(comm, s);
+  } else {
   NCCL_CHECK(ncclGroupStart());
   for (int w = 0; w < W; ++w) {
     if (w == me) continue;
@@ -322,6 +507,7 @@ int64_t Exchange::backward(const uint32_t* d_own_k, int32_t n_own, const float* 
                           static_cast<size_t>(send_rows[w]) * d, ncclFloat32, w, comm, s));
   }
   NCCL_CHECK(ncclGroupEnd());
+  }
   const int d4 = d / 4;
   if (n_own > 0) {
     owner_reduce_kernel<<<ceil_div(static_cast<int64_t>(n_own) * d4, 256), 256, 0, s>>>(

@@ -31,13 +31,26 @@ struct Exchange {
   Cnt8* sscan = nullptr;         // [cap] send slot of owned row j for each destination
   uint32_t* tile_cnt = nullptr;  // [tiles x 8] per-tile plane counts (planning scratch)
   uint32_t* tile_off = nullptr;  // [tiles x 8] exclusive tile offsets
-  int32_t* totals = nullptr;     // [16] recv rows per owner | send rows per destination
+  // [80]: recv rows per owner (8) | send rows per destination (8) | cnt[w][o] (64)
+  int32_t* totals = nullptr;
   float* buf = nullptr;          // [cap x d] forward send / backward receive rows
   float* gown = nullptr;         // [cap x d] owner-summed gradients, owned order
   std::vector<int64_t> recv_rows, send_rows, recv_off, send_off;  // host copies
+  // NVLink peer-store transport (all peers reachable): every rank's E and buf
+  bool p2p = false;
+  float* peer_E[8] = {};
+  float* peer_buf[8] = {};
+  float* bar = nullptr;                    // 1-float all-reduce used as a barrier
+  std::vector<int64_t> roff_all, boff_all;  // [w*8+o]: rank w's E block of owner o;
+                                            // [o*8+w]: owner o's buf block of source w
+  static constexpr int kTotals = 80;
 
   void init(int W, int me, int64_t cap, int d);
   void release();
+  // maps every peer's E / buf (CUDA IPC, handles all-gathered over NCCL) when
+  // all pairs have peer access; otherwise the exchange uses NCCL send/recv
+  void setup_p2p(float* E, ncclComm_t comm, cudaStream_t s);
+  void barrier(ncclComm_t comm, cudaStream_t s);
   // device-only planning (no host wait); totals land in `totals`
   void plan(const uint32_t* d_vid, int64_t n_global, int64_t per_worker, const uint32_t* d_uniq,
             const int32_t* d_U, const uint32_t* d_own_k, const int32_t* d_n_own, cudaStream_t s);

@@ -163,7 +163,10 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
     a2a_ = true;
     xch_.init(W_, rank_, umax, d_);
     CUDA_CHECK(cudaMalloc(&d_lvid_, sizeof(uint32_t) * n_local_));
-    CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_totals_), sizeof(int32_t) * 16, 0));
+    CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_totals_),
+                             sizeof(int32_t) * Exchange::kTotals, 0));
+    const char* np2p = std::getenv("SFCTR_NO_P2P");  // debugging: force NCCL send/recv
+    if (!(np2p && np2p[0] == '1')) xch_.setup_p2p(d_G_, comm_, stream_);
   }
   ensure_bias_tables(1024);
   CUDA_CHECK(cudaStreamSynchronize(stream_));
@@ -310,7 +313,7 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   if (a2a_) {  // exchange plan (touched masks, send/receive positions), device only
     xch_.plan(d_vid_, n_global_, static_cast<int64_t>(b_) * F_, d_uniq_, d_scalars_ + 0,
               lane_[0].own_k, lane_[0].counters + kCntOwned, s);
-    CUDA_CHECK(cudaMemcpyAsync(h_totals_, xch_.totals, sizeof(int32_t) * 16,
+    CUDA_CHECK(cudaMemcpyAsync(h_totals_, xch_.totals, sizeof(int32_t) * Exchange::kTotals,
                                cudaMemcpyDeviceToHost, s));
   }
   phase("manage_probe");
