@@ -356,7 +356,10 @@ __global__ void push_rows_p2p_kernel(const uint32_t* __restrict__ own_k,
       for (int c = lane; c < d4; c += 32) dst[c] = src[c];
     }
   }
-  __threadfence_system();
+  // one cumulative system-scope fence per CTA (after the CTA barrier) orders
+  // all of this CTA's peer stores before the barrier collective that follows
+  __syncthreads();
+  if (threadIdx.x == 0) __threadfence_system();
 }
 
 // Backward over NVLink: my partial-gradient block for owner o (rows
@@ -365,7 +368,8 @@ __global__ void push_block_p2p_kernel(const float4* __restrict__ dE, int64_t src
                                       int d4, float4* __restrict__ dst) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i < n * d4) dst[i] = dE[src_row * d4 + i];
-  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) __threadfence_system();
 }
 
 }  // namespace
@@ -436,7 +440,8 @@ void Exchange::barrier(ncclComm_t comm, cudaStream_t s) {
 }
 
 int64_t Exchange::forward(const uint32_t* d_own_k, const uint32_t* d_own_slot, int32_t n_own,
-                          const float* emb, float* E, ncclComm_t comm, cudaStream_t s) {
+                          const float* emb, float* E, ncclComm_t comm, cudaStream_t s,
+                          bool do_barrier) {
   const int d4 = d / 4;
   if (p2p) {
     PeerRows pr{};
@@ -451,7 +456,7 @@ int64_t Exchange::forward(const uint32_t* d_own_k, const uint32_t* d_own_slot, i
           d_own_k, d_own_slot, n_own, tm, sscan, W, reinterpret_cast<const float4*>(emb), d4, pr);
       CUDA_LAUNCH_CHECK();
     }
-    barrier(comm, s);
+    if (do_barrier) barrier(comm, s);
     return bytes;
   }
   if (n_own > 0) {

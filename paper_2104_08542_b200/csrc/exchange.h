@@ -58,8 +58,10 @@ struct Exchange {
   void local_vids(const uint32_t* d_vid_mine, int64_t n, uint32_t* d_lvid, cudaStream_t s);
   int64_t local_rows() const { return recv_off.empty() ? 0 : recv_off[8]; }
   // returns the bytes this rank sent
+  // with the peer-store transport the caller may defer the barrier (do_barrier = false)
   int64_t forward(const uint32_t* d_own_k, const uint32_t* d_own_slot, int32_t n_own,
-                  const float* emb, float* E, ncclComm_t comm, cudaStream_t s);
+                  const float* emb, float* E, ncclComm_t comm, cudaStream_t s,
+                  bool do_barrier = true);
   int64_t backward(const uint32_t* d_own_k, int32_t n_own, const float* dE, ncclComm_t comm,
                    cudaStream_t s);
 };

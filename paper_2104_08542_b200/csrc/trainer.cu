@@ -310,13 +310,14 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
                            s);
   }
   for (int l = 0; l < lanes_; ++l) lane_[l].probe(d_uniq_, cap, Wu, t, s);
+  phase("manage_probe");
   if (a2a_) {  // exchange plan (touched masks, send/receive positions), device only
     xch_.plan(d_vid_, n_global_, static_cast<int64_t>(b_) * F_, d_uniq_, d_scalars_ + 0,
               lane_[0].own_k, lane_[0].counters + kCntOwned, s);
     CUDA_CHECK(cudaMemcpyAsync(h_totals_, xch_.totals, sizeof(int32_t) * Exchange::kTotals,
                                cudaMemcpyDeviceToHost, s));
+    phase("exchange_plan");
   }
-  phase("manage_probe");
   CUDA_CHECK(cudaMemcpyAsync(h_scalars_, d_scalars_, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost, s));
   for (int l = 0; l < lanes_; ++l)
     CUDA_CHECK(cudaMemcpyAsync(h_counts_ + 8 * l, lane_[l].counters, sizeof(int32_t) * 8,
@@ -365,11 +366,13 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   size_t table_rows = static_cast<size_t>(U);
   if (a2a_) {
     xch_.set_counts(h_totals_);
-    stats_.nvlink_bytes +=
-        xch_.forward(lane_[0].own_k, lane_[0].own_slot, n_own[0], lane_[0].emb, d_G_, comm_, s);
+    stats_.nvlink_bytes += xch_.forward(lane_[0].own_k, lane_[0].own_slot, n_own[0],
+                                        lane_[0].emb, d_G_, comm_, s, /*barrier=*/false);
+    phase("exchange_embed");
+    if (xch_.p2p) xch_.barrier(comm_, s);
+    phase("exchange_barrier");
     table_rows = static_cast<size_t>(xch_.local_rows());
     xch_.local_vids(d_vid_ + static_cast<size_t>(lane0_) * b_ * F_, n_local_, d_lvid_, s);
-    phase("exchange_embed");
   } else {
     if (world_ > 1) CUDA_CHECK(cudaMemsetAsync(d_G_, 0, sizeof(float) * ud, s));
     for (int l = 0; l < lanes_; ++l)
