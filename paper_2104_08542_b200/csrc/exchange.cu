@@ -451,7 +451,23 @@ int64_t Exchange::forward(const uint32_t* d_own_k, const uint32_t* d_own_slot, i
       pr.e_off[w] = static_cast<uint32_t>(roff_all[w * 8 + me]);
       if (w != me) bytes += static_cast<int64_t>(send_rows[w]) * d * 4;
     }
-    if (n_own > 0) {
+    if (copy_engine) {
+      // pack locally (HBM), then one DMA copy per peer over NVLink
+      if (n_own > 0) {
+        pack_rows_kernel<<<ceil_div(static_cast<int64_t>(n_own) * 32, 256), 256, 0, s>>>(
+            d_own_k, d_own_slot, n_own, tm, sscan, totals, W, me, lpos,
+            reinterpret_cast<const float4*>(emb), d4, reinterpret_cast<float4*>(buf),
+            reinterpret_cast<float4*>(E));
+        CUDA_LAUNCH_CHECK();
+      }
+      for (int w = 0; w < W; ++w) {
+        if (w == me || send_rows[w] == 0) continue;
+        CUDA_CHECK(cudaMemcpyAsync(peer_E[w] + static_cast<size_t>(roff_all[w * 8 + me]) * d,
+                                   buf + static_cast<size_t>(send_off[w]) * d,
+                                   sizeof(float) * static_cast<size_t>(send_rows[w]) * d,
+                                   cudaMemcpyDeviceToDevice, s));
+      }
+    } else if (n_own > 0) {
       push_rows_p2p_kernel<<<ceil_div(static_cast<int64_t>(n_own) * 32, 256), 256, 0, s>>>(
           d_own_k, d_own_slot, n_own, tm, sscan, W, reinterpret_cast<const float4*>(emb), d4, pr);
       CUDA_LAUNCH_CHECK();
@@ -491,10 +507,17 @@ int64_t Exchange::backward(const uint32_t* d_own_k, int32_t n_own, const float* 
     for (int o = 0; o < W; ++o) {
       if (o == me || recv_rows[o] == 0) continue;
       const int64_t n = recv_rows[o];
-      push_block_p2p_kernel<<<ceil_div(n * d4, 256), 256, 0, s>>>(
-          reinterpret_cast<const float4*>(dE), recv_off[o], n, d4,
-          reinterpret_cast<float4*>(peer_buf[o]) + boff_all[o * 8 + me] * d4);
-      CUDA_LAUNCH_CHECK();
+      if (copy_engine) {
+        CUDA_CHECK(cudaMemcpyAsync(peer_buf[o] + static_cast<size_t>(boff_all[o * 8 + me]) * d,
+                                   dE + static_cast<size_t>(recv_off[o]) * d,
+                                   sizeof(float) * static_cast<size_t>(n) * d,
+                                   cudaMemcpyDeviceToDevice, s));
+      } else {
+        push_block_p2p_kernel<<<ceil_div(n * d4, 256), 256, 0, s>>>(
+            reinterpret_cast<const float4*>(dE), recv_off[o], n, d4,
+            reinterpret_cast<float4*>(peer_buf[o]) + boff_all[o * 8 + me] * d4);
+        CUDA_LAUNCH_CHECK();
+      }
       bytes += n * d * 4;
     }
     barrier(comm, s);
