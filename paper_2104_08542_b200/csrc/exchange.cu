@@ -160,6 +160,10 @@ __global__ void __launch_bounds__(256) plan_count_kernel(const uint32_t* __restr
                                                          uint32_t* __restrict__ tile_cnt) {
   __shared__ uint32_t wc[8][8];  // [warp][plane]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (blockIdx.x * kTile >= *live) {  // tile past the live count: nothing to rank
+    if (threadIdx.x < 8) tile_cnt[blockIdx.x * 8 + threadIdx.x] = 0;
+    return;
+  }
   uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int r = 0; r < 4; ++r) {
     const int i = blockIdx.x * kTile + r * 256 + threadIdx.x;
@@ -209,8 +213,9 @@ __global__ void __launch_bounds__(256) plan_rank_kernel(const uint32_t* __restri
                                                         const int32_t* __restrict__ totals,
                                                         Cnt8* __restrict__ ranks,
                                                         uint32_t* __restrict__ lpos) {
-  __shared__ uint32_t wc[4][8][8];  // [round][warp][plane]
+  __shared__ uint32_t wc[4][8][8];  // [round][warp][plane] -> exclusive offsets in tile order
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (blockIdx.x * kTile >= *live) return;  // no live element in this tile
   const unsigned lt = (1u << lane) - 1u;
   uint32_t m[4], pre[4][8];
   for (int r = 0; r < 4; ++r) {
@@ -224,18 +229,23 @@ __global__ void __launch_bounds__(256) plan_rank_kernel(const uint32_t* __restri
     }
   }
   __syncthreads();
+  if (threadIdx.x < 8) {  // plane p: exclusive prefix over (round, warp) in tile order
+    const int p = threadIdx.x;
+    uint32_t run = tile_off[blockIdx.x * 8 + p];
+    for (int rr = 0; rr < 4; ++rr)
+      for (int w = 0; w < 8; ++w) {
+        const uint32_t c = wc[rr][w][p];
+        wc[rr][w][p] = run;
+        run += c;
+      }
+  }
+  __syncthreads();
   for (int r = 0; r < 4; ++r) {
     const int i = blockIdx.x * kTile + r * 256 + threadIdx.x;
     if (i >= cap) continue;
     Cnt8 out{};
 #pragma unroll
-    for (int p = 0; p < 8; ++p) {
-      uint32_t off = tile_off[blockIdx.x * 8 + p];
-      for (int rr = 0; rr < r; ++rr)
-        for (int w = 0; w < 8; ++w) off += wc[rr][w][p];
-      for (int w = 0; w < warp; ++w) off += wc[r][w][p];
-      out.c[p] = off + pre[r][p];
-    }
+    for (int p = 0; p < 8; ++p) out.c[p] = wc[r][warp][p] + pre[r][p];
     if (SEND) {
       ranks[i] = out;
     } else if (m[r]) {  // lpos = owner block offset + rank within the owner's block
@@ -345,9 +355,10 @@ __global__ void push_rows_p2p_kernel(const uint32_t* __restrict__ own_k,
                                      const uint32_t* __restrict__ tm,
                                      const Cnt8* __restrict__ sscan, uint32_t W,
                                      const float4* __restrict__ emb, int d4, PeerRows pr) {
-  const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (j < n_own) {
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  // persistent warps (grid-stride) so the per-CTA fence below is paid once
+  for (int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < n_own; j += nwarps) {
     const uint32_t m = tm[own_k[j]];
     const float4* src = emb + static_cast<int64_t>(own_slot[j]) * d4;
     for (uint32_t w = 0; w < W; ++w) {
@@ -366,8 +377,9 @@ __global__ void push_rows_p2p_kernel(const uint32_t* __restrict__ own_k,
 // [src_row, src_row + n)) goes to o's receive buffer at dst_row.
 __global__ void push_block_p2p_kernel(const float4* __restrict__ dE, int64_t src_row, int64_t n,
                                       int d4, float4* __restrict__ dst) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i < n * d4) dst[i] = dE[src_row * d4 + i];
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n * d4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[i] = dE[src_row * d4 + i];
   __syncthreads();
   if (threadIdx.x == 0) __threadfence_system();
 }
@@ -468,7 +480,8 @@ int64_t Exchange::forward(const uint32_t* d_own_k, const uint32_t* d_own_slot, i
                                    cudaMemcpyDeviceToDevice, s));
       }
     } else if (n_own > 0) {
-      push_rows_p2p_kernel<<<ceil_div(static_cast<int64_t>(n_own) * 32, 256), 256, 0, s>>>(
+      push_rows_p2p_kernel<<<std::min(ceil_div(static_cast<int64_t>(n_own) * 32, 256), 148 * 8),
+                             256, 0, s>>>(
           d_own_k, d_own_slot, n_own, tm, sscan, W, reinterpret_cast<const float4*>(emb), d4, pr);
       CUDA_LAUNCH_CHECK();
     }
@@ -513,7 +526,7 @@ int64_t Exchange::backward(const uint32_t* d_own_k, int32_t n_own, const float* 
                                    sizeof(float) * static_cast<size_t>(n) * d,
                                    cudaMemcpyDeviceToDevice, s));
       } else {
-        push_block_p2p_kernel<<<ceil_div(n * d4, 256), 256, 0, s>>>(
+        push_block_p2p_kernel<<<std::min(ceil_div(n * d4, 256), 148 * 4), 256, 0, s>>>(
             reinterpret_cast<const float4*>(dE), recv_off[o], n, d4,
             reinterpret_cast<float4*>(peer_buf[o]) + boff_all[o * 8 + me] * d4);
         CUDA_LAUNCH_CHECK();
