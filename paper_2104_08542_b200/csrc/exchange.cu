@@ -107,8 +107,8 @@ void Exchange::init(int W_, int me_, int64_t cap_, int d_) {
   CUDA_CHECK(cudaMalloc(&lpos, sizeof(uint32_t) * cap));
   CUDA_CHECK(cudaMalloc(&sscan, sizeof(Cnt8) * cap));
   const int ntiles = ceil_div(cap, 1024);
-  CUDA_CHECK(cudaMalloc(&tile_cnt, sizeof(uint32_t) * 8 * ntiles));
-  CUDA_CHECK(cudaMalloc(&tile_off, sizeof(uint32_t) * 8 * ntiles));
+  CUDA_CHECK(cudaMalloc(&tile_cnt, sizeof(uint32_t) * 2 * 8 * ntiles));  // recv | send tables
+  CUDA_CHECK(cudaMalloc(&tile_off, sizeof(uint32_t) * 2 * 8 * ntiles));
   CUDA_CHECK(cudaMalloc(&totals, sizeof(int32_t) * kTotals));
   CUDA_CHECK(cudaMalloc(&buf, sizeof(float) * cap * d));
   CUDA_CHECK(cudaMalloc(&gown, sizeof(float) * cap * d));
@@ -153,7 +153,7 @@ __device__ __forceinline__ uint32_t plan_mask(int i, const uint32_t* __restrict_
 }
 
 template <bool SEND>
-__global__ void __launch_bounds__(256) plan_count_kernel(const uint32_t* __restrict__ keys,
+__device__ __forceinline__ void plan_count_tile(const uint32_t* __restrict__ keys,
                                                          const int32_t* __restrict__ live, int cap,
                                                          const uint32_t* __restrict__ tm,
                                                          uint32_t W, uint32_t me,
@@ -183,11 +183,16 @@ __global__ void __launch_bounds__(256) plan_count_kernel(const uint32_t* __restr
 }
 
 // warp p scans plane p over the tiles (exclusive), totals[p] = plane total
-__global__ void plan_scan_tiles_kernel(const uint32_t* __restrict__ tile_cnt, int ntiles,
-                                       uint32_t* __restrict__ tile_off,
-                                       int32_t* __restrict__ totals) {
-  const int p = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (p >= 8) return;
+// two tables at once (receive plan, send plan): warp q < 16 scans plane q % 8 of table q / 8
+__global__ void plan_scan_tiles_kernel(const uint32_t* __restrict__ tile_cnt_all, int ntiles,
+                                       uint32_t* __restrict__ tile_off_all,
+                                       int32_t* __restrict__ totals_all) {
+  const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (q >= 16) return;
+  const int p = q & 7;
+  const uint32_t* tile_cnt = tile_cnt_all + (q >> 3) * ntiles * 8;
+  uint32_t* tile_off = tile_off_all + (q >> 3) * ntiles * 8;
+  int32_t* totals = totals_all + (q >> 3) * 8;
   uint32_t carry = 0;
   for (int t0 = 0; t0 < ntiles; t0 += 32) {
     const int t = t0 + lane;
@@ -205,7 +210,7 @@ __global__ void plan_scan_tiles_kernel(const uint32_t* __restrict__ tile_cnt, in
 }
 
 template <bool SEND>
-__global__ void __launch_bounds__(256) plan_rank_kernel(const uint32_t* __restrict__ keys,
+__device__ __forceinline__ void plan_rank_tile(const uint32_t* __restrict__ keys,
                                                         const int32_t* __restrict__ live, int cap,
                                                         const uint32_t* __restrict__ tm,
                                                         uint32_t W, uint32_t me,
@@ -259,6 +264,29 @@ __global__ void __launch_bounds__(256) plan_rank_kernel(const uint32_t* __restri
   }
 }
 
+// blockIdx.y = 0: receive plan over the uniques; 1: send plan over my owned uniques
+__global__ void __launch_bounds__(256) plan_count_kernel(
+    const uint32_t* __restrict__ uniq, const int32_t* __restrict__ U,
+    const uint32_t* __restrict__ own_k, const int32_t* __restrict__ n_own, int cap,
+    const uint32_t* __restrict__ tm, uint32_t W, uint32_t me, int ntiles,
+    uint32_t* __restrict__ tile_cnt) {
+  if (blockIdx.y == 0) plan_count_tile<false>(uniq, U, cap, tm, W, me, tile_cnt);
+  else plan_count_tile<true>(own_k, n_own, cap, tm, W, me, tile_cnt + ntiles * 8);
+}
+
+__global__ void __launch_bounds__(256) plan_rank_kernel(
+    const uint32_t* __restrict__ uniq, const int32_t* __restrict__ U,
+    const uint32_t* __restrict__ own_k, const int32_t* __restrict__ n_own, int cap,
+    const uint32_t* __restrict__ tm, uint32_t W, uint32_t me, int ntiles,
+    const uint32_t* __restrict__ tile_off, const int32_t* __restrict__ totals,
+    Cnt8* __restrict__ sscan, uint32_t* __restrict__ lpos) {
+  if (blockIdx.y == 0)
+    plan_rank_tile<false>(uniq, U, cap, tm, W, me, tile_off, totals, nullptr, lpos);
+  else
+    plan_rank_tile<true>(own_k, n_own, cap, tm, W, me, tile_off + ntiles * 8, totals, sscan,
+                         nullptr);
+}
+
 }  // namespace
 
 void Exchange::plan(const uint32_t* d_vid, int64_t n_global, int64_t per_worker,
@@ -269,21 +297,14 @@ void Exchange::plan(const uint32_t* d_vid, int64_t n_global, int64_t per_worker,
   CUDA_CHECK(cudaMemsetAsync(tm, 0, sizeof(uint32_t) * cap, s));
   touch_mask_kernel<<<ceil_div(n_global, 256), 256, 0, s>>>(d_vid, n_global, per_worker, tm);
   CUDA_LAUNCH_CHECK();
-  // receive plan over the uniques
-  plan_count_kernel<false><<<ntiles, 256, 0, s>>>(d_uniq, d_U, c, tm, W, me, tile_cnt);
+  // receive plan (y = 0, over the uniques) and send plan (y = 1, over my owned uniques)
+  plan_count_kernel<<<dim3(ntiles, 2), 256, 0, s>>>(d_uniq, d_U, d_own_k, d_n_own, c, tm, W, me,
+                                                    ntiles, tile_cnt);
   CUDA_LAUNCH_CHECK();
-  plan_scan_tiles_kernel<<<1, 256, 0, s>>>(tile_cnt, ntiles, tile_off, totals);
+  plan_scan_tiles_kernel<<<1, 512, 0, s>>>(tile_cnt, ntiles, tile_off, totals);
   CUDA_LAUNCH_CHECK();
-  plan_rank_kernel<false><<<ntiles, 256, 0, s>>>(d_uniq, d_U, c, tm, W, me, tile_off, totals,
-                                                 nullptr, lpos);
-  CUDA_LAUNCH_CHECK();
-  // send plan over my owned uniques
-  plan_count_kernel<true><<<ntiles, 256, 0, s>>>(d_own_k, d_n_own, c, tm, W, me, tile_cnt);
-  CUDA_LAUNCH_CHECK();
-  plan_scan_tiles_kernel<<<1, 256, 0, s>>>(tile_cnt, ntiles, tile_off, totals + 8);
-  CUDA_LAUNCH_CHECK();
-  plan_rank_kernel<true><<<ntiles, 256, 0, s>>>(d_own_k, d_n_own, c, tm, W, me, tile_off,
-                                                totals, sscan, nullptr);
+  plan_rank_kernel<<<dim3(ntiles, 2), 256, 0, s>>>(d_uniq, d_U, d_own_k, d_n_own, c, tm, W, me,
+                                                   ntiles, tile_off, totals, sscan, lpos);
   CUDA_LAUNCH_CHECK();
   // every peer's layout (peer-store transport)
   CUDA_CHECK(cudaMemsetAsync(totals + 16, 0, sizeof(int32_t) * 64, s));

@@ -38,7 +38,7 @@ struct Exchange {
   std::vector<int64_t> recv_rows, send_rows, recv_off, send_off;  // host copies
   // NVLink peer-store transport (all peers reachable): every rank's E and buf
   bool p2p = false;
-  bool copy_engine = true;  // p2p rows move by DMA (pack + cudaMemcpyAsync) vs SM peer stores
+  bool copy_engine = false;  // p2p rows move by SM peer stores (default) or DMA (pack + memcpy)
   float* peer_E[8] = {};
   float* peer_buf[8] = {};
   float* bar = nullptr;                    // 1-float all-reduce used as a barrier

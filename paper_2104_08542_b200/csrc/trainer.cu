@@ -167,8 +167,8 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
                              sizeof(int32_t) * Exchange::kTotals, 0));
     const char* np2p = std::getenv("SFCTR_NO_P2P");  // debugging: force NCCL send/recv
     if (!(np2p && np2p[0] == '1')) xch_.setup_p2p(d_G_, comm_, stream_);
-    const char* sm = std::getenv("SFCTR_P2P_SM_STORES");  // SM peer stores instead of DMA
-    xch_.copy_engine = !(sm && sm[0] == '1');
+    const char* ce = std::getenv("SFCTR_P2P_COPY_ENGINE");  // DMA copies instead of SM stores
+    xch_.copy_engine = ce && ce[0] == '1';
   }
   ensure_bias_tables(1024);
   CUDA_CHECK(cudaStreamSynchronize(stream_));
