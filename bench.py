@@ -48,7 +48,9 @@ def parse():
     p.add_argument("--zipf", type=float, default=1.05)
     p.add_argument("--hidden", type=int, default=64)
     p.add_argument("--cache", type=int, default=1 << 19)
-    p.add_argument("--sync", default="allreduce", choices=["allreduce", "alltoall"])
+    # alltoall = owner-routed exchange of only the touched rows (default); allreduce = the
+    # reference's all-reduce of the zero-padded common embedding / gradients
+    p.add_argument("--sync", default="alltoall", choices=["allreduce", "alltoall"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-rows", type=int, default=2048, help="rows per CPU-baseline step")
     p.add_argument("--cpu-steps", type=int, default=3)
