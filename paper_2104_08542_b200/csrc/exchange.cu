@@ -394,6 +394,26 @@ __global__ void push_rows_p2p_kernel(const uint32_t* __restrict__ own_k,
   if (threadIdx.x == 0) __threadfence_system();
 }
 
+struct PeerBlocks {
+  float4* dst[8];      // owner o's receive buffer at my block
+  int64_t src_row[8];  // my dE rows of owner o start here
+  int64_t rows[8];     // 0 for myself
+};
+
+// Backward over NVLink, all owners in one launch (blockIdx.y = owner o): my
+// contiguous partial-gradient block for o is stored into o's receive buffer.
+__global__ void push_blocks_p2p_kernel(const float4* __restrict__ dE, int d4, PeerBlocks pb) {
+  const int o = blockIdx.y;
+  const int64_t n = pb.rows[o] * d4;
+  const float4* src = dE + pb.src_row[o] * d4;
+  float4* dst = pb.dst[o];
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[i] = src[i];
+  __syncthreads();
+  if (threadIdx.x == 0) __threadfence_system();
+}
+
 // Backward over NVLink: my partial-gradient block for owner o (rows
 // [src_row, src_row + n)) goes to o's receive buffer at dst_row.
 __global__ void push_block_p2p_kernel(const float4* __restrict__ dE, int64_t src_row, int64_t n,
@@ -535,27 +555,44 @@ int64_t Exchange::forward(const uint32_t* d_own_k, const uint32_t* d_own_slot, i
 
 int64_t Exchange::backward(const uint32_t* d_own_k, int32_t n_own, const float* dE, ncclComm_t comm,
                            cudaStream_t s) {
+  const int64_t bytes = backward_send(dE, comm, s);
+  if (p2p) barrier(comm, s);
+  backward_reduce(d_own_k, n_own, dE, s);
+  return bytes;
+}
+
+int64_t Exchange::backward_send(const float* dE, ncclComm_t comm, cudaStream_t s) {
   int64_t bytes = 0;
   if (p2p) {
     const int d4 = d / 4;
-    for (int o = 0; o < W; ++o) {
-      if (o == me || recv_rows[o] == 0) continue;
-      const int64_t n = recv_rows[o];
-      if (copy_engine) {
+    if (copy_engine) {
+      for (int o = 0; o < W; ++o) {
+        if (o == me || recv_rows[o] == 0) continue;
         CUDA_CHECK(cudaMemcpyAsync(peer_buf[o] + static_cast<size_t>(boff_all[o * 8 + me]) * d,
                                    dE + static_cast<size_t>(recv_off[o]) * d,
-                                   sizeof(float) * static_cast<size_t>(n) * d,
+                                   sizeof(float) * static_cast<size_t>(recv_rows[o]) * d,
                                    cudaMemcpyDeviceToDevice, s));
-      } else {
-        push_block_p2p_kernel<<<std::min(ceil_div(n * d4, 256), 148 * 4), 256, 0, s>>>(
-            reinterpret_cast<const float4*>(dE), recv_off[o], n, d4,
-            reinterpret_cast<float4*>(peer_buf[o]) + boff_all[o * 8 + me] * d4);
+        bytes += recv_rows[o] * d * 4;
+      }
+    } else {  // every peer block in one launch: blockIdx.y = owner
+      PeerBlocks pb{};
+      int64_t most = 0;
+      for (int o = 0; o < W; ++o) {
+        pb.dst[o] = reinterpret_cast<float4*>(peer_buf[o]) + boff_all[o * 8 + me] * d4;
+        pb.src_row[o] = recv_off[o];
+        pb.rows[o] = (o == me) ? 0 : recv_rows[o];
+        most = std::max<int64_t>(most, pb.rows[o]);
+        bytes += pb.rows[o] * d * 4;
+      }
+      if (most > 0) {
+        push_blocks_p2p_kernel<<<dim3(std::min(ceil_div(most * d4, 256), 148 * 2), W), 256, 0,
+                                 s>>>(reinterpret_cast<const float4*>(dE), d4, pb);
         CUDA_LAUNCH_CHECK();
       }
-      bytes += n * d * 4;
     }
-    barrier(comm, s);
-  } else {
+    return bytes;
+  }
+  {
   NCCL_CHECK(ncclGroupStart());
   for (int w = 0; w < W; ++w) {
     if (w == me) continue;
@@ -570,6 +607,11 @@ int64_t Exchange::backward(const uint32_t* d_own_k, int32_t n_own, const float* 
   }
   NCCL_CHECK(ncclGroupEnd());
   }
+  return bytes;
+}
+
+void Exchange::backward_reduce(const uint32_t* d_own_k, int32_t n_own, const float* dE,
+                               cudaStream_t s) {
   const int d4 = d / 4;
   if (n_own > 0) {
     owner_reduce_kernel<<<ceil_div(static_cast<int64_t>(n_own) * d4, 256), 256, 0, s>>>(
@@ -577,7 +619,6 @@ int64_t Exchange::backward(const uint32_t* d_own_k, int32_t n_own, const float* 
         reinterpret_cast<const float4*>(buf), d4, reinterpret_cast<float4*>(gown));
     CUDA_LAUNCH_CHECK();
   }
-  return bytes;
 }
 
 }  // namespace sfb

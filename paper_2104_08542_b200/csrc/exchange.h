@@ -65,6 +65,9 @@ struct Exchange {
                   bool do_barrier = true);
   int64_t backward(const uint32_t* d_own_k, int32_t n_own, const float* dE, ncclComm_t comm,
                    cudaStream_t s);
+  // the same in parts: send my partial gradients (no barrier), then the owner-side sum
+  int64_t backward_send(const float* dE, ncclComm_t comm, cudaStream_t s);
+  void backward_reduce(const uint32_t* d_own_k, int32_t n_own, const float* dE, cudaStream_t s);
 };
 
 }  // namespace sfb

@@ -416,7 +416,11 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   // ---- grad_synchronize (l.13)
   const float* grad_rows = d_dG_;
   if (a2a_) {
-    stats_.nvlink_bytes += xch_.backward(lane_[0].own_k, n_own[0], d_dG_, comm_, s);
+    stats_.nvlink_bytes += xch_.backward_send(d_dG_, comm_, s);
+    phase("exchange_grad_send");
+    if (xch_.p2p) xch_.barrier(comm_, s);
+    phase("exchange_grad_barrier");
+    xch_.backward_reduce(lane_[0].own_k, n_own[0], d_dG_, s);
     grad_rows = xch_.gown;
   } else if (world_ > 1) {
     NCCL_CHECK(ncclAllReduce(d_dG_, d_dG_, ud, ncclFloat32, ncclSum, comm_, s));
