@@ -52,6 +52,7 @@ struct TowerBufs {
 struct TowerTC {
   int rows_cap = 0, K = 0, H = 0, d = 0;
   int ldk = 0, ldh = 0, ldr = 0;  // padded K, H, rows
+  int dp = 0, Kp = 0;             // fused path: padded field width, F * dp
   int s1_max = 1, s3_max = 1;     // split-K factors of GEMM1 / GEMM3
   float *w_hi = nullptr, *w_lo = nullptr;    // [K x ldh]
   float *wt_hi = nullptr, *wt_lo = nullptr;  // [H x ldk]
@@ -71,6 +72,14 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc, const float* X, int ld
                                int32_t rows, int F, int d, const float* dense, float* logits,
                                float* dX, float emb_scale, float* grads, bool accumulate,
                                cudaStream_t s);
+// Fused path (tc_fused.cuh): X = G[vid] is gathered straight into the GEMM
+// operands and dX is scatter-added into dG (with the FM term) by the dX GEMM's
+// epilogue; neither touches HBM. Writes fm_s [rows x d]. Needs d % 4 == 0, d <= 128.
+bool tower_fused_supported(int d);
+void tower_forward_backward_fused(TowerBufs& t, TowerTC& tc, const float* G, const uint32_t* vid,
+                                  const uint8_t* labels, int32_t rows, int F, int d,
+                                  const float* dense, float* logits, float* fm_s, float emb_scale,
+                                  float* dG, float* grads, bool accumulate, cudaStream_t s);
 // fp32 SIMT reference tiles of the same tower (validation only; needs ldx == K)
 void tower_forward_backward_simt(TowerBufs& t, const float* X, const float* fm_s,
                                  const float* fm_sqp, const uint8_t* labels, int32_t rows, int F,

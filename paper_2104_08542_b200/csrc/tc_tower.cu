@@ -14,6 +14,7 @@
 #include <mutex>
 
 #include "kernels.h"
+#include "tc_fused.cuh"
 #include "tc_gemm.cuh"
 
 namespace sfb {
@@ -157,7 +158,138 @@ void split_k(int tiles, int nkb, int* splits, int* kps) {
   *splits = (nkb + *kps - 1) / *kps;
 }
 
+// ---------------- fused path (tc_fused.cuh) ----------------
+
+// W1 [K x H] packed -> hi/lo of the padded-field layouts: W1p [Kp x ldh], W1p^T [H x Kp]
+__global__ void prep_w1_padded_kernel(const float* __restrict__ w1, int F, int d, int dp, int H,
+                                      int ldh, int Kp, float* __restrict__ w_hi,
+                                      float* __restrict__ w_lo, float* __restrict__ wt_hi,
+                                      float* __restrict__ wt_lo) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<int64_t>(F) * d * H) return;
+  const int k = static_cast<int>(i / H), j = static_cast<int>(i % H);
+  const int kp = (k / d) * dp + (k % d);
+  const float v = w1[i];
+  const float h = rna(v), l = rna(v - h);
+  w_hi[static_cast<int64_t>(kp) * ldh + j] = h;
+  w_lo[static_cast<int64_t>(kp) * ldh + j] = l;
+  wt_hi[static_cast<int64_t>(j) * Kp + kp] = h;
+  wt_lo[static_cast<int64_t>(j) * Kp + kp] = l;
+}
+
+// dW1 [K x H] (packed) = sum_z part[z][kp(k)][:] in a fixed order (+= when accumulating)
+__global__ void dw1_reduce_padded_kernel(const float* __restrict__ part, int splits, int F, int d,
+                                         int dp, int H, float* __restrict__ out, int accumulate) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t n = static_cast<int64_t>(F) * d * H;
+  if (i >= n) return;
+  const int k = static_cast<int>(i / H), j = static_cast<int>(i % H);
+  const int64_t kp = (k / d) * dp + (k % d);
+  const int64_t ps = static_cast<int64_t>(F) * dp * H;
+  float s = 0.f;
+  for (int q = 0; q < splits; ++q) s += part[q * ps + kp * H + j];
+  out[i] = accumulate ? out[i] + s : s;
+}
+
+// Warp per row: sums the split-K partials of the gathered forward GEMM, gathers
+// the row's F embeddings through vid for the FM term (sum and sum of squares,
+// fm_s written for the scatter epilogue), then the DeepFM-lite head as in head_tc.
+__global__ void head_fused_kernel(int rows, int F, int d, int H, const float* __restrict__ part,
+                                  int splits, long long split_stride,
+                                  const uint32_t* __restrict__ vid, const float* __restrict__ G,
+                                  const float* __restrict__ b1, const float* __restrict__ w2,
+                                  const float* __restrict__ b2p,
+                                  const uint8_t* __restrict__ labels, float inv_rows,
+                                  float* __restrict__ logits, float* __restrict__ act,
+                                  float* __restrict__ dh, float* __restrict__ gz,
+                                  float* __restrict__ lossr, float* __restrict__ fm_s,
+                                  float* __restrict__ dh_hi, float* __restrict__ dh_lo, int ldh) {
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const int d4 = d >> 2;
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  float sq = 0.f;
+  const uint32_t* vr = vid + static_cast<int64_t>(r) * F;
+  for (int f = 0; f < F; ++f) {
+    const float4* g = reinterpret_cast<const float4*>(G + static_cast<int64_t>(__ldg(vr + f)) * d);
+    for (int c = lane; c < d4; c += 32) {  // d <= 128: lanes own fixed 16 B columns
+      const float4 a = __ldg(g + c);
+      s.x += a.x; s.y += a.y; s.z += a.z; s.w += a.w;
+      sq += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w;
+    }
+  }
+  float ss = s.x * s.x + s.y * s.y + s.z * s.z + s.w * s.w;
+  if (lane < d4) reinterpret_cast<float4*>(fm_s + static_cast<int64_t>(r) * d)[lane] = s;
+  float mlp = 0.f;
+  for (int j = lane; j < H; j += 32) {
+    float h = b1[j];
+    for (int z = 0; z < splits; ++z) h += part[z * split_stride + static_cast<long long>(r) * H + j];
+    act[static_cast<int64_t>(r) * H + j] = h;
+    mlp += fmaxf(h, 0.f) * w2[j];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mlp += __shfl_xor_sync(0xFFFFFFFFu, mlp, o);
+    ss += __shfl_xor_sync(0xFFFFFFFFu, ss, o);
+    sq += __shfl_xor_sync(0xFFFFFFFFu, sq, o);
+  }
+  const float z = 0.5f * (ss - sq) + (mlp + __ldg(b2p));
+  const float p = 1.f / (1.f + expf(-z));
+  const float y = labels[r] ? 1.f : 0.f;
+  constexpr float kClamp = 1e-7f;
+  const bool clamped = (p < kClamp) || (p > 1.f - kClamp);
+  const float pc = fminf(fmaxf(p, kClamp), 1.f - kClamp);
+  const float g = clamped ? 0.f : (p - y) * inv_rows;
+  for (int j = lane; j < H; j += 32) {
+    const int64_t o = static_cast<int64_t>(r) * H + j;
+    const float hv = act[o];
+    act[o] = fmaxf(hv, 0.f);
+    const float dv = hv > 0.f ? g * w2[j] : 0.f;
+    dh[o] = dv;
+    const float h = rna(dv), l = rna(dv - h);
+    dh_hi[static_cast<int64_t>(r) * ldh + j] = h;
+    dh_lo[static_cast<int64_t>(r) * ldh + j] = l;
+  }
+  if (lane == 0) {
+    logits[r] = z;
+    gz[r] = g;
+    lossr[r] = -(y * logf(pc) + (1.f - y) * log1pf(-pc));
+  }
+}
+
+template <bool A_MN>
+void launch_gather_gemm(dim3 grid, const CUtensorMap& bhi, const CUtensorMap& blo,
+                        const tc::FusedParams& p, cudaStream_t s) {
+  auto kern = tc::gather_gemm_kernel<A_MN>;
+  constexpr int smem = tc::Layout<64>::SMEM;
+  static bool configured = false;
+  if (!configured) {
+    CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = true;
+  }
+  kern<<<grid, tc::kFusedThreads, smem, s>>>(bhi, blo, p);
+  CUDA_LAUNCH_CHECK();
+}
+
+template <int BN>
+void launch_scatter_gemm(dim3 grid, const CUtensorMap& ah, const CUtensorMap& al,
+                         const CUtensorMap& bh, const CUtensorMap& bl, const tc::FusedParams& p,
+                         cudaStream_t s) {
+  auto kern = tc::scatter_gemm_kernel<BN>;
+  constexpr int smem = tc::Layout<BN, 2>::SMEM;
+  static bool configured = false;
+  if (!configured) {
+    CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = true;
+  }
+  kern<<<grid, 192, smem, s>>>(ah, al, bh, bl, p);
+  CUDA_LAUNCH_CHECK();
+}
+
 }  // namespace
+
+bool tower_fused_supported(int d) { return d % 4 == 0 && d <= 128; }
 
 void TowerTC::init(int rc, int k, int h, int d_) {
   release();
@@ -168,22 +300,32 @@ void TowerTC::init(int rc, int k, int h, int d_) {
   ldk = round_up(K, 4);
   ldh = round_up(H, 4);
   ldr = round_up(rc, 4);
-  const int nkb1 = (K + tc::BKE - 1) / tc::BKE;
-  int kps;
-  split_k(((rc + 127) / 128) * ((H + 63) / 64), nkb1, &s1_max, &kps);
+  // padded-field layout of the fused path: field f at [f*dp, f*dp + d), dp = round_up(d, 32)
+  dp = round_up(d, 32);
+  Kp = (K / d) * dp;
+  const int kmax = std::max(ldk, Kp);
+  int kps, s_a, s_b;
+  split_k(((rc + 127) / 128) * ((H + 63) / 64), (K + tc::BKE - 1) / tc::BKE, &s_a, &kps);
+  split_k(((rc + 127) / 128) * ((H + 63) / 64), (Kp + tc::BKE - 1) / tc::BKE, &s_b, &kps);
+  s1_max = std::max(s_a, s_b);
   const int nkb3 = (rc + tc::BKE - 1) / tc::BKE;
-  split_k(((K + 127) / 128) * ((H + 63) / 64), nkb3, &s3_max, &kps);
+  split_k(((K + 127) / 128) * ((H + 63) / 64), nkb3, &s_a, &kps);
+  split_k(((Kp + 127) / 128) * ((H + 63) / 64), nkb3, &s_b, &kps);
+  s3_max = std::max(s_a, s_b);
   auto alloc = [](float** p, size_t n) { CUDA_CHECK(cudaMalloc(p, sizeof(float) * std::max<size_t>(n, 1))); };
-  alloc(&w_hi, static_cast<size_t>(K) * ldh);
-  alloc(&w_lo, static_cast<size_t>(K) * ldh);
-  alloc(&wt_hi, static_cast<size_t>(H) * ldk);
-  alloc(&wt_lo, static_cast<size_t>(H) * ldk);
+  alloc(&w_hi, static_cast<size_t>(kmax) * ldh);
+  alloc(&w_lo, static_cast<size_t>(kmax) * ldh);
+  alloc(&wt_hi, static_cast<size_t>(H) * kmax);
+  alloc(&wt_lo, static_cast<size_t>(H) * kmax);
   alloc(&dh_hi, static_cast<size_t>(rc) * ldh);
   alloc(&dh_lo, static_cast<size_t>(rc) * ldh);
   alloc(&part1, static_cast<size_t>(s1_max) * rc * H);
-  alloc(&part3, static_cast<size_t>(s3_max) * K * H);
-  CUDA_CHECK(cudaMemset(w_hi, 0, sizeof(float) * K * ldh));
-  CUDA_CHECK(cudaMemset(w_lo, 0, sizeof(float) * K * ldh));
+  alloc(&part3, static_cast<size_t>(s3_max) * kmax * H);
+  // zero once: padding rows / columns of the W1 parts are never written
+  for (float* p : {w_hi, w_lo})
+    CUDA_CHECK(cudaMemset(p, 0, sizeof(float) * static_cast<size_t>(kmax) * ldh));
+  for (float* p : {wt_hi, wt_lo})
+    CUDA_CHECK(cudaMemset(p, 0, sizeof(float) * static_cast<size_t>(H) * kmax));
 }
 
 void TowerTC::release() {
@@ -290,6 +432,118 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc_, const float* X, int l
   }
   const int64_t kh = static_cast<int64_t>(K) * H;
   dw1_reduce(tc_.part3, s3, kh, g_w1, accumulate, s);
+  small_grads(t, rows, H, g_b1, g_w2, g_b2, g_loss, accumulate, s);
+}
+
+void tower_forward_backward_fused(TowerBufs& t, TowerTC& tc_, const float* G, const uint32_t* vid,
+                                  const uint8_t* labels, int32_t rows, int F, int d,
+                                  const float* dense, float* logits, float* fm_s, float emb_scale,
+                                  float* dG, float* grads, bool accumulate, cudaStream_t s) {
+  const int K = F * d, H = t.H;
+  const int dp = tc_.dp, Kp = tc_.Kp;
+  SFB_CHECK(tower_fused_supported(d) && rows <= tc_.rows_cap && K == tc_.K,
+            "fused tower: unsupported shape");
+  const float* w1 = dense;
+  const float* b1 = dense + static_cast<size_t>(K) * H;
+  const float* w2 = b1 + H;
+  const float* b2p = w2 + H;
+  float* g_w1 = grads;
+  float* g_b1 = grads + static_cast<size_t>(K) * H;
+  float* g_w2 = g_b1 + H;
+  float* g_b2 = g_w2 + H;
+  float* g_loss = g_b2 + 1;
+
+  prep_w1_padded_kernel<<<ceil_div(static_cast<int64_t>(K) * H, 256), 256, 0, s>>>(
+      w1, F, d, dp, H, tc_.ldh, Kp, tc_.w_hi, tc_.w_lo, tc_.wt_hi, tc_.wt_lo);
+  CUDA_LAUNCH_CHECK();
+
+  tc::FusedParams p{};
+  p.rows = rows;
+  p.F = F;
+  p.d = d;
+  p.dp = dp;
+  p.H = H;
+  p.vid = vid;
+  p.G = G;
+  p.fm_s = fm_s;
+  p.gz = t.gz;
+  p.scale = emb_scale;
+  p.dG = dG;
+
+  // ---- gathered forward GEMM: hpre partials = G[vid] W1 (split-K over fields)
+  const int mt = (rows + 127) / 128, nt = (H + 63) / 64;
+  const int nkb1 = Kp / tc::BKE;
+  int s1, kps1;
+  split_k(mt * nt, nkb1, &s1, &kps1);
+  {
+    const CUtensorMap bh = tmap(tc_.wt_hi, Kp, H, Kp, 32, 64);
+    const CUtensorMap bl = tmap(tc_.wt_lo, Kp, H, Kp, 32, 64);
+    tc::FusedParams q = p;
+    q.num_k_blocks = nkb1;
+    q.k_blocks_per_split = kps1;
+    q.out = tc_.part1;
+    q.ldo = H;
+    q.split_stride = static_cast<long long>(rows) * H;
+    launch_gather_gemm<false>(dim3(mt, nt, s1), bh, bl, q, s);
+  }
+  // ---- head: DeepFM-lite with the FM sums gathered through vid
+  head_fused_kernel<<<ceil_div(static_cast<int64_t>(rows) * 32, 256), 256, 0, s>>>(
+      rows, F, d, H, tc_.part1, s1, static_cast<long long>(rows) * H, vid, G, b1, w2, b2p, labels,
+      1.f / rows, logits, t.act, t.dh, t.gz, t.lossr, fm_s, tc_.dh_hi, tc_.dh_lo, tc_.ldh);
+  CUDA_LAUNCH_CHECK();
+  // ---- dX GEMM with the FM term + segment sum in the epilogue (one field per N tile)
+  {
+    const CUtensorMap ah = tmap(tc_.dh_hi, H, rows, tc_.ldh, 32, 128);
+    const CUtensorMap al = tmap(tc_.dh_lo, H, rows, tc_.ldh, 32, 128);
+    tc::FusedParams q = p;
+    q.num_k_blocks = (H + tc::BKE - 1) / tc::BKE;
+    const dim3 grid(mt, F);
+    switch (dp) {
+      case 32: {
+        const CUtensorMap bh = tmap(tc_.w_hi, H, Kp, tc_.ldh, 32, 32);
+        const CUtensorMap bl = tmap(tc_.w_lo, H, Kp, tc_.ldh, 32, 32);
+        launch_scatter_gemm<32>(grid, ah, al, bh, bl, q, s);
+        break;
+      }
+      case 64: {
+        const CUtensorMap bh = tmap(tc_.w_hi, H, Kp, tc_.ldh, 32, 64);
+        const CUtensorMap bl = tmap(tc_.w_lo, H, Kp, tc_.ldh, 32, 64);
+        launch_scatter_gemm<64>(grid, ah, al, bh, bl, q, s);
+        break;
+      }
+      case 96: {
+        const CUtensorMap bh = tmap(tc_.w_hi, H, Kp, tc_.ldh, 32, 96);
+        const CUtensorMap bl = tmap(tc_.w_lo, H, Kp, tc_.ldh, 32, 96);
+        launch_scatter_gemm<96>(grid, ah, al, bh, bl, q, s);
+        break;
+      }
+      default: {
+        const CUtensorMap bh = tmap(tc_.w_hi, H, Kp, tc_.ldh, 32, 128);
+        const CUtensorMap bl = tmap(tc_.w_lo, H, Kp, tc_.ldh, 32, 128);
+        launch_scatter_gemm<128>(grid, ah, al, bh, bl, q, s);
+        break;
+      }
+    }
+  }
+  // ---- gathered dW1 GEMM: partials = G[vid]^T dh (MN-major A and B), split-K over rows
+  const int nkb3 = (rows + tc::BKE - 1) / tc::BKE;
+  const int mt3 = (Kp + 127) / 128;
+  int s3, kps3;
+  split_k(mt3 * nt, nkb3, &s3, &kps3);
+  {
+    const CUtensorMap bh = tmap(tc_.dh_hi, H, rows, tc_.ldh, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    const CUtensorMap bl = tmap(tc_.dh_lo, H, rows, tc_.ldh, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    tc::FusedParams q = p;
+    q.num_k_blocks = nkb3;
+    q.k_blocks_per_split = kps3;
+    q.out = tc_.part3;
+    q.ldo = H;
+    q.split_stride = static_cast<long long>(Kp) * H;
+    launch_gather_gemm<true>(dim3(mt3, nt, s3), bh, bl, q, s);
+  }
+  dw1_reduce_padded_kernel<<<ceil_div(static_cast<int64_t>(K) * H, 256), 256, 0, s>>>(
+      tc_.part3, s3, F, d, dp, H, g_w1, accumulate ? 1 : 0);
+  CUDA_LAUNCH_CHECK();
   small_grads(t, rows, H, g_b1, g_w2, g_b2, g_loss, accumulate, s);
 }
 

@@ -147,6 +147,9 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
   // validation switch: the fp32 SIMT tiles instead of tcgen05 (only when rows are unpadded)
   const char* ts = std::getenv("SFCTR_TOWER_SIMT");
   tower_simt_ = ts && ts[0] == '1' && ldx_ == K_;
+  // fused gather/GEMM/scatter tower unless disabled (SFCTR_TOWER_UNFUSED=1, for A/B runs)
+  const char* tu = std::getenv("SFCTR_TOWER_UNFUSED");
+  tower_fused_ = !tower_simt_ && tower_fused_supported(d_) && !(tu && tu[0] == '1');
 
   const uint64_t owned_rows = (cfg_.vocabulary_size + W_ - 1) / W_;
   const uint64_t host_rows = cfg_.host_table_rows ? cfg_.host_table_rows : owned_rows;
@@ -398,6 +401,13 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
     const uint32_t* vid =
         a2a_ ? d_lvid_ : d_vid_ + static_cast<size_t>(lane0_ + l) * b_ * F_;
     const uint8_t* lab = d_labels + static_cast<size_t>(l) * b_;
+    if (tower_fused_) {  // gather -> GEMM -> scatter-add, X / dX never materialised
+      tower_forward_backward_fused(tower_, towertc_, d_G_, vid, lab, b_, F_, d_, d_dense_,
+                                   d_logits_ + static_cast<size_t>(l) * b_, d_fm_s_, emb_scale,
+                                   d_dG_, d_grads_, l > 0, s);
+      phase("tower_fused");
+      continue;
+    }
     gather_instances(vid, b_, F_, d_, ldx_, d_G_, d_X_, d_fm_s_, d_fm_sqp_, s);
     phase("gather_instances");
     if (tower_simt_)

@@ -104,6 +104,7 @@ class Trainer {
   int32_t* h_totals_ = nullptr;   // pinned [16] exchange plan totals
   int ldx_ = 0;
   bool tower_simt_ = false;
+  bool tower_fused_ = false;
   int64_t dense_steps_ = 0;
   int64_t steps_done_ = 0;
   int64_t led_[4] = {0, 0, 0, 0};
