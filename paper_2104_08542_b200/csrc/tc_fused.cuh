@@ -177,46 +177,48 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   } else {
     // ---------------- gather + split producers (8 warps), then epilogue (warps 2..5)
     const int t = threadIdx.x - 64;  // 0..255
+    // thread geometry. K-major (forward): tile row t%128, 16 of the block's 32
+    // columns (half t/128). MN-major (dW1): k-row t/8 (a batch row), 16 m-columns
+    // of atom (t%8)/2 (half t%2).
+    const int g_rr = t & 127, g_half_k = t >> 7;
+    const int g_kk = t >> 3, g_a = (t & 7) >> 1, g_half_m = t & 1;
+    auto fetch = [&](int i, float4 (&x)[4]) {
+      const int kb = kb0 + i;
+      int r, f, c0;
+      if constexpr (!A_MN) {
+        r = m0 + g_rr;
+        const int kcol = kb * BKE;  // padded column
+        f = kcol / p.dp;
+        c0 = kcol - f * p.dp + 16 * g_half_k;
+      } else {
+        r = kb * BKE + g_kk;
+        const int mcol = m0 + g_a * 32 + 16 * g_half_m;  // padded column
+        f = mcol / p.dp;
+        c0 = mcol - f * p.dp;
+      }
+      const bool valid = r < p.rows && f < p.F;
+      const uint32_t v = valid ? __ldg(p.vid + static_cast<int64_t>(r) * p.F + f) : 0u;
+      load_seg16(p.G, p.d, valid, v, c0, x);
+    };
+    float4 xa[4], xb[4];
+    if (nkb > 0) fetch(0, xa);
     for (int i = 0; i < nkb; ++i) {
+      if (i + 1 < nkb) fetch(i + 1, xb);  // next block's gathers in flight during this one
       const int s = i % ST;
       mbar_wait(empty + s, ((i / ST) & 1) ^ 1);
-      const int kb = kb0 + i;
-      float4 x[4], lo[4];
-      if constexpr (!A_MN) {
-        // row t%128 of the tile, 16 columns: half t/128 of the 32-wide block
-        const int rr = t & 127, half = t >> 7;
-        const int r = m0 + rr;
-        const int kcol = kb * BKE;  // padded column
-        const int f = kcol / p.dp, c0 = kcol - f * p.dp + 16 * half;
-        const bool valid = r < p.rows && f < p.F;
-        const uint32_t v = valid ? __ldg(p.vid + static_cast<int64_t>(r) * p.F + f) : 0u;
-        load_seg16(p.G, p.d, valid, v, c0, x);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float4 h = split_hi(x[q], lo[q]);
-          const uint32_t off = kmajor_off(rr, 4 * half + q);
-          *reinterpret_cast<float4*>(a_hi(s) + off) = h;
-          *reinterpret_cast<float4*>(a_lo(s) + off) = lo[q];
-        }
-      } else {
-        // k-row kk = t/8 (a batch row), 16 m-columns: atom (t%8)/2, half t%2
-        const int kk = t >> 3, a = (t & 7) >> 1, half = t & 1;
-        const int r = kb * BKE + kk;
-        const int mcol = m0 + a * 32 + 16 * half;  // padded column
-        const int f = mcol / p.dp, c0 = mcol - f * p.dp;
-        const bool valid = r < p.rows && f < p.F;
-        const uint32_t v = valid ? __ldg(p.vid + static_cast<int64_t>(r) * p.F + f) : 0u;
-        load_seg16(p.G, p.d, valid, v, c0, x);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float4 h = split_hi(x[q], lo[q]);
-          const uint32_t off = mnmajor_off(a * 32 + 16 * half + 4 * q, kk);
-          *reinterpret_cast<float4*>(a_hi(s) + off) = h;
-          *reinterpret_cast<float4*>(a_lo(s) + off) = lo[q];
-        }
+      for (int q = 0; q < 4; ++q) {
+        float4 lo;
+        const float4 h = split_hi(xa[q], lo);
+        const uint32_t off = A_MN ? mnmajor_off(g_a * 32 + 16 * g_half_m + 4 * q, g_kk)
+                                  : kmajor_off(g_rr, 4 * g_half_k + q);
+        *reinterpret_cast<float4*>(a_hi(s) + off) = h;
+        *reinterpret_cast<float4*>(a_lo(s) + off) = lo;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(readyA + s);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) xa[q] = xb[q];
     }
     if (warp < 6) {  // ---------------- epilogue (TMEM lane quarter = warp % 4)
       mbar_wait(tmem_full, 0);
@@ -338,36 +340,64 @@ __global__ void __launch_bounds__(192, 1)
       mma_commit(tmem_full);
     }
   } else {
-    // ---------------- epilogue: row per thread, FM term + scatter-add into dG
+    // ---------------- epilogue: TMEM -> smem tile, then row by row (lanes on
+    // consecutive 16 B of one row, as in segment_sum) FM term + scatter-add into dG
     mbar_wait(tmem_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const int q = warp & 3;
-    const int rr = q * 32 + lane;
-    const int r = m0 + rr;
     const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
-    const bool live = r < p.rows && nkb > 0;
-    const uint32_t v = live ? __ldg(p.vid + static_cast<int64_t>(r) * p.F + f) : 0u;
-    const float k = live ? p.scale * __ldg(p.gz + r) : 0.f;
-    const float4* S = reinterpret_cast<const float4*>(p.fm_s + static_cast<int64_t>(r) * p.d);
-    const float4* Gv = reinterpret_cast<const float4*>(p.G + static_cast<int64_t>(v) * p.d);
-    float* dst = p.dG + static_cast<int64_t>(v) * p.d;
+    float* tile = reinterpret_cast<float*>(smem);  // ring is free: all MMAs completed
+    constexpr int TS = BN + 1;
+    {
+      const int rr = q * 32 + lane;
 #pragma unroll 1
-    for (int c0 = 0; c0 < p.d; c0 += 16) {
-      float a[16];
-      tmem_ld16(trow + c0, a);  // columns past d exist in TMEM (BN >= d) and are ignored
-      if (!live) continue;
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        float a[16];
+        tmem_ld16(trow + c0, a);
 #pragma unroll
-      for (int j = 0; j < 16; j += 4) {
-        const int c = c0 + j;
-        if (c >= p.d) break;
-        const float4 s4 = __ldg(S + (c >> 2));
-        const float4 g4 = __ldg(Gv + (c >> 2));
-        asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + c),
-                     "f"(p.scale * a[j] + k * (s4.x - g4.x)),
-                     "f"(p.scale * a[j + 1] + k * (s4.y - g4.y)),
-                     "f"(p.scale * a[j + 2] + k * (s4.z - g4.z)),
-                     "f"(p.scale * a[j + 3] + k * (s4.w - g4.w))
-                     : "memory");
+        for (int j = 0; j < 16; ++j) tile[rr * TS + c0 + j] = a[j];
+      }
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    const int d4 = p.d >> 2;
+    const int w2 = warp - 2;
+    if (nkb > 0) {
+      // warp w2 owns tile rows w2 + 4 i (i < 32): lane i fetches row i's vid / gz once,
+      // then rows go 4 at a time with their G / fm_s loads all in flight
+      const int my_r = m0 + w2 + 4 * lane;
+      const bool my_live = my_r < p.rows;
+      const uint32_t my_v = my_live ? __ldg(p.vid + static_cast<int64_t>(my_r) * p.F + f) : 0u;
+      const float my_k = my_live ? p.scale * __ldg(p.gz + my_r) : 0.f;
+#pragma unroll 1
+      for (int i0 = 0; i0 < 32; i0 += 4) {
+        uint32_t vv[4];
+        float kk[4];
+        float4 s4[4], g4[4];
+        bool ok[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + u;
+          vv[u] = __shfl_sync(0xFFFFFFFFu, my_v, i);
+          kk[u] = __shfl_sync(0xFFFFFFFFu, my_k, i);
+          const int r = m0 + w2 + 4 * i;
+          ok[u] = r < p.rows && lane < d4;
+          if (ok[u]) {
+            s4[u] = __ldg(reinterpret_cast<const float4*>(p.fm_s + static_cast<int64_t>(r) * p.d) + lane);
+            g4[u] = __ldg(reinterpret_cast<const float4*>(p.G + static_cast<int64_t>(vv[u]) * p.d) + lane);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (!ok[u]) continue;
+          const float* a = tile + (w2 + 4 * (i0 + u)) * TS + 4 * lane;
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(
+                           p.dG + static_cast<int64_t>(vv[u]) * p.d + 4 * lane),
+                       "f"(p.scale * a[0] + kk[u] * (s4[u].x - g4[u].x)),
+                       "f"(p.scale * a[1] + kk[u] * (s4[u].y - g4[u].y)),
+                       "f"(p.scale * a[2] + kk[u] * (s4[u].z - g4[u].z)),
+                       "f"(p.scale * a[3] + kk[u] * (s4[u].w - g4[u].w))
+                       : "memory");
+        }
       }
     }
   }

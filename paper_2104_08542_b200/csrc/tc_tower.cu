@@ -211,12 +211,24 @@ __global__ void head_fused_kernel(int rows, int F, int d, int H, const float* __
   float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
   float sq = 0.f;
   const uint32_t* vr = vid + static_cast<int64_t>(r) * F;
-  for (int f = 0; f < F; ++f) {
-    const float4* g = reinterpret_cast<const float4*>(G + static_cast<int64_t>(__ldg(vr + f)) * d);
-    for (int c = lane; c < d4; c += 32) {  // d <= 128: lanes own fixed 16 B columns
-      const float4 a = __ldg(g + c);
-      s.x += a.x; s.y += a.y; s.z += a.z; s.w += a.w;
-      sq += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w;
+  // lane f < F fetches vid[r, f] once; rows then go 4 at a time (d <= 128: lane c
+  // owns the fixed 16 B column c of every row), all 4 gathers in flight
+  const uint32_t my_v = lane < F ? __ldg(vr + lane) : 0u;
+  for (int f0 = 0; f0 < F; f0 += 4) {
+    float4 a[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int f = f0 + u;
+      const uint32_t v = f < 32 ? __shfl_sync(0xFFFFFFFFu, my_v, f & 31)
+                                : (f < F ? __ldg(vr + f) : 0u);
+      a[u] = (f < F && lane < d4)
+                 ? __ldg(reinterpret_cast<const float4*>(G + static_cast<int64_t>(v) * d) + lane)
+                 : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      s.x += a[u].x; s.y += a[u].y; s.z += a[u].z; s.w += a[u].w;
+      sq += a[u].x * a[u].x + a[u].y * a[u].y + a[u].z * a[u].z + a[u].w * a[u].w;
     }
   }
   float ss = s.x * s.x + s.y * s.y + s.z * s.z + s.w * s.w;
