@@ -76,10 +76,11 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc, const float* X, int ld
 // operands and dX is scatter-added into dG (with the FM term) by the dX GEMM's
 // epilogue; neither touches HBM. Writes fm_s [rows x d]. Needs d % 4 == 0, d <= 128.
 bool tower_fused_supported(int d);
-void tower_forward_backward_fused(TowerBufs& t, TowerTC& tc, const float* G, const uint32_t* vid,
-                                  const uint8_t* labels, int32_t rows, int F, int d,
-                                  const float* dense, float* logits, float* fm_s, float emb_scale,
-                                  float* dG, float* grads, bool accumulate, cudaStream_t s);
+void tower_forward_backward_fused(TowerBufs& t, TowerTC& tc, const float* G, int64_t g_rows,
+                                  const uint32_t* vid, const uint8_t* labels, int32_t rows, int F,
+                                  int d, const float* dense, float* logits, float* fm_s,
+                                  float emb_scale, float* dG, float* grads, bool accumulate,
+                                  cudaStream_t s);
 // fp32 SIMT reference tiles of the same tower (validation only; needs ldx == K)
 void tower_forward_backward_simt(TowerBufs& t, const float* X, const float* fm_s,
                                  const float* fm_sqp, const uint8_t* labels, int32_t rows, int F,

@@ -410,5 +410,211 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
+// TMA row gather: 4 rows (by index) x one 32-float box of the 2D table G into
+// 4 consecutive 128 B smem rows (the tensor map's swizzle applies).
+__device__ __forceinline__ void tma_gather4(const CUtensorMap* map, uint64_t* bar, void* dst,
+                                            int col, uint32_t r0, uint32_t r1, uint32_t r2,
+                                            uint32_t r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(col), "r"(r0), "r"(r1),
+      "r"(r2), "r"(r3)
+      : "memory");
+}
+
+// Gathered-A GEMM with the gather done by TMA (tile::gather4 on the table G):
+// the producer warp issues 32 gather4 per k-block (one per lane, 4 rows each)
+// plus the B tiles; 4 split warps turn the raw tile into tf32 hi/lo parts in
+// place; one elected lane issues tcgen05.mma; the split warps then run the
+// epilogue (split-K partials). A_MN = false: forward (rows x K_pad) . W1p;
+// A_MN = true: dW1 (K_pad x rows) . dh.
+template <bool A_MN>
+__global__ void __launch_bounds__(192, 1)
+    gather4_gemm_kernel(const __grid_constant__ CUtensorMap tmG,
+                        const __grid_constant__ CUtensorMap tmBhi,
+                        const __grid_constant__ CUtensorMap tmBlo, const FusedParams p) {
+  constexpr int BN = 64;
+  using L = Layout<BN>;
+  constexpr int ST = L::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * L::STAGE_BYTES);
+  uint64_t* ready = full + ST;
+  uint64_t* empty = ready + ST;
+  uint64_t* tmem_full = empty + ST;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  auto a_hi = [&](int s) { return smem + s * L::STAGE_BYTES; };
+  auto a_lo = [&](int s) { return smem + s * L::STAGE_BYTES + A_BYTES; };
+  auto b_hi = [&](int s) { return smem + s * L::STAGE_BYTES + 2 * A_BYTES; };
+  auto b_lo = [&](int s) { return smem + s * L::STAGE_BYTES + 2 * A_BYTES + L::B_BYTES; };
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int kb0 = blockIdx.z * p.k_blocks_per_split;
+  const int kb1 = min(p.num_k_blocks, kb0 + p.k_blocks_per_split);
+  const int nkb = kb1 - kb0;
+  const int M = A_MN ? p.F * p.dp : p.rows;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(ready + s, 128);
+      mbar_init(empty + s, 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_holder)),
+                 "n"(L::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    // ---------------- producer warp: 32 x gather4 (A) + B tiles per k-block
+    // lane geometry: forward: rows m0 + 4 lane .. +3 (one field per k-block);
+    // dW1: atom a = lane / 8 (32 m-columns), batch rows 4 (lane % 8) .. +3 of the block
+    auto rows_for = [&](int i, uint32_t (&v)[4], int& col) {
+      const int kb = kb0 + i;
+      int f, r0;
+      if constexpr (!A_MN) {
+        const int kcol = kb * BKE;
+        f = kcol / p.dp;
+        col = kcol - f * p.dp;
+        r0 = m0 + 4 * lane;
+      } else {
+        const int mcol = m0 + (lane >> 3) * 32;
+        f = mcol / p.dp;
+        col = mcol - f * p.dp;
+        r0 = kb * BKE + 4 * (lane & 7);
+      }
+      const bool fok = f < p.F;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int r = r0 + j;
+        // rows past the batch gather row 0: forward -> masked output rows; dW1 ->
+        // multiplied by the zero-filled dh rows
+        v[j] = (fok && r < p.rows) ? __ldg(p.vid + static_cast<int64_t>(r) * p.F + f) : 0u;
+      }
+    };
+    uint32_t va[4], vb[4];
+    int ca = 0, cb = 0;
+    if (nkb > 0) rows_for(0, va, ca);
+    for (int i = 0; i < nkb; ++i) {
+      if (i + 1 < nkb) rows_for(i + 1, vb, cb);  // next block's row ids in flight
+      const int s = i % ST;
+      if (lane == 0) {
+        mbar_wait(empty + s, ((i / ST) & 1) ^ 1);
+        mbar_expect_tx(full + s, A_BYTES + 2 * L::B_BYTES);
+      }
+      __syncwarp();
+      const uint32_t dst = A_MN ? (lane >> 3) * 4096 + (lane & 7) * 512 : lane * 512;
+      tma_gather4(&tmG, full + s, a_hi(s) + dst, ca, va[0], va[1], va[2], va[3]);
+      if (lane == 0) {
+        const int kc = (kb0 + i) * BKE;
+        if constexpr (A_MN) {
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            tma_load_2d(&tmBhi, full + s, b_hi(s) + b * 4096, n0 + b * 32, kc);
+            tma_load_2d(&tmBlo, full + s, b_lo(s) + b * 4096, n0 + b * 32, kc);
+          }
+        } else {
+          tma_load_2d(&tmBhi, full + s, b_hi(s), kc, n0);
+          tma_load_2d(&tmBlo, full + s, b_lo(s), kc, n0);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) va[j] = vb[j];
+      ca = cb;
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      constexpr uint32_t idesc = idesc_tf32(BM, BN, A_MN ? 1 : 0, A_MN ? 1 : 0);
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % ST;
+        mbar_wait(ready + s, (i / ST) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+        for (int kk = 0; kk < BKE / 8; ++kk) {
+          uint64_t ah, al, bh, bl;
+          if constexpr (A_MN) {
+            ah = smem_desc(smem_u32(a_hi(s)) + kk * 1024, 4096, 512, 1);
+            al = smem_desc(smem_u32(a_lo(s)) + kk * 1024, 4096, 512, 1);
+            bh = smem_desc(smem_u32(b_hi(s)) + kk * 1024, 4096, 512, 1);
+            bl = smem_desc(smem_u32(b_lo(s)) + kk * 1024, 4096, 512, 1);
+          } else {
+            ah = smem_desc(smem_u32(a_hi(s)) + kk * 32, 16, 1024);
+            al = smem_desc(smem_u32(a_lo(s)) + kk * 32, 16, 1024);
+            bh = smem_desc(smem_u32(b_hi(s)) + kk * 32, 16, 1024);
+            bl = smem_desc(smem_u32(b_lo(s)) + kk * 32, 16, 1024);
+          }
+          mma_tf32(tmem, ah, bh, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+          mma_tf32(tmem, ah, bl, idesc, 1u);
+          mma_tf32(tmem, al, bh, idesc, 1u);
+        }
+        mma_commit(empty + s);
+      }
+      mma_commit(tmem_full);
+    }
+  } else {
+    const int t = threadIdx.x - 64;  // 0..127
+    for (int i = 0; i < nkb; ++i) {  // ---------------- in-place 3xTF32 split
+      const int s = i % ST;
+      mbar_wait(full + s, (i / ST) & 1);
+      float4* hi = reinterpret_cast<float4*>(a_hi(s));
+      float4* lo = reinterpret_cast<float4*>(a_lo(s));
+#pragma unroll 4
+      for (int e = t; e < A_BYTES / 16; e += 128) {
+        float4 l;
+        const float4 h = split_hi(hi[e], l);
+        hi[e] = h;
+        lo[e] = l;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(ready + s);
+    }
+    // ---------------- epilogue (split-K partials), staged for coalesced stores
+    mbar_wait(tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
+    float* tile = reinterpret_cast<float*>(smem);
+    constexpr int TS = BN + 1;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 8) {
+      float v[8];
+      tmem_ld8(trow + c0, v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) tile[row * TS + c0 + j] = v[j];
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    const int w2 = t >> 5;
+    if (nkb > 0)
+      for (int rr = w2; rr < BM; rr += 4) {
+        const int m = m0 + rr;
+        if (m >= M) break;
+        float* o = p.out + blockIdx.z * p.split_stride + static_cast<long long>(m) * p.ldo;
+#pragma unroll
+        for (int c = lane; c < BN; c += 32)
+          if (n0 + c < p.H) o[n0 + c] = tile[rr * TS + c];
+      }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(L::TMEM_COLS));
+  }
+}
+
 }  // namespace tc
 }  // namespace sfb

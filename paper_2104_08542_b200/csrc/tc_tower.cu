@@ -271,6 +271,20 @@ __global__ void head_fused_kernel(int rows, int F, int d, int H, const float* __
 }
 
 template <bool A_MN>
+void launch_gather4_gemm(dim3 grid, const CUtensorMap& g, const CUtensorMap& bhi,
+                         const CUtensorMap& blo, const tc::FusedParams& p, cudaStream_t s) {
+  auto kern = tc::gather4_gemm_kernel<A_MN>;
+  constexpr int smem = tc::Layout<64>::SMEM;
+  static bool configured = false;
+  if (!configured) {
+    CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = true;
+  }
+  kern<<<grid, 192, smem, s>>>(g, bhi, blo, p);
+  CUDA_LAUNCH_CHECK();
+}
+
+template <bool A_MN>
 void launch_gather_gemm(dim3 grid, const CUtensorMap& bhi, const CUtensorMap& blo,
                         const tc::FusedParams& p, cudaStream_t s) {
   auto kern = tc::gather_gemm_kernel<A_MN>;
@@ -447,10 +461,16 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc_, const float* X, int l
   small_grads(t, rows, H, g_b1, g_w2, g_b2, g_loss, accumulate, s);
 }
 
-void tower_forward_backward_fused(TowerBufs& t, TowerTC& tc_, const float* G, const uint32_t* vid,
-                                  const uint8_t* labels, int32_t rows, int F, int d,
-                                  const float* dense, float* logits, float* fm_s, float emb_scale,
-                                  float* dG, float* grads, bool accumulate, cudaStream_t s) {
+void tower_forward_backward_fused(TowerBufs& t, TowerTC& tc_, const float* G, int64_t g_rows,
+                                  const uint32_t* vid, const uint8_t* labels, int32_t rows, int F,
+                                  int d, const float* dense, float* logits, float* fm_s,
+                                  float emb_scale, float* dG, float* grads, bool accumulate,
+                                  cudaStream_t s) {
+  // A operand gathers: TMA tile::gather4 (default) or the SM producer warps
+  static const bool gather_tma_ = [] {
+    const char* e = std::getenv("SFCTR_GATHER_SM");
+    return !(e && e[0] == '1');
+  }();
   const int K = F * d, H = t.H;
   const int dp = tc_.dp, Kp = tc_.Kp;
   SFB_CHECK(tower_fused_supported(d) && rows <= tc_.rows_cap && K == tc_.K,
@@ -496,7 +516,12 @@ void tower_forward_backward_fused(TowerBufs& t, TowerTC& tc_, const float* G, co
     q.out = tc_.part1;
     q.ldo = H;
     q.split_stride = static_cast<long long>(rows) * H;
-    launch_gather_gemm<false>(dim3(mt, nt, s1), bh, bl, q, s);
+    if (gather_tma_) {
+      const CUtensorMap g = tmap(G, d, std::max<int64_t>(g_rows, 1), d, 32, 1);
+      launch_gather4_gemm<false>(dim3(mt, nt, s1), g, bh, bl, q, s);
+    } else {
+      launch_gather_gemm<false>(dim3(mt, nt, s1), bh, bl, q, s);
+    }
   }
   // ---- head: DeepFM-lite with the FM sums gathered through vid
   head_fused_kernel<<<ceil_div(static_cast<int64_t>(rows) * 32, 256), 256, 0, s>>>(
@@ -551,7 +576,13 @@ void tower_forward_backward_fused(TowerBufs& t, TowerTC& tc_, const float* G, co
     q.out = tc_.part3;
     q.ldo = H;
     q.split_stride = static_cast<long long>(Kp) * H;
-    launch_gather_gemm<true>(dim3(mt3, nt, s3), bh, bl, q, s);
+    if (gather_tma_) {
+      const CUtensorMap g = tmap(G, d, std::max<int64_t>(g_rows, 1), d, 32, 1,
+                                 CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+      launch_gather4_gemm<true>(dim3(mt3, nt, s3), g, bh, bl, q, s);
+    } else {
+      launch_gather_gemm<true>(dim3(mt3, nt, s3), bh, bl, q, s);
+    }
   }
   dw1_reduce_padded_kernel<<<ceil_div(static_cast<int64_t>(K) * H, 256), 256, 0, s>>>(
       tc_.part3, s3, F, d, dp, H, g_w1, accumulate ? 1 : 0);

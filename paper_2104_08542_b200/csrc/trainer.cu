@@ -402,7 +402,8 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
         a2a_ ? d_lvid_ : d_vid_ + static_cast<size_t>(lane0_ + l) * b_ * F_;
     const uint8_t* lab = d_labels + static_cast<size_t>(l) * b_;
     if (tower_fused_) {  // gather -> GEMM -> scatter-add, X / dX never materialised
-      tower_forward_backward_fused(tower_, towertc_, d_G_, vid, lab, b_, F_, d_, d_dense_,
+      tower_forward_backward_fused(tower_, towertc_, d_G_, static_cast<int64_t>(table_rows), vid,
+                                   lab, b_, F_, d_, d_dense_,
                                    d_logits_ + static_cast<size_t>(l) * b_, d_fm_s_, emb_scale,
                                    d_dG_, d_grads_, l > 0, s);
       phase("tower_fused");
