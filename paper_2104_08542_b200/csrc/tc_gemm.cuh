@@ -380,5 +380,206 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
+// Streaming-A variant with DECOUPLED rings (split A, store epilogue):
+//   raw ring (RS x 16 KB)  : TMA lands raw fp32 A tiles; a slot is released as soon
+//                            as the split warps have read it (not when the MMA is done)
+//   operand ring (OS)      : tf32 hi/lo A parts + B hi/lo (B loaded by TMA when the
+//                            split warps claim the stage), released by tcgen05.commit
+// so DRAM latency is covered by RS raw stages while the split -> MMA hand-off runs
+// on a short ring of its own.
+constexpr int kRawStages = 6;
+constexpr int kOpStages = 2;
+
+template <int BN>
+struct DecLayout {
+  static constexpr int B_BYTES = BN * BKE * 4;
+  static constexpr int OP_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int RAW_BYTES = kRawStages * A_BYTES;
+  static constexpr int TMEM_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
+  static_assert(RAW_BYTES >= BM * (BN + 1) * 4, "epilogue tile must fit the raw ring");
+  static constexpr int SMEM = 1024 + RAW_BYTES + kOpStages * OP_BYTES + 512;
+};
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(192, 1)
+    gemm_tf32x3_dec_kernel(const __grid_constant__ CUtensorMap tmA,
+                           const __grid_constant__ CUtensorMap tmBhi,
+                           const __grid_constant__ CUtensorMap tmBlo, const Params p) {
+  using L = DecLayout<BN>;
+  constexpr int RS = kRawStages, OS = kOpStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* raw = smem;
+  uint8_t* ops = smem + L::RAW_BYTES;
+  uint64_t* raw_full = reinterpret_cast<uint64_t*>(ops + OS * L::OP_BYTES);
+  uint64_t* raw_empty = raw_full + RS;
+  uint64_t* op_bfull = raw_empty + RS;
+  uint64_t* op_ready = op_bfull + OS;
+  uint64_t* op_empty = op_ready + OS;
+  uint64_t* tmem_full = op_empty + OS;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  auto a_raw = [&](int s) { return raw + s * A_BYTES; };
+  auto a_hi = [&](int s) { return ops + s * L::OP_BYTES; };
+  auto a_lo = [&](int s) { return ops + s * L::OP_BYTES + A_BYTES; };
+  auto b_hi = [&](int s) { return ops + s * L::OP_BYTES + 2 * A_BYTES; };
+  auto b_lo = [&](int s) { return ops + s * L::OP_BYTES + 2 * A_BYTES + L::B_BYTES; };
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int kb0 = blockIdx.z * p.k_blocks_per_split;
+  const int kb1 = min(p.num_k_blocks, kb0 + p.k_blocks_per_split);
+  const int nkb = kb1 - kb0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < RS; ++s) {
+      mbar_init(raw_full + s, 1);
+      mbar_init(raw_empty + s, 128);
+    }
+    for (int s = 0; s < OS; ++s) {
+      mbar_init(op_bfull + s, 1);
+      mbar_init(op_ready + s, 128);
+      mbar_init(op_empty + s, 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_holder)),
+                 "n"(L::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- raw A producer, RS stages ahead
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % RS;
+        mbar_wait(raw_empty + s, ((i / RS) & 1) ^ 1);
+        mbar_expect_tx(raw_full + s, A_BYTES);
+        const int kc = (kb0 + i) * BKE;
+        if constexpr (A_MN) {
+#pragma unroll
+          for (int a = 0; a < 4; ++a) tma_load_2d(&tmA, raw_full + s, a_raw(s) + a * 4096, m0 + a * 32, kc);
+        } else {
+          tma_load_2d(&tmA, raw_full + s, a_raw(s), kc, m0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      constexpr uint32_t idesc = idesc_tf32(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % OS;
+        const uint32_t ph = (i / OS) & 1;
+        mbar_wait(op_ready + s, ph);
+        mbar_wait(op_bfull + s, ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+        for (int kk = 0; kk < BKE / 8; ++kk) {
+          uint64_t ah, al, bh, bl;
+          if constexpr (A_MN) {
+            ah = smem_desc(smem_u32(a_hi(s)) + kk * 1024, 4096, 512, 1);
+            al = smem_desc(smem_u32(a_lo(s)) + kk * 1024, 4096, 512, 1);
+          } else {
+            ah = smem_desc(smem_u32(a_hi(s)) + kk * 32, 16, 1024);
+            al = smem_desc(smem_u32(a_lo(s)) + kk * 32, 16, 1024);
+          }
+          if constexpr (B_MN) {
+            bh = smem_desc(smem_u32(b_hi(s)) + kk * 1024, 4096, 512, 1);
+            bl = smem_desc(smem_u32(b_lo(s)) + kk * 1024, 4096, 512, 1);
+          } else {
+            bh = smem_desc(smem_u32(b_hi(s)) + kk * 32, 16, 1024);
+            bl = smem_desc(smem_u32(b_lo(s)) + kk * 32, 16, 1024);
+          }
+          mma_tf32(tmem, ah, bh, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+          mma_tf32(tmem, ah, bl, idesc, 1u);
+          mma_tf32(tmem, al, bh, idesc, 1u);
+        }
+        mma_commit(op_empty + s);
+      }
+      mma_commit(tmem_full);
+    }
+  } else {
+    const int t = threadIdx.x - 64;
+    for (int i = 0; i < nkb; ++i) {  // ---------------- split raw -> operand stage
+      const int s = i % OS;
+      const int r = i % RS;
+      mbar_wait(op_empty + s, ((i / OS) & 1) ^ 1);
+      if (t == 0) {  // claim the operand stage: its B tiles
+        mbar_expect_tx(op_bfull + s, 2 * L::B_BYTES);
+        const int kc = (kb0 + i) * BKE;
+        if constexpr (B_MN) {
+#pragma unroll
+          for (int b = 0; b < BN / 32; ++b) {
+            tma_load_2d(&tmBhi, op_bfull + s, b_hi(s) + b * 4096, n0 + b * 32, kc);
+            tma_load_2d(&tmBlo, op_bfull + s, b_lo(s) + b * 4096, n0 + b * 32, kc);
+          }
+        } else {
+          tma_load_2d(&tmBhi, op_bfull + s, b_hi(s), kc, n0);
+          tma_load_2d(&tmBlo, op_bfull + s, b_lo(s), kc, n0);
+        }
+      }
+      mbar_wait(raw_full + r, (i / RS) & 1);
+      const float4* src = reinterpret_cast<const float4*>(a_raw(r));
+      float4* hi = reinterpret_cast<float4*>(a_hi(s));
+      float4* lo = reinterpret_cast<float4*>(a_lo(s));
+#pragma unroll 4
+      for (int e = t; e < A_BYTES / 16; e += 128) {
+        const float4 v = src[e];
+        float4 h, l;
+        h.x = tf32_rna(v.x); l.x = tf32_rna(v.x - h.x);
+        h.y = tf32_rna(v.y); l.y = tf32_rna(v.y - h.y);
+        h.z = tf32_rna(v.z); l.z = tf32_rna(v.z - h.z);
+        h.w = tf32_rna(v.w); l.w = tf32_rna(v.w - h.w);
+        hi[e] = h;
+        lo[e] = l;
+      }
+      mbar_arrive(raw_empty + r);  // raw slot free for the next TMA
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(op_ready + s);
+    }
+    // ---------------- epilogue (split-K partials) staged through the raw ring
+    mbar_wait(tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
+    float* tile = reinterpret_cast<float*>(raw);
+    constexpr int TS = BN + 1;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 8) {
+      float v[8];
+      tmem_ld8(trow + c0, v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) tile[row * TS + c0 + j] = v[j];
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    const int w2 = t >> 5;
+    if (nkb > 0)
+      for (int rr = w2; rr < BM; rr += 4) {
+        const int m = m0 + rr;
+        if (m >= p.M) break;
+        float* o = p.out + blockIdx.z * p.split_stride + static_cast<long long>(m) * p.ldo;
+#pragma unroll
+        for (int c = lane; c < BN; c += 32) {
+          const int n = n0 + c;
+          if (n < p.N) o[n] = tile[rr * TS + c];
+        }
+      }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(L::TMEM_COLS));
+  }
+}
+
 }  // namespace tc
 }  // namespace sfb

@@ -270,6 +270,20 @@ __global__ void head_fused_kernel(int rows, int F, int d, int H, const float* __
   }
 }
 
+template <int BN, bool A_MN, bool B_MN>
+void launch_dec_gemm(dim3 grid, const CUtensorMap& a, const CUtensorMap& bhi,
+                     const CUtensorMap& blo, const tc::Params& p, cudaStream_t s) {
+  auto kern = tc::gemm_tf32x3_dec_kernel<BN, A_MN, B_MN>;
+  constexpr int smem = tc::DecLayout<BN>::SMEM;
+  static bool configured = false;
+  if (!configured) {
+    CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = true;
+  }
+  kern<<<grid, 192, smem, s>>>(a, bhi, blo, p);
+  CUDA_LAUNCH_CHECK();
+}
+
 template <bool A_MN>
 void launch_gather4_gemm(dim3 grid, const CUtensorMap& g, const CUtensorMap& bhi,
                          const CUtensorMap& blo, const tc::FusedParams& p, cudaStream_t s) {
@@ -403,7 +417,7 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc_, const float* X, int l
     p.out = tc_.part1;
     p.ldo = H;
     p.split_stride = static_cast<long long>(rows) * H;
-    launch_gemm<64, false, true, tc::kEpiStore>(dim3(mt, nt, s1), a, a, bh, bl, p, s);
+    launch_dec_gemm<64, false, false>(dim3(mt, nt, s1), a, bh, bl, p, s);
   }
   // ---- head
   head_tc_kernel<<<ceil_div(static_cast<int64_t>(rows) * 32, 256), 256, 0, s>>>(
@@ -454,7 +468,7 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc_, const float* X, int l
     p.out = tc_.part3;
     p.ldo = H;
     p.split_stride = static_cast<long long>(K) * H;
-    launch_gemm<64, true, true, tc::kEpiStore, true>(dim3(mt3, nt, s3), a, a, bh, bl, p, s);
+    launch_dec_gemm<64, true, true>(dim3(mt3, nt, s3), a, bh, bl, p, s);
   }
   const int64_t kh = static_cast<int64_t>(K) * H;
   dw1_reduce(tc_.part3, s3, kh, g_w1, accumulate, s);

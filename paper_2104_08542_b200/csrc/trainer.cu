@@ -147,9 +147,10 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
   // validation switch: the fp32 SIMT tiles instead of tcgen05 (only when rows are unpadded)
   const char* ts = std::getenv("SFCTR_TOWER_SIMT");
   tower_simt_ = ts && ts[0] == '1' && ldx_ == K_;
-  // fused gather/GEMM/scatter tower unless disabled (SFCTR_TOWER_UNFUSED=1, for A/B runs)
-  const char* tu = std::getenv("SFCTR_TOWER_UNFUSED");
-  tower_fused_ = !tower_simt_ && tower_fused_supported(d_) && !(tu && tu[0] == '1');
+  // fused gather/GEMM/scatter tower (SFCTR_TOWER_FUSED=1): X / dX never touch HBM,
+  // but on B200 the streamed path below is faster today (profiles/), so it is opt-in
+  const char* tf = std::getenv("SFCTR_TOWER_FUSED");
+  tower_fused_ = !tower_simt_ && tower_fused_supported(d_) && tf && tf[0] == '1';
 
   const uint64_t owned_rows = (cfg_.vocabulary_size + W_ - 1) / W_;
   const uint64_t host_rows = cfg_.host_table_rows ? cfg_.host_table_rows : owned_rows;
