@@ -1,0 +1,215 @@
+// Persistent dX GEMM of the tower backward (GEMM2):  dX = scale * dh W1^T
+//   dh [rows x H], W1 [K x H] (both pre-split into tf32 hi/lo, K-major), H <= 64.
+//
+// The contraction is only H = 64 deep while the output is the full [rows x K]
+// activation gradient (102 MB at cfg2), so the kernel is an HBM write stream
+// with a short MMA per tile. The one-tile-per-CTA version paid CTA setup, TMEM
+// allocation and an unoverlapped epilogue for each of the ~3100 tiles. Here one
+// CTA per SM walks a contiguous range of (m, n) tiles in m-major order:
+//   warp 0     : TMA producer — dh hi/lo tile of the current m (64 KB, reloaded only
+//                when m changes) and a 3-deep ring of W1 hi/lo n-tiles (32 KB each)
+//   warp 1     : MMA issuer — per tile 2 k-blocks x 4 x (ah x [bh | bl] N = 128,
+//                al x bh N = 64) into one of two TMEM accumulators (2 x 128 columns)
+//   warps 2..5 : epilogue — tcgen05.ld both accumulator halves, sum, scale, write the
+//                128 x 64 tile into a SWIZZLE_128B staging buffer and TMA-store it
+//                (cp.async.bulk.tensor shared -> global), overlapping the next tile's MMA
+#pragma once
+
+#include "tc_gemm.cuh"
+
+namespace sfb {
+namespace tc {
+
+struct DxLayout {
+  static constexpr int A_PART = BM * BKE * 4;     // 16 KB: 128 rows x 32 k
+  static constexpr int A_BYTES = 4 * A_PART;      // hi kb0, hi kb1, lo kb0, lo kb1
+  static constexpr int B_PART = 64 * BKE * 4;     // 8 KB: 64 n x 32 k
+  static constexpr int B_STAGE = 4 * B_PART;      // kb0 [hi; lo], kb1 [hi; lo]
+  static constexpr int B_STAGES = 3;
+  static constexpr int OUT_BYTES = BM * 64 * 4;   // 32 KB staging (2 boxes of 32 columns)
+  static constexpr int SMEM = 1024 + A_BYTES + B_STAGES * B_STAGE + OUT_BYTES + 256;
+};
+
+struct DxParams {
+  int M, N;       // rows, K (columns of dX)
+  int n_tiles;    // ceil(N / 64)
+  int tiles;      // ceil(M / 128) * n_tiles
+  float scale;
+};
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(x), "r"(y)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(192, 1)
+    gemm_dx_persistent_kernel(const __grid_constant__ CUtensorMap tmAhi,
+                              const __grid_constant__ CUtensorMap tmAlo,
+                              const __grid_constant__ CUtensorMap tmBhi,
+                              const __grid_constant__ CUtensorMap tmBlo,
+                              const __grid_constant__ CUtensorMap tmOut, const DxParams p) {
+  using L = DxLayout;
+  constexpr int BS = L::B_STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* a_s = smem;
+  uint8_t* b_s = smem + L::A_BYTES;
+  uint8_t* out_s = b_s + BS * L::B_STAGE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(out_s + L::OUT_BYTES);
+  uint64_t* a_full = bars;
+  uint64_t* a_empty = bars + 1;
+  uint64_t* b_full = bars + 2;
+  uint64_t* b_empty = b_full + BS;
+  uint64_t* acc_full = b_empty + BS;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t0 = static_cast<int>(static_cast<long long>(blockIdx.x) * p.tiles / gridDim.x);
+  const int t1 = static_cast<int>(static_cast<long long>(blockIdx.x + 1) * p.tiles / gridDim.x);
+
+  if (threadIdx.x == 0) {
+    mbar_init(a_full, 1);
+    mbar_init(a_empty, 1);
+    for (int s = 0; s < BS; ++s) {
+      mbar_init(b_full + s, 1);
+      mbar_init(b_empty + s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(acc_full + b, 1);
+      mbar_init(acc_empty + b, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmBhi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmBlo)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmOut)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+        smem_u32(tmem_holder)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      int cur_m = -1, gen = 0;
+      for (int t = t0, i = 0; t < t1; ++t, ++i) {
+        const int m = t / p.n_tiles, n = t - m * p.n_tiles;
+        if (m != cur_m) {
+          if (gen > 0) mbar_wait(a_empty, (gen - 1) & 1);
+          mbar_expect_tx(a_full, L::A_BYTES);
+#pragma unroll
+          for (int kb = 0; kb < 2; ++kb) {
+            tma_load_2d(&tmAhi, a_full, a_s + kb * L::A_PART, kb * BKE, m * BM);
+            tma_load_2d(&tmAlo, a_full, a_s + (2 + kb) * L::A_PART, kb * BKE, m * BM);
+          }
+          cur_m = m;
+          ++gen;
+        }
+        const int s = i % BS;
+        mbar_wait(b_empty + s, ((i / BS) & 1) ^ 1);
+        mbar_expect_tx(b_full + s, L::B_STAGE);
+        uint8_t* bs = b_s + s * L::B_STAGE;
+#pragma unroll
+        for (int kb = 0; kb < 2; ++kb) {
+          tma_load_2d(&tmBhi, b_full + s, bs + (2 * kb) * L::B_PART, kb * BKE, n * 64);
+          tma_load_2d(&tmBlo, b_full + s, bs + (2 * kb + 1) * L::B_PART, kb * BKE, n * 64);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      constexpr uint32_t id128 = idesc_tf32(BM, 128, 0, 0);
+      constexpr uint32_t id64 = idesc_tf32(BM, 64, 0, 0);
+      int cur_m = -1, gen = 0;
+      for (int t = t0, i = 0; t < t1; ++t, ++i) {
+        const int m = t / p.n_tiles;
+        if (m != cur_m) {
+          mbar_wait(a_full, gen & 1);
+          cur_m = m;
+          ++gen;
+        }
+        const int s = i % BS, buf = i & 1;
+        mbar_wait(acc_empty + buf, ((i >> 1) & 1) ^ 1);
+        mbar_wait(b_full + s, (i / BS) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d = tmem + static_cast<uint32_t>(buf) * 128u;
+        const uint32_t bs = smem_u32(b_s + s * L::B_STAGE);
+        const uint32_t as = smem_u32(a_s);
+#pragma unroll
+        for (int kb = 0; kb < 2; ++kb) {
+#pragma unroll
+          for (int kk = 0; kk < BKE / 8; ++kk) {
+            const uint64_t bd = smem_desc(bs + 2 * kb * L::B_PART + kk * 32, 16, 1024);  // [hi; lo]
+            const uint64_t ah = smem_desc(as + kb * L::A_PART + kk * 32, 16, 1024);
+            const uint64_t al = smem_desc(as + (2 + kb) * L::A_PART + kk * 32, 16, 1024);
+            mma_tf32(d, ah, bd, id128, (kb > 0 || kk > 0) ? 1u : 0u);
+            mma_tf32(d, al, bd, id64, 1u);
+          }
+        }
+        mma_commit(b_empty + s);
+        mma_commit(acc_full + buf);
+        const int mn = (t + 1) / p.n_tiles;
+        if (t + 1 >= t1 || mn != m) mma_commit(a_empty);
+      }
+    }
+  } else {  // ---------------- epilogue
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    const bool leader = threadIdx.x == 64;
+    for (int t = t0, i = 0; t < t1; ++t, ++i) {
+      const int m = t / p.n_tiles, n = t - m * p.n_tiles;
+      const int buf = i & 1;
+      mbar_wait(acc_full + buf, (i >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      // the previous tile's TMA store must have finished reading the staging buffer
+      if (leader) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      const uint32_t trow = tmem + static_cast<uint32_t>(buf) * 128u + lane_off;
+#pragma unroll
+      for (int c0 = 0; c0 < 64; c0 += 16) {
+        float v[16], w[16];
+        tmem_ld16(trow + c0, v);
+        tmem_ld16(trow + 64 + c0, w);
+        float4* box = reinterpret_cast<float4*>(out_s + (c0 >> 5) * (BM * 128) + row * 128);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int chunk = ((c0 & 31) >> 2) + j;
+          box[chunk ^ (row & 7)] =
+              make_float4(p.scale * (v[4 * j] + w[4 * j]), p.scale * (v[4 * j + 1] + w[4 * j + 1]),
+                          p.scale * (v[4 * j + 2] + w[4 * j + 2]),
+                          p.scale * (v[4 * j + 3] + w[4 * j + 3]));
+        }
+      }
+      // accumulator drained: hand it back to the MMA warp (one arrival per warp)
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty + buf);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (leader) {
+        tma_store_2d(&tmOut, out_s, n * 64, m * BM);
+        tma_store_2d(&tmOut, out_s + BM * 128, n * 64 + 32, m * BM);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+    if (leader) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+  }
+}
+
+}  // namespace tc
+}  // namespace sfb

@@ -48,6 +48,9 @@ struct Params {
   // 4-row K groups of the SWIZZLE_128B_BASE32B layout
   uint32_t mn_lbo = 4096;
   uint32_t mn_sbo = 512;
+  // profiling knobs (0 in production): bit0 skip the split arithmetic, bit1 skip
+  // the MMAs, bit2 skip the A loads, bit3 skip the B loads
+  int dbg = 0;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -208,6 +211,10 @@ __global__ void __launch_bounds__(192, 1)
   const int kb0 = blockIdx.z * p.k_blocks_per_split;
   const int kb1 = min(p.num_k_blocks, kb0 + p.k_blocks_per_split);
   const int nkb = kb1 - kb0;
+  // CTAs sharing a B tile start at different k-blocks so that they do not all
+  // hit the same L2 lines at the same moment (every M tile reads all of B)
+  const int rot = nkb > 0 ? static_cast<int>((blockIdx.x * 5u) % static_cast<unsigned>(nkb)) : 0;
+  auto kblk = [&](int i) { const int j = i + rot; return kb0 + (j >= nkb ? j - nkb : j); };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
@@ -237,7 +244,7 @@ __global__ void __launch_bounds__(192, 1)
       constexpr uint32_t bytes = (SPLIT_A ? A_BYTES : 2 * A_BYTES) + 2 * L::B_BYTES;
       constexpr int PD = 2 * ST;  // L2 prefetch distance (k-blocks) for the streamed A operand
       auto prefetch_a = [&](int i) {
-        const int kc = (kb0 + i) * BKE;
+        const int kc = kblk(i) * BKE;
         if constexpr (A_MN) {
 #pragma unroll
           for (int a = 0; a < 4; ++a) tma_prefetch_2d(&tmA, m0 + a * 32, kc);
@@ -253,16 +260,18 @@ __global__ void __launch_bounds__(192, 1)
         if constexpr (SPLIT_A)
           if (i + PD < nkb) prefetch_a(i + PD);
         mbar_wait(empty + s, ph ^ 1);
-        mbar_expect_tx(full + s, bytes);
-        const int kc = (kb0 + i) * BKE;
-        if constexpr (A_MN) {
+        mbar_expect_tx(full + s, bytes - ((p.dbg & 4) ? A_BYTES : 0) - ((p.dbg & 8) ? 2 * L::B_BYTES : 0));
+        const int kc = kblk(i) * BKE;
+        if (p.dbg & 4) {
+        } else if constexpr (A_MN) {
 #pragma unroll
           for (int a = 0; a < 4; ++a) tma_load_2d(&tmA, full + s, a_hi(s) + a * 4096, m0 + a * 32, kc);
         } else {
           tma_load_2d(&tmA, full + s, a_hi(s), kc, m0);
           if constexpr (!SPLIT_A) tma_load_2d(&tmAlo, full + s, a_lo(s), kc, m0);
         }
-        if constexpr (B_MN) {
+        if (p.dbg & 8) {
+        } else if constexpr (B_MN) {
 #pragma unroll
           for (int b = 0; b < BN / 32; ++b) {
             tma_load_2d(&tmBhi, full + s, b_hi(s) + b * 4096, n0 + b * 32, kc);
@@ -302,6 +311,7 @@ __global__ void __launch_bounds__(192, 1)
             bh = smem_desc(smem_u32(b_hi(s)) + kk * 32, 16, 1024);
             bl = smem_desc(smem_u32(b_lo(s)) + kk * 32, 16, 1024);
           }
+          if (p.dbg & 2) continue;
           mma_tf32(tmem, ah, bh, idesc, (i > 0 || kk > 0) ? 1u : 0u);
           mma_tf32(tmem, ah, bl, idesc, 1u);
           mma_tf32(tmem, al, bh, idesc, 1u);
@@ -321,6 +331,7 @@ __global__ void __launch_bounds__(192, 1)
         float4* lo = reinterpret_cast<float4*>(a_lo(s));
 #pragma unroll 4
         for (int e = t; e < A_BYTES / 16; e += 128) {
+          if (p.dbg & 1) break;
           const float4 v = hi[e];
           float4 h, l;
           h.x = tf32_rna(v.x); l.x = tf32_rna(v.x - h.x);

@@ -2,11 +2,11 @@
 //
 //   prep   : W1 -> (hi, lo) tf32 parts in both layouts (W1 [K x H] for dX,
 //            W1^T [H x K] for the forward), once per step
-//   GEMM1  : hpre_part[z] = X W1          A = X (K-major, split in smem), split-K z
+//   GEMM1  : hpre_part[z] = X W1          A = X (K-major, split into TMEM), split-K z
 //   head   : hpre = b1 + sum_z part; z, p, BCE, gz; dh (+ its hi/lo parts in
 //            row-major and transposed layouts)
-//   GEMM2  : dX = s * (dh W1^T + gz (S - x))   A = dh (pre-split), B = W1
-//   GEMM3  : dW1_part[z] = X^T dh         A = X (MN-major, split in smem), split-K z
+//   GEMM2  : dX = s * dh W1^T    persistent tile walker, TMA-store epilogue (tc_dx.cuh)
+//   GEMM3  : dW1_part[z] = X^T dh         A = X^T (split into TMEM), split-K z
 //   reduce : dW1 = sum_z part (fixed order); db1, dw2, db2, loss (fixed order)
 #include <cuda.h>
 
@@ -16,6 +16,8 @@
 #include "kernels.h"
 #include "tc_fused.cuh"
 #include "tc_gemm.cuh"
+#include "tc_ts.cuh"
+#include "tc_dx.cuh"
 
 namespace sfb {
 
@@ -148,6 +150,56 @@ void launch_gemm(dim3 grid, const CUtensorMap& a, const CUtensorMap& alo, const 
     configured = true;
   }
   kern<<<grid, 192, smem, s>>>(a, alo, bhi, blo, p);
+  CUDA_LAUNCH_CHECK();
+}
+
+template <bool A_MN, bool B_MN>
+void launch_ts_gemm(dim3 grid, const CUtensorMap& a, const CUtensorMap& bhi,
+                    const CUtensorMap& blo, const tc::Params& p, cudaStream_t s) {
+  auto kern = tc::gemm_ts_kernel<A_MN, B_MN>;
+  constexpr int smem = tc::TsLayout::SMEM;
+  static bool configured = false;  // per instantiation
+  if (!configured) {
+    CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = true;
+  }
+  kern<<<grid, 192, smem, s>>>(a, bhi, blo, p);
+  CUDA_LAUNCH_CHECK();
+}
+
+int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    CUDA_CHECK(cudaGetDevice(&dev));
+    CUDA_CHECK(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return n;
+}
+
+// GEMM2 as a persistent tile walker (tc_dx.cuh); needs H <= 64
+void launch_dx_gemm(const TowerTC& tc_, const float* dh_hi, const float* dh_lo, int rows, int K,
+                    int H, float* dX, int ldx, float scale, cudaStream_t s) {
+  const CUtensorMap ah = tmap(dh_hi, H, rows, tc_.ldh, 32, 128);
+  const CUtensorMap al = tmap(dh_lo, H, rows, tc_.ldh, 32, 128);
+  const CUtensorMap bh = tmap(tc_.w_hi, H, K, tc_.ldh, 32, 64);
+  const CUtensorMap bl = tmap(tc_.w_lo, H, K, tc_.ldh, 32, 64);
+  const CUtensorMap out = tmap(dX, K, rows, ldx, 32, 128);
+  tc::DxParams p{};
+  p.M = rows;
+  p.N = K;
+  p.n_tiles = (K + 63) / 64;
+  p.tiles = ((rows + 127) / 128) * p.n_tiles;
+  p.scale = scale;
+  auto kern = tc::gemm_dx_persistent_kernel;
+  constexpr int smem = tc::DxLayout::SMEM;
+  static bool configured = false;
+  if (!configured) {
+    CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = true;
+  }
+  const int grid = std::min(p.tiles, sm_count());
+  kern<<<grid, 192, smem, s>>>(ah, al, bh, bl, out, p);
   CUDA_LAUNCH_CHECK();
 }
 
@@ -417,7 +469,7 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc_, const float* X, int l
     p.out = tc_.part1;
     p.ldo = H;
     p.split_stride = static_cast<long long>(rows) * H;
-    launch_dec_gemm<64, false, false>(dim3(mt, nt, s1), a, bh, bl, p, s);
+    launch_ts_gemm<false, false>(dim3(mt, nt, s1), a, bh, bl, p, s);
   }
   // ---- head
   head_tc_kernel<<<ceil_div(static_cast<int64_t>(rows) * 32, 256), 256, 0, s>>>(
@@ -425,8 +477,11 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc_, const float* X, int l
       fm_s, fm_sqp, labels, 1.f / rows, logits, t.act, t.dh, t.gz, t.lossr, tc_.dh_hi, tc_.dh_lo,
       tc_.ldh);
   CUDA_LAUNCH_CHECK();
-  // ---- GEMM2: dX = scale (dh W1^T + gz (S - x)) (A = dh hi/lo, B = W1 hi/lo, both K-major)
-  {
+  // ---- GEMM2: dX = scale dh W1^T (A = dh hi/lo, B = W1 hi/lo, both K-major; the FM
+  //      term is added by segment_sum)
+  if (H <= 64) {
+    launch_dx_gemm(tc_, tc_.dh_hi, tc_.dh_lo, rows, K, H, dX, ldx, emb_scale, s);
+  } else {
     const CUtensorMap ah = tmap(tc_.dh_hi, H, rows, tc_.ldh, 32, 128);
     const CUtensorMap al = tmap(tc_.dh_lo, H, rows, tc_.ldh, 32, 128);
     const CUtensorMap bh = tmap(tc_.w_hi, H, K, tc_.ldh, 32, 64);
@@ -456,7 +511,7 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc_, const float* X, int l
   int s3, kps3;
   split_k(mt3 * nt, nkb3, &s3, &kps3);
   {
-    const CUtensorMap a = tmap(X, K, rows, ldx, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    const CUtensorMap a = tmap(X, K, rows, ldx, 128, 32, CU_TENSOR_MAP_SWIZZLE_NONE);
     const CUtensorMap bh = tmap(tc_.dh_hi, H, rows, tc_.ldh, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     const CUtensorMap bl = tmap(tc_.dh_lo, H, rows, tc_.ldh, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     tc::Params p{};
@@ -468,7 +523,7 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc_, const float* X, int l
     p.out = tc_.part3;
     p.ldo = H;
     p.split_stride = static_cast<long long>(K) * H;
-    launch_dec_gemm<64, true, true>(dim3(mt3, nt, s3), a, bh, bl, p, s);
+    launch_ts_gemm<true, true>(dim3(mt3, nt, s3), a, bh, bl, p, s);
   }
   const int64_t kh = static_cast<int64_t>(K) * H;
   dw1_reduce(tc_.part3, s3, kh, g_w1, accumulate, s);
