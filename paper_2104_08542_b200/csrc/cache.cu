@@ -185,10 +185,24 @@ __global__ void admit_kernel(int32_t n_work, const uint32_t* __restrict__ work_j
   } else {
     // HostStore::get_or_init lazy path (host_store.cpp:25-33)
     const uint64_t se = derive_seed_h(seed, embed_hash, f);
-    for (int c = lane; c < d; c += 32) {
-      emb[so + c] = static_cast<float>(uniform_from(splitmix_mix(se + (c + 1) * kGolden), -0.01, 0.01));
-      mom[so + c] = 0.f;
-      vel[so + c] = 0.f;
+    auto init = [&](int c) {
+      return static_cast<float>(uniform_from(splitmix_mix(se + (c + 1) * kGolden), -0.01, 0.01));
+    };
+    if ((d & 3) == 0) {  // 128-bit stores: lane = 4 consecutive columns
+      const int d4 = d >> 2;
+      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int c4 = lane; c4 < d4; c4 += 32) {
+        const int c = 4 * c4;
+        reinterpret_cast<float4*>(emb + so)[c4] = make_float4(init(c), init(c + 1), init(c + 2), init(c + 3));
+        reinterpret_cast<float4*>(mom + so)[c4] = z;
+        reinterpret_cast<float4*>(vel + so)[c4] = z;
+      }
+    } else {
+      for (int c = lane; c < d; c += 32) {
+        emb[so + c] = init(c);
+        mom[so + c] = 0.f;
+        vel[so + c] = 0.f;
+      }
     }
     if (lane == 0) steps[s] = 0;
   }

@@ -51,6 +51,7 @@ struct Params {
   // profiling knobs (0 in production): bit0 skip the split arithmetic, bit1 skip
   // the MMAs, bit2 skip the A loads, bit3 skip the B loads
   int dbg = 0;
+  long long* trace = nullptr;  // profiling: per-k-block clock64 stamps of CTA 0 (scratch only)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -76,6 +77,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// wait with a back-off between polls: for barriers the tensor core arrives on
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, int ns) {
+  while (!mbar_try(bar, parity)) __nanosleep(ns);
 }
 
 // TMA prefetch of a box into L2 (no smem, no barrier): lets the producer run

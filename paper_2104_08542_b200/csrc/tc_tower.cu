@@ -163,7 +163,7 @@ void launch_ts_gemm(dim3 grid, const CUtensorMap& a, const CUtensorMap& bhi,
     CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = true;
   }
-  kern<<<grid, 192, smem, s>>>(a, bhi, blo, p);
+  kern<<<grid, tc::kTsThreads, smem, s>>>(a, bhi, blo, p);
   CUDA_LAUNCH_CHECK();
 }
 
@@ -332,7 +332,7 @@ void launch_dec_gemm(dim3 grid, const CUtensorMap& a, const CUtensorMap& bhi,
     CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = true;
   }
-  kern<<<grid, 192, smem, s>>>(a, bhi, blo, p);
+  kern<<<grid, tc::kTsThreads, smem, s>>>(a, bhi, blo, p);
   CUDA_LAUNCH_CHECK();
 }
 

@@ -1,17 +1,21 @@
 // Streamed 3xTF32 GEMM with the A operand in TMEM (tcgen05.mma ... [d], [a_tmem], b_desc).
 //
-// The SS kernel (tc_gemm.cuh) is shared-memory-bandwidth bound for the tower's
-// skinny GEMMs (N = H = 64): every k-block the tensor core re-reads the A tile
-// from smem once per product (ah*bh, ah*bl, al*bh) and the split warps read the
-// raw tile and write back two parts, ~150 KB of smem traffic per 16 KB of A.
-// Here:
-//   * the split warps (thread = TMEM lane = A row) read the raw A row once from
-//     smem and write its tf32 hi/lo parts straight into TMEM (tcgen05.st);
-//   * B hi and lo sit back to back in smem, so [B_hi; B_lo] is ONE N = 128
-//     operand: ah x [bh | bl] lands in accumulator columns [0, 64) / [64, 128)
-//     with a single MMA, al x bh (N = 64) accumulates into [0, 64);
-//   * the epilogue sums the two accumulator halves.
-// Per k-block smem traffic: TMA 32 KB in, 16 KB split reads, 24 KB B reads.
+// Used for the tower's two X-streaming GEMMs (N = H = 64, K or M = the 3120-wide
+// activation): they are HBM streams of X with a skinny MMA, so the design goal is
+// bytes in flight, not MMA shape.
+//   * raw A tiles land by TMA in a deep smem ring (kTsARing x 16 KB) that is
+//     released as soon as the split warps have read a tile — not when the MMA is
+//     done — so ~7 tiles of X are always in flight per SM (Little's law at
+//     ~1.5 us loaded DRAM latency);
+//   * the split warps (thread = TMEM lane = A row; two warp groups taking alternate
+//     k-blocks) round the row to tf32 hi/lo in registers and write both parts
+//     straight into a TMEM stage (tcgen05.st);
+//   * B hi and lo come from L2 through their own ring (separate producer warp); they
+//     sit back to back in smem, so [B_hi; B_lo] is ONE N = 128 operand:
+//     ah x [bh | bl] lands in accumulator columns [0, 64) / [64, 128) with a single
+//     MMA and al x bh (N = 64) accumulates into [0, 64); the epilogue sums the halves.
+// Measured issue rate of that pair: 96 clk per 8-deep k step (tf32 TS, B200), i.e.
+// 384 clk per 32-wide k-block.
 //
 // A_MN = false: A = X tile [128 rows x 32 k], K-major, SWIZZLE_128B (GEMM1).
 // A_MN = true : A = X^T: TMA box {128 X-columns, 32 X-rows}, no swizzle; thread m
@@ -26,14 +30,17 @@
 namespace sfb {
 namespace tc {
 
-constexpr int kTsStages = 6;  // TMEM: 128 accumulator columns + 6 x 64 A columns = 512
+constexpr int kTsARing = 8;   // raw A tiles (smem)
+constexpr int kTsBRing = 4;   // B hi/lo tiles (smem)
+constexpr int kTsStages = 6;  // TMEM A stages: 128 accumulator columns + 6 x 64 = 512
+constexpr int kTsThreads = 352;  // 11 warps: A producer, MMA, 8 split/epilogue, B producer
 
 struct TsLayout {
-  static constexpr int A_RAW = BM * BKE * 4;          // 16 KB raw fp32 A tile
-  static constexpr int B_PART = 64 * BKE * 4;         // 8 KB per (hi | lo) part
-  static constexpr int STAGE_BYTES = A_RAW + 2 * B_PART;
-  static constexpr int SMEM = 1024 + kTsStages * STAGE_BYTES + 256;
-  static_assert(kTsStages * STAGE_BYTES >= BM * 65 * 4, "epilogue tile must fit the ring");
+  static constexpr int A_RAW = BM * BKE * 4;   // 16 KB raw fp32 A tile
+  static constexpr int B_PART = 64 * BKE * 4;  // 8 KB per (hi | lo) part
+  static constexpr int B_STAGE = 2 * B_PART;
+  static constexpr int SMEM = 1024 + kTsARing * A_RAW + kTsBRing * B_STAGE + 512;
+  static_assert(kTsARing * A_RAW >= BM * 65 * 4, "epilogue tile must fit the A ring");
 };
 
 __device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
@@ -58,25 +65,40 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) 
       : "memory");
 }
 
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+      "%13,%14,%15,%16};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]),
+      "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]),
+      "f"(v[15])
+      : "memory");
+}
+
 template <bool A_MN, bool B_MN>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kTsThreads, 1)
     gemm_ts_kernel(const __grid_constant__ CUtensorMap tmA,
                    const __grid_constant__ CUtensorMap tmBhi,
                    const __grid_constant__ CUtensorMap tmBlo, const Params p) {
   using L = TsLayout;
-  constexpr int ST = kTsStages;
+  constexpr int RA = kTsARing, RB = kTsBRing, TS = kTsStages;
   constexpr int BN = 64;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * L::STAGE_BYTES);
-  uint64_t* ready = full + ST;
-  uint64_t* empty = ready + ST;
-  uint64_t* tmem_full = empty + ST;
+  uint8_t* a_ring = smem;
+  uint8_t* b_ring = smem + RA * L::A_RAW;
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(b_ring + RB * L::B_STAGE);
+  uint64_t* a_empty = a_full + RA;
+  uint64_t* b_full = a_empty + RA;
+  uint64_t* b_empty = b_full + RB;
+  uint64_t* t_ready = b_empty + RB;
+  uint64_t* t_empty = t_ready + TS;
+  uint64_t* tmem_full = t_empty + TS;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tmem_full + 1);
-  auto a_raw = [&](int s) { return smem + s * L::STAGE_BYTES; };
-  auto b_hi = [&](int s) { return smem + s * L::STAGE_BYTES + L::A_RAW; };
-  auto b_lo = [&](int s) { return smem + s * L::STAGE_BYTES + L::A_RAW + L::B_PART; };
+  auto a_raw = [&](int s) { return a_ring + s * L::A_RAW; };
+  auto b_hi = [&](int s) { return b_ring + s * L::B_STAGE; };
+  auto b_lo = [&](int s) { return b_ring + s * L::B_STAGE + L::B_PART; };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
@@ -87,12 +109,20 @@ __global__ void __launch_bounds__(192, 1)
   // the same L2 lines at the same moment
   const int rot = nkb > 0 ? static_cast<int>((blockIdx.x * 5u) % static_cast<unsigned>(nkb)) : 0;
   auto kblk = [&](int i) { const int j = i + rot; return kb0 + (j >= nkb ? j - nkb : j); };
+  const bool tr = p.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < ST; ++s) {
-      mbar_init(full + s, 1);
-      mbar_init(ready + s, 128);
-      mbar_init(empty + s, 1);
+    for (int s = 0; s < RA; ++s) {
+      mbar_init(a_full + s, 1);
+      mbar_init(a_empty + s, 4);
+    }
+    for (int s = 0; s < RB; ++s) {
+      mbar_init(b_full + s, 1);
+      mbar_init(b_empty + s, 1);
+    }
+    for (int s = 0; s < TS; ++s) {
+      mbar_init(t_ready + s, 4);
+      mbar_init(t_empty + s, 1);
     }
     mbar_init(tmem_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -112,35 +142,42 @@ __global__ void __launch_bounds__(192, 1)
   auto a_col = [&](int s) { return tmem + 128u + static_cast<uint32_t>(s) * 64u; };  // hi | lo
 
   if (warp == 0) {
-    if (lane == 0) {  // ---------------- TMA producer
-      constexpr uint32_t bytes = L::A_RAW + 2 * L::B_PART;
-      constexpr int PD = 2 * ST;  // L2 prefetch distance (k-blocks) for the streamed A
-      auto prefetch_a = [&](int i) {
-        const int kc = kblk(i) * BKE;
-        if constexpr (A_MN) tma_prefetch_2d(&tmA, m0, kc);
-        else tma_prefetch_2d(&tmA, kc, m0);
-      };
-      for (int i = 0; i < PD && i < nkb; ++i) prefetch_a(i);
+    if (lane == 0) {  // ---------------- A producer: raw X tiles, RA deep
       for (int i = 0; i < nkb; ++i) {
-        const int s = i % ST;
-        const uint32_t ph = (i / ST) & 1;
-        if (i + PD < nkb) prefetch_a(i + PD);
-        mbar_wait(empty + s, ph ^ 1);
-        mbar_expect_tx(full + s, bytes - ((p.dbg & 4) ? L::A_RAW : 0) - ((p.dbg & 8) ? 2 * L::B_PART : 0));
-        const int kc = kblk(i) * BKE;
+        const int s = i % RA;
+        mbar_wait(a_empty + s, ((i / RA) & 1) ^ 1);
+        if (tr && i < 64) p.trace[i] = clock64();
         if (p.dbg & 4) {
-        } else if constexpr (A_MN) tma_load_2d(&tmA, full + s, a_raw(s), m0, kc);
-        else tma_load_2d(&tmA, full + s, a_raw(s), kc, m0);
+          mbar_arrive(a_full + s);
+          continue;
+        }
+        mbar_expect_tx(a_full + s, L::A_RAW);
+        const int kc = kblk(i) * BKE;
+        if constexpr (A_MN) tma_load_2d(&tmA, a_full + s, a_raw(s), m0, kc);
+        else tma_load_2d(&tmA, a_full + s, a_raw(s), kc, m0);
+      }
+    }
+  } else if (warp == 10) {
+    if (lane == 0) {  // ---------------- B producer: W / dh hi+lo tiles from L2
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % RB;
+        if (p.dbg & 128) mbar_wait_sleep(b_empty + s, ((i / RB) & 1) ^ 1, 256);
+        else mbar_wait(b_empty + s, ((i / RB) & 1) ^ 1);
         if (p.dbg & 8) {
-        } else if constexpr (B_MN) {
+          mbar_arrive(b_full + s);
+          continue;
+        }
+        mbar_expect_tx(b_full + s, L::B_STAGE);
+        const int kc = kblk(i) * BKE;
+        if constexpr (B_MN) {
 #pragma unroll
           for (int b = 0; b < BN / 32; ++b) {
-            tma_load_2d(&tmBhi, full + s, b_hi(s) + b * 4096, n0 + b * 32, kc);
-            tma_load_2d(&tmBlo, full + s, b_lo(s) + b * 4096, n0 + b * 32, kc);
+            tma_load_2d(&tmBhi, b_full + s, b_hi(s) + b * 4096, n0 + b * 32, kc);
+            tma_load_2d(&tmBlo, b_full + s, b_lo(s) + b * 4096, n0 + b * 32, kc);
           }
         } else {
-          tma_load_2d(&tmBhi, full + s, b_hi(s), kc, n0);
-          tma_load_2d(&tmBlo, full + s, b_lo(s), kc, n0);
+          tma_load_2d(&tmBhi, b_full + s, b_hi(s), kc, n0);
+          tma_load_2d(&tmBlo, b_full + s, b_lo(s), kc, n0);
         }
       }
     }
@@ -149,41 +186,45 @@ __global__ void __launch_bounds__(192, 1)
       constexpr uint32_t id128 = idesc_tf32(BM, 2 * BN, 0, B_MN ? 1 : 0);
       constexpr uint32_t id64 = idesc_tf32(BM, BN, 0, B_MN ? 1 : 0);
       for (int i = 0; i < nkb; ++i) {
-        const int s = i % ST;
-        const uint32_t ph = (i / ST) & 1;
-        mbar_wait(ready + s, ph);
+        const int t = i % TS, s = i % RB;
+        if (!(p.dbg & 32)) mbar_wait(t_ready + t, (i / TS) & 1);
+        if (tr && i < 64) p.trace[256 + i] = clock64();
+        if (!(p.dbg & 32)) mbar_wait(b_full + s, (i / RB) & 1);
+        if (tr && i < 64) p.trace[192 + i] = clock64();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
         for (int kk = 0; kk < BKE / 8; ++kk) {
           uint64_t bd;
           if constexpr (B_MN) bd = smem_desc(smem_u32(b_hi(s)) + kk * 1024, 4096, 512, 1);
           else bd = smem_desc(smem_u32(b_hi(s)) + kk * 32, 16, 1024);
-          const uint32_t ah = a_col(s) + kk * 8, al = a_col(s) + 32 + kk * 8;
+          const uint32_t ah = a_col(t) + kk * 8, al = a_col(t) + 32 + kk * 8;
           if (p.dbg & 2) continue;
           mma_tf32_ts(tmem, ah, bd, id128, (i > 0 || kk > 0) ? 1u : 0u);  // [hh | hl]
           mma_tf32_ts(tmem, al, bd, id64, 1u);                              // += lh
         }
-        mma_commit(empty + s);  // frees the smem stage and the TMEM A stage
+        mma_commit(b_empty + s);
+        mma_commit(t_empty + t);
       }
       mma_commit(tmem_full);
     }
   } else {
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    // ---------------- split: raw A row -> tf32 hi / lo columns in TMEM. The two warp
+    // groups take alternate k-blocks so one group's TMEM-store latency overlaps the
+    // other's loads and rounding.
+    const int q = warp & 3;          // TMEM lane quarter this warp may access
+    const int h = (warp - 2) >> 2;   // warp group: k-blocks i = h (mod 2)
     const int row = q * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
-    // ---------------- split: raw A row -> tf32 hi / lo columns in TMEM
-    for (int i = 0; i < nkb; ++i) {
-      const int s = i % ST;
-      const uint32_t ph = (i / ST) & 1;
-      mbar_wait(empty + s, ph ^ 1);  // the MMAs of k-block i - ST have left this TMEM stage
-      mbar_wait(full + s, ph);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const bool tl = tr && threadIdx.x == 64;
+    for (int i = h; i < nkb; i += 2) {
+      const int s = i % RA, t = i % TS;
+      mbar_wait(a_full + s, (i / RA) & 1);
+      if (tl && i < 64) p.trace[64 + i] = clock64();
       float hi[32], lo[32];
       if (p.dbg & 1) {
-        mbar_arrive(ready + s);
-        continue;
-      }
-      if constexpr (A_MN) {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) hi[k] = 0.f;
+      } else if constexpr (A_MN) {
         const float* src = reinterpret_cast<const float*>(a_raw(s)) + row;
 #pragma unroll
         for (int k = 0; k < 32; ++k) hi[k] = src[k * BM];
@@ -204,38 +245,52 @@ __global__ void __launch_bounds__(192, 1)
         hi[k] = tf32_rna(v);
         lo[k] = tf32_rna(v - hi[k]);
       }
-      tmem_st32(a_col(s) + lane_off, hi);
-      tmem_st32(a_col(s) + 32 + lane_off, lo);
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mbar_arrive(ready + s);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(a_empty + s);  // raw tile consumed: the TMA may refill it
+      if (p.dbg & 128) mbar_wait_sleep(t_empty + t, ((i / TS) & 1) ^ 1, 256);
+      else mbar_wait(t_empty + t, ((i / TS) & 1) ^ 1);  // MMAs of k-block i - TS left this stage
+      if (!(p.dbg & 64)) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (!(p.dbg & 16)) {
+          tmem_st32(a_col(t) + lane_off, hi);
+          tmem_st32(a_col(t) + 32 + lane_off, lo);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      } else if (p.dbg & 1) {
+        hi[0] += lo[5];  // keep the registers live
+        if (hi[0] == 12345.f) p.out[0] = hi[0];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(t_ready + t);
+      if (tl && i < 64) p.trace[128 + i] = clock64();
     }
     // ---------------- epilogue: acc[:, c] + acc[:, 64 + c] -> smem tile -> coalesced store
     mbar_wait(tmem_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t trow = tmem + lane_off;
-    float* tile = reinterpret_cast<float*>(smem);
-    constexpr int TS = BN + 1;
+    float* tile = reinterpret_cast<float*>(smem);  // A ring: every raw tile has been consumed
+    constexpr int TSW = BN + 1;
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
+    for (int c0 = 32 * h; c0 < 32 * h + 32; c0 += 16) {
       float v[16], w[16];
       tmem_ld16(trow + c0, v);
       tmem_ld16(trow + BN + c0, w);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) tile[row * TS + c0 + j] = v[j] + w[j];
+      for (int j = 0; j < 16; ++j) tile[row * TSW + c0 + j] = v[j] + w[j];
     }
-    asm volatile("bar.sync 1, 128;" ::: "memory");
-    const int w2 = (threadIdx.x - 64) >> 5;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    const int w2 = warp - 2;  // 0..7
     if (nkb > 0) {
 #pragma unroll 1
-      for (int r = w2; r < BM; r += 4) {
+      for (int r = w2; r < BM; r += 8) {
         const int m = m0 + r;
         if (m >= p.M) break;
         float* o = p.out + blockIdx.z * p.split_stride + static_cast<long long>(m) * p.ldo;
 #pragma unroll
         for (int c = lane; c < BN; c += 32) {
           const int n = n0 + c;
-          if (n < p.N) o[n] = tile[r * TS + c];
+          if (n < p.N) o[n] = tile[r * TSW + c];
         }
       }
     }
