@@ -3,8 +3,11 @@
 
 Workload (BASELINE.json configs[1]): Criteo-shaped DeepFM-lite, 39 sparse
 fields, 33.8M-row table, d=80, hidden 64, batch 8192 per GPU, Zipf 1.05,
-lazy Adam, MixCache with a 2^19-slot (0.48 GiB of emb+m+v) HBM cache per GPU
-over a pinned host table. One process per GPU (torchrun), weak scaling.
+lazy Adam. MixCache sized for the B200: by default (--cache 0) the whole owned
+shard of the table (33.8M/W rows x emb+m+v = 32 GB at W=1) is the HBM cache, so
+rows are lazily initialised on first touch and never leave HBM; --cache N runs
+the paper's small-cache regime (e.g. 2^19 slots = 0.48 GiB) over the pinned host
+table with LRU eviction over PCIe. One process per GPU (torchrun), weak scaling.
 
 Arms
   ours       : `value` = samples/s with each step's batch already resident in
@@ -47,7 +50,8 @@ def parse():
     p.add_argument("--vocab", type=int, default=33_800_000)
     p.add_argument("--zipf", type=float, default=1.05)
     p.add_argument("--hidden", type=int, default=64)
-    p.add_argument("--cache", type=int, default=1 << 19)
+    p.add_argument("--cache", type=int, default=0,
+                   help="HBM cache slots per GPU; 0 = the whole owned shard")
     # alltoall = owner-routed exchange of only the touched rows (default); allreduce = the
     # reference's all-reduce of the zero-padded common embedding / gradients
     p.add_argument("--sync", default="alltoall", choices=["allreduce", "alltoall"])
@@ -321,11 +325,18 @@ def cpu_sample(args, workers, rows_total, steps, threads):
     c.num_fields = args.fields
     c.embedding_dim = args.dim
     c.vocabulary_size = args.vocab
-    c.cache_capacity = args.cache
+    # per-worker cache: the arm's own size, capped at what the sample can touch (every
+    # id of every step) — with no evictions possible the computation is identical, and
+    # the fp64 port does not allocate a 33.8M-slot table for a 2048-row sample
+    shard = (args.vocab + workers - 1) // workers
+    cap = args.cache if 0 < args.cache < shard else shard
+    c.cache_capacity = min(cap, rows_total * args.fields * steps + 1)
     c.hidden_dim = args.hidden
     c.zipf_exponent = args.zipf
     c.num_threads = threads
     sim = O.orc_sim_create(C.byref(c))
+    if not sim:
+        raise RuntimeError("oracle: " + str(O.orc_last_error()))
     rows = c.batch_size_per_worker * workers
     batches = [oracle_generate(rows, args.fields, args.vocab, 7, args.zipf, s) for s in range(steps)]
     times = []
@@ -354,7 +365,9 @@ def run_reference(args, D):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (oracle port of the reference SyntheticGenerator)",
             "config": {"workload": WORKLOAD, "global_batch": args.batch * D.world,
-                       "sample_rows_per_step": rows_step, "cache_slots_per_gpu": args.cache},
+                       "sample_rows_per_step": rows_step,
+                       "cache_slots_per_gpu": args.cache if args.cache > 0
+                       else (args.vocab + D.world - 1) // D.world},
             "impl": "reference",
             "cpu_baseline": {"value": round(val, 1), "unit": "samples/s", "cores": threads,
                              "kind": "port",

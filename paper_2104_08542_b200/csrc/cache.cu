@@ -48,7 +48,7 @@ __global__ void probe_kernel(const uint32_t* __restrict__ own_k,
                              const uint32_t* __restrict__ index, uint32_t C, int32_t t,
                              int32_t* __restrict__ last_use, int32_t* __restrict__ mark,
                              uint32_t* __restrict__ own_slot, uint32_t* __restrict__ miss,
-                             int32_t* __restrict__ marked) {
+                             int32_t* __restrict__ marked, uint32_t* __restrict__ own_f) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= cap) return;
   if (j >= *n_own_ptr) {
@@ -63,9 +63,28 @@ __global__ void probe_kernel(const uint32_t* __restrict__ own_k,
     own_slot[j] = s;
     miss[j] = 0;
   } else {
-    own_slot[j] = kEmpty;
+    own_slot[j] = s;  // kOnHost / kNever until admit assigns the slot
+    own_f[j] = f;
     miss[j] = 1;
   }
+}
+
+// work list of the misses (global_ids order) with their probe-time feature / index entry
+__global__ void compact_work_kernel(const uint32_t* __restrict__ miss,
+                                    const uint32_t* __restrict__ rank, int32_t n,
+                                    const uint32_t* __restrict__ own_f,
+                                    const uint32_t* __restrict__ own_slot,
+                                    uint32_t* __restrict__ work_j, uint32_t* __restrict__ work_f,
+                                    uint32_t* __restrict__ work_w, int32_t* __restrict__ count) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (miss[i]) {
+    const uint32_t r = rank[i];
+    work_j[r] = static_cast<uint32_t>(i);
+    work_f[r] = own_f[i];
+    work_w[r] = own_slot[i];
+  }
+  if (i == n - 1) *count = static_cast<int32_t>(rank[i] + miss[i]);
 }
 
 // needed_soon for resident owned features of a lookahead batch
@@ -142,11 +161,16 @@ __global__ void evict_kernel(int32_t n_evict, const uint64_t* __restrict__ sorte
 }
 
 // push_parameters_to_cache: one warp per admitted feature.
+// One warp per kAdmitRows admitted rows. The probe already recorded each miss's
+// feature and index entry (work_f / work_w), so the per-row facts are coalesced loads:
+// lane l < kAdmitRows takes row i0 + l (bookkeeping + its lazy-init seed), then all 32
+// lanes fill the group's (row, 16 B chunk) items with 128-bit stores.
+constexpr int kAdmitRows = 8;
 __global__ void admit_kernel(int32_t n_work, const uint32_t* __restrict__ work_j,
-                             const uint32_t* __restrict__ own_k, const uint32_t* __restrict__ gids,
-                             uint32_t W, int d, const uint32_t* __restrict__ free_stack,
-                             int32_t free_top, uint32_t* __restrict__ index,
-                             const float* __restrict__ host_rows,
+                             const uint32_t* __restrict__ work_f,
+                             const uint32_t* __restrict__ work_w, uint32_t W, int d,
+                             const uint32_t* __restrict__ free_stack, int32_t free_top,
+                             uint32_t* __restrict__ index, const float* __restrict__ host_rows,
                              const int32_t* __restrict__ host_steps, uint64_t seed,
                              uint64_t embed_hash, float* __restrict__ emb, float* __restrict__ mom,
                              float* __restrict__ vel, int32_t* __restrict__ steps,
@@ -154,65 +178,76 @@ __global__ void admit_kernel(int32_t n_work, const uint32_t* __restrict__ work_j
                              uint64_t* __restrict__ admit_seq, uint64_t seq0,
                              int32_t* __restrict__ mark, int32_t t,
                              uint32_t* __restrict__ own_slot, int32_t* __restrict__ n_from_host) {
-  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t i0 =
+      ((blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5) * kAdmitRows;
   const int lane = threadIdx.x & 31;
-  if (i >= n_work) return;
-  const uint32_t j = work_j[i];
-  const uint32_t f = gids[own_k[j]];
-  const uint64_t r = f / W;
-  const uint32_t s = free_stack[free_top - 1 - i];
-  const size_t so = static_cast<size_t>(s) * d;
-  const uint32_t where = index[r];
-  if (where == kOnHost) {
-    const float* src = host_rows + r * 3 * d;
-    if ((d & 3) == 0) {
-      const int d4 = d >> 2;
-      for (int c = lane; c < 3 * d4; c += 32) {
-        const int which = c / d4, cc = c - which * d4;
-        float* dst = (which == 0 ? emb : which == 1 ? mom : vel) + so;
-        reinterpret_cast<float4*>(dst)[cc] = reinterpret_cast<const float4*>(src)[c];
+  if (i0 >= n_work) return;
+  const int64_t mi = i0 + lane;
+  const bool mine = lane < kAdmitRows && mi < n_work;
+  uint32_t my_f = 0, my_s = 0, my_where = kNever;
+  uint64_t my_se = 0;
+  if (mine) {
+    const uint32_t j = work_j[mi];
+    my_f = work_f[mi];
+    my_where = work_w[mi];
+    my_s = free_stack[free_top - 1 - mi];
+    slot_feat[my_s] = my_f;
+    last_use[my_s] = t;
+    admit_seq[my_s] = seq0 + static_cast<uint64_t>(mi);
+    mark[my_s] = t;
+    index[my_f / W] = my_s;
+    own_slot[j] = my_s;
+    if (my_where == kOnHost) steps[my_s] = host_steps[my_f / W];
+    else {
+      steps[my_s] = 0;
+      my_se = derive_seed_h(seed, embed_hash, my_f);  // HostStore::get_or_init (host_store.cpp:25-33)
+    }
+  }
+  const unsigned from_host = __ballot_sync(0xFFFFFFFFu, mine && my_where == kOnHost);
+  if (lane == 0 && from_host) atomicAdd(n_from_host, __popc(from_host));
+  const int nrows = n_work - i0 < kAdmitRows ? static_cast<int>(n_work - i0) : kAdmitRows;
+  const bool vec = (d & 3) == 0;
+  const int per = vec ? d >> 2 : d;  // items per row: 16 B chunks (or scalars)
+  const int items = nrows * per;
+  for (int base = 0; base < items; base += 32) {  // uniform trip count: all lanes shuffle
+    const int it = base + lane;
+    const int k = it < items ? it / per : 0;
+    const uint32_t f = __shfl_sync(0xFFFFFFFFu, my_f, k);
+    const uint32_t sl = __shfl_sync(0xFFFFFFFFu, my_s, k);
+    const uint32_t where = __shfl_sync(0xFFFFFFFFu, my_where, k);
+    const uint64_t se = __shfl_sync(0xFFFFFFFFu, my_se, k);
+    if (it >= items) continue;
+    const int c = it - k * per;  // chunk (or column) within the row
+    const size_t so = static_cast<size_t>(sl) * d;
+    if (where == kOnHost) {
+      const float* src = host_rows + static_cast<uint64_t>(f / W) * 3 * d;
+      if (vec) {
+        const float4* s4 = reinterpret_cast<const float4*>(src);
+        reinterpret_cast<float4*>(emb + so)[c] = s4[c];
+        reinterpret_cast<float4*>(mom + so)[c] = s4[per + c];
+        reinterpret_cast<float4*>(vel + so)[c] = s4[2 * per + c];
+      } else {
+        emb[so + c] = src[c];
+        mom[so + c] = src[d + c];
+        vel[so + c] = src[2 * d + c];
       }
     } else {
-      for (int c = lane; c < 3 * d; c += 32) {
-        const int which = c / d, cc = c - which * d;
-        (which == 0 ? emb : which == 1 ? mom : vel)[so + cc] = src[c];
-      }
-    }
-    if (lane == 0) {
-      steps[s] = host_steps[r];
-      atomicAdd(n_from_host, 1);
-    }
-  } else {
-    // HostStore::get_or_init lazy path (host_store.cpp:25-33)
-    const uint64_t se = derive_seed_h(seed, embed_hash, f);
-    auto init = [&](int c) {
-      return static_cast<float>(uniform_from(splitmix_mix(se + (c + 1) * kGolden), -0.01, 0.01));
-    };
-    if ((d & 3) == 0) {  // 128-bit stores: lane = 4 consecutive columns
-      const int d4 = d >> 2;
-      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int c4 = lane; c4 < d4; c4 += 32) {
-        const int c = 4 * c4;
-        reinterpret_cast<float4*>(emb + so)[c4] = make_float4(init(c), init(c + 1), init(c + 2), init(c + 3));
-        reinterpret_cast<float4*>(mom + so)[c4] = z;
-        reinterpret_cast<float4*>(vel + so)[c4] = z;
-      }
-    } else {
-      for (int c = lane; c < d; c += 32) {
+      auto init = [&](int col) {
+        return static_cast<float>(
+            uniform_from(splitmix_mix(se + (col + 1) * kGolden), -0.01, 0.01));
+      };
+      if (vec) {
+        const int c0 = 4 * c;
+        reinterpret_cast<float4*>(emb + so)[c] =
+            make_float4(init(c0), init(c0 + 1), init(c0 + 2), init(c0 + 3));
+        reinterpret_cast<float4*>(mom + so)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        reinterpret_cast<float4*>(vel + so)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      } else {
         emb[so + c] = init(c);
         mom[so + c] = 0.f;
         vel[so + c] = 0.f;
       }
     }
-    if (lane == 0) steps[s] = 0;
-  }
-  if (lane == 0) {
-    slot_feat[s] = f;
-    last_use[s] = t;
-    admit_seq[s] = seq0 + i;
-    mark[s] = t;
-    index[r] = s;
-    own_slot[j] = s;
   }
 }
 
@@ -281,6 +316,9 @@ void CacheLane::init(uint64_t capacity, int dim, uint64_t owned_rows, uint64_t h
   CUDA_CHECK(cudaMalloc(&miss, sizeof(uint32_t) * umax));
   CUDA_CHECK(cudaMalloc(&miss_rank, sizeof(uint32_t) * umax));
   CUDA_CHECK(cudaMalloc(&work_j, sizeof(uint32_t) * umax));
+  CUDA_CHECK(cudaMalloc(&own_f, sizeof(uint32_t) * umax));
+  CUDA_CHECK(cudaMalloc(&work_f, sizeof(uint32_t) * umax));
+  CUDA_CHECK(cudaMalloc(&work_w, sizeof(uint32_t) * umax));
   CUDA_CHECK(cudaMalloc(&keys, sizeof(uint64_t) * C));
   CUDA_CHECK(cudaMalloc(&keys_sorted, sizeof(uint64_t) * C));
   CUDA_CHECK(cudaMalloc(&ids, sizeof(uint32_t) * C));
@@ -301,6 +339,7 @@ void CacheLane::release() {
                   static_cast<void*>(index), static_cast<void*>(flag), static_cast<void*>(rank),
                   static_cast<void*>(own_k), static_cast<void*>(own_slot), static_cast<void*>(miss),
                   static_cast<void*>(miss_rank), static_cast<void*>(work_j),
+                  static_cast<void*>(own_f), static_cast<void*>(work_f), static_cast<void*>(work_w),
                   static_cast<void*>(keys), static_cast<void*>(keys_sorted),
                   static_cast<void*>(ids), static_cast<void*>(ids_sorted), temp,
                   static_cast<void*>(counters)})
@@ -333,11 +372,13 @@ void CacheLane::probe(const uint32_t* d_gids, int32_t cap, uint32_t W, int32_t t
   if (cap <= 0) return;
   probe_kernel<<<ceil_div(cap, 256), 256, 0, s>>>(own_k, counters + kCntOwned, cap, d_gids, W,
                                                   index, static_cast<uint32_t>(C), t, last_use,
-                                                  mark, own_slot, miss, counters + kCntMarked);
+                                                  mark, own_slot, miss, counters + kCntMarked,
+                                                  own_f);
   CUDA_LAUNCH_CHECK();
   exclusive_scan_u32(temp, scan_bytes, miss, miss_rank, cap, s);
-  compact_kernel<<<ceil_div(cap, 256), 256, 0, s>>>(miss, miss_rank, cap, work_j,
-                                                    counters + kCntWorking);
+  compact_work_kernel<<<ceil_div(cap, 256), 256, 0, s>>>(miss, miss_rank, cap, own_f, own_slot,
+                                                         work_j, work_f, work_w,
+                                                         counters + kCntWorking);
   CUDA_LAUNCH_CHECK();
 }
 
@@ -358,8 +399,8 @@ void CacheLane::evict(int32_t n_evict, uint32_t W, int32_t t, cudaStream_t s) {
 void CacheLane::admit(int32_t n_work, const uint32_t* d_gids, uint32_t W, uint64_t seed, int32_t t,
                       cudaStream_t s) {
   if (n_work <= 0) return;
-  admit_kernel<<<ceil_div(static_cast<int64_t>(n_work) * 32, 256), 256, 0, s>>>(
-      n_work, work_j, own_k, d_gids, W, d, free_stack, free_top, index, host_rows, host_steps,
+  admit_kernel<<<ceil_div(ceil_div(static_cast<int64_t>(n_work), kAdmitRows) * 32, 256), 256, 0, s>>>(
+      n_work, work_j, work_f, work_w, W, d, free_stack, free_top, index, host_rows, host_steps,
       seed, fnv1a64("embed"), emb, mom, vel, steps, slot_feat, last_use, admit_seq, next_seq, mark,
       t, own_slot, counters + kCntFromHost);
   CUDA_LAUNCH_CHECK();

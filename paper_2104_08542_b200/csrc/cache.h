@@ -35,6 +35,9 @@ struct CacheLane {
   // per-step scratch
   uint32_t *flag = nullptr, *rank = nullptr, *own_k = nullptr, *own_slot = nullptr;
   uint32_t *miss = nullptr, *miss_rank = nullptr, *work_j = nullptr;
+  // probe-time facts about the misses, so admit reads them coalesced instead of
+  // chasing work_j -> own_k -> gids -> index: feature and index entry (kOnHost / kNever)
+  uint32_t *own_f = nullptr, *work_f = nullptr, *work_w = nullptr;
   uint64_t *keys = nullptr, *keys_sorted = nullptr;
   uint32_t *ids = nullptr, *ids_sorted = nullptr;
   void* temp = nullptr;

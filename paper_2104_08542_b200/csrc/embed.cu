@@ -48,25 +48,19 @@ __global__ void gather_instances_v4(const uint32_t* __restrict__ vid, int32_t ro
   float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
   float sq = 0.f;
   int f = 0;
-  for (; f + 4 <= F; f += 4) {  // 4 independent row loads in flight
-    const uint32_t v0 = __ldg(vr + f), v1 = __ldg(vr + f + 1), v2 = __ldg(vr + f + 2),
-                   v3 = __ldg(vr + f + 3);
-    const float4 a0 = __ldg(G + static_cast<int64_t>(v0) * d4 + c);
-    const float4 a1 = __ldg(G + static_cast<int64_t>(v1) * d4 + c);
-    const float4 a2 = __ldg(G + static_cast<int64_t>(v2) * d4 + c);
-    const float4 a3 = __ldg(G + static_cast<int64_t>(v3) * d4 + c);
-    xr[(f + 0) * d4] = a0;
-    xr[(f + 1) * d4] = a1;
-    xr[(f + 2) * d4] = a2;
-    xr[(f + 3) * d4] = a3;
-    s.x += a0.x; s.y += a0.y; s.z += a0.z; s.w += a0.w;
-    sq += a0.x * a0.x + a0.y * a0.y + a0.z * a0.z + a0.w * a0.w;
-    s.x += a1.x; s.y += a1.y; s.z += a1.z; s.w += a1.w;
-    sq += a1.x * a1.x + a1.y * a1.y + a1.z * a1.z + a1.w * a1.w;
-    s.x += a2.x; s.y += a2.y; s.z += a2.z; s.w += a2.w;
-    sq += a2.x * a2.x + a2.y * a2.y + a2.z * a2.z + a2.w * a2.w;
-    s.x += a3.x; s.y += a3.y; s.z += a3.z; s.w += a3.w;
-    sq += a3.x * a3.x + a3.y * a3.y + a3.z * a3.z + a3.w * a3.w;
+  for (; f + 8 <= F; f += 8) {  // 8 independent row loads in flight
+    uint32_t v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldg(vr + f + u);
+    float4 a[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a[u] = __ldg(G + static_cast<int64_t>(v[u]) * d4 + c);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {  // fields summed in order (same as the scalar loop)
+      xr[(f + u) * d4] = a[u];
+      s.x += a[u].x; s.y += a[u].y; s.z += a[u].z; s.w += a[u].w;
+      sq += a[u].x * a[u].x + a[u].y * a[u].y + a[u].z * a[u].z + a[u].w * a[u].w;
+    }
   }
   for (; f < F; ++f) {
     const float4 a = __ldg(G + static_cast<int64_t>(__ldg(vr + f)) * d4 + c);
