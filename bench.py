@@ -156,7 +156,7 @@ def run_ours(args, D):
     r0, nrows = sdist.rows_of(rank, tr.lanes, args.batch)
     F = args.fields
     W, K = args.warmup, args.steps
-    nb = W + 2 * K
+    nb = W + 3 * K  # warm-up | value | phase breakdown | e2e
     # device-resident batches (value arm) and pinned host copies (e2e arm)
     d_feat = torch.empty((nb, nrows * F), dtype=torch.int64, device=f"cuda:{dev}")
     d_lab = torch.empty((nb, nrows), dtype=torch.uint8, device=f"cuda:{dev}")
@@ -173,8 +173,8 @@ def run_ours(args, D):
     stream = torch.cuda.ExternalStream(tr.stream, device=f"cuda:{dev}")
     d_loss = torch.zeros(1, dtype=torch.float32, device=f"cuda:{dev}")
 
-    # ---- value: device-resident inputs, CUDA events on the trainer stream
-    tr.set_timing(True)
+    # ---- value: device-resident inputs, CUDA events on the trainer stream (no
+    # per-phase events inside this region; the breakdown is a separate pass below)
     phases = {}
     stats_acc = {}
     clocks = Clocks(dev)
@@ -184,30 +184,41 @@ def run_ours(args, D):
     clocks.start()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    fill0 = tr.stats()["total_filled_from_host"]
+    st0 = tr.stats()  # running totals before the timed region (waits for the stream)
     ev0.record(stream)
     for i in range(K):
         s = W + i
         tr.step_device(s, d_feat[s].data_ptr(), d_lab[s].data_ptr(), None, d_loss.data_ptr())
-        st = tr.stats()  # host-side per-step counters (no device sync)
-        launches += st["kernel_launches"]
-        for k2, v in st.items():
-            if not k2.startswith("total"):
-                stats_acc[k2] = stats_acc.get(k2, 0) + v
     ev1.record(stream)
     ev1.synchronize()
     torch.cuda.synchronize()
     dev_ms = ev0.elapsed_time(ev1)
     clk = clocks.stop()
-    tr.synchronize()  # deferred device counters + phase events
-    phases = dict(tr.phase_times())
-    filled = tr.stats()["total_filled_from_host"] - fill0
-    stats_acc["filled_from_host"] = filled
-    stats_acc["pcie_h2d_bytes"] = filled * (3 * args.dim + 1) * 4
+    tr.synchronize()  # deferred device counters
+    st1 = tr.stats()
+    tot = {k2: st1[k2] - st0[k2] for k2 in st1 if k2.startswith("total")}
+    launches = tot["total_kernel_launches"]
+    filled = tot["total_filled_from_host"]
+    stats_acc = {"unique": tot["total_unique"], "owned": tot["total_owned"],
+                 "working": tot["total_working"], "evicted": tot["total_evicted"],
+                 "filled_from_host": filled, "pcie_h2d_bytes": filled * (3 * args.dim + 1) * 4,
+                 "pcie_d2h_bytes": tot["total_evicted"] * (3 * args.dim + 1) * 4,
+                 "nvlink_bytes": tot["total_nvlink_bytes"], "kernel_launches": launches,
+                 "host_wait_free_steps": tot["total_free_steps"]}
     D.barrier()
-    tr.set_timing(False)
     ms_step = D.max(dev_ms) / K
     loss_dev = float(d_loss.item())
+
+    # ---- per-phase breakdown: K more device-resident steps with phase events
+    tr.set_timing(True)
+    D.barrier()
+    for i in range(K):
+        s = W + K + i
+        tr.step_device(s, d_feat[s].data_ptr(), d_lab[s].data_ptr(), None, d_loss.data_ptr())
+    tr.synchronize()
+    phases = dict(tr.phase_times())
+    tr.set_timing(False)
+    D.barrier()
 
     # ---- e2e: host batch -> H2D -> step -> D2H loss, through the public API
     D.barrier()
@@ -215,7 +226,7 @@ def run_ours(args, D):
     w0 = time.perf_counter()
     losses = []
     for i in range(K):
-        s = W + K + i
+        s = W + 2 * K + i
         losses.append(tr.step(s, hf[s], hl[s]))
     torch.cuda.synchronize()
     e2e_s = D.max(time.perf_counter() - w0)

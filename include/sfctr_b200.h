@@ -210,6 +210,10 @@ typedef struct sfctr_step_stats {
   int64_t total_evicted;
   int64_t total_filled_from_host;
   int64_t total_kernel_launches;
+  int64_t total_unique;
+  int64_t total_owned;
+  int64_t total_nvlink_bytes;
+  int64_t total_free_steps; /* steps that ran without a mid-step host wait */
 } sfctr_step_stats;
 int sfctr_trainer_stats(sfctr_trainer* t, sfctr_step_stats* out);
 

@@ -40,6 +40,14 @@ __global__ void compact_kernel(const uint32_t* __restrict__ flag, const uint32_t
   if (i == n - 1) *count = static_cast<int32_t>(rank[i] + flag[i]);
 }
 
+__global__ void own_all_kernel(const int32_t* __restrict__ U_ptr, uint32_t* __restrict__ own_k,
+                               int32_t* __restrict__ count) {
+  const int32_t U = *U_ptr;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < U; j += gridDim.x * blockDim.x)
+    own_k[j] = static_cast<uint32_t>(j);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *count = U;
+}
+
 // Probe the owned features of batch t: hits are touched and marked needed_soon,
 // misses flagged for admission.
 __global__ void probe_kernel(const uint32_t* __restrict__ own_k,
@@ -125,8 +133,8 @@ __global__ void evict_kernel(int32_t n_evict, const uint64_t* __restrict__ sorte
                              const float* __restrict__ mom, const float* __restrict__ vel,
                              const int32_t* __restrict__ steps, float* __restrict__ host_rows,
                              int32_t* __restrict__ host_steps, uint32_t* __restrict__ index,
-                             uint32_t* __restrict__ free_stack, int32_t free_top,
-                             int32_t* __restrict__ err) {
+                             uint32_t* __restrict__ free_stack,
+                             const int32_t* __restrict__ free_top_ptr, int32_t* __restrict__ err) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= n_evict) return;
@@ -156,7 +164,7 @@ __global__ void evict_kernel(int32_t n_evict, const uint64_t* __restrict__ sorte
     host_steps[r] = steps[s];
     index[r] = kOnHost;
     slot_feat[s] = kEmpty;
-    free_stack[free_top + warp] = s;
+    free_stack[*free_top_ptr + warp] = s;
   }
 }
 
@@ -166,18 +174,22 @@ __global__ void evict_kernel(int32_t n_evict, const uint64_t* __restrict__ sorte
 // lane l < kAdmitRows takes row i0 + l (bookkeeping + its lazy-init seed), then all 32
 // lanes fill the group's (row, 16 B chunk) items with 128-bit stores.
 constexpr int kAdmitRows = 8;
-__global__ void admit_kernel(int32_t n_work, const uint32_t* __restrict__ work_j,
+__global__ void admit_kernel(const int32_t* __restrict__ counters, int32_t n_evict,
+                             const uint32_t* __restrict__ work_j,
                              const uint32_t* __restrict__ work_f,
                              const uint32_t* __restrict__ work_w, uint32_t W, int d,
-                             const uint32_t* __restrict__ free_stack, int32_t free_top,
+                             const uint32_t* __restrict__ free_stack,
                              uint32_t* __restrict__ index, const float* __restrict__ host_rows,
                              const int32_t* __restrict__ host_steps, uint64_t seed,
                              uint64_t embed_hash, float* __restrict__ emb, float* __restrict__ mom,
                              float* __restrict__ vel, int32_t* __restrict__ steps,
                              uint32_t* __restrict__ slot_feat, int32_t* __restrict__ last_use,
-                             uint64_t* __restrict__ admit_seq, uint64_t seq0,
+                             uint64_t* __restrict__ admit_seq,
                              int32_t* __restrict__ mark, int32_t t,
                              uint32_t* __restrict__ own_slot, int32_t* __restrict__ n_from_host) {
+  const int32_t n_work = counters[kCntWorking];
+  const int32_t free_top = counters[kCntFreeTop] + n_evict;
+  const uint64_t seq0 = *reinterpret_cast<const uint64_t*>(counters + kCntSeq);
   const int64_t i0 =
       ((blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5) * kAdmitRows;
   const int lane = threadIdx.x & 31;
@@ -261,6 +273,13 @@ __global__ void init_lane_kernel(uint32_t C, uint32_t* slot_feat, int32_t* last_
   }
 }
 
+// device free-stack height and admit_seq after this step's evictions and admissions
+__global__ void advance_kernel(int32_t* counters, int32_t n_evict) {
+  const int32_t n_work = counters[kCntWorking];
+  counters[kCntFreeTop] += n_evict - n_work;
+  *reinterpret_cast<uint64_t*>(counters + kCntSeq) += static_cast<uint64_t>(n_work);
+}
+
 __global__ void fill_u32(uint32_t* p, uint64_t n, uint32_t v) {
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
@@ -328,6 +347,7 @@ void CacheLane::init(uint64_t capacity, int dim, uint64_t owned_rows, uint64_t h
   CUDA_CHECK(cudaMalloc(&temp, std::max(scan_bytes, sort_bytes)));
   CUDA_CHECK(cudaMalloc(&counters, sizeof(int32_t) * 8));
   CUDA_CHECK(cudaMemset(counters, 0, sizeof(int32_t) * 8));
+  CUDA_CHECK(cudaMemcpy(counters + kCntFreeTop, &free_top, sizeof(int32_t), cudaMemcpyHostToDevice));
   CUDA_CHECK(cudaDeviceSynchronize());
 }
 
@@ -352,6 +372,12 @@ void CacheLane::release() {
 void CacheLane::select_owned(const uint32_t* d_gids, const int32_t* d_U, int32_t cap, uint32_t W,
                              uint32_t w, cudaStream_t s) {
   if (cap <= 0) return;
+  if (W == 1) {  // a single worker owns every unique: own_k = identity, count = U
+    own_all_kernel<<<std::max(1, std::min(ceil_div(cap, 256), 148 * 8)), 256, 0, s>>>(
+        d_U, own_k, counters + kCntOwned);
+    CUDA_LAUNCH_CHECK();
+    return;
+  }
   owned_flag_kernel<<<ceil_div(cap, 256), 256, 0, s>>>(d_gids, d_U, cap, W, w, flag);
   CUDA_LAUNCH_CHECK();
   exclusive_scan_u32(temp, scan_bytes, flag, rank, cap, s);
@@ -391,21 +417,22 @@ void CacheLane::evict(int32_t n_evict, uint32_t W, int32_t t, cudaStream_t s) {
                      static_cast<int64_t>(C), 64, s);
   evict_kernel<<<ceil_div(static_cast<int64_t>(n_evict) * 32, 256), 256, 0, s>>>(
       n_evict, keys_sorted, ids_sorted, slot_feat, W, d, emb, mom, vel, steps, host_rows,
-      host_steps, index, free_stack, free_top, counters + kCntError);
+      host_steps, index, free_stack, counters + kCntFreeTop, counters + kCntError);
   CUDA_LAUNCH_CHECK();
-  free_top += n_evict;
 }
 
-void CacheLane::admit(int32_t n_work, const uint32_t* d_gids, uint32_t W, uint64_t seed, int32_t t,
+void CacheLane::admit(int32_t n_bound, int32_t n_evict, uint32_t W, uint64_t seed, int32_t t,
                       cudaStream_t s) {
-  if (n_work <= 0) return;
-  admit_kernel<<<ceil_div(ceil_div(static_cast<int64_t>(n_work), kAdmitRows) * 32, 256), 256, 0, s>>>(
-      n_work, work_j, work_f, work_w, W, d, free_stack, free_top, index, host_rows, host_steps,
-      seed, fnv1a64("embed"), emb, mom, vel, steps, slot_feat, last_use, admit_seq, next_seq, mark,
-      t, own_slot, counters + kCntFromHost);
+  if (n_bound > 0) {
+    admit_kernel<<<ceil_div(ceil_div(static_cast<int64_t>(n_bound), kAdmitRows) * 32, 256), 256, 0,
+                   s>>>(counters, n_evict, work_j, work_f, work_w, W, d, free_stack, index,
+                        host_rows, host_steps, seed, fnv1a64("embed"), emb, mom, vel, steps,
+                        slot_feat, last_use, admit_seq, mark, t, own_slot,
+                        counters + kCntFromHost);
+    CUDA_LAUNCH_CHECK();
+  }
+  advance_kernel<<<1, 1, 0, s>>>(counters, n_evict);
   CUDA_LAUNCH_CHECK();
-  free_top -= n_work;
-  next_seq += static_cast<uint64_t>(n_work);
 }
 
 }  // namespace sfb

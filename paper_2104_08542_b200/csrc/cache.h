@@ -7,7 +7,18 @@
 namespace sfb {
 
 // device counters per lane; kCntMarked = resident slots stamped needed_soon this step
-enum { kCntOwned = 0, kCntWorking = 1, kCntFromHost = 2, kCntError = 3, kCntMarked = 4 };
+// kCntFreeTop = free-stack height and kCntSeq (u64 over [6, 8)) = next admit_seq: both
+// live on the device (admit / evict read and advance them), host copies are refreshed at
+// every step that waits on the host
+enum {
+  kCntOwned = 0,
+  kCntWorking = 1,
+  kCntFromHost = 2,
+  kCntError = 3,
+  kCntMarked = 4,
+  kCntFreeTop = 5,
+  kCntSeq = 6
+};
 
 struct CacheLane {
   uint64_t C = 0;       // slots (cache_capacity)
@@ -26,8 +37,8 @@ struct CacheLane {
   uint64_t* admit_seq = nullptr;  // [C]
   int32_t* mark = nullptr;        // [C] step stamp: needed_soon <=> mark == t
   uint32_t* free_stack = nullptr; // [C] LIFO free list
-  int32_t free_top = 0;           // host mirror of the free-stack height
-  uint64_t next_seq = 0;          // host mirror of next admit_seq
+  int32_t free_top = 0;           // host copy of counters[kCntFreeTop] (refreshed at host waits)
+  uint64_t next_seq = 0;          // host copy of the device admit_seq counter
   uint32_t* index = nullptr;      // [rows] slot | kOnHost | kNever
   float* host_rows = nullptr;     // pinned mapped [host_cap * 3d]
   int32_t* host_steps = nullptr;  // pinned mapped [host_cap]
@@ -54,8 +65,11 @@ struct CacheLane {
   void mark_window(const uint32_t* d_gids, const int32_t* d_U, int32_t cap, uint32_t W, uint32_t w,
                    int32_t t, cudaStream_t s);
   void probe(const uint32_t* d_gids, int32_t cap, uint32_t W, int32_t t, cudaStream_t s);
+  // victims go on top of the device free stack; n_evict is host-known (sync steps only)
   void evict(int32_t n_evict, uint32_t W, int32_t t, cudaStream_t s);
-  void admit(int32_t n_work, const uint32_t* d_gids, uint32_t W, uint64_t seed, int32_t t,
+  // admits counters[kCntWorking] rows (device count, <= n_bound) from the device free
+  // stack, then advances the device free-stack height (+ n_evict - n_work) and admit_seq
+  void admit(int32_t n_bound, int32_t n_evict, uint32_t W, uint64_t seed, int32_t t,
              cudaStream_t s);
 };
 

@@ -14,23 +14,29 @@ __device__ __forceinline__ T ldg_stream(const T* p) {
 }
 
 __global__ void gather_cache_v4(const uint32_t* __restrict__ own_k,
-                                const uint32_t* __restrict__ own_slot, int32_t n_own, int d4,
+                                const uint32_t* __restrict__ own_slot, const int32_t* __restrict__ n_ptr, int32_t n_bound, int d4,
                                 const float4* __restrict__ emb, float4* __restrict__ G) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= static_cast<int64_t>(n_own) * d4) return;
-  const int64_t j = i / d4;
-  const int c = static_cast<int>(i - j * d4);
-  G[static_cast<int64_t>(own_k[j]) * d4 + c] = emb[static_cast<int64_t>(own_slot[j]) * d4 + c];
+  const int32_t n_own = n_ptr ? *n_ptr : n_bound;
+  const int64_t n = static_cast<int64_t>(n_own) * d4;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j = i / d4;
+    const int c = static_cast<int>(i - j * d4);
+    G[static_cast<int64_t>(own_k[j]) * d4 + c] = emb[static_cast<int64_t>(own_slot[j]) * d4 + c];
+  }
 }
 
 __global__ void gather_cache_s(const uint32_t* __restrict__ own_k,
-                               const uint32_t* __restrict__ own_slot, int32_t n_own, int d,
+                               const uint32_t* __restrict__ own_slot, const int32_t* __restrict__ n_ptr, int32_t n_bound, int d,
                                const float* __restrict__ emb, float* __restrict__ G) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= static_cast<int64_t>(n_own) * d) return;
-  const int64_t j = i / d;
-  const int c = static_cast<int>(i - j * d);
-  G[static_cast<int64_t>(own_k[j]) * d + c] = emb[static_cast<int64_t>(own_slot[j]) * d + c];
+  const int32_t n_own = n_ptr ? *n_ptr : n_bound;
+  const int64_t n = static_cast<int64_t>(n_own) * d;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j = i / d;
+    const int c = static_cast<int>(i - j * d);
+    G[static_cast<int64_t>(own_k[j]) * d + c] = emb[static_cast<int64_t>(own_slot[j]) * d + c];
+  }
 }
 
 // Thread per (row, 16 B column chunk); loops over the F fields of the row.
@@ -164,77 +170,88 @@ __global__ void fm_grad_add_kernel(const float* __restrict__ X, int32_t rows, in
 // Lazy Adam: t = adam_steps + 1 per row; bias
 // corrections 1 - beta^t from host-built fp64 tables.
 __global__ void sparse_adam_kernel(const uint32_t* __restrict__ own_k,
-                                   const uint32_t* __restrict__ own_slot, int32_t n_own, int d,
+                                   const uint32_t* __restrict__ own_slot, const int32_t* __restrict__ n_ptr, int32_t n_bound, int d,
                                    const float* __restrict__ dG, float* __restrict__ emb,
                                    float* __restrict__ mom, float* __restrict__ vel,
                                    const int32_t* __restrict__ steps, const float* __restrict__ bc1,
                                    const float* __restrict__ bc2, float lr, float b1, float b2,
                                    float omb1, float omb2, float eps) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= static_cast<int64_t>(n_own) * d) return;
-  const int64_t j = i / d;
-  const int c = static_cast<int>(i - j * d);
-  const uint32_t s = own_slot[j];
-  const int t = steps[s] + 1;
-  const float g = dG[static_cast<int64_t>(own_k ? own_k[j] : j) * d + c];
-  const int64_t o = static_cast<int64_t>(s) * d + c;
-  const float m = b1 * mom[o] + omb1 * g;
-  const float v = b2 * vel[o] + omb2 * g * g;
-  mom[o] = m;
-  vel[o] = v;
-  const float mh = m / bc1[t], vh = v / bc2[t];
-  emb[o] -= lr * mh / (sqrtf(vh) + eps);
+  const int32_t n_own = n_ptr ? *n_ptr : n_bound;
+  const int64_t n = static_cast<int64_t>(n_own) * d;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j = i / d;
+    const int c = static_cast<int>(i - j * d);
+    const uint32_t s = own_slot[j];
+    const int t = steps[s] + 1;
+    const float g = dG[static_cast<int64_t>(own_k ? own_k[j] : j) * d + c];
+    const int64_t o = static_cast<int64_t>(s) * d + c;
+    const float m = b1 * mom[o] + omb1 * g;
+    const float v = b2 * vel[o] + omb2 * g * g;
+    mom[o] = m;
+    vel[o] = v;
+    const float mh = m / bc1[t], vh = v / bc2[t];
+    emb[o] -= lr * mh / (sqrtf(vh) + eps);
+  }
 }
 
 __global__ void sparse_adam_v4(const uint32_t* __restrict__ own_k,
-                               const uint32_t* __restrict__ own_slot, int32_t n_own, int d4,
+                               const uint32_t* __restrict__ own_slot, const int32_t* __restrict__ n_ptr, int32_t n_bound, int d4,
                                const float4* __restrict__ dG, float4* __restrict__ emb,
                                float4* __restrict__ mom, float4* __restrict__ vel,
                                const int32_t* __restrict__ steps, const float* __restrict__ bc1,
                                const float* __restrict__ bc2, float lr, float b1, float b2,
                                float omb1, float omb2, float eps) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= static_cast<int64_t>(n_own) * d4) return;
-  const int64_t j = i / d4;
-  const int c = static_cast<int>(i - j * d4);
-  const uint32_t s = __ldg(own_slot + j);
-  const int t = __ldg(steps + s) + 1;
-  const float c1 = __ldg(bc1 + t), c2 = __ldg(bc2 + t);
-  const float4 g = __ldg(dG + static_cast<int64_t>(own_k ? __ldg(own_k + j) : j) * d4 + c);
-  const int64_t o = static_cast<int64_t>(s) * d4 + c;
-  float4 m = mom[o], v = vel[o], e = emb[o];
-#define SFB_ADAM(X)                                   \
-  m.X = b1 * m.X + omb1 * g.X;                        \
-  v.X = b2 * v.X + omb2 * g.X * g.X;                  \
+  const int32_t n_own = n_ptr ? *n_ptr : n_bound;
+  const int64_t n = static_cast<int64_t>(n_own) * d4;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j = i / d4;
+    const int c = static_cast<int>(i - j * d4);
+    const uint32_t s = __ldg(own_slot + j);
+    const int t = __ldg(steps + s) + 1;
+    const float c1 = __ldg(bc1 + t), c2 = __ldg(bc2 + t);
+    const float4 g = __ldg(dG + static_cast<int64_t>(own_k ? __ldg(own_k + j) : j) * d4 + c);
+    const int64_t o = static_cast<int64_t>(s) * d4 + c;
+    float4 m = mom[o], v = vel[o], e = emb[o];
+#define SFB_ADAM(X)                    \
+  m.X = b1 * m.X + omb1 * g.X;         \
+  v.X = b2 * v.X + omb2 * g.X * g.X;   \
   e.X -= lr * (m.X / c1) / (sqrtf(v.X / c2) + eps);
-  SFB_ADAM(x) SFB_ADAM(y) SFB_ADAM(z) SFB_ADAM(w)
+    SFB_ADAM(x) SFB_ADAM(y) SFB_ADAM(z) SFB_ADAM(w)
 #undef SFB_ADAM
-  mom[o] = m;
-  vel[o] = v;
-  emb[o] = e;
+    mom[o] = m;
+    vel[o] = v;
+    emb[o] = e;
+  }
 }
 
-__global__ void steps_inc_kernel(const uint32_t* __restrict__ own_slot, int32_t n_own,
+__global__ void steps_inc_kernel(const uint32_t* __restrict__ own_slot, const int32_t* __restrict__ n_ptr, int32_t n_bound,
                                  int32_t* __restrict__ steps) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j < n_own) steps[own_slot[j]] += 1;
+  const int32_t n_own = n_ptr ? *n_ptr : n_bound;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n_own; j += gridDim.x * blockDim.x)
+    steps[own_slot[j]] += 1;
 }
 
 }  // namespace
 
 int fm_sq_parts(int d) { return (d & 3) == 0 ? d / 4 : d; }
 
-void gather_cache(const uint32_t* own_k, const uint32_t* own_slot, int32_t n_own, const float* emb,
-                  int d, float* G, cudaStream_t s) {
+// grid for the count-bounded grid-stride kernels: one resident wave of 256-thread CTAs
+// (148 SMs x 8), fewer when the bound is small; the device count ends the loops
+static int wave_grid(int64_t n_bound) { return std::max(1, std::min(ceil_div(n_bound, 256), 148 * 8)); }
+
+void gather_cache(const uint32_t* own_k, const uint32_t* own_slot, int32_t n_own,
+                  const int32_t* d_n_own, const float* emb, int d, float* G, cudaStream_t s) {
   if (n_own <= 0) return;
   if ((d & 3) == 0) {
     const int64_t n = static_cast<int64_t>(n_own) * (d / 4);
-    gather_cache_v4<<<ceil_div(n, 256), 256, 0, s>>>(own_k, own_slot, n_own, d / 4,
+    gather_cache_v4<<<wave_grid(n), 256, 0, s>>>(own_k, own_slot, d_n_own, n_own, d / 4,
                                                      reinterpret_cast<const float4*>(emb),
                                                      reinterpret_cast<float4*>(G));
   } else {
     const int64_t n = static_cast<int64_t>(n_own) * d;
-    gather_cache_s<<<ceil_div(n, 256), 256, 0, s>>>(own_k, own_slot, n_own, d, emb, G);
+    gather_cache_s<<<wave_grid(n), 256, 0, s>>>(own_k, own_slot, d_n_own, n_own, d, emb, G);
   }
   CUDA_LAUNCH_CHECK();
 }
@@ -288,7 +305,7 @@ void segment_sum(const uint32_t* vid, int32_t n, int F, int d, int ldx, const fl
 }
 
 void sparse_adam(const uint32_t* own_k /* gradient row index, or null = j */,
-                 const uint32_t* own_slot, int32_t n_own, const float* dG,
+                 const uint32_t* own_slot, int32_t n_own, const int32_t* d_n_own, const float* dG,
                  int d, float* emb, float* mom, float* vel, int32_t* steps, const float* bc1,
                  const float* bc2, float lr, double beta1, double beta2, float eps, cudaStream_t s) {
   if (n_own <= 0) return;
@@ -296,18 +313,18 @@ void sparse_adam(const uint32_t* own_k /* gradient row index, or null = j */,
   const float omb2 = static_cast<float>(1.0 - beta2);
   if ((d & 3) == 0) {
     const int64_t n = static_cast<int64_t>(n_own) * (d / 4);
-    sparse_adam_v4<<<ceil_div(n, 256), 256, 0, s>>>(
-        own_k, own_slot, n_own, d / 4, reinterpret_cast<const float4*>(dG),
+    sparse_adam_v4<<<wave_grid(n), 256, 0, s>>>(
+        own_k, own_slot, d_n_own, n_own, d / 4, reinterpret_cast<const float4*>(dG),
         reinterpret_cast<float4*>(emb), reinterpret_cast<float4*>(mom),
         reinterpret_cast<float4*>(vel), steps, bc1, bc2, lr, beta1, beta2, omb1, omb2, eps);
   } else {
     const int64_t n = static_cast<int64_t>(n_own) * d;
-    sparse_adam_kernel<<<ceil_div(n, 256), 256, 0, s>>>(own_k, own_slot, n_own, d, dG, emb, mom,
+    sparse_adam_kernel<<<wave_grid(n), 256, 0, s>>>(own_k, own_slot, d_n_own, n_own, d, dG, emb, mom,
                                                         vel, steps, bc1, bc2, lr, beta1, beta2,
                                                         omb1, omb2, eps);
   }
   CUDA_LAUNCH_CHECK();
-  steps_inc_kernel<<<ceil_div(n_own, 256), 256, 0, s>>>(own_slot, n_own, steps);
+  steps_inc_kernel<<<wave_grid(n_own), 256, 0, s>>>(own_slot, d_n_own, n_own, steps);
   CUDA_LAUNCH_CHECK();
 }
 

@@ -142,6 +142,9 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
   CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_scalars_), sizeof(int32_t) * 8, 0));
   CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_counts_), sizeof(int32_t) * 8 * lanes_, 0));
   CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_loss_), sizeof(float), 0));
+  CUDA_CHECK(cudaMalloc(&d_acc_, sizeof(int64_t) * 8));
+  CUDA_CHECK(cudaMemset(d_acc_, 0, sizeof(int64_t) * 8));
+  CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_acc_), sizeof(int64_t) * 8, 0));
   tower_.init(b_, K_, H_, d_);
   towertc_.init(b_, K_, H_, d_);
   // validation switch: the fp32 SIMT tiles instead of tcgen05 (only when rows are unpadded)
@@ -160,6 +163,7 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
   const int64_t umax = std::min<int64_t>(n_global_, static_cast<int64_t>(cfg_.vocabulary_size));
   for (int l = 0; l < lanes_; ++l)
     lane_[l].init(cfg_.cache_capacity, d_, owned_rows, host_rows, umax);
+  free_lb_.assign(lanes_, static_cast<int64_t>(cfg_.cache_capacity));
   if (world_ > 1 && cfg_.sync_mode == SFCTR_SYNC_ALLTOALL) {
     if (lanes_ != 1) fail(kConfig, "sync=alltoall needs one worker per process");
     if (W_ > 8) fail(kConfig, "sync=alltoall supports at most 8 workers (one NVSwitch box)");
@@ -199,8 +203,9 @@ Trainer::~Trainer() {
                   static_cast<void*>(d_dense_), static_cast<void*>(d_dense_m_),
                   static_cast<void*>(d_dense_v_), static_cast<void*>(d_grads_),
                   static_cast<void*>(d_loss_), static_cast<void*>(d_bc1_),
-                  static_cast<void*>(d_bc2_)})
+                  static_cast<void*>(d_bc2_), static_cast<void*>(d_acc_)})
     if (p) cudaFree(p);
+  if (h_acc_) cudaFreeHost(h_acc_);
   if (h_scalars_) cudaFreeHost(h_scalars_);
   if (h_counts_) cudaFreeHost(h_counts_);
   if (h_loss_) cudaFreeHost(h_loss_);
@@ -227,6 +232,40 @@ void Trainer::ensure_bias_tables(int64_t t_max) {
   CUDA_CHECK(cudaMemcpy(d_bc2_, b2.data(), sizeof(float) * (cap + 1), cudaMemcpyHostToDevice));
   bc_cap_ = cap;
 }
+
+namespace {
+
+struct LaneCounters {
+  const int32_t* c[8];
+};
+
+// totals of a step that skipped the host wait: U, owned, working, interworker ledger bytes
+// (allreduce_bytes per worker, comm.hpp:36-41, with the per-step integer division)
+__global__ void acc_kernel(LaneCounters lc, int lanes, const int32_t* __restrict__ U_ptr,
+                           int64_t* __restrict__ acc, int W, int d, int64_t P) {
+  int64_t owned = 0, working = 0;
+  for (int l = 0; l < lanes; ++l) {
+    owned += lc.c[l][kCntOwned];
+    working += lc.c[l][kCntWorking];
+  }
+  const int64_t U = *U_ptr;
+  auto arb = [&](int64_t p) { return 2 * static_cast<int64_t>(W - 1) * p / W; };
+  acc[0] += U;
+  acc[1] += owned;
+  acc[2] += working;
+  acc[3] += static_cast<int64_t>(lanes) * (2 * arb(U * d * 4) + arb(P * 4));
+}
+
+// dG[0 : U*d) = 0 with U read on the device
+__global__ void zero_rows_kernel(float4* __restrict__ p, const int32_t* __restrict__ U_ptr, int d4,
+                                 int64_t bound) {
+  const int64_t n = static_cast<int64_t>(*U_ptr) * d4;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n && i < bound;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    p[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+}  // namespace
 
 void Trainer::phase(const char* name) {
   if (!timing_) return;
@@ -275,11 +314,16 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
     next.total_evicted = stats_.total_evicted;
     next.total_filled_from_host = stats_.total_filled_from_host;
     next.total_kernel_launches = stats_.total_kernel_launches;
+    next.total_unique = stats_.total_unique;
+    next.total_owned = stats_.total_owned;
+    next.total_nvlink_bytes = stats_.total_nvlink_bytes;
     stats_ = next;
   }
 
   // ---- Data-Loader: ids to u32, all-gather the global batch, VSI (Algorithm 1 l.2-3)
-  CUDA_CHECK(cudaMemsetAsync(d_scalars_, 0, sizeof(int32_t) * 8, s));
+  // [1] (bad-id flag) is sticky until a host check has seen it
+  CUDA_CHECK(cudaMemsetAsync(d_scalars_, 0, sizeof(int32_t), s));
+  CUDA_CHECK(cudaMemsetAsync(d_scalars_ + 2, 0, sizeof(int32_t) * 6, s));
   ids_to_u32(d_features, d_ids32_, n_local_, cfg_.vocabulary_size, d_scalars_ + 1, s);
   const uint32_t* gids = d_ids32_;
   if (world_ > 1) {
@@ -297,7 +341,7 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   for (int l = 0; l < lanes_; ++l) {
     // per-step counters; kCntFromHost (index 2) stays cumulative
     CUDA_CHECK(cudaMemsetAsync(lane_[l].counters, 0, sizeof(int32_t) * 2, s));
-    CUDA_CHECK(cudaMemsetAsync(lane_[l].counters + 3, 0, sizeof(int32_t) * 5, s));
+    CUDA_CHECK(cudaMemsetAsync(lane_[l].counters + 3, 0, sizeof(int32_t) * 2, s));
     lane_[l].select_owned(d_uniq_, d_scalars_ + 0, cap, Wu, static_cast<uint32_t>(lane0_ + l), s);
   }
   // window batches t+1..t+L-1 (needed_soon), one at a time through the window scratch
@@ -324,44 +368,65 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
                                cudaMemcpyDeviceToHost, s));
     phase("exchange_plan");
   }
-  CUDA_CHECK(cudaMemcpyAsync(h_scalars_, d_scalars_, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost, s));
-  for (int l = 0; l < lanes_; ++l)
-    CUDA_CHECK(cudaMemcpyAsync(h_counts_ + 8 * l, lane_[l].counters, sizeof(int32_t) * 8,
-                               cudaMemcpyDeviceToHost, s));
-  CUDA_CHECK(cudaStreamSynchronize(s));
-  const int32_t U = h_scalars_[0];
-  if (h_scalars_[1]) fail(kLogic, "feature id >= vocabulary size in the batch", step);
-  stats_.unique = U;
-  std::vector<int32_t> n_own(lanes_), n_work(lanes_);
-  for (int l = 0; l < lanes_; ++l) n_own[l] = h_counts_[8 * l + kCntOwned];
-  // capacity check before any state moves (push_parameters_to_cache deadlock)
-  for (int l = 0; l < lanes_; ++l) {
-    n_work[l] = n_own[l] > 0 ? h_counts_[8 * l + kCntWorking] : 0;
-    const CacheLane& L = lane_[l];
-    const int64_t occupied = static_cast<int64_t>(L.C) - L.free_top;
-    const int64_t marked = h_counts_[8 * l + kCntMarked];
-    const int64_t evictable = occupied - marked;
-    if (n_work[l] > L.free_top + evictable)
-      fail(kRun,
-           "capacity deadlock on worker " + std::to_string(lane0_ + l) + ": need " +
-               std::to_string(n_work[l]) + " slots, " + std::to_string(L.free_top + evictable) +
-               " free or evictable (capacity=" + std::to_string(L.C) +
-               " occupied=" + std::to_string(occupied) + " free=" + std::to_string(L.free_top) +
-               " pinned=0 needed_soon=" + std::to_string(marked) + ")",
-           step);
-  }
-  for (int l = 0; l < lanes_; ++l) {
-    CacheLane& L = lane_[l];
-    const int32_t n_evict = std::max<int32_t>(0, n_work[l] - L.free_top);
-    L.evict(n_evict, Wu, t, s);
-    L.admit(n_work[l], d_uniq_, Wu, cfg_.seed, t, s);
-    led_[0] += static_cast<int64_t>(n_work[l]) * d_ * 12;
-    led_[1] += static_cast<int64_t>(n_evict) * d_ * 12;
-    led_[3] += n_evict;
-    stats_.owned += n_own[l];
-    stats_.working += n_work[l];
-    stats_.evicted += n_evict;
-    stats_.pcie_d2h_bytes += static_cast<int64_t>(n_evict) * (3 * d_ + 1) * 4;
+  // Host wait: needed for evictions (the LRU victim count), the capacity check and the
+  // NCCL / exchange sizes. A single-process step whose admissions provably fit the free
+  // slots (free_lb_ >= the per-step admission bound umax) skips it: every kernel below
+  // reads the unique / owned / working counts from the device.
+  const int64_t bound = lane_[0].umax;
+  bool free_step = world_ == 1;
+  for (int l = 0; l < lanes_ && free_step; ++l) free_step = free_lb_[l] >= bound;
+  int32_t U = 0;
+  std::vector<int32_t> n_own(lanes_, static_cast<int32_t>(bound)), n_work(lanes_, 0);
+  if (!free_step) {
+    CUDA_CHECK(cudaMemcpyAsync(h_scalars_, d_scalars_, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost, s));
+    for (int l = 0; l < lanes_; ++l)
+      CUDA_CHECK(cudaMemcpyAsync(h_counts_ + 8 * l, lane_[l].counters, sizeof(int32_t) * 8,
+                                 cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    U = h_scalars_[0];
+    if (h_scalars_[1]) fail(kLogic, "feature id >= vocabulary size in the batch", step);
+    stats_.unique = U;
+    for (int l = 0; l < lanes_; ++l) {
+      CacheLane& L = lane_[l];
+      n_own[l] = h_counts_[8 * l + kCntOwned];
+      L.free_top = h_counts_[8 * l + kCntFreeTop];
+      std::memcpy(&L.next_seq, h_counts_ + 8 * l + kCntSeq, sizeof(uint64_t));
+    }
+    // capacity check before any state moves (push_parameters_to_cache deadlock)
+    for (int l = 0; l < lanes_; ++l) {
+      n_work[l] = n_own[l] > 0 ? h_counts_[8 * l + kCntWorking] : 0;
+      const CacheLane& L = lane_[l];
+      const int64_t occupied = static_cast<int64_t>(L.C) - L.free_top;
+      const int64_t marked = h_counts_[8 * l + kCntMarked];
+      const int64_t evictable = occupied - marked;
+      if (n_work[l] > L.free_top + evictable)
+        fail(kRun,
+             "capacity deadlock on worker " + std::to_string(lane0_ + l) + ": need " +
+                 std::to_string(n_work[l]) + " slots, " + std::to_string(L.free_top + evictable) +
+                 " free or evictable (capacity=" + std::to_string(L.C) +
+                 " occupied=" + std::to_string(occupied) + " free=" + std::to_string(L.free_top) +
+                 " pinned=0 needed_soon=" + std::to_string(marked) + ")",
+             step);
+    }
+    for (int l = 0; l < lanes_; ++l) {
+      CacheLane& L = lane_[l];
+      const int32_t n_evict = std::max<int32_t>(0, n_work[l] - L.free_top);
+      L.evict(n_evict, Wu, t, s);
+      L.admit(n_work[l], n_evict, Wu, cfg_.seed, t, s);
+      free_lb_[l] = static_cast<int64_t>(L.free_top) + n_evict - n_work[l];
+      led_[0] += static_cast<int64_t>(n_work[l]) * d_ * 12;
+      led_[1] += static_cast<int64_t>(n_evict) * d_ * 12;
+      led_[3] += n_evict;
+      stats_.owned += n_own[l];
+      stats_.working += n_work[l];
+      stats_.evicted += n_evict;
+      stats_.pcie_d2h_bytes += static_cast<int64_t>(n_evict) * (3 * d_ + 1) * 4;
+    }
+  } else {
+    for (int l = 0; l < lanes_; ++l) {
+      lane_[l].admit(static_cast<int32_t>(bound), 0, Wu, cfg_.seed, t, s);
+      free_lb_[l] -= bound;
+    }
   }
   phase("manage_evict_admit");
 
@@ -369,7 +434,7 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   const size_t ud = static_cast<size_t>(U) * d_;
   // rows of the table the lanes gather from: all U uniques (all-reduce scheme) or
   // only the ones this rank touches (owner-routed all-to-all)
-  size_t table_rows = static_cast<size_t>(U);
+  size_t table_rows = free_step ? static_cast<size_t>(n_global_) : static_cast<size_t>(U);
   if (a2a_) {
     xch_.set_counts(h_totals_);
     stats_.nvlink_bytes += xch_.forward(lane_[0].own_k, lane_[0].own_slot, n_own[0],
@@ -382,7 +447,8 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   } else {
     if (world_ > 1) CUDA_CHECK(cudaMemsetAsync(d_G_, 0, sizeof(float) * ud, s));
     for (int l = 0; l < lanes_; ++l)
-      gather_cache(lane_[l].own_k, lane_[l].own_slot, n_own[l], lane_[l].emb, d_, d_G_, s);
+      gather_cache(lane_[l].own_k, lane_[l].own_slot, n_own[l], lane_[l].counters + kCntOwned,
+                   lane_[l].emb, d_, d_G_, s);
     phase("gather_cache");
     if (world_ > 1) {
       NCCL_CHECK(ncclAllReduce(d_G_, d_G_, ud, ncclFloat32, ncclSum, comm_, s));
@@ -393,10 +459,14 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   // interworker ledger: the reference's accounting model, allreduce_bytes per
   // worker for each all-reduce, whatever the device scheme
   auto arb = [&](int64_t payload) { return 2 * static_cast<int64_t>(W_ - 1) * payload / W_; };
-  led_[2] += static_cast<int64_t>(lanes_) * arb(static_cast<int64_t>(ud) * 4);
+  if (!free_step) led_[2] += static_cast<int64_t>(lanes_) * arb(static_cast<int64_t>(ud) * 4);
 
   // ---- per lane: gather_instances, forward_backward, segment_sum (l.11-12)
-  CUDA_CHECK(cudaMemsetAsync(d_dG_, 0, sizeof(float) * table_rows * d_, s));
+  if (free_step && d_ % 4 == 0)
+    zero_rows_kernel<<<148 * 8, 256, 0, s>>>(reinterpret_cast<float4*>(d_dG_), d_scalars_ + 0,
+                                             d_ / 4, n_global_ * (d_ / 4));
+  else
+    CUDA_CHECK(cudaMemsetAsync(d_dG_, 0, sizeof(float) * table_rows * d_, s));
   const float emb_scale = 1.f / static_cast<float>(W_);
   for (int l = 0; l < lanes_; ++l) {
     const uint32_t* vid =
@@ -442,14 +512,16 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
     NCCL_CHECK(ncclAllReduce(d_grads_, d_grads_, P_ + 1, ncclFloat32, ncclSum, comm_, s));
     stats_.nvlink_bytes += static_cast<int64_t>(P_ + 1) * 4;
   }
-  led_[2] += static_cast<int64_t>(lanes_) *
-             (arb(static_cast<int64_t>(ud) * 4) + arb(static_cast<int64_t>(P_) * 4));
+  if (!free_step)
+    led_[2] += static_cast<int64_t>(lanes_) *
+               (arb(static_cast<int64_t>(ud) * 4) + arb(static_cast<int64_t>(P_) * 4));
   phase(a2a_ ? "exchange_grad" : "allreduce_grad");
 
   // ---- update_sparse (l.14) + dense Adam
   ensure_bias_tables(steps_done_ + 2);
   for (int l = 0; l < lanes_; ++l)
-    sparse_adam(a2a_ ? nullptr : lane_[l].own_k, lane_[l].own_slot, n_own[l], grad_rows, d_,
+    sparse_adam(a2a_ ? nullptr : lane_[l].own_k, lane_[l].own_slot, n_own[l],
+                lane_[l].counters + kCntOwned, grad_rows, d_,
                 lane_[l].emb,
                 lane_[l].mom, lane_[l].vel, lane_[l].steps, d_bc1_, d_bc2_,
                 static_cast<float>(cfg_.learning_rate), static_cast<float>(cfg_.adam_beta1),
@@ -467,11 +539,26 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
                                         d_loss ? d_loss : d_loss_);
   CUDA_LAUNCH_CHECK();
   phase("dense_adam");
+  if (free_step) {
+    LaneCounters lc{};
+    for (int l = 0; l < lanes_; ++l) lc.c[l] = lane_[l].counters;
+    acc_kernel<<<1, 1, 0, s>>>(lc, lanes_, d_scalars_ + 0, d_acc_, W_, d_,
+                               static_cast<int64_t>(P_));
+    CUDA_LAUNCH_CHECK();
+    acc_pending_ = true;
+    free_steps_ += 1;
+  }
+  last_step_free_ = free_step;
   steps_done_ += 1;
   stats_.kernel_launches = g_launches - launches0;
   stats_.total_steps += 1;
-  stats_.total_working += stats_.working;
+  if (!free_step) {  // free steps fold their device totals in at the next refresh()
+    stats_.total_working += stats_.working;
+    stats_.total_unique += stats_.unique;
+    stats_.total_owned += stats_.owned;
+  }
   stats_.total_evicted += stats_.evicted;
+  stats_.total_nvlink_bytes += stats_.nvlink_bytes;
   stats_.total_kernel_launches += stats_.kernel_launches;
 }
 
@@ -479,6 +566,12 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
 // and the number of admissions that read a row back from the host table
 // (cumulative on the device; the delta covers every step since the last call).
 void Trainer::check_device_errors(int64_t step) {
+  int32_t bad = 0;
+  CUDA_CHECK(cudaMemcpy(&bad, d_scalars_ + 1, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if (bad) {
+    CUDA_CHECK(cudaMemset(d_scalars_ + 1, 0, sizeof(int32_t)));
+    fail(kLogic, "feature id >= vocabulary size in the batch", step);
+  }
   int64_t cum = 0;
   for (int l = 0; l < lanes_; ++l) {
     int32_t c[8];
@@ -514,14 +607,59 @@ double Trainer::step_host(int64_t step, const uint64_t* features, const uint8_t*
   CUDA_CHECK(cudaMemcpyAsync(h_loss_, d_loss_, sizeof(float), cudaMemcpyDeviceToHost, stream_));
   CUDA_CHECK(cudaStreamSynchronize(stream_));
   check_device_errors(step);
+  refresh();
   finish_phases();
   return static_cast<double>(*h_loss_);
+}
+
+void Trainer::refresh() {
+  CUDA_CHECK(cudaSetDevice(dev_));
+  CUDA_CHECK(cudaStreamSynchronize(stream_));
+  if (acc_pending_) {
+    CUDA_CHECK(cudaMemcpy(h_acc_, d_acc_, sizeof(int64_t) * 8, cudaMemcpyDeviceToHost));
+    CUDA_CHECK(cudaMemset(d_acc_, 0, sizeof(int64_t) * 8));
+    stats_.total_unique += h_acc_[0];
+    stats_.total_owned += h_acc_[1];
+    stats_.total_working += h_acc_[2];
+    led_[0] += h_acc_[2] * d_ * 12;
+    led_[2] += h_acc_[3];
+    acc_pending_ = false;
+  }
+  for (int l = 0; l < lanes_; ++l) {
+    int32_t c[8];
+    CUDA_CHECK(cudaMemcpy(c, lane_[l].counters, sizeof(c), cudaMemcpyDeviceToHost));
+    lane_[l].free_top = c[kCntFreeTop];
+    std::memcpy(&lane_[l].next_seq, c + kCntSeq, sizeof(uint64_t));
+    free_lb_[l] = lane_[l].free_top;
+    if (last_step_free_) {  // per-step counters of the last step, read back now
+      if (l == 0) {
+        int32_t U = 0;
+        CUDA_CHECK(cudaMemcpy(&U, d_scalars_, sizeof(int32_t), cudaMemcpyDeviceToHost));
+        stats_.unique = U;
+        stats_.owned = stats_.working = 0;
+      }
+      stats_.owned += c[kCntOwned];
+      stats_.working += c[kCntWorking];
+    }
+  }
+}
+
+sfctr_step_stats Trainer::stats() {
+  refresh();
+  stats_.total_free_steps = free_steps_;
+  return stats_;
+}
+
+uint64_t Trainer::free_count(int lane) {
+  refresh();
+  return static_cast<uint64_t>(lane_.at(lane).free_top);
 }
 
 void Trainer::synchronize() {
   CUDA_CHECK(cudaSetDevice(dev_));
   CUDA_CHECK(cudaStreamSynchronize(stream_));
   check_device_errors(steps_done_ - 1);
+  refresh();
   finish_phases();
 }
 
@@ -618,7 +756,8 @@ void Trainer::set_dense(const float* w1, const float* b1, const float* w2, const
   if (b2) CUDA_CHECK(cudaMemcpy(d_dense_ + kh + 2 * H_, b2, sizeof(float), cudaMemcpyHostToDevice));
 }
 
-void Trainer::ledger(int64_t out[4]) const {
+void Trainer::ledger(int64_t out[4]) {
+  refresh();
   for (int i = 0; i < 4; ++i) out[i] = led_[i];
 }
 

@@ -27,6 +27,7 @@ class Trainer {
   double step_host(int64_t step, const uint64_t* features, const uint8_t* labels,
                    const uint64_t* window);
   void synchronize();
+  int64_t free_steps() const { return free_steps_; }
 
   cudaStream_t stream() const { return stream_; }
   int lanes() const { return lanes_; }
@@ -34,12 +35,12 @@ class Trainer {
 
   void logits(float* out);
   void cache_slots(int lane, uint64_t* feature, int64_t* last_use, uint64_t* admit_seq);
-  uint64_t free_count(int lane) const { return static_cast<uint64_t>(lane_.at(lane).free_top); }
+  uint64_t free_count(int lane);
   int64_t snapshot(uint64_t* features, float* rows, int64_t* steps);
   void get_dense(float* w1, float* b1, float* w2, float* b2);
   void set_dense(const float* w1, const float* b1, const float* w2, const float* b2);
-  void ledger(int64_t out[4]) const;
-  sfctr_step_stats stats() const { return stats_; }
+  void ledger(int64_t out[4]);
+  sfctr_step_stats stats();
   // enabling (re)starts the per-phase accumulation; phase_times() returns the
   // per-phase device-time sums over the steps run since
   void set_timing(bool on) {
@@ -56,6 +57,9 @@ class Trainer {
   void phase(const char* name);
   void finish_phases();
   void check_device_errors(int64_t step);
+  // waits for the stream, folds the device-side totals of host-wait-free steps into the
+  // host ledger / stats, refreshes the per-step counters and the free-stack copies
+  void refresh();
 
   sfctr_config cfg_;
   int rank_, world_, lanes_, W_, lane0_, dev_;
@@ -108,6 +112,16 @@ class Trainer {
   int64_t dense_steps_ = 0;
   int64_t steps_done_ = 0;
   int64_t led_[4] = {0, 0, 0, 0};
+  // Steps that need no host wait (world 1, no eviction possible) run the manager on
+  // device counts alone: free_lb_[l] is a lower bound of lane l's device free-stack
+  // height (exact after every waiting step, minus the per-step admission bound after
+  // each free one); d_acc_ accumulates their totals: U, owned, working, interworker bytes
+  std::vector<int64_t> free_lb_;
+  int64_t* d_acc_ = nullptr;
+  int64_t* h_acc_ = nullptr;
+  bool acc_pending_ = false;    // d_acc_ holds steps not folded into the host totals yet
+  bool last_step_free_ = false; // the last step skipped the host wait
+  int64_t free_steps_ = 0;      // steps run without a host wait (for the bench / tests)
   int64_t from_host_seen_ = 0;
   sfctr_step_stats stats_{};
 

@@ -107,7 +107,8 @@ class StepStats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in (
         "unique", "owned", "working", "evicted", "filled_from_host", "pcie_h2d_bytes",
         "pcie_d2h_bytes", "nvlink_bytes", "kernel_launches", "total_steps", "total_working",
-        "total_evicted", "total_filled_from_host", "total_kernel_launches")]
+        "total_evicted", "total_filled_from_host", "total_kernel_launches", "total_unique",
+        "total_owned", "total_nvlink_bytes", "total_free_steps")]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
