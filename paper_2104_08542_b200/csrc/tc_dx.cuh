@@ -124,25 +124,26 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
-      constexpr uint32_t id128 = idesc_tf32(BM, 128, 0, 0);
-      constexpr uint32_t id64 = idesc_tf32(BM, 64, 0, 0);
-      int cur_m = -1, gen = 0;
-      for (int t = t0, i = 0; t < t1; ++t, ++i) {
-        const int m = t / p.n_tiles;
-        if (m != cur_m) {
-          mbar_wait(a_full, gen & 1);
-          cur_m = m;
-          ++gen;
-        }
-        const int s = i % BS, buf = i & 1;
-        mbar_wait(acc_empty + buf, ((i >> 1) & 1) ^ 1);
-        mbar_wait(b_full + s, (i / BS) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  } else if (warp == 1) {  // ---------------- MMA issuer (warp-wide loop, elected issue)
+    constexpr uint32_t id128 = idesc_tf32(BM, 128, 0, 0);
+    constexpr uint32_t id64 = idesc_tf32(BM, 64, 0, 0);
+    const uint32_t as = smem_u32(a_s);
+    const uint32_t bs0 = smem_u32(b_s);
+    int cur_m = -1, gen = 0;
+    for (int t = t0, i = 0; t < t1; ++t, ++i) {
+      const int m = t / p.n_tiles;
+      if (m != cur_m) {
+        mbar_wait(a_full, gen & 1);
+        cur_m = m;
+        ++gen;
+      }
+      const int s = i % BS, buf = i & 1;
+      mbar_wait(acc_empty + buf, ((i >> 1) & 1) ^ 1);
+      mbar_wait(b_full + s, (i / BS) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (elect_one()) {
         const uint32_t d = tmem + static_cast<uint32_t>(buf) * 128u;
-        const uint32_t bs = smem_u32(b_s + s * L::B_STAGE);
-        const uint32_t as = smem_u32(a_s);
+        const uint32_t bs = bs0 + static_cast<uint32_t>(s) * L::B_STAGE;
 #pragma unroll
         for (int kb = 0; kb < 2; ++kb) {
 #pragma unroll
@@ -159,6 +160,7 @@ __global__ void __launch_bounds__(192, 1)
         const int mn = (t + 1) / p.n_tiles;
         if (t + 1 >= t1 || mn != m) mma_commit(a_empty);
       }
+      __syncwarp();
     }
   } else {  // ---------------- epilogue
     const int q = warp & 3;

@@ -181,32 +181,36 @@ __global__ void __launch_bounds__(kTsThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
-      constexpr uint32_t id128 = idesc_tf32(BM, 2 * BN, 0, B_MN ? 1 : 0);
-      constexpr uint32_t id64 = idesc_tf32(BM, BN, 0, B_MN ? 1 : 0);
-      for (int i = 0; i < nkb; ++i) {
-        const int t = i % TS, s = i % RB;
-        if (!(p.dbg & 32)) mbar_wait(t_ready + t, (i / TS) & 1);
-        if (tr && i < 64) p.trace[256 + i] = clock64();
-        if (!(p.dbg & 32)) mbar_wait(b_full + s, (i / RB) & 1);
-        if (tr && i < 64) p.trace[192 + i] = clock64();
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  } else if (warp == 1) {  // ---------------- MMA issuer (warp-wide loop, elected issue)
+    constexpr uint32_t id128 = idesc_tf32(BM, 2 * BN, 0, B_MN ? 1 : 0);
+    constexpr uint32_t id64 = idesc_tf32(BM, BN, 0, B_MN ? 1 : 0);
+    const uint32_t b0 = smem_u32(b_ring);
+    for (int i = 0; i < nkb; ++i) {
+      const int t = i % TS, s = i % RB;
+      mbar_wait(t_ready + t, (i / TS) & 1);
+      if (tr && lane == 0 && i < 64) p.trace[256 + i] = clock64();
+      mbar_wait(b_full + s, (i / RB) & 1);
+      if (tr && lane == 0 && i < 64) p.trace[192 + i] = clock64();
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (elect_one()) {
+        const uint32_t bs = b0 + static_cast<uint32_t>(s) * L::B_STAGE;
+        const uint32_t at = tmem + 128u + static_cast<uint32_t>(t) * 64u;
 #pragma unroll
         for (int kk = 0; kk < BKE / 8; ++kk) {
           uint64_t bd;
-          if constexpr (B_MN) bd = smem_desc(smem_u32(b_hi(s)) + kk * 1024, 4096, 512, 1);
-          else bd = smem_desc(smem_u32(b_hi(s)) + kk * 32, 16, 1024);
-          const uint32_t ah = a_col(t) + kk * 8, al = a_col(t) + 32 + kk * 8;
+          if constexpr (B_MN) bd = smem_desc(bs + kk * 1024, 4096, 512, 1);
+          else bd = smem_desc(bs + kk * 32, 16, 1024);
           if (p.dbg & 2) continue;
-          mma_tf32_ts(tmem, ah, bd, id128, (i > 0 || kk > 0) ? 1u : 0u);  // [hh | hl]
-          mma_tf32_ts(tmem, al, bd, id64, 1u);                              // += lh
+          mma_tf32_ts(tmem, at + kk * 8, bd, id128, (i > 0 || kk > 0) ? 1u : 0u);  // [hh | hl]
+          mma_tf32_ts(tmem, at + 32 + kk * 8, bd, id64, 1u);                         // += lh
         }
         mma_commit(b_empty + s);
         mma_commit(t_empty + t);
       }
-      mma_commit(tmem_full);
+      __syncwarp();
     }
+    if (elect_one()) mma_commit(tmem_full);
+    __syncwarp();
   } else {
     // ---------------- split: raw A row -> tf32 hi / lo columns in TMEM. The two warp
     // groups take alternate k-blocks so one group's TMEM-store latency overlaps the
