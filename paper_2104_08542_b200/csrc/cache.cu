@@ -25,11 +25,18 @@ namespace {
 // Counts live on the device (U, n_own): grids cover the upper bound `cap`
 // and entries past the live count are flagged 0, so no host round trip is
 // needed to size the manage kernels.
+// first != nullptr: also clears the VSI first-position table behind the batch
+// (the reset VSI would otherwise launch separately; every unique passes here once)
 __global__ void owned_flag_kernel(const uint32_t* __restrict__ gids,
                                   const int32_t* __restrict__ U_ptr, int32_t cap, uint32_t W,
-                                  uint32_t w, uint32_t* __restrict__ flag) {
+                                  uint32_t w, uint32_t* __restrict__ flag,
+                                  uint32_t* __restrict__ first) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < cap) flag[i] = (i < *U_ptr && gids[i] % W == w) ? 1u : 0u;
+  if (i >= cap) return;
+  const bool live = i < *U_ptr;
+  const uint32_t f = live ? gids[i] : 0u;
+  flag[i] = (live && f % W == w) ? 1u : 0u;
+  if (first && live) first[f] = kEmpty;
 }
 
 __global__ void compact_kernel(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ rank,
@@ -41,10 +48,13 @@ __global__ void compact_kernel(const uint32_t* __restrict__ flag, const uint32_t
 }
 
 __global__ void own_all_kernel(const int32_t* __restrict__ U_ptr, uint32_t* __restrict__ own_k,
-                               int32_t* __restrict__ count) {
+                               int32_t* __restrict__ count, const uint32_t* __restrict__ gids,
+                               uint32_t* __restrict__ first) {
   const int32_t U = *U_ptr;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < U; j += gridDim.x * blockDim.x)
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < U; j += gridDim.x * blockDim.x) {
     own_k[j] = static_cast<uint32_t>(j);
+    if (first) first[gids[j]] = kEmpty;  // VSI table reset (see owned_flag_kernel)
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) *count = U;
 }
 
@@ -370,15 +380,15 @@ void CacheLane::release() {
 }
 
 void CacheLane::select_owned(const uint32_t* d_gids, const int32_t* d_U, int32_t cap, uint32_t W,
-                             uint32_t w, cudaStream_t s) {
+                             uint32_t w, uint32_t* vsi_first, cudaStream_t s) {
   if (cap <= 0) return;
   if (W == 1) {  // a single worker owns every unique: own_k = identity, count = U
     own_all_kernel<<<std::max(1, std::min(ceil_div(cap, 256), 148 * 8)), 256, 0, s>>>(
-        d_U, own_k, counters + kCntOwned);
+        d_U, own_k, counters + kCntOwned, d_gids, vsi_first);
     CUDA_LAUNCH_CHECK();
     return;
   }
-  owned_flag_kernel<<<ceil_div(cap, 256), 256, 0, s>>>(d_gids, d_U, cap, W, w, flag);
+  owned_flag_kernel<<<ceil_div(cap, 256), 256, 0, s>>>(d_gids, d_U, cap, W, w, flag, vsi_first);
   CUDA_LAUNCH_CHECK();
   exclusive_scan_u32(temp, scan_bytes, flag, rank, cap, s);
   compact_kernel<<<ceil_div(cap, 256), 256, 0, s>>>(flag, rank, cap, own_k, counters + kCntOwned);

@@ -60,8 +60,9 @@ struct CacheLane {
   void release();
 
   // U / n_own are device counts; `cap` bounds the grids (the global batch size)
+  // vsi_first (nullable): VSI first-position table to clear behind the batch
   void select_owned(const uint32_t* d_gids, const int32_t* d_U, int32_t cap, uint32_t W,
-                    uint32_t w, cudaStream_t s);
+                    uint32_t w, uint32_t* vsi_first, cudaStream_t s);
   void mark_window(const uint32_t* d_gids, const int32_t* d_U, int32_t cap, uint32_t W, uint32_t w,
                    int32_t t, cudaStream_t s);
   void probe(const uint32_t* d_gids, int32_t cap, uint32_t W, int32_t t, cudaStream_t s);

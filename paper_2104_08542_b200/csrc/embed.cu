@@ -14,15 +14,19 @@ __device__ __forceinline__ T ldg_stream(const T* p) {
 }
 
 __global__ void gather_cache_v4(const uint32_t* __restrict__ own_k,
-                                const uint32_t* __restrict__ own_slot, const int32_t* __restrict__ n_ptr, int32_t n_bound, int d4,
-                                const float4* __restrict__ emb, float4* __restrict__ G) {
+                                const uint32_t* __restrict__ own_slot,
+                                const int32_t* __restrict__ n_ptr, int32_t n_bound, int d4,
+                                const float4* __restrict__ emb, float4* __restrict__ G,
+                                float4* __restrict__ dG_zero) {
   const int32_t n_own = n_ptr ? *n_ptr : n_bound;
   const int64_t n = static_cast<int64_t>(n_own) * d4;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t j = i / d4;
     const int c = static_cast<int>(i - j * d4);
-    G[static_cast<int64_t>(own_k[j]) * d4 + c] = emb[static_cast<int64_t>(own_slot[j]) * d4 + c];
+    const int64_t g = static_cast<int64_t>(own_k[j]) * d4 + c;
+    G[g] = emb[static_cast<int64_t>(own_slot[j]) * d4 + c];
+    if (dG_zero) dG_zero[g] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
 }
 
@@ -242,13 +246,16 @@ int fm_sq_parts(int d) { return (d & 3) == 0 ? d / 4 : d; }
 static int wave_grid(int64_t n_bound) { return std::max(1, std::min(ceil_div(n_bound, 256), 148 * 8)); }
 
 void gather_cache(const uint32_t* own_k, const uint32_t* own_slot, int32_t n_own,
-                  const int32_t* d_n_own, const float* emb, int d, float* G, cudaStream_t s) {
+                  const int32_t* d_n_own, const float* emb, int d, float* G, float* dG_zero,
+                  cudaStream_t s) {
+  SFB_CHECK(!dG_zero || (d & 3) == 0, "gather_cache: fused dG zeroing needs d % 4 == 0");
   if (n_own <= 0) return;
   if ((d & 3) == 0) {
     const int64_t n = static_cast<int64_t>(n_own) * (d / 4);
     gather_cache_v4<<<wave_grid(n), 256, 0, s>>>(own_k, own_slot, d_n_own, n_own, d / 4,
                                                      reinterpret_cast<const float4*>(emb),
-                                                     reinterpret_cast<float4*>(G));
+                                                     reinterpret_cast<float4*>(G),
+                                                     reinterpret_cast<float4*>(dG_zero));
   } else {
     const int64_t n = static_cast<int64_t>(n_own) * d;
     gather_cache_s<<<wave_grid(n), 256, 0, s>>>(own_k, own_slot, d_n_own, n_own, d, emb, G);
@@ -307,7 +314,8 @@ void segment_sum(const uint32_t* vid, int32_t n, int F, int d, int ldx, const fl
 void sparse_adam(const uint32_t* own_k /* gradient row index, or null = j */,
                  const uint32_t* own_slot, int32_t n_own, const int32_t* d_n_own, const float* dG,
                  int d, float* emb, float* mom, float* vel, int32_t* steps, const float* bc1,
-                 const float* bc2, float lr, double beta1, double beta2, float eps, cudaStream_t s) {
+                 const float* bc2, float lr, double beta1, double beta2, float eps, cudaStream_t s,
+                 bool inc_steps) {
   if (n_own <= 0) return;
   const float omb1 = static_cast<float>(1.0 - beta1);
   const float omb2 = static_cast<float>(1.0 - beta2);
@@ -324,8 +332,10 @@ void sparse_adam(const uint32_t* own_k /* gradient row index, or null = j */,
                                                         omb1, omb2, eps);
   }
   CUDA_LAUNCH_CHECK();
-  steps_inc_kernel<<<wave_grid(n_own), 256, 0, s>>>(own_slot, d_n_own, n_own, steps);
-  CUDA_LAUNCH_CHECK();
+  if (inc_steps) {
+    steps_inc_kernel<<<wave_grid(n_own), 256, 0, s>>>(own_slot, d_n_own, n_own, steps);
+    CUDA_LAUNCH_CHECK();
+  }
 }
 
 }  // namespace sfb

@@ -9,8 +9,10 @@ namespace sfb {
 // ---------------- embed.cu — worker ops ----------------
 // gather_cache: G[own_k[j]] = emb[own_slot[j]] for j < n_own
 // n_own bounds the grid; d_n_own (nullable) is the device count the kernels honour
+// dG_zero (nullable, d % 4 == 0): also zero the gradient rows G's rows map to
 void gather_cache(const uint32_t* own_k, const uint32_t* own_slot, int32_t n_own,
-                  const int32_t* d_n_own, const float* emb, int d, float* G, cudaStream_t s);
+                  const int32_t* d_n_own, const float* emb, int d, float* G, float* dG_zero,
+                  cudaStream_t s);
 // gather_instances + FM sums: X[i] = G[vid[i]] for the lane's rows; s[r] = sum_f X[r,f];
 // sqp[r, c4] = partial sum of squares
 void gather_instances(const uint32_t* vid, int32_t rows, int F, int d, int ldx, const float* G,
@@ -32,7 +34,8 @@ void fm_grad_add(const float* X, int32_t rows, int F, int d, int ldx, const floa
 void sparse_adam(const uint32_t* grad_idx, const uint32_t* own_slot, int32_t n_own,
                  const int32_t* d_n_own, const float* dG,
                  int d, float* emb, float* mom, float* vel, int32_t* steps, const float* bc1,
-                 const float* bc2, float lr, double beta1, double beta2, float eps, cudaStream_t s);
+                 const float* bc2, float lr, double beta1, double beta2, float eps, cudaStream_t s,
+                 bool inc_steps = true);  // false: the caller bumps the per-row step counts
 
 // ---------------- tower.cu — DeepFM-lite ----------------
 struct TowerBufs {

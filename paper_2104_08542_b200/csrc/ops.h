@@ -42,8 +42,10 @@ struct VsiScratch {
   void release();
 };
 // ids u32 [n] -> global_ids u32 [U] (first-appearance order), vids u32 [n], *d_unique.
+// reset = false leaves the first-position table dirty: the caller clears it (the
+// trainer folds that into its owned-set kernel)
 void vsi_device(VsiScratch& v, const uint32_t* d_ids, int64_t n, uint32_t* d_gids,
-                uint32_t* d_vids, int32_t* d_unique, cudaStream_t s);
+                uint32_t* d_vids, int32_t* d_unique, cudaStream_t s, bool reset = true);
 // u64 -> u32 with range check; *d_bad set to 1 when any id >= limit
 void ids_to_u32(const uint64_t* d_in, uint32_t* d_out, int64_t n, uint64_t limit, int32_t* d_bad,
                 cudaStream_t s);

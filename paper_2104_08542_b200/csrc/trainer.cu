@@ -239,21 +239,59 @@ struct LaneCounters {
   const int32_t* c[8];
 };
 
-// totals of a step that skipped the host wait: U, owned, working, interworker ledger bytes
-// (allreduce_bytes per worker, comm.hpp:36-41, with the per-step integer division)
-__global__ void acc_kernel(LaneCounters lc, int lanes, const int32_t* __restrict__ U_ptr,
-                           int64_t* __restrict__ acc, int W, int d, int64_t P) {
-  int64_t owned = 0, working = 0;
-  for (int l = 0; l < lanes; ++l) {
-    owned += lc.c[l][kCntOwned];
-    working += lc.c[l][kCntWorking];
+// The step's tail in one launch: dense Adam over the P dense parameters (same math as
+// dense_adam, tower.cu), the per-row Adam step counts of the rows sparse_adam just
+// updated, the loss, and (host-wait-free steps) the step totals.
+struct TailArgs {
+  float *p, *m, *v;
+  const float* g;
+  int64_t n;
+  float gs, lr, b1, b2, omb1, omb2, eps, bc1, bc2;
+  const float* loss_sum;
+  float inv_w;
+  float* loss_out;
+  int lanes;
+  const uint32_t* own_slot[8];
+  const int32_t* n_own[8];
+  int32_t* steps[8];
+  int64_t* acc;  // nullptr: no totals this step
+  LaneCounters cnt;
+  const int32_t* U;
+  int W, d;
+  int64_t P;
+};
+
+__global__ void tail_kernel(TailArgs a) {
+  const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = tid; i < a.n; i += stride) {
+    const float gi = a.g[i] * a.gs;
+    const float mi = a.b1 * a.m[i] + a.omb1 * gi;
+    const float vi = a.b2 * a.v[i] + a.omb2 * gi * gi;
+    a.m[i] = mi;
+    a.v[i] = vi;
+    a.p[i] -= a.lr * (mi / a.bc1) / (sqrtf(vi / a.bc2) + a.eps);
   }
-  const int64_t U = *U_ptr;
-  auto arb = [&](int64_t p) { return 2 * static_cast<int64_t>(W - 1) * p / W; };
-  acc[0] += U;
-  acc[1] += owned;
-  acc[2] += working;
-  acc[3] += static_cast<int64_t>(lanes) * (2 * arb(U * d * 4) + arb(P * 4));
+  for (int l = 0; l < a.lanes; ++l) {
+    const int32_t n = *a.n_own[l];
+    for (int64_t j = tid; j < n; j += stride) a.steps[l][a.own_slot[l][j]] += 1;
+  }
+  if (tid == 0) {
+    *a.loss_out = *a.loss_sum * a.inv_w;
+    if (a.acc) {
+      int64_t owned = 0, working = 0;
+      for (int l = 0; l < a.lanes; ++l) {
+        owned += a.cnt.c[l][kCntOwned];
+        working += a.cnt.c[l][kCntWorking];
+      }
+      const int64_t U = *a.U;
+      auto arb = [&](int64_t q) { return 2 * static_cast<int64_t>(a.W - 1) * q / a.W; };
+      a.acc[0] += U;
+      a.acc[1] += owned;
+      a.acc[2] += working;
+      a.acc[3] += static_cast<int64_t>(a.lanes) * (2 * arb(U * a.d * 4) + arb(a.P * 4));
+    }
+  }
 }
 
 // dG[0 : U*d) = 0 with U read on the device
@@ -332,7 +370,7 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
     stats_.nvlink_bytes += n_local_ * 4;
   }
   phase("ids_allgather");
-  vsi_device(vsi_, gids, n_global_, d_uniq_, d_vid_, d_scalars_ + 0, s);
+  vsi_device(vsi_, gids, n_global_, d_uniq_, d_vid_, d_scalars_ + 0, s, /*reset=*/false);
   phase("vsi");
   // ---- Host-Manager: MixCache per lane (Algorithm 1 l.4-7). The unique and
   // owned counts stay on the device (grids cover the batch-size bound), so the
@@ -342,7 +380,8 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
     // per-step counters; kCntFromHost (index 2) stays cumulative
     CUDA_CHECK(cudaMemsetAsync(lane_[l].counters, 0, sizeof(int32_t) * 2, s));
     CUDA_CHECK(cudaMemsetAsync(lane_[l].counters + 3, 0, sizeof(int32_t) * 2, s));
-    lane_[l].select_owned(d_uniq_, d_scalars_ + 0, cap, Wu, static_cast<uint32_t>(lane0_ + l), s);
+    lane_[l].select_owned(d_uniq_, d_scalars_ + 0, cap, Wu, static_cast<uint32_t>(lane0_ + l),
+                          l == 0 ? vsi_.d_first : nullptr, s);
   }
   // window batches t+1..t+L-1 (needed_soon), one at a time through the window scratch
   const int nwin = cfg_.lookahead_depth - 1;
@@ -435,6 +474,8 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   // rows of the table the lanes gather from: all U uniques (all-reduce scheme) or
   // only the ones this rank touches (owner-routed all-to-all)
   size_t table_rows = free_step ? static_cast<size_t>(n_global_) : static_cast<size_t>(U);
+  // one worker: gather_cache writes every one of the U rows, so it zeroes dG as it goes
+  const bool zero_in_gather = W_ == 1 && !a2a_ && d_ % 4 == 0;
   if (a2a_) {
     xch_.set_counts(h_totals_);
     stats_.nvlink_bytes += xch_.forward(lane_[0].own_k, lane_[0].own_slot, n_own[0],
@@ -448,7 +489,7 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
     if (world_ > 1) CUDA_CHECK(cudaMemsetAsync(d_G_, 0, sizeof(float) * ud, s));
     for (int l = 0; l < lanes_; ++l)
       gather_cache(lane_[l].own_k, lane_[l].own_slot, n_own[l], lane_[l].counters + kCntOwned,
-                   lane_[l].emb, d_, d_G_, s);
+                   lane_[l].emb, d_, d_G_, zero_in_gather ? d_dG_ : nullptr, s);
     phase("gather_cache");
     if (world_ > 1) {
       NCCL_CHECK(ncclAllReduce(d_G_, d_G_, ud, ncclFloat32, ncclSum, comm_, s));
@@ -462,7 +503,8 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   if (!free_step) led_[2] += static_cast<int64_t>(lanes_) * arb(static_cast<int64_t>(ud) * 4);
 
   // ---- per lane: gather_instances, forward_backward, segment_sum (l.11-12)
-  if (free_step && d_ % 4 == 0)
+  if (zero_in_gather) {
+  } else if (free_step && d_ % 4 == 0)
     zero_rows_kernel<<<148 * 8, 256, 0, s>>>(reinterpret_cast<float4*>(d_dG_), d_scalars_ + 0,
                                              d_ / 4, n_global_ * (d_ / 4));
   else
@@ -525,26 +567,48 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
                 lane_[l].emb,
                 lane_[l].mom, lane_[l].vel, lane_[l].steps, d_bc1_, d_bc2_,
                 static_cast<float>(cfg_.learning_rate), static_cast<float>(cfg_.adam_beta1),
-                static_cast<float>(cfg_.adam_beta2), static_cast<float>(cfg_.adam_epsilon), s);
+                static_cast<float>(cfg_.adam_beta2), static_cast<float>(cfg_.adam_epsilon), s,
+                /*inc_steps=*/false);
   phase("sparse_adam");
   dense_steps_ += 1;
   const double bc1 = 1.0 - std::pow(cfg_.adam_beta1, static_cast<double>(dense_steps_));
   const double bc2 = 1.0 - std::pow(cfg_.adam_beta2, static_cast<double>(dense_steps_));
-  dense_adam(d_dense_, d_dense_m_, d_dense_v_, d_grads_, static_cast<int64_t>(P_),
-             1.f / static_cast<float>(W_), static_cast<float>(cfg_.learning_rate),
-             cfg_.adam_beta1, cfg_.adam_beta2,
-             static_cast<float>(cfg_.adam_epsilon), static_cast<float>(bc1),
-             static_cast<float>(bc2), s);
-  finalize_loss_kernel<<<1, 32, 0, s>>>(d_grads_ + P_, 1.f / static_cast<float>(W_),
-                                        d_loss ? d_loss : d_loss_);
-  CUDA_LAUNCH_CHECK();
+  {
+    TailArgs a{};
+    a.p = d_dense_;
+    a.m = d_dense_m_;
+    a.v = d_dense_v_;
+    a.g = d_grads_;
+    a.n = static_cast<int64_t>(P_);
+    a.gs = 1.f / static_cast<float>(W_);
+    a.lr = static_cast<float>(cfg_.learning_rate);
+    a.b1 = static_cast<float>(cfg_.adam_beta1);
+    a.b2 = static_cast<float>(cfg_.adam_beta2);
+    a.omb1 = static_cast<float>(1.0 - cfg_.adam_beta1);
+    a.omb2 = static_cast<float>(1.0 - cfg_.adam_beta2);
+    a.eps = static_cast<float>(cfg_.adam_epsilon);
+    a.bc1 = static_cast<float>(bc1);
+    a.bc2 = static_cast<float>(bc2);
+    a.loss_sum = d_grads_ + P_;
+    a.inv_w = 1.f / static_cast<float>(W_);
+    a.loss_out = d_loss ? d_loss : d_loss_;
+    a.lanes = lanes_;
+    for (int l = 0; l < lanes_; ++l) {
+      a.own_slot[l] = lane_[l].own_slot;
+      a.n_own[l] = lane_[l].counters + kCntOwned;
+      a.steps[l] = lane_[l].steps;
+      a.cnt.c[l] = lane_[l].counters;
+    }
+    a.acc = free_step ? d_acc_ : nullptr;
+    a.U = d_scalars_ + 0;
+    a.W = W_;
+    a.d = d_;
+    a.P = static_cast<int64_t>(P_);
+    tail_kernel<<<148 * 4, 256, 0, s>>>(a);
+    CUDA_LAUNCH_CHECK();
+  }
   phase("dense_adam");
   if (free_step) {
-    LaneCounters lc{};
-    for (int l = 0; l < lanes_; ++l) lc.c[l] = lane_[l].counters;
-    acc_kernel<<<1, 1, 0, s>>>(lc, lanes_, d_scalars_ + 0, d_acc_, W_, d_,
-                               static_cast<int64_t>(P_));
-    CUDA_LAUNCH_CHECK();
     acc_pending_ = true;
     free_steps_ += 1;
   }

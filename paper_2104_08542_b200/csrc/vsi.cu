@@ -7,14 +7,16 @@
 //   1. first[f] = min position of f    (direct-mapped table over the
 //      vocabulary in HBM; warp __match_any_sync pre-dedup so only one lane per
 //      distinct id in a warp issues the atomicMin)
-//   2. flag[i]  = (first[f_i] == i)    (i is a first appearance)
-//   3. rank     = exclusive scan(flag) (U = rank[n-1] + flag[n-1])
+//   2. flag[i]  = (first[f_i] == i)    (i is a first appearance; evaluated inside
+//   3. rank     = exclusive scan(flag)  the CUB scan; U = rank[n-1] + flag[n-1])
 //   4. global_ids[rank[i]] = f_i for flagged i;  vid[i] = rank[first[f_i]]
 //   5. first[global_ids[k]] = unseen   (reset only the touched entries)
 // The direct-mapped table (4 B per vocabulary id: 135 MB at 33.8M ids) is the
 // HBM-rich choice: no probing, no tombstones, one sector per access.
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 
 #include "ops.h"
 
@@ -43,24 +45,19 @@ __global__ void vsi_first_kernel(const uint32_t* __restrict__ ids, int64_t n,
   if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicMin(first + f, static_cast<uint32_t>(i));
 }
 
-__global__ void vsi_flag_kernel(const uint32_t* __restrict__ ids, int64_t n,
-                                const uint32_t* __restrict__ first, uint32_t* __restrict__ flag) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i < n) flag[i] = (__ldg(first + ids[i]) == static_cast<uint32_t>(i)) ? 1u : 0u;
-}
-
 __global__ void vsi_emit_kernel(const uint32_t* __restrict__ ids, int64_t n,
                                 const uint32_t* __restrict__ first,
-                                const uint32_t* __restrict__ flag,
                                 const uint32_t* __restrict__ rank, uint32_t* __restrict__ gids,
                                 uint32_t* __restrict__ vids, int32_t* __restrict__ unique) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= n) return;
   const uint32_t f = ids[i];
   const uint32_t r = rank[i];
-  if (flag[i]) gids[r] = f;
-  vids[i] = __ldg(rank + __ldg(first + f));
-  if (i == n - 1) *unique = static_cast<int32_t>(r + flag[i]);
+  const uint32_t fi = __ldg(first + f);
+  const uint32_t flag = fi == static_cast<uint32_t>(i) ? 1u : 0u;
+  if (flag) gids[r] = f;
+  vids[i] = __ldg(rank + fi);
+  if (i == n - 1) *unique = static_cast<int32_t>(r + flag);
 }
 
 __global__ void vsi_reset_kernel(const uint32_t* __restrict__ gids,
@@ -88,6 +85,24 @@ __global__ void u32_to_u64_kernel(const uint32_t* __restrict__ in, uint64_t* __r
                                   int64_t n) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i < n) out[i] = in[i];
+}
+
+// flag[i] = (first[ids[i]] == i), evaluated inside the scan (no flag array / kernel)
+struct FirstFlag {
+  const uint32_t* ids;
+  const uint32_t* first;
+  __device__ uint32_t operator()(int i) const {
+    return __ldg(first + __ldg(ids + i)) == static_cast<uint32_t>(i) ? 1u : 0u;
+  }
+};
+using FlagIt = thrust::transform_iterator<FirstFlag, thrust::counting_iterator<int>>;
+
+size_t flag_scan_temp_bytes(int64_t n) {
+  size_t bytes = 0;
+  FlagIt it(thrust::counting_iterator<int>(0), FirstFlag{nullptr, nullptr});
+  CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, it, static_cast<uint32_t*>(nullptr),
+                                           static_cast<int>(n)));
+  return bytes;
 }
 
 }  // namespace
@@ -129,7 +144,7 @@ void VsiScratch::init(uint64_t ks, int64_t c) {
   CUDA_CHECK(cudaMalloc(&d_first, sizeof(uint32_t) * key_space));
   CUDA_CHECK(cudaMalloc(&d_flag, sizeof(uint32_t) * cap));
   CUDA_CHECK(cudaMalloc(&d_rank, sizeof(uint32_t) * cap));
-  cub_bytes = scan_temp_bytes(cap);
+  cub_bytes = std::max(scan_temp_bytes(cap), flag_scan_temp_bytes(cap));
   CUDA_CHECK(cudaMalloc(&d_cub, cub_bytes));
   fill_u32_kernel<<<1184, 256>>>(d_first, static_cast<int64_t>(key_space), kUnseen);
   CUDA_LAUNCH_CHECK();
@@ -146,19 +161,23 @@ void VsiScratch::release() {
 }
 
 void vsi_device(VsiScratch& v, const uint32_t* d_ids, int64_t n, uint32_t* d_gids,
-                uint32_t* d_vids, int32_t* d_unique, cudaStream_t s) {
+                uint32_t* d_vids, int32_t* d_unique, cudaStream_t s, bool reset) {
   SFB_CHECK(n > 0 && n <= v.cap, "vsi batch exceeds scratch capacity");
   const int grid = ceil_div(n, 256);
   vsi_first_kernel<<<grid, 256, 0, s>>>(d_ids, n, v.d_first);
   CUDA_LAUNCH_CHECK();
-  vsi_flag_kernel<<<grid, 256, 0, s>>>(d_ids, n, v.d_first, v.d_flag);
+  {
+    FlagIt it(thrust::counting_iterator<int>(0), FirstFlag{d_ids, v.d_first});
+    size_t bytes = v.cub_bytes;
+    CUDA_CHECK(cub::DeviceScan::ExclusiveSum(v.d_cub, bytes, it, v.d_rank, static_cast<int>(n), s));
+    g_launches += 2;  // init + decoupled look-back scan
+  }
+  vsi_emit_kernel<<<grid, 256, 0, s>>>(d_ids, n, v.d_first, v.d_rank, d_gids, d_vids, d_unique);
   CUDA_LAUNCH_CHECK();
-  exclusive_scan_u32(v.d_cub, v.cub_bytes, v.d_flag, v.d_rank, n, s);
-  vsi_emit_kernel<<<grid, 256, 0, s>>>(d_ids, n, v.d_first, v.d_flag, v.d_rank, d_gids, d_vids,
-                                       d_unique);
-  CUDA_LAUNCH_CHECK();
-  vsi_reset_kernel<<<std::min(grid, 148 * 8), 256, 0, s>>>(d_gids, d_unique, v.d_first);
-  CUDA_LAUNCH_CHECK();
+  if (reset) {
+    vsi_reset_kernel<<<std::min(grid, 148 * 8), 256, 0, s>>>(d_gids, d_unique, v.d_first);
+    CUDA_LAUNCH_CHECK();
+  }
 }
 
 void ids_to_u32(const uint64_t* d_in, uint32_t* d_out, int64_t n, uint64_t limit, int32_t* d_bad,
