@@ -69,14 +69,17 @@ struct TowerTC {
 };
 int tower_ldx(int K);  // row stride of X / dX (K rounded up to 4 floats)
 
-// Forward + head + backward of one lane's rows on the tensor cores. X and dX
+// Forward + head + backward of one lane's rows on the tensor cores. w1_split_ready: the
+// caller already holds W1's tf32 hi/lo parts in tc (the trainer's tail kernel writes them
+// when it updates W1), so the per-call prep pass is skipped. X and dX
 // have row stride ldx = tower_ldx(K); dX is scaled by emb_scale; dense grads go
 // to grads = [dW1 | db1 | dw2 | db2 | loss_sum] (accumulated when accumulate).
 void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc, const float* X, int ldx,
                                const float* fm_s, const float* fm_sqp, const uint8_t* labels,
                                int32_t rows, int F, int d, const float* dense, float* logits,
                                float* dX, float emb_scale, float* grads, bool accumulate,
-                               cudaStream_t s);
+                               cudaStream_t s,
+                               bool w1_split_ready = false);
 // Fused path (tc_fused.cuh): X = G[vid] is gathered straight into the GEMM
 // operands and dX is scatter-added into dG (with the FM term) by the dX GEMM's
 // epilogue; neither touches HBM. Writes fm_s [rows x d]. Needs d % 4 == 0, d <= 128.

@@ -432,7 +432,7 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc_, const float* X, int l
                                const float* fm_s, const float* fm_sqp, const uint8_t* labels,
                                int32_t rows, int F, int d, const float* dense, float* logits,
                                float* dX, float emb_scale, float* grads, bool accumulate,
-                               cudaStream_t s) {
+                               cudaStream_t s, bool w1_split_ready) {
   const int K = F * d, H = t.H;
   SFB_CHECK(rows <= t.rows_cap && rows <= tc_.rows_cap && K == tc_.K && ldx == tc_.ldk,
             "tower buffers too small");
@@ -447,9 +447,11 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc_, const float* X, int l
   float* g_loss = g_b2 + 1;
 
   // W1 hi/lo in both layouts
-  prep_w1_kernel<<<ceil_div(static_cast<int64_t>(K) * H, 256), 256, 0, s>>>(
-      w1, K, H, tc_.ldh, tc_.ldk, tc_.w_hi, tc_.w_lo, tc_.wt_hi, tc_.wt_lo);
-  CUDA_LAUNCH_CHECK();
+  if (!w1_split_ready) {
+    prep_w1_kernel<<<ceil_div(static_cast<int64_t>(K) * H, 256), 256, 0, s>>>(
+        w1, K, H, tc_.ldh, tc_.ldk, tc_.w_hi, tc_.w_lo, tc_.wt_hi, tc_.wt_lo);
+    CUDA_LAUNCH_CHECK();
+  }
 
   // ---- GEMM1: hpre partials = X W1 (A = X K-major, B = W1^T)
   const int nkb1 = (K + tc::BKE - 1) / tc::BKE;

@@ -12,6 +12,8 @@
 // payloads and the eviction sort; everything else is asynchronous.
 #include "trainer.h"
 
+#include "tc_gemm.cuh"
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -254,6 +256,9 @@ struct TailArgs {
   const uint32_t* own_slot[8];
   const int32_t* n_own[8];
   int32_t* steps[8];
+  // W1's tf32 hi/lo parts in both tower layouts (nullptr: not maintained here)
+  float *w_hi, *w_lo, *wt_hi, *wt_lo;
+  int K, H, ldh, ldk;
   int64_t* acc;  // nullptr: no totals this step
   LaneCounters cnt;
   const int32_t* U;
@@ -270,7 +275,16 @@ __global__ void tail_kernel(TailArgs a) {
     const float vi = a.b2 * a.v[i] + a.omb2 * gi * gi;
     a.m[i] = mi;
     a.v[i] = vi;
-    a.p[i] -= a.lr * (mi / a.bc1) / (sqrtf(vi / a.bc2) + a.eps);
+    const float pn = a.p[i] - a.lr * (mi / a.bc1) / (sqrtf(vi / a.bc2) + a.eps);
+    a.p[i] = pn;
+    if (a.w_hi && i < static_cast<int64_t>(a.K) * a.H) {  // same split as prep_w1 (tc_tower.cu)
+      const int k = static_cast<int>(i / a.H), j = static_cast<int>(i % a.H);
+      const float h = tc::tf32_rna(pn), lo = tc::tf32_rna(pn - h);
+      a.w_hi[static_cast<int64_t>(k) * a.ldh + j] = h;
+      a.w_lo[static_cast<int64_t>(k) * a.ldh + j] = lo;
+      a.wt_hi[static_cast<int64_t>(j) * a.ldk + k] = h;
+      a.wt_lo[static_cast<int64_t>(j) * a.ldk + k] = lo;
+    }
   }
   for (int l = 0; l < a.lanes; ++l) {
     const int32_t n = *a.n_own[l];
@@ -531,7 +545,7 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
     else
       tower_forward_backward_tc(tower_, towertc_, d_X_, ldx_, d_fm_s_, d_fm_sqp_, lab, b_, F_, d_,
                                 d_dense_, d_logits_ + static_cast<size_t>(l) * b_, d_dX_,
-                                emb_scale, d_grads_, l > 0, s);
+                                emb_scale, d_grads_, l > 0, s, w1_split_ready_);
     phase("tower");
     segment_sum(vid, b_ * F_, F_, d_, ldx_, d_dX_, d_G_, d_fm_s_, tower_.gz, emb_scale, d_dG_, s);
     phase("segment_sum");
@@ -599,6 +613,16 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
       a.steps[l] = lane_[l].steps;
       a.cnt.c[l] = lane_[l].counters;
     }
+    if (!tower_fused_ && !tower_simt_) {
+      a.w_hi = towertc_.w_hi;
+      a.w_lo = towertc_.w_lo;
+      a.wt_hi = towertc_.wt_hi;
+      a.wt_lo = towertc_.wt_lo;
+      a.K = K_;
+      a.H = H_;
+      a.ldh = towertc_.ldh;
+      a.ldk = towertc_.ldk;
+    }
     a.acc = free_step ? d_acc_ : nullptr;
     a.U = d_scalars_ + 0;
     a.W = W_;
@@ -606,6 +630,7 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
     a.P = static_cast<int64_t>(P_);
     tail_kernel<<<148 * 4, 256, 0, s>>>(a);
     CUDA_LAUNCH_CHECK();
+    w1_split_ready_ = a.w_hi != nullptr;
   }
   phase("dense_adam");
   if (free_step) {
@@ -813,6 +838,7 @@ void Trainer::get_dense(float* w1, float* b1, float* w2, float* b2) {
 
 void Trainer::set_dense(const float* w1, const float* b1, const float* w2, const float* b2) {
   CUDA_CHECK(cudaStreamSynchronize(stream_));
+  w1_split_ready_ = false;
   const size_t kh = static_cast<size_t>(K_) * H_;
   if (w1) CUDA_CHECK(cudaMemcpy(d_dense_, w1, sizeof(float) * kh, cudaMemcpyHostToDevice));
   if (b1) CUDA_CHECK(cudaMemcpy(d_dense_ + kh, b1, sizeof(float) * H_, cudaMemcpyHostToDevice));

@@ -109,6 +109,7 @@ class Trainer {
   int ldx_ = 0;
   bool tower_simt_ = false;
   bool tower_fused_ = false;
+  bool w1_split_ready_ = false;  // towertc_ holds the tf32 parts of the current W1
   int64_t dense_steps_ = 0;
   int64_t steps_done_ = 0;
   int64_t led_[4] = {0, 0, 0, 0};
