@@ -17,7 +17,7 @@ __global__ void gather_cache_v4(const uint32_t* __restrict__ own_k,
                                 const uint32_t* __restrict__ own_slot,
                                 const int32_t* __restrict__ n_ptr, int32_t n_bound, int d4,
                                 const float4* __restrict__ emb, float4* __restrict__ G,
-                                float4* __restrict__ dG_zero) {
+                                float4* __restrict__ dG_zero, float* __restrict__ B_zero) {
   const int32_t n_own = n_ptr ? *n_ptr : n_bound;
   const int64_t n = static_cast<int64_t>(n_own) * d4;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -27,6 +27,7 @@ __global__ void gather_cache_v4(const uint32_t* __restrict__ own_k,
     const int64_t g = static_cast<int64_t>(own_k[j]) * d4 + c;
     G[g] = emb[static_cast<int64_t>(own_slot[j]) * d4 + c];
     if (dG_zero) dG_zero[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (B_zero && c == 0) B_zero[own_k[j]] = 0.f;
   }
 }
 
@@ -123,10 +124,14 @@ __global__ void fm_sums_kernel(const float* __restrict__ X, int32_t rows, int F,
 //   dX_mlp[p] + scale * gz[r] * (S_r - v_p)          (FM: d/dv_f sum_{i<j}<v_i,v_j>)
 // The tower writes the MLP part; the FM part is added here, where v_p = G[vid[p]]
 // is an L2-resident re-read of the row being scattered to.
+// Bsum != nullptr (deferred FM correction): the -scale*gz[r]*v_p part is linear in the
+// row v_p = G[vid[p]], so it is summed per unique row as Bsum[u] = sum_p gz[r] and applied
+// once by the optimizer (g -= scale * Bsum[u] * G[u], G[u] being the row it updates);
+// this pass then reads only dX, not a gathered G row per position.
 __global__ void segment_sum_v4(const uint32_t* __restrict__ vid, int32_t n, int F, int d4,
                                const float4* __restrict__ dX, const float4* __restrict__ G,
                                const float4* __restrict__ fm_s, const float* __restrict__ gz,
-                               float scale, float* __restrict__ dG) {
+                               float scale, float* __restrict__ dG, float* __restrict__ Bsum) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= static_cast<int64_t>(n) * d4) return;
   const int64_t p = i / d4;
@@ -134,10 +139,18 @@ __global__ void segment_sum_v4(const uint32_t* __restrict__ vid, int32_t n, int 
   const int64_t r = p / F;
   const uint32_t v = __ldg(vid + p);
   const float4 a = __ldcs(dX + i);
-  const float4 e = __ldg(G + static_cast<int64_t>(v) * d4 + c);
   const float4 s = __ldg(fm_s + r * d4 + c);
-  const float k = scale * __ldg(gz + r);
+  const float gr = __ldg(gz + r);
+  const float k = scale * gr;
   float* dst = dG + (static_cast<int64_t>(v) * d4 + c) * 4;
+  if (Bsum) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(a.x + k * s.x),
+                 "f"(a.y + k * s.y), "f"(a.z + k * s.z), "f"(a.w + k * s.w)
+                 : "memory");
+    if (c == 0) atomicAdd(Bsum + v, gr);
+    return;
+  }
+  const float4 e = __ldg(G + static_cast<int64_t>(v) * d4 + c);
   asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst),
                "f"(a.x + k * (s.x - e.x)), "f"(a.y + k * (s.y - e.y)), "f"(a.z + k * (s.z - e.z)),
                "f"(a.w + k * (s.w - e.w))
@@ -205,7 +218,8 @@ __global__ void sparse_adam_v4(const uint32_t* __restrict__ own_k,
                                float4* __restrict__ mom, float4* __restrict__ vel,
                                const int32_t* __restrict__ steps, const float* __restrict__ bc1,
                                const float* __restrict__ bc2, float lr, float b1, float b2,
-                               float omb1, float omb2, float eps) {
+                               float omb1, float omb2, float eps, const float* __restrict__ Bsum,
+                               float fm_scale) {
   const int32_t n_own = n_ptr ? *n_ptr : n_bound;
   const int64_t n = static_cast<int64_t>(n_own) * d4;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -215,9 +229,17 @@ __global__ void sparse_adam_v4(const uint32_t* __restrict__ own_k,
     const uint32_t s = __ldg(own_slot + j);
     const int t = __ldg(steps + s) + 1;
     const float c1 = __ldg(bc1 + t), c2 = __ldg(bc2 + t);
-    const float4 g = __ldg(dG + static_cast<int64_t>(own_k ? __ldg(own_k + j) : j) * d4 + c);
+    const int64_t gr = own_k ? __ldg(own_k + j) : j;
+    float4 g = __ldg(dG + gr * d4 + c);
     const int64_t o = static_cast<int64_t>(s) * d4 + c;
     float4 m = mom[o], v = vel[o], e = emb[o];
+    if (Bsum) {  // deferred FM term of segment_sum: e is the G row of the forward pass
+      const float kb = fm_scale * __ldg(Bsum + gr);
+      g.x -= kb * e.x;
+      g.y -= kb * e.y;
+      g.z -= kb * e.z;
+      g.w -= kb * e.w;
+    }
 #define SFB_ADAM(X)                    \
   m.X = b1 * m.X + omb1 * g.X;         \
   v.X = b2 * v.X + omb2 * g.X * g.X;   \
@@ -247,7 +269,7 @@ static int wave_grid(int64_t n_bound) { return std::max(1, std::min(ceil_div(n_b
 
 void gather_cache(const uint32_t* own_k, const uint32_t* own_slot, int32_t n_own,
                   const int32_t* d_n_own, const float* emb, int d, float* G, float* dG_zero,
-                  cudaStream_t s) {
+                  cudaStream_t s, float* B_zero) {
   SFB_CHECK(!dG_zero || (d & 3) == 0, "gather_cache: fused dG zeroing needs d % 4 == 0");
   if (n_own <= 0) return;
   if ((d & 3) == 0) {
@@ -255,7 +277,7 @@ void gather_cache(const uint32_t* own_k, const uint32_t* own_slot, int32_t n_own
     gather_cache_v4<<<wave_grid(n), 256, 0, s>>>(own_k, own_slot, d_n_own, n_own, d / 4,
                                                      reinterpret_cast<const float4*>(emb),
                                                      reinterpret_cast<float4*>(G),
-                                                     reinterpret_cast<float4*>(dG_zero));
+                                                     reinterpret_cast<float4*>(dG_zero), B_zero);
   } else {
     const int64_t n = static_cast<int64_t>(n_own) * d;
     gather_cache_s<<<wave_grid(n), 256, 0, s>>>(own_k, own_slot, d_n_own, n_own, d, emb, G);
@@ -297,15 +319,16 @@ void fm_grad_add(const float* X, int32_t rows, int F, int d, int ldx, const floa
 
 void segment_sum(const uint32_t* vid, int32_t n, int F, int d, int ldx, const float* dX,
                  const float* G, const float* fm_s, const float* gz, float scale, float* dG,
-                 cudaStream_t s) {
+                 cudaStream_t s, float* Bsum) {
   if (n <= 0) return;
   if ((d & 3) == 0 && ldx == F * d) {
     const int64_t m = static_cast<int64_t>(n) * (d / 4);
     segment_sum_v4<<<ceil_div(m, 256), 256, 0, s>>>(
         vid, n, F, d / 4, reinterpret_cast<const float4*>(dX), reinterpret_cast<const float4*>(G),
-        reinterpret_cast<const float4*>(fm_s), gz, scale, dG);
+        reinterpret_cast<const float4*>(fm_s), gz, scale, dG, Bsum);
   } else {
     const int64_t m = static_cast<int64_t>(n) * d;
+    SFB_CHECK(!Bsum, "segment_sum: deferred FM term needs d % 4 == 0");
     segment_sum_s<<<ceil_div(m, 256), 256, 0, s>>>(vid, n, F, d, ldx, dX, G, fm_s, gz, scale, dG);
   }
   CUDA_LAUNCH_CHECK();
@@ -315,7 +338,7 @@ void sparse_adam(const uint32_t* own_k /* gradient row index, or null = j */,
                  const uint32_t* own_slot, int32_t n_own, const int32_t* d_n_own, const float* dG,
                  int d, float* emb, float* mom, float* vel, int32_t* steps, const float* bc1,
                  const float* bc2, float lr, double beta1, double beta2, float eps, cudaStream_t s,
-                 bool inc_steps) {
+                 bool inc_steps, const float* Bsum, float fm_scale) {
   if (n_own <= 0) return;
   const float omb1 = static_cast<float>(1.0 - beta1);
   const float omb2 = static_cast<float>(1.0 - beta2);
@@ -324,8 +347,10 @@ void sparse_adam(const uint32_t* own_k /* gradient row index, or null = j */,
     sparse_adam_v4<<<wave_grid(n), 256, 0, s>>>(
         own_k, own_slot, d_n_own, n_own, d / 4, reinterpret_cast<const float4*>(dG),
         reinterpret_cast<float4*>(emb), reinterpret_cast<float4*>(mom),
-        reinterpret_cast<float4*>(vel), steps, bc1, bc2, lr, beta1, beta2, omb1, omb2, eps);
+        reinterpret_cast<float4*>(vel), steps, bc1, bc2, lr, beta1, beta2, omb1, omb2, eps, Bsum,
+        fm_scale);
   } else {
+    SFB_CHECK(!Bsum, "sparse_adam: deferred FM term needs d % 4 == 0");
     const int64_t n = static_cast<int64_t>(n_own) * d;
     sparse_adam_kernel<<<wave_grid(n), 256, 0, s>>>(own_k, own_slot, d_n_own, n_own, d, dG, emb, mom,
                                                         vel, steps, bc1, bc2, lr, beta1, beta2,

@@ -12,7 +12,7 @@ namespace sfb {
 // dG_zero (nullable, d % 4 == 0): also zero the gradient rows G's rows map to
 void gather_cache(const uint32_t* own_k, const uint32_t* own_slot, int32_t n_own,
                   const int32_t* d_n_own, const float* emb, int d, float* G, float* dG_zero,
-                  cudaStream_t s);
+                  cudaStream_t s, float* B_zero = nullptr);
 // gather_instances + FM sums: X[i] = G[vid[i]] for the lane's rows; s[r] = sum_f X[r,f];
 // sqp[r, c4] = partial sum of squares
 void gather_instances(const uint32_t* vid, int32_t rows, int F, int d, int ldx, const float* G,
@@ -23,9 +23,11 @@ void fm_sums(const float* X, int32_t rows, int F, int d, int ldx, float* fm_s, f
              cudaStream_t s);
 // segment_sum: dG[vid[p]] += dX_mlp[p] + scale*gz[r]*(fm_s[r] - G[vid[p]]) for the lane's
 // positions p = (r, f) (vector red.global.add.v4.f32)
+// Bsum != nullptr: the -scale*gz*G term is deferred: Bsum[vid[p]] += gz[r], and
+// sparse_adam(..., Bsum, scale) subtracts scale * Bsum[u] * G[u] from the row's gradient
 void segment_sum(const uint32_t* vid, int32_t n, int F, int d, int ldx, const float* dX,
                  const float* G, const float* fm_s, const float* gz, float scale, float* dG,
-                 cudaStream_t s);
+                 cudaStream_t s, float* Bsum = nullptr);
 // dX[r, k] += scale * gz[r] * (fm_s[r, k % d] - X[r, k]) (FM part, standalone model op)
 void fm_grad_add(const float* X, int32_t rows, int F, int d, int ldx, const float* fm_s,
                  const float* gz, float scale, float* dX, cudaStream_t s);
@@ -35,7 +37,8 @@ void sparse_adam(const uint32_t* grad_idx, const uint32_t* own_slot, int32_t n_o
                  const int32_t* d_n_own, const float* dG,
                  int d, float* emb, float* mom, float* vel, int32_t* steps, const float* bc1,
                  const float* bc2, float lr, double beta1, double beta2, float eps, cudaStream_t s,
-                 bool inc_steps = true);  // false: the caller bumps the per-row step counts
+                 bool inc_steps = true,  // false: the caller bumps the per-row step counts
+                 const float* Bsum = nullptr, float fm_scale = 0.f);  // deferred FM term
 
 // ---------------- tower.cu — DeepFM-lite ----------------
 struct TowerBufs {

@@ -116,6 +116,7 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
   const size_t gd = static_cast<size_t>(n_global_) * d_;
   CUDA_CHECK(cudaMalloc(&d_G_, sizeof(float) * gd));
   CUDA_CHECK(cudaMalloc(&d_dG_, sizeof(float) * gd));
+  CUDA_CHECK(cudaMalloc(&d_B_, sizeof(float) * n_global_));
   ldx_ = tower_ldx(K_);
   const size_t bk = static_cast<size_t>(b_) * ldx_;
   CUDA_CHECK(cudaMalloc(&d_X_, sizeof(float) * bk));
@@ -205,7 +206,8 @@ Trainer::~Trainer() {
                   static_cast<void*>(d_dense_), static_cast<void*>(d_dense_m_),
                   static_cast<void*>(d_dense_v_), static_cast<void*>(d_grads_),
                   static_cast<void*>(d_loss_), static_cast<void*>(d_bc1_),
-                  static_cast<void*>(d_bc2_), static_cast<void*>(d_acc_)})
+                  static_cast<void*>(d_bc2_), static_cast<void*>(d_acc_),
+                  static_cast<void*>(d_B_)})
     if (p) cudaFree(p);
   if (h_acc_) cudaFreeHost(h_acc_);
   if (h_scalars_) cudaFreeHost(h_scalars_);
@@ -490,6 +492,9 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   size_t table_rows = free_step ? static_cast<size_t>(n_global_) : static_cast<size_t>(U);
   // one worker: gather_cache writes every one of the U rows, so it zeroes dG as it goes
   const bool zero_in_gather = W_ == 1 && !a2a_ && d_ % 4 == 0;
+  // one worker also defers segment_sum's -scale*gz*G term to sparse_adam (which reads the
+  // same G row as emb[slot]): the scatter pass then does not re-gather G per position
+  const bool defer_fm = zero_in_gather && !tower_fused_;
   if (a2a_) {
     xch_.set_counts(h_totals_);
     stats_.nvlink_bytes += xch_.forward(lane_[0].own_k, lane_[0].own_slot, n_own[0],
@@ -503,7 +508,8 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
     if (world_ > 1) CUDA_CHECK(cudaMemsetAsync(d_G_, 0, sizeof(float) * ud, s));
     for (int l = 0; l < lanes_; ++l)
       gather_cache(lane_[l].own_k, lane_[l].own_slot, n_own[l], lane_[l].counters + kCntOwned,
-                   lane_[l].emb, d_, d_G_, zero_in_gather ? d_dG_ : nullptr, s);
+                   lane_[l].emb, d_, d_G_, zero_in_gather ? d_dG_ : nullptr, s,
+                   zero_in_gather ? d_B_ : nullptr);
     phase("gather_cache");
     if (world_ > 1) {
       NCCL_CHECK(ncclAllReduce(d_G_, d_G_, ud, ncclFloat32, ncclSum, comm_, s));
@@ -547,7 +553,8 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
                                 d_dense_, d_logits_ + static_cast<size_t>(l) * b_, d_dX_,
                                 emb_scale, d_grads_, l > 0, s, w1_split_ready_);
     phase("tower");
-    segment_sum(vid, b_ * F_, F_, d_, ldx_, d_dX_, d_G_, d_fm_s_, tower_.gz, emb_scale, d_dG_, s);
+    segment_sum(vid, b_ * F_, F_, d_, ldx_, d_dX_, d_G_, d_fm_s_, tower_.gz, emb_scale, d_dG_, s,
+                defer_fm ? d_B_ : nullptr);
     phase("segment_sum");
   }
 
@@ -582,7 +589,7 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
                 lane_[l].mom, lane_[l].vel, lane_[l].steps, d_bc1_, d_bc2_,
                 static_cast<float>(cfg_.learning_rate), static_cast<float>(cfg_.adam_beta1),
                 static_cast<float>(cfg_.adam_beta2), static_cast<float>(cfg_.adam_epsilon), s,
-                /*inc_steps=*/false);
+                /*inc_steps=*/false, defer_fm ? d_B_ : nullptr, emb_scale);
   phase("sparse_adam");
   dense_steps_ += 1;
   const double bc1 = 1.0 - std::pow(cfg_.adam_beta1, static_cast<double>(dense_steps_));

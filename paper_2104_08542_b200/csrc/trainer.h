@@ -82,6 +82,7 @@ class Trainer {
   uint32_t* d_wvid_ = nullptr;
   float* d_G_ = nullptr;            // global common embedding [U x d]
   float* d_dG_ = nullptr;           // global common gradients [U x d]
+  float* d_B_ = nullptr;            // [U] deferred FM coefficient per unique (one worker)
   float* d_X_ = nullptr;            // minibatch embeddings [b x K]
   float* d_dX_ = nullptr;
   float* d_fm_s_ = nullptr;
