@@ -71,64 +71,82 @@ def measured_peaks():
 
 
 class Clocks:
-    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock / throttle-reason sampler for the timed region (B200_PROFILING.md clocks line).
+    NVML polled from a thread every ~1 ms: the timed region is only milliseconds long,
+    shorter than nvidia-smi's sampling period."""
+
 
     def __init__(self, index):
         self.index = index
-        self.proc = None
-        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{index}.csv")
+        self.th = None
+        self.sm, self.mx, self.reasons, self.err = [], [], set(), None
+
+    def _run(self):
+        import pynvml
+        reasons = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                   "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                   "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                   "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+        h = self.h
+        try:
+            while not self.stop_flag or not self.sm:
+                self.sm.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                for n, bit in reasons.items():
+                    if r & bit:
+                        self.reasons.add(n)
+                time.sleep(0.001)
+            pynvml.nvmlShutdown()
+        except Exception as e:  # noqa: BLE001
+            self.err = str(e)
 
     def start(self):
-        os.makedirs(os.path.dirname(self.path), exist_ok=True)
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-        try:
-            self.fh = open(self.path, "w")
-            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                          "-i", str(self.index), "-lms", "100"], stdout=self.fh,
-                                         stderr=subprocess.DEVNULL)
-        except Exception:
-            self.proc = None
+        import threading
+
+        import pynvml
+        try:  # NVML init (slow the first time) happens before the timed region
+            pynvml.nvmlInit()
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.mx.append(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+        except Exception as e:  # noqa: BLE001
+            self.err = str(e)
+            return
+        self.stop_flag = False
+        self.th = threading.Thread(target=self._run, daemon=True)
+        self.th.start()
+        while not self.sm and self.th.is_alive():
+            time.sleep(0.0005)
 
     def stop(self):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        self.proc.wait(timeout=10)
-        self.fh.close()
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                mx.append(float(parts[2]))
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.th:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["sampler not started"]}
+        self.stop_flag = True
+        self.th.join(timeout=10)
+        out = {"sm_mhz": statistics.median(self.sm) if self.sm else None,
+               "sm_max_mhz": max(self.mx) if self.mx else None, "reasons": sorted(self.reasons),
+               "samples": len(self.sm), "sampler": "nvml 1 ms"}
+        if self.err:
+            out["error"] = self.err
+        return out
 
 
 def phase_bytes(name, U, Uw, n, b, d, F, H, Ntot):
     """Algorithmic bytes (or FLOPs for the tower) per step for each phase."""
     if name == "vsi":
         return 8 * Ntot + 12 * U, "B"
-    if name == "gather_cache":
-        return 8 * Uw + 8 * d * Uw, "B"
+    if name == "gather_cache":  # + the fused zeroing of dG / the FM coefficients (W = 1)
+        return 8 * Uw + 8 * d * Uw + (4 * d * U + 4 * U if Ntot == n else 0), "B"
     if name == "gather_instances":
         return 4 * n + 8 * d * n + 4 * b * d + b * d, "B"
     if name == "segment_sum":
         return 4 * n + 4 * d * n + 4 * d * U, "B"
     if name == "sparse_adam":
         return 28 * d * Uw + 12 * Uw, "B"
-    if name == "tower":
+    if name in ("tower_gemm1", "tower_gemm3"):  # X [b x F*d] streamed once (W1 / dh from L2)
+        return 4 * b * F * d, "B"
+    if name == "tower_gemm2":  # dX [b x F*d] written once
+        return 4 * b * F * d, "B"
+    if name == "tower":  # SIMT validation tiles (SFCTR_TOWER_SIMT=1)
         return 6 * b * F * d * H, "FLOP"
     return None, None
 
@@ -257,7 +275,18 @@ def run_ours(args, D):
                 row.update(flops=int(amount), tflops=round(tf, 2),
                            frac_bf16_sustained=round(tf / peaks["bf16_tflops_sustained"], 4))
         kernels[nm] = row
-    # dominant kernel = the largest phase with an algorithmic model
+    tower_ms = sum(v["ms"] for k2, v in kernels.items() if k2.startswith("tower"))
+    if tower_ms > 0:  # the tower as a whole, for reference: 3 GEMMs (3xTF32) + head + reductions
+        fl = 3 * 6 * args.batch * F * d * H
+        kernels["tower_total"] = {"ms": round(tower_ms, 4), "tf32_flops": fl,
+                                  "tflops": round(fl / (tower_ms / 1e3) / 1e12, 2)}
+    traffic = {}
+    try:  # DRAM bytes per launch from the committed ncu --set full capture (profiles/)
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_launch", {})
+    except Exception:
+        pass
+    # dominant kernel = the largest single-kernel phase with an algorithmic model
     cand = [(v["ms"], k2) for k2, v in kernels.items() if "bytes" in v or "flops" in v]
     dom = max(cand)[1] if cand else None
     roofline = None
@@ -265,8 +294,9 @@ def run_ours(args, D):
         r = kernels[dom]
         if "bytes" in r:
             roofline = {"kernel": dom, "bound": "hbm", "achieved": r["gbs"], "peak": peaks["hbm_gbs"],
-                        "unit": "GB/s", "frac": r["frac_hbm"], "traffic": None,
-                        "peak_source": peak_kind}
+                        "unit": "GB/s", "frac": r["frac_hbm"], "traffic": traffic.get(dom),
+                        "algorithmic_bytes": r["bytes"],
+                        "peak_source": peak_kind + " (copy GB/s, MEASURED_PEAKS.json)"}
         else:
             roofline = {"kernel": dom, "bound": "tensor", "achieved": r["tflops"],
                         "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",

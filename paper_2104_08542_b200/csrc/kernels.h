@@ -40,6 +40,15 @@ void sparse_adam(const uint32_t* grad_idx, const uint32_t* own_slot, int32_t n_o
                  bool inc_steps = true,  // false: the caller bumps the per-row step counts
                  const float* Bsum = nullptr, float fm_scale = 0.f);  // deferred FM term
 
+// Optional callback between the tower's stages (the trainer records a phase event there).
+struct PhaseHook {
+  void (*fn)(void* ctx, const char* name) = nullptr;
+  void* ctx = nullptr;
+  void operator()(const char* name) const {
+    if (fn) fn(ctx, name);
+  }
+};
+
 // ---------------- tower.cu — DeepFM-lite ----------------
 struct TowerBufs {
   int rows_cap = 0, K = 0, H = 0, d = 0;
@@ -82,7 +91,7 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc, const float* X, int ld
                                int32_t rows, int F, int d, const float* dense, float* logits,
                                float* dX, float emb_scale, float* grads, bool accumulate,
                                cudaStream_t s,
-                               bool w1_split_ready = false);
+                               bool w1_split_ready = false, const PhaseHook& hook = {});
 // Fused path (tc_fused.cuh): X = G[vid] is gathered straight into the GEMM
 // operands and dX is scatter-added into dG (with the FM term) by the dX GEMM's
 // epilogue; neither touches HBM. Writes fm_s [rows x d]. Needs d % 4 == 0, d <= 128.

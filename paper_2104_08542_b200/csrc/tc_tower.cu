@@ -432,7 +432,8 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc_, const float* X, int l
                                const float* fm_s, const float* fm_sqp, const uint8_t* labels,
                                int32_t rows, int F, int d, const float* dense, float* logits,
                                float* dX, float emb_scale, float* grads, bool accumulate,
-                               cudaStream_t s, bool w1_split_ready) {
+                               cudaStream_t s, bool w1_split_ready,
+                               const PhaseHook& hook) {
   const int K = F * d, H = t.H;
   SFB_CHECK(rows <= t.rows_cap && rows <= tc_.rows_cap && K == tc_.K && ldx == tc_.ldk,
             "tower buffers too small");
@@ -473,12 +474,14 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc_, const float* X, int l
     p.split_stride = static_cast<long long>(rows) * H;
     launch_ts_gemm<false, false>(dim3(mt, nt, s1), a, bh, bl, p, s);
   }
+  hook("tower_gemm1");
   // ---- head
   head_tc_kernel<<<ceil_div(static_cast<int64_t>(rows) * 32, 256), 256, 0, s>>>(
       rows, H, d, fm_sq_parts(d), tc_.part1, s1, static_cast<long long>(rows) * H, b1, w2, b2p,
       fm_s, fm_sqp, labels, 1.f / rows, logits, t.act, t.dh, t.gz, t.lossr, tc_.dh_hi, tc_.dh_lo,
       tc_.ldh);
   CUDA_LAUNCH_CHECK();
+  hook("tower_head");
   // ---- GEMM2: dX = scale dh W1^T (A = dh hi/lo, B = W1 hi/lo, both K-major; the FM
   //      term is added by segment_sum)
   if (H <= 64) {
@@ -507,6 +510,7 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc_, const float* X, int l
     launch_gemm<64, false, false, tc::kEpiDx, false, 2>(dim3(mt, (K + 63) / 64, 1), ah, al, bh, bl,
                                                        p, s);
   }
+  hook("tower_gemm2");
   // ---- GEMM3: dW1 partials = X^T dh (A = X MN-major, B = dh hi/lo MN-major)
   const int nkb3 = (rows + tc::BKE - 1) / tc::BKE;
   const int mt3 = (K + 127) / 128;
@@ -527,6 +531,7 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc_, const float* X, int l
     p.split_stride = static_cast<long long>(K) * H;
     launch_ts_gemm<true, true>(dim3(mt3, nt, s3), a, bh, bl, p, s);
   }
+  hook("tower_gemm3");
   const int64_t kh = static_cast<int64_t>(K) * H;
   dw1_reduce(tc_.part3, s3, kh, g_w1, accumulate, s);
   small_grads(t, rows, H, g_b1, g_w2, g_b2, g_loss, accumulate, s);

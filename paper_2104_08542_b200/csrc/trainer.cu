@@ -551,8 +551,12 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
     else
       tower_forward_backward_tc(tower_, towertc_, d_X_, ldx_, d_fm_s_, d_fm_sqp_, lab, b_, F_, d_,
                                 d_dense_, d_logits_ + static_cast<size_t>(l) * b_, d_dX_,
-                                emb_scale, d_grads_, l > 0, s, w1_split_ready_);
-    phase("tower");
+                                emb_scale, d_grads_, l > 0, s, w1_split_ready_,
+                                PhaseHook{[](void* c, const char* n) {
+                                             static_cast<Trainer*>(c)->phase(n);
+                                           },
+                                           this});
+    phase(tower_simt_ ? "tower" : "tower_reduce");
     segment_sum(vid, b_ * F_, F_, d_, ldx_, d_dX_, d_G_, d_fm_s_, tower_.gz, emb_scale, d_dG_, s,
                 defer_fm ? d_B_ : nullptr);
     phase("segment_sum");
