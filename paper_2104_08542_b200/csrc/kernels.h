@@ -40,6 +40,17 @@ void sparse_adam(const uint32_t* grad_idx, const uint32_t* own_slot, int32_t n_o
                  bool inc_steps = true,  // false: the caller bumps the per-row step counts
                  const float* Bsum = nullptr, float fm_scale = 0.f);  // deferred FM term
 
+// Fused segment sum for the tower's dX GEMM (one worker, deferred FM term): the epilogue
+// scatter-adds into dG / Bsum instead of writing dX (see tc_dx.cuh, embed.cu segment_sum).
+struct DxScatter {
+  const uint32_t* vid;
+  const float* fm_s;
+  const float* gz;
+  float* dG;
+  float* Bsum;
+  int F, d;
+};
+
 // Optional callback between the tower's stages (the trainer records a phase event there).
 struct PhaseHook {
   void (*fn)(void* ctx, const char* name) = nullptr;
@@ -91,7 +102,10 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc, const float* X, int ld
                                int32_t rows, int F, int d, const float* dense, float* logits,
                                float* dX, float emb_scale, float* grads, bool accumulate,
                                cudaStream_t s,
-                               bool w1_split_ready = false, const PhaseHook& hook = {});
+                               bool w1_split_ready = false, const PhaseHook& hook = {},
+                               const DxScatter* scatter = nullptr);
+// whether the fused dX scatter (tc_dx.cuh) fits: d % 4 == 0 and its smem tables
+bool dx_scatter_fits(int F, int d);
 // Fused path (tc_fused.cuh): X = G[vid] is gathered straight into the GEMM
 // operands and dX is scatter-added into dG (with the FM term) by the dX GEMM's
 // epilogue; neither touches HBM. Writes fm_s [rows x d]. Needs d % 4 == 0, d <= 128.

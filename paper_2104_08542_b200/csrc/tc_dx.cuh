@@ -13,6 +13,16 @@
 //   warps 2..5 : epilogue — tcgen05.ld both accumulator halves, sum, scale, write the
 //                128 x 64 tile into a SWIZZLE_128B staging buffer and TMA-store it
 //                (cp.async.bulk.tensor shared -> global), overlapping the next tile's MMA
+//
+// SCATTER = true fuses the segment sum into the epilogue (one worker, deferred FM term):
+// dX is never written; every 16 B chunk of a tile row goes straight to
+//   dG[vid[r, f]][c..c+3] += scale * (acc + gz[r] * fm_s[r][c..c+3])   (red.global.add.v4.f32)
+// with (f, c) = divmod(column, d), and Bsum[vid[r, f]] += gz[r] once per position (the
+// column c == 0 chunk). vid / gz of the CTA's current 128 rows are staged in smem when m
+// changes (once per ~21 tiles). The accumulator is drained to an smem value tile first
+// (thread = row), then each half-warp scatters one row's 16 chunks: consecutive lanes hit
+// consecutive 16 B of the same dG row, so a red instruction is 2 coalesced 256 B segments
+// instead of 32 scattered 16 B ones.
 #pragma once
 
 #include "tc_gemm.cuh"
@@ -35,7 +45,20 @@ struct DxParams {
   int n_tiles;    // ceil(N / 64)
   int tiles;      // ceil(M / 128) * n_tiles
   float scale;
+  // SCATTER only
+  const uint32_t* vid;  // [M x F] table rows of the positions
+  const float* fm_s;    // [M x d] FM field sums
+  const float* gz;      // [M]
+  float* dG;            // [rows x d] gradient table (red.add)
+  float* Bsum;          // [rows] deferred FM coefficients (red.add)
+  int F, d;
 };
+
+// smem for the scatter epilogue: value tile [128 x 68] f32, vid [128 x F] u32, gz [128]
+constexpr int kDxTileStride = 68;  // 64 columns + 4 pad (16 B aligned rows, fewer conflicts)
+__host__ __device__ constexpr int dx_scatter_bytes(int F, int d) {
+  return BM * kDxTileStride * 4 + BM * F * 4 + BM * 4 + 0 * d;
+}
 
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int x, int y) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
@@ -44,7 +67,14 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
                : "memory");
 }
 
-__global__ void __launch_bounds__(192, 1)
+// SCATTER runs kDxScatterWarps epilogue warps (several per TMEM lane quarter): the scatter is bound by how
+// many red.global.add instructions are in flight per SM
+constexpr int kDxScatterWarps = 16;  // 4 per TMEM lane quarter
+template <bool SCATTER>
+constexpr int dx_threads() { return SCATTER ? 64 + 32 * kDxScatterWarps : 192; }
+
+template <bool SCATTER>
+__global__ void __launch_bounds__(dx_threads<SCATTER>(), 1)
     gemm_dx_persistent_kernel(const __grid_constant__ CUtensorMap tmAhi,
                               const __grid_constant__ CUtensorMap tmAlo,
                               const __grid_constant__ CUtensorMap tmBhi,
@@ -57,8 +87,9 @@ __global__ void __launch_bounds__(192, 1)
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* a_s = smem;
   uint8_t* b_s = smem + L::A_BYTES;
-  uint8_t* out_s = b_s + BS * L::B_STAGE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(out_s + L::OUT_BYTES);
+  uint8_t* out_s = b_s + BS * L::B_STAGE;  // TMA-store staging, or the scatter tables
+  uint64_t* bars = reinterpret_cast<uint64_t*>(
+      out_s + (SCATTER ? ((dx_scatter_bytes(p.F, p.d) + 15) & ~15) : L::OUT_BYTES));
   uint64_t* a_full = bars;
   uint64_t* a_empty = bars + 1;
   uint64_t* b_full = bars + 2;
@@ -80,7 +111,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(acc_full + b, 1);
-      mbar_init(acc_empty + b, 4);
+      mbar_init(acc_empty + b, SCATTER ? kDxScatterWarps : 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmBhi)) : "memory");
@@ -161,6 +192,86 @@ __global__ void __launch_bounds__(192, 1)
         if (t + 1 >= t1 || mn != m) mma_commit(a_empty);
       }
       __syncwarp();
+    }
+  } else if constexpr (SCATTER) {  // ---------------- scatter epilogue (segment sum)
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    constexpr int EW = kDxScatterWarps, CW = 64 / (EW / 4);  // columns each warp drains
+    const int et = threadIdx.x - 64;  // 0 .. 32 EW - 1
+    const int ew = et >> 5;           // epilogue warp
+    const int h = ew >> 2;            // column slice [CW h, CW h + CW) this warp drains
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    const int F = p.F, d = p.d;
+    float* tile = reinterpret_cast<float*>(out_s);
+    uint32_t* vid_s = reinterpret_cast<uint32_t*>(out_s + BM * kDxTileStride * 4);
+    float* gz_s = reinterpret_cast<float*>(vid_s + BM * F);
+    int cur_m = -1;
+    for (int t = t0, i = 0; t < t1; ++t, ++i) {
+      const int m = t / p.n_tiles, n = t - m * p.n_tiles;
+      const int buf = i & 1;
+      const int r0 = m * BM;
+      if (m != cur_m) {  // stage this m-tile's vid / gz (the previous tile's scatter is done)
+        for (int idx = et; idx < BM * F; idx += 32 * EW) {
+          const int r = idx / F;
+          vid_s[idx] = r0 + r < p.M ? __ldg(p.vid + static_cast<int64_t>(r0) * F + idx) : 0u;
+        }
+        if (et < BM) gz_s[et] = r0 + et < p.M ? __ldg(p.gz + r0 + et) : 0.f;
+        cur_m = m;
+      }
+      mbar_wait(acc_full + buf, (i >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      // (1) accumulator -> value tile, thread = row
+      const uint32_t trow = tmem + static_cast<uint32_t>(buf) * 128u + lane_off;
+#pragma unroll
+      for (int c0 = CW * h; c0 < CW * h + CW; c0 += 16) {
+        float v[16], w[16];
+        tmem_ld16(trow + c0, v);
+        tmem_ld16(trow + 64 + c0, w);
+        float4* dst = reinterpret_cast<float4*>(tile + row * kDxTileStride + c0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          dst[j] = make_float4(v[4 * j] + w[4 * j], v[4 * j + 1] + w[4 * j + 1],
+                               v[4 * j + 2] + w[4 * j + 2], v[4 * j + 3] + w[4 * j + 3]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty + buf);  // the MMA of the next tile may start
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");
+      // (2) half-warp per row: lane & 15 = 16 B chunk of the tile's 64 columns
+      const int j = lane & 15;
+      const int col = n * 64 + 4 * j;
+      const int f = col / d, cc = col - f * d;
+      // 8 rows per half-warp, all fm_s loads in flight before the first red (the reds
+      // must not serialise behind one L2 round trip each)
+#pragma unroll 1
+      for (int b0 = 0; b0 < BM / (2 * EW); b0 += 8) {
+        constexpr int NB = BM / (2 * EW) < 8 ? BM / (2 * EW) : 8;
+        float4 fm[NB];
+        bool ok[NB];
+#pragma unroll
+        for (int u8 = 0; u8 < NB; ++u8) {
+          const int rr = 2 * EW * (b0 + u8) + 2 * ew + (lane >> 4);
+          ok[u8] = r0 + rr < p.M && col < p.N;
+          fm[u8] = ok[u8] ? __ldg(reinterpret_cast<const float4*>(
+                                p.fm_s + static_cast<int64_t>(r0 + rr) * d + cc))
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u8 = 0; u8 < NB; ++u8) {
+          const int rr = 2 * EW * (b0 + u8) + 2 * ew + (lane >> 4);
+          if (!ok[u8]) continue;
+          const float4 a = *reinterpret_cast<const float4*>(tile + rr * kDxTileStride + 4 * j);
+          const float g = gz_s[rr];
+          const float k = p.scale * g;
+          const uint32_t u = vid_s[rr * F + f];
+          float* dst = p.dG + static_cast<int64_t>(u) * d + cc;
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst),
+                       "f"(p.scale * a.x + k * fm[u8].x), "f"(p.scale * a.y + k * fm[u8].y),
+                       "f"(p.scale * a.z + k * fm[u8].z), "f"(p.scale * a.w + k * fm[u8].w));
+          if (cc == 0) atomicAdd(p.Bsum + u, g);
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");  // value tile / tables free
     }
   } else {  // ---------------- epilogue
     const int q = warp & 3;

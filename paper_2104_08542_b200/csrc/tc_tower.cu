@@ -177,28 +177,49 @@ int sm_count() {
   return n;
 }
 
-// GEMM2 as a persistent tile walker (tc_dx.cuh); needs H <= 64
+// GEMM2 as a persistent tile walker (tc_dx.cuh); needs H <= 64. With `sc`, the segment
+// sum is fused into the epilogue (dX is never written).
 void launch_dx_gemm(const TowerTC& tc_, const float* dh_hi, const float* dh_lo, int rows, int K,
-                    int H, float* dX, int ldx, float scale, cudaStream_t s) {
+                    int H, float* dX, int ldx, float scale, const DxScatter* sc, cudaStream_t s) {
   const CUtensorMap ah = tmap(dh_hi, H, rows, tc_.ldh, 32, 128);
   const CUtensorMap al = tmap(dh_lo, H, rows, tc_.ldh, 32, 128);
   const CUtensorMap bh = tmap(tc_.w_hi, H, K, tc_.ldh, 32, 64);
   const CUtensorMap bl = tmap(tc_.w_lo, H, K, tc_.ldh, 32, 64);
-  const CUtensorMap out = tmap(dX, K, rows, ldx, 32, 128);
   tc::DxParams p{};
   p.M = rows;
   p.N = K;
   p.n_tiles = (K + 63) / 64;
   p.tiles = ((rows + 127) / 128) * p.n_tiles;
   p.scale = scale;
-  auto kern = tc::gemm_dx_persistent_kernel;
+  const int grid = std::min(p.tiles, sm_count());
+  if (sc) {
+    p.vid = sc->vid;
+    p.fm_s = sc->fm_s;
+    p.gz = sc->gz;
+    p.dG = sc->dG;
+    p.Bsum = sc->Bsum;
+    p.F = sc->F;
+    p.d = sc->d;
+    auto kern = tc::gemm_dx_persistent_kernel<true>;
+    const int smem = 1024 + tc::DxLayout::A_BYTES + tc::DxLayout::B_STAGES * tc::DxLayout::B_STAGE +
+                     ((tc::dx_scatter_bytes(p.F, p.d) + 15) & ~15) + 256;
+    static int configured = 0;
+    if (smem > configured) {
+      CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      configured = smem;
+    }
+    kern<<<grid, tc::dx_threads<true>(), smem, s>>>(ah, al, bh, bl, bh, p);
+    CUDA_LAUNCH_CHECK();
+    return;
+  }
+  const CUtensorMap out = tmap(dX, K, rows, ldx, 32, 128);
+  auto kern = tc::gemm_dx_persistent_kernel<false>;
   constexpr int smem = tc::DxLayout::SMEM;
   static bool configured = false;
   if (!configured) {
     CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = true;
   }
-  const int grid = std::min(p.tiles, sm_count());
   kern<<<grid, 192, smem, s>>>(ah, al, bh, bl, out, p);
   CUDA_LAUNCH_CHECK();
 }
@@ -381,6 +402,14 @@ void launch_scatter_gemm(dim3 grid, const CUtensorMap& ah, const CUtensorMap& al
 
 }  // namespace
 
+bool dx_scatter_fits(int F, int d) {
+  return d % 4 == 0 &&
+         1024 + tc::DxLayout::A_BYTES + tc::DxLayout::B_STAGES * tc::DxLayout::B_STAGE +
+                 ((tc::dx_scatter_bytes(F, d) + 15) & ~15) + 256 <=
+             227 * 1024;
+}
+
+
 bool tower_fused_supported(int d) { return d % 4 == 0 && d <= 128; }
 
 void TowerTC::init(int rc, int k, int h, int d_) {
@@ -433,7 +462,8 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc_, const float* X, int l
                                int32_t rows, int F, int d, const float* dense, float* logits,
                                float* dX, float emb_scale, float* grads, bool accumulate,
                                cudaStream_t s, bool w1_split_ready,
-                               const PhaseHook& hook) {
+                               const PhaseHook& hook,
+                               const DxScatter* scatter) {
   const int K = F * d, H = t.H;
   SFB_CHECK(rows <= t.rows_cap && rows <= tc_.rows_cap && K == tc_.K && ldx == tc_.ldk,
             "tower buffers too small");
@@ -484,8 +514,10 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc_, const float* X, int l
   hook("tower_head");
   // ---- GEMM2: dX = scale dh W1^T (A = dh hi/lo, B = W1 hi/lo, both K-major; the FM
   //      term is added by segment_sum)
+  SFB_CHECK(!scatter || (H <= 64 && dx_scatter_fits(scatter->F, scatter->d)),
+            "fused dX scatter needs H <= 64 and the staging tables to fit in smem");
   if (H <= 64) {
-    launch_dx_gemm(tc_, tc_.dh_hi, tc_.dh_lo, rows, K, H, dX, ldx, emb_scale, s);
+    launch_dx_gemm(tc_, tc_.dh_hi, tc_.dh_lo, rows, K, H, dX, ldx, emb_scale, scatter, s);
   } else {
     const CUtensorMap ah = tmap(tc_.dh_hi, H, rows, tc_.ldh, 32, 128);
     const CUtensorMap al = tmap(tc_.dh_lo, H, rows, tc_.ldh, 32, 128);

@@ -495,6 +495,8 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   // one worker also defers segment_sum's -scale*gz*G term to sparse_adam (which reads the
   // same G row as emb[slot]): the scatter pass then does not re-gather G per position
   const bool defer_fm = zero_in_gather && !tower_fused_;
+  // ... and the segment sum then runs inside the tower's dX GEMM epilogue (dX never hits HBM)
+  const bool fuse_scatter = defer_fm && !tower_simt_ && H_ <= 64 && dx_scatter_fits(F_, d_);
   if (a2a_) {
     xch_.set_counts(h_totals_);
     stats_.nvlink_bytes += xch_.forward(lane_[0].own_k, lane_[0].own_slot, n_own[0],
@@ -544,6 +546,7 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
     }
     gather_instances(vid, b_, F_, d_, ldx_, d_G_, d_X_, d_fm_s_, d_fm_sqp_, s);
     phase("gather_instances");
+    const DxScatter sc{vid, d_fm_s_, tower_.gz, d_dG_, d_B_, F_, d_};
     if (tower_simt_)
       tower_forward_backward_simt(tower_, d_X_, d_fm_s_, d_fm_sqp_, lab, b_, F_, d_, d_dense_,
                                   d_logits_ + static_cast<size_t>(l) * b_, d_dX_, emb_scale,
@@ -555,9 +558,11 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
                                 PhaseHook{[](void* c, const char* n) {
                                              static_cast<Trainer*>(c)->phase(n);
                                            },
-                                           this});
+                                           this},
+                                fuse_scatter ? &sc : nullptr);
     phase(tower_simt_ ? "tower" : "tower_reduce");
-    segment_sum(vid, b_ * F_, F_, d_, ldx_, d_dX_, d_G_, d_fm_s_, tower_.gz, emb_scale, d_dG_, s,
+    if (!fuse_scatter)
+      segment_sum(vid, b_ * F_, F_, d_, ldx_, d_dX_, d_G_, d_fm_s_, tower_.gz, emb_scale, d_dG_, s,
                 defer_fm ? d_B_ : nullptr);
     phase("segment_sum");
   }
