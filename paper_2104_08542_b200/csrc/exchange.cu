@@ -93,6 +93,9 @@ __global__ void owner_reduce_kernel(const uint32_t* __restrict__ own_k, int32_t 
   g[i] = acc;
 }
 
+__global__ void offsets_kernel(const int32_t* __restrict__ totals, int me,
+                               int32_t* __restrict__ offs);
+
 }  // namespace
 
 void Exchange::init(int W_, int me_, int64_t cap_, int d_) {
@@ -110,6 +113,8 @@ void Exchange::init(int W_, int me_, int64_t cap_, int d_) {
   CUDA_CHECK(cudaMalloc(&tile_cnt, sizeof(uint32_t) * 2 * 8 * ntiles));  // recv | send tables
   CUDA_CHECK(cudaMalloc(&tile_off, sizeof(uint32_t) * 2 * 8 * ntiles));
   CUDA_CHECK(cudaMalloc(&totals, sizeof(int32_t) * kTotals));
+  CUDA_CHECK(cudaMalloc(&offs, sizeof(int32_t) * 160));
+  CUDA_CHECK(cudaMemset(offs, 0, sizeof(int32_t) * 160));
   CUDA_CHECK(cudaMalloc(&buf, sizeof(float) * cap * d));
   CUDA_CHECK(cudaMalloc(&gown, sizeof(float) * cap * d));
 }
@@ -124,7 +129,8 @@ void Exchange::release() {
   if (bar) cudaFree(bar);
   for (void* p : {static_cast<void*>(tm), static_cast<void*>(lpos), static_cast<void*>(sscan),
                   static_cast<void*>(tile_cnt), static_cast<void*>(tile_off),
-                  static_cast<void*>(totals), static_cast<void*>(buf), static_cast<void*>(gown)})
+                  static_cast<void*>(totals), static_cast<void*>(buf), static_cast<void*>(gown),
+                  static_cast<void*>(offs)})
     if (p) cudaFree(p);
   *this = Exchange();
 }
@@ -311,6 +317,8 @@ void Exchange::plan(const uint32_t* d_vid, int64_t n_global, int64_t per_worker,
   count_matrix_kernel<<<std::min(ceil_div(c, 256), 148 * 4), 256, 0, s>>>(d_uniq, d_U, c, tm, W,
                                                                            totals + 16);
   CUDA_LAUNCH_CHECK();
+  offsets_kernel<<<1, 1, 0, s>>>(totals, me, offs);
+  CUDA_LAUNCH_CHECK();
 }
 
 void Exchange::local_vids(const uint32_t* d_vid_mine, int64_t n, uint32_t* d_lvid, cudaStream_t s) {
@@ -426,6 +434,156 @@ __global__ void push_block_p2p_kernel(const float4* __restrict__ dE, int64_t src
 }
 
 }  // namespace
+
+namespace {
+
+// the host's set_counts, on the device (one thread): every rank's receive layout
+__global__ void offsets_kernel(const int32_t* __restrict__ totals, int me, int32_t* __restrict__ offs) {
+  const int32_t* cnt = totals + 16;  // cnt[w][o]
+  int32_t* roff = offs + Exchange::kOffRoff;
+  int32_t* boff = offs + Exchange::kOffBoff;
+  int32_t* recv_off = offs + Exchange::kOffRecv;
+  int32_t* send_off = offs + Exchange::kOffSend;
+  for (int w = 0; w < 8; ++w) {
+    roff[w * 8] = 0;
+    for (int o = 1; o < 8; ++o) roff[w * 8 + o] = roff[w * 8 + o - 1] + cnt[w * 8 + o - 1];
+  }
+  for (int o = 0; o < 8; ++o) {
+    boff[o * 8] = 0;
+    for (int w = 1; w < 8; ++w)
+      boff[o * 8 + w] = boff[o * 8 + w - 1] + (w - 1 == o ? 0 : cnt[(w - 1) * 8 + o]);
+  }
+  recv_off[0] = 0;
+  send_off[0] = 0;
+  for (int o = 0; o < 8; ++o) {
+    recv_off[o + 1] = recv_off[o] + totals[o];
+    send_off[o + 1] = send_off[o] + (o == me ? 0 : totals[8 + o]);
+  }
+}
+
+// forward over NVLink, offsets from the device plan (see push_rows_p2p_kernel)
+__global__ void push_rows_p2p_dev_kernel(const uint32_t* __restrict__ own_k,
+                                         const uint32_t* __restrict__ own_slot,
+                                         const int32_t* __restrict__ n_ptr,
+                                         const uint32_t* __restrict__ tm,
+                                         const Cnt8* __restrict__ sscan, uint32_t W, uint32_t me,
+                                         const int32_t* __restrict__ offs,
+                                         const float4* __restrict__ emb, int d4, PeerRows pr) {
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int32_t n_own = *n_ptr;
+  uint32_t e_off[8];
+#pragma unroll
+  for (int w = 0; w < 8; ++w) e_off[w] = w < static_cast<int>(W) ? offs[Exchange::kOffRoff + w * 8 + me] : 0u;
+  for (int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < n_own; j += nwarps) {
+    const uint32_t m = tm[own_k[j]];
+    const float4* src = emb + static_cast<int64_t>(own_slot[j]) * d4;
+#pragma unroll
+    for (uint32_t w = 0; w < 8; ++w) {
+      if (w >= W || !((m >> w) & 1u)) continue;
+      float4* dst = pr.E[w] + static_cast<int64_t>(e_off[w] + sscan[j].c[w]) * d4;
+      for (int c = lane; c < d4; c += 32) dst[c] = src[c];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) __threadfence_system();
+}
+
+// backward over NVLink, block sizes / offsets from the device plan (blockIdx.y = owner)
+__global__ void push_blocks_p2p_dev_kernel(const float4* __restrict__ dE, int d4, uint32_t me,
+                                           const int32_t* __restrict__ totals,
+                                           const int32_t* __restrict__ offs, PeerRows pr) {
+  const int o = blockIdx.y;
+  if (o != static_cast<int>(me)) {
+    const int64_t n = static_cast<int64_t>(totals[o]) * d4;
+    const float4* src = dE + static_cast<int64_t>(offs[Exchange::kOffRecv + o]) * d4;
+    float4* dst = pr.buf[o] + static_cast<int64_t>(offs[Exchange::kOffBoff + o * 8 + me]) * d4;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+      dst[i] = src[i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) __threadfence_system();
+}
+
+__global__ void zero_rows_dev_kernel(float4* __restrict__ p, const int32_t* __restrict__ offs,
+                                     int d4) {
+  const int64_t n = static_cast<int64_t>(offs[Exchange::kOffRecv + 8]) * d4;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    p[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+__global__ void owner_reduce_dev_kernel(const uint32_t* __restrict__ own_k,
+                                        const int32_t* __restrict__ n_ptr,
+                                        const uint32_t* __restrict__ tm,
+                                        const Cnt8* __restrict__ sscan,
+                                        const int32_t* __restrict__ totals, uint32_t W, uint32_t me,
+                                        const uint32_t* __restrict__ lpos,
+                                        const float4* __restrict__ dE,
+                                        const float4* __restrict__ recvbuf, int d4,
+                                        float4* __restrict__ g) {
+  const int64_t n = static_cast<int64_t>(*n_ptr) * d4;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j = i / d4;
+    const int c = static_cast<int>(i - j * d4);
+    const uint32_t k = own_k[j];
+    const uint32_t m = tm[k];
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t soff = 0;
+    for (uint32_t w = 0; w < W; ++w) {  // fixed source order (same as owner_reduce_kernel)
+      if ((m >> w) & 1u) {
+        const float4 v = (w == me) ? dE[static_cast<int64_t>(lpos[k]) * d4 + c]
+                                   : recvbuf[static_cast<int64_t>(soff + sscan[j].c[w]) * d4 + c];
+        acc.x += v.x;
+        acc.y += v.y;
+        acc.z += v.z;
+        acc.w += v.w;
+      }
+      if (w != me) soff += static_cast<uint32_t>(totals[8 + w]);
+    }
+    g[i] = acc;
+  }
+}
+
+}  // namespace
+
+void Exchange::forward_dev(const uint32_t* d_own_k, const uint32_t* d_own_slot, int32_t n_bound,
+                           const int32_t* d_n_own, const float* emb, cudaStream_t s) {
+  PeerRows pr{};
+  for (int w = 0; w < W; ++w) pr.E[w] = reinterpret_cast<float4*>(peer_E[w]);
+  push_rows_p2p_dev_kernel<<<std::max(1, std::min(ceil_div(static_cast<int64_t>(n_bound) * 32, 256),
+                                                  148 * 8)),
+                             256, 0, s>>>(d_own_k, d_own_slot, d_n_own, tm, sscan, W, me, offs,
+                                          reinterpret_cast<const float4*>(emb), d / 4, pr);
+  CUDA_LAUNCH_CHECK();
+}
+
+void Exchange::backward_send_dev(const float* dE, cudaStream_t s) {
+  PeerRows pr{};
+  for (int o = 0; o < W; ++o) pr.buf[o] = reinterpret_cast<float4*>(peer_buf[o]);
+  push_blocks_p2p_dev_kernel<<<dim3(148 * 2, W), 256, 0, s>>>(reinterpret_cast<const float4*>(dE),
+                                                              d / 4, me, totals, offs, pr);
+  CUDA_LAUNCH_CHECK();
+}
+
+void Exchange::backward_reduce_dev(const uint32_t* d_own_k, int32_t n_bound, const int32_t* d_n_own,
+                                   const float* dE, cudaStream_t s) {
+  const int d4 = d / 4;
+  owner_reduce_dev_kernel<<<std::max(1, std::min(ceil_div(static_cast<int64_t>(n_bound) * d4, 256),
+                                                 148 * 8)),
+                            256, 0, s>>>(d_own_k, d_n_own, tm, sscan, totals, W, me, lpos,
+                                         reinterpret_cast<const float4*>(dE),
+                                         reinterpret_cast<const float4*>(buf), d4,
+                                         reinterpret_cast<float4*>(gown));
+  CUDA_LAUNCH_CHECK();
+}
+
+void Exchange::zero_local_dev(float* dE, cudaStream_t s) {
+  zero_rows_dev_kernel<<<148 * 8, 256, 0, s>>>(reinterpret_cast<float4*>(dE), offs, d / 4);
+  CUDA_LAUNCH_CHECK();
+}
 
 void Exchange::setup_p2p(float* E, ncclComm_t comm, cudaStream_t s) {
   int dev = 0;

@@ -45,6 +45,10 @@ struct Exchange {
   std::vector<int64_t> roff_all, boff_all;  // [w*8+o]: rank w's E block of owner o;
                                             // [o*8+w]: owner o's buf block of source w
   static constexpr int kTotals = 80;
+  // device copy of the layout set_counts derives on the host, written by plan():
+  // [0, 64) roff_all, [64, 128) boff_all, [128, 137) recv_off, [137, 146) send_off
+  int32_t* offs = nullptr;
+  static constexpr int kOffRoff = 0, kOffBoff = 64, kOffRecv = 128, kOffSend = 137;
 
   void init(int W, int me, int64_t cap, int d);
   void release();
@@ -63,6 +67,16 @@ struct Exchange {
   int64_t forward(const uint32_t* d_own_k, const uint32_t* d_own_slot, int32_t n_own,
                   const float* emb, float* E, ncclComm_t comm, cudaStream_t s,
                   bool do_barrier = true);
+  // Peer-store transport driven by device counts only (no host copy of the plan):
+  // n_bound bounds the grids, d_n_own is the owned count; nothing returns bytes
+  void forward_dev(const uint32_t* d_own_k, const uint32_t* d_own_slot, int32_t n_bound,
+                   const int32_t* d_n_own, const float* emb, cudaStream_t s);
+  void backward_send_dev(const float* dE, cudaStream_t s);
+  void backward_reduce_dev(const uint32_t* d_own_k, int32_t n_bound, const int32_t* d_n_own,
+                           const float* dE, cudaStream_t s);
+  // dE[0 : local rows) = 0 with the row count read on the device
+  void zero_local_dev(float* dE, cudaStream_t s);
+  bool device_driven() const { return p2p && !copy_engine; }
   int64_t backward(const uint32_t* d_own_k, int32_t n_own, const float* dE, ncclComm_t comm,
                    cudaStream_t s);
   // the same in parts: send my partial gradients (no barrier), then the owner-side sum

@@ -262,6 +262,8 @@ struct TailArgs {
   float *w_hi, *w_lo, *wt_hi, *wt_lo;
   int K, H, ldh, ldk;
   int64_t* acc;  // nullptr: no totals this step
+  const int32_t* xtotals;  // owner-routed exchange plan totals (nullptr: none)
+  int me;
   LaneCounters cnt;
   const int32_t* U;
   int W, d;
@@ -306,6 +308,9 @@ __global__ void tail_kernel(TailArgs a) {
       a.acc[1] += owned;
       a.acc[2] += working;
       a.acc[3] += static_cast<int64_t>(a.lanes) * (2 * arb(U * a.d * 4) + arb(a.P * 4));
+      if (a.xtotals)  // rows pushed to / received from peers, both directions
+        for (int w = 0; w < a.W; ++w)
+          if (w != a.me) a.acc[4] += static_cast<int64_t>(a.xtotals[8 + w] + a.xtotals[w]) * a.d * 4;
     }
   }
 }
@@ -416,20 +421,24 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   }
   for (int l = 0; l < lanes_; ++l) lane_[l].probe(d_uniq_, cap, Wu, t, s);
   phase("manage_probe");
+  // Host wait: needed for evictions (the LRU victim count), the capacity check and the
+  // NCCL / exchange sizes. A step whose admissions provably fit the free slots
+  // (free_lb_ >= the per-step admission bound umax) skips it when nothing else needs host
+  // counts: one process, or the owner-routed exchange over peer stores (its layout is
+  // derived on the device). Every kernel below reads the unique / owned / working counts
+  // and the exchange plan from the device.
+  const int64_t bound = lane_[0].umax;
+  const bool xdev = a2a_ && xch_.device_driven();
+  bool free_step = world_ == 1 || xdev;
+  for (int l = 0; l < lanes_ && free_step; ++l) free_step = free_lb_[l] >= bound;
   if (a2a_) {  // exchange plan (touched masks, send/receive positions), device only
     xch_.plan(d_vid_, n_global_, static_cast<int64_t>(b_) * F_, d_uniq_, d_scalars_ + 0,
               lane_[0].own_k, lane_[0].counters + kCntOwned, s);
-    CUDA_CHECK(cudaMemcpyAsync(h_totals_, xch_.totals, sizeof(int32_t) * Exchange::kTotals,
-                               cudaMemcpyDeviceToHost, s));
+    if (!free_step)
+      CUDA_CHECK(cudaMemcpyAsync(h_totals_, xch_.totals, sizeof(int32_t) * Exchange::kTotals,
+                                 cudaMemcpyDeviceToHost, s));
     phase("exchange_plan");
   }
-  // Host wait: needed for evictions (the LRU victim count), the capacity check and the
-  // NCCL / exchange sizes. A single-process step whose admissions provably fit the free
-  // slots (free_lb_ >= the per-step admission bound umax) skips it: every kernel below
-  // reads the unique / owned / working counts from the device.
-  const int64_t bound = lane_[0].umax;
-  bool free_step = world_ == 1;
-  for (int l = 0; l < lanes_ && free_step; ++l) free_step = free_lb_[l] >= bound;
   int32_t U = 0;
   std::vector<int32_t> n_own(lanes_, static_cast<int32_t>(bound)), n_work(lanes_, 0);
   if (!free_step) {
@@ -498,13 +507,21 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   // ... and the segment sum then runs inside the tower's dX GEMM epilogue (dX never hits HBM)
   const bool fuse_scatter = defer_fm && !tower_simt_ && H_ <= 64 && dx_scatter_fits(F_, d_);
   if (a2a_) {
-    xch_.set_counts(h_totals_);
-    stats_.nvlink_bytes += xch_.forward(lane_[0].own_k, lane_[0].own_slot, n_own[0],
-                                        lane_[0].emb, d_G_, comm_, s, /*barrier=*/false);
+    if (!free_step) {
+      xch_.set_counts(h_totals_);
+      for (int w = 0; w < W_; ++w)  // rows this rank pushes / receives, both directions
+        if (w != rank_) stats_.nvlink_bytes += (h_totals_[8 + w] + h_totals_[w]) * 4ll * d_;
+    }
+    if (xdev)
+      xch_.forward_dev(lane_[0].own_k, lane_[0].own_slot, n_own[0],
+                       lane_[0].counters + kCntOwned, lane_[0].emb, s);
+    else
+      xch_.forward(lane_[0].own_k, lane_[0].own_slot, n_own[0], lane_[0].emb, d_G_, comm_, s,
+                   /*barrier=*/false);
     phase("exchange_embed");
     if (xch_.p2p) xch_.barrier(comm_, s);
     phase("exchange_barrier");
-    table_rows = static_cast<size_t>(xch_.local_rows());
+    table_rows = free_step ? static_cast<size_t>(n_global_) : static_cast<size_t>(xch_.local_rows());
     xch_.local_vids(d_vid_ + static_cast<size_t>(lane0_) * b_ * F_, n_local_, d_lvid_, s);
   } else {
     if (world_ > 1) CUDA_CHECK(cudaMemsetAsync(d_G_, 0, sizeof(float) * ud, s));
@@ -526,6 +543,8 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
 
   // ---- per lane: gather_instances, forward_backward, segment_sum (l.11-12)
   if (zero_in_gather) {
+  } else if (xdev) {
+    xch_.zero_local_dev(d_dG_, s);
   } else if (free_step && d_ % 4 == 0)
     zero_rows_kernel<<<148 * 8, 256, 0, s>>>(reinterpret_cast<float4*>(d_dG_), d_scalars_ + 0,
                                              d_ / 4, n_global_ * (d_ / 4));
@@ -570,11 +589,17 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   // ---- grad_synchronize (l.13)
   const float* grad_rows = d_dG_;
   if (a2a_) {
-    stats_.nvlink_bytes += xch_.backward_send(d_dG_, comm_, s);
+    if (xdev)
+      xch_.backward_send_dev(d_dG_, s);
+    else
+      xch_.backward_send(d_dG_, comm_, s);
     phase("exchange_grad_send");
     if (xch_.p2p) xch_.barrier(comm_, s);
     phase("exchange_grad_barrier");
-    xch_.backward_reduce(lane_[0].own_k, n_own[0], d_dG_, s);
+    if (xdev)
+      xch_.backward_reduce_dev(lane_[0].own_k, n_own[0], lane_[0].counters + kCntOwned, d_dG_, s);
+    else
+      xch_.backward_reduce(lane_[0].own_k, n_own[0], d_dG_, s);
     grad_rows = xch_.gown;
   } else if (world_ > 1) {
     NCCL_CHECK(ncclAllReduce(d_dG_, d_dG_, ud, ncclFloat32, ncclSum, comm_, s));
@@ -640,6 +665,8 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
       a.ldk = towertc_.ldk;
     }
     a.acc = free_step ? d_acc_ : nullptr;
+    a.xtotals = xdev ? xch_.totals : nullptr;
+    a.me = rank_;
     a.U = d_scalars_ + 0;
     a.W = W_;
     a.d = d_;
@@ -728,6 +755,7 @@ void Trainer::refresh() {
     stats_.total_working += h_acc_[2];
     led_[0] += h_acc_[2] * d_ * 12;
     led_[2] += h_acc_[3];
+    stats_.total_nvlink_bytes += h_acc_[4];
     acc_pending_ = false;
   }
   for (int l = 0; l < lanes_; ++l) {
