@@ -55,6 +55,8 @@ def parse():
     # alltoall = owner-routed exchange of only the touched rows (default); allreduce = the
     # reference's all-reduce of the zero-padded common embedding / gradients
     p.add_argument("--sync", default="alltoall", choices=["allreduce", "alltoall"])
+    # pipelined = the manager stage of step t+1 overlaps step t's training (identical results)
+    p.add_argument("--mode", default="pipelined", choices=["pipelined", "sequential"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-rows", type=int, default=2048, help="rows per CPU-baseline step")
     p.add_argument("--cpu-steps", type=int, default=3)
@@ -166,6 +168,7 @@ def run_ours(args, D):
                     embedding_dim=args.dim, vocabulary_size=args.vocab, cache_capacity=args.cache,
                     hidden_dim=args.hidden, zipf_exponent=args.zipf, seed=7)
     cfg.apply("sync", args.sync)
+    cfg.apply("mode", args.mode)
     nid = sdist.nccl_id_for(D, sb.nccl_unique_id)
     t0 = time.time()
     tr = sb.Trainer(cfg, rank=rank, world=world, nccl_id=nid, device=dev)
@@ -222,7 +225,8 @@ def run_ours(args, D):
                  "filled_from_host": filled, "pcie_h2d_bytes": filled * (3 * args.dim + 1) * 4,
                  "pcie_d2h_bytes": tot["total_evicted"] * (3 * args.dim + 1) * 4,
                  "nvlink_bytes": tot["total_nvlink_bytes"], "kernel_launches": launches,
-                 "host_wait_free_steps": tot["total_free_steps"]}
+                 "host_wait_free_steps": tot["total_free_steps"],
+                 "pinned_waits": tot["total_pinned_waits"]}
     D.barrier()
     ms_step = D.max(dev_ms) / K
     loss_dev = float(d_loss.item())
@@ -243,9 +247,17 @@ def run_ours(args, D):
     torch.cuda.synchronize()
     w0 = time.perf_counter()
     losses = []
-    for i in range(K):
-        s = W + 2 * K + i
-        losses.append(tr.step(s, hf[s], hl[s]))
+    if args.mode == "pipelined":  # one step in flight: submit step s, then read loss of s-1
+        for i in range(K):
+            s = W + 2 * K + i
+            tr.submit(s, hf[s], hl[s])
+            if i > 0:
+                losses.append(tr.loss(s - 1))
+        losses.append(tr.loss(W + 3 * K - 1))
+    else:
+        for i in range(K):
+            s = W + 2 * K + i
+            losses.append(tr.step(s, hf[s], hl[s]))
     torch.cuda.synchronize()
     e2e_s = D.max(time.perf_counter() - w0)
     D.barrier()
@@ -333,7 +345,7 @@ def run_ours(args, D):
         "data": "synthetic (device Zipf generator, bit-exact with the reference SyntheticGenerator)",
         "config": {"workload": WORKLOAD, "global_batch": rows_global, "fields": F, "dim": d,
                    "vocab": args.vocab, "hidden": H, "zipf": args.zipf,
-                   "cache_slots_per_gpu": args.cache, "sync": args.sync,
+                   "cache_slots_per_gpu": args.cache, "sync": args.sync, "mode": args.mode,
                    "parallelism": f"dp{world} (embedding rows owned f mod {world})",
                    "l2": "no flush: per-step working set > L2 (X alone is 102 MB/GPU)",
                    "setup_s": round(setup_s, 2)},

@@ -47,6 +47,9 @@ int sfctr_abi_version(void);
  * ------------------------------------------------------------------- */
 enum { SFCTR_STRATEGY_HOST = 0, SFCTR_STRATEGY_PREFETCH = 1, SFCTR_STRATEGY_CACHE = 2 };
 enum { SFCTR_SYNC_ALLREDUCE = 0, SFCTR_SYNC_ALLTOALL = 1 };
+/* RunMode (config.hpp:30): pipelined overlaps the manager stage of step t+1 with the
+ * training of step t; results are identical to sequential. */
+enum { SFCTR_MODE_SEQUENTIAL = 0, SFCTR_MODE_PIPELINED = 1 };
 
 typedef struct sfctr_config {
   /* reference fields, config.hpp:44-71 (same defaults) */
@@ -68,6 +71,7 @@ typedef struct sfctr_config {
   /* B200 extensions (config keys in parentheses) */
   int32_t sync_mode;             /* (sync) allreduce (reference scheme) | alltoall (owner-routed) */
   uint64_t host_table_rows;      /* (host_rows) pinned host-table rows per worker; 0 = ceil(vocab/W) */
+  int32_t run_mode;              /* (mode) sequential | pipelined — RunMode, config.hpp:30 */
 } sfctr_config;
 
 void sfctr_config_default(sfctr_config* cfg);
@@ -166,6 +170,15 @@ int sfctr_trainer_step(sfctr_trainer* t, int64_t step, const uint64_t* features,
 int sfctr_trainer_step_device(sfctr_trainer* t, int64_t step, const uint64_t* d_features,
                               const uint8_t* d_labels, const uint64_t* d_window_features,
                               float* d_loss);
+/* The host-buffer step split in two, for a driver that keeps one step in flight
+ * (pipelined mode overlaps the manager stage of step t+1 with step t's training):
+ * submit enqueues the H2D copies of the inputs, the step and the D2H copy of its loss,
+ * and returns; loss waits for that step's loss. At most two submitted steps may be
+ * outstanding: read the loss of step t before submitting step t+2 (else LOGIC). The
+ * host input buffers must stay untouched until the step's loss has been read. */
+int sfctr_trainer_submit(sfctr_trainer* t, int64_t step, const uint64_t* features,
+                         const uint8_t* labels, const uint64_t* window_features);
+int sfctr_trainer_loss(sfctr_trainer* t, int64_t step, double* loss);
 /* Waits for the trainer's stream; reports deferred device-side errors. */
 int sfctr_trainer_synchronize(sfctr_trainer* t);
 /* cudaStream_t the trainer launches on */
@@ -214,6 +227,9 @@ typedef struct sfctr_step_stats {
   int64_t total_owned;
   int64_t total_nvlink_bytes;
   int64_t total_free_steps; /* steps that ran without a mid-step host wait */
+  int64_t pinned_waits;     /* pipelined: 1 if the last step's eviction had to wait for the
+                               previous step's rows to be unpinned */
+  int64_t total_pinned_waits;
 } sfctr_step_stats;
 int sfctr_trainer_stats(sfctr_trainer* t, sfctr_step_stats* out);
 

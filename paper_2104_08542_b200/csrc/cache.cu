@@ -121,18 +121,29 @@ __global__ void mark_window_kernel(const uint32_t* __restrict__ gids,
 
 // LRU key per slot: eligible = occupied && !needed_soon (pins are implied by
 // BSP stream order: batch t-1's update has completed before manage(t) runs).
+// old_cnt (nullable): number of eligible slots last used before step t-1, i.e. not
+// touched by the batch still training when the manager runs one step ahead
+// (pipelined mode); victims drawn only from those are the sequential-mode victims.
 __global__ void victim_keys_kernel(uint32_t C, const uint32_t* __restrict__ slot_feat,
                                    const int32_t* __restrict__ mark, int32_t t,
                                    const int32_t* __restrict__ last_use,
                                    const uint64_t* __restrict__ admit_seq,
-                                   uint64_t* __restrict__ keys, uint32_t* __restrict__ ids) {
+                                   uint64_t* __restrict__ keys, uint32_t* __restrict__ ids,
+                                   int32_t* __restrict__ old_cnt) {
   const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= C) return;
-  const bool eligible = slot_feat[s] != kEmpty && mark[s] != t;
-  keys[s] = eligible ? (static_cast<uint64_t>(last_use[s] + 1) << 40) |
-                           (admit_seq[s] & ((1ull << 40) - 1))
-                     : ~0ull;
-  ids[s] = s;
+  bool old = false;
+  if (s < C) {
+    const bool eligible = slot_feat[s] != kEmpty && mark[s] != t;
+    const int32_t lu = last_use[s];
+    keys[s] = eligible ? (static_cast<uint64_t>(lu + 1) << 40) | (admit_seq[s] & ((1ull << 40) - 1))
+                       : ~0ull;
+    ids[s] = s;
+    old = eligible && lu < t - 1;
+  }
+  if (old_cnt) {
+    const int n = __syncthreads_count(old);
+    if (threadIdx.x == 0 && n) atomicAdd(old_cnt, n);
+  }
 }
 
 // pull_parameters_to_host: one warp per victim, 16 B zero-copy stores to the
@@ -340,8 +351,11 @@ void CacheLane::init(uint64_t capacity, int dim, uint64_t owned_rows, uint64_t h
   // per-step scratch
   CUDA_CHECK(cudaMalloc(&flag, sizeof(uint32_t) * umax));
   CUDA_CHECK(cudaMalloc(&rank, sizeof(uint32_t) * umax));
-  CUDA_CHECK(cudaMalloc(&own_k, sizeof(uint32_t) * umax));
-  CUDA_CHECK(cudaMalloc(&own_slot, sizeof(uint32_t) * umax));
+  for (int k = 0; k < 2; ++k) {
+    CUDA_CHECK(cudaMalloc(&own_k_set[k], sizeof(uint32_t) * umax));
+    CUDA_CHECK(cudaMalloc(&own_slot_set[k], sizeof(uint32_t) * umax));
+  }
+  use(0);
   CUDA_CHECK(cudaMalloc(&miss, sizeof(uint32_t) * umax));
   CUDA_CHECK(cudaMalloc(&miss_rank, sizeof(uint32_t) * umax));
   CUDA_CHECK(cudaMalloc(&work_j, sizeof(uint32_t) * umax));
@@ -355,8 +369,8 @@ void CacheLane::init(uint64_t capacity, int dim, uint64_t owned_rows, uint64_t h
   scan_bytes = scan_temp_bytes(umax);
   sort_bytes = sort_pairs_temp_bytes(static_cast<int64_t>(C));
   CUDA_CHECK(cudaMalloc(&temp, std::max(scan_bytes, sort_bytes)));
-  CUDA_CHECK(cudaMalloc(&counters, sizeof(int32_t) * 8));
-  CUDA_CHECK(cudaMemset(counters, 0, sizeof(int32_t) * 8));
+  CUDA_CHECK(cudaMalloc(&counters, sizeof(int32_t) * kCntWords));
+  CUDA_CHECK(cudaMemset(counters, 0, sizeof(int32_t) * kCntWords));
   CUDA_CHECK(cudaMemcpy(counters + kCntFreeTop, &free_top, sizeof(int32_t), cudaMemcpyHostToDevice));
   CUDA_CHECK(cudaDeviceSynchronize());
 }
@@ -367,7 +381,9 @@ void CacheLane::release() {
                   static_cast<void*>(last_use), static_cast<void*>(admit_seq),
                   static_cast<void*>(mark), static_cast<void*>(free_stack),
                   static_cast<void*>(index), static_cast<void*>(flag), static_cast<void*>(rank),
-                  static_cast<void*>(own_k), static_cast<void*>(own_slot), static_cast<void*>(miss),
+                  static_cast<void*>(own_k_set[0]), static_cast<void*>(own_slot_set[0]),
+                  static_cast<void*>(own_k_set[1]), static_cast<void*>(own_slot_set[1]),
+                  static_cast<void*>(miss),
                   static_cast<void*>(miss_rank), static_cast<void*>(work_j),
                   static_cast<void*>(own_f), static_cast<void*>(work_f), static_cast<void*>(work_w),
                   static_cast<void*>(keys), static_cast<void*>(keys_sorted),
@@ -418,11 +434,16 @@ void CacheLane::probe(const uint32_t* d_gids, int32_t cap, uint32_t W, int32_t t
   CUDA_LAUNCH_CHECK();
 }
 
-void CacheLane::evict(int32_t n_evict, uint32_t W, int32_t t, cudaStream_t s) {
-  if (n_evict <= 0) return;
+void CacheLane::victim_keys(int32_t t, bool count_old, cudaStream_t s) {
   victim_keys_kernel<<<ceil_div(C, 256), 256, 0, s>>>(static_cast<uint32_t>(C), slot_feat, mark, t,
-                                                      last_use, admit_seq, keys, ids);
+                                                      last_use, admit_seq, keys, ids,
+                                                      count_old ? counters + kCntOld : nullptr);
   CUDA_LAUNCH_CHECK();
+}
+
+void CacheLane::evict(int32_t n_evict, uint32_t W, int32_t t, cudaStream_t s, bool keys_ready) {
+  if (n_evict <= 0) return;
+  if (!keys_ready) victim_keys(t, false, s);
   sort_pairs_u64_u32(temp, sort_bytes, keys, keys_sorted, ids, ids_sorted,
                      static_cast<int64_t>(C), 64, s);
   evict_kernel<<<ceil_div(static_cast<int64_t>(n_evict) * 32, 256), 256, 0, s>>>(

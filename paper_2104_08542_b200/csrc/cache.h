@@ -17,7 +17,9 @@ enum {
   kCntError = 3,
   kCntMarked = 4,
   kCntFreeTop = 5,
-  kCntSeq = 6
+  kCntSeq = 6,  // u64 over [6, 8)
+  kCntOld = 8,  // pipelined manager: eligible victims older than the in-flight batch
+  kCntWords = 16
 };
 
 struct CacheLane {
@@ -43,8 +45,10 @@ struct CacheLane {
   float* host_rows = nullptr;     // pinned mapped [host_cap * 3d]
   int32_t* host_steps = nullptr;  // pinned mapped [host_cap]
 
-  // per-step scratch
+  // per-step scratch; own_k / own_slot are read by the training stage, so they come in
+  // two sets (step parity) and the manager of step t+1 fills one while step t trains
   uint32_t *flag = nullptr, *rank = nullptr, *own_k = nullptr, *own_slot = nullptr;
+  uint32_t *own_k_set[2] = {nullptr, nullptr}, *own_slot_set[2] = {nullptr, nullptr};
   uint32_t *miss = nullptr, *miss_rank = nullptr, *work_j = nullptr;
   // probe-time facts about the misses, so admit reads them coalesced instead of
   // chasing work_j -> own_k -> gids -> index: feature and index entry (kOnHost / kNever)
@@ -53,11 +57,15 @@ struct CacheLane {
   uint32_t *ids = nullptr, *ids_sorted = nullptr;
   void* temp = nullptr;
   size_t scan_bytes = 0, sort_bytes = 0;
-  int32_t* counters = nullptr;  // [8] device counters (kCnt*)
+  int32_t* counters = nullptr;  // [kCntWords] device counters (kCnt*)
 
   void init(uint64_t capacity, int dim, uint64_t owned_rows, uint64_t host_rows_cap,
             int64_t max_unique);
   void release();
+  void use(int set) {
+    own_k = own_k_set[set];
+    own_slot = own_slot_set[set];
+  }
 
   // U / n_own are device counts; `cap` bounds the grids (the global batch size)
   // vsi_first (nullable): VSI first-position table to clear behind the batch
@@ -66,8 +74,12 @@ struct CacheLane {
   void mark_window(const uint32_t* d_gids, const int32_t* d_U, int32_t cap, uint32_t W, uint32_t w,
                    int32_t t, cudaStream_t s);
   void probe(const uint32_t* d_gids, int32_t cap, uint32_t W, int32_t t, cudaStream_t s);
-  // victims go on top of the device free stack; n_evict is host-known (sync steps only)
-  void evict(int32_t n_evict, uint32_t W, int32_t t, cudaStream_t s);
+  // LRU keys of every slot (eligible = occupied && !needed_soon); with count_old, also
+  // counts the eligible slots whose last use precedes step t-1 into counters[kCntOld]
+  void victim_keys(int32_t t, bool count_old, cudaStream_t s);
+  // victims go on top of the device free stack; n_evict is host-known (sync steps only);
+  // keys_ready: victim_keys already ran for this step
+  void evict(int32_t n_evict, uint32_t W, int32_t t, cudaStream_t s, bool keys_ready = false);
   // admits counters[kCntWorking] rows (device count, <= n_bound) from the device free
   // stack, then advances the device free-stack height (+ n_evict - n_work) and admit_seq
   void admit(int32_t n_bound, int32_t n_evict, uint32_t W, uint64_t seed, int32_t t,

@@ -91,6 +91,11 @@ void apply_entry(sfctr_config& c, const std::string& key, const std::string& val
     else if (value == "alltoall") c.sync_mode = SFCTR_SYNC_ALLTOALL;
     else sfb::fail(sfb::kConfig, "config key 'sync': expected allreduce or alltoall");
   } else if (key == "host_rows") c.host_table_rows = parse_u64(key, value);
+  else if (key == "mode") {  // run_mode_from_string (config.cpp:49-53)
+    if (value == "pipelined") c.run_mode = SFCTR_MODE_PIPELINED;
+    else if (value == "sequential") c.run_mode = SFCTR_MODE_SEQUENTIAL;
+    else sfb::fail(sfb::kConfig, "unknown mode '" + value + "' (expected pipelined or sequential)");
+  }
   else sfb::fail(sfb::kConfig, "unknown config key '" + key + "'");
 }
 
@@ -158,6 +163,7 @@ void sfctr_config_default(sfctr_config* c) {  // config.hpp:44-71
   c->hidden_dim = 64;
   c->sync_mode = SFCTR_SYNC_ALLREDUCE;
   c->host_table_rows = 0;
+  c->run_mode = SFCTR_MODE_SEQUENTIAL;
 }
 
 int sfctr_config_validate(const sfctr_config* c) {
@@ -408,6 +414,19 @@ int sfctr_trainer_step(sfctr_trainer* t, int64_t step, const uint64_t* features,
 int sfctr_trainer_step_device(sfctr_trainer* t, int64_t step, const uint64_t* d_features,
                               const uint8_t* d_labels, const uint64_t* d_window, float* d_loss) {
   return guarded([&] { t->t->step_device(step, d_features, d_labels, d_window, d_loss); });
+}
+
+int sfctr_trainer_submit(sfctr_trainer* t, int64_t step, const uint64_t* features,
+                         const uint8_t* labels, const uint64_t* window) {
+  return guarded([&] { t->t->submit_host(step, features, labels, window); });
+}
+
+int sfctr_trainer_loss(sfctr_trainer* t, int64_t step, double* loss) {
+  return guarded([&] {
+    const double l = t->t->loss_of(step);
+    if (!std::isfinite(l)) sfb::fail(sfb::kRun, "non-finite loss", step);
+    if (loss) *loss = l;
+  });
 }
 
 int sfctr_trainer_synchronize(sfctr_trainer* t) {

@@ -106,15 +106,18 @@ void Exchange::init(int W_, int me_, int64_t cap_, int d_) {
   d = d_;
   SFB_CHECK(W <= 8, "alltoall sync supports at most 8 workers");
   SFB_CHECK((d & 3) == 0, "alltoall sync needs embedding_dim % 4 == 0");
-  CUDA_CHECK(cudaMalloc(&tm, sizeof(uint32_t) * cap));
-  CUDA_CHECK(cudaMalloc(&lpos, sizeof(uint32_t) * cap));
-  CUDA_CHECK(cudaMalloc(&sscan, sizeof(Cnt8) * cap));
   const int ntiles = ceil_div(cap, 1024);
-  CUDA_CHECK(cudaMalloc(&tile_cnt, sizeof(uint32_t) * 2 * 8 * ntiles));  // recv | send tables
-  CUDA_CHECK(cudaMalloc(&tile_off, sizeof(uint32_t) * 2 * 8 * ntiles));
-  CUDA_CHECK(cudaMalloc(&totals, sizeof(int32_t) * kTotals));
-  CUDA_CHECK(cudaMalloc(&offs, sizeof(int32_t) * 160));
-  CUDA_CHECK(cudaMemset(offs, 0, sizeof(int32_t) * 160));
+  for (PlanSet& p : sets) {
+    CUDA_CHECK(cudaMalloc(&p.tm, sizeof(uint32_t) * cap));
+    CUDA_CHECK(cudaMalloc(&p.lpos, sizeof(uint32_t) * cap));
+    CUDA_CHECK(cudaMalloc(&p.sscan, sizeof(Cnt8) * cap));
+    CUDA_CHECK(cudaMalloc(&p.tile_cnt, sizeof(uint32_t) * 2 * 8 * ntiles));  // recv | send tables
+    CUDA_CHECK(cudaMalloc(&p.tile_off, sizeof(uint32_t) * 2 * 8 * ntiles));
+    CUDA_CHECK(cudaMalloc(&p.totals, sizeof(int32_t) * kTotals));
+    CUDA_CHECK(cudaMalloc(&p.offs, sizeof(int32_t) * 160));
+    CUDA_CHECK(cudaMemset(p.offs, 0, sizeof(int32_t) * 160));
+  }
+  use(0);
   CUDA_CHECK(cudaMalloc(&buf, sizeof(float) * cap * d));
   CUDA_CHECK(cudaMalloc(&gown, sizeof(float) * cap * d));
 }
@@ -127,10 +130,13 @@ void Exchange::release() {
       if (peer_buf[w]) cudaIpcCloseMemHandle(peer_buf[w]);
     }
   if (bar) cudaFree(bar);
-  for (void* p : {static_cast<void*>(tm), static_cast<void*>(lpos), static_cast<void*>(sscan),
-                  static_cast<void*>(tile_cnt), static_cast<void*>(tile_off),
-                  static_cast<void*>(totals), static_cast<void*>(buf), static_cast<void*>(gown),
-                  static_cast<void*>(offs)})
+  for (const PlanSet& q : sets)
+    for (void* p : {static_cast<void*>(q.tm), static_cast<void*>(q.lpos),
+                    static_cast<void*>(q.sscan), static_cast<void*>(q.tile_cnt),
+                    static_cast<void*>(q.tile_off), static_cast<void*>(q.totals),
+                    static_cast<void*>(q.offs)})
+      if (p) cudaFree(p);
+  for (void* p : {static_cast<void*>(buf), static_cast<void*>(gown)})
     if (p) cudaFree(p);
   *this = Exchange();
 }

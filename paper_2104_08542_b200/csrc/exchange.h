@@ -49,6 +49,23 @@ struct Exchange {
   // [0, 64) roff_all, [64, 128) boff_all, [128, 137) recv_off, [137, 146) send_off
   int32_t* offs = nullptr;
   static constexpr int kOffRoff = 0, kOffBoff = 64, kOffRecv = 128, kOffSend = 137;
+  // The plan (tm .. offs) is written by the manager stage and read by the training stage:
+  // two sets (step parity), so the plan of step t+1 is built while step t trains.
+  struct PlanSet {
+    uint32_t *tm = nullptr, *lpos = nullptr, *tile_cnt = nullptr, *tile_off = nullptr;
+    Cnt8* sscan = nullptr;
+    int32_t *totals = nullptr, *offs = nullptr;
+  };
+  PlanSet sets[2];
+  void use(int set) {
+    tm = sets[set].tm;
+    lpos = sets[set].lpos;
+    sscan = sets[set].sscan;
+    tile_cnt = sets[set].tile_cnt;
+    tile_off = sets[set].tile_off;
+    totals = sets[set].totals;
+    offs = sets[set].offs;
+  }
 
   void init(int W, int me, int64_t cap, int d);
   void release();

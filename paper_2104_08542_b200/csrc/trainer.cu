@@ -65,6 +65,8 @@ void validate_config(const sfctr_config& c) {  // config.cpp:55-78 + device limi
           "global batch ids must fit 31 bits");
   require(c.sync_mode == SFCTR_SYNC_ALLREDUCE || c.sync_mode == SFCTR_SYNC_ALLTOALL,
           "sync must be allreduce or alltoall");
+  require(c.run_mode == SFCTR_MODE_SEQUENTIAL || c.run_mode == SFCTR_MODE_PIPELINED,
+          "mode must be pipelined or sequential");
 }
 
 Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nccl_id, int device)
@@ -91,22 +93,44 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
   }
   CUDA_CHECK(cudaSetDevice(device));
   CUDA_CHECK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  pipelined_ = cfg_.run_mode == SFCTR_MODE_PIPELINED;
+  mstream_ = stream_;
+  if (pipelined_) {  // the manager stage gets the higher priority: it gates the next step
+    int lo = 0, hi = 0;
+    CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CUDA_CHECK(cudaStreamCreateWithPriority(&mstream_, cudaStreamNonBlocking, hi));
+  }
   if (world_ > 1) {
     if (!nccl_id) fail(kConfig, "world > 1 needs an NCCL unique id");
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, sizeof(id));
     NCCL_CHECK(ncclCommInitRank(&comm_, world_, id, rank_));
+    // collectives of the two stages overlap, so they run on separate communicators
+    mcomm_ = comm_;
+    if (pipelined_) NCCL_CHECK(ncclCommSplit(comm_, 0, rank_, &mcomm_, nullptr));
   }
 
   vsi_.init(cfg_.vocabulary_size, n_global_);
-  CUDA_CHECK(cudaMalloc(&d_in_feat_, sizeof(uint64_t) * n_local_));
-  CUDA_CHECK(cudaMalloc(&d_in_lab_, static_cast<size_t>(lanes_) * b_));
-  if (cfg_.lookahead_depth > 1)
-    CUDA_CHECK(cudaMalloc(&d_in_win_, sizeof(uint64_t) * n_local_ * (cfg_.lookahead_depth - 1)));
+  if (lanes_ > 8) fail(kConfig, "at most 8 worker lanes per process");
+  for (int k = 0; k < 2; ++k) {  // per-step-parity sets (see trainer.h)
+    CUDA_CHECK(cudaMalloc(&d_in_feat_set_[k], sizeof(uint64_t) * n_local_));
+    CUDA_CHECK(cudaMalloc(&d_in_lab_set_[k], static_cast<size_t>(lanes_) * b_));
+    if (cfg_.lookahead_depth > 1)
+      CUDA_CHECK(cudaMalloc(&d_in_win_set_[k],
+                            sizeof(uint64_t) * n_local_ * (cfg_.lookahead_depth - 1)));
+    CUDA_CHECK(cudaMalloc(&d_uniq_set_[k], sizeof(uint32_t) * n_global_));
+    CUDA_CHECK(cudaMalloc(&d_vid_set_[k], sizeof(uint32_t) * n_global_));
+    CUDA_CHECK(cudaMalloc(&d_snap_[k], sizeof(int32_t) * (1 + kCntWords * lanes_)));
+    CUDA_CHECK(cudaMemset(d_snap_[k], 0, sizeof(int32_t) * (1 + kCntWords * lanes_)));
+    CUDA_CHECK(cudaMalloc(&d_loss_set_[k], sizeof(float)));
+    CUDA_CHECK(cudaEventCreateWithFlags(&prep_done_[k], cudaEventDisableTiming));
+    CUDA_CHECK(cudaEventCreateWithFlags(&train_done_[k], cudaEventDisableTiming));
+    CUDA_CHECK(cudaEventCreateWithFlags(&loss_ev_[k], cudaEventDisableTiming));
+  }
+  d_uniq_ = d_uniq_set_[0];
+  d_vid_ = d_vid_set_[0];
   CUDA_CHECK(cudaMalloc(&d_ids32_, sizeof(uint32_t) * n_local_));
   CUDA_CHECK(cudaMalloc(&d_gids_, sizeof(uint32_t) * n_global_));
-  CUDA_CHECK(cudaMalloc(&d_uniq_, sizeof(uint32_t) * n_global_));
-  CUDA_CHECK(cudaMalloc(&d_vid_, sizeof(uint32_t) * n_global_));
   CUDA_CHECK(cudaMalloc(&d_scalars_, sizeof(int32_t) * 8));
   CUDA_CHECK(cudaMemset(d_scalars_, 0, sizeof(int32_t) * 8));
   if (cfg_.lookahead_depth > 1) {
@@ -128,7 +152,7 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
   CUDA_CHECK(cudaMalloc(&d_dense_m_, sizeof(float) * P_));
   CUDA_CHECK(cudaMalloc(&d_dense_v_, sizeof(float) * P_));
   CUDA_CHECK(cudaMalloc(&d_grads_, sizeof(float) * (P_ + 1)));
-  CUDA_CHECK(cudaMalloc(&d_loss_, sizeof(float)));
+  d_loss_ = d_loss_set_[0];
   CUDA_CHECK(cudaMemset(d_dense_, 0, sizeof(float) * P_));
   CUDA_CHECK(cudaMemset(d_dense_m_, 0, sizeof(float) * P_));
   CUDA_CHECK(cudaMemset(d_dense_v_, 0, sizeof(float) * P_));
@@ -143,8 +167,9 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
       std::sqrt(6.0 / static_cast<double>(H_ + 1)));
   CUDA_LAUNCH_CHECK();
   CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_scalars_), sizeof(int32_t) * 8, 0));
-  CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_counts_), sizeof(int32_t) * 8 * lanes_, 0));
-  CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_loss_), sizeof(float), 0));
+  CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_counts_),
+                           sizeof(int32_t) * kCntWords * lanes_, 0));
+  CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_loss_ring_), sizeof(float) * 2, 0));
   CUDA_CHECK(cudaMalloc(&d_acc_, sizeof(int64_t) * 8));
   CUDA_CHECK(cudaMemset(d_acc_, 0, sizeof(int64_t) * 8));
   CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_acc_), sizeof(int64_t) * 8, 0));
@@ -187,6 +212,7 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
 
 Trainer::~Trainer() {
   cudaSetDevice(dev_);
+  if (mstream_) cudaStreamSynchronize(mstream_);
   if (stream_) cudaStreamSynchronize(stream_);
   for (auto& l : lane_) l.release();
   tower_.release();
@@ -195,26 +221,35 @@ Trainer::~Trainer() {
   if (d_lvid_) cudaFree(d_lvid_);
   if (h_totals_) cudaFreeHost(h_totals_);
   vsi_.release();
-  for (void* p : {static_cast<void*>(d_in_feat_), static_cast<void*>(d_in_lab_),
-                  static_cast<void*>(d_in_win_), static_cast<void*>(d_ids32_),
-                  static_cast<void*>(d_gids_), static_cast<void*>(d_uniq_),
-                  static_cast<void*>(d_vid_), static_cast<void*>(d_scalars_),
+  for (int k = 0; k < 2; ++k) {
+    for (void* p : {static_cast<void*>(d_in_feat_set_[k]), static_cast<void*>(d_in_lab_set_[k]),
+                    static_cast<void*>(d_in_win_set_[k]), static_cast<void*>(d_uniq_set_[k]),
+                    static_cast<void*>(d_vid_set_[k]), static_cast<void*>(d_snap_[k]),
+                    static_cast<void*>(d_loss_set_[k])})
+      if (p) cudaFree(p);
+    for (cudaEvent_t e : {prep_done_[k], train_done_[k], loss_ev_[k]})
+      if (e) cudaEventDestroy(e);
+  }
+  for (void* p : {static_cast<void*>(d_ids32_),
+                  static_cast<void*>(d_gids_), static_cast<void*>(d_scalars_),
                   static_cast<void*>(d_wuniq_), static_cast<void*>(d_wvid_),
                   static_cast<void*>(d_G_), static_cast<void*>(d_dG_), static_cast<void*>(d_X_),
                   static_cast<void*>(d_dX_), static_cast<void*>(d_fm_s_),
                   static_cast<void*>(d_fm_sqp_), static_cast<void*>(d_logits_),
                   static_cast<void*>(d_dense_), static_cast<void*>(d_dense_m_),
                   static_cast<void*>(d_dense_v_), static_cast<void*>(d_grads_),
-                  static_cast<void*>(d_loss_), static_cast<void*>(d_bc1_),
+                  static_cast<void*>(d_bc1_),
                   static_cast<void*>(d_bc2_), static_cast<void*>(d_acc_),
                   static_cast<void*>(d_B_)})
     if (p) cudaFree(p);
   if (h_acc_) cudaFreeHost(h_acc_);
   if (h_scalars_) cudaFreeHost(h_scalars_);
   if (h_counts_) cudaFreeHost(h_counts_);
-  if (h_loss_) cudaFreeHost(h_loss_);
+  if (h_loss_ring_) cudaFreeHost(h_loss_ring_);
   for (auto e : ev_) cudaEventDestroy(e);
+  if (mcomm_ && mcomm_ != comm_) ncclCommDestroy(mcomm_);
   if (comm_) ncclCommDestroy(comm_);
+  if (mstream_ && mstream_ != stream_) cudaStreamDestroy(mstream_);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -326,25 +361,32 @@ __global__ void zero_rows_kernel(float4* __restrict__ p, const int32_t* __restri
 
 }  // namespace
 
-void Trainer::phase(const char* name) {
+void Trainer::phase(const char* name, cudaStream_t s) {
   if (!timing_) return;
+  if (!s) s = stream_;
   cudaEvent_t e;
   CUDA_CHECK(cudaEventCreate(&e));
-  CUDA_CHECK(cudaEventRecord(e, stream_));
+  CUDA_CHECK(cudaEventRecord(e, s));
   ev_.push_back(e);
   ev_names_.emplace_back(name);
+  ev_streams_.push_back(s);
 }
 
 // Sums, per phase name, the device time between consecutive phase events of
 // every step recorded since the last call (events accumulate across steps so
-// a timed region needs no extra host synchronisation).
+// a timed region needs no extra host synchronisation). A phase spans from the
+// previous event on the SAME stream (manager and training stages are timed
+// separately in pipelined mode).
 void Trainer::finish_phases() {
   if (ev_.size() < 2) return;
-  CUDA_CHECK(cudaEventSynchronize(ev_.back()));
+  sync_all();
   for (size_t i = 1; i < ev_.size(); ++i) {
     if (ev_names_[i] == "start") continue;
+    size_t j = i;
+    while (j > 0 && ev_streams_[j - 1] != ev_streams_[i]) --j;
+    if (j == 0) continue;
     float ms = 0;
-    CUDA_CHECK(cudaEventElapsedTime(&ms, ev_[i - 1], ev_[i]));
+    CUDA_CHECK(cudaEventElapsedTime(&ms, ev_[j - 1], ev_[i]));
     auto it = std::find_if(phase_ms_.begin(), phase_ms_.end(),
                            [&](const auto& p) { return p.first == ev_names_[i]; });
     if (it == phase_ms_.end()) phase_ms_.emplace_back(ev_names_[i], ms);
@@ -353,7 +395,30 @@ void Trainer::finish_phases() {
   for (auto e : ev_) cudaEventDestroy(e);
   ev_.clear();
   ev_names_.clear();
+  ev_streams_.clear();
 }
+
+void Trainer::sync_all() {
+  CUDA_CHECK(cudaSetDevice(dev_));
+  if (mstream_ != stream_) CUDA_CHECK(cudaStreamSynchronize(mstream_));
+  CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+namespace {
+// U and every lane's counters as the manager stage left them: the training stage reads
+// this copy, so the next step's manager may reset and advance the live counters
+struct SnapArgs {
+  const int32_t* U;
+  const int32_t* cnt[8];
+  int lanes;
+  int32_t* out;
+};
+__global__ void snap_kernel(SnapArgs a) {
+  const int i = threadIdx.x;
+  if (i == 0) a.out[0] = *a.U;
+  if (i < kCntWords * a.lanes) a.out[1 + i] = a.cnt[i / kCntWords][i % kCntWords];
+}
+}  // namespace
 
 void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_t* d_labels,
                           const uint64_t* d_window, float* d_loss) {
@@ -361,11 +426,22 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   const int64_t launches0 = g_launches;
   const int32_t t = static_cast<int32_t>(step);
   const uint32_t Wu = static_cast<uint32_t>(W_);
-  cudaStream_t s = stream_;
+  // sm: manager stage (Data-Loader + Host-Manager of Fig. 4), sw: training stage
+  cudaStream_t sm = mstream_, sw = stream_;
   if (step < 0 || step >= (1ll << 23)) fail(kLogic, "step index out of the supported range");
   if (cfg_.lookahead_depth > 1 && !d_window)
     fail(kLogic, "lookahead > 1 needs the window batches");
-  phase("start");
+  const int k = static_cast<int>(step & 1);  // buffer set of this step
+  // the set's previous user (step t-2) must have finished training before it is refilled
+  if (pipelined_ && train_pending_[k]) CUDA_CHECK(cudaStreamWaitEvent(sm, train_done_[k]));
+  d_uniq_ = d_uniq_set_[k];
+  d_vid_ = d_vid_set_[k];
+  for (auto& L : lane_) L.use(k);
+  if (a2a_) xch_.use(k);
+  int32_t* snap = d_snap_[k];
+  auto snap_cnt = [&](int l) { return snap + 1 + kCntWords * l; };
+  phase("start", sm);
+  if (sm != sw) phase("start", sw);
   {  // per-step fields restart, running totals carry over
     sfctr_step_stats next{};
     next.total_steps = stats_.total_steps;
@@ -376,92 +452,98 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
     next.total_unique = stats_.total_unique;
     next.total_owned = stats_.total_owned;
     next.total_nvlink_bytes = stats_.total_nvlink_bytes;
+    next.total_pinned_waits = stats_.total_pinned_waits;
     stats_ = next;
   }
 
+  // ==== manager stage (stream sm) ====
   // ---- Data-Loader: ids to u32, all-gather the global batch, VSI (Algorithm 1 l.2-3)
   // [1] (bad-id flag) is sticky until a host check has seen it
-  CUDA_CHECK(cudaMemsetAsync(d_scalars_, 0, sizeof(int32_t), s));
-  CUDA_CHECK(cudaMemsetAsync(d_scalars_ + 2, 0, sizeof(int32_t) * 6, s));
-  ids_to_u32(d_features, d_ids32_, n_local_, cfg_.vocabulary_size, d_scalars_ + 1, s);
+  CUDA_CHECK(cudaMemsetAsync(d_scalars_, 0, sizeof(int32_t), sm));
+  CUDA_CHECK(cudaMemsetAsync(d_scalars_ + 2, 0, sizeof(int32_t) * 6, sm));
+  ids_to_u32(d_features, d_ids32_, n_local_, cfg_.vocabulary_size, d_scalars_ + 1, sm);
   const uint32_t* gids = d_ids32_;
   if (world_ > 1) {
-    NCCL_CHECK(ncclAllGather(d_ids32_, d_gids_, static_cast<size_t>(n_local_), ncclUint32, comm_, s));
+    NCCL_CHECK(ncclAllGather(d_ids32_, d_gids_, static_cast<size_t>(n_local_), ncclUint32, mcomm_, sm));
     gids = d_gids_;
     stats_.nvlink_bytes += n_local_ * 4;
   }
-  phase("ids_allgather");
-  vsi_device(vsi_, gids, n_global_, d_uniq_, d_vid_, d_scalars_ + 0, s, /*reset=*/false);
-  phase("vsi");
+  phase("ids_allgather", sm);
+  vsi_device(vsi_, gids, n_global_, d_uniq_, d_vid_, d_scalars_ + 0, sm, /*reset=*/false);
+  phase("vsi", sm);
   // ---- Host-Manager: MixCache per lane (Algorithm 1 l.4-7). The unique and
   // owned counts stay on the device (grids cover the batch-size bound), so the
   // step waits on the host only once, after the probe.
   const int32_t cap = static_cast<int32_t>(lane_[0].umax);
   for (int l = 0; l < lanes_; ++l) {
-    // per-step counters; kCntFromHost (index 2) stays cumulative
-    CUDA_CHECK(cudaMemsetAsync(lane_[l].counters, 0, sizeof(int32_t) * 2, s));
-    CUDA_CHECK(cudaMemsetAsync(lane_[l].counters + 3, 0, sizeof(int32_t) * 2, s));
+    // per-step counters; kCntFromHost (index 2), kCntFreeTop and kCntSeq carry over
+    CUDA_CHECK(cudaMemsetAsync(lane_[l].counters, 0, sizeof(int32_t) * 2, sm));
+    CUDA_CHECK(cudaMemsetAsync(lane_[l].counters + 3, 0, sizeof(int32_t) * 2, sm));
+    CUDA_CHECK(cudaMemsetAsync(lane_[l].counters + kCntOld, 0, sizeof(int32_t), sm));
     lane_[l].select_owned(d_uniq_, d_scalars_ + 0, cap, Wu, static_cast<uint32_t>(lane0_ + l),
-                          l == 0 ? vsi_.d_first : nullptr, s);
+                          l == 0 ? vsi_.d_first : nullptr, sm);
   }
   // window batches t+1..t+L-1 (needed_soon), one at a time through the window scratch
   const int nwin = cfg_.lookahead_depth - 1;
   for (int j = 0; j < nwin; ++j) {
     const uint64_t* wfeat = d_window + static_cast<size_t>(j) * n_local_;
-    ids_to_u32(wfeat, d_ids32_, n_local_, cfg_.vocabulary_size, d_scalars_ + 1, s);
+    ids_to_u32(wfeat, d_ids32_, n_local_, cfg_.vocabulary_size, d_scalars_ + 1, sm);
     const uint32_t* wg = d_ids32_;
     if (world_ > 1) {
-      NCCL_CHECK(ncclAllGather(d_ids32_, d_gids_, static_cast<size_t>(n_local_), ncclUint32, comm_, s));
+      NCCL_CHECK(ncclAllGather(d_ids32_, d_gids_, static_cast<size_t>(n_local_), ncclUint32, mcomm_, sm));
       wg = d_gids_;
     }
-    vsi_device(vsi_, wg, n_global_, d_wuniq_, d_wvid_, d_scalars_ + 2, s);
+    vsi_device(vsi_, wg, n_global_, d_wuniq_, d_wvid_, d_scalars_ + 2, sm);
     for (int l = 0; l < lanes_; ++l)
       lane_[l].mark_window(d_wuniq_, d_scalars_ + 2, cap, Wu, static_cast<uint32_t>(lane0_ + l), t,
-                           s);
+                           sm);
   }
-  for (int l = 0; l < lanes_; ++l) lane_[l].probe(d_uniq_, cap, Wu, t, s);
-  phase("manage_probe");
+  for (int l = 0; l < lanes_; ++l) lane_[l].probe(d_uniq_, cap, Wu, t, sm);
+  phase("manage_probe", sm);
   // Host wait: needed for evictions (the LRU victim count), the capacity check and the
   // NCCL / exchange sizes. A step whose admissions provably fit the free slots
   // (free_lb_ >= the per-step admission bound umax) skips it when nothing else needs host
   // counts: one process, or the owner-routed exchange over peer stores (its layout is
   // derived on the device). Every kernel below reads the unique / owned / working counts
-  // and the exchange plan from the device.
+  // and the exchange plan from the device. In pipelined mode the wait is on the manager
+  // stream only: the previous step keeps training meanwhile.
   const int64_t bound = lane_[0].umax;
   const bool xdev = a2a_ && xch_.device_driven();
   bool free_step = world_ == 1 || xdev;
   for (int l = 0; l < lanes_ && free_step; ++l) free_step = free_lb_[l] >= bound;
   if (a2a_) {  // exchange plan (touched masks, send/receive positions), device only
     xch_.plan(d_vid_, n_global_, static_cast<int64_t>(b_) * F_, d_uniq_, d_scalars_ + 0,
-              lane_[0].own_k, lane_[0].counters + kCntOwned, s);
+              lane_[0].own_k, lane_[0].counters + kCntOwned, sm);
     if (!free_step)
       CUDA_CHECK(cudaMemcpyAsync(h_totals_, xch_.totals, sizeof(int32_t) * Exchange::kTotals,
-                                 cudaMemcpyDeviceToHost, s));
-    phase("exchange_plan");
+                                 cudaMemcpyDeviceToHost, sm));
+    phase("exchange_plan", sm);
   }
   int32_t U = 0;
   std::vector<int32_t> n_own(lanes_, static_cast<int32_t>(bound)), n_work(lanes_, 0);
   if (!free_step) {
-    CUDA_CHECK(cudaMemcpyAsync(h_scalars_, d_scalars_, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaMemcpyAsync(h_scalars_, d_scalars_, sizeof(int32_t) * 2, cudaMemcpyDeviceToHost, sm));
     for (int l = 0; l < lanes_; ++l)
-      CUDA_CHECK(cudaMemcpyAsync(h_counts_ + 8 * l, lane_[l].counters, sizeof(int32_t) * 8,
-                                 cudaMemcpyDeviceToHost, s));
-    CUDA_CHECK(cudaStreamSynchronize(s));
+      CUDA_CHECK(cudaMemcpyAsync(h_counts_ + kCntWords * l, lane_[l].counters,
+                                 sizeof(int32_t) * kCntWords, cudaMemcpyDeviceToHost, sm));
+    CUDA_CHECK(cudaStreamSynchronize(sm));
     U = h_scalars_[0];
     if (h_scalars_[1]) fail(kLogic, "feature id >= vocabulary size in the batch", step);
     stats_.unique = U;
     for (int l = 0; l < lanes_; ++l) {
       CacheLane& L = lane_[l];
-      n_own[l] = h_counts_[8 * l + kCntOwned];
-      L.free_top = h_counts_[8 * l + kCntFreeTop];
-      std::memcpy(&L.next_seq, h_counts_ + 8 * l + kCntSeq, sizeof(uint64_t));
+      const int32_t* hc = h_counts_ + kCntWords * l;
+      n_own[l] = hc[kCntOwned];
+      L.free_top = hc[kCntFreeTop];
+      std::memcpy(&L.next_seq, hc + kCntSeq, sizeof(uint64_t));
     }
     // capacity check before any state moves (push_parameters_to_cache deadlock)
     for (int l = 0; l < lanes_; ++l) {
-      n_work[l] = n_own[l] > 0 ? h_counts_[8 * l + kCntWorking] : 0;
+      const int32_t* hc = h_counts_ + kCntWords * l;
+      n_work[l] = n_own[l] > 0 ? hc[kCntWorking] : 0;
       const CacheLane& L = lane_[l];
       const int64_t occupied = static_cast<int64_t>(L.C) - L.free_top;
-      const int64_t marked = h_counts_[8 * l + kCntMarked];
+      const int64_t marked = hc[kCntMarked];
       const int64_t evictable = occupied - marked;
       if (n_work[l] > L.free_top + evictable)
         fail(kRun,
@@ -472,11 +554,40 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
                  " pinned=0 needed_soon=" + std::to_string(marked) + ")",
              step);
     }
+    // Pipelined eviction safety (pinned => not evictable): step t-1 may
+    // still be training on its rows (last_use == t-1). The sequential-mode victims are the
+    // n_evict smallest (last_use, admit_seq) keys; when at least n_evict eligible slots
+    // are older than t-1 those victims are all among them and eviction overlaps step t-1.
+    // Otherwise the manager waits for step t-1 to finish first. Either way the victims,
+    // and so every result, equal sequential mode's.
+    bool keys_ready = false;
+    if (pipelined_ && train_pending_[k ^ 1]) {
+      bool any = false;
+      for (int l = 0; l < lanes_; ++l)
+        if (n_work[l] > lane_[l].free_top) {
+          lane_[l].victim_keys(t, /*count_old=*/true, sm);
+          CUDA_CHECK(cudaMemcpyAsync(h_counts_ + kCntWords * l + kCntOld,
+                                     lane_[l].counters + kCntOld, sizeof(int32_t),
+                                     cudaMemcpyDeviceToHost, sm));
+          any = true;
+        }
+      if (any) {
+        CUDA_CHECK(cudaStreamSynchronize(sm));
+        keys_ready = true;
+        bool wait = false;
+        for (int l = 0; l < lanes_; ++l)
+          wait |= n_work[l] - lane_[l].free_top > h_counts_[kCntWords * l + kCntOld];
+        if (wait) {
+          CUDA_CHECK(cudaStreamWaitEvent(sm, train_done_[k ^ 1]));
+          stats_.pinned_waits += 1;
+        }
+      }
+    }
     for (int l = 0; l < lanes_; ++l) {
       CacheLane& L = lane_[l];
       const int32_t n_evict = std::max<int32_t>(0, n_work[l] - L.free_top);
-      L.evict(n_evict, Wu, t, s);
-      L.admit(n_work[l], n_evict, Wu, cfg_.seed, t, s);
+      L.evict(n_evict, Wu, t, sm, keys_ready);
+      L.admit(n_work[l], n_evict, Wu, cfg_.seed, t, sm);
       free_lb_[l] = static_cast<int64_t>(L.free_top) + n_evict - n_work[l];
       led_[0] += static_cast<int64_t>(n_work[l]) * d_ * 12;
       led_[1] += static_cast<int64_t>(n_evict) * d_ * 12;
@@ -488,12 +599,27 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
     }
   } else {
     for (int l = 0; l < lanes_; ++l) {
-      lane_[l].admit(static_cast<int32_t>(bound), 0, Wu, cfg_.seed, t, s);
+      lane_[l].admit(static_cast<int32_t>(bound), 0, Wu, cfg_.seed, t, sm);
       free_lb_[l] -= bound;
     }
   }
-  phase("manage_evict_admit");
+  {
+    SnapArgs sa{};
+    sa.U = d_scalars_ + 0;
+    for (int l = 0; l < lanes_; ++l) sa.cnt[l] = lane_[l].counters;
+    sa.lanes = lanes_;
+    sa.out = snap;
+    snap_kernel<<<1, 1 + kCntWords * 8, 0, sm>>>(sa);
+    CUDA_LAUNCH_CHECK();
+  }
+  phase("manage_evict_admit", sm);
+  if (sm != sw) {  // hand the step to the training stage
+    CUDA_CHECK(cudaEventRecord(prep_done_[k], sm));
+    CUDA_CHECK(cudaStreamWaitEvent(sw, prep_done_[k]));
+  }
 
+  // ==== training stage (stream sw) ====
+  cudaStream_t s = sw;
   // ---- GPU-Worker forward (Algorithm 1 l.9-11)
   const size_t ud = static_cast<size_t>(U) * d_;
   // rows of the table the lanes gather from: all U uniques (all-reduce scheme) or
@@ -513,28 +639,28 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
         if (w != rank_) stats_.nvlink_bytes += (h_totals_[8 + w] + h_totals_[w]) * 4ll * d_;
     }
     if (xdev)
-      xch_.forward_dev(lane_[0].own_k, lane_[0].own_slot, n_own[0],
-                       lane_[0].counters + kCntOwned, lane_[0].emb, s);
+      xch_.forward_dev(lane_[0].own_k, lane_[0].own_slot, n_own[0], snap_cnt(0) + kCntOwned,
+                       lane_[0].emb, s);
     else
       xch_.forward(lane_[0].own_k, lane_[0].own_slot, n_own[0], lane_[0].emb, d_G_, comm_, s,
                    /*barrier=*/false);
-    phase("exchange_embed");
+    phase("exchange_embed", s);
     if (xch_.p2p) xch_.barrier(comm_, s);
-    phase("exchange_barrier");
+    phase("exchange_barrier", s);
     table_rows = free_step ? static_cast<size_t>(n_global_) : static_cast<size_t>(xch_.local_rows());
     xch_.local_vids(d_vid_ + static_cast<size_t>(lane0_) * b_ * F_, n_local_, d_lvid_, s);
   } else {
     if (world_ > 1) CUDA_CHECK(cudaMemsetAsync(d_G_, 0, sizeof(float) * ud, s));
     for (int l = 0; l < lanes_; ++l)
-      gather_cache(lane_[l].own_k, lane_[l].own_slot, n_own[l], lane_[l].counters + kCntOwned,
+      gather_cache(lane_[l].own_k, lane_[l].own_slot, n_own[l], snap_cnt(l) + kCntOwned,
                    lane_[l].emb, d_, d_G_, zero_in_gather ? d_dG_ : nullptr, s,
                    zero_in_gather ? d_B_ : nullptr);
-    phase("gather_cache");
+    phase("gather_cache", s);
     if (world_ > 1) {
       NCCL_CHECK(ncclAllReduce(d_G_, d_G_, ud, ncclFloat32, ncclSum, comm_, s));
       stats_.nvlink_bytes += static_cast<int64_t>(ud) * 4;
     }
-    phase("allreduce_embed");
+    phase("allreduce_embed", s);
   }
   // interworker ledger: the reference's accounting model, allreduce_bytes per
   // worker for each all-reduce, whatever the device scheme
@@ -546,7 +672,7 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   } else if (xdev) {
     xch_.zero_local_dev(d_dG_, s);
   } else if (free_step && d_ % 4 == 0)
-    zero_rows_kernel<<<148 * 8, 256, 0, s>>>(reinterpret_cast<float4*>(d_dG_), d_scalars_ + 0,
+    zero_rows_kernel<<<148 * 8, 256, 0, s>>>(reinterpret_cast<float4*>(d_dG_), snap + 0,
                                              d_ / 4, n_global_ * (d_ / 4));
   else
     CUDA_CHECK(cudaMemsetAsync(d_dG_, 0, sizeof(float) * table_rows * d_, s));
@@ -560,11 +686,11 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
                                    lab, b_, F_, d_, d_dense_,
                                    d_logits_ + static_cast<size_t>(l) * b_, d_fm_s_, emb_scale,
                                    d_dG_, d_grads_, l > 0, s);
-      phase("tower_fused");
+      phase("tower_fused", s);
       continue;
     }
     gather_instances(vid, b_, F_, d_, ldx_, d_G_, d_X_, d_fm_s_, d_fm_sqp_, s);
-    phase("gather_instances");
+    phase("gather_instances", s);
     const DxScatter sc{vid, d_fm_s_, tower_.gz, d_dG_, d_B_, F_, d_};
     if (tower_simt_)
       tower_forward_backward_simt(tower_, d_X_, d_fm_s_, d_fm_sqp_, lab, b_, F_, d_, d_dense_,
@@ -579,11 +705,12 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
                                            },
                                            this},
                                 fuse_scatter ? &sc : nullptr);
-    phase(tower_simt_ ? "tower" : "tower_reduce");
-    if (!fuse_scatter)
+    phase(tower_simt_ ? "tower" : "tower_reduce", s);
+    if (!fuse_scatter) {
       segment_sum(vid, b_ * F_, F_, d_, ldx_, d_dX_, d_G_, d_fm_s_, tower_.gz, emb_scale, d_dG_, s,
-                defer_fm ? d_B_ : nullptr);
-    phase("segment_sum");
+                  defer_fm ? d_B_ : nullptr);
+      phase("segment_sum", s);
+    }
   }
 
   // ---- grad_synchronize (l.13)
@@ -593,11 +720,11 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
       xch_.backward_send_dev(d_dG_, s);
     else
       xch_.backward_send(d_dG_, comm_, s);
-    phase("exchange_grad_send");
+    phase("exchange_grad_send", s);
     if (xch_.p2p) xch_.barrier(comm_, s);
-    phase("exchange_grad_barrier");
+    phase("exchange_grad_barrier", s);
     if (xdev)
-      xch_.backward_reduce_dev(lane_[0].own_k, n_own[0], lane_[0].counters + kCntOwned, d_dG_, s);
+      xch_.backward_reduce_dev(lane_[0].own_k, n_own[0], snap_cnt(0) + kCntOwned, d_dG_, s);
     else
       xch_.backward_reduce(lane_[0].own_k, n_own[0], d_dG_, s);
     grad_rows = xch_.gown;
@@ -612,19 +739,19 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   if (!free_step)
     led_[2] += static_cast<int64_t>(lanes_) *
                (arb(static_cast<int64_t>(ud) * 4) + arb(static_cast<int64_t>(P_) * 4));
-  phase(a2a_ ? "exchange_grad" : "allreduce_grad");
+  if (world_ > 1) phase(a2a_ ? "exchange_grad" : "allreduce_grad", s);
 
   // ---- update_sparse (l.14) + dense Adam
   ensure_bias_tables(steps_done_ + 2);
   for (int l = 0; l < lanes_; ++l)
     sparse_adam(a2a_ ? nullptr : lane_[l].own_k, lane_[l].own_slot, n_own[l],
-                lane_[l].counters + kCntOwned, grad_rows, d_,
+                snap_cnt(l) + kCntOwned, grad_rows, d_,
                 lane_[l].emb,
                 lane_[l].mom, lane_[l].vel, lane_[l].steps, d_bc1_, d_bc2_,
                 static_cast<float>(cfg_.learning_rate), static_cast<float>(cfg_.adam_beta1),
                 static_cast<float>(cfg_.adam_beta2), static_cast<float>(cfg_.adam_epsilon), s,
                 /*inc_steps=*/false, defer_fm ? d_B_ : nullptr, emb_scale);
-  phase("sparse_adam");
+  phase("sparse_adam", s);
   dense_steps_ += 1;
   const double bc1 = 1.0 - std::pow(cfg_.adam_beta1, static_cast<double>(dense_steps_));
   const double bc2 = 1.0 - std::pow(cfg_.adam_beta2, static_cast<double>(dense_steps_));
@@ -646,13 +773,13 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
     a.bc2 = static_cast<float>(bc2);
     a.loss_sum = d_grads_ + P_;
     a.inv_w = 1.f / static_cast<float>(W_);
-    a.loss_out = d_loss ? d_loss : d_loss_;
+    a.loss_out = d_loss ? d_loss : d_loss_set_[k];
     a.lanes = lanes_;
     for (int l = 0; l < lanes_; ++l) {
       a.own_slot[l] = lane_[l].own_slot;
-      a.n_own[l] = lane_[l].counters + kCntOwned;
+      a.n_own[l] = snap_cnt(l) + kCntOwned;
       a.steps[l] = lane_[l].steps;
-      a.cnt.c[l] = lane_[l].counters;
+      a.cnt.c[l] = snap_cnt(l);
     }
     if (!tower_fused_ && !tower_simt_) {
       a.w_hi = towertc_.w_hi;
@@ -667,7 +794,7 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
     a.acc = free_step ? d_acc_ : nullptr;
     a.xtotals = xdev ? xch_.totals : nullptr;
     a.me = rank_;
-    a.U = d_scalars_ + 0;
+    a.U = snap + 0;
     a.W = W_;
     a.d = d_;
     a.P = static_cast<int64_t>(P_);
@@ -675,7 +802,11 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
     CUDA_LAUNCH_CHECK();
     w1_split_ready_ = a.w_hi != nullptr;
   }
-  phase("dense_adam");
+  phase("dense_adam", s);
+  if (pipelined_) {
+    CUDA_CHECK(cudaEventRecord(train_done_[k], sw));
+    train_pending_[k] = true;
+  }
   if (free_step) {
     acc_pending_ = true;
     free_steps_ += 1;
@@ -692,6 +823,7 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   stats_.total_evicted += stats_.evicted;
   stats_.total_nvlink_bytes += stats_.nvlink_bytes;
   stats_.total_kernel_launches += stats_.kernel_launches;
+  stats_.total_pinned_waits += stats_.pinned_waits;
 }
 
 // Folds the deferred device counters in: capacity errors flagged by kernels
@@ -706,7 +838,7 @@ void Trainer::check_device_errors(int64_t step) {
   }
   int64_t cum = 0;
   for (int l = 0; l < lanes_; ++l) {
-    int32_t c[8];
+    int32_t c[kCntWords];
     CUDA_CHECK(cudaMemcpy(c, lane_[l].counters, sizeof(c), cudaMemcpyDeviceToHost));
     if (c[kCntError]) {
       const auto& L = lane_[l];
@@ -724,29 +856,56 @@ void Trainer::check_device_errors(int64_t step) {
   stats_.pcie_h2d_bytes = delta * (3 * d_ + 1) * 4;
 }
 
-double Trainer::step_host(int64_t step, const uint64_t* features, const uint8_t* labels,
+void Trainer::submit_host(int64_t step, const uint64_t* features, const uint8_t* labels,
                           const uint64_t* window) {
   CUDA_CHECK(cudaSetDevice(dev_));
-  CUDA_CHECK(cudaMemcpyAsync(d_in_feat_, features, sizeof(uint64_t) * n_local_,
-                             cudaMemcpyHostToDevice, stream_));
-  CUDA_CHECK(cudaMemcpyAsync(d_in_lab_, labels, static_cast<size_t>(lanes_) * b_,
-                             cudaMemcpyHostToDevice, stream_));
+  const int k = static_cast<int>(step & 1);
+  if (loss_step_[k] >= 0 && loss_step_[k] != step)
+    fail(kLogic, "read the loss of step " + std::to_string(loss_step_[k]) +
+                     " (loss_of) before submitting step " + std::to_string(step));
+  // the staging set was last read by step t-2: the manager stream waits for it below
+  // (step_device), so the copies go on the manager stream after that wait
+  cudaStream_t sm = mstream_;
+  if (pipelined_ && train_pending_[k]) CUDA_CHECK(cudaStreamWaitEvent(sm, train_done_[k]));
+  CUDA_CHECK(cudaMemcpyAsync(d_in_feat_set_[k], features, sizeof(uint64_t) * n_local_,
+                             cudaMemcpyHostToDevice, sm));
+  CUDA_CHECK(cudaMemcpyAsync(d_in_lab_set_[k], labels, static_cast<size_t>(lanes_) * b_,
+                             cudaMemcpyHostToDevice, sm));
   if (window && cfg_.lookahead_depth > 1)
-    CUDA_CHECK(cudaMemcpyAsync(d_in_win_, window,
+    CUDA_CHECK(cudaMemcpyAsync(d_in_win_set_[k], window,
                                sizeof(uint64_t) * n_local_ * (cfg_.lookahead_depth - 1),
-                               cudaMemcpyHostToDevice, stream_));
-  step_device(step, d_in_feat_, d_in_lab_, window ? d_in_win_ : nullptr, d_loss_);
-  CUDA_CHECK(cudaMemcpyAsync(h_loss_, d_loss_, sizeof(float), cudaMemcpyDeviceToHost, stream_));
-  CUDA_CHECK(cudaStreamSynchronize(stream_));
+                               cudaMemcpyHostToDevice, sm));
+  step_device(step, d_in_feat_set_[k], d_in_lab_set_[k], window ? d_in_win_set_[k] : nullptr,
+              d_loss_set_[k]);
+  CUDA_CHECK(cudaMemcpyAsync(h_loss_ring_ + k, d_loss_set_[k], sizeof(float),
+                             cudaMemcpyDeviceToHost, stream_));
+  CUDA_CHECK(cudaEventRecord(loss_ev_[k], stream_));
+  loss_step_[k] = step;
+}
+
+double Trainer::loss_of(int64_t step) {
+  CUDA_CHECK(cudaSetDevice(dev_));
+  const int k = static_cast<int>(step & 1);
+  if (loss_step_[k] != step)
+    fail(kLogic, "no outstanding step " + std::to_string(step) + " (submit it first)");
+  CUDA_CHECK(cudaEventSynchronize(loss_ev_[k]));
+  loss_step_[k] = -1;
   check_device_errors(step);
+  return static_cast<double>(h_loss_ring_[k]);
+}
+
+double Trainer::step_host(int64_t step, const uint64_t* features, const uint8_t* labels,
+                          const uint64_t* window) {
+  submit_host(step, features, labels, window);
+  const double l = loss_of(step);
   refresh();
   finish_phases();
-  return static_cast<double>(*h_loss_);
+  return l;
 }
 
 void Trainer::refresh() {
   CUDA_CHECK(cudaSetDevice(dev_));
-  CUDA_CHECK(cudaStreamSynchronize(stream_));
+  sync_all();
   if (acc_pending_) {
     CUDA_CHECK(cudaMemcpy(h_acc_, d_acc_, sizeof(int64_t) * 8, cudaMemcpyDeviceToHost));
     CUDA_CHECK(cudaMemset(d_acc_, 0, sizeof(int64_t) * 8));
@@ -759,7 +918,7 @@ void Trainer::refresh() {
     acc_pending_ = false;
   }
   for (int l = 0; l < lanes_; ++l) {
-    int32_t c[8];
+    int32_t c[kCntWords];
     CUDA_CHECK(cudaMemcpy(c, lane_[l].counters, sizeof(c), cudaMemcpyDeviceToHost));
     lane_[l].free_top = c[kCntFreeTop];
     std::memcpy(&lane_[l].next_seq, c + kCntSeq, sizeof(uint64_t));
@@ -790,19 +949,19 @@ uint64_t Trainer::free_count(int lane) {
 
 void Trainer::synchronize() {
   CUDA_CHECK(cudaSetDevice(dev_));
-  CUDA_CHECK(cudaStreamSynchronize(stream_));
+  sync_all();
   check_device_errors(steps_done_ - 1);
   refresh();
   finish_phases();
 }
 
 void Trainer::logits(float* out) {
-  CUDA_CHECK(cudaStreamSynchronize(stream_));
+  sync_all();
   CUDA_CHECK(cudaMemcpy(out, d_logits_, sizeof(float) * lanes_ * b_, cudaMemcpyDeviceToHost));
 }
 
 void Trainer::cache_slots(int lane, uint64_t* feature, int64_t* last_use, uint64_t* admit_seq) {
-  CUDA_CHECK(cudaStreamSynchronize(stream_));
+  sync_all();
   const CacheLane& L = lane_.at(lane);
   std::vector<uint32_t> f(L.C);
   std::vector<int32_t> lu(L.C);
@@ -817,7 +976,7 @@ void Trainer::cache_slots(int lane, uint64_t* feature, int64_t* last_use, uint64
 }
 
 int64_t Trainer::snapshot(uint64_t* features, float* rows, int64_t* steps) {
-  CUDA_CHECK(cudaStreamSynchronize(stream_));
+  sync_all();
   struct Src {
     int lane;
     uint32_t where;  // slot or kOnHost
@@ -872,7 +1031,7 @@ int64_t Trainer::snapshot(uint64_t* features, float* rows, int64_t* steps) {
 }
 
 void Trainer::get_dense(float* w1, float* b1, float* w2, float* b2) {
-  CUDA_CHECK(cudaStreamSynchronize(stream_));
+  sync_all();
   const size_t kh = static_cast<size_t>(K_) * H_;
   if (w1) CUDA_CHECK(cudaMemcpy(w1, d_dense_, sizeof(float) * kh, cudaMemcpyDeviceToHost));
   if (b1) CUDA_CHECK(cudaMemcpy(b1, d_dense_ + kh, sizeof(float) * H_, cudaMemcpyDeviceToHost));
@@ -881,7 +1040,7 @@ void Trainer::get_dense(float* w1, float* b1, float* w2, float* b2) {
 }
 
 void Trainer::set_dense(const float* w1, const float* b1, const float* w2, const float* b2) {
-  CUDA_CHECK(cudaStreamSynchronize(stream_));
+  sync_all();
   w1_split_ready_ = false;
   const size_t kh = static_cast<size_t>(K_) * H_;
   if (w1) CUDA_CHECK(cudaMemcpy(d_dense_, w1, sizeof(float) * kh, cudaMemcpyHostToDevice));

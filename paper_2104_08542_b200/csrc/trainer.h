@@ -26,6 +26,13 @@ class Trainer {
   // host-buffer variant: H2D copies, step, loss read back
   double step_host(int64_t step, const uint64_t* features, const uint8_t* labels,
                    const uint64_t* window);
+  // the same split in two: submit_host enqueues the H2D copies, the step and the D2H copy
+  // of its loss and returns; loss_of(step) waits for that loss. At most two submitted
+  // steps are outstanding (the loss of step t must be read before step t+2 is submitted).
+  void submit_host(int64_t step, const uint64_t* features, const uint8_t* labels,
+                   const uint64_t* window);
+  double loss_of(int64_t step);
+  bool pipelined() const { return pipelined_; }
   void synchronize();
   int64_t free_steps() const { return free_steps_; }
 
@@ -54,7 +61,8 @@ class Trainer {
 
  private:
   void ensure_bias_tables(int64_t t_max);
-  void phase(const char* name);
+  void phase(const char* name, cudaStream_t s = nullptr);
+  void sync_all();
   void finish_phases();
   void check_device_errors(int64_t step);
   // waits for the stream, folds the device-side totals of host-wait-free steps into the
@@ -66,17 +74,34 @@ class Trainer {
   int d_, F_, b_, H_, K_;
   int64_t n_local_, n_global_;  // ids per step: this process / whole global batch
   size_t P_;                    // dense parameter count
-  cudaStream_t stream_ = nullptr;
+  cudaStream_t stream_ = nullptr;   // training stage (GPU-Worker)
   ncclComm_t comm_ = nullptr;
+  // Pipelined mode (RunMode::kPipelined, config.hpp:30): the manager stage
+  // (ids, VSI, MixCache admission/eviction, exchange plan) of step t+1 runs on mstream_
+  // while step t trains on stream_. Buffers the training stage reads come in two sets
+  // (step parity); prep_done_/train_done_ order the stages. Sequential mode issues both
+  // stages on stream_.
+  bool pipelined_ = false;
+  cudaStream_t mstream_ = nullptr;
+  ncclComm_t mcomm_ = nullptr;       // manager-stage communicator (id all-gather)
+  cudaEvent_t prep_done_[2] = {}, train_done_[2] = {};
+  bool train_pending_[2] = {false, false};
+  int32_t* d_snap_[2] = {};          // [1 + kCntWords * lanes]: U, then every lane's counters
+  uint32_t* d_uniq_set_[2] = {};
+  uint32_t* d_vid_set_[2] = {};
+  uint64_t* d_in_feat_set_[2] = {};
+  uint8_t* d_in_lab_set_[2] = {};
+  uint64_t* d_in_win_set_[2] = {};
+  float* d_loss_set_[2] = {};
+  float* h_loss_ring_ = nullptr;     // pinned [2]
+  cudaEvent_t loss_ev_[2] = {};
+  int64_t loss_step_[2] = {-1, -1};
 
   VsiScratch vsi_;
-  uint64_t* d_in_feat_ = nullptr;   // staging for host inputs
-  uint8_t* d_in_lab_ = nullptr;
-  uint64_t* d_in_win_ = nullptr;
   uint32_t* d_ids32_ = nullptr;     // local ids, u32
   uint32_t* d_gids_ = nullptr;      // global batch ids (all-gathered)
-  uint32_t* d_uniq_ = nullptr;      // global_ids [U]
-  uint32_t* d_vid_ = nullptr;       // virtual ids [n_global]
+  uint32_t* d_uniq_ = nullptr;      // global_ids [U]        (current set, see d_uniq_set_)
+  uint32_t* d_vid_ = nullptr;       // virtual ids [n_global] (current set)
   int32_t* d_scalars_ = nullptr;    // [0]=U, [1]=bad id flag, [2..]=window U
   uint32_t* d_wuniq_ = nullptr;     // window batch uniques (one batch at a time)
   uint32_t* d_wvid_ = nullptr;
@@ -92,13 +117,12 @@ class Trainer {
   float* d_dense_m_ = nullptr;
   float* d_dense_v_ = nullptr;
   float* d_grads_ = nullptr;        // [P + 1] (+ loss sum)
-  float* d_loss_ = nullptr;
+  float* d_loss_ = nullptr;         // current set's loss (host-buffer steps)
   float* d_bc1_ = nullptr;          // sparse Adam bias-correction tables [t_cap + 1]
   float* d_bc2_ = nullptr;
   int64_t bc_cap_ = 0, bc_filled_ = 0;
   int32_t* h_scalars_ = nullptr;    // pinned mirrors
-  int32_t* h_counts_ = nullptr;     // [lanes * 8]
-  float* h_loss_ = nullptr;
+  int32_t* h_counts_ = nullptr;     // [lanes * kCntWords]
 
   std::vector<CacheLane> lane_;
   TowerBufs tower_;
@@ -130,6 +154,7 @@ class Trainer {
   bool timing_ = false;
   std::vector<cudaEvent_t> ev_;
   std::vector<std::string> ev_names_;
+  std::vector<cudaStream_t> ev_streams_;
   std::vector<std::pair<std::string, float>> phase_ms_;
 };
 

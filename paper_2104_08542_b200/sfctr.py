@@ -79,6 +79,7 @@ class Config(C.Structure):
         ("hidden_dim", C.c_int32),
         ("sync_mode", C.c_int32),
         ("host_table_rows", C.c_uint64),
+        ("run_mode", C.c_int32),
     ]
 
     def __init__(self, **kw):
@@ -108,7 +109,8 @@ class StepStats(C.Structure):
         "unique", "owned", "working", "evicted", "filled_from_host", "pcie_h2d_bytes",
         "pcie_d2h_bytes", "nvlink_bytes", "kernel_launches", "total_steps", "total_working",
         "total_evicted", "total_filled_from_host", "total_kernel_launches", "total_unique",
-        "total_owned", "total_nvlink_bytes", "total_free_steps")]
+        "total_owned", "total_nvlink_bytes", "total_free_steps", "pinned_waits",
+        "total_pinned_waits")]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -154,6 +156,8 @@ SIGNATURES = [
     ("sfctr_trainer_destroy", None, [P]),
     ("sfctr_trainer_step", C.c_int, [P, C.c_int64, P, P, P, C.POINTER(C.c_double)]),
     ("sfctr_trainer_step_device", C.c_int, [P, C.c_int64, P, P, P, P]),
+    ("sfctr_trainer_submit", C.c_int, [P, C.c_int64, P, P, P]),
+    ("sfctr_trainer_loss", C.c_int, [P, C.c_int64, C.POINTER(C.c_double)]),
     ("sfctr_trainer_synchronize", C.c_int, [P]),
     ("sfctr_trainer_stream", P, [P]),
     ("sfctr_trainer_logits", C.c_int, [P, f32p]),
@@ -357,6 +361,25 @@ class Trainer:
         loss = C.c_double(0)
         _check(lib().sfctr_trainer_step(self._h, step, _ptr(f), _ptr(y), _ptr(w), C.byref(loss)))
         return loss.value
+
+    def submit(self, step, features, labels, window=None):
+        """Enqueue one step on HOST buffers without waiting (read it back with loss()).
+        The arrays must stay alive and unchanged until loss(step) returns."""
+        f = np.ascontiguousarray(features, np.uint64)
+        y = np.ascontiguousarray(labels, np.uint8)
+        assert f.size == self.rows * self.fields and y.size == self.rows
+        w = None if window is None else np.ascontiguousarray(window, np.uint64)
+        self._keep = getattr(self, "_keep", {})
+        self._keep[step] = (f, y, w)
+        _check(lib().sfctr_trainer_submit(self._h, step, _ptr(f), _ptr(y), _ptr(w)))
+
+    def loss(self, step):
+        l = C.c_double(0)
+        try:
+            _check(lib().sfctr_trainer_loss(self._h, step, C.byref(l)))
+        finally:
+            getattr(self, "_keep", {}).pop(step, None)
+        return l.value
 
     def step_device(self, step, d_features, d_labels, d_window=None, d_loss=None):
         _check(lib().sfctr_trainer_step_device(self._h, step, d_features, d_labels, d_window,

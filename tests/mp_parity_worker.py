@@ -18,6 +18,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--sync", default="allreduce")
     ap.add_argument("--steps", type=int, default=6)
+    ap.add_argument("--mode", default="sequential")
     args = ap.parse_args()
     import torch
     import torch.distributed as td
@@ -32,15 +33,24 @@ def main():
                     vocabulary_size=200_000, cache_capacity=2500, hidden_dim=32,
                     zipf_exponent=1.05)
     cfg.apply("sync", args.sync)
+    cfg.apply("mode", args.mode)
     nid = dist.nccl_id_for(D, sb.nccl_unique_id)
     tr = sb.Trainer(cfg, rank=D.rank, world=W, nccl_id=nid, device=D.local_rank)
     gen = sb.SyntheticGenerator(cfg, device=D.local_rank)
     r0, n = dist.rows_of(D.rank, tr.lanes, cfg.batch_size_per_worker)
     F = cfg.num_fields
     losses = []
-    for t in range(args.steps):
-        f, y = gen.generate(t, r0, n)
-        losses.append(tr.step(t, f, y))
+    if args.mode == "pipelined":  # one step in flight: submit t, then read the loss of t-1
+        batches = [gen.generate(t, r0, n) for t in range(args.steps)]
+        for t in range(args.steps):
+            tr.submit(t, *batches[t])
+            if t > 0:
+                losses.append(tr.loss(t - 1))
+        losses.append(tr.loss(args.steps - 1))
+    else:
+        for t in range(args.steps):
+            f, y = gen.generate(t, r0, n)
+            losses.append(tr.step(t, f, y))
     feats, rows, steps = tr.snapshot()
     slots = tr.cache_slots(0)[0]
     led = tr.ledger()
@@ -101,7 +111,7 @@ def main():
         if led_d != led_o.tolist():
             print("ledger differs", led_d, led_o.tolist())
             ok = False
-        print(f"sync={args.sync} W={W} parity {'ok' if ok else 'FAILED'}; nvlink bytes/step "
+        print(f"sync={args.sync} mode={args.mode} W={W} parity {'ok' if ok else 'FAILED'}; nvlink bytes/step "
               f"{[g[7]['nvlink_bytes'] for g in gathered]}", flush=True)
     flag = torch.tensor([1 if ok else 0])
     td.broadcast(flag, 0)

@@ -25,12 +25,13 @@ def _port():
 
 
 @pytest.mark.skipif(sb.device_count() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("sync", ["allreduce", "alltoall"])
-def test_two_rank_parity(sync):
+@pytest.mark.parametrize("sync,mode", [("allreduce", "sequential"), ("alltoall", "sequential"),
+                                       ("allreduce", "pipelined"), ("alltoall", "pipelined")])
+def test_two_rank_parity(sync, mode):
     n = min(sb.device_count(), 4)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
-           os.path.join(ROOT, "tests", "mp_parity_worker.py"), "--sync", sync]
+           os.path.join(ROOT, "tests", "mp_parity_worker.py"), "--sync", sync, "--mode", mode]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     print(out.stdout[-3000:], out.stderr[-3000:])
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
