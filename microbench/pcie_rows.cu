@@ -114,6 +114,40 @@ __global__ void swap_warp(int n, const uint32_t* wrows, const uint32_t* rrows, c
   }
 }
 
+
+// TMA bulk stores: each warp stages a row (SoA -> AoS) in shared memory and lane 0 issues
+// one cp.async.bulk shared->global (host) of the whole 960 B row; 4 stages per warp
+constexpr int kStages = 4;
+__global__ void write_tma(int n, const uint32_t* rows, const uint32_t* slots, const float4* emb,
+                          const float4* mom, const float4* vel, float4* host) {
+  __shared__ __align__(128) float4 sm[8][kStages][3 * D4];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = gridDim.x * 8;
+  int it = 0;
+  for (int w = blockIdx.x * 8 + wib; w < n; w += nw, ++it) {
+    const int st = it % kStages;
+    if (it >= kStages) {  // the bulk store that used this stage must have read smem
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kStages - 1) : "memory");
+      __syncwarp();
+    }
+    const size_t r = rows[w], s = slots[w];
+    for (int c = lane; c < 3 * D4; c += 32) {
+      const int which = c / D4, cc = c - which * D4;
+      sm[wib][st][c] = (which == 0 ? emb : which == 1 ? mom : vel)[s * D4 + cc];
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(&sm[wib][st][0]));
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(host + r * 3 * D4),
+                   "r"(sa), "n"(3 * D4 * 16)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 int main(int argc, char** argv) {
   const int n = argc > 1 ? atoi(argv[1]) : 94000;
   const size_t host_rows = argc > 2 ? strtoull(argv[2], 0, 10) : 8000000;  // 7.7 GB
@@ -182,6 +216,11 @@ int main(int argc, char** argv) {
     timeit(nm, mb, [&] {
       write_flat<<<g, 256, 0, s1>>>(n, d_rows, d_slots, emb, mom, vel, host);
     });
+  }
+  for (int g : {148, 148 * 2, 148 * 4, 148 * 8}) {
+    char nm[64];
+    snprintf(nm, sizeof nm, "write_tma (grid %d)", g);
+    timeit(nm, mb, [&] { write_tma<<<g, 256, 0, s1>>>(n, d_rows, d_slots, emb, mom, vel, host); });
   }
   timeit("stage+CE D2H (contiguous)", mb, [&] {
     gather_stage<<<148 * 8, 256, 0, s1>>>(n, d_slots, emb, mom, vel, stage);

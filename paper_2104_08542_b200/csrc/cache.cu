@@ -284,6 +284,107 @@ __global__ void admit_kernel(const int32_t* __restrict__ counters, int32_t n_evi
   }
 }
 
+// Fused pull_parameters_to_host + push_parameters_to_cache for eviction steps: admission
+// i < n_evict lands in the slot of victim n_evict-1-i (the LIFO pop order of evict's pushes,
+// cache_buffer.cpp:41-42,64), so one warp writes that victim back to the pinned host table
+// and then fills its slot, and admissions i >= n_evict pop the free stack below the victims.
+// Every warp both stores to and loads from host memory, which keeps PCIe busy in both
+// directions at once (the write-back alone runs at ~44 GB/s of SM stores; see
+// microbench/pcie_rows.cu). The slot's victim state is staged in registers before the
+// admitted row overwrites it: 3*d/4 <= 64 float4 chunks per row (d <= 84).
+__global__ void __launch_bounds__(256) swap_kernel(
+    const int32_t* __restrict__ counters, int32_t n_evict,
+    const uint64_t* __restrict__ sorted_keys, const uint32_t* __restrict__ sorted_ids,
+    const uint32_t* __restrict__ work_j, const uint32_t* __restrict__ work_f,
+    const uint32_t* __restrict__ work_w, uint32_t W, int d4,
+    const uint32_t* __restrict__ free_stack, uint32_t* __restrict__ index,
+    float4* __restrict__ host_rows, int32_t* __restrict__ host_steps, uint64_t seed,
+    uint64_t embed_hash, float4* __restrict__ emb, float4* __restrict__ mom,
+    float4* __restrict__ vel, int32_t* __restrict__ steps, uint32_t* __restrict__ slot_feat,
+    int32_t* __restrict__ last_use, uint64_t* __restrict__ admit_seq,
+    int32_t* __restrict__ mark, int32_t t, uint32_t* __restrict__ own_slot,
+    int32_t* __restrict__ n_from_host, int32_t* __restrict__ err) {
+  const int32_t n_work = counters[kCntWorking];
+  const int32_t free_top = counters[kCntFreeTop];
+  const uint64_t seq0 = *reinterpret_cast<const uint64_t*>(counters + kCntSeq);
+  const int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= n_work) return;
+  const int per = 3 * d4;  // float4 chunks per row: emb | m | v
+  auto src_of = [&](int c, float4* e, float4* m, float4* v, size_t so) -> float4* {
+    const int which = c / d4;
+    return (which == 0 ? e : which == 1 ? m : v) + so + (c - which * d4);
+  };
+  uint32_t s;
+  float4 keep[2];
+  if (i < n_evict) {
+    const int64_t vi = n_evict - 1 - i;
+    if (sorted_keys[vi] == ~0ull) {  // fewer eligible slots than needed: capacity deadlock
+      if (lane == 0) *err = 1;
+      return;
+    }
+    s = sorted_ids[vi];
+    const uint32_t fo = slot_feat[s];
+    const uint64_t ro = fo / W;
+    const size_t so = static_cast<size_t>(s) * d4;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int c = lane + 32 * q;
+      if (c < per) keep[q] = *src_of(c, emb, mom, vel, so);
+    }
+    float4* dst = host_rows + ro * per;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int c = lane + 32 * q;
+      if (c < per) dst[c] = keep[q];
+    }
+    if (lane == 0) {
+      host_steps[ro] = steps[s];
+      index[ro] = kOnHost;
+    }
+  } else {
+    s = free_stack[free_top - 1 - (i - n_evict)];
+  }
+  const uint32_t f = work_f[i];
+  const uint32_t where = work_w[i];
+  const uint64_t r = f / W;
+  const size_t so = static_cast<size_t>(s) * d4;
+  if (where == kOnHost) {
+    const float4* src = host_rows + r * per;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int c = lane + 32 * q;
+      if (c < per) *src_of(c, emb, mom, vel, so) = src[c];
+    }
+  } else {
+    const uint64_t se = derive_seed_h(seed, embed_hash, f);  // HostStore::get_or_init
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int c = lane + 32 * q;
+      if (c >= per) continue;
+      float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (c < d4) {
+        auto init = [&](int col) {
+          return static_cast<float>(uniform_from(splitmix_mix(se + (col + 1) * kGolden), -0.01, 0.01));
+        };
+        x = make_float4(init(4 * c), init(4 * c + 1), init(4 * c + 2), init(4 * c + 3));
+      }
+      *src_of(c, emb, mom, vel, so) = x;
+    }
+  }
+  if (lane == 0) {
+    steps[s] = where == kOnHost ? host_steps[r] : 0;
+    slot_feat[s] = f;
+    last_use[s] = t;
+    admit_seq[s] = seq0 + static_cast<uint64_t>(i);
+    mark[s] = t;
+    index[r] = s;
+    own_slot[work_j[i]] = s;
+  }
+  const unsigned fh = __ballot_sync(0xFFFFFFFFu, lane == 0 && where == kOnHost);
+  if (lane == 0 && fh) atomicAdd(n_from_host, 1);
+}
+
 __global__ void init_lane_kernel(uint32_t C, uint32_t* slot_feat, int32_t* last_use,
                                  int32_t* mark, uint32_t* free_stack) {
   for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < C; s += gridDim.x * blockDim.x) {
@@ -449,6 +550,29 @@ void CacheLane::evict(int32_t n_evict, uint32_t W, int32_t t, cudaStream_t s, bo
   evict_kernel<<<ceil_div(static_cast<int64_t>(n_evict) * 32, 256), 256, 0, s>>>(
       n_evict, keys_sorted, ids_sorted, slot_feat, W, d, emb, mom, vel, steps, host_rows,
       host_steps, index, free_stack, counters + kCntFreeTop, counters + kCntError);
+  CUDA_LAUNCH_CHECK();
+}
+
+bool CacheLane::swap_supported() const { return (d & 3) == 0 && 3 * (d / 4) <= 64; }
+
+void CacheLane::evict_admit(int32_t n_evict, int32_t n_work, uint32_t W, uint64_t seed, int32_t t,
+                            cudaStream_t s, bool keys_ready) {
+  if (n_evict <= 0 || !swap_supported()) {
+    evict(n_evict, W, t, s, keys_ready);
+    admit(n_work, n_evict, W, seed, t, s);
+    return;
+  }
+  if (!keys_ready) victim_keys(t, false, s);
+  sort_pairs_u64_u32(temp, sort_bytes, keys, keys_sorted, ids, ids_sorted,
+                     static_cast<int64_t>(C), 64, s);
+  swap_kernel<<<ceil_div(static_cast<int64_t>(n_work) * 32, 256), 256, 0, s>>>(
+      counters, n_evict, keys_sorted, ids_sorted, work_j, work_f, work_w, W, d / 4, free_stack,
+      index, reinterpret_cast<float4*>(host_rows), host_steps, seed, fnv1a64("embed"),
+      reinterpret_cast<float4*>(emb), reinterpret_cast<float4*>(mom),
+      reinterpret_cast<float4*>(vel), steps, slot_feat, last_use, admit_seq, mark, t, own_slot,
+      counters + kCntFromHost, counters + kCntError);
+  CUDA_LAUNCH_CHECK();
+  advance_kernel<<<1, 1, 0, s>>>(counters, n_evict);
   CUDA_LAUNCH_CHECK();
 }
 

@@ -84,6 +84,11 @@ struct CacheLane {
   // stack, then advances the device free-stack height (+ n_evict - n_work) and admit_seq
   void admit(int32_t n_bound, int32_t n_evict, uint32_t W, uint64_t seed, int32_t t,
              cudaStream_t s);
+  // eviction step (host-known n_evict / n_work): write-back and admission fused per slot
+  // (swap_kernel) when the row fits the register staging, else evict() then admit()
+  void evict_admit(int32_t n_evict, int32_t n_work, uint32_t W, uint64_t seed, int32_t t,
+                   cudaStream_t s, bool keys_ready);
+  bool swap_supported() const;
 };
 
 }  // namespace sfb

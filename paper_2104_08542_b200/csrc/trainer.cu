@@ -586,8 +586,7 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
     for (int l = 0; l < lanes_; ++l) {
       CacheLane& L = lane_[l];
       const int32_t n_evict = std::max<int32_t>(0, n_work[l] - L.free_top);
-      L.evict(n_evict, Wu, t, sm, keys_ready);
-      L.admit(n_work[l], n_evict, Wu, cfg_.seed, t, sm);
+      L.evict_admit(n_evict, n_work[l], Wu, cfg_.seed, t, sm, keys_ready);
       free_lb_[l] = static_cast<int64_t>(L.free_top) + n_evict - n_work[l];
       led_[0] += static_cast<int64_t>(n_work[l]) * d_ * 12;
       led_[1] += static_cast<int64_t>(n_evict) * d_ * 12;
