@@ -132,12 +132,15 @@ class Clocks:
         return out
 
 
-def phase_bytes(name, U, Uw, n, b, d, F, H, Ntot):
-    """Algorithmic bytes (or FLOPs for the tower) per step for each phase."""
+def phase_bytes(name, U, Uw, n, b, d, F, H, Ntot, fused_scatter=False):
+    """Algorithmic bytes (or FLOPs for the tower) per step for each phase.
+    fused_scatter: the segment sum runs in the dX GEMM's epilogue (one worker)."""
     if name == "vsi":
         return 8 * Ntot + 12 * U, "B"
     if name == "gather_cache":  # + the fused zeroing of dG / the FM coefficients (W = 1)
         return 8 * Uw + 8 * d * Uw + (4 * d * U + 4 * U if Ntot == n else 0), "B"
+    if name == "zero_grads":  # one worker: dG[0:U) and the FM coefficients cleared
+        return 4 * d * U + 4 * U, "B"
     if name == "gather_instances":
         return 4 * n + 8 * d * n + 4 * b * d + b * d, "B"
     if name == "segment_sum":
@@ -146,7 +149,9 @@ def phase_bytes(name, U, Uw, n, b, d, F, H, Ntot):
         return 28 * d * Uw + 12 * Uw, "B"
     if name in ("tower_gemm1", "tower_gemm3"):  # X [b x F*d] streamed once (W1 / dh from L2)
         return 4 * b * F * d, "B"
-    if name == "tower_gemm2":  # dX [b x F*d] written once
+    if name == "tower_gemm2":  # dX [b x F*d] written once, or (fused) scattered into dG
+        if fused_scatter:
+            return 4 * n + 4 * d * n + 4 * d * U, "B"
         return 4 * b * F * d, "B"
     if name == "tower":  # SIMT validation tiles (SFCTR_TOWER_SIMT=1)
         return 6 * b * F * d * H, "FLOP"
@@ -275,7 +280,8 @@ def run_ours(args, D):
     d, H = args.dim, args.hidden
     kernels = {}
     for nm, ms in phase_ms.items():
-        amount, unit = phase_bytes(nm, U, Uw, n, args.batch, d, F, H, Ntot)
+        amount, unit = phase_bytes(nm, U, Uw, n, args.batch, d, F, H, Ntot,
+                                   fused_scatter="segment_sum" not in phase_ms)
         row = {"ms": round(ms, 4)}
         if amount is not None and ms > 0:
             if unit == "B":

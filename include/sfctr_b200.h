@@ -115,6 +115,31 @@ uint64_t sfctr_generator_shard_start(const sfctr_generator* g, int32_t field);
 int sfctr_initial_embedding(uint64_t seed, uint64_t feature, int32_t dim, int device, double* out);
 
 /* ---------------------------------------------------------------------
+ * Criteo ingest — CriteoReader (criteo.hpp:37-58, criteo.cpp:25-98)
+ * TSV "label \t 13 numerics \t 26 categorical tokens" parsed and hashed on the device
+ * (fnv1a64(token) % vocab, empty token -> 0), bit-exact with the reference. The whole
+ * file is parsed at open (streamed through pinned chunks); malformed lines are
+ * SFCTR_ERR_DATA with the reference's "path:line: ..." message; a missing file or
+ * fields != 26 is SFCTR_ERR_CONFIG. Batches of num_workers * batch_size_per_worker rows
+ * wrap around at the end of the file (read_batch, criteo.cpp:81-98).
+ * ------------------------------------------------------------------- */
+typedef struct sfctr_criteo sfctr_criteo;
+int sfctr_criteo_open(const char* path, const sfctr_config* cfg, int device, sfctr_criteo** out);
+/* the same over bytes already in memory; `name` replaces the path in messages */
+int sfctr_criteo_open_buffer(const char* data, size_t n, const char* name, const sfctr_config* cfg,
+                             int device, sfctr_criteo** out);
+void sfctr_criteo_destroy(sfctr_criteo* r);
+int64_t sfctr_criteo_row_count(const sfctr_criteo* r);           /* row_count() */
+uint64_t sfctr_criteo_token_hash(const char* token, size_t n);   /* token_hash() */
+/* rows [row0, row0+nrows) of batch `step`: features [nrows*26] u64, labels [nrows] */
+int sfctr_criteo_read_batch(sfctr_criteo* r, int64_t step, int32_t row0, int32_t nrows,
+                            uint64_t* features, uint8_t* labels);
+int sfctr_criteo_read_batch_device(sfctr_criteo* r, int64_t step, int32_t row0, int32_t nrows,
+                                   uint64_t* d_features, uint8_t* d_labels, void* stream);
+/* bytes and lines parsed; device span of the ingest, first chunk copy to last parse (ms) */
+int sfctr_criteo_stats(const sfctr_criteo* r, int64_t* bytes, int64_t* lines, double* parse_ms);
+
+/* ---------------------------------------------------------------------
  * Virtual Sparse Id — virtual_sparse_id(const RawBatch&, int) (vsi.hpp:29)
  * ------------------------------------------------------------------- */
 typedef struct sfctr_vsi sfctr_vsi;

@@ -160,11 +160,59 @@ class Trainer {
     check(sfctr_trainer_ledger(t_, out.data()));
     return out;
   }
+  // pipelined driving (one step in flight): submit, then loss of the previous step
+  void submit(std::int64_t step, const RawBatch& rows) {
+    auto& f = staged_[step & 1];
+    f.first.resize(rows.features.size());
+    for (std::size_t i = 0; i < f.first.size(); ++i) f.first[i] = rows.features[i].value;
+    f.second = rows.labels;
+    check(sfctr_trainer_submit(t_, step, f.first.data(), f.second.data(), nullptr));
+  }
+  double loss(std::int64_t step) {
+    double l = 0;
+    check(sfctr_trainer_loss(t_, step, &l));
+    return l;
+  }
   sfctr_trainer* handle() { return t_; }
 
  private:
   Config cfg_;
   sfctr_trainer* t_ = nullptr;
+  // host inputs of the (at most two) submitted steps, alive until their loss is read
+  std::pair<std::vector<std::uint64_t>, std::vector<std::uint8_t>> staged_[2];
+};
+
+// CriteoReader (criteo.hpp:37-58): the TSV is parsed and hashed on the device at
+// construction; read_batch(step) returns the wrapping global batch (criteo.cpp:81-98).
+class CriteoReader {
+ public:
+  static constexpr int kNumericColumns = 13;
+  static constexpr int kCategoricalColumns = 26;
+  CriteoReader(const std::string& path, const Config& cfg, int device = 0) : cfg_(cfg) {
+    check(sfctr_criteo_open(path.c_str(), &cfg_.c, device, &r_));
+  }
+  ~CriteoReader() { sfctr_criteo_destroy(r_); }
+  CriteoReader(const CriteoReader&) = delete;
+  CriteoReader& operator=(const CriteoReader&) = delete;
+  RawBatch read_batch(std::int64_t step) const {
+    RawBatch b;
+    b.rows = cfg_.c.num_workers * cfg_.c.batch_size_per_worker;
+    b.fields = kCategoricalColumns;
+    std::vector<std::uint64_t> f(static_cast<std::size_t>(b.rows) * b.fields);
+    b.labels.resize(b.rows);
+    check(sfctr_criteo_read_batch(r_, step, 0, b.rows, f.data(), b.labels.data()));
+    b.features.reserve(f.size());
+    for (auto v : f) b.features.emplace_back(v);
+    return b;
+  }
+  std::int64_t row_count() const { return sfctr_criteo_row_count(r_); }
+  static std::uint64_t token_hash(const std::string& token) {
+    return sfctr_criteo_token_hash(token.data(), token.size());
+  }
+
+ private:
+  Config cfg_;
+  sfctr_criteo* r_ = nullptr;
 };
 
 }  // namespace b200

@@ -21,6 +21,7 @@
 #include "sfctr/cache_buffer.hpp"
 #include "sfctr/comm.hpp"
 #include "sfctr/config.hpp"
+#include "sfctr/criteo.hpp"
 #include "sfctr/generator.hpp"
 #include "sfctr/host_store.hpp"
 #include "sfctr/rng.hpp"
@@ -220,6 +221,28 @@ int ref_config_check(const char* key, const char* value, int validate_after) {
     if (key) sfctr::apply_config_entry(c, key, value);
     if (validate_after) c.validate();
   });
+}
+
+// ---- CriteoReader (criteo.cpp) ----
+// Returns a reader or nullptr (status in *rc: 1 ConfigError, 2 DataError; ref_last_error()).
+void* ref_criteo_open(const char* path, int fields, std::uint64_t vocab, int workers, int batch,
+                      int* rc) {
+  sfctr::CriteoReader* r = nullptr;
+  *rc = guarded([&] {
+    r = new sfctr::CriteoReader(path, make_cfg(workers, 16, fields, batch, vocab, 7, 1.2));
+  });
+  return *rc == 0 ? r : nullptr;
+}
+void ref_criteo_destroy(void* r) { delete static_cast<sfctr::CriteoReader*>(r); }
+std::int64_t ref_criteo_rows(void* r) { return static_cast<sfctr::CriteoReader*>(r)->row_count(); }
+void ref_criteo_read_batch(void* r, std::int64_t step, std::uint64_t* features,
+                           std::uint8_t* labels) {
+  auto b = static_cast<sfctr::CriteoReader*>(r)->read_batch(step);
+  for (std::size_t i = 0; i < b.features.size(); ++i) features[i] = b.features[i].value;
+  std::memcpy(labels, b.labels.data(), b.labels.size());
+}
+std::uint64_t ref_criteo_token_hash(const char* token, std::size_t n) {
+  return sfctr::CriteoReader::token_hash(std::string(token, n));
 }
 
 }  // extern "C"

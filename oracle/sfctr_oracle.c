@@ -957,3 +957,54 @@ void orc_sim_ledger(const orc_sim* s, int64_t out[4]) {
 }
 
 int64_t orc_sim_last_unique(const orc_sim* s) { return s->last_u; }
+
+/* ======================= criteo.cpp:27-98 ======================= */
+int64_t orc_criteo_parse(const char* data, size_t n, uint64_t vocab, uint64_t* features,
+                         uint8_t* labels, int64_t cap_rows, int64_t* err_line, char* err_msg,
+                         size_t msg_cap) {
+  int64_t rows = 0, lineno = 0;
+  size_t pos = 0;
+  while (pos < n) { /* std::getline over '\n' (criteo.cpp:41-45) */
+    const char* nl = memchr(data + pos, '\n', n - pos);
+    size_t end = nl ? (size_t)(nl - data) : n;
+    const size_t next = nl ? end + 1 : n;
+    ++lineno;
+    if (end > pos && data[end - 1] == '\r') --end;
+    if (end == pos) { pos = next; continue; }
+    size_t tabs[40];
+    size_t ntab = 0;
+    for (size_t i = pos; i < end; ++i)
+      if (data[i] == '\t') { if (ntab < 40) tabs[ntab] = i; ++ntab; }
+    if (ntab != 39) { /* criteo.cpp:59-63 */
+      *err_line = lineno;
+      snprintf(err_msg, msg_cap, "expected 40 tab-separated columns, got %zu", ntab + 1);
+      return -1;
+    }
+    if (!(tabs[0] == pos + 1 && (data[pos] == '0' || data[pos] == '1'))) { /* :64-68 */
+      *err_line = lineno;
+      snprintf(err_msg, msg_cap, "label must be 0 or 1, got '%.*s'", (int)(tabs[0] - pos),
+               data + pos);
+      return -1;
+    }
+    if (rows >= cap_rows) return -3;
+    labels[rows] = data[pos] == '1' ? 1 : 0;
+    for (int f = 0; f < 26; ++f) { /* :69-76 */
+      const size_t a = tabs[13 + f] + 1, b = f == 25 ? end : tabs[14 + f];
+      features[rows * 26 + f] = b > a ? orc_fnv1a64(data + a, b - a) % vocab : 0;
+    }
+    ++rows;
+    pos = next;
+  }
+  if (rows == 0) return -2; /* :78 */
+  return rows;
+}
+
+void orc_criteo_read_batch(const uint64_t* features, const uint8_t* labels, int64_t rows,
+                           int64_t step, int global_rows, uint64_t* out_f, uint8_t* out_l) {
+  int64_t src = (step * global_rows) % rows; /* criteo.cpp:88-96 */
+  for (int r = 0; r < global_rows; ++r) {
+    out_l[r] = labels[src];
+    for (int f = 0; f < 26; ++f) out_f[(size_t)r * 26 + f] = features[src * 26 + f];
+    src = (src + 1) % rows;
+  }
+}

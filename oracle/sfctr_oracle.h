@@ -36,6 +36,19 @@ double orc_truth_weight(uint64_t seed, uint64_t feature);
 void orc_initial_embedding(uint64_t seed, uint64_t feature, int dim, double* out);
 int64_t orc_allreduce_bytes(int64_t payload, int workers);
 
+/* ---- criteo.cpp:27-98 (CriteoReader) ----
+ * Parses a whole TSV held in memory: rows = data lines (empty / "\r"-only lines
+ * skipped), features [rows*26] = fnv1a64(token) % vocab (0 for an empty token),
+ * labels [rows]. Returns rows (>= 0), or -1 with *err_line (1-based, counting every
+ * line) and err_msg (the reference's text after "path:line: ") for the first malformed
+ * line, or -2 when there is no data row. Capacity: cap_rows rows. */
+int64_t orc_criteo_parse(const char* data, size_t n, uint64_t vocab, uint64_t* features,
+                         uint8_t* labels, int64_t cap_rows, int64_t* err_line, char* err_msg,
+                         size_t msg_cap);
+/* read_batch(step): global_rows rows starting at (step*global_rows) % rows, wrapping */
+void orc_criteo_read_batch(const uint64_t* features, const uint8_t* labels, int64_t rows,
+                           int64_t step, int global_rows, uint64_t* out_f, uint8_t* out_l);
+
 /* ---- generator.cpp:32-108 ---- */
 typedef struct orc_gen orc_gen;
 orc_gen* orc_gen_create(int global_rows, int fields, uint64_t vocab, uint64_t seed, double zipf);

@@ -437,16 +437,24 @@ void CacheLane::init(uint64_t capacity, int dim, uint64_t owned_rows, uint64_t h
   CUDA_LAUNCH_CHECK();
   fill_u32<<<1184, 256>>>(index, rows, kNever);
   CUDA_LAUNCH_CHECK();
-  // pinned, mapped host table: [emb | m | v] per owned row + adam step counts
-  const size_t hbytes = sizeof(float) * static_cast<size_t>(host_cap) * 3 * d;
-  if (cudaHostAlloc(reinterpret_cast<void**>(&host_rows), hbytes,
-                    cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
-    cudaGetLastError();
-    fail(kConfig, "cannot pin " + std::to_string(hbytes >> 20) +
-                      " MiB for the host table (set host_rows / vocab smaller)");
+  // pinned, mapped host table: [emb | m | v] per owned row + adam step counts. A cache that
+  // holds the whole owned shard never evicts, so no row ever lives on the host: no table.
+  if (C >= rows) host_cap = 0;
+  if (host_cap == 0) {
+    free_top = static_cast<int32_t>(C);
+    next_seq = 0;
   }
-  CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&host_steps), sizeof(int32_t) * host_cap,
-                           cudaHostAllocMapped | cudaHostAllocPortable));
+  const size_t hbytes = sizeof(float) * static_cast<size_t>(host_cap) * 3 * d;
+  if (host_cap > 0) {
+    if (cudaHostAlloc(reinterpret_cast<void**>(&host_rows), hbytes,
+                      cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+      cudaGetLastError();
+      fail(kConfig, "cannot pin " + std::to_string(hbytes >> 20) +
+                        " MiB for the host table (set host_rows / vocab smaller)");
+    }
+    CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&host_steps), sizeof(int32_t) * host_cap,
+                             cudaHostAllocMapped | cudaHostAllocPortable));
+  }
   free_top = static_cast<int32_t>(C);
   next_seq = 0;
   // per-step scratch

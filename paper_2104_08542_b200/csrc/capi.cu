@@ -2,11 +2,13 @@
 // engine's sfb::Error and maps it to a status code + thread-local message,
 // mirroring the reference's exception classes (error.hpp:28-56).
 #include <cstring>
+#include <functional>
 #include <fstream>
 #include <memory>
 #include <sstream>
 #include <string>
 
+#include "criteo.h"
 #include "trainer.h"
 
 namespace {
@@ -122,6 +124,16 @@ struct sfctr_generator {
   int64_t cap = 0;
 };
 
+struct sfctr_criteo {
+  int device;
+  int32_t global_rows;
+  sfb::CriteoTable table;
+  ~sfctr_criteo() {
+    cudaSetDevice(device);
+    table.release();
+  }
+};
+
 struct sfctr_vsi {
   int device;
   sfb::VsiScratch scratch;
@@ -222,6 +234,116 @@ int sfctr_device_count(int* count) {
   }
   *count = n;
   return sfb::kOk;
+}
+
+// ---------------- Criteo ingest (CriteoReader, criteo.hpp:37-58) ----------------
+namespace {
+struct MemBuf : std::streambuf {  // read-only istream over caller memory
+  MemBuf(const char* p, size_t n) {
+    char* b = const_cast<char*>(p ? p : "");
+    setg(b, b, b + n);
+  }
+  pos_type seekoff(off_type off, std::ios_base::seekdir dir, std::ios_base::openmode) override {
+    char* target = dir == std::ios_base::beg ? eback() + off
+                   : dir == std::ios_base::cur ? gptr() + off
+                                               : egptr() + off;
+    if (target < eback() || target > egptr()) return pos_type(off_type(-1));
+    setg(eback(), target, egptr());
+    return pos_type(target - eback());
+  }
+  pos_type seekpos(pos_type pos, std::ios_base::openmode m) override {
+    return seekoff(off_type(pos), std::ios_base::beg, m);
+  }
+};
+
+void criteo_common(const sfctr_config* cfg, int device, int64_t bytes, sfctr_criteo** out,
+                   const std::function<void(sfb::CriteoTable&)>& fill) {
+  if (!cfg || !out) sfb::fail(sfb::kLogic, "null argument");
+  DeviceScope ds(device);
+  auto r = std::make_unique<sfctr_criteo>();
+  r->device = device;
+  r->global_rows = cfg->num_workers * cfg->batch_size_per_worker;
+  if (r->global_rows <= 0) sfb::fail(sfb::kConfig, "bad batch shape");
+  size_t chunk = std::min<size_t>(64ull << 20, std::max<int64_t>(bytes + 64, 1 << 16));
+  if (const char* e = std::getenv("SFCTR_CRITEO_CHUNK"))  // tests: force multi-chunk streaming
+    chunk = std::max<size_t>(std::strtoull(e, nullptr, 10), 4096);
+  r->table.init(cfg->vocabulary_size, cfg->num_fields, bytes, chunk);
+  fill(r->table);
+  *out = r.release();
+}
+}  // namespace
+
+int sfctr_criteo_open(const char* path, const sfctr_config* cfg, int device, sfctr_criteo** out) {
+  return guarded([&] {
+    if (!path) sfb::fail(sfb::kLogic, "null path");
+    if (cfg && cfg->num_fields != 26)  // criteo.cpp:31-34 (before the file is touched)
+      sfb::fail(sfb::kConfig, "criteo format has 26 categorical fields; fields=" +
+                                  std::to_string(cfg->num_fields) + " was configured");
+    std::ifstream in(path, std::ios::binary);
+    if (!in) sfb::fail(sfb::kConfig, std::string("cannot open criteo file: ") + path);
+    in.seekg(0, std::ios::end);
+    const int64_t bytes = static_cast<int64_t>(in.tellg());
+    in.seekg(0);
+    criteo_common(cfg, device, bytes, out, [&](sfb::CriteoTable& t) { t.ingest(in, path); });
+  });
+}
+
+int sfctr_criteo_open_buffer(const char* data, size_t n, const char* name, const sfctr_config* cfg,
+                             int device, sfctr_criteo** out) {
+  return guarded([&] {
+    if (!data && n) sfb::fail(sfb::kLogic, "null data");
+    MemBuf mb(data, n);  // the caller's bytes, read in place (no copy into a string)
+    std::istream in(&mb);
+    criteo_common(cfg, device, static_cast<int64_t>(n), out,
+                  [&](sfb::CriteoTable& t) { t.ingest(in, name ? name : "<buffer>"); });
+  });
+}
+
+void sfctr_criteo_destroy(sfctr_criteo* r) { delete r; }
+
+int64_t sfctr_criteo_row_count(const sfctr_criteo* r) { return r ? r->table.rows : -1; }
+
+uint64_t sfctr_criteo_token_hash(const char* token, size_t n) { return sfb::fnv1a64(token, n); }
+
+int sfctr_criteo_read_batch_device(sfctr_criteo* r, int64_t step, int32_t row0, int32_t nrows,
+                                   uint64_t* d_features, uint8_t* d_labels, void* stream) {
+  return guarded([&] {
+    DeviceScope ds(r->device);
+    r->table.read_batch(step, r->global_rows, row0, nrows, d_features, d_labels,
+                        static_cast<cudaStream_t>(stream));
+  });
+}
+
+int sfctr_criteo_read_batch(sfctr_criteo* r, int64_t step, int32_t row0, int32_t nrows,
+                            uint64_t* features, uint8_t* labels) {
+  return guarded([&] {
+    DeviceScope ds(r->device);
+    uint64_t* df = nullptr;
+    uint8_t* dl = nullptr;
+    CUDA_CHECK(cudaMalloc(&df, sizeof(uint64_t) * 26 * std::max(nrows, 1)));
+    CUDA_CHECK(cudaMalloc(&dl, std::max(nrows, 1)));
+    try {
+      r->table.read_batch(step, r->global_rows, row0, nrows, df, dl, r->table.stream);
+      CUDA_CHECK(cudaMemcpyAsync(features, df, sizeof(uint64_t) * 26 * nrows,
+                                 cudaMemcpyDeviceToHost, r->table.stream));
+      CUDA_CHECK(cudaMemcpyAsync(labels, dl, nrows, cudaMemcpyDeviceToHost, r->table.stream));
+      CUDA_CHECK(cudaStreamSynchronize(r->table.stream));
+    } catch (...) {
+      cudaFree(df);
+      cudaFree(dl);
+      throw;
+    }
+    cudaFree(df);
+    cudaFree(dl);
+  });
+}
+
+int sfctr_criteo_stats(const sfctr_criteo* r, int64_t* bytes, int64_t* lines, double* parse_ms) {
+  return guarded([&] {
+    if (bytes) *bytes = r->table.bytes;
+    if (lines) *lines = r->table.lines;
+    if (parse_ms) *parse_ms = r->table.parse_ms;
+  });
 }
 
 // ---------------- generator ----------------

@@ -31,6 +31,17 @@ __global__ void gather_cache_v4(const uint32_t* __restrict__ own_k,
   }
 }
 
+// one worker without a materialised G: only dG[0:U) and B[0:U) need clearing
+__global__ void zero_rows_b_kernel(const int32_t* __restrict__ n_ptr, int d4,
+                                   float4* __restrict__ dG, float* __restrict__ B) {
+  const int64_t n = static_cast<int64_t>(*n_ptr) * d4;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    dG[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i % d4 == 0) B[i / d4] = 0.f;
+  }
+}
+
 __global__ void gather_cache_s(const uint32_t* __restrict__ own_k,
                                const uint32_t* __restrict__ own_slot, const int32_t* __restrict__ n_ptr, int32_t n_bound, int d,
                                const float* __restrict__ emb, float* __restrict__ G) {
@@ -47,9 +58,12 @@ __global__ void gather_cache_s(const uint32_t* __restrict__ own_k,
 // Thread per (row, 16 B column chunk); loops over the F fields of the row.
 // Writes X (streaming store: it is consumed once by the tower) and the FM
 // partial sums.
+// slot_of != nullptr (one worker): G is not materialised; unique k's row is read from the
+// cache slot slot_of[k] (= own_slot, an L2-resident table) instead.
 __global__ void gather_instances_v4(const uint32_t* __restrict__ vid, int32_t rows, int F, int d4,
                                     const float4* __restrict__ G, float4* __restrict__ X,
-                                    float4* __restrict__ fm_s, float* __restrict__ fm_sqp) {
+                                    float4* __restrict__ fm_s, float* __restrict__ fm_sqp,
+                                    const uint32_t* __restrict__ slot_of) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= static_cast<int64_t>(rows) * d4) return;
   const int64_t r = i / d4;
@@ -63,6 +77,10 @@ __global__ void gather_instances_v4(const uint32_t* __restrict__ vid, int32_t ro
     uint32_t v[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) v[u] = __ldg(vr + f + u);
+    if (slot_of) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldg(slot_of + v[u]);
+    }
     float4 a[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) a[u] = __ldg(G + static_cast<int64_t>(v[u]) * d4 + c);
@@ -74,7 +92,9 @@ __global__ void gather_instances_v4(const uint32_t* __restrict__ vid, int32_t ro
     }
   }
   for (; f < F; ++f) {
-    const float4 a = __ldg(G + static_cast<int64_t>(__ldg(vr + f)) * d4 + c);
+    uint32_t v = __ldg(vr + f);
+    if (slot_of) v = __ldg(slot_of + v);
+    const float4 a = __ldg(G + static_cast<int64_t>(v) * d4 + c);
     xr[f * d4] = a;
     s.x += a.x; s.y += a.y; s.z += a.z; s.w += a.w;
     sq += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w;
@@ -285,14 +305,24 @@ void gather_cache(const uint32_t* own_k, const uint32_t* own_slot, int32_t n_own
   CUDA_LAUNCH_CHECK();
 }
 
+void zero_rows_b(const int32_t* d_n, int32_t n_bound, int d, float* dG, float* B, cudaStream_t s) {
+  SFB_CHECK((d & 3) == 0, "zero_rows_b needs d % 4 == 0");
+  if (n_bound <= 0) return;
+  zero_rows_b_kernel<<<wave_grid(static_cast<int64_t>(n_bound) * (d / 4)), 256, 0, s>>>(
+      d_n, d / 4, reinterpret_cast<float4*>(dG), B);
+  CUDA_LAUNCH_CHECK();
+}
+
 void gather_instances(const uint32_t* vid, int32_t rows, int F, int d, int ldx, const float* G,
-                      float* X, float* fm_s, float* fm_sqp, cudaStream_t s) {
+                      float* X, float* fm_s, float* fm_sqp, cudaStream_t s,
+                      const uint32_t* slot_of) {
   if (rows <= 0) return;
+  SFB_CHECK(!slot_of || (d & 3) == 0, "gather_instances: slot indirection needs d % 4 == 0");
   if ((d & 3) == 0) {
     const int64_t n = static_cast<int64_t>(rows) * (d / 4);
     gather_instances_v4<<<ceil_div(n, 256), 256, 0, s>>>(
         vid, rows, F, d / 4, reinterpret_cast<const float4*>(G), reinterpret_cast<float4*>(X),
-        reinterpret_cast<float4*>(fm_s), fm_sqp);
+        reinterpret_cast<float4*>(fm_s), fm_sqp, slot_of);
   } else {
     const int64_t n = static_cast<int64_t>(rows) * d;
     gather_instances_s<<<ceil_div(n, 256), 256, 0, s>>>(vid, rows, F, d, ldx, G, X, fm_s, fm_sqp);

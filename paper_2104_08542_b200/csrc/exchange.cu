@@ -28,7 +28,9 @@ __global__ void touch_mask_kernel(const uint32_t* __restrict__ vid, int64_t n, i
   const uint32_t bit = 1u << static_cast<uint32_t>(i / per_worker);
   const unsigned peers = __match_any_sync(active, v);
   const uint32_t bits = __reduce_or_sync(peers, bit);
-  if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicOr(tm + v, bits);
+  // hot ids: most warps find their bits already set — skip the contended atomic then
+  if ((threadIdx.x & 31) == __ffs(peers) - 1 && (__ldcg(tm + v) & bits) != bits)
+    atomicOr(tm + v, bits);
 }
 
 __global__ void lvid_kernel(const uint32_t* __restrict__ vid, int64_t n,
@@ -467,89 +469,160 @@ __global__ void offsets_kernel(const int32_t* __restrict__ totals, int me, int32
   }
 }
 
-// forward over NVLink, offsets from the device plan (see push_rows_p2p_kernel)
-__global__ void push_rows_p2p_dev_kernel(const uint32_t* __restrict__ own_k,
-                                         const uint32_t* __restrict__ own_slot,
-                                         const int32_t* __restrict__ n_ptr,
-                                         const uint32_t* __restrict__ tm,
-                                         const Cnt8* __restrict__ sscan, uint32_t W, uint32_t me,
-                                         const int32_t* __restrict__ offs,
-                                         const float4* __restrict__ emb, int d4, PeerRows pr) {
-  const int lane = threadIdx.x & 31;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  const int32_t n_own = *n_ptr;
+// forward over NVLink, offsets from the device plan (see push_rows_p2p_kernel). Flat
+// (owned row, 16 B chunk) items, two per thread per round with independent load chains,
+// so many rows' index loads and row reads are in flight at once; each chunk is stored to
+// every rank that touches the row (my own E included).
+__global__ void __launch_bounds__(256) push_rows_p2p_dev_kernel(
+    const uint32_t* __restrict__ own_k, const uint32_t* __restrict__ own_slot,
+    const int32_t* __restrict__ n_ptr, const uint32_t* __restrict__ tm,
+    const Cnt8* __restrict__ sscan, uint32_t W, uint32_t me, const int32_t* __restrict__ offs,
+    const float4* __restrict__ emb, int d4, PeerRows pr) {
+  const int64_t n = static_cast<int64_t>(*n_ptr) * d4;
   uint32_t e_off[8];
 #pragma unroll
-  for (int w = 0; w < 8; ++w) e_off[w] = w < static_cast<int>(W) ? offs[Exchange::kOffRoff + w * 8 + me] : 0u;
-  for (int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < n_own; j += nwarps) {
-    const uint32_t m = tm[own_k[j]];
-    const float4* src = emb + static_cast<int64_t>(own_slot[j]) * d4;
+  for (int w = 0; w < 8; ++w)
+    e_off[w] = w < static_cast<int>(W) ? offs[Exchange::kOffRoff + w * 8 + me] : 0u;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i0 < n;
+       i0 += 2 * stride) {
+    int64_t j[2];
+    int c[2];
+    bool ok[2];
+    uint32_t m[2];
+    float4 v[2];
 #pragma unroll
-    for (uint32_t w = 0; w < 8; ++w) {
-      if (w >= W || !((m >> w) & 1u)) continue;
-      float4* dst = pr.E[w] + static_cast<int64_t>(e_off[w] + sscan[j].c[w]) * d4;
-      for (int c = lane; c < d4; c += 32) dst[c] = src[c];
+    for (int u = 0; u < 2; ++u) {
+      const int64_t i = i0 + u * stride;
+      ok[u] = i < n;
+      j[u] = ok[u] ? i / d4 : 0;
+      c[u] = static_cast<int>(i - j[u] * d4);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      m[u] = ok[u] ? __ldg(tm + __ldg(own_k + j[u])) : 0u;
+      v[u] = ok[u] ? __ldg(emb + static_cast<int64_t>(__ldg(own_slot + j[u])) * d4 + c[u])
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      uint32_t mm = m[u] & ((1u << W) - 1u);
+      while (mm) {
+        const int w = __ffs(mm) - 1;
+        mm &= mm - 1;
+        const uint32_t pos = e_off[w] + __ldg(&sscan[j[u]].c[w]);
+        pr.E[w][static_cast<int64_t>(pos) * d4 + c[u]] = v[u];
+      }
     }
   }
   __syncthreads();
   if (threadIdx.x == 0) __threadfence_system();
 }
 
-// backward over NVLink, block sizes / offsets from the device plan (blockIdx.y = owner)
+// Deferred FM term (fm != nullptr): the segment sum left -scale * B[r] * E[r] out of the
+// local gradient row r (B[r] = sum of gz over the positions that hit r); it is added here,
+// as the row leaves for its owner, and in owner_reduce for the owner's own rows.
+struct FmDefer {
+  const float4* E;  // local table rows (the forward's G)
+  const float* B;
+  float scale;
+};
+__device__ __forceinline__ float4 with_fm(float4 v, const FmDefer& fm, int64_t row, int c, int d4) {
+  const float k = fm.scale * __ldg(fm.B + row);
+  const float4 e = __ldg(fm.E + row * d4 + c);
+  v.x -= k * e.x;
+  v.y -= k * e.y;
+  v.z -= k * e.z;
+  v.w -= k * e.w;
+  return v;
+}
+
 __global__ void push_blocks_p2p_dev_kernel(const float4* __restrict__ dE, int d4, uint32_t me,
                                            const int32_t* __restrict__ totals,
-                                           const int32_t* __restrict__ offs, PeerRows pr) {
+                                           const int32_t* __restrict__ offs, PeerRows pr,
+                                           FmDefer fm) {
   const int o = blockIdx.y;
   if (o != static_cast<int>(me)) {
     const int64_t n = static_cast<int64_t>(totals[o]) * d4;
-    const float4* src = dE + static_cast<int64_t>(offs[Exchange::kOffRecv + o]) * d4;
+    const int64_t r0 = offs[Exchange::kOffRecv + o];
+    const float4* src = dE + r0 * d4;
     float4* dst = pr.buf[o] + static_cast<int64_t>(offs[Exchange::kOffBoff + o * 8 + me]) * d4;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-      dst[i] = src[i];
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+      float4 v = src[i];
+      if (fm.B) {
+        const int64_t q = i / d4;
+        v = with_fm(v, fm, r0 + q, static_cast<int>(i - q * d4), d4);
+      }
+      dst[i] = v;
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) __threadfence_system();
 }
 
 __global__ void zero_rows_dev_kernel(float4* __restrict__ p, const int32_t* __restrict__ offs,
-                                     int d4) {
+                                     int d4, float* __restrict__ B) {
   const int64_t n = static_cast<int64_t>(offs[Exchange::kOffRecv + 8]) * d4;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     p[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (B && i % d4 == 0) B[i / d4] = 0.f;
+  }
 }
 
-__global__ void owner_reduce_dev_kernel(const uint32_t* __restrict__ own_k,
-                                        const int32_t* __restrict__ n_ptr,
-                                        const uint32_t* __restrict__ tm,
-                                        const Cnt8* __restrict__ sscan,
-                                        const int32_t* __restrict__ totals, uint32_t W, uint32_t me,
-                                        const uint32_t* __restrict__ lpos,
-                                        const float4* __restrict__ dE,
-                                        const float4* __restrict__ recvbuf, int d4,
-                                        float4* __restrict__ g) {
+__global__ void __launch_bounds__(256) owner_reduce_dev_kernel(
+    const uint32_t* __restrict__ own_k, const int32_t* __restrict__ n_ptr,
+    const uint32_t* __restrict__ tm, const Cnt8* __restrict__ sscan,
+    const int32_t* __restrict__ totals, uint32_t W, uint32_t me, const uint32_t* __restrict__ lpos,
+    const float4* __restrict__ dE, const float4* __restrict__ recvbuf, int d4,
+    float4* __restrict__ g, FmDefer fm) {
   const int64_t n = static_cast<int64_t>(*n_ptr) * d4;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t j = i / d4;
-    const int c = static_cast<int>(i - j * d4);
-    const uint32_t k = own_k[j];
-    const uint32_t m = tm[k];
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    uint32_t soff = 0;
-    for (uint32_t w = 0; w < W; ++w) {  // fixed source order (same as owner_reduce_kernel)
-      if ((m >> w) & 1u) {
-        const float4 v = (w == me) ? dE[static_cast<int64_t>(lpos[k]) * d4 + c]
-                                   : recvbuf[static_cast<int64_t>(soff + sscan[j].c[w]) * d4 + c];
+  uint32_t soff[8];  // start of source w's block in my receive buffer
+  uint32_t run = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+    soff[w] = run;
+    if (w < static_cast<int>(W) && w != static_cast<int>(me)) run += static_cast<uint32_t>(totals[8 + w]);
+  }
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i0 < n;
+       i0 += 2 * stride) {
+    int64_t j[2];
+    int c[2];
+    bool ok[2];
+    uint32_t k[2], m[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t i = i0 + u * stride;
+      ok[u] = i < n;
+      j[u] = ok[u] ? i / d4 : 0;
+      c[u] = static_cast<int>(i - j[u] * d4);
+      k[u] = ok[u] ? __ldg(own_k + j[u]) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) m[u] = ok[u] ? __ldg(tm + k[u]) : 0u;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (!ok[u]) continue;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (uint32_t w = 0; w < W; ++w) {  // fixed source order (same as owner_reduce_kernel)
+        if (!((m[u] >> w) & 1u)) continue;
+        float4 v;
+        if (w == me) {
+          const int64_t lr = __ldg(lpos + k[u]);
+          v = dE[lr * d4 + c[u]];
+          if (fm.B) v = with_fm(v, fm, lr, c[u], d4);
+        } else {
+          v = __ldg(recvbuf + static_cast<int64_t>(soff[w] + __ldg(&sscan[j[u]].c[w])) * d4 + c[u]);
+        }
         acc.x += v.x;
         acc.y += v.y;
         acc.z += v.z;
         acc.w += v.w;
       }
-      if (w != me) soff += static_cast<uint32_t>(totals[8 + w]);
+      g[i0 + u * stride] = acc;
     }
-    g[i] = acc;
   }
 }
 
@@ -559,35 +632,39 @@ void Exchange::forward_dev(const uint32_t* d_own_k, const uint32_t* d_own_slot, 
                            const int32_t* d_n_own, const float* emb, cudaStream_t s) {
   PeerRows pr{};
   for (int w = 0; w < W; ++w) pr.E[w] = reinterpret_cast<float4*>(peer_E[w]);
-  push_rows_p2p_dev_kernel<<<std::max(1, std::min(ceil_div(static_cast<int64_t>(n_bound) * 32, 256),
-                                                  148 * 8)),
+  push_rows_p2p_dev_kernel<<<std::max(1, std::min(ceil_div(static_cast<int64_t>(n_bound) * (d / 4), 512),
+                                                  148 * 16)),
                              256, 0, s>>>(d_own_k, d_own_slot, d_n_own, tm, sscan, W, me, offs,
                                           reinterpret_cast<const float4*>(emb), d / 4, pr);
   CUDA_LAUNCH_CHECK();
 }
 
-void Exchange::backward_send_dev(const float* dE, cudaStream_t s) {
+void Exchange::backward_send_dev(const float* dE, cudaStream_t s, const float* E, const float* B,
+                                 float fm_scale) {
   PeerRows pr{};
   for (int o = 0; o < W; ++o) pr.buf[o] = reinterpret_cast<float4*>(peer_buf[o]);
-  push_blocks_p2p_dev_kernel<<<dim3(148 * 2, W), 256, 0, s>>>(reinterpret_cast<const float4*>(dE),
-                                                              d / 4, me, totals, offs, pr);
+  push_blocks_p2p_dev_kernel<<<dim3(148 * 2, W), 256, 0, s>>>(
+      reinterpret_cast<const float4*>(dE), d / 4, me, totals, offs, pr,
+      FmDefer{reinterpret_cast<const float4*>(E), B, fm_scale});
   CUDA_LAUNCH_CHECK();
 }
 
 void Exchange::backward_reduce_dev(const uint32_t* d_own_k, int32_t n_bound, const int32_t* d_n_own,
-                                   const float* dE, cudaStream_t s) {
+                                   const float* dE, cudaStream_t s, const float* E, const float* B,
+                                   float fm_scale) {
   const int d4 = d / 4;
-  owner_reduce_dev_kernel<<<std::max(1, std::min(ceil_div(static_cast<int64_t>(n_bound) * d4, 256),
-                                                 148 * 8)),
+  owner_reduce_dev_kernel<<<std::max(1, std::min(ceil_div(static_cast<int64_t>(n_bound) * d4, 512),
+                                                 148 * 16)),
                             256, 0, s>>>(d_own_k, d_n_own, tm, sscan, totals, W, me, lpos,
                                          reinterpret_cast<const float4*>(dE),
                                          reinterpret_cast<const float4*>(buf), d4,
-                                         reinterpret_cast<float4*>(gown));
+                                         reinterpret_cast<float4*>(gown),
+                                         FmDefer{reinterpret_cast<const float4*>(E), B, fm_scale});
   CUDA_LAUNCH_CHECK();
 }
 
-void Exchange::zero_local_dev(float* dE, cudaStream_t s) {
-  zero_rows_dev_kernel<<<148 * 8, 256, 0, s>>>(reinterpret_cast<float4*>(dE), offs, d / 4);
+void Exchange::zero_local_dev(float* dE, cudaStream_t s, float* B) {
+  zero_rows_dev_kernel<<<148 * 8, 256, 0, s>>>(reinterpret_cast<float4*>(dE), offs, d / 4, B);
   CUDA_LAUNCH_CHECK();
 }
 

@@ -88,11 +88,15 @@ struct Exchange {
   // n_bound bounds the grids, d_n_own is the owned count; nothing returns bytes
   void forward_dev(const uint32_t* d_own_k, const uint32_t* d_own_slot, int32_t n_bound,
                    const int32_t* d_n_own, const float* emb, cudaStream_t s);
-  void backward_send_dev(const float* dE, cudaStream_t s);
+  // B != nullptr: the segment sum deferred the FM term -fm_scale * B[r] * E[r] of local row
+  // r; both the push to the owners and the owner's reduction add it
+  void backward_send_dev(const float* dE, cudaStream_t s, const float* E = nullptr,
+                         const float* B = nullptr, float fm_scale = 0.f);
   void backward_reduce_dev(const uint32_t* d_own_k, int32_t n_bound, const int32_t* d_n_own,
-                           const float* dE, cudaStream_t s);
-  // dE[0 : local rows) = 0 with the row count read on the device
-  void zero_local_dev(float* dE, cudaStream_t s);
+                           const float* dE, cudaStream_t s, const float* E = nullptr,
+                           const float* B = nullptr, float fm_scale = 0.f);
+  // dE[0 : local rows) = 0 (and B[0 : local rows) when given), row count read on the device
+  void zero_local_dev(float* dE, cudaStream_t s, float* B = nullptr);
   bool device_driven() const { return p2p && !copy_engine; }
   int64_t backward(const uint32_t* d_own_k, int32_t n_own, const float* dE, ncclComm_t comm,
                    cudaStream_t s);

@@ -15,8 +15,13 @@ void gather_cache(const uint32_t* own_k, const uint32_t* own_slot, int32_t n_own
                   cudaStream_t s, float* B_zero = nullptr);
 // gather_instances + FM sums: X[i] = G[vid[i]] for the lane's rows; s[r] = sum_f X[r,f];
 // sqp[r, c4] = partial sum of squares
+// slot_of (nullable, d % 4 == 0): read unique k's row from G = the cache table at slot
+// slot_of[k] (one worker: no separate G copy)
 void gather_instances(const uint32_t* vid, int32_t rows, int F, int d, int ldx, const float* G,
-                      float* X, float* fm_s, float* fm_sqp, cudaStream_t s);
+                      float* X, float* fm_s, float* fm_sqp, cudaStream_t s,
+                      const uint32_t* slot_of = nullptr);
+// dG[0 : n*d) = 0 and B[0 : n) = 0 with n = *d_n (bounded by n_bound)
+void zero_rows_b(const int32_t* d_n, int32_t n_bound, int d, float* dG, float* B, cudaStream_t s);
 int fm_sq_parts(int d);  // columns of fm_sqp per row
 // FM sums of a materialised X (standalone model op)
 void fm_sums(const float* X, int32_t rows, int F, int d, int ldx, float* fm_s, float* fm_sqp,

@@ -628,9 +628,14 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   const bool zero_in_gather = W_ == 1 && !a2a_ && d_ % 4 == 0;
   // one worker also defers segment_sum's -scale*gz*G term to sparse_adam (which reads the
   // same G row as emb[slot]): the scatter pass then does not re-gather G per position
-  const bool defer_fm = zero_in_gather && !tower_fused_;
+  // (the owner-routed exchange over peer stores defers it too: the push to the owner and the
+  // owner's reduction add it per local row, see FmDefer in exchange.cu)
+  const bool defer_fm = (zero_in_gather || (xdev && d_ % 4 == 0)) && !tower_fused_;
   // ... and the segment sum then runs inside the tower's dX GEMM epilogue (dX never hits HBM)
   const bool fuse_scatter = defer_fm && !tower_simt_ && H_ <= 64 && dx_scatter_fits(F_, d_);
+  // ... and the forward reads the cache rows in place (own_k is the identity at W = 1, so
+  // unique k's row is emb[own_slot[k]]): G is never materialised
+  const bool direct_emb = defer_fm && zero_in_gather;
   if (a2a_) {
     if (!free_step) {
       xch_.set_counts(h_totals_);
@@ -650,16 +655,19 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
     xch_.local_vids(d_vid_ + static_cast<size_t>(lane0_) * b_ * F_, n_local_, d_lvid_, s);
   } else {
     if (world_ > 1) CUDA_CHECK(cudaMemsetAsync(d_G_, 0, sizeof(float) * ud, s));
-    for (int l = 0; l < lanes_; ++l)
-      gather_cache(lane_[l].own_k, lane_[l].own_slot, n_own[l], snap_cnt(l) + kCntOwned,
-                   lane_[l].emb, d_, d_G_, zero_in_gather ? d_dG_ : nullptr, s,
-                   zero_in_gather ? d_B_ : nullptr);
-    phase("gather_cache", s);
+    if (direct_emb)  // no G copy: gather_instances reads the cache rows through own_slot
+      zero_rows_b(snap_cnt(0) + kCntOwned, n_own[0], d_, d_dG_, d_B_, s);
+    else
+      for (int l = 0; l < lanes_; ++l)
+        gather_cache(lane_[l].own_k, lane_[l].own_slot, n_own[l], snap_cnt(l) + kCntOwned,
+                     lane_[l].emb, d_, d_G_, zero_in_gather ? d_dG_ : nullptr, s,
+                     zero_in_gather ? d_B_ : nullptr);
+    phase(direct_emb ? "zero_grads" : "gather_cache", s);
     if (world_ > 1) {
       NCCL_CHECK(ncclAllReduce(d_G_, d_G_, ud, ncclFloat32, ncclSum, comm_, s));
       stats_.nvlink_bytes += static_cast<int64_t>(ud) * 4;
     }
-    phase("allreduce_embed", s);
+    if (world_ > 1) phase("allreduce_embed", s);
   }
   // interworker ledger: the reference's accounting model, allreduce_bytes per
   // worker for each all-reduce, whatever the device scheme
@@ -669,7 +677,7 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   // ---- per lane: gather_instances, forward_backward, segment_sum (l.11-12)
   if (zero_in_gather) {
   } else if (xdev) {
-    xch_.zero_local_dev(d_dG_, s);
+    xch_.zero_local_dev(d_dG_, s, defer_fm ? d_B_ : nullptr);
   } else if (free_step && d_ % 4 == 0)
     zero_rows_kernel<<<148 * 8, 256, 0, s>>>(reinterpret_cast<float4*>(d_dG_), snap + 0,
                                              d_ / 4, n_global_ * (d_ / 4));
@@ -688,7 +696,8 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
       phase("tower_fused", s);
       continue;
     }
-    gather_instances(vid, b_, F_, d_, ldx_, d_G_, d_X_, d_fm_s_, d_fm_sqp_, s);
+    gather_instances(vid, b_, F_, d_, ldx_, direct_emb ? lane_[0].emb : d_G_, d_X_, d_fm_s_,
+                     d_fm_sqp_, s, direct_emb ? lane_[0].own_slot : nullptr);
     phase("gather_instances", s);
     const DxScatter sc{vid, d_fm_s_, tower_.gz, d_dG_, d_B_, F_, d_};
     if (tower_simt_)
@@ -715,15 +724,17 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   // ---- grad_synchronize (l.13)
   const float* grad_rows = d_dG_;
   if (a2a_) {
+    const bool xfm = xdev && defer_fm;
     if (xdev)
-      xch_.backward_send_dev(d_dG_, s);
+      xch_.backward_send_dev(d_dG_, s, xfm ? d_G_ : nullptr, xfm ? d_B_ : nullptr, emb_scale);
     else
       xch_.backward_send(d_dG_, comm_, s);
     phase("exchange_grad_send", s);
     if (xch_.p2p) xch_.barrier(comm_, s);
     phase("exchange_grad_barrier", s);
     if (xdev)
-      xch_.backward_reduce_dev(lane_[0].own_k, n_own[0], snap_cnt(0) + kCntOwned, d_dG_, s);
+      xch_.backward_reduce_dev(lane_[0].own_k, n_own[0], snap_cnt(0) + kCntOwned, d_dG_, s,
+                               xfm ? d_G_ : nullptr, xfm ? d_B_ : nullptr, emb_scale);
     else
       xch_.backward_reduce(lane_[0].own_k, n_own[0], d_dG_, s);
     grad_rows = xch_.gown;
@@ -749,7 +760,7 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
                 lane_[l].mom, lane_[l].vel, lane_[l].steps, d_bc1_, d_bc2_,
                 static_cast<float>(cfg_.learning_rate), static_cast<float>(cfg_.adam_beta1),
                 static_cast<float>(cfg_.adam_beta2), static_cast<float>(cfg_.adam_epsilon), s,
-                /*inc_steps=*/false, defer_fm ? d_B_ : nullptr, emb_scale);
+                /*inc_steps=*/false, defer_fm && !a2a_ ? d_B_ : nullptr, emb_scale);
   phase("sparse_adam", s);
   dense_steps_ += 1;
   const double bc1 = 1.0 - std::pow(cfg_.adam_beta1, static_cast<double>(dense_steps_));

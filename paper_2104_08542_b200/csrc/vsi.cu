@@ -42,7 +42,10 @@ __global__ void vsi_first_kernel(const uint32_t* __restrict__ ids, int64_t n,
   // lanes holding the same id; positions grow with the lane index, so the
   // lowest peer holds the warp-local first appearance
   const unsigned peers = __match_any_sync(active, f);
-  if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicMin(first + f, static_cast<uint32_t>(i));
+  // hot ids (low unique ratios) hit the same word from many warps: skip the atomic when an
+  // earlier position is already recorded (first[] only ever decreases)
+  if ((threadIdx.x & 31) == __ffs(peers) - 1 && __ldcg(first + f) > static_cast<uint32_t>(i))
+    atomicMin(first + f, static_cast<uint32_t>(i));
 }
 
 __global__ void vsi_emit_kernel(const uint32_t* __restrict__ ids, int64_t n,

@@ -157,6 +157,16 @@ SIGNATURES = [
     ("sfctr_trainer_step", C.c_int, [P, C.c_int64, P, P, P, C.POINTER(C.c_double)]),
     ("sfctr_trainer_step_device", C.c_int, [P, C.c_int64, P, P, P, P]),
     ("sfctr_trainer_submit", C.c_int, [P, C.c_int64, P, P, P]),
+    ("sfctr_criteo_open", C.c_int, [C.c_char_p, P, C.c_int, C.POINTER(P)]),
+    ("sfctr_criteo_open_buffer", C.c_int, [C.c_char_p, C.c_size_t, C.c_char_p, P, C.c_int,
+                                           C.POINTER(P)]),
+    ("sfctr_criteo_destroy", None, [P]),
+    ("sfctr_criteo_row_count", C.c_int64, [P]),
+    ("sfctr_criteo_token_hash", C.c_uint64, [C.c_char_p, C.c_size_t]),
+    ("sfctr_criteo_read_batch", C.c_int, [P, C.c_int64, C.c_int32, C.c_int32, u64p, u8p]),
+    ("sfctr_criteo_read_batch_device", C.c_int, [P, C.c_int64, C.c_int32, C.c_int32, P, P, P]),
+    ("sfctr_criteo_stats", C.c_int, [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                     C.POINTER(C.c_double)]),
     ("sfctr_trainer_loss", C.c_int, [P, C.c_int64, C.POINTER(C.c_double)]),
     ("sfctr_trainer_synchronize", C.c_int, [P]),
     ("sfctr_trainer_stream", P, [P]),
@@ -489,3 +499,63 @@ def model_forward_backward(x, labels, w1, b1, w2, b2, fields, dim, hidden, devic
         _ptr(dw2), _ptr(db2)))
     return {"loss": loss.value, "logits": logits, "dx": dx, "dw1": dw1, "db1": db1, "dw2": dw2,
             "db2": float(db2[0])}
+
+
+class CriteoReader:
+    """CriteoReader (criteo.hpp:37-58) on the device: the TSV is parsed and hashed by the
+    sm_100a kernels at construction; read_batch(step) returns the wrapping global batch."""
+
+    kNumericColumns = 13
+    kCategoricalColumns = 26
+
+    def __init__(self, path, config: Config, device=0, _buffer=None, _name=None):
+        self.config = config
+        self.global_rows = config.num_workers * config.batch_size_per_worker
+        h = P()
+        if _buffer is None:
+            _check(lib().sfctr_criteo_open(str(path).encode(), C.byref(config), device,
+                                           C.byref(h)))
+        else:
+            _check(lib().sfctr_criteo_open_buffer(_buffer, len(_buffer),
+                                                  (_name or "<buffer>").encode(),
+                                                  C.byref(config), device, C.byref(h)))
+        self._h = h
+
+    @classmethod
+    def from_bytes(cls, data: bytes, config: Config, name="<buffer>", device=0):
+        return cls(None, config, device, _buffer=data, _name=name)
+
+    @staticmethod
+    def token_hash(token) -> int:
+        b = token.encode() if isinstance(token, str) else bytes(token)
+        return lib().sfctr_criteo_token_hash(b, len(b))
+
+    def row_count(self) -> int:
+        return lib().sfctr_criteo_row_count(self._h)
+
+    def read_batch(self, step, row0=0, nrows=None):
+        n = self.global_rows - row0 if nrows is None else nrows
+        f = np.zeros(n * 26, np.uint64)
+        y = np.zeros(n, np.uint8)
+        _check(lib().sfctr_criteo_read_batch(self._h, step, row0, n, f, y))
+        return f, y
+
+    def read_batch_device(self, step, row0, nrows, d_features, d_labels, stream=None):
+        _check(lib().sfctr_criteo_read_batch_device(self._h, step, row0, nrows, d_features,
+                                                    d_labels, stream))
+
+    def stats(self):
+        b, l, ms = C.c_int64(0), C.c_int64(0), C.c_double(0)
+        _check(lib().sfctr_criteo_stats(self._h, C.byref(b), C.byref(l), C.byref(ms)))
+        return {"bytes": b.value, "lines": l.value, "parse_ms": ms.value}
+
+    def close(self):
+        if self._h:
+            lib().sfctr_criteo_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

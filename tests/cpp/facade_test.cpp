@@ -3,7 +3,10 @@
 // (sfctr::SyntheticGenerator::generate, sfctr::virtual_sparse_id from the
 // reference TUs in oracle/_ref/libsfctr_ref.so). Exit 0 = identical.
 #include <cstdio>
+#include <fstream>
+#include <random>
 
+#include "sfctr/criteo.hpp"
 #include "sfctr/generator.hpp"
 #include "sfctr/vsi.hpp"
 #include "sfctr_b200.hpp"
@@ -52,6 +55,44 @@ int main() {
     c.set("workers", "0").validate();
     return 1;
   } catch (const sfctr::ConfigError&) {
+  }
+  // CriteoReader: the reference's own reader vs the device reader on one generated file
+  {
+    const char* path = "/tmp/sfctr_facade_criteo.tsv";
+    std::mt19937_64 rng(3);
+    std::ofstream out(path, std::ios::binary);
+    for (int r = 0; r < 500; ++r) {
+      out << (rng() & 1);
+      for (int c = 0; c < 13; ++c) out << '\t' << (rng() % 3 ? std::to_string(rng() % 999) : "");
+      for (int c = 0; c < 26; ++c) {
+        out << '\t';
+        if (rng() % 10) out << std::hex << (rng() & 0xffffffffu) << std::dec;
+      }
+      out << (r % 7 == 0 ? "\r\n" : "\n");
+      if (r % 50 == 0) out << "\n";
+    }
+    out.close();
+    sfctr::SimConfig cc = rc;
+    cc.num_fields = 26;
+    cc.batch_size_per_worker = 96;
+    sfctr::b200::Config cb = bc;
+    cb.set("batch_size", "96");
+    sfctr::CriteoReader ref_rd(path, cc);
+    sfctr::b200::CriteoReader dev_rd(path, cb);
+    if (ref_rd.row_count() != dev_rd.row_count()) {
+      std::printf("criteo row count mismatch\n");
+      return 1;
+    }
+    for (int step = 0; step < 4; ++step) {
+      const sfctr::RawBatch a = ref_rd.read_batch(step), b = dev_rd.read_batch(step);
+      if (a.features != b.features || a.labels != b.labels) {
+        std::printf("criteo batch mismatch at step %d\n", step);
+        return 1;
+      }
+    }
+    if (sfctr::CriteoReader::token_hash("68fd1e64") !=
+        sfctr::b200::CriteoReader::token_hash("68fd1e64"))
+      return 1;
   }
   sfctr::b200::Trainer tr(bc);
   const double loss = tr.step(0, dev_gen.generate(0));

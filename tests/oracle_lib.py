@@ -91,6 +91,11 @@ def oracle():
           C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int])
     _sig(L, "orc_manager_example", C.c_int64,
          [C.c_uint64, u64p, C.c_int, u64p, C.c_int, u64p, C.c_int, u64p, u64p])
+    _sig(L, "orc_criteo_parse", C.c_int64,
+         [C.c_char_p, C.c_size_t, C.c_uint64, u64p, u8p, C.c_int64, C.POINTER(C.c_int64),
+          C.c_char_p, C.c_size_t])
+    _sig(L, "orc_criteo_read_batch", None,
+         [u64p, u8p, C.c_int64, C.c_int64, C.c_int, u64p, u8p])
     _oracle = L
     return L
 
@@ -131,6 +136,12 @@ def ref():
     _sig(L, "ref_cache_slots", None, [C.c_void_p, u64p, i64p, u64p])
     _sig(L, "ref_cache_host_row", C.c_int, [C.c_void_p, C.c_uint64, f64p, C.POINTER(C.c_int64)])
     _sig(L, "ref_config_check", C.c_int, [C.c_char_p, C.c_char_p, C.c_int])
+    _sig(L, "ref_criteo_open", C.c_void_p,
+         [C.c_char_p, C.c_int, C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_int)])
+    _sig(L, "ref_criteo_destroy", None, [C.c_void_p])
+    _sig(L, "ref_criteo_rows", C.c_int64, [C.c_void_p])
+    _sig(L, "ref_criteo_read_batch", None, [C.c_void_p, C.c_int64, u64p, u8p])
+    _sig(L, "ref_criteo_token_hash", C.c_uint64, [C.c_char_p, C.c_size_t])
     _ref = L
     return L
 
@@ -199,3 +210,51 @@ def fnv_digest_fast(*arrays):
     L = oracle()
     buf = b"".join(np.ascontiguousarray(a).view(np.uint8).tobytes() for a in arrays)
     return L.orc_fnv1a64(buf, len(buf))
+
+
+# ---------------- Criteo TSV (criteo.cpp) ----------------
+
+def make_criteo_tsv(rows, seed=0, edge_cases=True):
+    """Synthetic Criteo-format bytes: label, 13 numerics, 26 hex tokens per line, with
+    the reader's edge cases mixed in (empty categorical cells, CRLF endings, empty and
+    "\r"-only lines, long and non-hex tokens, no final newline)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for r in range(rows):
+        lab = str(int(rng.integers(0, 2)))
+        nums = [str(int(x)) if rng.random() > 0.2 else "" for x in rng.integers(0, 5000, 13)]
+        cats = []
+        for f in range(26):
+            u = rng.random()
+            if edge_cases and u < 0.08:
+                cats.append("")
+            elif edge_cases and u < 0.1:
+                cats.append("tok_" + "x" * int(rng.integers(1, 40)))
+            else:
+                cats.append("%08x" % int(rng.integers(0, 1 << 32)))
+        line = "\t".join([lab] + nums + cats)
+        if edge_cases and rng.random() < 0.1:
+            line += "\r"
+        out.append(line)
+        if edge_cases and rng.random() < 0.03:
+            out.append("" if rng.random() < 0.5 else "\r")
+    data = "\n".join(out)
+    if not edge_cases or rng.random() < 0.5:
+        data += "\n"
+    return data.encode()
+
+
+def oracle_criteo(data, vocab):
+    """(features [rows*26] u64, labels [rows] u8) or raises ValueError(line, message)."""
+    O = oracle()
+    cap = data.count(b"\n") + 2
+    f = np.zeros(cap * 26, np.uint64)
+    y = np.zeros(cap, np.uint8)
+    line = C.c_int64(0)
+    msg = C.create_string_buffer(512)
+    rows = O.orc_criteo_parse(data, len(data), vocab, f, y, cap, C.byref(line), msg, 512)
+    if rows == -1:
+        raise ValueError(line.value, msg.value.decode())
+    if rows == -2:
+        raise ValueError(0, "no data rows")
+    return f[:rows * 26].copy(), y[:rows].copy()
