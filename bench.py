@@ -236,7 +236,8 @@ def run_ours(args, D):
     ms_step = D.max(dev_ms) / K
     loss_dev = float(d_loss.item())
 
-    # ---- per-phase breakdown: K more device-resident steps with phase events
+    # ---- per-phase breakdown: K more device-resident steps with phase events (the trainer
+    # issues both stages on one stream while timing, so each phase time is its own)
     tr.set_timing(True)
     D.barrier()
     for i in range(K):

@@ -2,6 +2,9 @@
 // engine's sfb::Error and maps it to a status code + thread-local message,
 // mirroring the reference's exception classes (error.hpp:28-56).
 #include <cstring>
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
 #include <functional>
 #include <fstream>
 #include <memory>
@@ -238,23 +241,6 @@ int sfctr_device_count(int* count) {
 
 // ---------------- Criteo ingest (CriteoReader, criteo.hpp:37-58) ----------------
 namespace {
-struct MemBuf : std::streambuf {  // read-only istream over caller memory
-  MemBuf(const char* p, size_t n) {
-    char* b = const_cast<char*>(p ? p : "");
-    setg(b, b, b + n);
-  }
-  pos_type seekoff(off_type off, std::ios_base::seekdir dir, std::ios_base::openmode) override {
-    char* target = dir == std::ios_base::beg ? eback() + off
-                   : dir == std::ios_base::cur ? gptr() + off
-                                               : egptr() + off;
-    if (target < eback() || target > egptr()) return pos_type(off_type(-1));
-    setg(eback(), target, egptr());
-    return pos_type(target - eback());
-  }
-  pos_type seekpos(pos_type pos, std::ios_base::openmode m) override {
-    return seekoff(off_type(pos), std::ios_base::beg, m);
-  }
-};
 
 void criteo_common(const sfctr_config* cfg, int device, int64_t bytes, sfctr_criteo** out,
                    const std::function<void(sfb::CriteoTable&)>& fill) {
@@ -279,12 +265,31 @@ int sfctr_criteo_open(const char* path, const sfctr_config* cfg, int device, sfc
     if (cfg && cfg->num_fields != 26)  // criteo.cpp:31-34 (before the file is touched)
       sfb::fail(sfb::kConfig, "criteo format has 26 categorical fields; fields=" +
                                   std::to_string(cfg->num_fields) + " was configured");
-    std::ifstream in(path, std::ios::binary);
-    if (!in) sfb::fail(sfb::kConfig, std::string("cannot open criteo file: ") + path);
-    in.seekg(0, std::ios::end);
-    const int64_t bytes = static_cast<int64_t>(in.tellg());
-    in.seekg(0);
-    criteo_common(cfg, device, bytes, out, [&](sfb::CriteoTable& t) { t.ingest(in, path); });
+    const int fd = ::open(path, O_RDONLY);
+    if (fd < 0) sfb::fail(sfb::kConfig, std::string("cannot open criteo file: ") + path);
+    struct stat st {};
+    if (fstat(fd, &st) != 0 || !S_ISREG(st.st_mode)) {
+      ::close(fd);
+      sfb::fail(sfb::kConfig, std::string("cannot open criteo file: ") + path);
+    }
+    const size_t bytes = static_cast<size_t>(st.st_size);
+    auto read_at = [fd, path](char* dst, size_t off, size_t n) {
+      while (n) {
+        const ssize_t r = ::pread(fd, dst, n, static_cast<off_t>(off));
+        if (r <= 0) sfb::fail(sfb::kData, std::string("read error in ") + path);
+        dst += r;
+        off += static_cast<size_t>(r);
+        n -= static_cast<size_t>(r);
+      }
+    };
+    try {
+      criteo_common(cfg, device, static_cast<int64_t>(bytes), out,
+                    [&](sfb::CriteoTable& t) { t.ingest(read_at, bytes, path); });
+    } catch (...) {
+      ::close(fd);
+      throw;
+    }
+    ::close(fd);
   });
 }
 
@@ -292,10 +297,9 @@ int sfctr_criteo_open_buffer(const char* data, size_t n, const char* name, const
                              int device, sfctr_criteo** out) {
   return guarded([&] {
     if (!data && n) sfb::fail(sfb::kLogic, "null data");
-    MemBuf mb(data, n);  // the caller's bytes, read in place (no copy into a string)
-    std::istream in(&mb);
+    auto read_at = [data](char* dst, size_t off, size_t m) { std::memcpy(dst, data + off, m); };
     criteo_common(cfg, device, static_cast<int64_t>(n), out,
-                  [&](sfb::CriteoTable& t) { t.ingest(in, name ? name : "<buffer>"); });
+                  [&](sfb::CriteoTable& t) { t.ingest(read_at, n, name ? name : "<buffer>"); });
   });
 }
 

@@ -1,12 +1,15 @@
 // Criteo TSV ingest on the device (criteo.cu) — CriteoReader (core/include/sfctr/criteo.hpp:37-58).
 #pragma once
 
-#include <istream>
+#include <functional>
 #include <string>
 
 #include "ops.h"
 
 namespace sfb {
+
+// reads source bytes [off, off + n) into dst (thread-safe: called from several threads)
+using ByteReader = std::function<void(char* dst, size_t off, size_t n)>;
 
 struct CriteoTable {
   uint64_t vocab = 0;
@@ -33,7 +36,7 @@ struct CriteoTable {
   // byte_bound: total input size (bounds the row count); chunk: streaming unit
   void init(uint64_t vocab, int fields, int64_t byte_bound, size_t chunk = 64ull << 20);
   void release();
-  void ingest(std::istream& in, const std::string& name);
+  void ingest(const ByteReader& read_at, size_t total, const std::string& name);
   void enqueue_chunk(int k, size_t n);
   // rows [row0, row0 + nrows) of global batch `step` (global_rows rows), wrapping at the end
   void read_batch(int64_t step, int32_t global_rows, int32_t row0, int32_t nrows,

@@ -426,14 +426,16 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   const int64_t launches0 = g_launches;
   const int32_t t = static_cast<int32_t>(step);
   const uint32_t Wu = static_cast<uint32_t>(W_);
-  // sm: manager stage (Data-Loader + Host-Manager of Fig. 4), sw: training stage
-  cudaStream_t sm = mstream_, sw = stream_;
+  // sm: manager stage (Data-Loader + Host-Manager of Fig. 4), sw: training stage. With
+  // per-phase timing on, both stages go on one stream so every phase's time is its own.
+  cudaStream_t sm = timing_ ? stream_ : mstream_, sw = stream_;
+  const bool piped = pipelined_ && sm != sw;
   if (step < 0 || step >= (1ll << 23)) fail(kLogic, "step index out of the supported range");
   if (cfg_.lookahead_depth > 1 && !d_window)
     fail(kLogic, "lookahead > 1 needs the window batches");
   const int k = static_cast<int>(step & 1);  // buffer set of this step
   // the set's previous user (step t-2) must have finished training before it is refilled
-  if (pipelined_ && train_pending_[k]) CUDA_CHECK(cudaStreamWaitEvent(sm, train_done_[k]));
+  if (piped && train_pending_[k]) CUDA_CHECK(cudaStreamWaitEvent(sm, train_done_[k]));
   d_uniq_ = d_uniq_set_[k];
   d_vid_ = d_vid_set_[k];
   for (auto& L : lane_) L.use(k);
@@ -561,7 +563,7 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
     // Otherwise the manager waits for step t-1 to finish first. Either way the victims,
     // and so every result, equal sequential mode's.
     bool keys_ready = false;
-    if (pipelined_ && train_pending_[k ^ 1]) {
+    if (piped && train_pending_[k ^ 1]) {
       bool any = false;
       for (int l = 0; l < lanes_; ++l)
         if (n_work[l] > lane_[l].free_top) {
@@ -875,8 +877,8 @@ void Trainer::submit_host(int64_t step, const uint64_t* features, const uint8_t*
                      " (loss_of) before submitting step " + std::to_string(step));
   // the staging set was last read by step t-2: the manager stream waits for it below
   // (step_device), so the copies go on the manager stream after that wait
-  cudaStream_t sm = mstream_;
-  if (pipelined_ && train_pending_[k]) CUDA_CHECK(cudaStreamWaitEvent(sm, train_done_[k]));
+  cudaStream_t sm = timing_ ? stream_ : mstream_;  // the stream step_device's manager uses
+  if (sm != stream_ && train_pending_[k]) CUDA_CHECK(cudaStreamWaitEvent(sm, train_done_[k]));
   CUDA_CHECK(cudaMemcpyAsync(d_in_feat_set_[k], features, sizeof(uint64_t) * n_local_,
                              cudaMemcpyHostToDevice, sm));
   CUDA_CHECK(cudaMemcpyAsync(d_in_lab_set_[k], labels, static_cast<size_t>(lanes_) * b_,
