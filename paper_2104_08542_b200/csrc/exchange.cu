@@ -130,8 +130,10 @@ void Exchange::release() {
       if (w == me) continue;
       if (peer_E[w]) cudaIpcCloseMemHandle(peer_E[w]);
       if (peer_buf[w]) cudaIpcCloseMemHandle(peer_buf[w]);
+      if (peer_flags[w]) cudaIpcCloseMemHandle(peer_flags[w]);
     }
   if (bar) cudaFree(bar);
+  if (flags) cudaFree(flags);
   for (const PlanSet& q : sets)
     for (void* p : {static_cast<void*>(q.tm), static_cast<void*>(q.lpos),
                     static_cast<void*>(q.sscan), static_cast<void*>(q.tile_cnt),
@@ -519,6 +521,14 @@ __global__ void __launch_bounds__(256) push_rows_p2p_dev_kernel(
   if (threadIdx.x == 0) __threadfence_system();
 }
 
+struct OwnerAdam {
+  float4 *emb, *mom, *vel;
+  const uint32_t* own_slot;
+  const int32_t* steps;
+  const float *bc1, *bc2;
+  float lr, b1, b2, omb1, omb2, eps;
+};
+
 // Deferred FM term (fm != nullptr): the segment sum left -scale * B[r] * E[r] out of the
 // local gradient row r (B[r] = sum of gz over the positions that hit r); it is added here,
 // as the row leaves for its owner, and in owner_reduce for the owner's own rows.
@@ -571,12 +581,15 @@ __global__ void zero_rows_dev_kernel(float4* __restrict__ p, const int32_t* __re
   }
 }
 
+// ADAM: the owner's sum goes straight into the lazy Adam update of its cache slot (same
+// math as sparse_adam_v4, embed.cu) instead of being written to gown and read back.
+template <bool ADAM>
 __global__ void __launch_bounds__(256) owner_reduce_dev_kernel(
     const uint32_t* __restrict__ own_k, const int32_t* __restrict__ n_ptr,
     const uint32_t* __restrict__ tm, const Cnt8* __restrict__ sscan,
     const int32_t* __restrict__ totals, uint32_t W, uint32_t me, const uint32_t* __restrict__ lpos,
     const float4* __restrict__ dE, const float4* __restrict__ recvbuf, int d4,
-    float4* __restrict__ g, FmDefer fm) {
+    float4* __restrict__ g, FmDefer fm, OwnerAdam a) {
   const int64_t n = static_cast<int64_t>(*n_ptr) * d4;
   uint32_t soff[8];  // start of source w's block in my receive buffer
   uint32_t run = 0;
@@ -621,7 +634,24 @@ __global__ void __launch_bounds__(256) owner_reduce_dev_kernel(
         acc.z += v.z;
         acc.w += v.w;
       }
-      g[i0 + u * stride] = acc;
+      if constexpr (ADAM) {  // update_sparse, lazy per-row step count
+        const uint32_t s = __ldg(a.own_slot + j[u]);
+        const int t = __ldg(a.steps + s) + 1;
+        const float c1 = __ldg(a.bc1 + t), c2 = __ldg(a.bc2 + t);
+        const int64_t o = static_cast<int64_t>(s) * d4 + c[u];
+        float4 mm = a.mom[o], vv = a.vel[o], e = a.emb[o];
+#define SFB_ADAM(X)                                   \
+  mm.X = a.b1 * mm.X + a.omb1 * acc.X;                \
+  vv.X = a.b2 * vv.X + a.omb2 * acc.X * acc.X;        \
+  e.X -= a.lr * (mm.X / c1) / (sqrtf(vv.X / c2) + a.eps);
+        SFB_ADAM(x) SFB_ADAM(y) SFB_ADAM(z) SFB_ADAM(w)
+#undef SFB_ADAM
+        a.mom[o] = mm;
+        a.vel[o] = vv;
+        a.emb[o] = e;
+      } else {
+        g[i0 + u * stride] = acc;
+      }
     }
   }
 }
@@ -653,13 +683,32 @@ void Exchange::backward_reduce_dev(const uint32_t* d_own_k, int32_t n_bound, con
                                    const float* dE, cudaStream_t s, const float* E, const float* B,
                                    float fm_scale) {
   const int d4 = d / 4;
-  owner_reduce_dev_kernel<<<std::max(1, std::min(ceil_div(static_cast<int64_t>(n_bound) * d4, 512),
+  owner_reduce_dev_kernel<false><<<std::max(1, std::min(ceil_div(static_cast<int64_t>(n_bound) * d4, 512),
                                                  148 * 16)),
                             256, 0, s>>>(d_own_k, d_n_own, tm, sscan, totals, W, me, lpos,
                                          reinterpret_cast<const float4*>(dE),
                                          reinterpret_cast<const float4*>(buf), d4,
                                          reinterpret_cast<float4*>(gown),
-                                         FmDefer{reinterpret_cast<const float4*>(E), B, fm_scale});
+                                         FmDefer{reinterpret_cast<const float4*>(E), B, fm_scale},
+                                         OwnerAdam{});
+  CUDA_LAUNCH_CHECK();
+}
+
+void Exchange::backward_reduce_adam_dev(const uint32_t* d_own_k, int32_t n_bound,
+                                        const int32_t* d_n_own, const float* dE, cudaStream_t s,
+                                        const float* E, const float* B, float fm_scale,
+                                        const AdamRows& ar) {
+  const int d4 = d / 4;
+  OwnerAdam a{reinterpret_cast<float4*>(ar.emb), reinterpret_cast<float4*>(ar.mom),
+              reinterpret_cast<float4*>(ar.vel), ar.own_slot, ar.steps, ar.bc1, ar.bc2, ar.lr,
+              ar.b1, ar.b2, ar.omb1, ar.omb2, ar.eps};
+  owner_reduce_dev_kernel<true><<<std::max(1, std::min(ceil_div(static_cast<int64_t>(n_bound) * d4, 512),
+                                                       148 * 16)),
+                                  256, 0, s>>>(d_own_k, d_n_own, tm, sscan, totals, W, me, lpos,
+                                               reinterpret_cast<const float4*>(dE),
+                                               reinterpret_cast<const float4*>(buf), d4, nullptr,
+                                               FmDefer{reinterpret_cast<const float4*>(E), B, fm_scale},
+                                               a);
   CUDA_LAUNCH_CHECK();
 }
 
@@ -696,16 +745,19 @@ void Exchange::setup_p2p(float* E, ncclComm_t comm, cudaStream_t s) {
   CUDA_CHECK(cudaStreamSynchronize(s));
   cudaFree(d_ok);
   if (!ok) return;
-  // exchange IPC handles of E and buf
-  cudaIpcMemHandle_t mine[2];
+  // exchange IPC handles of E, buf and the barrier flags
+  CUDA_CHECK(cudaMalloc(&flags, sizeof(uint64_t) * 8));
+  CUDA_CHECK(cudaMemset(flags, 0, sizeof(uint64_t) * 8));
+  cudaIpcMemHandle_t mine[3];
   CUDA_CHECK(cudaIpcGetMemHandle(&mine[0], E));
   CUDA_CHECK(cudaIpcGetMemHandle(&mine[1], buf));
+  CUDA_CHECK(cudaIpcGetMemHandle(&mine[2], flags));
   const size_t hb = sizeof(mine);
   uint8_t* d_h = nullptr;
   CUDA_CHECK(cudaMalloc(&d_h, hb * W));
   CUDA_CHECK(cudaMemcpyAsync(d_h + hb * me, mine, hb, cudaMemcpyHostToDevice, s));
   NCCL_CHECK(ncclAllGather(d_h + hb * me, d_h, hb, ncclUint8, comm, s));
-  std::vector<cudaIpcMemHandle_t> all(2 * W);
+  std::vector<cudaIpcMemHandle_t> all(3 * W);
   CUDA_CHECK(cudaMemcpyAsync(all.data(), d_h, hb * W, cudaMemcpyDeviceToHost, s));
   CUDA_CHECK(cudaStreamSynchronize(s));
   cudaFree(d_h);
@@ -713,23 +765,58 @@ void Exchange::setup_p2p(float* E, ncclComm_t comm, cudaStream_t s) {
     if (w == me) {
       peer_E[w] = E;
       peer_buf[w] = buf;
+      peer_flags[w] = flags;
       continue;
     }
     void* pe = nullptr;
     void* pb = nullptr;
-    CUDA_CHECK(cudaIpcOpenMemHandle(&pe, all[2 * w], cudaIpcMemLazyEnablePeerAccess));
-    CUDA_CHECK(cudaIpcOpenMemHandle(&pb, all[2 * w + 1], cudaIpcMemLazyEnablePeerAccess));
+    void* pf = nullptr;
+    CUDA_CHECK(cudaIpcOpenMemHandle(&pe, all[3 * w], cudaIpcMemLazyEnablePeerAccess));
+    CUDA_CHECK(cudaIpcOpenMemHandle(&pb, all[3 * w + 1], cudaIpcMemLazyEnablePeerAccess));
+    CUDA_CHECK(cudaIpcOpenMemHandle(&pf, all[3 * w + 2], cudaIpcMemLazyEnablePeerAccess));
     peer_E[w] = static_cast<float*>(pe);
     peer_buf[w] = static_cast<float*>(pb);
+    peer_flags[w] = static_cast<uint64_t*>(pf);
   }
   CUDA_CHECK(cudaMalloc(&bar, sizeof(float)));
   CUDA_CHECK(cudaMemset(bar, 0, sizeof(float)));
   p2p = true;
 }
 
+namespace {
+struct PeerFlags {
+  uint64_t* peer[8];  // every rank's flag words (mine included)
+};
+// NVLink flag barrier: rank me stores epoch into slot me of every peer's flags (release,
+// system scope) and waits until every peer's store into its own slot has arrived (acquire).
+// The peer stores being published were made by the previous kernel on this stream, which
+// ended every block with __threadfence_system(). A peer that never arrives (crashed rank)
+// traps after ~20 s instead of hanging the GPU.
+__global__ void flag_barrier_kernel(PeerFlags pf, int W, int me, uint64_t epoch) {
+  const int w = threadIdx.x;
+  if (w >= W || w == me) return;
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(pf.peer[w] + me), "l"(epoch) : "memory");
+  const uint64_t* mine = pf.peer[me] + w;
+  uint64_t v = 0;
+  long long t0 = clock64();
+  for (;;) {
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
+    if (v >= epoch) break;
+    if (clock64() - t0 > 40ll * 1000 * 1000 * 1000) __trap();
+  }
+}
+}  // namespace
+
 void Exchange::barrier(ncclComm_t comm, cudaStream_t s) {
   // stream-ordered rendezvous: every rank's peer stores (kernel complete +
-  // system fence) precede its contribution, so after this all are visible
+  // system fence) precede its arrival, so after this all are visible
+  if (flags && !nccl_barrier) {
+    PeerFlags pf{};
+    for (int w = 0; w < W; ++w) pf.peer[w] = peer_flags[w];
+    flag_barrier_kernel<<<1, 32, 0, s>>>(pf, W, me, ++epoch);
+    CUDA_LAUNCH_CHECK();
+    return;
+  }
   NCCL_CHECK(ncclAllReduce(bar, bar, 1, ncclFloat32, ncclSum, comm, s));
 }
 

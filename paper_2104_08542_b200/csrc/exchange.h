@@ -41,7 +41,11 @@ struct Exchange {
   bool copy_engine = false;  // p2p rows move by SM peer stores (default) or DMA (pack + memcpy)
   float* peer_E[8] = {};
   float* peer_buf[8] = {};
-  float* bar = nullptr;                    // 1-float all-reduce used as a barrier
+  float* bar = nullptr;                    // 1-float all-reduce barrier (NCCL fallback)
+  uint64_t* flags = nullptr;               // [8] NVLink flag barrier: slot w = rank w's epoch
+  uint64_t* peer_flags[8] = {};
+  uint64_t epoch = 0;
+  bool nccl_barrier = false;               // SFCTR_NCCL_BARRIER=1: all-reduce barrier instead
   std::vector<int64_t> roff_all, boff_all;  // [w*8+o]: rank w's E block of owner o;
                                             // [o*8+w]: owner o's buf block of source w
   static constexpr int kTotals = 80;
@@ -95,6 +99,17 @@ struct Exchange {
   void backward_reduce_dev(const uint32_t* d_own_k, int32_t n_bound, const int32_t* d_n_own,
                            const float* dE, cudaStream_t s, const float* E = nullptr,
                            const float* B = nullptr, float fm_scale = 0.f);
+  // the owner's reduction fused with the lazy Adam update of its rows (no gown round trip)
+  struct AdamRows {
+    float *emb, *mom, *vel;
+    const uint32_t* own_slot;
+    const int32_t* steps;
+    const float *bc1, *bc2;
+    float lr, b1, b2, omb1, omb2, eps;
+  };
+  void backward_reduce_adam_dev(const uint32_t* d_own_k, int32_t n_bound, const int32_t* d_n_own,
+                                const float* dE, cudaStream_t s, const float* E, const float* B,
+                                float fm_scale, const AdamRows& ar);
   // dE[0 : local rows) = 0 (and B[0 : local rows) when given), row count read on the device
   void zero_local_dev(float* dE, cudaStream_t s, float* B = nullptr);
   bool device_driven() const { return p2p && !copy_engine; }

@@ -94,6 +94,7 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
   CUDA_CHECK(cudaSetDevice(device));
   CUDA_CHECK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   pipelined_ = cfg_.run_mode == SFCTR_MODE_PIPELINED;
+  if (const char* e = std::getenv("SFCTR_NO_FREE_STEPS")) no_free_steps_ = e[0] == '1';
   mstream_ = stream_;
   if (pipelined_) {  // the manager stage gets the higher priority: it gates the next step
     int lo = 0, hi = 0;
@@ -205,6 +206,8 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
     if (!(np2p && np2p[0] == '1')) xch_.setup_p2p(d_G_, comm_, stream_);
     const char* ce = std::getenv("SFCTR_P2P_COPY_ENGINE");  // DMA copies instead of SM stores
     xch_.copy_engine = ce && ce[0] == '1';
+    const char* nb = std::getenv("SFCTR_NCCL_BARRIER");
+    xch_.nccl_barrier = nb && nb[0] == '1';
   }
   ensure_bias_tables(1024);
   CUDA_CHECK(cudaStreamSynchronize(stream_));
@@ -511,7 +514,7 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   // stream only: the previous step keeps training meanwhile.
   const int64_t bound = lane_[0].umax;
   const bool xdev = a2a_ && xch_.device_driven();
-  bool free_step = world_ == 1 || xdev;
+  bool free_step = (world_ == 1 || xdev) && !no_free_steps_;
   for (int l = 0; l < lanes_ && free_step; ++l) free_step = free_lb_[l] >= bound;
   if (a2a_) {  // exchange plan (touched masks, send/receive positions), device only
     xch_.plan(d_vid_, n_global_, static_cast<int64_t>(b_) * F_, d_uniq_, d_scalars_ + 0,
@@ -725,6 +728,7 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
 
   // ---- grad_synchronize (l.13)
   const float* grad_rows = d_dG_;
+  bool fused_adam = false;  // owner reduction + sparse Adam fused (owner-routed, peer stores)
   if (a2a_) {
     const bool xfm = xdev && defer_fm;
     if (xdev)
@@ -734,9 +738,8 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
     phase("exchange_grad_send", s);
     if (xch_.p2p) xch_.barrier(comm_, s);
     phase("exchange_grad_barrier", s);
-    if (xdev)
-      xch_.backward_reduce_dev(lane_[0].own_k, n_own[0], snap_cnt(0) + kCntOwned, d_dG_, s,
-                               xfm ? d_G_ : nullptr, xfm ? d_B_ : nullptr, emb_scale);
+    if (xdev)  // reduce + update_sparse in one pass (the dense all-reduce goes first)
+      fused_adam = true;
     else
       xch_.backward_reduce(lane_[0].own_k, n_own[0], d_dG_, s);
     grad_rows = xch_.gown;
@@ -755,7 +758,19 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
 
   // ---- update_sparse (l.14) + dense Adam
   ensure_bias_tables(steps_done_ + 2);
-  for (int l = 0; l < lanes_; ++l)
+  if (fused_adam) {
+    const bool xfm = defer_fm;
+    Exchange::AdamRows ar{lane_[0].emb, lane_[0].mom, lane_[0].vel, lane_[0].own_slot,
+                          lane_[0].steps, d_bc1_, d_bc2_,
+                          static_cast<float>(cfg_.learning_rate),
+                          static_cast<float>(cfg_.adam_beta1), static_cast<float>(cfg_.adam_beta2),
+                          static_cast<float>(1.0 - cfg_.adam_beta1),
+                          static_cast<float>(1.0 - cfg_.adam_beta2),
+                          static_cast<float>(cfg_.adam_epsilon)};
+    xch_.backward_reduce_adam_dev(lane_[0].own_k, n_own[0], snap_cnt(0) + kCntOwned, d_dG_, s,
+                                  xfm ? d_G_ : nullptr, xfm ? d_B_ : nullptr, emb_scale, ar);
+  }
+  for (int l = 0; l < lanes_ && !fused_adam; ++l)
     sparse_adam(a2a_ ? nullptr : lane_[l].own_k, lane_[l].own_slot, n_own[l],
                 snap_cnt(l) + kCntOwned, grad_rows, d_,
                 lane_[l].emb,

@@ -82,6 +82,7 @@ class Trainer {
   // (step parity); prep_done_/train_done_ order the stages. Sequential mode issues both
   // stages on stream_.
   bool pipelined_ = false;
+  bool no_free_steps_ = false;  // experiment switch: every step waits for the exact counts
   cudaStream_t mstream_ = nullptr;
   ncclComm_t mcomm_ = nullptr;       // manager-stage communicator (id all-gather)
   cudaEvent_t prep_done_[2] = {}, train_done_[2] = {};
