@@ -557,14 +557,23 @@ __global__ void push_blocks_p2p_dev_kernel(const float4* __restrict__ dE, int d4
     const int64_t r0 = offs[Exchange::kOffRecv + o];
     const float4* src = dE + r0 * d4;
     float4* dst = pr.buf[o] + static_cast<int64_t>(offs[Exchange::kOffBoff + o * 8 + me]) * d4;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-      float4 v = src[i];
-      if (fm.B) {
-        const int64_t q = i / d4;
-        v = with_fm(v, fm, r0 + q, static_cast<int>(i - q * d4), d4);
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i0 < n;
+         i0 += 2 * stride) {  // two independent rows' chunks in flight per thread
+      float4 v[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int64_t i = i0 + u * stride;
+        if (i >= n) continue;
+        v[u] = src[i];
+        if (fm.B) {
+          const int64_t q = i / d4;
+          v[u] = with_fm(v[u], fm, r0 + q, static_cast<int>(i - q * d4), d4);
+        }
       }
-      dst[i] = v;
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        if (i0 + u * stride < n) dst[i0 + u * stride] = v[u];
     }
   }
   __syncthreads();
@@ -673,7 +682,7 @@ void Exchange::backward_send_dev(const float* dE, cudaStream_t s, const float* E
                                  float fm_scale) {
   PeerRows pr{};
   for (int o = 0; o < W; ++o) pr.buf[o] = reinterpret_cast<float4*>(peer_buf[o]);
-  push_blocks_p2p_dev_kernel<<<dim3(148 * 2, W), 256, 0, s>>>(
+  push_blocks_p2p_dev_kernel<<<dim3(148 * 4, W), 256, 0, s>>>(
       reinterpret_cast<const float4*>(dE), d / 4, me, totals, offs, pr,
       FmDefer{reinterpret_cast<const float4*>(E), B, fm_scale});
   CUDA_LAUNCH_CHECK();

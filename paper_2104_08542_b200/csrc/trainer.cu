@@ -109,6 +109,9 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
     // collectives of the two stages overlap, so they run on separate communicators
     mcomm_ = comm_;
     if (pipelined_) NCCL_CHECK(ncclCommSplit(comm_, 0, rank_, &mcomm_, nullptr));
+    CUDA_CHECK(cudaStreamCreateWithFlags(&dstream_, cudaStreamNonBlocking));
+    CUDA_CHECK(cudaEventCreateWithFlags(&dense_ready_, cudaEventDisableTiming));
+    CUDA_CHECK(cudaEventCreateWithFlags(&dense_done_, cudaEventDisableTiming));
   }
 
   vsi_.init(cfg_.vocabulary_size, n_global_);
@@ -250,6 +253,10 @@ Trainer::~Trainer() {
   if (h_counts_) cudaFreeHost(h_counts_);
   if (h_loss_ring_) cudaFreeHost(h_loss_ring_);
   for (auto e : ev_) cudaEventDestroy(e);
+  if (dstream_) cudaStreamSynchronize(dstream_);
+  for (cudaEvent_t e : {dense_ready_, dense_done_})
+    if (e) cudaEventDestroy(e);
+  if (dstream_) cudaStreamDestroy(dstream_);
   if (mcomm_ && mcomm_ != comm_) ncclCommDestroy(mcomm_);
   if (comm_) ncclCommDestroy(comm_);
   if (mstream_ && mstream_ != stream_) cudaStreamDestroy(mstream_);
@@ -727,6 +734,17 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   }
 
   // ---- grad_synchronize (l.13)
+  // The dense gradients are final here: with the flag-barrier exchange (no other NCCL call
+  // on comm_ in this stage) their all-reduce runs on a side stream, overlapping the
+  // embedding-gradient exchange; the tail waits for it.
+  const bool dense_side = world_ > 1 && xdev && !xch_.nccl_barrier && !timing_;
+  if (dense_side) {
+    CUDA_CHECK(cudaEventRecord(dense_ready_, s));
+    CUDA_CHECK(cudaStreamWaitEvent(dstream_, dense_ready_));
+    NCCL_CHECK(ncclAllReduce(d_grads_, d_grads_, P_ + 1, ncclFloat32, ncclSum, comm_, dstream_));
+    CUDA_CHECK(cudaEventRecord(dense_done_, dstream_));
+    stats_.nvlink_bytes += static_cast<int64_t>(P_ + 1) * 4;
+  }
   const float* grad_rows = d_dG_;
   bool fused_adam = false;  // owner reduction + sparse Adam fused (owner-routed, peer stores)
   if (a2a_) {
@@ -747,7 +765,7 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
     NCCL_CHECK(ncclAllReduce(d_dG_, d_dG_, ud, ncclFloat32, ncclSum, comm_, s));
     stats_.nvlink_bytes += static_cast<int64_t>(ud) * 4;
   }
-  if (world_ > 1) {
+  if (world_ > 1 && !dense_side) {
     NCCL_CHECK(ncclAllReduce(d_grads_, d_grads_, P_ + 1, ncclFloat32, ncclSum, comm_, s));
     stats_.nvlink_bytes += static_cast<int64_t>(P_ + 1) * 4;
   }
@@ -779,6 +797,7 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
                 static_cast<float>(cfg_.adam_beta2), static_cast<float>(cfg_.adam_epsilon), s,
                 /*inc_steps=*/false, defer_fm && !a2a_ ? d_B_ : nullptr, emb_scale);
   phase("sparse_adam", s);
+  if (dense_side) CUDA_CHECK(cudaStreamWaitEvent(s, dense_done_));
   dense_steps_ += 1;
   const double bc1 = 1.0 - std::pow(cfg_.adam_beta1, static_cast<double>(dense_steps_));
   const double bc2 = 1.0 - std::pow(cfg_.adam_beta2, static_cast<double>(dense_steps_));

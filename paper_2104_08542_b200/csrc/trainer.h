@@ -85,6 +85,8 @@ class Trainer {
   bool no_free_steps_ = false;  // experiment switch: every step waits for the exact counts
   cudaStream_t mstream_ = nullptr;
   ncclComm_t mcomm_ = nullptr;       // manager-stage communicator (id all-gather)
+  cudaStream_t dstream_ = nullptr;   // dense-gradient all-reduce, overlapping the row exchange
+  cudaEvent_t dense_ready_ = nullptr, dense_done_ = nullptr;
   cudaEvent_t prep_done_[2] = {}, train_done_[2] = {};
   bool train_pending_[2] = {false, false};
   int32_t* d_snap_[2] = {};          // [1 + kCntWords * lanes]: U, then every lane's counters
