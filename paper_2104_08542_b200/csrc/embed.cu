@@ -60,47 +60,63 @@ __global__ void gather_cache_s(const uint32_t* __restrict__ own_k,
 // partial sums.
 // slot_of != nullptr (one worker): G is not materialised; unique k's row is read from the
 // cache slot slot_of[k] (= own_slot, an L2-resident table) instead.
-__global__ void gather_instances_v4(const uint32_t* __restrict__ vid, int32_t rows, int F, int d4,
-                                    const float4* __restrict__ G, float4* __restrict__ X,
-                                    float4* __restrict__ fm_s, float* __restrict__ fm_sqp,
-                                    const uint32_t* __restrict__ slot_of) {
+// Two threads per (row, 16 B chunk), adjacent lanes, each gathering half of the F fields
+// (8 row loads in flight), the FM partial sums combined with one shuffle: twice the
+// threads of a whole-row loop, so the kernel reaches two waves and hides the HBM latency.
+__global__ void __launch_bounds__(256, 4) gather_instances_v4(
+    const uint32_t* __restrict__ vid, int32_t rows, int F, int d4, const float4* __restrict__ G,
+    float4* __restrict__ X, float4* __restrict__ fm_s, float* __restrict__ fm_sqp,
+    const uint32_t* __restrict__ slot_of) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= static_cast<int64_t>(rows) * d4) return;
-  const int64_t r = i / d4;
-  const int c = static_cast<int>(i - r * d4);
+  const int64_t p = i >> 1;
+  const int h = static_cast<int>(i & 1);
+  const bool valid = p < static_cast<int64_t>(rows) * d4;
+  const int64_t r = valid ? p / d4 : 0;
+  const int c = static_cast<int>(p - r * d4);
+  const int Fh = (F + 1) >> 1;
+  const int f0 = h ? Fh : 0, f1 = h ? F : Fh;
   const uint32_t* vr = vid + r * F;
   float4* xr = X + r * F * d4 + c;
   float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
   float sq = 0.f;
-  int f = 0;
-  for (; f + 8 <= F; f += 8) {  // 8 independent row loads in flight
-    uint32_t v[8];
+  if (valid) {
+    int f = f0;
+    for (; f + 8 <= f1; f += 8) {  // 8 independent row loads in flight
+      uint32_t v[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = __ldg(vr + f + u);
-    if (slot_of) {
+      for (int u = 0; u < 8; ++u) v[u] = __ldg(vr + f + u);
+      if (slot_of) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = __ldg(slot_of + v[u]);
+        for (int u = 0; u < 8; ++u) v[u] = __ldg(slot_of + v[u]);
+      }
+      float4 a[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] = __ldg(G + static_cast<int64_t>(v[u]) * d4 + c);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        xr[(f + u) * d4] = a[u];
+        s.x += a[u].x; s.y += a[u].y; s.z += a[u].z; s.w += a[u].w;
+        sq += a[u].x * a[u].x + a[u].y * a[u].y + a[u].z * a[u].z + a[u].w * a[u].w;
+      }
     }
-    float4 a[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) a[u] = __ldg(G + static_cast<int64_t>(v[u]) * d4 + c);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {  // fields summed in order (same as the scalar loop)
-      xr[(f + u) * d4] = a[u];
-      s.x += a[u].x; s.y += a[u].y; s.z += a[u].z; s.w += a[u].w;
-      sq += a[u].x * a[u].x + a[u].y * a[u].y + a[u].z * a[u].z + a[u].w * a[u].w;
+    for (; f < f1; ++f) {
+      uint32_t v = __ldg(vr + f);
+      if (slot_of) v = __ldg(slot_of + v);
+      const float4 a = __ldg(G + static_cast<int64_t>(v) * d4 + c);
+      xr[f * d4] = a;
+      s.x += a.x; s.y += a.y; s.z += a.z; s.w += a.w;
+      sq += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w;
     }
   }
-  for (; f < F; ++f) {
-    uint32_t v = __ldg(vr + f);
-    if (slot_of) v = __ldg(slot_of + v);
-    const float4 a = __ldg(G + static_cast<int64_t>(v) * d4 + c);
-    xr[f * d4] = a;
-    s.x += a.x; s.y += a.y; s.z += a.z; s.w += a.w;
-    sq += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w;
+  s.x += __shfl_xor_sync(0xFFFFFFFFu, s.x, 1);
+  s.y += __shfl_xor_sync(0xFFFFFFFFu, s.y, 1);
+  s.z += __shfl_xor_sync(0xFFFFFFFFu, s.z, 1);
+  s.w += __shfl_xor_sync(0xFFFFFFFFu, s.w, 1);
+  sq += __shfl_xor_sync(0xFFFFFFFFu, sq, 1);
+  if (valid && h == 0) {
+    fm_s[r * d4 + c] = s;
+    fm_sqp[r * d4 + c] = sq;
   }
-  fm_s[r * d4 + c] = s;
-  fm_sqp[r * d4 + c] = sq;
 }
 
 __global__ void gather_instances_s(const uint32_t* __restrict__ vid, int32_t rows, int F, int d,
@@ -319,7 +335,7 @@ void gather_instances(const uint32_t* vid, int32_t rows, int F, int d, int ldx, 
   if (rows <= 0) return;
   SFB_CHECK(!slot_of || (d & 3) == 0, "gather_instances: slot indirection needs d % 4 == 0");
   if ((d & 3) == 0) {
-    const int64_t n = static_cast<int64_t>(rows) * (d / 4);
+    const int64_t n = static_cast<int64_t>(rows) * (d / 4) * 2;  // two threads per chunk
     gather_instances_v4<<<ceil_div(n, 256), 256, 0, s>>>(
         vid, rows, F, d / 4, reinterpret_cast<const float4*>(G), reinterpret_cast<float4*>(X),
         reinterpret_cast<float4*>(fm_s), fm_sqp, slot_of);
