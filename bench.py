@@ -41,8 +41,8 @@ METRIC = "training samples/sec"
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
-    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--steps", type=int, default=100)
+    p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--batch", type=int, default=8192)
     p.add_argument("--fields", type=int, default=39)
@@ -72,64 +72,61 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
+_SAMPLER = r"""
+import sys, time, pynvml
+pynvml.nvmlInit()
+hs = [pynvml.nvmlDeviceGetHandleByIndex(int(i)) for i in sys.argv[1].split(",")]
+mx = [pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM) for h in hs]
+print("max", *mx, flush=True)
+period = float(sys.argv[2])
+while True:
+    for i, h in enumerate(hs):
+        print(i, pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+              pynvml.nvmlDeviceGetCurrentClocksEventReasons(h), flush=True)
+    time.sleep(period)
+"""
+
+
 class Clocks:
-    """SM clock / throttle-reason sampler for the timed region (B200_PROFILING.md clocks line).
-    NVML polled from a thread every ~1 ms: the timed region is only milliseconds long,
-    shorter than nvidia-smi's sampling period."""
+    """SM clock / throttle-reason sampler for the timed region (B200_PROFILING.md clocks line):
+    NVML polled every 5 ms for every GPU of the job from ONE separate process started by
+    rank 0 (no GIL or driver-lock contention inside the ranks that issue the steps)."""
 
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
 
-    def __init__(self, index):
-        self.index = index
-        self.th = None
-        self.sm, self.mx, self.reasons, self.err = [], [], set(), None
-
-    def _run(self):
-        import pynvml
-        reasons = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
-                   "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
-                   "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
-                   "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
-        h = self.h
-        try:
-            while not self.stop_flag or not self.sm:
-                self.sm.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
-                r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                for n, bit in reasons.items():
-                    if r & bit:
-                        self.reasons.add(n)
-                time.sleep(0.001)
-            pynvml.nvmlShutdown()
-        except Exception as e:  # noqa: BLE001
-            self.err = str(e)
+    def __init__(self, indices, period_s=0.005):
+        self.indices, self.period = list(indices), period_s
+        self.proc = None
 
     def start(self):
-        import threading
-
-        import pynvml
-        try:  # NVML init (slow the first time) happens before the timed region
-            pynvml.nvmlInit()
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-            self.mx.append(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
-        except Exception as e:  # noqa: BLE001
-            self.err = str(e)
-            return
-        self.stop_flag = False
-        self.th = threading.Thread(target=self._run, daemon=True)
-        self.th.start()
-        while not self.sm and self.th.is_alive():
-            time.sleep(0.0005)
+        try:
+            self.proc = subprocess.Popen(
+                [sys.executable, "-c", _SAMPLER, ",".join(map(str, self.indices)), str(self.period)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            first = self.proc.stdout.readline().split()  # "max ..." once NVML is up
+            self.mx = [int(x) for x in first[1:]] if first and first[0] == "max" else []
+        except Exception:  # noqa: BLE001
+            self.proc = None
 
     def stop(self):
-        if not self.th:
+        if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["sampler not started"]}
-        self.stop_flag = True
-        self.th.join(timeout=10)
-        out = {"sm_mhz": statistics.median(self.sm) if self.sm else None,
-               "sm_max_mhz": max(self.mx) if self.mx else None, "reasons": sorted(self.reasons),
-               "samples": len(self.sm), "sampler": "nvml 1 ms"}
-        if self.err:
-            out["error"] = self.err
-        return out
+        self.proc.terminate()
+        out_txt, _ = self.proc.communicate(timeout=10)
+        sm, reasons = [], set()
+        for line in out_txt.splitlines():
+            f = line.split()
+            if len(f) != 3:
+                continue
+            sm.append(int(f[1]))
+            for n, bit in self.REASONS.items():
+                if int(f[2]) & bit:
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(self.mx) if self.mx else None, "reasons": sorted(reasons),
+                "samples": len(sm), "gpus": len(self.indices),
+                "sampler": "nvml 5 ms, separate process"}
 
 
 def phase_bytes(name, U, Uw, n, b, d, F, H, Ntot, fused_scatter=False):
@@ -203,23 +200,26 @@ def run_ours(args, D):
     # per-phase events inside this region; the breakdown is a separate pass below)
     phases = {}
     stats_acc = {}
-    clocks = Clocks(dev)
+    clocks = Clocks(range(world)) if rank == 0 else None
     launches = 0
+    if clocks:
+        clocks.start()
     D.barrier()
     torch.cuda.synchronize()
-    clocks.start()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     st0 = tr.stats()  # running totals before the timed region (waits for the stream)
     ev0.record(stream)
+    h0 = time.perf_counter()
     for i in range(K):
         s = W + i
         tr.step_device(s, d_feat[s].data_ptr(), d_lab[s].data_ptr(), None, d_loss.data_ptr())
+    host_issue_ms = (time.perf_counter() - h0) * 1e3 / K
     ev1.record(stream)
     ev1.synchronize()
     torch.cuda.synchronize()
     dev_ms = ev0.elapsed_time(ev1)
-    clk = clocks.stop()
+    clk = clocks.stop() if clocks else None
     tr.synchronize()  # deferred device counters
     st1 = tr.stats()
     tot = {k2: st1[k2] - st0[k2] for k2 in st1 if k2.startswith("total")}
@@ -360,6 +360,7 @@ def run_ours(args, D):
                 "h2d_bytes_per_step": int(nrows * F * 8 + nrows),
                 "d2h_bytes_per_step": 4},
         "gpu_launches": int(launches),
+        "host_issue_ms_per_step": round(D.max(host_issue_ms), 4),
         "roofline": roofline,
         "kernels": kernels,
         "mixcache": mix,

@@ -92,15 +92,17 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
     fail(kCuda, "no CUDA device available (the device path has no CPU fallback)");
   }
   CUDA_CHECK(cudaSetDevice(device));
-  CUDA_CHECK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   pipelined_ = cfg_.run_mode == SFCTR_MODE_PIPELINED;
+  int prio_lo = 0, prio_hi = 0;
+  CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  // the training stage is the step's critical path: in pipelined mode its CTAs are
+  // scheduled ahead of the manager stage's (which only has to finish within the step)
+  CUDA_CHECK(cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking,
+                                          pipelined_ ? prio_hi : prio_lo));
   if (const char* e = std::getenv("SFCTR_NO_FREE_STEPS")) no_free_steps_ = e[0] == '1';
   mstream_ = stream_;
-  if (pipelined_) {  // the manager stage gets the higher priority: it gates the next step
-    int lo = 0, hi = 0;
-    CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    CUDA_CHECK(cudaStreamCreateWithPriority(&mstream_, cudaStreamNonBlocking, hi));
-  }
+  if (pipelined_)
+    CUDA_CHECK(cudaStreamCreateWithPriority(&mstream_, cudaStreamNonBlocking, prio_lo));
   if (world_ > 1) {
     if (!nccl_id) fail(kConfig, "world > 1 needs an NCCL unique id");
     ncclUniqueId id;
