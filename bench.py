@@ -129,7 +129,7 @@ class Clocks:
                 "sampler": "nvml 5 ms, separate process"}
 
 
-def phase_bytes(name, U, Uw, n, b, d, F, H, Ntot, fused_scatter=False):
+def phase_bytes(name, U, Uw, n, b, d, F, H, Ntot, fused_scatter=False, xrecv=0):
     """Algorithmic bytes (or FLOPs for the tower) per step for each phase.
     fused_scatter: the segment sum runs in the dX GEMM's epilogue (one worker)."""
     if name == "vsi":
@@ -142,8 +142,8 @@ def phase_bytes(name, U, Uw, n, b, d, F, H, Ntot, fused_scatter=False):
         return 4 * n + 8 * d * n + 4 * b * d + b * d, "B"
     if name == "segment_sum":
         return 4 * n + 4 * d * n + 4 * d * U, "B"
-    if name == "sparse_adam":
-        return 28 * d * Uw + 12 * Uw, "B"
+    if name == "sparse_adam":  # (owner-routed: + the owner's read of the pushed gradient rows)
+        return 28 * d * Uw + 12 * Uw + xrecv, "B"
     if name in ("tower_gemm1", "tower_gemm3"):  # X [b x F*d] streamed once (W1 / dh from L2)
         return 4 * b * F * d, "B"
     if name == "tower_gemm2":  # dX [b x F*d] written once, or (fused) scattered into dG
@@ -279,10 +279,14 @@ def run_ours(args, D):
     n = args.batch * F
     Ntot = world * n
     d, H = args.dim, args.hidden
+    # owner-routed exchange: nvlink_bytes counts the forward rows pushed + received once;
+    # per direction each GPU moves about half of it each way, forward and backward alike
+    xrecv = per_step.get("nvlink_bytes", 0) / 2 if (world > 1 and args.sync == "alltoall") else 0
     kernels = {}
     for nm, ms in phase_ms.items():
         amount, unit = phase_bytes(nm, U, Uw, n, args.batch, d, F, H, Ntot,
-                                   fused_scatter="segment_sum" not in phase_ms)
+                                   fused_scatter="segment_sum" not in phase_ms,
+                                   xrecv=xrecv)
         row = {"ms": round(ms, 4)}
         if amount is not None and ms > 0:
             if unit == "B":
@@ -333,7 +337,16 @@ def run_ours(args, D):
         sync = {"ms": round(sync_ms, 4), "bytes_per_step": int(nv), "scheme": args.sync,
                 "busbw_gbs": round(busbytes / (sync_ms / 1e3) / 1e9, 1) if sync_ms else None,
                 "peak_gbs": 770.0, "peak_source": "B200_PROFILING.md measured peer copy",
-                "note": "time includes the exchange planning-free phases only"}
+                "note": "busbw over every sync phase (id all-gather, plan, barriers included)"}
+        if args.sync == "alltoall":  # the row moves alone: bytes per direction / push time
+            per_dir = nv / 2
+            fwd, bwd = phase_ms.get("exchange_embed", 0), phase_ms.get("exchange_grad_send", 0)
+            sync["rows"] = {"bytes_per_direction": int(per_dir),
+                            "fwd_push_ms": round(fwd, 4), "bwd_push_ms": round(bwd, 4),
+                            "fwd_gbs": round(per_dir / (fwd / 1e3) / 1e9, 1) if fwd else None,
+                            "bwd_gbs": round(per_dir / (bwd / 1e3) / 1e9, 1) if bwd else None,
+                            "frac_fwd": round(per_dir / (fwd / 1e3) / 1e9 / 770.0, 3) if fwd else None,
+                            "frac_bwd": round(per_dir / (bwd / 1e3) / 1e9 / 770.0, 3) if bwd else None}
     fill_ms = phase_ms.get("manage_evict_admit", 0.0)
     mix = {"cache_slots_per_gpu": args.cache, "owned_uniques_per_step": round(Uw, 1),
            "misses_per_step": round(per_step.get("working", 0), 1),
