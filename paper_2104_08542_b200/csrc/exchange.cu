@@ -672,7 +672,7 @@ void Exchange::forward_dev(const uint32_t* d_own_k, const uint32_t* d_own_slot, 
   PeerRows pr{};
   for (int w = 0; w < W; ++w) pr.E[w] = reinterpret_cast<float4*>(peer_E[w]);
   push_rows_p2p_dev_kernel<<<std::max(1, std::min(ceil_div(static_cast<int64_t>(n_bound) * (d / 4), 512),
-                                                  148 * 16)),
+                                                  148 * 2)),
                              256, 0, s>>>(d_own_k, d_own_slot, d_n_own, tm, sscan, W, me, offs,
                                           reinterpret_cast<const float4*>(emb), d / 4, pr);
   CUDA_LAUNCH_CHECK();
@@ -682,7 +682,10 @@ void Exchange::backward_send_dev(const float* dE, cudaStream_t s, const float* E
                                  float fm_scale) {
   PeerRows pr{};
   for (int o = 0; o < W; ++o) pr.buf[o] = reinterpret_cast<float4*>(peer_buf[o]);
-  push_blocks_p2p_dev_kernel<<<dim3(148 * 4, W), 256, 0, s>>>(
+  // one wave of writers per destination: more concurrent NVLink writers congest the switch
+  // (microbench/nvlink_push.cu: 569 GB/s out per GPU with 148 CTAs per peer at W = 4,
+  // 444 GB/s with 592, 406 GB/s with 1184)
+  push_blocks_p2p_dev_kernel<<<dim3(148, W), 256, 0, s>>>(
       reinterpret_cast<const float4*>(dE), d / 4, me, totals, offs, pr,
       FmDefer{reinterpret_cast<const float4*>(E), B, fm_scale});
   CUDA_LAUNCH_CHECK();
