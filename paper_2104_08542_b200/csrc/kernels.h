@@ -49,6 +49,7 @@ void sparse_adam(const uint32_t* grad_idx, const uint32_t* own_slot, int32_t n_o
 // scatter-adds into dG / Bsum instead of writing dX (see tc_dx.cuh, embed.cu segment_sum).
 struct DxScatter {
   const uint32_t* vid;
+  const uint32_t* remap;  // nullable: the table row of position i is remap[vid[i]]
   const float* fm_s;
   const float* gz;
   float* dG;

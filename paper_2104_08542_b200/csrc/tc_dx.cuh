@@ -47,6 +47,7 @@ struct DxParams {
   float scale;
   // SCATTER only
   const uint32_t* vid;  // [M x F] table rows of the positions
+  const uint32_t* remap;  // nullable: row = remap[vid] (owner-routed: global unique -> local row)
   const float* fm_s;    // [M x d] FM field sums
   const float* gz;      // [M]
   float* dG;            // [rows x d] gradient table (red.add)
@@ -213,7 +214,9 @@ __global__ void __launch_bounds__(dx_threads<SCATTER>(), 1)
       if (m != cur_m) {  // stage this m-tile's vid / gz (the previous tile's scatter is done)
         for (int idx = et; idx < BM * F; idx += 32 * EW) {
           const int r = idx / F;
-          vid_s[idx] = r0 + r < p.M ? __ldg(p.vid + static_cast<int64_t>(r0) * F + idx) : 0u;
+          uint32_t v = r0 + r < p.M ? __ldg(p.vid + static_cast<int64_t>(r0) * F + idx) : 0u;
+          if (p.remap && r0 + r < p.M) v = __ldg(p.remap + v);
+          vid_s[idx] = v;
         }
         if (et < BM) gz_s[et] = r0 + et < p.M ? __ldg(p.gz + r0 + et) : 0.f;
         cur_m = m;

@@ -194,6 +194,7 @@ void launch_dx_gemm(const TowerTC& tc_, const float* dh_hi, const float* dh_lo, 
   const int grid = std::min(p.tiles, sm_count());
   if (sc) {
     p.vid = sc->vid;
+    p.remap = sc->remap;
     p.fm_s = sc->fm_s;
     p.gz = sc->gz;
     p.dG = sc->dG;

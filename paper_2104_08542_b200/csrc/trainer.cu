@@ -650,6 +650,8 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   // ... and the forward reads the cache rows in place (own_k is the identity at W = 1, so
   // unique k's row is emb[own_slot[k]]): G is never materialised
   const bool direct_emb = defer_fm && zero_in_gather;
+  // owner-routed: positions index the local table through lpos (no lvid pass)
+  const bool remap_local = a2a_ && fuse_scatter && d_ % 4 == 0;
   if (a2a_) {
     if (!free_step) {
       xch_.set_counts(h_totals_);
@@ -666,7 +668,10 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
     if (xch_.p2p) xch_.barrier(comm_, s);
     phase("exchange_barrier", s);
     table_rows = free_step ? static_cast<size_t>(n_global_) : static_cast<size_t>(xch_.local_rows());
-    xch_.local_vids(d_vid_ + static_cast<size_t>(lane0_) * b_ * F_, n_local_, d_lvid_, s);
+    // with the fused scatter the forward gather and the dX epilogue look the local row up
+    // themselves (vid -> lpos[vid]); otherwise the local row of every position is materialised
+    if (!remap_local)
+      xch_.local_vids(d_vid_ + static_cast<size_t>(lane0_) * b_ * F_, n_local_, d_lvid_, s);
   } else {
     if (world_ > 1) CUDA_CHECK(cudaMemsetAsync(d_G_, 0, sizeof(float) * ud, s));
     if (direct_emb)  // no G copy: gather_instances reads the cache rows through own_slot
@@ -699,8 +704,10 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
     CUDA_CHECK(cudaMemsetAsync(d_dG_, 0, sizeof(float) * table_rows * d_, s));
   const float emb_scale = 1.f / static_cast<float>(W_);
   for (int l = 0; l < lanes_; ++l) {
-    const uint32_t* vid =
-        a2a_ ? d_lvid_ : d_vid_ + static_cast<size_t>(lane0_ + l) * b_ * F_;
+    const uint32_t* vid = a2a_ && !remap_local
+                              ? d_lvid_
+                              : d_vid_ + static_cast<size_t>(lane0_ + l) * b_ * F_;
+    const uint32_t* remap = remap_local ? xch_.lpos : nullptr;
     const uint8_t* lab = d_labels + static_cast<size_t>(l) * b_;
     if (tower_fused_) {  // gather -> GEMM -> scatter-add, X / dX never materialised
       tower_forward_backward_fused(tower_, towertc_, d_G_, static_cast<int64_t>(table_rows), vid,
@@ -711,9 +718,9 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
       continue;
     }
     gather_instances(vid, b_, F_, d_, ldx_, direct_emb ? lane_[0].emb : d_G_, d_X_, d_fm_s_,
-                     d_fm_sqp_, s, direct_emb ? lane_[0].own_slot : nullptr);
+                     d_fm_sqp_, s, direct_emb ? lane_[0].own_slot : remap);
     phase("gather_instances", s);
-    const DxScatter sc{vid, d_fm_s_, tower_.gz, d_dG_, d_B_, F_, d_};
+    const DxScatter sc{vid, remap, d_fm_s_, tower_.gz, d_dG_, d_B_, F_, d_};
     if (tower_simt_)
       tower_forward_backward_simt(tower_, d_X_, d_fm_s_, d_fm_sqp_, lab, b_, F_, d_, d_dense_,
                                   d_logits_ + static_cast<size_t>(l) * b_, d_dX_, emb_scale,
