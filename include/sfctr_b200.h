@@ -195,6 +195,16 @@ int sfctr_trainer_step(sfctr_trainer* t, int64_t step, const uint64_t* features,
 int sfctr_trainer_step_device(sfctr_trainer* t, int64_t step, const uint64_t* d_features,
                               const uint8_t* d_labels, const uint64_t* d_window_features,
                               float* d_loss);
+/* The device step split into its two stages (Algorithm 1): prepare = Host-Manager
+ * (all-gather ids, virtual_sparse_id, manager_get + pull_parameters_to_host +
+ * push_parameters_to_cache, exchange plan), train = GPU-Worker
+ * (gather_cache ... update_sparse). Both only enqueue. prepare(t) must
+ * be followed by train(t) before prepare(t+1) (else SFCTR_ERR_LOGIC); in pipelined mode
+ * prepare(t+1) runs on the manager stream while train(t) is still executing.
+ * sfctr_trainer_step_device(t) == prepare(t) + train(t). */
+int sfctr_trainer_prepare(sfctr_trainer* t, int64_t step, const uint64_t* d_features,
+                          const uint64_t* d_window_features);
+int sfctr_trainer_train(sfctr_trainer* t, int64_t step, const uint8_t* d_labels, float* d_loss);
 /* The host-buffer step split in two, for a driver that keeps one step in flight
  * (pipelined mode overlaps the manager stage of step t+1 with step t's training):
  * submit enqueues the H2D copies of the inputs, the step and the D2H copy of its loss,

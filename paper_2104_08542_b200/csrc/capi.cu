@@ -542,6 +542,15 @@ int sfctr_trainer_step_device(sfctr_trainer* t, int64_t step, const uint64_t* d_
   return guarded([&] { t->t->step_device(step, d_features, d_labels, d_window, d_loss); });
 }
 
+int sfctr_trainer_prepare(sfctr_trainer* t, int64_t step, const uint64_t* d_features,
+                          const uint64_t* d_window) {
+  return guarded([&] { t->t->prepare(step, d_features, d_window); });
+}
+
+int sfctr_trainer_train(sfctr_trainer* t, int64_t step, const uint8_t* d_labels, float* d_loss) {
+  return guarded([&] { t->t->train(step, d_labels, d_loss); });
+}
+
 int sfctr_trainer_submit(sfctr_trainer* t, int64_t step, const uint64_t* features,
                          const uint8_t* labels, const uint64_t* window) {
   return guarded([&] { t->t->submit_host(step, features, labels, window); });

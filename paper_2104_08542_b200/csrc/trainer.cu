@@ -432,9 +432,14 @@ __global__ void snap_kernel(SnapArgs a) {
 }
 }  // namespace
 
-void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_t* d_labels,
-                          const uint64_t* d_window, float* d_loss) {
+// Host-Manager stage of step t (Algorithm 1 l.2-7; manager_get + pull_parameters_to_host +
+// push_parameters_to_cache): ids, VSI, MixCache, exchange plan, enqueued on
+// the manager stream. The training stage of the same step must follow (train()) before the
+// next step is prepared.
+void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* d_window) {
   CUDA_CHECK(cudaSetDevice(dev_));
+  if (prep_.step >= 0)
+    fail(kLogic, "step " + std::to_string(prep_.step) + " was prepared but not trained");
   const int64_t launches0 = g_launches;
   const int32_t t = static_cast<int32_t>(step);
   const uint32_t Wu = static_cast<uint32_t>(W_);
@@ -626,10 +631,35 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
     CUDA_LAUNCH_CHECK();
   }
   phase("manage_evict_admit", sm);
-  if (sm != sw) {  // hand the step to the training stage
-    CUDA_CHECK(cudaEventRecord(prep_done_[k], sm));
-    CUDA_CHECK(cudaStreamWaitEvent(sw, prep_done_[k]));
-  }
+  if (sm != sw) CUDA_CHECK(cudaEventRecord(prep_done_[k], sm));
+  prep_.step = step;
+  prep_.k = k;
+  prep_.sm = sm;
+  prep_.free_step = free_step;
+  prep_.xdev = xdev;
+  prep_.U = U;
+  prep_.n_own = n_own;
+  prep_.launches0 = launches0;
+}
+
+// GPU-Worker stage of the prepared step t (Algorithm 1 l.9-14; gather_cache ...
+// update_sparse), enqueued on the training stream behind its manager stage.
+void Trainer::train(int64_t step, const uint8_t* d_labels, float* d_loss) {
+  CUDA_CHECK(cudaSetDevice(dev_));
+  if (prep_.step != step)
+    fail(kLogic, "train(" + std::to_string(step) + ") without prepare(" + std::to_string(step) + ")");
+  const int64_t launches0 = prep_.launches0;
+  const int32_t t = static_cast<int32_t>(step);
+  const int k = prep_.k;
+  cudaStream_t sm = prep_.sm, sw = stream_;
+  const bool free_step = prep_.free_step, xdev = prep_.xdev;
+  const int32_t U = prep_.U;
+  const std::vector<int32_t> n_own = prep_.n_own;
+  int32_t* snap = d_snap_[k];
+  auto snap_cnt = [&](int l) { return snap + 1 + kCntWords * l; };
+  prep_.step = -1;
+  if (sm != sw) CUDA_CHECK(cudaStreamWaitEvent(sw, prep_done_[k]));
+  (void)t;
 
   // ==== training stage (stream sw) ====
   cudaStream_t s = sw;
@@ -879,6 +909,12 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
   stats_.total_nvlink_bytes += stats_.nvlink_bytes;
   stats_.total_kernel_launches += stats_.kernel_launches;
   stats_.total_pinned_waits += stats_.pinned_waits;
+}
+
+void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_t* d_labels,
+                          const uint64_t* d_window, float* d_loss) {
+  prepare(step, d_features, d_window);
+  train(step, d_labels, d_loss);
 }
 
 // Folds the deferred device counters in: capacity errors flagged by kernels

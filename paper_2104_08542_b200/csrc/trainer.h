@@ -23,6 +23,10 @@ class Trainer {
   // one BSP step over this process's rows; inputs on the device
   void step_device(int64_t step, const uint64_t* d_features, const uint8_t* d_labels,
                    const uint64_t* d_window, float* d_loss);
+  // the same in its two stages (prepare = Host-Manager, train = GPU-Worker); prepare(t)
+  // must be followed by train(t) before prepare(t + 1)
+  void prepare(int64_t step, const uint64_t* d_features, const uint64_t* d_window);
+  void train(int64_t step, const uint8_t* d_labels, float* d_loss);
   // host-buffer variant: H2D copies, step, loss read back
   double step_host(int64_t step, const uint64_t* features, const uint8_t* labels,
                    const uint64_t* window);
@@ -81,6 +85,15 @@ class Trainer {
   // while step t trains on stream_. Buffers the training stage reads come in two sets
   // (step parity); prep_done_/train_done_ order the stages. Sequential mode issues both
   // stages on stream_.
+  struct Prepared {  // what the manager stage of a step hands to its training stage
+    int64_t step = -1;
+    int k = 0;
+    cudaStream_t sm = nullptr;
+    bool free_step = false, xdev = false;
+    int32_t U = 0;
+    std::vector<int32_t> n_own;
+    int64_t launches0 = 0;
+  } prep_;
   bool pipelined_ = false;
   bool no_free_steps_ = false;  // experiment switch: every step waits for the exact counts
   cudaStream_t mstream_ = nullptr;

@@ -157,6 +157,8 @@ SIGNATURES = [
     ("sfctr_trainer_step", C.c_int, [P, C.c_int64, P, P, P, C.POINTER(C.c_double)]),
     ("sfctr_trainer_step_device", C.c_int, [P, C.c_int64, P, P, P, P]),
     ("sfctr_trainer_submit", C.c_int, [P, C.c_int64, P, P, P]),
+    ("sfctr_trainer_prepare", C.c_int, [P, C.c_int64, P, P]),
+    ("sfctr_trainer_train", C.c_int, [P, C.c_int64, P, P]),
     ("sfctr_criteo_open", C.c_int, [C.c_char_p, P, C.c_int, C.POINTER(P)]),
     ("sfctr_criteo_open_buffer", C.c_int, [C.c_char_p, C.c_size_t, C.c_char_p, P, C.c_int,
                                            C.POINTER(P)]),
@@ -390,6 +392,14 @@ class Trainer:
         finally:
             getattr(self, "_keep", {}).pop(step, None)
         return l.value
+
+    def prepare_device(self, step, d_features, d_window=None):
+        """Host-Manager stage of `step` (device buffers), enqueued."""
+        _check(lib().sfctr_trainer_prepare(self._h, step, d_features, d_window))
+
+    def train_device(self, step, d_labels, d_loss=None):
+        """GPU-Worker stage of the prepared `step`, enqueued."""
+        _check(lib().sfctr_trainer_train(self._h, step, d_labels, d_loss))
 
     def step_device(self, step, d_features, d_labels, d_window=None, d_loss=None):
         _check(lib().sfctr_trainer_step_device(self._h, step, d_features, d_labels, d_window,

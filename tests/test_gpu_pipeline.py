@@ -161,3 +161,40 @@ def test_submit_protocol_errors():
         tr.loss(5)
     assert np.isfinite(tr.loss(0)) and np.isfinite(tr.loss(1))
     tr.close()
+
+
+def test_prepare_train_split_matches_step():
+    """sfctr_trainer_prepare + sfctr_trainer_train (the Host-Manager / GPU-Worker stages)
+    give the same run as sfctr_trainer_step_device, and misuse is a LogicError."""
+    import torch
+    cfg = sb.Config(num_workers=1, batch_size_per_worker=64, num_fields=8, embedding_dim=8,
+                    vocabulary_size=5000, cache_capacity=700, hidden_dim=16, zipf_exponent=1.1)
+    cfg.apply("mode", "pipelined")
+    batches = _batches(cfg, 8)
+    feats = [torch.from_numpy(f.view(np.int64)).cuda() for f, _, _ in batches]
+    labs = [torch.from_numpy(y).cuda() for _, y, _ in batches]
+    outs = []
+    for split in (False, True):
+        tr = sb.Trainer(cfg)
+        loss = torch.zeros(len(batches), dtype=torch.float32, device="cuda")
+        for t in range(len(batches)):
+            lp = loss[t:t + 1].data_ptr()
+            if split:
+                tr.prepare_device(t, feats[t].data_ptr())
+                tr.train_device(t, labs[t].data_ptr(), lp)
+            else:
+                tr.step_device(t, feats[t].data_ptr(), labs[t].data_ptr(), None, lp)
+        tr.synchronize()
+        outs.append((loss.cpu().numpy(), tr.snapshot(), tr.ledger(), tr.cache_slots(0)))
+        if split:
+            tr.prepare_device(len(batches), feats[0].data_ptr())
+            with pytest.raises(sb.LogicError):  # prepared but not trained
+                tr.prepare_device(len(batches) + 1, feats[1].data_ptr())
+            with pytest.raises(sb.LogicError):  # train of a step that was not prepared
+                tr.train_device(len(batches) + 5, labs[0].data_ptr())
+        tr.close()
+    (l0, s0, g0, c0), (l1, s1, g1, c1) = outs
+    assert np.allclose(l0, l1, rtol=1e-6)
+    assert g0 == g1 and all(np.array_equal(a, b) for a, b in zip(c0, c1))
+    assert np.array_equal(s0[0], s1[0]) and np.array_equal(s0[2], s1[2])
+    check_rows_close(s1[1], s0[1].astype(np.float64), s1[2], cfg.embedding_dim, cfg.learning_rate)
