@@ -29,10 +29,11 @@ struct CacheLane {
   uint64_t host_cap = 0;
   int64_t umax = 0;     // max uniques per step (scratch sizing)
 
-  // CacheBuffer slots (cache_buffer.hpp:42-50), structure of arrays
-  float* emb = nullptr;        // [C*d]
-  float* mom = nullptr;        // [C*d]
-  float* vel = nullptr;        // [C*d]
+  // CacheBuffer slots (cache_buffer.hpp:42-50): the ParamEntry state of slot s is the
+  // contiguous row [emb | m | v] at emb + 3d*s (mom = emb + d, vel = emb + 2d: same stride)
+  float* emb = nullptr;        // [C x 3d] allocation
+  float* mom = nullptr;        // = emb + d
+  float* vel = nullptr;        // = emb + 2d
   int32_t* steps = nullptr;    // [C]  ParamEntry::adam_steps
   uint32_t* slot_feat = nullptr;  // [C] feature, kEmpty when free
   int32_t* last_use = nullptr;    // [C]

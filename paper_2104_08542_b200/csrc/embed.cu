@@ -25,7 +25,7 @@ __global__ void gather_cache_v4(const uint32_t* __restrict__ own_k,
     const int64_t j = i / d4;
     const int c = static_cast<int>(i - j * d4);
     const int64_t g = static_cast<int64_t>(own_k[j]) * d4 + c;
-    G[g] = emb[static_cast<int64_t>(own_slot[j]) * d4 + c];
+    G[g] = emb[static_cast<int64_t>(own_slot[j]) * 3 * d4 + c];  // cache rows: [emb | m | v]
     if (dG_zero) dG_zero[g] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (B_zero && c == 0) B_zero[own_k[j]] = 0.f;
   }
@@ -51,7 +51,7 @@ __global__ void gather_cache_s(const uint32_t* __restrict__ own_k,
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t j = i / d;
     const int c = static_cast<int>(i - j * d);
-    G[static_cast<int64_t>(own_k[j]) * d + c] = emb[static_cast<int64_t>(own_slot[j]) * d + c];
+    G[static_cast<int64_t>(own_k[j]) * d + c] = emb[static_cast<int64_t>(own_slot[j]) * 3 * d + c];
   }
 }
 
@@ -66,7 +66,8 @@ __global__ void gather_cache_s(const uint32_t* __restrict__ own_k,
 __global__ void __launch_bounds__(256, 4) gather_instances_v4(
     const uint32_t* __restrict__ vid, int32_t rows, int F, int d4, const float4* __restrict__ G,
     float4* __restrict__ X, float4* __restrict__ fm_s, float* __restrict__ fm_sqp,
-    const uint32_t* __restrict__ slot_of) {
+    const uint32_t* __restrict__ slot_of, int g4) {
+  // g4: row stride of G in float4 (d/4 for a common table, 3d/4 for the cache rows)
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const int64_t p = i >> 1;
   const int h = static_cast<int>(i & 1);
@@ -91,7 +92,7 @@ __global__ void __launch_bounds__(256, 4) gather_instances_v4(
       }
       float4 a[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) a[u] = __ldg(G + static_cast<int64_t>(v[u]) * d4 + c);
+      for (int u = 0; u < 8; ++u) a[u] = __ldg(G + static_cast<int64_t>(v[u]) * g4 + c);
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         xr[(f + u) * d4] = a[u];
@@ -102,7 +103,7 @@ __global__ void __launch_bounds__(256, 4) gather_instances_v4(
     for (; f < f1; ++f) {
       uint32_t v = __ldg(vr + f);
       if (slot_of) v = __ldg(slot_of + v);
-      const float4 a = __ldg(G + static_cast<int64_t>(v) * d4 + c);
+      const float4 a = __ldg(G + static_cast<int64_t>(v) * g4 + c);
       xr[f * d4] = a;
       s.x += a.x; s.y += a.y; s.z += a.z; s.w += a.w;
       sq += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w;
@@ -238,7 +239,7 @@ __global__ void sparse_adam_kernel(const uint32_t* __restrict__ own_k,
     const uint32_t s = own_slot[j];
     const int t = steps[s] + 1;
     const float g = dG[static_cast<int64_t>(own_k ? own_k[j] : j) * d + c];
-    const int64_t o = static_cast<int64_t>(s) * d + c;
+    const int64_t o = static_cast<int64_t>(s) * 3 * d + c;  // cache rows: [emb | m | v]
     const float m = b1 * mom[o] + omb1 * g;
     const float v = b2 * vel[o] + omb2 * g * g;
     mom[o] = m;
@@ -267,7 +268,7 @@ __global__ void sparse_adam_v4(const uint32_t* __restrict__ own_k,
     const float c1 = __ldg(bc1 + t), c2 = __ldg(bc2 + t);
     const int64_t gr = own_k ? __ldg(own_k + j) : j;
     float4 g = __ldg(dG + gr * d4 + c);
-    const int64_t o = static_cast<int64_t>(s) * d4 + c;
+    const int64_t o = static_cast<int64_t>(s) * 3 * d4 + c;  // cache rows: [emb | m | v]
     float4 m = mom[o], v = vel[o], e = emb[o];
     if (Bsum) {  // deferred FM term of segment_sum: e is the G row of the forward pass
       const float kb = fm_scale * __ldg(Bsum + gr);
@@ -331,14 +332,14 @@ void zero_rows_b(const int32_t* d_n, int32_t n_bound, int d, float* dG, float* B
 
 void gather_instances(const uint32_t* vid, int32_t rows, int F, int d, int ldx, const float* G,
                       float* X, float* fm_s, float* fm_sqp, cudaStream_t s,
-                      const uint32_t* slot_of) {
+                      const uint32_t* slot_of, int g_ld) {
   if (rows <= 0) return;
   SFB_CHECK(!slot_of || (d & 3) == 0, "gather_instances: slot indirection needs d % 4 == 0");
   if ((d & 3) == 0) {
     const int64_t n = static_cast<int64_t>(rows) * (d / 4) * 2;  // two threads per chunk
     gather_instances_v4<<<ceil_div(n, 256), 256, 0, s>>>(
         vid, rows, F, d / 4, reinterpret_cast<const float4*>(G), reinterpret_cast<float4*>(X),
-        reinterpret_cast<float4*>(fm_s), fm_sqp, slot_of);
+        reinterpret_cast<float4*>(fm_s), fm_sqp, slot_of, (g_ld ? g_ld : d) / 4);
   } else {
     const int64_t n = static_cast<int64_t>(rows) * d;
     gather_instances_s<<<ceil_div(n, 256), 256, 0, s>>>(vid, rows, F, d, ldx, G, X, fm_s, fm_sqp);

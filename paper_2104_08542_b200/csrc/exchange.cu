@@ -53,7 +53,7 @@ __global__ void pack_rows_kernel(const uint32_t* __restrict__ own_k,
   if (j >= n_own) return;
   const uint32_t k = own_k[j];
   const uint32_t m = tm[k];
-  const float4* src = emb + static_cast<int64_t>(own_slot[j]) * d4;
+  const float4* src = emb + static_cast<int64_t>(own_slot[j]) * 3 * d4;  // [emb | m | v] rows
   uint32_t soff = 0;
   for (uint32_t w = 0; w < W; ++w) {
     if ((m >> w) & 1u) {
@@ -399,7 +399,7 @@ __global__ void push_rows_p2p_kernel(const uint32_t* __restrict__ own_k,
   // persistent warps (grid-stride) so the per-CTA fence below is paid once
   for (int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < n_own; j += nwarps) {
     const uint32_t m = tm[own_k[j]];
-    const float4* src = emb + static_cast<int64_t>(own_slot[j]) * d4;
+    const float4* src = emb + static_cast<int64_t>(own_slot[j]) * 3 * d4;  // [emb | m | v] rows
     for (uint32_t w = 0; w < W; ++w) {
       if (!((m >> w) & 1u)) continue;
       float4* dst = pr.E[w] + static_cast<int64_t>(pr.e_off[w] + sscan[j].c[w]) * d4;
@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(256) push_rows_p2p_dev_kernel(
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       m[u] = ok[u] ? __ldg(tm + __ldg(own_k + j[u])) : 0u;
-      v[u] = ok[u] ? __ldg(emb + static_cast<int64_t>(__ldg(own_slot + j[u])) * d4 + c[u])
+      v[u] = ok[u] ? __ldg(emb + static_cast<int64_t>(__ldg(own_slot + j[u])) * 3 * d4 + c[u])
                    : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
@@ -647,7 +647,7 @@ __global__ void __launch_bounds__(256) owner_reduce_dev_kernel(
         const uint32_t s = __ldg(a.own_slot + j[u]);
         const int t = __ldg(a.steps + s) + 1;
         const float c1 = __ldg(a.bc1 + t), c2 = __ldg(a.bc2 + t);
-        const int64_t o = static_cast<int64_t>(s) * d4 + c[u];
+        const int64_t o = static_cast<int64_t>(s) * 3 * d4 + c[u];  // [emb | m | v] rows
         float4 mm = a.mom[o], vv = a.vel[o], e = a.emb[o];
 #define SFB_ADAM(X)                                   \
   mm.X = a.b1 * mm.X + a.omb1 * acc.X;                \

@@ -19,7 +19,7 @@ void gather_cache(const uint32_t* own_k, const uint32_t* own_slot, int32_t n_own
 // slot_of[k] (one worker: no separate G copy)
 void gather_instances(const uint32_t* vid, int32_t rows, int F, int d, int ldx, const float* G,
                       float* X, float* fm_s, float* fm_sqp, cudaStream_t s,
-                      const uint32_t* slot_of = nullptr);
+                      const uint32_t* slot_of = nullptr, int g_ld = 0);  // g_ld: G row stride (0 = d)
 // dG[0 : n*d) = 0 and B[0 : n) = 0 with n = *d_n (bounded by n_bound)
 void zero_rows_b(const int32_t* d_n, int32_t n_bound, int d, float* dG, float* B, cudaStream_t s);
 int fm_sq_parts(int d);  // columns of fm_sqp per row

@@ -748,7 +748,8 @@ void Trainer::train(int64_t step, const uint8_t* d_labels, float* d_loss) {
       continue;
     }
     gather_instances(vid, b_, F_, d_, ldx_, direct_emb ? lane_[0].emb : d_G_, d_X_, d_fm_s_,
-                     d_fm_sqp_, s, direct_emb ? lane_[0].own_slot : remap);
+                     d_fm_sqp_, s, direct_emb ? lane_[0].own_slot : remap,
+                     direct_emb ? 3 * d_ : d_);  // cache rows are [emb | m | v]
     phase("gather_instances", s);
     const DxScatter sc{vid, remap, d_fm_s_, tower_.gz, d_dG_, d_B_, F_, d_};
     if (tower_simt_)
@@ -1085,19 +1086,15 @@ int64_t Trainer::snapshot(uint64_t* features, float* rows, int64_t* steps) {
   }
   if (!features) return static_cast<int64_t>(all.size());
   const int d3 = 3 * d_;
-  std::vector<std::vector<float>> ce(lanes_), cm(lanes_), cv(lanes_);
+  std::vector<std::vector<float>> ce(lanes_);
   std::vector<std::vector<int32_t>> cs(lanes_);
   if (rows || steps)
     for (int l = 0; l < lanes_; ++l) {
       const CacheLane& L = lane_[l];
-      const size_t cd = static_cast<size_t>(L.C) * d_;
+      const size_t cd = static_cast<size_t>(L.C) * d_ * 3;  // [emb | m | v] per slot
       ce[l].resize(cd);
-      cm[l].resize(cd);
-      cv[l].resize(cd);
       cs[l].resize(L.C);
       CUDA_CHECK(cudaMemcpy(ce[l].data(), L.emb, sizeof(float) * cd, cudaMemcpyDeviceToHost));
-      CUDA_CHECK(cudaMemcpy(cm[l].data(), L.mom, sizeof(float) * cd, cudaMemcpyDeviceToHost));
-      CUDA_CHECK(cudaMemcpy(cv[l].data(), L.vel, sizeof(float) * cd, cudaMemcpyDeviceToHost));
       CUDA_CHECK(cudaMemcpy(cs[l].data(), L.steps, sizeof(int32_t) * L.C, cudaMemcpyDeviceToHost));
     }
   int64_t i = 0;
@@ -1109,10 +1106,8 @@ int64_t Trainer::snapshot(uint64_t* features, float* rows, int64_t* steps) {
       if (src.where == kOnHost) {
         std::memcpy(o, L.host_rows + src.r * d3, sizeof(float) * d3);
       } else {
-        const size_t so = static_cast<size_t>(src.where) * d_;
-        std::memcpy(o, ce[src.lane].data() + so, sizeof(float) * d_);
-        std::memcpy(o + d_, cm[src.lane].data() + so, sizeof(float) * d_);
-        std::memcpy(o + 2 * d_, cv[src.lane].data() + so, sizeof(float) * d_);
+        std::memcpy(o, ce[src.lane].data() + static_cast<size_t>(src.where) * d3,
+                    sizeof(float) * d3);
       }
     }
     if (steps) steps[i] = src.where == kOnHost ? L.host_steps[src.r] : cs[src.lane][src.where];
