@@ -112,6 +112,11 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
     mcomm_ = comm_;
     if (pipelined_) NCCL_CHECK(ncclCommSplit(comm_, 0, rank_, &mcomm_, nullptr));
     CUDA_CHECK(cudaStreamCreateWithFlags(&dstream_, cudaStreamNonBlocking));
+    const char* ni = std::getenv("SFCTR_NCCL_IDS");  // debugging: NCCL id all-gather
+    if (!(ni && ni[0] == '1')) {
+      idg_.init(world_, rank_, n_local_);
+      if (!idg_.setup_p2p(comm_, stream_)) idg_.release();
+    }
     CUDA_CHECK(cudaEventCreateWithFlags(&dense_ready_, cudaEventDisableTiming));
     CUDA_CHECK(cudaEventCreateWithFlags(&dense_done_, cudaEventDisableTiming));
   }
@@ -256,6 +261,7 @@ Trainer::~Trainer() {
   if (h_loss_ring_) cudaFreeHost(h_loss_ring_);
   for (auto e : ev_) cudaEventDestroy(e);
   if (dstream_) cudaStreamSynchronize(dstream_);
+  idg_.release();
   for (cudaEvent_t e : {dense_ready_, dense_done_})
     if (e) cudaEventDestroy(e);
   if (dstream_) cudaStreamDestroy(dstream_);
@@ -480,12 +486,17 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
   // [1] (bad-id flag) is sticky until a host check has seen it
   CUDA_CHECK(cudaMemsetAsync(d_scalars_, 0, sizeof(int32_t), sm));
   CUDA_CHECK(cudaMemsetAsync(d_scalars_ + 2, 0, sizeof(int32_t) * 6, sm));
-  ids_to_u32(d_features, d_ids32_, n_local_, cfg_.vocabulary_size, d_scalars_ + 1, sm);
   const uint32_t* gids = d_ids32_;
-  if (world_ > 1) {
-    NCCL_CHECK(ncclAllGather(d_ids32_, d_gids_, static_cast<size_t>(n_local_), ncclUint32, mcomm_, sm));
-    gids = d_gids_;
+  if (world_ > 1 && idg_.p2p) {  // u64 -> u32 + peer stores into every rank's buffer
+    gids = idg_.gather(d_features, cfg_.vocabulary_size, d_scalars_ + 1, k, sm);
     stats_.nvlink_bytes += n_local_ * 4;
+  } else {
+    ids_to_u32(d_features, d_ids32_, n_local_, cfg_.vocabulary_size, d_scalars_ + 1, sm);
+    if (world_ > 1) {
+      NCCL_CHECK(ncclAllGather(d_ids32_, d_gids_, static_cast<size_t>(n_local_), ncclUint32, mcomm_, sm));
+      gids = d_gids_;
+      stats_.nvlink_bytes += n_local_ * 4;
+    }
   }
   phase("ids_allgather", sm);
   vsi_device(vsi_, gids, n_global_, d_uniq_, d_vid_, d_scalars_ + 0, sm, /*reset=*/false);

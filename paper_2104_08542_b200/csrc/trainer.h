@@ -9,6 +9,7 @@
 #include "../../include/sfctr_b200.h"
 #include "cache.h"
 #include "exchange.h"
+#include "idgather.h"
 #include "kernels.h"
 
 namespace sfb {
@@ -98,6 +99,7 @@ class Trainer {
   bool no_free_steps_ = false;  // experiment switch: every step waits for the exact counts
   cudaStream_t mstream_ = nullptr;
   ncclComm_t mcomm_ = nullptr;       // manager-stage communicator (id all-gather)
+  IdGather idg_;                     // NVLink peer-store id all-gather (world > 1)
   cudaStream_t dstream_ = nullptr;   // dense-gradient all-reduce, overlapping the row exchange
   cudaEvent_t dense_ready_ = nullptr, dense_done_ = nullptr;
   cudaEvent_t prep_done_[2] = {}, train_done_[2] = {};
