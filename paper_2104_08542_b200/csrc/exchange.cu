@@ -18,19 +18,17 @@ namespace sfb {
 namespace {
 
 // tm[vid[i]] |= 1 << worker(i); warp peers with the same vid pre-combine
+// bit w of tm[v] = worker w (positions [w * per_worker, (w + 1) * per_worker)) touches
+// unique v. The word is read first and the atomic skipped when the bit is already set: hot
+// ids (low unique ratios) are seen by most warps, and a plain read is far cheaper than
+// either a contended atomic or a warp-wide __match_any_sync pre-dedup.
 __global__ void touch_mask_kernel(const uint32_t* __restrict__ vid, int64_t n, int64_t per_worker,
                                   uint32_t* __restrict__ tm) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  const bool valid = i < n;
-  const uint32_t v = valid ? vid[i] : 0xFFFFFFFFu;
-  const unsigned active = __ballot_sync(0xFFFFFFFFu, valid);
-  if (!valid) return;
+  if (i >= n) return;
+  const uint32_t v = __ldg(vid + i);
   const uint32_t bit = 1u << static_cast<uint32_t>(i / per_worker);
-  const unsigned peers = __match_any_sync(active, v);
-  const uint32_t bits = __reduce_or_sync(peers, bit);
-  // hot ids: most warps find their bits already set — skip the contended atomic then
-  if ((threadIdx.x & 31) == __ffs(peers) - 1 && (__ldcg(tm + v) & bits) != bits)
-    atomicOr(tm + v, bits);
+  if ((__ldcg(tm + v) & bit) == 0) atomicOr(tm + v, bit);
 }
 
 __global__ void lvid_kernel(const uint32_t* __restrict__ vid, int64_t n,
@@ -307,12 +305,13 @@ __global__ void __launch_bounds__(256) plan_rank_kernel(
 
 void Exchange::plan(const uint32_t* d_vid, int64_t n_global, int64_t per_worker,
                     const uint32_t* d_uniq, const int32_t* d_U, const uint32_t* d_own_k,
-                    const int32_t* d_n_own, cudaStream_t s) {
+                    const int32_t* d_n_own, cudaStream_t s, const PhaseHook& hook) {
   const int c = static_cast<int>(cap);
   const int ntiles = ceil_div(c, kTile);
   CUDA_CHECK(cudaMemsetAsync(tm, 0, sizeof(uint32_t) * cap, s));
   touch_mask_kernel<<<ceil_div(n_global, 256), 256, 0, s>>>(d_vid, n_global, per_worker, tm);
   CUDA_LAUNCH_CHECK();
+  hook("plan_touch");
   // receive plan (y = 0, over the uniques) and send plan (y = 1, over my owned uniques)
   plan_count_kernel<<<dim3(ntiles, 2), 256, 0, s>>>(d_uniq, d_U, d_own_k, d_n_own, c, tm, W, me,
                                                     ntiles, tile_cnt);
@@ -322,6 +321,7 @@ void Exchange::plan(const uint32_t* d_vid, int64_t n_global, int64_t per_worker,
   plan_rank_kernel<<<dim3(ntiles, 2), 256, 0, s>>>(d_uniq, d_U, d_own_k, d_n_own, c, tm, W, me,
                                                    ntiles, tile_off, totals, sscan, lpos);
   CUDA_LAUNCH_CHECK();
+  hook("plan_rank");
   // every peer's layout (peer-store transport)
   CUDA_CHECK(cudaMemsetAsync(totals + 16, 0, sizeof(int32_t) * 64, s));
   count_matrix_kernel<<<std::min(ceil_div(c, 256), 148 * 4), 256, 0, s>>>(d_uniq, d_U, c, tm, W,

@@ -6,7 +6,7 @@
 #include <string>
 #include <vector>
 
-#include "ops.h"
+#include "kernels.h"
 
 namespace sfb {
 
@@ -79,7 +79,8 @@ struct Exchange {
   void barrier(ncclComm_t comm, cudaStream_t s);
   // device-only planning (no host wait); totals land in `totals`
   void plan(const uint32_t* d_vid, int64_t n_global, int64_t per_worker, const uint32_t* d_uniq,
-            const int32_t* d_U, const uint32_t* d_own_k, const int32_t* d_n_own, cudaStream_t s);
+            const int32_t* d_U, const uint32_t* d_own_k, const int32_t* d_n_own, cudaStream_t s,
+            const PhaseHook& hook = PhaseHook{});
   void set_counts(const int32_t* h_totals);  // after the step's host wait
   void local_vids(const uint32_t* d_vid_mine, int64_t n, uint32_t* d_lvid, cudaStream_t s);
   int64_t local_rows() const { return recv_off.empty() ? 0 : recv_off[8]; }

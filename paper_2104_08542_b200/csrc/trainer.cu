@@ -542,8 +542,17 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
   bool free_step = (world_ == 1 || xdev) && !no_free_steps_;
   for (int l = 0; l < lanes_ && free_step; ++l) free_step = free_lb_[l] >= bound;
   if (a2a_) {  // exchange plan (touched masks, send/receive positions), device only
+    struct HookCtx {
+      Trainer* tr;
+      cudaStream_t s;
+    } hc{this, sm};
     xch_.plan(d_vid_, n_global_, static_cast<int64_t>(b_) * F_, d_uniq_, d_scalars_ + 0,
-              lane_[0].own_k, lane_[0].counters + kCntOwned, sm);
+              lane_[0].own_k, lane_[0].counters + kCntOwned, sm,
+              PhaseHook{[](void* c, const char* n) {
+                          auto* h = static_cast<HookCtx*>(c);
+                          h->tr->phase(n, h->s);
+                        },
+                        &hc});
     if (!free_step)
       CUDA_CHECK(cudaMemcpyAsync(h_totals_, xch_.totals, sizeof(int32_t) * Exchange::kTotals,
                                  cudaMemcpyDeviceToHost, sm));

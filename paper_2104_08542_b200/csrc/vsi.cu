@@ -5,8 +5,7 @@
 // A sort-unique would give sorted order, so the kernels use the
 // min-position formulation instead (SURVEY §7 hard part (i)):
 //   1. first[f] = min position of f    (direct-mapped table over the
-//      vocabulary in HBM; warp __match_any_sync pre-dedup so only one lane per
-//      distinct id in a warp issues the atomicMin)
+//      vocabulary in HBM; read-before-atomicMin skips the contended atomics)
 //   2. flag[i]  = (first[f_i] == i)    (i is a first appearance; evaluated inside
 //   3. rank     = exclusive scan(flag)  the CUB scan; U = rank[n-1] + flag[n-1])
 //   4. global_ids[rank[i]] = f_i for flagged i;  vid[i] = rank[first[f_i]]
@@ -32,20 +31,17 @@ __global__ void fill_u32_kernel(uint32_t* p, int64_t n, uint32_t v) {
     p[i] = v;
 }
 
+// first[f] = min position of f. Consecutive positions of a warp are consecutive fields of
+// one row (disjoint vocabulary shards), so a warp rarely holds one id twice and a
+// __match_any_sync pre-dedup costs more than it saves; instead the word is read first and
+// the atomic skipped when an earlier position is already recorded (first[] only decreases),
+// which removes the contended atomics on hot ids.
 __global__ void vsi_first_kernel(const uint32_t* __restrict__ ids, int64_t n,
                                  uint32_t* __restrict__ first) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  const bool valid = i < n;
-  const uint32_t f = valid ? ids[i] : 0xFFFFFFFFu;
-  const unsigned active = __ballot_sync(0xFFFFFFFFu, valid);
-  if (!valid) return;
-  // lanes holding the same id; positions grow with the lane index, so the
-  // lowest peer holds the warp-local first appearance
-  const unsigned peers = __match_any_sync(active, f);
-  // hot ids (low unique ratios) hit the same word from many warps: skip the atomic when an
-  // earlier position is already recorded (first[] only ever decreases)
-  if ((threadIdx.x & 31) == __ffs(peers) - 1 && __ldcg(first + f) > static_cast<uint32_t>(i))
-    atomicMin(first + f, static_cast<uint32_t>(i));
+  if (i >= n) return;
+  const uint32_t f = __ldg(ids + i);
+  if (__ldcg(first + f) > static_cast<uint32_t>(i)) atomicMin(first + f, static_cast<uint32_t>(i));
 }
 
 __global__ void vsi_emit_kernel(const uint32_t* __restrict__ ids, int64_t n,
