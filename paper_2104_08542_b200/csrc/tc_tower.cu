@@ -81,7 +81,9 @@ __global__ void prep_w1_kernel(const float* __restrict__ w1, int K, int H, int l
   wt_lo[static_cast<int64_t>(j) * ldk + k] = l;
 }
 
-// Warp per row: sums the split-K partials of GEMM1, then the DeepFM-lite head.
+// Warp per row: sums the split-K partials of GEMM1, then the DeepFM-lite head. sg_part
+// (nullable): each block's 8 rows reduced to (db1 | dw2 | db2 | loss) partials, [block][2H+2]
+// (the first pass of small_grads, fused; H <= 64)
 __global__ void head_tc_kernel(int rows, int H, int d, int sq_parts, const float* __restrict__ part,
                                int splits, long long split_stride, const float* __restrict__ b1,
                                const float* __restrict__ w2, const float* __restrict__ b2p,
@@ -90,10 +92,22 @@ __global__ void head_tc_kernel(int rows, int H, int d, int sq_parts, const float
                                float* __restrict__ logits, float* __restrict__ act,
                                float* __restrict__ dh, float* __restrict__ gz,
                                float* __restrict__ lossr, float* __restrict__ dh_hi,
-                               float* __restrict__ dh_lo, int ldh) {
+                               float* __restrict__ dh_lo, int ldh, float* __restrict__ sg_part) {
+  __shared__ float sg[8][2 * 64 + 2];
   const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (r >= rows) return;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  if (r >= rows) {  // (rows % 8 != 0) this warp's row contributes nothing
+    if (sg_part) {
+      for (int j = lane; j < 2 * H + 2; j += 32) sg[wib][j] = 0.f;
+      __syncthreads();
+      for (int j = threadIdx.x; j < 2 * H + 2; j += blockDim.x) {
+        float t = 0.f;
+        for (int w = 0; w < 8; ++w) t += sg[w][j];
+        sg_part[static_cast<int64_t>(blockIdx.x) * (2 * H + 2) + j] = t;
+      }
+    }
+    return;
+  }
   float mlp = 0.f;
   for (int j = lane; j < H; j += 32) {
     float h = b1[j];
@@ -129,11 +143,28 @@ __global__ void head_tc_kernel(int rows, int H, int d, int sq_parts, const float
     const float h = rna(dv), l = rna(dv - h);
     dh_hi[static_cast<int64_t>(r) * ldh + j] = h;
     dh_lo[static_cast<int64_t>(r) * ldh + j] = l;
+    if (sg_part) {
+      sg[wib][j] = dv;                    // db1
+      sg[wib][H + j] = g * fmaxf(hv, 0.f);  // dw2
+    }
   }
+  const float lr_ = -(y * logf(pc) + (1.f - y) * log1pf(-pc));
   if (lane == 0) {
     logits[r] = z;
     gz[r] = g;
-    lossr[r] = -(y * logf(pc) + (1.f - y) * log1pf(-pc));
+    lossr[r] = lr_;
+    if (sg_part) {
+      sg[wib][2 * H] = g;
+      sg[wib][2 * H + 1] = lr_;
+    }
+  }
+  if (sg_part) {
+    __syncthreads();
+    for (int j = threadIdx.x; j < 2 * H + 2; j += blockDim.x) {  // rows in order
+      float t = 0.f;
+      for (int w = 0; w < 8; ++w) t += sg[w][j];
+      sg_part[static_cast<int64_t>(blockIdx.x) * (2 * H + 2) + j] = t;
+    }
   }
 }
 
@@ -510,7 +541,7 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc_, const float* X, int l
   head_tc_kernel<<<ceil_div(static_cast<int64_t>(rows) * 32, 256), 256, 0, s>>>(
       rows, H, d, fm_sq_parts(d), tc_.part1, s1, static_cast<long long>(rows) * H, b1, w2, b2p,
       fm_s, fm_sqp, labels, 1.f / rows, logits, t.act, t.dh, t.gz, t.lossr, tc_.dh_hi, tc_.dh_lo,
-      tc_.ldh);
+      tc_.ldh, H <= 64 ? t.sg_part : nullptr);
   CUDA_LAUNCH_CHECK();
   hook("tower_head");
   // ---- GEMM2: dX = scale dh W1^T (A = dh hi/lo, B = W1 hi/lo, both K-major; the FM
@@ -567,7 +598,10 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc_, const float* X, int l
   hook("tower_gemm3");
   const int64_t kh = static_cast<int64_t>(K) * H;
   dw1_reduce(tc_.part3, s3, kh, g_w1, accumulate, s);
-  small_grads(t, rows, H, g_b1, g_w2, g_b2, g_loss, accumulate, s);
+  if (H <= 64)  // the head left per-block partials: only the final pass remains
+    small_grads_final(t, ceil_div(rows, 8), rows, H, g_b1, g_w2, g_b2, g_loss, accumulate, s);
+  else
+    small_grads(t, rows, H, g_b1, g_w2, g_b2, g_loss, accumulate, s);
 }
 
 void tower_forward_backward_fused(TowerBufs& t, TowerTC& tc_, const float* G, int64_t g_rows,

@@ -298,7 +298,8 @@ void TowerBufs::init(int rc, int k, int h, int dim) {
   const int kt = ceil_div(K, TB), ht = ceil_div(H, TB);
   splits = std::max(1, std::min(ceil_div(rc, BK), (2 * 148 + kt * ht - 1) / (kt * ht)));
   CUDA_CHECK(cudaMalloc(&part, sizeof(float) * static_cast<size_t>(splits) * K * H));
-  CUDA_CHECK(cudaMalloc(&sg_part, sizeof(float) * 256 * (2 * h + 2)));  // kSgChunks rows
+  // kSgChunks chunks, or one per 8 rows when the tensor-core head writes them
+  CUDA_CHECK(cudaMalloc(&sg_part, sizeof(float) * std::max(256, (rows_cap + 7) / 8) * (2 * h + 2)));
 }
 
 void TowerBufs::release() {
@@ -385,6 +386,13 @@ __global__ void small_grads_p2(const float* __restrict__ part, int chunks, int H
   *dst = accumulate ? *dst + s : s;
 }
 }  // namespace
+
+void small_grads_final(TowerBufs& t, int chunks, int rows, int H, float* g_b1, float* g_w2,
+                       float* g_b2, float* g_loss, bool accumulate, cudaStream_t s) {
+  small_grads_p2<<<ceil_div(2 * H + 2, 8), 256, 0, s>>>(t.sg_part, chunks, H, 1.f / rows, g_b1,
+                                                         g_w2, g_b2, g_loss, accumulate ? 1 : 0);
+  CUDA_LAUNCH_CHECK();
+}
 
 void small_grads(TowerBufs& t, int rows, int H, float* g_b1, float* g_w2, float* g_b2,
                  float* g_loss, bool accumulate, cudaStream_t s) {
