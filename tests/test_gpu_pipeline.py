@@ -198,3 +198,46 @@ def test_prepare_train_split_matches_step():
     assert g0 == g1 and all(np.array_equal(a, b) for a, b in zip(c0, c1))
     assert np.array_equal(s0[0], s1[0]) and np.array_equal(s0[2], s1[2])
     check_rows_close(s1[1], s0[1].astype(np.float64), s1[2], cfg.embedding_dim, cfg.learning_rate)
+
+
+@pytest.mark.parametrize("lanes,slack", [(1, 8), (1, 200), (4, 4), (4, 60)])
+def test_pipelined_long_run_stress(lanes, slack):
+    """40 pipelined steps with steady evictions (and pinned waits when the cache is tight):
+    every step's slot table stays bit-exact with the oracle's — a cross-stream race in the
+    double-buffered state would show up as a diverging slot table or ledger."""
+    cfg = sb.Config(num_workers=lanes, batch_size_per_worker=256 // lanes, num_fields=6,
+                    embedding_dim=8, vocabulary_size=8000, cache_capacity=1, hidden_dim=16,
+                    zipf_exponent=0.9)
+    cfg.apply("mode", "pipelined")
+    batches = _batches(cfg, 40)
+    owned = max(int(np.sum(oracle_vsi(f, 256, 6)[0] % lanes == w))
+                for f, _, _ in batches for w in range(lanes))
+    cap = owned + slack  # tight: evictions reach into the previous (in-flight) batch's rows
+    cfg.cache_capacity = cap
+    O, sim, ol = _oracle(cfg, batches)
+    tr = sb.Trainer(cfg)
+    losses = []
+    for t, (f, y, w) in enumerate(batches):
+        tr.submit(t, f, y, w)
+        if t > 0:
+            losses.append(tr.loss(t - 1))
+    losses.append(tr.loss(len(batches) - 1))
+    assert np.all(np.abs(np.array(losses) - ol) <= 1e-5 * np.abs(ol))
+    for w in range(lanes):
+        of, olu, oseq = orc_slots(sim, w, cap)
+        df, dlu, dseq = tr.cache_slots(w)
+        assert np.array_equal(df, of)
+        occ = of != np.iinfo(np.uint64).max
+        assert np.array_equal(dlu[occ], olu[occ]) and np.array_equal(dseq[occ], oseq[occ])
+    led = np.zeros(4, np.int64)
+    O.orc_sim_ledger(sim, led)
+    dl = tr.ledger()
+    assert [dl["host_to_worker"], dl["worker_to_host"], dl["interworker"],
+            dl["swap_events"]] == led.tolist()
+    assert dl["swap_events"] > 0
+    of, orows, ost = orc_snapshot(sim, cfg.embedding_dim)
+    df, drows, dst = tr.snapshot()
+    assert np.array_equal(df, of) and np.array_equal(dst, ost)
+    check_rows_close(drows, orows, dst, cfg.embedding_dim, cfg.learning_rate)
+    O.orc_sim_destroy(sim)
+    tr.close()
