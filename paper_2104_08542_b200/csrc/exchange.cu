@@ -13,6 +13,8 @@
 // 0..W-1 in that fixed order (the reference's ordered sum).
 #include "exchange.h"
 
+#include <cstdlib>
+
 namespace sfb {
 
 namespace {
@@ -671,8 +673,12 @@ void Exchange::forward_dev(const uint32_t* d_own_k, const uint32_t* d_own_slot, 
                            const int32_t* d_n_own, const float* emb, cudaStream_t s) {
   PeerRows pr{};
   for (int w = 0; w < W; ++w) pr.E[w] = reinterpret_cast<float4*>(peer_E[w]);
+  static const int fwd_blocks = [] {  // experiment switch: SFCTR_FWD_PUSH_BLOCKS
+    const char* e = std::getenv("SFCTR_FWD_PUSH_BLOCKS");
+    return e ? std::max(1, atoi(e)) : 148 * 2;
+  }();
   push_rows_p2p_dev_kernel<<<std::max(1, std::min(ceil_div(static_cast<int64_t>(n_bound) * (d / 4), 512),
-                                                  148 * 2)),
+                                                  fwd_blocks)),
                              256, 0, s>>>(d_own_k, d_own_slot, d_n_own, tm, sscan, W, me, offs,
                                           reinterpret_cast<const float4*>(emb), d / 4, pr);
   CUDA_LAUNCH_CHECK();
