@@ -304,6 +304,9 @@ __global__ void __launch_bounds__(256) swap_kernel(
     int32_t* __restrict__ last_use, uint64_t* __restrict__ admit_seq,
     int32_t* __restrict__ mark, int32_t t, uint32_t* __restrict__ own_slot,
     int32_t* __restrict__ n_from_host, int32_t* __restrict__ err) {
+  __shared__ __align__(128) float4 wb_stage[8][64];   // per warp: the victim row (<= 64 chunks)
+  __shared__ __align__(128) float4 adm_stage[8][64];  // per warp: the refilled host row
+  __shared__ __align__(8) uint64_t adm_bar[8];
   const int32_t n_work = counters[kCntWorking];
   const int32_t free_top = counters[kCntFreeTop];
   const uint64_t seq0 = *reinterpret_cast<const uint64_t*>(counters + kCntSeq);
@@ -332,11 +335,23 @@ __global__ void __launch_bounds__(256) swap_kernel(
       const int c = lane + 32 * q;
       if (c < per) keep[q] = *src_of(c, emb, mom, vel, so);
     }
-    float4* dst = host_rows + ro * per;
+    // write-back by one TMA bulk store per row (smem -> pinned host row): larger PCIe
+    // writes than 16 B SM stores (microbench/pcie_rows.cu: 48 vs 44.5 GB/s)
+    float4* stage = wb_stage[threadIdx.x >> 5];
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       const int c = lane + 32 * q;
-      if (c < per) dst[c] = keep[q];
+      if (c < per) stage[c] = keep[q];
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                       host_rows + ro * per),
+                   "r"(sa), "r"(per * 16)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
     if (lane == 0) {
       host_steps[ro] = steps[s];
@@ -350,11 +365,33 @@ __global__ void __launch_bounds__(256) swap_kernel(
   const uint64_t r = f / W;
   const size_t so = static_cast<size_t>(s) * 3 * d4;
   if (where == kOnHost) {
-    const float4* src = host_rows + r * per;
+    // refill by one TMA bulk load of the host row (one large PCIe read instead of 16 B SM
+    // loads), completion tracked by the warp's mbarrier
+    const int wid = threadIdx.x >> 5;
+    float4* astage = adm_stage[wid];
+    const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&adm_bar[wid]));
+    if (lane == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                   "r"(per * 16)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              static_cast<uint32_t>(__cvta_generic_to_shared(astage))),
+          "l"(host_rows + r * per), "r"(per * 16), "r"(bar)
+          : "memory");
+    }
+    __syncwarp();
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+        "@!p bra W;\n\t}" ::"r"(bar)
+        : "memory");
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       const int c = lane + 32 * q;
-      if (c < per) *src_of(c, emb, mom, vel, so) = src[c];
+      if (c < per) *src_of(c, emb, mom, vel, so) = astage[c];
     }
   } else {
     const uint64_t se = derive_seed_h(seed, embed_hash, f);  // HostStore::get_or_init
@@ -383,6 +420,8 @@ __global__ void __launch_bounds__(256) swap_kernel(
   }
   const unsigned fh = __ballot_sync(0xFFFFFFFFu, lane == 0 && where == kOnHost);
   if (lane == 0 && fh) atomicAdd(n_from_host, 1);
+  // the staged row must be read (and written) before the warp's shared memory is released
+  if (lane == 0 && i < n_evict) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 __global__ void init_lane_kernel(uint32_t C, uint32_t* slot_feat, int32_t* last_use,
