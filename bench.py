@@ -253,12 +253,17 @@ def run_ours(args, D):
     torch.cuda.synchronize()
     w0 = time.perf_counter()
     losses = []
+    t_sub = t_wait = 0.0
     if args.mode == "pipelined":  # one step in flight: submit step s, then read loss of s-1
         for i in range(K):
             s = W + 2 * K + i
+            a0 = time.perf_counter()
             tr.submit(s, hf[s], hl[s])
+            a1 = time.perf_counter()
             if i > 0:
                 losses.append(tr.loss(s - 1))
+            t_sub += a1 - a0
+            t_wait += time.perf_counter() - a1
         losses.append(tr.loss(W + 3 * K - 1))
     else:
         for i in range(K):
@@ -370,6 +375,8 @@ def run_ours(args, D):
                    "l2": "no flush: per-step working set > L2 (X alone is 102 MB/GPU)",
                    "setup_s": round(setup_s, 2)},
         "e2e": {"value": round(e2e_value, 1), "unit": "samples/s",
+                "host_submit_ms_per_step": round(t_sub * 1e3 / K, 4),
+                "host_loss_wait_ms_per_step": round(t_wait * 1e3 / K, 4),
                 "h2d_bytes_per_step": int(nrows * F * 8 + nrows),
                 "d2h_bytes_per_step": 4},
         "gpu_launches": int(launches),
