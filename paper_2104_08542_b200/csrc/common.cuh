@@ -95,6 +95,15 @@ __device__ __forceinline__ double uniform_from(uint64_t x, double lo, double hi)
 }
 #endif
 
+#ifdef __CUDACC__
+// a / b for the flat-index kernels: a 32-bit divide (a few instructions) instead of the
+// ~70-instruction 64-bit one whenever the index fits, which it does at every shipped size
+__device__ __forceinline__ int64_t idiv(int64_t a, int b) {
+  return a <= 0xFFFFFFFFll ? static_cast<int64_t>(static_cast<uint32_t>(a) / static_cast<uint32_t>(b))
+                           : a / b;
+}
+#endif
+
 // Slot / index sentinels of the device MixCache.
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;   // slot_feature of a free slot
 constexpr uint32_t kNever = 0xFFFFFFFFu;   // index[r]: row never touched (lazy init on admit)

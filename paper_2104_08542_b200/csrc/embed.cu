@@ -22,7 +22,7 @@ __global__ void gather_cache_v4(const uint32_t* __restrict__ own_k,
   const int64_t n = static_cast<int64_t>(n_own) * d4;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t j = i / d4;
+    const int64_t j = idiv(i, d4);
     const int c = static_cast<int>(i - j * d4);
     const int64_t g = static_cast<int64_t>(own_k[j]) * d4 + c;
     G[g] = emb[static_cast<int64_t>(own_slot[j]) * 3 * d4 + c];  // cache rows: [emb | m | v]
@@ -38,7 +38,8 @@ __global__ void zero_rows_b_kernel(const int32_t* __restrict__ n_ptr, int d4,
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     dG[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (i % d4 == 0) B[i / d4] = 0.f;
+    const int64_t j = idiv(i, d4);
+    if (i == j * d4) B[j] = 0.f;
   }
 }
 
@@ -49,7 +50,7 @@ __global__ void gather_cache_s(const uint32_t* __restrict__ own_k,
   const int64_t n = static_cast<int64_t>(n_own) * d;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t j = i / d;
+    const int64_t j = idiv(i, d);
     const int c = static_cast<int>(i - j * d);
     G[static_cast<int64_t>(own_k[j]) * d + c] = emb[static_cast<int64_t>(own_slot[j]) * 3 * d + c];
   }
@@ -72,7 +73,7 @@ __global__ void __launch_bounds__(256, 4) gather_instances_v4(
   const int64_t p = i >> 1;
   const int h = static_cast<int>(i & 1);
   const bool valid = p < static_cast<int64_t>(rows) * d4;
-  const int64_t r = valid ? p / d4 : 0;
+  const int64_t r = valid ? idiv(p, d4) : 0;
   const int c = static_cast<int>(p - r * d4);
   const int Fh = (F + 1) >> 1;
   const int f0 = h ? Fh : 0, f1 = h ? F : Fh;
@@ -125,7 +126,7 @@ __global__ void gather_instances_s(const uint32_t* __restrict__ vid, int32_t row
                                    float* __restrict__ fm_s, float* __restrict__ fm_sqp) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= static_cast<int64_t>(rows) * d) return;
-  const int64_t r = i / d;
+  const int64_t r = idiv(i, d);
   const int c = static_cast<int>(i - r * d);
   float s = 0.f, sq = 0.f;
   for (int f = 0; f < F; ++f) {
@@ -143,7 +144,7 @@ __global__ void fm_sums_kernel(const float* __restrict__ X, int32_t rows, int F,
   // thread per (row, column c); one partial per column (parts == d here)
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= static_cast<int64_t>(rows) * d) return;
-  const int64_t r = i / d;
+  const int64_t r = idiv(i, d);
   const int c = static_cast<int>(i - r * d);
   float s = 0.f, sq = 0.f;
   for (int f = 0; f < F; ++f) {
@@ -171,9 +172,9 @@ __global__ void segment_sum_v4(const uint32_t* __restrict__ vid, int32_t n, int 
                                float scale, float* __restrict__ dG, float* __restrict__ Bsum) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= static_cast<int64_t>(n) * d4) return;
-  const int64_t p = i / d4;
+  const int64_t p = idiv(i, d4);
   const int c = static_cast<int>(i - p * d4);
-  const int64_t r = p / F;
+  const int64_t r = idiv(p, F);
   const uint32_t v = __ldg(vid + p);
   const float4 a = __ldcs(dX + i);
   const float4 s = __ldg(fm_s + r * d4 + c);
@@ -200,9 +201,9 @@ __global__ void segment_sum_s(const uint32_t* __restrict__ vid, int32_t n, int F
                               float scale, float* __restrict__ dG) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= static_cast<int64_t>(n) * d) return;
-  const int64_t p = i / d;  // position = row * F + field
+  const int64_t p = idiv(i, d);  // position = row * F + field
   const int c = static_cast<int>(i - p * d);
-  const int64_t r = p / F;
+  const int64_t r = idiv(p, F);
   const int f = static_cast<int>(p - r * F);
   const int64_t v = vid[p];
   const float g = dX[r * ldx + f * d + c] + scale * gz[r] * (fm_s[r * d + c] - G[v * d + c]);
@@ -234,7 +235,7 @@ __global__ void sparse_adam_kernel(const uint32_t* __restrict__ own_k,
   const int64_t n = static_cast<int64_t>(n_own) * d;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t j = i / d;
+    const int64_t j = idiv(i, d);
     const int c = static_cast<int>(i - j * d);
     const uint32_t s = own_slot[j];
     const int t = steps[s] + 1;
@@ -261,7 +262,7 @@ __global__ void sparse_adam_v4(const uint32_t* __restrict__ own_k,
   const int64_t n = static_cast<int64_t>(n_own) * d4;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t j = i / d4;
+    const int64_t j = idiv(i, d4);
     const int c = static_cast<int>(i - j * d4);
     const uint32_t s = __ldg(own_slot + j);
     const int t = __ldg(steps + s) + 1;

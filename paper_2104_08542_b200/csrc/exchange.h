@@ -27,6 +27,7 @@ struct Exchange {
   int W = 0, me = 0, d = 0;
   int64_t cap = 0;               // bound on uniques per step
   uint32_t* tm = nullptr;        // [cap] touched-by-worker bitmask per unique
+  uint8_t* tb8 = nullptr;        // [cap x 8] touched bytes (planning scratch, kept zero)
   uint32_t* lpos = nullptr;      // [cap] row in the local table E (or ~0)
   Cnt8* sscan = nullptr;         // [cap] send slot of owned row j for each destination
   uint32_t* tile_cnt = nullptr;  // [tiles x 8] per-tile plane counts (planning scratch)
