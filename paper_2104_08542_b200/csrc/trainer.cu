@@ -150,8 +150,12 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
   }
   const size_t gd = static_cast<size_t>(n_global_) * d_;
   CUDA_CHECK(cudaMalloc(&d_G_, sizeof(float) * gd));
-  CUDA_CHECK(cudaMalloc(&d_dG_, sizeof(float) * gd));
-  CUDA_CHECK(cudaMalloc(&d_B_, sizeof(float) * n_global_));
+  for (int k = 0; k < 2; ++k) {  // per step parity: the manager stage clears the next step's
+    CUDA_CHECK(cudaMalloc(&d_dG_set_[k], sizeof(float) * gd));  // set while this one trains
+    CUDA_CHECK(cudaMalloc(&d_B_set_[k], sizeof(float) * n_global_));
+  }
+  d_dG_ = d_dG_set_[0];
+  d_B_ = d_B_set_[0];
   ldx_ = tower_ldx(K_);
   const size_t bk = static_cast<size_t>(b_) * ldx_;
   CUDA_CHECK(cudaMalloc(&d_X_, sizeof(float) * bk));
@@ -246,14 +250,16 @@ Trainer::~Trainer() {
   for (void* p : {static_cast<void*>(d_ids32_),
                   static_cast<void*>(d_gids_), static_cast<void*>(d_scalars_),
                   static_cast<void*>(d_wuniq_), static_cast<void*>(d_wvid_),
-                  static_cast<void*>(d_G_), static_cast<void*>(d_dG_), static_cast<void*>(d_X_),
+                  static_cast<void*>(d_G_), static_cast<void*>(d_dG_set_[0]),
+                  static_cast<void*>(d_dG_set_[1]), static_cast<void*>(d_B_set_[0]),
+                  static_cast<void*>(d_B_set_[1]), static_cast<void*>(d_X_),
                   static_cast<void*>(d_dX_), static_cast<void*>(d_fm_s_),
                   static_cast<void*>(d_fm_sqp_), static_cast<void*>(d_logits_),
                   static_cast<void*>(d_dense_), static_cast<void*>(d_dense_m_),
                   static_cast<void*>(d_dense_v_), static_cast<void*>(d_grads_),
                   static_cast<void*>(d_bc1_),
                   static_cast<void*>(d_bc2_), static_cast<void*>(d_acc_),
-                  static_cast<void*>(d_B_)})
+                  })
     if (p) cudaFree(p);
   if (h_acc_) cudaFreeHost(h_acc_);
   if (h_scalars_) cudaFreeHost(h_scalars_);
@@ -461,6 +467,8 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
   if (piped && train_pending_[k]) CUDA_CHECK(cudaStreamWaitEvent(sm, train_done_[k]));
   d_uniq_ = d_uniq_set_[k];
   d_vid_ = d_vid_set_[k];
+  d_dG_ = d_dG_set_[k];
+  d_B_ = d_B_set_[k];
   for (auto& L : lane_) L.use(k);
   if (a2a_) xch_.use(k);
   int32_t* snap = d_snap_[k];
@@ -650,6 +658,12 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
     snap_kernel<<<1, 1 + kCntWords * 8, 0, sm>>>(sa);
     CUDA_LAUNCH_CHECK();
   }
+  // Clear this step's gradient table (its parity set) here, off the training stage's path:
+  // one worker clears dG[0 : U) / B, the owner-routed exchange its local rows.
+  if (early_clear_direct())
+    zero_rows_b(snap + 1 + kCntOwned, static_cast<int32_t>(bound), d_, d_dG_, d_B_, sm);
+  else if (xdev)
+    xch_.zero_local_dev(d_dG_, sm, d_ % 4 == 0 && !tower_fused_ ? d_B_ : nullptr);
   phase("manage_evict_admit", sm);
   if (sm != sw) CUDA_CHECK(cudaEventRecord(prep_done_[k], sm));
   prep_.step = step;
@@ -724,14 +738,15 @@ void Trainer::train(int64_t step, const uint8_t* d_labels, float* d_loss) {
       xch_.local_vids(d_vid_ + static_cast<size_t>(lane0_) * b_ * F_, n_local_, d_lvid_, s);
   } else {
     if (world_ > 1) CUDA_CHECK(cudaMemsetAsync(d_G_, 0, sizeof(float) * ud, s));
-    if (direct_emb)  // no G copy: gather_instances reads the cache rows through own_slot
-      zero_rows_b(snap_cnt(0) + kCntOwned, n_own[0], d_, d_dG_, d_B_, s);
-    else
+    // one worker: no G copy (gather_instances reads the cache rows through own_slot) and
+    // dG / B were cleared by the manager stage
+    if (!direct_emb) {
       for (int l = 0; l < lanes_; ++l)
         gather_cache(lane_[l].own_k, lane_[l].own_slot, n_own[l], snap_cnt(l) + kCntOwned,
                      lane_[l].emb, d_, d_G_, zero_in_gather ? d_dG_ : nullptr, s,
                      zero_in_gather ? d_B_ : nullptr);
-    phase(direct_emb ? "zero_grads" : "gather_cache", s);
+      phase("gather_cache", s);
+    }
     if (world_ > 1) {
       NCCL_CHECK(ncclAllReduce(d_G_, d_G_, ud, ncclFloat32, ncclSum, comm_, s));
       stats_.nvlink_bytes += static_cast<int64_t>(ud) * 4;
@@ -745,8 +760,7 @@ void Trainer::train(int64_t step, const uint8_t* d_labels, float* d_loss) {
 
   // ---- per lane: gather_instances, forward_backward, segment_sum (l.11-12)
   if (zero_in_gather) {
-  } else if (xdev) {
-    xch_.zero_local_dev(d_dG_, s, defer_fm ? d_B_ : nullptr);
+  } else if (xdev) {  // cleared by the manager stage
   } else if (free_step && d_ % 4 == 0)
     zero_rows_kernel<<<148 * 8, 256, 0, s>>>(reinterpret_cast<float4*>(d_dG_), snap + 0,
                                              d_ / 4, n_global_ * (d_ / 4));

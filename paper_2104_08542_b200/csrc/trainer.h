@@ -106,6 +106,12 @@ class Trainer {
   bool train_pending_[2] = {false, false};
   int32_t* d_snap_[2] = {};          // [1 + kCntWords * lanes]: U, then every lane's counters
   uint32_t* d_uniq_set_[2] = {};
+  float* d_dG_set_[2] = {};          // gradient tables (dG / the exchange's dE), per parity
+  float* d_B_set_[2] = {};
+  // one worker, fused FM deferral: dG / B are cleared by the manager stage (see train())
+  bool early_clear_direct() const {
+    return W_ == 1 && !a2a_ && d_ % 4 == 0 && !tower_fused_;
+  }
   uint32_t* d_vid_set_[2] = {};
   uint64_t* d_in_feat_set_[2] = {};
   uint8_t* d_in_lab_set_[2] = {};
