@@ -103,7 +103,7 @@ __global__ void head_tc_kernel(int rows, int H, int d, int sq_parts, const float
       for (int j = threadIdx.x; j < 2 * H + 2; j += blockDim.x) {
         float t = 0.f;
         for (int w = 0; w < 8; ++w) t += sg[w][j];
-        sg_part[static_cast<int64_t>(blockIdx.x) * (2 * H + 2) + j] = t;
+        sg_part[static_cast<int64_t>(j) * gridDim.x + blockIdx.x] = t;  // output-major
       }
     }
     return;
@@ -163,7 +163,7 @@ __global__ void head_tc_kernel(int rows, int H, int d, int sq_parts, const float
     for (int j = threadIdx.x; j < 2 * H + 2; j += blockDim.x) {  // rows in order
       float t = 0.f;
       for (int w = 0; w < 8; ++w) t += sg[w][j];
-      sg_part[static_cast<int64_t>(blockIdx.x) * (2 * H + 2) + j] = t;
+      sg_part[static_cast<int64_t>(j) * gridDim.x + blockIdx.x] = t;  // output-major
     }
   }
 }

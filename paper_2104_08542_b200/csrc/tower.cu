@@ -367,17 +367,20 @@ __global__ void small_grads_p1(const float* __restrict__ dh, const float* __rest
     out[2 * H + 1] = red[1][0];
   }
 }
+// out_major: part is [2H+2][chunks] (the tensor-core head's layout, coalesced here), else
+// [chunks][2H+2] (small_grads_p1)
 __global__ void small_grads_p2(const float* __restrict__ part, int chunks, int H, float inv_rows,
                                float* __restrict__ g_db1, float* __restrict__ g_dw2,
                                float* __restrict__ g_db2, float* __restrict__ g_loss,
-                               int accumulate) {
+                               int accumulate, int out_major = 0) {
   // warp per output; lanes take chunks lane, lane+32, ...; fixed shuffle tree (deterministic)
   const int n = 2 * H + 2;
   const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (i >= n) return;
   float s = 0.f;
-  for (int c = lane; c < chunks; c += 32) s += part[static_cast<int64_t>(c) * n + i];
+  for (int c = lane; c < chunks; c += 32)
+    s += out_major ? part[static_cast<int64_t>(i) * chunks + c] : part[static_cast<int64_t>(c) * n + i];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
   if (lane) return;
@@ -390,7 +393,8 @@ __global__ void small_grads_p2(const float* __restrict__ part, int chunks, int H
 void small_grads_final(TowerBufs& t, int chunks, int rows, int H, float* g_b1, float* g_w2,
                        float* g_b2, float* g_loss, bool accumulate, cudaStream_t s) {
   small_grads_p2<<<ceil_div(2 * H + 2, 8), 256, 0, s>>>(t.sg_part, chunks, H, 1.f / rows, g_b1,
-                                                         g_w2, g_b2, g_loss, accumulate ? 1 : 0);
+                                                         g_w2, g_b2, g_loss, accumulate ? 1 : 0,
+                                                         /*out_major=*/1);
   CUDA_LAUNCH_CHECK();
 }
 
