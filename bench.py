@@ -254,17 +254,18 @@ def run_ours(args, D):
     w0 = time.perf_counter()
     losses = []
     t_sub = t_wait = 0.0
-    if args.mode == "pipelined":  # one step in flight: submit step s, then read loss of s-1
+    if args.mode == "pipelined":  # two steps in flight: submit step s, read the loss of s-2
         for i in range(K):
             s = W + 2 * K + i
             a0 = time.perf_counter()
             tr.submit(s, hf[s], hl[s])
             a1 = time.perf_counter()
-            if i > 0:
-                losses.append(tr.loss(s - 1))
+            if i > 1:
+                losses.append(tr.loss(s - 2))
             t_sub += a1 - a0
             t_wait += time.perf_counter() - a1
-        losses.append(tr.loss(W + 3 * K - 1))
+        for s in range(W + 3 * K - min(2, K), W + 3 * K):
+            losses.append(tr.loss(s))
     else:
         for i in range(K):
             s = W + 2 * K + i

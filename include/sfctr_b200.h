@@ -208,8 +208,8 @@ int sfctr_trainer_train(sfctr_trainer* t, int64_t step, const uint8_t* d_labels,
 /* The host-buffer step split in two, for a driver that keeps one step in flight
  * (pipelined mode overlaps the manager stage of step t+1 with step t's training):
  * submit enqueues the H2D copies of the inputs, the step and the D2H copy of its loss,
- * and returns; loss waits for that step's loss. At most two submitted steps may be
- * outstanding: read the loss of step t before submitting step t+2 (else LOGIC). The
+ * and returns; loss waits for that step's loss. At most four submitted steps may be
+ * outstanding: read the loss of step t before submitting step t+4 (else LOGIC). The
  * host input buffers must stay untouched until the step's loss has been read. */
 int sfctr_trainer_submit(sfctr_trainer* t, int64_t step, const uint64_t* features,
                          const uint8_t* labels, const uint64_t* window_features);

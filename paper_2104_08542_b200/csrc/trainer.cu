@@ -136,7 +136,7 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
     CUDA_CHECK(cudaMalloc(&d_loss_set_[k], sizeof(float)));
     CUDA_CHECK(cudaEventCreateWithFlags(&prep_done_[k], cudaEventDisableTiming));
     CUDA_CHECK(cudaEventCreateWithFlags(&train_done_[k], cudaEventDisableTiming));
-    CUDA_CHECK(cudaEventCreateWithFlags(&loss_ev_[k], cudaEventDisableTiming));
+
   }
   d_uniq_ = d_uniq_set_[0];
   d_vid_ = d_vid_set_[0];
@@ -184,7 +184,9 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
   CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_scalars_), sizeof(int32_t) * 8, 0));
   CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_counts_),
                            sizeof(int32_t) * kCntWords * lanes_, 0));
-  CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_loss_ring_), sizeof(float) * 2, 0));
+  CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_loss_ring_), sizeof(float) * kLossRing, 0));
+  for (int q = 0; q < kLossRing; ++q)
+    CUDA_CHECK(cudaEventCreateWithFlags(&loss_ev_[q], cudaEventDisableTiming));
   CUDA_CHECK(cudaMalloc(&d_acc_, sizeof(int64_t) * 8));
   CUDA_CHECK(cudaMemset(d_acc_, 0, sizeof(int64_t) * 8));
   CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_acc_), sizeof(int64_t) * 8, 0));
@@ -244,7 +246,7 @@ Trainer::~Trainer() {
                     static_cast<void*>(d_vid_set_[k]), static_cast<void*>(d_snap_[k]),
                     static_cast<void*>(d_loss_set_[k])})
       if (p) cudaFree(p);
-    for (cudaEvent_t e : {prep_done_[k], train_done_[k], loss_ev_[k]})
+    for (cudaEvent_t e : {prep_done_[k], train_done_[k]})
       if (e) cudaEventDestroy(e);
   }
   for (void* p : {static_cast<void*>(d_ids32_),
@@ -265,6 +267,8 @@ Trainer::~Trainer() {
   if (h_scalars_) cudaFreeHost(h_scalars_);
   if (h_counts_) cudaFreeHost(h_counts_);
   if (h_loss_ring_) cudaFreeHost(h_loss_ring_);
+  for (cudaEvent_t e : loss_ev_)
+    if (e) cudaEventDestroy(e);
   for (auto e : ev_) cudaEventDestroy(e);
   if (dstream_) cudaStreamSynchronize(dstream_);
   idg_.release();
@@ -986,8 +990,9 @@ void Trainer::submit_host(int64_t step, const uint64_t* features, const uint8_t*
                           const uint64_t* window) {
   CUDA_CHECK(cudaSetDevice(dev_));
   const int k = static_cast<int>(step & 1);
-  if (loss_step_[k] >= 0 && loss_step_[k] != step)
-    fail(kLogic, "read the loss of step " + std::to_string(loss_step_[k]) +
+  const int q = static_cast<int>(step % kLossRing);  // loss slot
+  if (loss_step_[q] >= 0 && loss_step_[q] != step)
+    fail(kLogic, "read the loss of step " + std::to_string(loss_step_[q]) +
                      " (loss_of) before submitting step " + std::to_string(step));
   // the staging set was last read by step t-2: the manager stream waits for it below
   // (step_device), so the copies go on the manager stream after that wait
@@ -1003,21 +1008,21 @@ void Trainer::submit_host(int64_t step, const uint64_t* features, const uint8_t*
                                cudaMemcpyHostToDevice, sm));
   step_device(step, d_in_feat_set_[k], d_in_lab_set_[k], window ? d_in_win_set_[k] : nullptr,
               d_loss_set_[k]);
-  CUDA_CHECK(cudaMemcpyAsync(h_loss_ring_ + k, d_loss_set_[k], sizeof(float),
+  CUDA_CHECK(cudaMemcpyAsync(h_loss_ring_ + q, d_loss_set_[k], sizeof(float),
                              cudaMemcpyDeviceToHost, stream_));
-  CUDA_CHECK(cudaEventRecord(loss_ev_[k], stream_));
-  loss_step_[k] = step;
+  CUDA_CHECK(cudaEventRecord(loss_ev_[q], stream_));
+  loss_step_[q] = step;
 }
 
 double Trainer::loss_of(int64_t step) {
   CUDA_CHECK(cudaSetDevice(dev_));
-  const int k = static_cast<int>(step & 1);
-  if (loss_step_[k] != step)
+  const int q = static_cast<int>(step % kLossRing);
+  if (loss_step_[q] != step)
     fail(kLogic, "no outstanding step " + std::to_string(step) + " (submit it first)");
-  CUDA_CHECK(cudaEventSynchronize(loss_ev_[k]));
-  loss_step_[k] = -1;
+  CUDA_CHECK(cudaEventSynchronize(loss_ev_[q]));
+  loss_step_[q] = -1;
   check_device_errors(step);
-  return static_cast<double>(h_loss_ring_[k]);
+  return static_cast<double>(h_loss_ring_[q]);
 }
 
 double Trainer::step_host(int64_t step, const uint64_t* features, const uint8_t* labels,

@@ -32,8 +32,8 @@ class Trainer {
   double step_host(int64_t step, const uint64_t* features, const uint8_t* labels,
                    const uint64_t* window);
   // the same split in two: submit_host enqueues the H2D copies, the step and the D2H copy
-  // of its loss and returns; loss_of(step) waits for that loss. At most two submitted
-  // steps are outstanding (the loss of step t must be read before step t+2 is submitted).
+  // of its loss and returns; loss_of(step) waits for that loss. At most four submitted
+  // steps are outstanding (the loss of step t must be read before step t+4 is submitted).
   void submit_host(int64_t step, const uint64_t* features, const uint8_t* labels,
                    const uint64_t* window);
   double loss_of(int64_t step);
@@ -117,9 +117,12 @@ class Trainer {
   uint8_t* d_in_lab_set_[2] = {};
   uint64_t* d_in_win_set_[2] = {};
   float* d_loss_set_[2] = {};
-  float* h_loss_ring_ = nullptr;     // pinned [2]
-  cudaEvent_t loss_ev_[2] = {};
-  int64_t loss_step_[2] = {-1, -1};
+  // losses of submitted steps (slot = step % kLossRing): the host may run up to kLossRing
+  // steps ahead of the loss it reads; the device-side parity sets are ordered by events
+  static constexpr int kLossRing = 4;
+  float* h_loss_ring_ = nullptr;     // pinned [kLossRing]
+  cudaEvent_t loss_ev_[kLossRing] = {};
+  int64_t loss_step_[kLossRing] = {-1, -1, -1, -1};
 
   VsiScratch vsi_;
   uint32_t* d_ids32_ = nullptr;     // local ids, u32

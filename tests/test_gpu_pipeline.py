@@ -36,12 +36,13 @@ def _run(cfg, batches, mode):
     tr = sb.Trainer(cfg)
     assert tr.config.run_mode == (1 if mode == "pipelined" else 0)
     losses = []
-    if mode == "pipelined":  # keep one step in flight
+    if mode == "pipelined":  # keep two steps in flight (the host runs a step ahead)
         for t, (f, y, w) in enumerate(batches):
             tr.submit(t, f, y, w)
-            if t > 0:
-                losses.append(tr.loss(t - 1))
-        losses.append(tr.loss(len(batches) - 1))
+            if t > 1:
+                losses.append(tr.loss(t - 2))
+        for t in range(max(0, len(batches) - 2), len(batches)):
+            losses.append(tr.loss(t))
     else:
         for t, (f, y, w) in enumerate(batches):
             losses.append(tr.step(t, f, y, window=w))
@@ -152,14 +153,14 @@ def test_submit_protocol_errors():
     cfg.apply("mode", "pipelined")
     tr = sb.Trainer(cfg)
     gen = sb.SyntheticGenerator(cfg)
-    b = [gen.generate(t) for t in range(3)]
-    tr.submit(0, *b[0])
-    tr.submit(1, *b[1])
+    b = [gen.generate(t) for t in range(5)]
+    for t in range(4):  # up to four steps may be outstanding
+        tr.submit(t, *b[t])
     with pytest.raises(sb.LogicError):  # loss of step 0 not read yet
-        tr.submit(2, *b[2])
+        tr.submit(4, *b[4])
     with pytest.raises(sb.LogicError):  # never submitted
-        tr.loss(5)
-    assert np.isfinite(tr.loss(0)) and np.isfinite(tr.loss(1))
+        tr.loss(9)
+    assert all(np.isfinite(tr.loss(t)) for t in range(4))
     tr.close()
 
 
