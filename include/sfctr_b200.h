@@ -205,7 +205,7 @@ int sfctr_trainer_step_device(sfctr_trainer* t, int64_t step, const uint64_t* d_
 int sfctr_trainer_prepare(sfctr_trainer* t, int64_t step, const uint64_t* d_features,
                           const uint64_t* d_window_features);
 int sfctr_trainer_train(sfctr_trainer* t, int64_t step, const uint8_t* d_labels, float* d_loss);
-/* The host-buffer step split in two, for a driver that keeps one step in flight
+/* The host-buffer step split in two, for a driver that keeps steps in flight
  * (pipelined mode overlaps the manager stage of step t+1 with step t's training):
  * submit enqueues the H2D copies of the inputs, the step and the D2H copy of its loss,
  * and returns; loss waits for that step's loss. At most four submitted steps may be
