@@ -221,6 +221,23 @@ __global__ void __launch_bounds__(dx_threads<SCATTER>(), 1)
         if (et < BM) gz_s[et] = r0 + et < p.M ? __ldg(p.gz + r0 + et) : 0.f;
         cur_m = m;
       }
+      // (0) this tile's FM sums (they do not depend on the accumulator): loads issued
+      // before the wait, so their L2 latency overlaps the MMA / TMEM drain
+      const int j = lane & 15;
+      const int col = n * 64 + 4 * j;
+      const int f = col / d, cc = col - f * d;
+      constexpr int NB = BM / (2 * EW);  // rows per half-warp per tile
+      static_assert(NB >= 1 && NB <= 8, "scatter epilogue row split");
+      float4 fm[NB];
+      bool ok[NB];
+#pragma unroll
+      for (int u8 = 0; u8 < NB; ++u8) {
+        const int rr = 2 * EW * u8 + 2 * ew + (lane >> 4);
+        ok[u8] = r0 + rr < p.M && col < p.N;
+        fm[u8] = ok[u8] ? __ldg(reinterpret_cast<const float4*>(
+                              p.fm_s + static_cast<int64_t>(r0 + rr) * d + cc))
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
       mbar_wait(acc_full + buf, (i >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       // (1) accumulator -> value tile, thread = row
@@ -232,47 +249,28 @@ __global__ void __launch_bounds__(dx_threads<SCATTER>(), 1)
         tmem_ld16(trow + 64 + c0, w);
         float4* dst = reinterpret_cast<float4*>(tile + row * kDxTileStride + c0);
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          dst[j] = make_float4(v[4 * j] + w[4 * j], v[4 * j + 1] + w[4 * j + 1],
-                               v[4 * j + 2] + w[4 * j + 2], v[4 * j + 3] + w[4 * j + 3]);
+        for (int jj = 0; jj < 4; ++jj)
+          dst[jj] = make_float4(v[4 * jj] + w[4 * jj], v[4 * jj + 1] + w[4 * jj + 1],
+                                v[4 * jj + 2] + w[4 * jj + 2], v[4 * jj + 3] + w[4 * jj + 3]);
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(acc_empty + buf);  // the MMA of the next tile may start
       asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");
       // (2) half-warp per row: lane & 15 = 16 B chunk of the tile's 64 columns
-      const int j = lane & 15;
-      const int col = n * 64 + 4 * j;
-      const int f = col / d, cc = col - f * d;
-      // 8 rows per half-warp, all fm_s loads in flight before the first red (the reds
-      // must not serialise behind one L2 round trip each)
-#pragma unroll 1
-      for (int b0 = 0; b0 < BM / (2 * EW); b0 += 8) {
-        constexpr int NB = BM / (2 * EW) < 8 ? BM / (2 * EW) : 8;
-        float4 fm[NB];
-        bool ok[NB];
 #pragma unroll
-        for (int u8 = 0; u8 < NB; ++u8) {
-          const int rr = 2 * EW * (b0 + u8) + 2 * ew + (lane >> 4);
-          ok[u8] = r0 + rr < p.M && col < p.N;
-          fm[u8] = ok[u8] ? __ldg(reinterpret_cast<const float4*>(
-                                p.fm_s + static_cast<int64_t>(r0 + rr) * d + cc))
-                          : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int u8 = 0; u8 < NB; ++u8) {
-          const int rr = 2 * EW * (b0 + u8) + 2 * ew + (lane >> 4);
-          if (!ok[u8]) continue;
-          const float4 a = *reinterpret_cast<const float4*>(tile + rr * kDxTileStride + 4 * j);
-          const float g = gz_s[rr];
-          const float k = p.scale * g;
-          const uint32_t u = vid_s[rr * F + f];
-          float* dst = p.dG + static_cast<int64_t>(u) * d + cc;
-          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst),
-                       "f"(p.scale * a.x + k * fm[u8].x), "f"(p.scale * a.y + k * fm[u8].y),
-                       "f"(p.scale * a.z + k * fm[u8].z), "f"(p.scale * a.w + k * fm[u8].w));
-          if (cc == 0) atomicAdd(p.Bsum + u, g);
-        }
+      for (int u8 = 0; u8 < NB; ++u8) {
+        const int rr = 2 * EW * u8 + 2 * ew + (lane >> 4);
+        if (!ok[u8]) continue;
+        const float4 a = *reinterpret_cast<const float4*>(tile + rr * kDxTileStride + 4 * j);
+        const float g = gz_s[rr];
+        const float k = p.scale * g;
+        const uint32_t u = vid_s[rr * F + f];
+        float* dstg = p.dG + static_cast<int64_t>(u) * d + cc;
+        asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dstg),
+                     "f"(p.scale * a.x + k * fm[u8].x), "f"(p.scale * a.y + k * fm[u8].y),
+                     "f"(p.scale * a.z + k * fm[u8].z), "f"(p.scale * a.w + k * fm[u8].w));
+        if (cc == 0) atomicAdd(p.Bsum + u, g);
       }
       asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");  // value tile / tables free
     }
