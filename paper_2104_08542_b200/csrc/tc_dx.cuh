@@ -212,11 +212,29 @@ __global__ void __launch_bounds__(dx_threads<SCATTER>(), 1)
       const int buf = i & 1;
       const int r0 = m * BM;
       if (m != cur_m) {  // stage this m-tile's vid / gz (the previous tile's scatter is done)
-        for (int idx = et; idx < BM * F; idx += 32 * EW) {
-          const int r = idx / F;
-          uint32_t v = r0 + r < p.M ? __ldg(p.vid + static_cast<int64_t>(r0) * F + idx) : 0u;
-          if (p.remap && r0 + r < p.M) v = __ldg(p.remap + v);
-          vid_s[idx] = v;
+        // 8 independent loads in flight per thread (a plain loop is a chain of dependent
+        // L2 round trips: ~10 per thread per m-tile, twice that with the remap)
+        const int nst = BM * F;
+        for (int base = 0; base < nst; base += 32 * EW * 8) {
+          uint32_t v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int idx = base + u * 32 * EW + et;
+            const bool in = idx < nst && r0 + idx / F < p.M;
+            v[u] = in ? __ldg(p.vid + static_cast<int64_t>(r0) * F + idx) : 0u;
+          }
+          if (p.remap) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int idx = base + u * 32 * EW + et;
+              if (idx < nst && r0 + idx / F < p.M) v[u] = __ldg(p.remap + v[u]);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int idx = base + u * 32 * EW + et;
+            if (idx < nst) vid_s[idx] = v[u];
+          }
         }
         if (et < BM) gz_s[et] = r0 + et < p.M ? __ldg(p.gz + r0 + et) : 0.f;
         cur_m = m;
