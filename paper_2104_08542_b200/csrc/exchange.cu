@@ -539,6 +539,62 @@ __global__ void __launch_bounds__(256) push_rows_p2p_dev_kernel(
   if (threadIdx.x == 0) __threadfence_system();
 }
 
+// Forward in two phases (SFCTR_FWD_STAGED=1; the fused push_rows kernel is the default):
+// pack_fwd gathers every owned row a peer touches into that
+// peer's contiguous block of the staging buffer (HBM only, many threads for the random slot
+// reads) and writes my own touched rows straight into my E; push_fwd then copies each block
+// to its destination's E with one wave of writer CTAs per peer (the backward's pattern,
+// which sustains ~0.7 of the peer-copy peak where the fused gather+push reached ~0.6).
+__global__ void __launch_bounds__(256) pack_fwd_kernel(
+    const uint32_t* __restrict__ own_k, const uint32_t* __restrict__ own_slot,
+    const int32_t* __restrict__ n_ptr, const uint32_t* __restrict__ tm,
+    const Cnt8* __restrict__ sscan, uint32_t W, uint32_t me, const int32_t* __restrict__ offs,
+    const float4* __restrict__ emb, int d4, float4* __restrict__ E_mine,
+    float4* __restrict__ stage) {
+  const int64_t n = static_cast<int64_t>(*n_ptr) * d4;
+  const uint32_t e_me = offs[Exchange::kOffRoff + me * 8 + me];
+  uint32_t soff[8];
+#pragma unroll
+  for (int w = 0; w < 8; ++w) soff[w] = w < static_cast<int>(W) ? offs[Exchange::kOffSend + w] : 0u;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    const int64_t j = idiv(i, d4);
+    const int c = static_cast<int>(i - j * d4);
+    uint32_t m = __ldg(tm + __ldg(own_k + j)) & ((1u << W) - 1u);
+    const float4 v = __ldg(emb + static_cast<int64_t>(__ldg(own_slot + j)) * 3 * d4 + c);
+    while (m) {
+      const int w = __ffs(m) - 1;
+      m &= m - 1;
+      const uint32_t r = __ldg(&sscan[j].c[w]);
+      if (w == static_cast<int>(me)) E_mine[static_cast<int64_t>(e_me + r) * d4 + c] = v;
+      else stage[static_cast<int64_t>(soff[w] + r) * d4 + c] = v;
+    }
+  }
+}
+
+// blockIdx.y = destination w: my staged block for w -> rank w's E at my owner offset
+__global__ void push_fwd_kernel(const float4* __restrict__ stage, int d4, uint32_t me,
+                                const int32_t* __restrict__ totals,
+                                const int32_t* __restrict__ offs, PeerRows pr) {
+  const int w = blockIdx.y;
+  if (w != static_cast<int>(me)) {
+    const int64_t n = static_cast<int64_t>(totals[8 + w]) * d4;
+    const float4* src = stage + static_cast<int64_t>(offs[Exchange::kOffSend + w]) * d4;
+    float4* dst = pr.E[w] + static_cast<int64_t>(offs[Exchange::kOffRoff + w * 8 + me]) * d4;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i0 < n;
+         i0 += 2 * stride) {
+      const float4 a = src[i0];
+      const bool two = i0 + stride < n;
+      const float4 b = two ? src[i0 + stride] : a;
+      dst[i0] = a;
+      if (two) dst[i0 + stride] = b;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) __threadfence_system();
+}
+
 struct OwnerAdam {
   float4 *emb, *mom, *vel;
   const uint32_t* own_slot;
@@ -696,10 +752,31 @@ void Exchange::forward_dev(const uint32_t* d_own_k, const uint32_t* d_own_slot, 
     const char* e = std::getenv("SFCTR_FWD_PUSH_BLOCKS");
     return e ? std::max(1, atoi(e)) : 148 * 2;
   }();
-  push_rows_p2p_dev_kernel<<<std::max(1, std::min(ceil_div(static_cast<int64_t>(n_bound) * (d / 4), 512),
-                                                  fwd_blocks)),
-                             256, 0, s>>>(d_own_k, d_own_slot, d_n_own, tm, sscan, W, me, offs,
-                                          reinterpret_cast<const float4*>(emb), d / 4, pr);
+  // SFCTR_FWD_STAGED=1: pack per destination, then block pushes (measured slower at cfg2:
+  // 93.5 vs 80 us at N = 4, the pack's HBM pass costs more than the pushes gain)
+  static const bool fused = [] {
+    const char* e = std::getenv("SFCTR_FWD_STAGED");
+    return !(e && e[0] == '1');
+  }();
+  if (fused) {
+    push_rows_p2p_dev_kernel<<<std::max(1, std::min(ceil_div(static_cast<int64_t>(n_bound) * (d / 4), 512),
+                                                    fwd_blocks)),
+                               256, 0, s>>>(d_own_k, d_own_slot, d_n_own, tm, sscan, W, me, offs,
+                                            reinterpret_cast<const float4*>(emb), d / 4, pr);
+    CUDA_LAUNCH_CHECK();
+    return;
+  }
+  // the staging rows live in buf: it is free until the backward, which peers only start
+  // after this step's forward barrier
+  pack_fwd_kernel<<<std::max(1, std::min(ceil_div(static_cast<int64_t>(n_bound) * (d / 4), 256),
+                                         148 * 16)),
+                    256, 0, s>>>(d_own_k, d_own_slot, d_n_own, tm, sscan, W, me, offs,
+                                 reinterpret_cast<const float4*>(emb), d / 4,
+                                 reinterpret_cast<float4*>(peer_E[me]),
+                                 reinterpret_cast<float4*>(buf));
+  CUDA_LAUNCH_CHECK();
+  push_fwd_kernel<<<dim3(148, W), 256, 0, s>>>(reinterpret_cast<const float4*>(buf), d / 4, me,
+                                                totals, offs, pr);
   CUDA_LAUNCH_CHECK();
 }
 
