@@ -705,10 +705,12 @@ __global__ void __launch_bounds__(256) owner_reduce_dev_kernel(
     for (int u = 0; u < 2; ++u) {
       if (!ok[u]) continue;
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (uint32_t w = 0; w < W; ++w) {  // fixed source order (same as owner_reduce_kernel)
-        if (!((m[u] >> w) & 1u)) continue;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {  // fixed source order (same as owner_reduce_kernel);
+        // unrolled over the 8 possible sources so soff[] stays in registers
+        if (w >= static_cast<int>(W) || !((m[u] >> w) & 1u)) continue;
         float4 v;
-        if (w == me) {
+        if (w == static_cast<int>(me)) {
           const int64_t lr = __ldg(lpos + k[u]);
           v = dE[lr * d4 + c[u]];
           if (fm.B) v = with_fm(v, fm, lr, c[u], d4);
