@@ -101,8 +101,11 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
                                           pipelined_ ? prio_hi : prio_lo));
   if (const char* e = std::getenv("SFCTR_NO_FREE_STEPS")) no_free_steps_ = e[0] == '1';
   mstream_ = stream_;
-  if (pipelined_)
+  if (pipelined_) {
     CUDA_CHECK(cudaStreamCreateWithPriority(&mstream_, cudaStreamNonBlocking, prio_lo));
+    CUDA_CHECK(cudaStreamCreateWithFlags(&cstream_, cudaStreamNonBlocking));
+    for (auto& e : in_ready_) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   if (world_ > 1) {
     if (!nccl_id) fail(kConfig, "world > 1 needs an NCCL unique id");
     ncclUniqueId id;
@@ -278,6 +281,9 @@ Trainer::~Trainer() {
   if (mcomm_ && mcomm_ != comm_) ncclCommDestroy(mcomm_);
   if (comm_) ncclCommDestroy(comm_);
   if (mstream_ && mstream_ != stream_) cudaStreamDestroy(mstream_);
+  if (cstream_) cudaStreamDestroy(cstream_);
+  for (cudaEvent_t e : in_ready_)
+    if (e) cudaEventDestroy(e);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -469,6 +475,10 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
   const int k = static_cast<int>(step & 1);  // buffer set of this step
   // the set's previous user (step t-2) must have finished training before it is refilled
   if (piped && train_pending_[k]) CUDA_CHECK(cudaStreamWaitEvent(sm, train_done_[k]));
+  if (input_wait_) {  // host inputs staged on the copy stream (submit_host)
+    CUDA_CHECK(cudaStreamWaitEvent(sm, in_ready_[k]));
+    input_wait_ = false;
+  }
   d_uniq_ = d_uniq_set_[k];
   d_vid_ = d_vid_set_[k];
   d_dG_ = d_dG_set_[k];
@@ -669,7 +679,10 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
   else if (xdev)
     xch_.zero_local_dev(d_dG_, sm, d_ % 4 == 0 && !tower_fused_ ? d_B_ : nullptr);
   phase("manage_evict_admit", sm);
-  if (sm != sw) CUDA_CHECK(cudaEventRecord(prep_done_[k], sm));
+  if (sm != sw) {
+    CUDA_CHECK(cudaEventRecord(prep_done_[k], sm));
+    prep_recorded_[k] = true;
+  }
   prep_.step = step;
   prep_.k = k;
   prep_.sm = sm;
@@ -994,18 +1007,26 @@ void Trainer::submit_host(int64_t step, const uint64_t* features, const uint8_t*
   if (loss_step_[q] >= 0 && loss_step_[q] != step)
     fail(kLogic, "read the loss of step " + std::to_string(loss_step_[q]) +
                      " (loss_of) before submitting step " + std::to_string(step));
-  // the staging set was last read by step t-2: the manager stream waits for it below
-  // (step_device), so the copies go on the manager stream after that wait
-  cudaStream_t sm = timing_ ? stream_ : mstream_;  // the stream step_device's manager uses
-  if (sm != stream_ && train_pending_[k]) CUDA_CHECK(cudaStreamWaitEvent(sm, train_done_[k]));
+  // Staging set k was last read by step t-2: its ids / window by t-2's manager stage, its
+  // labels by t-2's training stage. Pipelined: the copies run on their own stream as soon as
+  // those readers are done (the ids usually long before step t-2 finishes training), and the
+  // manager stage of step t waits for them. Otherwise they go on the manager's stream.
+  const bool piped = pipelined_ && !timing_;
+  cudaStream_t cs = piped ? cstream_ : stream_;
+  if (piped && prep_recorded_[k]) CUDA_CHECK(cudaStreamWaitEvent(cs, prep_done_[k]));
   CUDA_CHECK(cudaMemcpyAsync(d_in_feat_set_[k], features, sizeof(uint64_t) * n_local_,
-                             cudaMemcpyHostToDevice, sm));
-  CUDA_CHECK(cudaMemcpyAsync(d_in_lab_set_[k], labels, static_cast<size_t>(lanes_) * b_,
-                             cudaMemcpyHostToDevice, sm));
+                             cudaMemcpyHostToDevice, cs));
   if (window && cfg_.lookahead_depth > 1)
     CUDA_CHECK(cudaMemcpyAsync(d_in_win_set_[k], window,
                                sizeof(uint64_t) * n_local_ * (cfg_.lookahead_depth - 1),
-                               cudaMemcpyHostToDevice, sm));
+                               cudaMemcpyHostToDevice, cs));
+  if (piped && train_pending_[k]) CUDA_CHECK(cudaStreamWaitEvent(cs, train_done_[k]));
+  CUDA_CHECK(cudaMemcpyAsync(d_in_lab_set_[k], labels, static_cast<size_t>(lanes_) * b_,
+                             cudaMemcpyHostToDevice, cs));
+  if (piped) {
+    CUDA_CHECK(cudaEventRecord(in_ready_[k], cs));
+    input_wait_ = true;
+  }
   step_device(step, d_in_feat_set_[k], d_in_lab_set_[k], window ? d_in_win_set_[k] : nullptr,
               d_loss_set_[k]);
   CUDA_CHECK(cudaMemcpyAsync(h_loss_ring_ + q, d_loss_set_[k], sizeof(float),

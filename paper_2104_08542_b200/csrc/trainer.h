@@ -103,6 +103,10 @@ class Trainer {
   cudaStream_t dstream_ = nullptr;   // dense-gradient all-reduce, overlapping the row exchange
   cudaEvent_t dense_ready_ = nullptr, dense_done_ = nullptr;
   cudaEvent_t prep_done_[2] = {}, train_done_[2] = {};
+  bool prep_recorded_[2] = {false, false};
+  cudaStream_t cstream_ = nullptr;   // host-input copies (pipelined submit_host)
+  cudaEvent_t in_ready_[2] = {};
+  bool input_wait_ = false;          // the next prepare() waits for in_ready_
   bool train_pending_[2] = {false, false};
   int32_t* d_snap_[2] = {};          // [1 + kCntWords * lanes]: U, then every lane's counters
   uint32_t* d_uniq_set_[2] = {};
