@@ -108,19 +108,53 @@ __global__ void head_tc_kernel(int rows, int H, int d, int sq_parts, const float
     }
     return;
   }
-  float mlp = 0.f;
-  for (int j = lane; j < H; j += 32) {
-    float h = b1[j];
-    for (int z = 0; z < splits; ++z) h += part[z * split_stride + static_cast<long long>(r) * H + j];
-    act[static_cast<int64_t>(r) * H + j] = h;  // pre-activation for now
-    mlp += fmaxf(h, 0.f) * w2[j];
+  float mlp = 0.f, ss = 0.f, sq = 0.f;
+  float hreg[2] = {0.f, 0.f};
+  // H = 64 (the DeepFM-lite width), <= 4 split-K partials, d <= 128: every load of the row is
+  // issued up front (the generic loops chain one L2 round trip per load); same sums, same order
+  const bool fast = H == 64 && splits <= 4 && d <= 128 && sq_parts <= 32;
+  if (fast) {
+    float pv[4][2];
+#pragma unroll
+    for (int z = 0; z < 4; ++z) {
+      const float* pz = part + z * split_stride + static_cast<long long>(r) * 64;
+      pv[z][0] = z < splits ? __ldg(pz + lane) : 0.f;
+      pv[z][1] = z < splits ? __ldg(pz + lane + 32) : 0.f;
+    }
+    float fs[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int c = lane + 32 * q;
+      fs[q] = c < d ? __ldg(fm_s + static_cast<int64_t>(r) * d + c) : 0.f;
+    }
+    sq = lane < sq_parts ? __ldg(fm_sqp + static_cast<int64_t>(r) * sq_parts + lane) : 0.f;
+    float h0 = __ldg(b1 + lane), h1 = __ldg(b1 + lane + 32);
+#pragma unroll
+    for (int z = 0; z < 4; ++z)
+      if (z < splits) {
+        h0 += pv[z][0];
+        h1 += pv[z][1];
+      }
+    hreg[0] = h0;
+    hreg[1] = h1;
+    mlp = fmaxf(h0, 0.f) * __ldg(w2 + lane);
+    mlp += fmaxf(h1, 0.f) * __ldg(w2 + lane + 32);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (lane + 32 * q < d) ss += fs[q] * fs[q];
+  } else {
+    for (int j = lane; j < H; j += 32) {
+      float h = b1[j];
+      for (int z = 0; z < splits; ++z) h += part[z * split_stride + static_cast<long long>(r) * H + j];
+      act[static_cast<int64_t>(r) * H + j] = h;  // pre-activation for now
+      mlp += fmaxf(h, 0.f) * w2[j];
+    }
+    for (int c = lane; c < d; c += 32) {
+      const float v = fm_s[static_cast<int64_t>(r) * d + c];
+      ss += v * v;
+    }
+    for (int c = lane; c < sq_parts; c += 32) sq += fm_sqp[static_cast<int64_t>(r) * sq_parts + c];
   }
-  float ss = 0.f, sq = 0.f;
-  for (int c = lane; c < d; c += 32) {
-    const float v = fm_s[static_cast<int64_t>(r) * d + c];
-    ss += v * v;
-  }
-  for (int c = lane; c < sq_parts; c += 32) sq += fm_sqp[static_cast<int64_t>(r) * sq_parts + c];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     mlp += __shfl_xor_sync(0xFFFFFFFFu, mlp, o);
@@ -136,7 +170,7 @@ __global__ void head_tc_kernel(int rows, int H, int d, int sq_parts, const float
   const float g = clamped ? 0.f : (p - y) * inv_rows;
   for (int j = lane; j < H; j += 32) {
     const int64_t o = static_cast<int64_t>(r) * H + j;
-    const float hv = act[o];
+    const float hv = fast ? hreg[j >> 5] : act[o];
     act[o] = fmaxf(hv, 0.f);
     const float dv = hv > 0.f ? g * w2[j] : 0.f;
     dh[o] = dv;
