@@ -935,7 +935,7 @@ void Trainer::train(int64_t step, const uint8_t* d_labels, float* d_loss) {
     a.W = W_;
     a.d = d_;
     a.P = static_cast<int64_t>(P_);
-    tail_kernel<<<148 * 4, 256, 0, s>>>(a);
+    tail_kernel<<<148 * 8, 256, 0, s>>>(a);  // one pass over the dense parameters and the rows
     CUDA_LAUNCH_CHECK();
     w1_split_ready_ = a.w_hi != nullptr;
   }
