@@ -390,11 +390,39 @@ __global__ void small_grads_p2(const float* __restrict__ part, int chunks, int H
 }
 }  // namespace
 
+// block per output over output-major partials [2H+2][chunks]: 256 threads, a fixed-order
+// strided sum then a fixed shuffle / shared-memory tree (deterministic)
+__global__ void small_grads_final_kernel(const float* __restrict__ part, int chunks, int H,
+                                         float inv_rows, float* __restrict__ g_db1,
+                                         float* __restrict__ g_dw2, float* __restrict__ g_db2,
+                                         float* __restrict__ g_loss, int accumulate) {
+  __shared__ float red[8];
+  const int i = blockIdx.x, tid = threadIdx.x;
+  const float* row = part + static_cast<int64_t>(i) * chunks;
+  float a[4] = {0.f, 0.f, 0.f, 0.f};
+  int c = tid;
+  for (; c + 3 * 256 < chunks; c += 4 * 256) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a[u] += __ldg(row + c + u * 256);
+  }
+  for (; c < chunks; c += 256) a[0] += __ldg(row + c);
+  float v = (a[0] + a[1]) + (a[2] + a[3]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  if ((tid & 31) == 0) red[tid >> 5] = v;
+  __syncthreads();
+  if (tid != 0) return;
+  float sum = 0.f;
+  for (int w = 0; w < 8; ++w) sum += red[w];
+  float* dst = i < H ? g_db1 + i : (i < 2 * H ? g_dw2 + (i - H) : (i == 2 * H ? g_db2 : g_loss));
+  if (i == 2 * H + 1) sum *= inv_rows;
+  *dst = accumulate ? *dst + sum : sum;
+}
+
 void small_grads_final(TowerBufs& t, int chunks, int rows, int H, float* g_b1, float* g_w2,
                        float* g_b2, float* g_loss, bool accumulate, cudaStream_t s) {
-  small_grads_p2<<<ceil_div(2 * H + 2, 8), 256, 0, s>>>(t.sg_part, chunks, H, 1.f / rows, g_b1,
-                                                         g_w2, g_b2, g_loss, accumulate ? 1 : 0,
-                                                         /*out_major=*/1);
+  small_grads_final_kernel<<<2 * H + 2, 256, 0, s>>>(t.sg_part, chunks, H, 1.f / rows, g_b1, g_w2,
+                                                     g_b2, g_loss, accumulate ? 1 : 0);
   CUDA_LAUNCH_CHECK();
 }
 
