@@ -128,6 +128,10 @@ void tower_forward_backward_simt(TowerBufs& t, const float* X, const float* fm_s
                                  float emb_scale, float* grads, bool accumulate, cudaStream_t s);
 void dw1_reduce(const float* part, int splits, int64_t n, float* out, bool accumulate,
                 cudaStream_t s);
+// dW1's split-K sum and the small-gradient final pass over t.sg_part in one launch
+void tower_reduce(const float* part3, int splits, int64_t kh, float* g_w1, TowerBufs& t,
+                  int chunks, int rows, int H, float* g_b1, float* g_w2, float* g_b2,
+                  float* g_loss, bool accumulate, cudaStream_t s);
 // the final pass alone, over `chunks` partials already in t.sg_part (the head wrote them)
 void small_grads_final(TowerBufs& t, int chunks, int rows, int H, float* g_b1, float* g_w2,
                        float* g_b2, float* g_loss, bool accumulate, cudaStream_t s);

@@ -631,11 +631,13 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc_, const float* X, int l
   }
   hook("tower_gemm3");
   const int64_t kh = static_cast<int64_t>(K) * H;
-  dw1_reduce(tc_.part3, s3, kh, g_w1, accumulate, s);
-  if (H <= 64)  // the head left per-block partials: only the final pass remains
-    small_grads_final(t, ceil_div(rows, 8), rows, H, g_b1, g_w2, g_b2, g_loss, accumulate, s);
-  else
+  if (H <= 64) {  // the head left per-block partials: one launch finishes every dense gradient
+    tower_reduce(tc_.part3, s3, kh, g_w1, t, ceil_div(rows, 8), rows, H, g_b1, g_w2, g_b2, g_loss,
+                 accumulate, s);
+  } else {
+    dw1_reduce(tc_.part3, s3, kh, g_w1, accumulate, s);
     small_grads(t, rows, H, g_b1, g_w2, g_b2, g_loss, accumulate, s);
+  }
 }
 
 void tower_forward_backward_fused(TowerBufs& t, TowerTC& tc_, const float* G, int64_t g_rows,

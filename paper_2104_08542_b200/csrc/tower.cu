@@ -419,6 +419,60 @@ __global__ void small_grads_final_kernel(const float* __restrict__ part, int chu
   *dst = accumulate ? *dst + sum : sum;
 }
 
+// dW1 split-K sum (blocks [0, nb)) and the small-gradient final pass (blocks nb ..) in one
+// launch; the split partials are loaded before they are summed (in split order)
+__global__ void tower_reduce_kernel(const float* __restrict__ part3, int splits, int64_t kh,
+                                    float* __restrict__ g_w1, int nb, const float* __restrict__ sg,
+                                    int chunks, int H, float inv_rows, float* __restrict__ g_db1,
+                                    float* __restrict__ g_dw2, float* __restrict__ g_db2,
+                                    float* __restrict__ g_loss, int accumulate) {
+  if (static_cast<int>(blockIdx.x) < nb) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= kh) return;
+    float v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = q < splits ? __ldg(part3 + q * kh + i) : 0.f;
+    float s = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q < splits) s += v[q];
+    for (int q = 8; q < splits; ++q) s += __ldg(part3 + q * kh + i);
+    g_w1[i] = accumulate ? g_w1[i] + s : s;
+    return;
+  }
+  __shared__ float red[8];
+  const int i = blockIdx.x - nb, tid = threadIdx.x;
+  const float* row = sg + static_cast<int64_t>(i) * chunks;
+  float a[4] = {0.f, 0.f, 0.f, 0.f};
+  int c = tid;
+  for (; c + 3 * 256 < chunks; c += 4 * 256) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a[u] += __ldg(row + c + u * 256);
+  }
+  for (; c < chunks; c += 256) a[0] += __ldg(row + c);
+  float v = (a[0] + a[1]) + (a[2] + a[3]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  if ((tid & 31) == 0) red[tid >> 5] = v;
+  __syncthreads();
+  if (tid != 0) return;
+  float sum = 0.f;
+  for (int w = 0; w < 8; ++w) sum += red[w];
+  float* dst = i < H ? g_db1 + i : (i < 2 * H ? g_dw2 + (i - H) : (i == 2 * H ? g_db2 : g_loss));
+  if (i == 2 * H + 1) sum *= inv_rows;
+  *dst = accumulate ? *dst + sum : sum;
+}
+
+void tower_reduce(const float* part3, int splits, int64_t kh, float* g_w1, TowerBufs& t,
+                  int chunks, int rows, int H, float* g_b1, float* g_w2, float* g_b2,
+                  float* g_loss, bool accumulate, cudaStream_t s) {
+  const int nb = ceil_div(kh, 256);
+  tower_reduce_kernel<<<nb + 2 * H + 2, 256, 0, s>>>(part3, splits, kh, g_w1, nb, t.sg_part, chunks,
+                                                     H, 1.f / rows, g_b1, g_w2, g_b2, g_loss,
+                                                     accumulate ? 1 : 0);
+  CUDA_LAUNCH_CHECK();
+}
+
 void small_grads_final(TowerBufs& t, int chunks, int rows, int H, float* g_b1, float* g_w2,
                        float* g_b2, float* g_loss, bool accumulate, cudaStream_t s) {
   small_grads_final_kernel<<<2 * H + 2, 256, 0, s>>>(t.sg_part, chunks, H, 1.f / rows, g_b1, g_w2,
