@@ -669,6 +669,7 @@ __global__ void zero_rows_dev_kernel(float4* __restrict__ p, const int32_t* __re
 
 // ADAM: the owner's sum goes straight into the lazy Adam update of its cache slot (same
 // math as sparse_adam_v4, embed.cu) instead of being written to gown and read back.
+constexpr int kOwnU = 1;  // (row, chunk) items per thread per round (2 measured no better)
 template <bool ADAM>
 __global__ void __launch_bounds__(256) owner_reduce_dev_kernel(
     const uint32_t* __restrict__ own_k, const int32_t* __restrict__ n_ptr,
@@ -686,13 +687,13 @@ __global__ void __launch_bounds__(256) owner_reduce_dev_kernel(
   }
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i0 < n;
-       i0 += 2 * stride) {
-    int64_t j[2];
-    int c[2];
-    bool ok[2];
-    uint32_t k[2], m[2];
+       i0 += kOwnU * stride) {
+    int64_t j[kOwnU];
+    int c[kOwnU];
+    bool ok[kOwnU];
+    uint32_t k[kOwnU], m[kOwnU];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < kOwnU; ++u) {
       const int64_t i = i0 + u * stride;
       ok[u] = i < n;
       j[u] = ok[u] ? idiv(i, d4) : 0;
@@ -700,9 +701,9 @@ __global__ void __launch_bounds__(256) owner_reduce_dev_kernel(
       k[u] = ok[u] ? __ldg(own_k + j[u]) : 0u;
     }
 #pragma unroll
-    for (int u = 0; u < 2; ++u) m[u] = ok[u] ? __ldg(tm + k[u]) : 0u;
+    for (int u = 0; u < kOwnU; ++u) m[u] = ok[u] ? __ldg(tm + k[u]) : 0u;
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < kOwnU; ++u) {
       if (!ok[u]) continue;
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
@@ -818,7 +819,7 @@ void Exchange::backward_reduce_adam_dev(const uint32_t* d_own_k, int32_t n_bound
   OwnerAdam a{reinterpret_cast<float4*>(ar.emb), reinterpret_cast<float4*>(ar.mom),
               reinterpret_cast<float4*>(ar.vel), ar.own_slot, ar.steps, ar.bc1, ar.bc2, ar.lr,
               ar.b1, ar.b2, ar.omb1, ar.omb2, ar.eps};
-  owner_reduce_dev_kernel<true><<<std::max(1, std::min(ceil_div(static_cast<int64_t>(n_bound) * d4, 512),
+  owner_reduce_dev_kernel<true><<<std::max(1, std::min(ceil_div(static_cast<int64_t>(n_bound) * d4, 256),
                                                        148 * 16)),
                                   256, 0, s>>>(d_own_k, d_n_own, tm, sscan, totals, W, me, lpos,
                                                reinterpret_cast<const float4*>(dE),
