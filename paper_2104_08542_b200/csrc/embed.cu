@@ -64,7 +64,7 @@ __global__ void gather_cache_s(const uint32_t* __restrict__ own_k,
 // Two threads per (row, 16 B chunk), adjacent lanes, each gathering half of the F fields
 // (8 row loads in flight), the FM partial sums combined with one shuffle: twice the
 // threads of a whole-row loop, so the kernel reaches two waves and hides the HBM latency.
-__global__ void __launch_bounds__(256, 4) gather_instances_v4(
+__global__ void __launch_bounds__(256, 5) gather_instances_v4(
     const uint32_t* __restrict__ vid, int32_t rows, int F, int d4, const float4* __restrict__ G,
     float4* __restrict__ X, float4* __restrict__ fm_s, float* __restrict__ fm_sqp,
     const uint32_t* __restrict__ slot_of, int g4) {
