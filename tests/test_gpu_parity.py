@@ -336,3 +336,13 @@ def test_cfg2_step_properties(golden):
     loss2 = tr.step(1, *gen.generate(1))
     assert np.isfinite(loss2)
     tr.close()
+
+
+@pytest.mark.parametrize("env", ["SFCTR_TOWER_FUSED", "SFCTR_TOWER_SIMT"])
+def test_trainer_alternative_towers(monkeypatch, env):
+    """The opt-in tower paths (fused gather->GEMM->scatter, fp32 SIMT validation tiles) hold
+    the same parity bars (d = 16 so the fused path applies, K = F*d unpadded for SIMT)."""
+    monkeypatch.setenv(env, "1")
+    cfg = sb.Config(num_workers=1, batch_size_per_worker=128, num_fields=8, embedding_dim=16,
+                    vocabulary_size=20000, cache_capacity=1200, hidden_dim=32, zipf_exponent=1.05)
+    run_parity(cfg, 5)
