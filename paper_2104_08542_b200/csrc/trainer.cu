@@ -187,7 +187,11 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
   CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_scalars_), sizeof(int32_t) * 8, 0));
   CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_counts_),
                            sizeof(int32_t) * kCntWords * lanes_, 0));
-  CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_loss_ring_), sizeof(float) * kLossRing, 0));
+  // mapped: the step's last kernel stores the loss straight into the host slot (no D2H copy
+  // between one step's training stage and the next on the worker stream)
+  CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_loss_ring_), sizeof(float) * kLossRing,
+                           cudaHostAllocMapped));
+  CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_loss_ring_), h_loss_ring_, 0));
   for (int q = 0; q < kLossRing; ++q)
     CUDA_CHECK(cudaEventCreateWithFlags(&loss_ev_[q], cudaEventDisableTiming));
   CUDA_CHECK(cudaMalloc(&d_acc_, sizeof(int64_t) * 8));
@@ -1028,9 +1032,7 @@ void Trainer::submit_host(int64_t step, const uint64_t* features, const uint8_t*
     input_wait_ = true;
   }
   step_device(step, d_in_feat_set_[k], d_in_lab_set_[k], window ? d_in_win_set_[k] : nullptr,
-              d_loss_set_[k]);
-  CUDA_CHECK(cudaMemcpyAsync(h_loss_ring_ + q, d_loss_set_[k], sizeof(float),
-                             cudaMemcpyDeviceToHost, stream_));
+              d_loss_ring_ + q);  // the tail kernel writes the host slot (mapped memory)
   CUDA_CHECK(cudaEventRecord(loss_ev_[q], stream_));
   loss_step_[q] = step;
 }

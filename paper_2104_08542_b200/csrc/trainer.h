@@ -124,7 +124,8 @@ class Trainer {
   // losses of submitted steps (slot = step % kLossRing): the host may run up to kLossRing
   // steps ahead of the loss it reads; the device-side parity sets are ordered by events
   static constexpr int kLossRing = 4;
-  float* h_loss_ring_ = nullptr;     // pinned [kLossRing]
+  float* h_loss_ring_ = nullptr;     // pinned, mapped [kLossRing]
+  float* d_loss_ring_ = nullptr;     // its device alias
   cudaEvent_t loss_ev_[kLossRing] = {};
   int64_t loss_step_[kLossRing] = {-1, -1, -1, -1};
 

@@ -31,17 +31,17 @@ def _batches(cfg, steps):
     return out
 
 
-def _run(cfg, batches, mode):
+def _run(cfg, batches, mode, inflight=2):
     cfg.apply("mode", mode)
     tr = sb.Trainer(cfg)
     assert tr.config.run_mode == (1 if mode == "pipelined" else 0)
     losses = []
-    if mode == "pipelined":  # keep two steps in flight (the host runs a step ahead)
+    if mode == "pipelined":  # keep `inflight` steps outstanding (the host runs ahead)
         for t, (f, y, w) in enumerate(batches):
             tr.submit(t, f, y, w)
-            if t > 1:
-                losses.append(tr.loss(t - 2))
-        for t in range(max(0, len(batches) - 2), len(batches)):
+            if t >= inflight:
+                losses.append(tr.loss(t - inflight))
+        for t in range(max(0, len(batches) - inflight), len(batches)):
             losses.append(tr.loss(t))
     else:
         for t, (f, y, w) in enumerate(batches):
@@ -69,10 +69,10 @@ def _oracle(cfg, batches):
     return O, sim, np.array(losses)
 
 
-def check_modes(cfg, steps):
+def check_modes(cfg, steps, inflight=2):
     batches = _batches(cfg, steps)
     seq = _run(cfg, batches, "sequential")
-    pip = _run(cfg, batches, "pipelined")
+    pip = _run(cfg, batches, "pipelined", inflight)
     # pipelined == sequential (semantic transparency)
     assert np.allclose(pip["losses"], seq["losses"], rtol=1e-6, atol=0)
     assert pip["ledger"] == seq["ledger"]
@@ -145,6 +145,22 @@ def test_pipelined_whole_shard_free_steps():
                     zipf_exponent=1.05)
     st = check_modes(cfg, 6)
     assert st["total_free_steps"] == 6
+
+
+@pytest.mark.parametrize("inflight", [1, 3])
+def test_pipelined_host_queue_depths(inflight):
+    """Besides the step it submits, the host leaves 1 or 3 steps unread (3 = the loss ring's
+    depth), so the two device buffer sets are reused while earlier steps are still queued
+    and each loss lands in its mapped host slot: results must not change."""
+    cfg = sb.Config(num_workers=1, batch_size_per_worker=64, num_fields=8, embedding_dim=8,
+                    vocabulary_size=5000, cache_capacity=700, hidden_dim=16, zipf_exponent=1.1)
+    st = check_modes(cfg, 12, inflight)
+    assert st["total_evicted"] > 0
+    cfg = sb.Config(num_workers=1, batch_size_per_worker=512, num_fields=13, embedding_dim=16,
+                    vocabulary_size=200_000, cache_capacity=200_000, hidden_dim=32,
+                    zipf_exponent=1.05)
+    st = check_modes(cfg, 8, inflight)
+    assert st["total_free_steps"] == 8
 
 
 def test_submit_protocol_errors():
