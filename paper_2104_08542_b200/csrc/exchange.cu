@@ -669,7 +669,6 @@ __global__ void zero_rows_dev_kernel(float4* __restrict__ p, const int32_t* __re
 
 // ADAM: the owner's sum goes straight into the lazy Adam update of its cache slot (same
 // math as sparse_adam_v4, embed.cu) instead of being written to gown and read back.
-constexpr int kOwnU = 1;  // (row, chunk) items per thread per round (2 measured no better)
 template <bool ADAM>
 __global__ void __launch_bounds__(256) owner_reduce_dev_kernel(
     const uint32_t* __restrict__ own_k, const int32_t* __restrict__ n_ptr,
@@ -686,61 +685,60 @@ __global__ void __launch_bounds__(256) owner_reduce_dev_kernel(
     if (w < static_cast<int>(W) && w != static_cast<int>(me)) run += static_cast<uint32_t>(totals[8 + w]);
   }
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i0 < n;
-       i0 += kOwnU * stride) {
-    int64_t j[kOwnU];
-    int c[kOwnU];
-    bool ok[kOwnU];
-    uint32_t k[kOwnU], m[kOwnU];
-#pragma unroll
-    for (int u = 0; u < kOwnU; ++u) {
-      const int64_t i = i0 + u * stride;
-      ok[u] = i < n;
-      j[u] = ok[u] ? idiv(i, d4) : 0;
-      c[u] = static_cast<int>(i - j[u] * d4);
-      k[u] = ok[u] ? __ldg(own_k + j[u]) : 0u;
+  // One (row, chunk) item per thread per round. The loads are issued in three dependent
+  // levels instead of a chain: (own_k, own_slot) by row; then the source mask, the local
+  // row, the step count and the [emb | m | v] state by key / slot; then the gradient rows
+  // and the bias corrections. The Adam state does not depend on the gradient sum, so it
+  // is in flight while the sources are read.
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += stride) {
+    const int64_t j = idiv(i, d4);
+    const int c = static_cast<int>(i - j * d4);
+    const uint32_t k = __ldg(own_k + j);
+    uint32_t s = 0;
+    if constexpr (ADAM) s = __ldg(a.own_slot + j);
+    const uint32_t m = __ldg(tm + k);
+    const int64_t lr = ((m >> me) & 1u) ? static_cast<int64_t>(__ldg(lpos + k)) : 0;
+    int t = 0;
+    int64_t o = 0;
+    float4 mm, vv, e;
+    if constexpr (ADAM) {
+      t = __ldg(a.steps + s) + 1;
+      o = static_cast<int64_t>(s) * 3 * d4 + c;  // [emb | m | v] rows
+      mm = a.mom[o];
+      vv = a.vel[o];
+      e = a.emb[o];
     }
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int u = 0; u < kOwnU; ++u) m[u] = ok[u] ? __ldg(tm + k[u]) : 0u;
-#pragma unroll
-    for (int u = 0; u < kOwnU; ++u) {
-      if (!ok[u]) continue;
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-      for (int w = 0; w < 8; ++w) {  // fixed source order (same as owner_reduce_kernel);
-        // unrolled over the 8 possible sources so soff[] stays in registers
-        if (w >= static_cast<int>(W) || !((m[u] >> w) & 1u)) continue;
-        float4 v;
-        if (w == static_cast<int>(me)) {
-          const int64_t lr = __ldg(lpos + k[u]);
-          v = dE[lr * d4 + c[u]];
-          if (fm.B) v = with_fm(v, fm, lr, c[u], d4);
-        } else {
-          v = __ldg(recvbuf + static_cast<int64_t>(soff[w] + __ldg(&sscan[j[u]].c[w])) * d4 + c[u]);
-        }
-        acc.x += v.x;
-        acc.y += v.y;
-        acc.z += v.z;
-        acc.w += v.w;
+    for (int w = 0; w < 8; ++w) {  // fixed source order (same as owner_reduce_kernel);
+      // unrolled over the 8 possible sources so soff[] stays in registers
+      if (w >= static_cast<int>(W) || !((m >> w) & 1u)) continue;
+      float4 v;
+      if (w == static_cast<int>(me)) {
+        v = dE[lr * d4 + c];
+        if (fm.B) v = with_fm(v, fm, lr, c, d4);
+      } else {
+        v = __ldg(recvbuf + static_cast<int64_t>(soff[w] + __ldg(&sscan[j].c[w])) * d4 + c);
       }
-      if constexpr (ADAM) {  // update_sparse, lazy per-row step count
-        const uint32_t s = __ldg(a.own_slot + j[u]);
-        const int t = __ldg(a.steps + s) + 1;
-        const float c1 = __ldg(a.bc1 + t), c2 = __ldg(a.bc2 + t);
-        const int64_t o = static_cast<int64_t>(s) * 3 * d4 + c[u];  // [emb | m | v] rows
-        float4 mm = a.mom[o], vv = a.vel[o], e = a.emb[o];
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    if constexpr (ADAM) {  // update_sparse, lazy per-row step count
+      const float c1 = __ldg(a.bc1 + t), c2 = __ldg(a.bc2 + t);
 #define SFB_ADAM(X)                                   \
   mm.X = a.b1 * mm.X + a.omb1 * acc.X;                \
   vv.X = a.b2 * vv.X + a.omb2 * acc.X * acc.X;        \
   e.X -= a.lr * (mm.X / c1) / (sqrtf(vv.X / c2) + a.eps);
-        SFB_ADAM(x) SFB_ADAM(y) SFB_ADAM(z) SFB_ADAM(w)
+      SFB_ADAM(x) SFB_ADAM(y) SFB_ADAM(z) SFB_ADAM(w)
 #undef SFB_ADAM
-        a.mom[o] = mm;
-        a.vel[o] = vv;
-        a.emb[o] = e;
-      } else {
-        g[i0 + u * stride] = acc;
-      }
+      a.mom[o] = mm;
+      a.vel[o] = vv;
+      a.emb[o] = e;
+    } else {
+      g[i] = acc;
     }
   }
 }
