@@ -526,10 +526,11 @@ __global__ void __launch_bounds__(256) push_rows_p2p_dev_kernel(
     }
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
-      uint32_t mm = m[u] & ((1u << W) - 1u);
-      while (mm) {
-        const int w = __ffs(mm) - 1;
-        mm &= mm - 1;
+      const uint32_t mm = m[u] & ((1u << W) - 1u);
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {  // unrolled over the 8 possible destinations: e_off[] and
+        // pr.E[] are indexed statically (no local-memory copy of either)
+        if (!((mm >> w) & 1u)) continue;
         const uint32_t pos = e_off[w] + __ldg(&sscan[j[u]].c[w]);
         pr.E[w][static_cast<int64_t>(pos) * d4 + c[u]] = v[u];
       }

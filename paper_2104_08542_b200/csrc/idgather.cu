@@ -34,14 +34,18 @@ __global__ void __launch_bounds__(256) push_ids_kernel(const uint64_t* __restric
                                  a.y < limit ? static_cast<uint32_t>(a.y) : 0u,
                                  b.x < limit ? static_cast<uint32_t>(b.x) : 0u,
                                  b.y < limit ? static_cast<uint32_t>(b.y) : 0u);
-      for (int w = 0; w < W; ++w) reinterpret_cast<uint4*>(pd.dst[w] + off)[q] = v;
+#pragma unroll
+      for (int w = 0; w < 8; ++w)  // static peer index: pd stays in the parameter bank
+        if (w < W) reinterpret_cast<uint4*>(pd.dst[w] + off)[q] = v;
     }
   } else {
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
       const uint64_t a = in[i];
       if (a >= limit) *bad = 1;
       const uint32_t v = a < limit ? static_cast<uint32_t>(a) : 0u;
-      for (int w = 0; w < W; ++w) pd.dst[w][off + i] = v;
+#pragma unroll
+      for (int w = 0; w < 8; ++w)
+        if (w < W) pd.dst[w][off + i] = v;
     }
   }
   __syncthreads();
