@@ -392,7 +392,16 @@ void sparse_adam(const uint32_t* own_k /* gradient row index, or null = j */,
   const float omb2 = static_cast<float>(1.0 - beta2);
   if ((d & 3) == 0) {
     const int64_t n = static_cast<int64_t>(n_own) * (d / 4);
-    sparse_adam_v4<<<wave_grid(n), 256, 0, s>>>(
+    // one wave of resident CTAs: a grid of 148 x 8 with 5 resident per SM (43 registers) ran
+    // the grid-stride loop in 1.6 waves, the last one at 60 % occupancy
+    static const int per_sm = [] {
+      int b = 0;
+      if (const char* e = std::getenv("SFCTR_ADAM_CTAS_PER_SM")) b = atoi(e);  // experiment switch
+      if (b <= 0) CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sparse_adam_v4, 256, 0));
+      return std::max(1, b);
+    }();
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 148 * per_sm)));
+    sparse_adam_v4<<<grid, 256, 0, s>>>(
         own_k, own_slot, d_n_own, n_own, d / 4, reinterpret_cast<const float4*>(dG),
         reinterpret_cast<float4*>(emb), reinterpret_cast<float4*>(mom),
         reinterpret_cast<float4*>(vel), steps, bc1, bc2, lr, beta1, beta2, omb1, omb2, eps, Bsum,
