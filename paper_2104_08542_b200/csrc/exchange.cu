@@ -671,7 +671,7 @@ __global__ void zero_rows_dev_kernel(float4* __restrict__ p, const int32_t* __re
 // ADAM: the owner's sum goes straight into the lazy Adam update of its cache slot (same
 // math as sparse_adam_v4, embed.cu) instead of being written to gown and read back.
 template <bool ADAM>
-__global__ void __launch_bounds__(256) owner_reduce_dev_kernel(
+__global__ void __launch_bounds__(256, 5) owner_reduce_dev_kernel(
     const uint32_t* __restrict__ own_k, const int32_t* __restrict__ n_ptr,
     const uint32_t* __restrict__ tm, const Cnt8* __restrict__ sscan,
     const int32_t* __restrict__ totals, uint32_t W, uint32_t me, const uint32_t* __restrict__ lpos,
@@ -819,7 +819,7 @@ void Exchange::backward_reduce_adam_dev(const uint32_t* d_own_k, int32_t n_bound
               reinterpret_cast<float4*>(ar.vel), ar.own_slot, ar.steps, ar.bc1, ar.bc2, ar.lr,
               ar.b1, ar.b2, ar.omb1, ar.omb2, ar.eps};
   owner_reduce_dev_kernel<true><<<std::max(1, std::min(ceil_div(static_cast<int64_t>(n_bound) * d4, 256),
-                                                       148 * 16)),
+                                                       148 * 15)),
                                   256, 0, s>>>(d_own_k, d_n_own, tm, sscan, totals, W, me, lpos,
                                                reinterpret_cast<const float4*>(dE),
                                                reinterpret_cast<const float4*>(buf), d4, nullptr,
