@@ -70,7 +70,8 @@ typedef struct sfctr_config {
   int32_t hidden_dim;            /* h  (hidden)          default 64 */
   /* B200 extensions (config keys in parentheses) */
   int32_t sync_mode;             /* (sync) allreduce (reference scheme) | alltoall (owner-routed) */
-  uint64_t host_table_rows;      /* (host_rows) pinned host-table rows per worker; 0 = ceil(vocab/W) */
+  uint64_t host_table_rows;      /* (host_rows) host-pool rows pinned up front per worker (the pool
+                                    of evicted rows grows on demand beyond it); 0 = none */
   int32_t run_mode;              /* (mode) sequential | pipelined — RunMode, config.hpp:30 */
 } sfctr_config;
 
@@ -207,8 +208,8 @@ int sfctr_trainer_prepare(sfctr_trainer* t, int64_t step, const uint64_t* d_feat
 int sfctr_trainer_train(sfctr_trainer* t, int64_t step, const uint8_t* d_labels, float* d_loss);
 /* The host-buffer step split in two, for a driver that keeps steps in flight
  * (pipelined mode overlaps the manager stage of step t+1 with step t's training):
- * submit enqueues the H2D copies of the inputs, the step and the D2H copy of its loss,
- * and returns; loss waits for that step's loss. At most four submitted steps may be
+ * submit enqueues the H2D copies of the inputs and the step (whose last kernel stores the
+ * loss straight into a mapped pinned slot: no D2H copy on the stream), and returns; loss waits for that step's loss. At most four submitted steps may be
  * outstanding: read the loss of step t before submitting step t+4 (else LOGIC). The
  * host input buffers must stay untouched until the step's loss has been read. */
 int sfctr_trainer_submit(sfctr_trainer* t, int64_t step, const uint64_t* features,
@@ -225,6 +226,10 @@ int sfctr_trainer_logits(sfctr_trainer* t, float* out);
  * last_use, admit_seq — CacheBuffer::slots() (cache_buffer.hpp:63). */
 int sfctr_trainer_cache_slots(sfctr_trainer* t, int32_t lane, uint64_t* feature,
                               int64_t* last_use, uint64_t* admit_seq);
+/* The same for slots [first, first + count) only (clamped to the capacity): large caches
+ * need not be copied whole. */
+int sfctr_trainer_cache_slots_range(sfctr_trainer* t, int32_t lane, uint64_t first, uint64_t count,
+                                    uint64_t* feature, int64_t* last_use, uint64_t* admit_seq);
 /* Free-slot count of a local lane (CacheBuffer::free_count, cache_buffer.hpp:56). */
 int sfctr_trainer_free_count(sfctr_trainer* t, int32_t lane, uint64_t* out);
 /* HostStore::snapshot_sorted (host_store.hpp:85-86) over every feature this
@@ -233,6 +238,16 @@ int sfctr_trainer_free_count(sfctr_trainer* t, int32_t lane, uint64_t* out);
  * velocity, fp32), steps [count]. */
 int sfctr_trainer_snapshot(sfctr_trainer* t, int64_t* count, uint64_t* features, float* rows,
                            int64_t* steps);
+/* HostStore::peek (host_store.hpp:69-70) for n features owned by this process, wherever
+ * their state lives (HBM cache slot or host pool): rows [n*3d] = embedding|momentum|
+ * velocity (fp32), steps [n] (adam_steps). A feature that was never touched, or that
+ * another process owns, is SFCTR_ERR_LOGIC. */
+int sfctr_trainer_peek_rows(sfctr_trainer* t, int64_t n, const uint64_t* features, float* rows,
+                            int64_t* steps);
+/* Dense parameters and their Adam state, each [P] = w1 [F*d*h] | b1 [h] | w2 [h] | b2 [1],
+ * and the dense Adam step (any pointer may be NULL). */
+int sfctr_trainer_dense_state(sfctr_trainer* t, float* params, float* m, float* v,
+                              int64_t* step);
 /* Dense (replicated) parameters: w1 [F*d*h] row-major (k, j), b1 [h], w2 [h], b2 [1]. */
 int sfctr_trainer_get_dense(sfctr_trainer* t, float* w1, float* b1, float* w2, float* b2);
 int sfctr_trainer_set_dense(sfctr_trainer* t, const float* w1, const float* b1, const float* w2,

@@ -293,15 +293,30 @@ void orc_dense_init(uint64_t seed, int K, int h, double* w1, double* b1, double*
 #define ORC_CHUNKS 16 /* fixed row chunks: summation order independent of threads */
 #define P_CLAMP 1e-7
 
-double orc_model_fwd_bwd(const double* x, const uint8_t* labels, int rows, int fields, int dim,
+/* dxabs / dabs (tests only, may be NULL): the same sums over |terms| — the condition
+ * scale of every gradient entry (dxabs [rows, F*d]; dabs [P] = |W1| | |b1| | |w2| | |b2|
+ * parts, summed over rows and divided like the gradients).
+ * dxamb / damb (with dxabs / dabs): the gradient mass behind ReLU decisions that fp32 does
+ * not determine — hidden units with |hpre| <= 1e-5 (|b1| + sum_k |x_k w_kj|), whose
+ * derivative may legitimately come out either way on the device: sum of |gz w2_j w_kj|
+ * (dx) and |x_k gz w2_j|, |gz w2_j| (W1, b1) over those units. *n_amb counts them. */
+#define AMB_RTOL 1e-5
+static double model_core(const double* x, const uint8_t* labels, int rows, int fields, int dim,
                          int hidden, const double* w1, const double* b1, const double* w2,
                          double b2, double* logits, double* dx, double* dw1, double* db1,
-                         double* dw2, double* db2, int num_threads) {
+                         double* dw2, double* db2, int num_threads, double* dxabs, double* dabs,
+                         double* dxamb, double* damb, int64_t* n_amb) {
   const int K = fields * dim, H = hidden;
   const int want_dense = (dw1 != NULL);
+  const int want_abs = want_dense && dabs != NULL;
   double loss_chunk[ORC_CHUNKS] = {0};
   double* pw1 = want_dense ? (double*)calloc((size_t)ORC_CHUNKS * K * H, sizeof(double)) : NULL;
   double* pv = want_dense ? (double*)calloc((size_t)ORC_CHUNKS * (2 * H + 1), sizeof(double)) : NULL;
+  double* paw1 = want_abs ? (double*)calloc((size_t)ORC_CHUNKS * K * H, sizeof(double)) : NULL;
+  double* pav = want_abs ? (double*)calloc((size_t)ORC_CHUNKS * (2 * H + 1), sizeof(double)) : NULL;
+  double* pmw1 = want_abs ? (double*)calloc((size_t)ORC_CHUNKS * K * H, sizeof(double)) : NULL;
+  double* pmv = want_abs ? (double*)calloc((size_t)ORC_CHUNKS * H, sizeof(double)) : NULL;
+  int64_t amb_chunk[ORC_CHUNKS] = {0};
   const double inv_rows = 1.0 / (double)rows;
 #ifdef _OPENMP
   if (num_threads > 0) omp_set_num_threads(num_threads);
@@ -312,6 +327,9 @@ double orc_model_fwd_bwd(const double* x, const uint8_t* labels, int rows, int f
     double* hpre = (double*)malloc(sizeof(double) * H);
     double* dh = (double*)malloc(sizeof(double) * H);
     double* s = (double*)malloc(sizeof(double) * dim);
+    double* sa = (double*)malloc(sizeof(double) * dim);
+    double* hsc = (double*)malloc(sizeof(double) * H);
+    double* da = (double*)malloc(sizeof(double) * H); /* |gz w2_j| of ambiguous units, else 0 */
     double lsum = 0;
     for (int r = r0; r < r1; ++r) {
       const double* xr = x + (size_t)r * K;
@@ -326,11 +344,12 @@ double orc_model_fwd_bwd(const double* x, const uint8_t* labels, int rows, int f
       for (int j = 0; j < H; ++j) mlp += (hpre[j] > 0 ? hpre[j] : 0) * w2[j];
       /* FM second order: sum_{i<j} <v_i,v_j> = 0.5 (|sum v|^2 - sum |v|^2) */
       double sq = 0;
-      for (int c2 = 0; c2 < dim; ++c2) s[c2] = 0;
+      for (int c2 = 0; c2 < dim; ++c2) s[c2] = sa[c2] = 0;
       for (int f = 0; f < fields; ++f)
         for (int c2 = 0; c2 < dim; ++c2) {
           const double v = xr[f * dim + c2];
           s[c2] += v;
+          sa[c2] += fabs(v);
           sq += v * v;
         }
       double ss = 0;
@@ -346,6 +365,21 @@ double orc_model_fwd_bwd(const double* x, const uint8_t* labels, int rows, int f
       /* d(mean loss)/dz; zero where the clamp is active */
       const double gz = clamped ? 0.0 : (p - y) * inv_rows;
       for (int j = 0; j < H; ++j) dh[j] = hpre[j] > 0 ? gz * w2[j] : 0.0;
+      int any_amb = 0;
+      if (dxabs) {
+        for (int j = 0; j < H; ++j) hsc[j] = fabs(b1[j]);
+        for (int k = 0; k < K; ++k) {
+          const double xv = fabs(xr[k]);
+          const double* wk = w1 + (size_t)k * H;
+          for (int j = 0; j < H; ++j) hsc[j] += xv * fabs(wk[j]);
+        }
+        for (int j = 0; j < H; ++j) {
+          const int amb = fabs(hpre[j]) <= AMB_RTOL * hsc[j];
+          da[j] = amb ? fabs(gz * w2[j]) : 0.0;
+          any_amb |= amb && da[j] > 0;
+          amb_chunk[c] += amb;
+        }
+      }
       if (dx) {
         double* dxr = dx + (size_t)r * K;
         for (int k = 0; k < K; ++k) {
@@ -354,6 +388,14 @@ double orc_model_fwd_bwd(const double* x, const uint8_t* labels, int rows, int f
           for (int j = 0; j < H; ++j) acc += dh[j] * wk[j];
           const int c2 = k % dim;
           dxr[k] = acc + gz * (s[c2] - xr[k]);
+          if (dxabs) {
+            double aa = 0, am = 0;
+            for (int j = 0; j < H; ++j) aa += fabs(dh[j] * wk[j]);
+            if (any_amb)
+              for (int j = 0; j < H; ++j) am += da[j] * fabs(wk[j]);
+            dxabs[(size_t)r * K + k] = aa + fabs(gz) * (sa[c2] + fabs(xr[k]));
+            dxamb[(size_t)r * K + k] = am;
+          }
         }
       }
       if (want_dense) {
@@ -369,12 +411,39 @@ double orc_model_fwd_bwd(const double* x, const uint8_t* labels, int rows, int f
           cv[H + j] += gz * (hpre[j] > 0 ? hpre[j] : 0);        /* dw2 */
         }
         cv[2 * H] += gz; /* db2 */
+        if (want_abs) {
+          double* aw1 = paw1 + (size_t)c * K * H;
+          double* av = pav + (size_t)c * (2 * H + 1);
+          for (int k = 0; k < K; ++k) {
+            const double xv = fabs(xr[k]);
+            double* wk = aw1 + (size_t)k * H;
+            for (int j = 0; j < H; ++j) wk[j] += xv * fabs(dh[j]);
+          }
+          for (int j = 0; j < H; ++j) {
+            av[j] += fabs(dh[j]);
+            av[H + j] += fabs(gz) * (hpre[j] > 0 ? hpre[j] : 0);
+          }
+          av[2 * H] += fabs(gz);
+          if (any_amb) {
+            double* mw1 = pmw1 + (size_t)c * K * H;
+            for (int k = 0; k < K; ++k) {
+              const double xv = fabs(xr[k]);
+              double* wk = mw1 + (size_t)k * H;
+              for (int j = 0; j < H; ++j) wk[j] += xv * da[j];
+            }
+            double* mv = pmv + (size_t)c * H;
+            for (int j = 0; j < H; ++j) mv[j] += da[j];
+          }
+        }
       }
     }
     loss_chunk[c] = lsum;
     free(hpre);
     free(dh);
     free(s);
+    free(sa);
+    free(hsc);
+    free(da);
   }
   double loss = 0;
   for (int c = 0; c < ORC_CHUNKS; ++c) loss += loss_chunk[c];
@@ -396,7 +465,39 @@ double orc_model_fwd_bwd(const double* x, const uint8_t* labels, int rows, int f
     free(pw1);
     free(pv);
   }
+  if (want_abs) {
+    memset(dabs, 0, sizeof(double) * ((size_t)K * H + 2 * H + 1));
+    memset(damb, 0, sizeof(double) * ((size_t)K * H + 2 * H + 1));
+    for (int c = 0; c < ORC_CHUNKS; ++c) {
+      const double* aw1 = paw1 + (size_t)c * K * H;
+      const double* mw1 = pmw1 + (size_t)c * K * H;
+      for (size_t i = 0; i < (size_t)K * H; ++i) {
+        dabs[i] += aw1[i];
+        damb[i] += mw1[i];
+      }
+      const double* av = pav + (size_t)c * (2 * H + 1);
+      for (int j = 0; j < 2 * H + 1; ++j) dabs[(size_t)K * H + j] += av[j];
+      const double* mv = pmv + (size_t)c * H;
+      for (int j = 0; j < H; ++j) damb[(size_t)K * H + j] += mv[j];
+    }
+    free(paw1);
+    free(pav);
+    free(pmw1);
+    free(pmv);
+  }
+  if (n_amb) {
+    *n_amb = 0;
+    for (int c = 0; c < ORC_CHUNKS; ++c) *n_amb += amb_chunk[c];
+  }
   return loss * inv_rows;
+}
+
+double orc_model_fwd_bwd(const double* x, const uint8_t* labels, int rows, int fields, int dim,
+                         int hidden, const double* w1, const double* b1, const double* w2,
+                         double b2, double* logits, double* dx, double* dw1, double* db1,
+                         double* dw2, double* db2, int num_threads) {
+  return model_core(x, labels, rows, fields, dim, hidden, w1, b1, w2, b2, logits, dx, dw1, db1,
+                    dw2, db2, num_threads, NULL, NULL, NULL, NULL, NULL);
 }
 
 /* ======================= HostStore / CacheBuffer / manager ======================= */
@@ -704,6 +805,10 @@ struct orc_sim {
   double *mw1, *vw1, *mb1, *vb1, *mw2, *vw2, mb2, vb2; /* dense Adam state */
   int64_t dense_steps;
   int64_t last_u;
+  /* tests: the last step's summed gradients and their condition scales (sums of |terms|) */
+  int keep_grads;
+  double *last_g, *last_gabs, *last_dg, *last_dgabs, *last_gamb, *last_dgamb;
+  int64_t last_amb;
 };
 
 orc_sim* orc_sim_create(const orc_config* cfg) {
@@ -740,6 +845,8 @@ orc_sim* orc_sim_create(const orc_config* cfg) {
 
 void orc_sim_destroy(orc_sim* s) {
   if (!s) return;
+  free(s->last_g); free(s->last_gabs); free(s->last_dg); free(s->last_dgabs);
+  free(s->last_gamb); free(s->last_dgamb);
   for (int w = 0; w < s->W; ++w) cache_free(&s->caches[w]);
   free(s->caches);
   host_free(&s->host);
@@ -832,18 +939,30 @@ int orc_sim_step(orc_sim* s, int64_t step, const uint64_t* features, const uint8
   double* dw = (double*)malloc(sizeof(double) * P);
   double* x = (double*)malloc(sizeof(double) * (size_t)b * K);
   double* dx = (double*)malloc(sizeof(double) * (size_t)b * K);
+  const int ka = s->keep_grads;
+  double* dxa = ka ? (double*)malloc(sizeof(double) * (size_t)b * K) : NULL;
+  double* gca = ka ? (double*)calloc((size_t)U * d, sizeof(double)) : NULL;
+  double* dwa = ka ? (double*)malloc(sizeof(double) * P) : NULL;
+  double* dsa = ka ? (double*)calloc(P, sizeof(double)) : NULL;
+  double* dxm = ka ? (double*)malloc(sizeof(double) * (size_t)b * K) : NULL;
+  double* gcm = ka ? (double*)calloc((size_t)U * d, sizeof(double)) : NULL;
+  double* dwm = ka ? (double*)malloc(sizeof(double) * P) : NULL;
+  double* dsm = ka ? (double*)calloc(P, sizeof(double)) : NULL;
+  int64_t amb_total = 0;
   double lossum = 0;
   for (int w = 0; w < W; ++w) {
     const int r0 = w * b; /* contiguous even split, vsi.cpp:48-52 */
+    int64_t amb_w = 0;
     for (int r = 0; r < b; ++r)
       for (int f = 0; f < F; ++f) {
         const uint64_t v = vids[(size_t)(r0 + r) * F + f];
         memcpy(x + (size_t)r * K + (size_t)f * d, gce + v * d, sizeof(double) * d);
       }
-    const double lw = orc_model_fwd_bwd(x, labels + r0, b, F, d, H, s->w1, s->b1, s->w2, s->b2,
-                                        logits ? logits + r0 : NULL, dx, dw, dw + (size_t)K * H,
-                                        dw + (size_t)K * H + H, dw + (size_t)K * H + 2 * H,
-                                        s->cfg.num_threads);
+    const double lw = model_core(x, labels + r0, b, F, d, H, s->w1, s->b1, s->w2, s->b2,
+                                 logits ? logits + r0 : NULL, dx, dw, dw + (size_t)K * H,
+                                 dw + (size_t)K * H + H, dw + (size_t)K * H + 2 * H,
+                                 s->cfg.num_threads, dxa, dwa, dxm, dwm, &amb_w);
+    amb_total += amb_w;
     if (!isfinite(lw)) {
       snprintf(g_err, sizeof g_err, "step %lld: non-finite loss", (long long)step);
       rc = 4;
@@ -859,10 +978,23 @@ int orc_sim_step(orc_sim* s, int64_t step, const uint64_t* features, const uint8
         const uint64_t v = vids[(size_t)(r0 + r) * F + f];
         const double* g = dx + (size_t)r * K + (size_t)f * d;
         for (int c = 0; c < d; ++c) lcg[v * d + c] += g[c] * scale;
+        if (ka) {
+          const double* ga = dxa + (size_t)r * K + (size_t)f * d;
+          const double* gm = dxm + (size_t)r * K + (size_t)f * d;
+          for (int c = 0; c < d; ++c) {
+            gca[v * d + c] += ga[c] * scale;
+            gcm[v * d + c] += gm[c] * scale;
+          }
+        }
       }
     /* grad_synchronize: ordered sum over workers */
     for (size_t i = 0; i < (size_t)U * d; ++i) gcg[i] += lcg[i];
     for (size_t i = 0; i < P; ++i) dsum[i] += dw[i];
+    if (ka)
+      for (size_t i = 0; i < P; ++i) {
+        dsa[i] += dwa[i];
+        dsm[i] += dwm[i];
+      }
   }
   s->led.inter += (int64_t)W * (orc_allreduce_bytes(U * d * 4, W) +
                                 orc_allreduce_bytes((int64_t)P * 4, W));
@@ -878,6 +1010,27 @@ int orc_sim_step(orc_sim* s, int64_t step, const uint64_t* features, const uint8
     }
   /* dense: mean over workers, then Adam with the global step */
   for (size_t i = 0; i < P; ++i) dsum[i] /= (double)W;
+  if (ka) {
+    for (size_t i = 0; i < P; ++i) {
+      dsa[i] /= (double)W;
+      dsm[i] /= (double)W;
+    }
+    free(s->last_g); free(s->last_gabs); free(s->last_dg); free(s->last_dgabs);
+    free(s->last_gamb); free(s->last_dgamb);
+    s->last_gamb = gcm;
+    s->last_dgamb = dsm;
+    s->last_amb = amb_total;
+    free(dxm);
+    free(dwm);
+    s->last_g = (double*)malloc(sizeof(double) * (size_t)U * d);
+    memcpy(s->last_g, gcg, sizeof(double) * (size_t)U * d);
+    s->last_gabs = gca;
+    s->last_dg = (double*)malloc(sizeof(double) * P);
+    memcpy(s->last_dg, dsum, sizeof(double) * P);
+    s->last_dgabs = dsa;
+    free(dxa);
+    free(dwa);
+  }
   s->dense_steps += 1;
   adam(s->w1, s->mw1, s->vw1, dsum, (size_t)K * H, s->dense_steps, &s->cfg);
   adam(s->b1, s->mb1, s->vb1, dsum + (size_t)K * H, (size_t)H, s->dense_steps, &s->cfg);
@@ -1007,4 +1160,102 @@ void orc_criteo_read_batch(const uint64_t* features, const uint8_t* labels, int6
     for (int f = 0; f < 26; ++f) out_f[(size_t)r * 26 + f] = features[src * 26 + f];
     src = (src + 1) % rows;
   }
+}
+
+/* ---- state access for per-step parity from identical state (tests only) ----
+ * The row of feature f lives in its owner's cache (f mod W) or the host table; a
+ * never-touched feature has no state (returns -1). */
+static entry_t* find_entry(orc_sim* s, uint64_t f) {
+  cache_t* c = &s->caches[f % (uint64_t)s->W];
+  const int64_t slot = cache_slot_of(c, f);
+  if (slot >= 0) return &c->slots[slot].entry;
+  int64_t* v = hm_find(&s->host.table, f);
+  return v ? &s->host.pool[*v] : NULL;
+}
+
+int64_t orc_sim_get_rows(orc_sim* s, int64_t n, const uint64_t* features, double* rows,
+                         int64_t* steps) {
+  const int d3 = 3 * s->d;
+  int64_t absent = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const entry_t* e = find_entry(s, features[i]);
+    if (!e) {  /* never touched: no state yet */
+      ++absent;
+      if (rows) memset(rows + i * d3, 0, sizeof(double) * d3);
+      if (steps) steps[i] = -1;
+      continue;
+    }
+    if (rows) memcpy(rows + i * d3, e->data, sizeof(double) * d3);
+    if (steps) steps[i] = e->steps;
+  }
+  return absent;
+}
+
+int orc_sim_set_rows(orc_sim* s, int64_t n, const uint64_t* features, const double* rows,
+                     const int64_t* steps) {
+  const int d3 = 3 * s->d;
+  for (int64_t i = 0; i < n; ++i) {
+    entry_t* e = find_entry(s, features[i]);
+    if (!e) {
+      snprintf(g_err, sizeof g_err, "feature %llu has no state", (unsigned long long)features[i]);
+      return -1;
+    }
+    if (rows) memcpy(e->data, rows + i * d3, sizeof(double) * d3);
+    if (steps) e->steps = steps[i];
+  }
+  return 0;
+}
+
+/* dense parameters and Adam moments, each [P] = W1 | b1 | w2 | b2, and the dense step */
+static void dense_io(orc_sim* s, double* p, double* m, double* v, int64_t* step, int set) {
+  const size_t kh = (size_t)s->K * s->H, H = (size_t)s->H;
+  double* bufs[3] = {p, m, v};
+  double* w1s[3] = {s->w1, s->mw1, s->vw1};
+  double* b1s[3] = {s->b1, s->mb1, s->vb1};
+  double* w2s[3] = {s->w2, s->mw2, s->vw2};
+  double* b2s[3] = {&s->b2, &s->mb2, &s->vb2};
+  for (int q = 0; q < 3; ++q) {
+    double* b = bufs[q];
+    if (!b) continue;
+    double* parts[4] = {w1s[q], b1s[q], w2s[q], b2s[q]};
+    const size_t lens[4] = {kh, H, H, 1};
+    size_t off = 0;
+    for (int k = 0; k < 4; ++k) {
+      if (set) memcpy(parts[k], b + off, sizeof(double) * lens[k]);
+      else memcpy(b + off, parts[k], sizeof(double) * lens[k]);
+      off += lens[k];
+    }
+  }
+  if (step) {
+    if (set) s->dense_steps = *step;
+    else *step = s->dense_steps;
+  }
+}
+void orc_sim_get_dense_state(orc_sim* s, double* p, double* m, double* v, int64_t* step) {
+  dense_io(s, p, m, v, step, 0);
+}
+void orc_sim_set_dense_state(orc_sim* s, const double* p, const double* m, const double* v,
+                             const int64_t* step) {
+  dense_io(s, (double*)p, (double*)m, (double*)v, (int64_t*)step, 1);
+}
+
+void orc_sim_keep_grads(orc_sim* s, int on) { s->keep_grads = on; }
+
+/* the last step's summed embedding gradients g [U*d] (global_ids order) with their
+ * condition scales gabs (sums of |terms|), and the dense gradients (worker mean) dg [P]
+ * with dgabs [P]; gamb / dgamb: the gradient mass behind fp32-undetermined ReLU decisions
+ * (model_core), n_amb: how many (row, unit) decisions were undetermined; 0, or -1 when
+ * keep_grads was off */
+int orc_sim_last_grads(const orc_sim* s, double* g, double* gabs, double* dg, double* dgabs,
+                       double* gamb, double* dgamb, int64_t* n_amb) {
+  if (!s->last_g) return -1;
+  const size_t ud = (size_t)s->last_u * s->d, P = (size_t)s->K * s->H + 2 * s->H + 1;
+  if (g) memcpy(g, s->last_g, sizeof(double) * ud);
+  if (gabs) memcpy(gabs, s->last_gabs, sizeof(double) * ud);
+  if (dg) memcpy(dg, s->last_dg, sizeof(double) * P);
+  if (dgabs) memcpy(dgabs, s->last_dgabs, sizeof(double) * P);
+  if (gamb) memcpy(gamb, s->last_gamb, sizeof(double) * ud);
+  if (dgamb) memcpy(dgamb, s->last_dgamb, sizeof(double) * P);
+  if (n_amb) *n_amb = s->last_amb;
+  return 0;
 }

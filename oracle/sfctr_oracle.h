@@ -116,6 +116,28 @@ void orc_sim_ledger(const orc_sim* s, int64_t out[4]);
 /* last step's VSI unique count */
 int64_t orc_sim_last_unique(const orc_sim* s);
 
+/* Per-step parity from identical state: read / overwrite the [emb|m|v] rows and adam
+ * step counts of touched features (wherever they live), and the dense parameters with
+ * their Adam moments ([P] = W1 | b1 | w2 | b2) and the dense step. get_rows returns the
+ * number of features without state (zero rows, step -1); set_rows returns 0, or -1 for a
+ * feature without state. */
+int64_t orc_sim_get_rows(orc_sim* s, int64_t n, const uint64_t* features, double* rows,
+                         int64_t* steps);
+int orc_sim_set_rows(orc_sim* s, int64_t n, const uint64_t* features, const double* rows,
+                     const int64_t* steps);
+void orc_sim_get_dense_state(orc_sim* s, double* p, double* m, double* v, int64_t* step);
+void orc_sim_set_dense_state(orc_sim* s, const double* p, const double* m, const double* v,
+                             const int64_t* step);
+
+/* keep the next steps' gradients and their condition scales (sums of |terms| over every
+ * addition that forms them) for orc_sim_last_grads: g / gabs [U*d] in global_ids order,
+ * dense dg / dgabs [P] (worker mean); gamb / dgamb: the gradient mass behind ReLU
+ * decisions fp32 does not determine (|hpre| <= 1e-5 (|b1| + sum |x w|)), n_amb: their
+ * count. Returns -1 when nothing was kept. */
+void orc_sim_keep_grads(orc_sim* s, int on);
+int orc_sim_last_grads(const orc_sim* s, double* g, double* gabs, double* dg, double* dgabs,
+                       double* gamb, double* dgamb, int64_t* n_amb);
+
 /* initial dense parameters: W1 ~ U(-a,a), a = sqrt(6/(K+h)),
  * stream derive_seed(seed,"dense_w1",0); w2 ~ U(-a2,a2), a2 = sqrt(6/(h+1)),
  * stream "dense_w2"; b1 = b2 = 0 */

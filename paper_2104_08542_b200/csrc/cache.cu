@@ -13,9 +13,12 @@
 //                   cache_buffer.cpp:41-42), admit_seq = seq0 + i, last_use = t
 //
 // Per-row state moves host <-> HBM by zero-copy loads/stores from the kernels
-// (PCIe); never-touched rows are initialised on the device with the
-// reference's initial_embedding stream (generator.cpp:110-115) instead of
-// being read over PCIe.
+// (PCIe) into a lazily grown pool of pinned host slabs (HostPool, cache.h);
+// never-touched rows are initialised on the device with the reference's
+// initial_embedding stream (generator.cpp:110-115) instead of being read over
+// PCIe, so only rows that were evicted at least once hold host memory. The
+// LRU victims are selected exactly by a last_use histogram + a threshold step
+// + a sort of the few candidates at or below it (never a sort over C slots).
 #include "cache.h"
 
 namespace sfb {
@@ -81,7 +84,7 @@ __global__ void probe_kernel(const uint32_t* __restrict__ own_k,
     own_slot[j] = s;
     miss[j] = 0;
   } else {
-    own_slot[j] = s;  // kOnHost / kNever until admit assigns the slot
+    own_slot[j] = s;  // host slot / kNever until admit assigns the slot
     own_f[j] = f;
     miss[j] = 1;
   }
@@ -119,42 +122,130 @@ __global__ void mark_window_kernel(const uint32_t* __restrict__ gids,
   if (s < C && atomicExch(mark + s, t) != t) atomicAdd(marked, 1);
 }
 
-// LRU key per slot: eligible = occupied && !needed_soon (pins are implied by
-// BSP stream order: batch t-1's update has completed before manage(t) runs).
-// old_cnt (nullable): number of eligible slots last used before step t-1, i.e. not
-// touched by the batch still training when the manager runs one step ahead
-// (pipelined mode); victims drawn only from those are the sequential-mode victims.
-__global__ void victim_keys_kernel(uint32_t C, const uint32_t* __restrict__ slot_feat,
-                                   const int32_t* __restrict__ mark, int32_t t,
-                                   const int32_t* __restrict__ last_use,
-                                   const uint64_t* __restrict__ admit_seq,
-                                   uint64_t* __restrict__ keys, uint32_t* __restrict__ ids,
-                                   int32_t* __restrict__ old_cnt) {
-  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  bool old = false;
-  if (s < C) {
-    const bool eligible = slot_feat[s] != kEmpty && mark[s] != t;
-    const int32_t lu = last_use[s];
-    keys[s] = eligible ? (static_cast<uint64_t>(lu + 1) << 40) | (admit_seq[s] & ((1ull << 40) - 1))
-                       : ~0ull;
-    ids[s] = s;
-    old = eligible && lu < t - 1;
-  }
-  if (old_cnt) {
-    const int n = __syncthreads_count(old);
-    if (threadIdx.x == 0 && n) atomicAdd(old_cnt, n);
+// LRU histogram over last_use of the eligible slots (occupied && !needed_soon; pins are
+// implied by BSP stream order: batch t-1's update has completed before manage(t) runs, and
+// the pipelined manager checks counters[kCntOld] before evicting). Slots admitted together
+// sit next to each other (LIFO free stack), so a warp's eligible lanes mostly share one
+// last_use: one atomic per distinct value per warp (match_any).
+__global__ void lru_hist_kernel(uint32_t C, const uint32_t* __restrict__ slot_feat,
+                                const int32_t* __restrict__ mark, int32_t t,
+                                const int32_t* __restrict__ last_use, uint32_t* __restrict__ hist) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t w0 = ((blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5) * 32;
+       w0 < C; w0 += nwarps * 32) {
+    const uint64_t s = w0 + lane;
+    bool el = false;
+    int32_t lu = 0;
+    if (s < C) {
+      el = slot_feat[s] != kEmpty && mark[s] != t;
+      if (el) lu = last_use[s];
+    }
+    const unsigned act = __ballot_sync(0xFFFFFFFFu, el);
+    if (el) {
+      const unsigned peers = __match_any_sync(act, lu);
+      if (lane == __ffs(peers) - 1) atomicAdd(hist + lu, static_cast<uint32_t>(__popc(peers)));
+    }
   }
 }
 
-// pull_parameters_to_host: one warp per victim, 16 B zero-copy stores to the
-// pinned host table; the slot goes on top of the free stack.
+// One block: the threshold step T = min{T : #(last_use <= T) >= n_evict} (t when fewer
+// eligible slots exist: the capacity deadlock is then flagged by the eviction kernel), and
+// #(last_use < t-1) for the pipelined manager.
+__global__ void __launch_bounds__(1024) lru_select_kernel(const uint32_t* __restrict__ hist,
+                                                          int32_t nbins, int32_t n_evict,
+                                                          int32_t t, int32_t* __restrict__ cnt) {
+  __shared__ uint64_t part[1024];
+  __shared__ int32_t found;
+  const int tid = threadIdx.x;
+  const int per = (nbins + 1023) / 1024;
+  const int lo = min(nbins, tid * per), hi = min(nbins, lo + per);
+  uint64_t sum = 0, old = 0;
+  for (int i = lo; i < hi; ++i) {
+    sum += hist[i];
+    if (i < t - 1) old += hist[i];
+  }
+  part[tid] = sum;
+  if (tid == 0) found = t;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {  // inclusive scan of the chunk sums
+    const uint64_t v = tid >= off ? part[tid - off] : 0;
+    __syncthreads();
+    part[tid] += v;
+    __syncthreads();
+  }
+  const uint64_t before = tid ? part[tid - 1] : 0;
+  if (before < static_cast<uint64_t>(n_evict) && part[tid] >= static_cast<uint64_t>(n_evict)) {
+    uint64_t run = before;
+    for (int i = lo; i < hi; ++i) {
+      run += hist[i];
+      if (run >= static_cast<uint64_t>(n_evict)) {
+        found = i;
+        break;
+      }
+    }
+  }
+  // old: reduce the per-thread counts
+  __syncthreads();
+  part[tid] = old;
+  __syncthreads();
+  for (int off = 512; off > 0; off >>= 1) {
+    if (tid < off) part[tid] += part[tid + off];
+    __syncthreads();
+  }
+  if (tid == 0) {
+    cnt[kCntSelT] = found;
+    cnt[kCntOld] = static_cast<int32_t>(part[0] < 0x7FFFFFFFull ? part[0] : 0x7FFFFFFFull);
+    cnt[kCntSelN] = 0;
+  }
+}
+
+// The victim candidates: eligible slots with last_use <= T, key (last_use, admit_seq).
+// At most n_evict - 1 + #(last_use == T) <= n_evict + umax of them (the slots last used at
+// step T were touched by that step's owned uniques). Unused entries keep the ~0 key.
+__global__ void lru_collect_kernel(uint32_t C, const uint32_t* __restrict__ slot_feat,
+                                   const int32_t* __restrict__ mark, int32_t t,
+                                   const int32_t* __restrict__ last_use,
+                                   const uint64_t* __restrict__ admit_seq,
+                                   int32_t* __restrict__ cnt, int64_t cap,
+                                   uint64_t* __restrict__ keys, uint32_t* __restrict__ ids) {
+  const int lane = threadIdx.x & 31;
+  const int32_t T = cnt[kCntSelT];
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t w0 = ((blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5) * 32;
+       w0 < C; w0 += nwarps * 32) {
+    const uint64_t s = w0 + lane;
+    bool take = false;
+    int32_t lu = 0;
+    if (s < C && slot_feat[s] != kEmpty && mark[s] != t) {
+      lu = last_use[s];
+      take = lu <= T;
+    }
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, take);
+    if (!m) continue;
+    int32_t base = 0;
+    if (lane == __ffs(m) - 1) base = atomicAdd(cnt + kCntSelN, __popc(m));
+    base = __shfl_sync(0xFFFFFFFFu, base, __ffs(m) - 1);
+    if (take) {
+      const int64_t pos = base + __popc(m & ((1u << lane) - 1u));
+      if (pos < cap) {
+        keys[pos] = (static_cast<uint64_t>(lu + 1) << 40) | (admit_seq[s] & ((1ull << 40) - 1));
+        ids[pos] = static_cast<uint32_t>(s);
+      }
+    }
+  }
+}
+
+// pull_parameters_to_host: one warp per victim, 16 B zero-copy stores into the victim's
+// host slot (its old one, or a new one from the pool); the slot goes on top of the free
+// stack.
 __global__ void evict_kernel(int32_t n_evict, const uint64_t* __restrict__ sorted_keys,
                              const uint32_t* __restrict__ sorted_ids, uint32_t* __restrict__ slot_feat,
                              uint32_t W, int d, const float* __restrict__ emb,
                              const float* __restrict__ mom, const float* __restrict__ vel,
-                             const int32_t* __restrict__ steps, float* __restrict__ host_rows,
-                             int32_t* __restrict__ host_steps, uint32_t* __restrict__ index,
-                             uint32_t* __restrict__ free_stack,
+                             const int32_t* __restrict__ steps, HostTab host,
+                             uint32_t* __restrict__ slot_host, int32_t* __restrict__ host_next,
+                             uint32_t* __restrict__ index, uint32_t* __restrict__ free_stack,
                              const int32_t* __restrict__ free_top_ptr, int32_t* __restrict__ err) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -166,7 +257,13 @@ __global__ void evict_kernel(int32_t n_evict, const uint64_t* __restrict__ sorte
   const uint32_t s = sorted_ids[warp];
   const uint32_t f = slot_feat[s];
   const uint64_t r = f / W;
-  float* dst = host_rows + r * 3 * d;
+  uint32_t h = 0;
+  if (lane == 0) {
+    h = slot_host[s];
+    if (h == kNoHost) h = static_cast<uint32_t>(atomicAdd(host_next, 1));
+  }
+  h = __shfl_sync(0xFFFFFFFFu, h, 0);
+  float* dst = host.row(h, 3 * d);
   const size_t so = static_cast<size_t>(s) * 3 * d;  // slot rows: [emb | m | v]
   if ((d & 3) == 0) {
     const int d4 = d >> 2;
@@ -182,9 +279,10 @@ __global__ void evict_kernel(int32_t n_evict, const uint64_t* __restrict__ sorte
     }
   }
   if (lane == 0) {
-    host_steps[r] = steps[s];
-    index[r] = kOnHost;
+    *host.step(h) = steps[s];
+    index[r] = kHostBit | h;
     slot_feat[s] = kEmpty;
+    slot_host[s] = kNoHost;
     free_stack[*free_top_ptr + warp] = s;
   }
 }
@@ -200,8 +298,8 @@ __global__ void admit_kernel(const int32_t* __restrict__ counters, int32_t n_evi
                              const uint32_t* __restrict__ work_f,
                              const uint32_t* __restrict__ work_w, uint32_t W, int d,
                              const uint32_t* __restrict__ free_stack,
-                             uint32_t* __restrict__ index, const float* __restrict__ host_rows,
-                             const int32_t* __restrict__ host_steps, uint64_t seed,
+                             uint32_t* __restrict__ index, HostTab host,
+                             uint32_t* __restrict__ slot_host, uint64_t seed,
                              uint64_t embed_hash, float* __restrict__ emb, float* __restrict__ mom,
                              float* __restrict__ vel, int32_t* __restrict__ steps,
                              uint32_t* __restrict__ slot_feat, int32_t* __restrict__ last_use,
@@ -230,13 +328,16 @@ __global__ void admit_kernel(const int32_t* __restrict__ counters, int32_t n_evi
     mark[my_s] = t;
     index[my_f / W] = my_s;
     own_slot[j] = my_s;
-    if (my_where == kOnHost) steps[my_s] = host_steps[my_f / W];
-    else {
+    if (on_host(my_where)) {
+      steps[my_s] = *host.step(my_where & ~kHostBit);
+      slot_host[my_s] = my_where & ~kHostBit;
+    } else {
       steps[my_s] = 0;
+      slot_host[my_s] = kNoHost;
       my_se = derive_seed_h(seed, embed_hash, my_f);  // HostStore::get_or_init (host_store.cpp:25-33)
     }
   }
-  const unsigned from_host = __ballot_sync(0xFFFFFFFFu, mine && my_where == kOnHost);
+  const unsigned from_host = __ballot_sync(0xFFFFFFFFu, mine && on_host(my_where));
   if (lane == 0 && from_host) atomicAdd(n_from_host, __popc(from_host));
   const int nrows = n_work - i0 < kAdmitRows ? static_cast<int>(n_work - i0) : kAdmitRows;
   const bool vec = (d & 3) == 0;
@@ -245,15 +346,14 @@ __global__ void admit_kernel(const int32_t* __restrict__ counters, int32_t n_evi
   for (int base = 0; base < items; base += 32) {  // uniform trip count: all lanes shuffle
     const int it = base + lane;
     const int k = it < items ? it / per : 0;
-    const uint32_t f = __shfl_sync(0xFFFFFFFFu, my_f, k);
     const uint32_t sl = __shfl_sync(0xFFFFFFFFu, my_s, k);
     const uint32_t where = __shfl_sync(0xFFFFFFFFu, my_where, k);
     const uint64_t se = __shfl_sync(0xFFFFFFFFu, my_se, k);
     if (it >= items) continue;
     const int c = it - k * per;  // chunk (or column) within the row
     const size_t so = static_cast<size_t>(sl) * 3 * d;  // slot rows: [emb | m | v]
-    if (where == kOnHost) {
-      const float* src = host_rows + static_cast<uint64_t>(f / W) * 3 * d;
+    if (on_host(where)) {
+      const float* src = host.row(where & ~kHostBit, 3 * d);
       if (vec) {
         const float4* s4 = reinterpret_cast<const float4*>(src);
         reinterpret_cast<float4*>(emb + so)[c] = s4[c];
@@ -297,8 +397,8 @@ __global__ void __launch_bounds__(256) swap_kernel(
     const uint64_t* __restrict__ sorted_keys, const uint32_t* __restrict__ sorted_ids,
     const uint32_t* __restrict__ work_j, const uint32_t* __restrict__ work_f,
     const uint32_t* __restrict__ work_w, uint32_t W, int d4,
-    const uint32_t* __restrict__ free_stack, uint32_t* __restrict__ index,
-    float4* __restrict__ host_rows, int32_t* __restrict__ host_steps, uint64_t seed,
+    const uint32_t* __restrict__ free_stack, uint32_t* __restrict__ index, HostTab host,
+    uint32_t* __restrict__ slot_host, int32_t* __restrict__ host_next, uint64_t seed,
     uint64_t embed_hash, float4* __restrict__ emb, float4* __restrict__ mom,
     float4* __restrict__ vel, int32_t* __restrict__ steps, uint32_t* __restrict__ slot_feat,
     int32_t* __restrict__ last_use, uint64_t* __restrict__ admit_seq,
@@ -329,6 +429,12 @@ __global__ void __launch_bounds__(256) swap_kernel(
     s = sorted_ids[vi];
     const uint32_t fo = slot_feat[s];
     const uint64_t ro = fo / W;
+    uint32_t ho = 0;  // the victim's host slot: its old one, or a new one from the pool
+    if (lane == 0) {
+      ho = slot_host[s];
+      if (ho == kNoHost) ho = static_cast<uint32_t>(atomicAdd(host_next, 1));
+    }
+    ho = __shfl_sync(0xFFFFFFFFu, ho, 0);
     const size_t so = static_cast<size_t>(s) * 3 * d4;
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
@@ -348,14 +454,14 @@ __global__ void __launch_bounds__(256) swap_kernel(
     if (lane == 0) {
       const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
       asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
-                       host_rows + ro * per),
+                       host.row(ho, 4 * per)),
                    "r"(sa), "r"(per * 16)
                    : "memory");
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
     if (lane == 0) {
-      host_steps[ro] = steps[s];
-      index[ro] = kOnHost;
+      *host.step(ho) = steps[s];
+      index[ro] = kHostBit | ho;
     }
   } else {
     s = free_stack[free_top - 1 - (i - n_evict)];
@@ -364,7 +470,7 @@ __global__ void __launch_bounds__(256) swap_kernel(
   const uint32_t where = work_w[i];
   const uint64_t r = f / W;
   const size_t so = static_cast<size_t>(s) * 3 * d4;
-  if (where == kOnHost) {
+  if (on_host(where)) {
     // refill by one TMA bulk load of the host row (one large PCIe read instead of 16 B SM
     // loads), completion tracked by the warp's mbarrier
     const int wid = threadIdx.x >> 5;
@@ -379,7 +485,7 @@ __global__ void __launch_bounds__(256) swap_kernel(
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
               static_cast<uint32_t>(__cvta_generic_to_shared(astage))),
-          "l"(host_rows + r * per), "r"(per * 16), "r"(bar)
+          "l"(host.row(where & ~kHostBit, 4 * per)), "r"(per * 16), "r"(bar)
           : "memory");
     }
     __syncwarp();
@@ -410,7 +516,8 @@ __global__ void __launch_bounds__(256) swap_kernel(
     }
   }
   if (lane == 0) {
-    steps[s] = where == kOnHost ? host_steps[r] : 0;
+    steps[s] = on_host(where) ? *host.step(where & ~kHostBit) : 0;
+    slot_host[s] = on_host(where) ? (where & ~kHostBit) : kNoHost;
     slot_feat[s] = f;
     last_use[s] = t;
     admit_seq[s] = seq0 + static_cast<uint64_t>(i);
@@ -418,7 +525,7 @@ __global__ void __launch_bounds__(256) swap_kernel(
     index[r] = s;
     own_slot[work_j[i]] = s;
   }
-  const unsigned fh = __ballot_sync(0xFFFFFFFFu, lane == 0 && where == kOnHost);
+  const unsigned fh = __ballot_sync(0xFFFFFFFFu, lane == 0 && on_host(where));
   if (lane == 0 && fh) atomicAdd(n_from_host, 1);
   // the staged row must be read (and written) before the warp's shared memory is released
   if (lane == 0 && i < n_evict) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -449,12 +556,75 @@ __global__ void fill_u32(uint32_t* p, uint64_t n, uint32_t v) {
 
 }  // namespace
 
-void CacheLane::init(uint64_t capacity, int dim, uint64_t owned_rows, uint64_t host_rows_cap,
+void HostPool::init(int dim, uint64_t owned_rows, uint64_t reserve_rows) {
+  d = dim;
+  // slab_rows = 2^shift: the largest power of two with slab_rows * 12d <= 256 MB, but no
+  // larger than the owned shard needs (small tables get small slabs)
+  const uint64_t row_bytes = 12ull * static_cast<uint64_t>(dim);
+  shift = 10;
+  while (shift < 30 && (2ull << shift) * row_bytes <= (256ull << 20) &&
+         (1ull << shift) < owned_rows)
+    ++shift;
+  CUDA_CHECK(cudaMalloc(&d_rows, sizeof(float*) * kMaxSlabs));
+  CUDA_CHECK(cudaMalloc(&d_steps, sizeof(int32_t*) * kMaxSlabs));
+  CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_rows_tab), sizeof(float*) * kMaxSlabs, 0));
+  CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_steps_tab), sizeof(int32_t*) * kMaxSlabs, 0));
+  cap = hi = 0;
+  if (reserve_rows) ensure(reserve_rows, nullptr);
+}
+
+void HostPool::ensure(uint64_t slots, cudaStream_t s) {
+  if (slots <= cap) return;
+  const uint64_t slab_rows = 1ull << shift;
+  const size_t first = rows_h.size();
+  while (cap < slots) {
+    if (rows_h.size() >= static_cast<size_t>(kMaxSlabs) || cap + slab_rows > (1ull << 31) - 1)
+      fail(kRun, "host pool exhausted: " + std::to_string(cap) + " evicted rows per worker");
+    float* r = nullptr;
+    int32_t* st = nullptr;
+    const size_t rb = sizeof(float) * slab_rows * 3 * d;
+    if (cudaHostAlloc(reinterpret_cast<void**>(&r), rb, cudaHostAllocMapped | cudaHostAllocPortable) !=
+            cudaSuccess ||
+        cudaHostAlloc(reinterpret_cast<void**>(&st), sizeof(int32_t) * slab_rows,
+                      cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+      cudaGetLastError();
+      if (r) cudaFreeHost(r);
+      fail(kRun, "cannot pin " + std::to_string(rb >> 20) + " MiB more for the host pool (" +
+                     std::to_string(cap) + " evicted rows held)");
+    }
+    float* rd = nullptr;
+    int32_t* sd = nullptr;
+    CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&rd), r, 0));
+    CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&sd), st, 0));
+    h_rows_tab[rows_h.size()] = rd;
+    h_steps_tab[rows_h.size()] = sd;
+    rows_h.push_back(r);
+    steps_h.push_back(st);
+    cap += slab_rows;
+  }
+  const size_t n = rows_h.size() - first;
+  CUDA_CHECK(cudaMemcpyAsync(d_rows + first, h_rows_tab + first, sizeof(float*) * n,
+                             cudaMemcpyHostToDevice, s));
+  CUDA_CHECK(cudaMemcpyAsync(d_steps + first, h_steps_tab + first, sizeof(int32_t*) * n,
+                             cudaMemcpyHostToDevice, s));
+  if (!s) CUDA_CHECK(cudaStreamSynchronize(nullptr));
+}
+
+void HostPool::release() {
+  for (float* p : rows_h) cudaFreeHost(p);
+  for (int32_t* p : steps_h) cudaFreeHost(p);
+  if (d_rows) cudaFree(d_rows);
+  if (d_steps) cudaFree(d_steps);
+  if (h_rows_tab) cudaFreeHost(h_rows_tab);
+  if (h_steps_tab) cudaFreeHost(h_steps_tab);
+  *this = HostPool();
+}
+
+void CacheLane::init(uint64_t capacity, int dim, uint64_t owned_rows, uint64_t host_reserve,
                      int64_t max_unique) {
   C = capacity;
   d = dim;
   rows = owned_rows;
-  host_cap = host_rows_cap;
   umax = max_unique > 0 ? max_unique : 1;
   const size_t cd = static_cast<size_t>(C) * d;
   // one [C x 3d] table: slot s holds [emb | m | v] contiguously (960 B at d = 80), so the
@@ -472,29 +642,17 @@ void CacheLane::init(uint64_t capacity, int dim, uint64_t owned_rows, uint64_t h
   CUDA_CHECK(cudaMemset(admit_seq, 0, sizeof(uint64_t) * C));
   CUDA_CHECK(cudaMalloc(&mark, sizeof(int32_t) * C));
   CUDA_CHECK(cudaMalloc(&free_stack, sizeof(uint32_t) * C));
+  CUDA_CHECK(cudaMalloc(&slot_host, sizeof(uint32_t) * C));
+  CUDA_CHECK(cudaMemset(slot_host, 0xFF, sizeof(uint32_t) * C));
   CUDA_CHECK(cudaMalloc(&index, sizeof(uint32_t) * rows));
   init_lane_kernel<<<592, 256>>>(static_cast<uint32_t>(C), slot_feat, last_use, mark, free_stack);
   CUDA_LAUNCH_CHECK();
   fill_u32<<<1184, 256>>>(index, rows, kNever);
   CUDA_LAUNCH_CHECK();
-  // pinned, mapped host table: [emb | m | v] per owned row + adam step counts. A cache that
-  // holds the whole owned shard never evicts, so no row ever lives on the host: no table.
-  if (C >= rows) host_cap = 0;
-  if (host_cap == 0) {
-    free_top = static_cast<int32_t>(C);
-    next_seq = 0;
-  }
-  const size_t hbytes = sizeof(float) * static_cast<size_t>(host_cap) * 3 * d;
-  if (host_cap > 0) {
-    if (cudaHostAlloc(reinterpret_cast<void**>(&host_rows), hbytes,
-                      cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
-      cudaGetLastError();
-      fail(kConfig, "cannot pin " + std::to_string(hbytes >> 20) +
-                        " MiB for the host table (set host_rows / vocab smaller)");
-    }
-    CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&host_steps), sizeof(int32_t) * host_cap,
-                             cudaHostAllocMapped | cudaHostAllocPortable));
-  }
+  // host pool: a cache that holds the whole owned shard never evicts, so no row ever lives
+  // on the host and nothing is pinned; otherwise `host_reserve` slots are pinned up front
+  // and the pool grows on demand at eviction steps
+  host.init(d, rows, C >= rows ? 0 : host_reserve);
   free_top = static_cast<int32_t>(C);
   next_seq = 0;
   // per-step scratch
@@ -511,12 +669,16 @@ void CacheLane::init(uint64_t capacity, int dim, uint64_t owned_rows, uint64_t h
   CUDA_CHECK(cudaMalloc(&own_f, sizeof(uint32_t) * umax));
   CUDA_CHECK(cudaMalloc(&work_f, sizeof(uint32_t) * umax));
   CUDA_CHECK(cudaMalloc(&work_w, sizeof(uint32_t) * umax));
-  CUDA_CHECK(cudaMalloc(&keys, sizeof(uint64_t) * C));
-  CUDA_CHECK(cudaMalloc(&keys_sorted, sizeof(uint64_t) * C));
-  CUDA_CHECK(cudaMalloc(&ids, sizeof(uint32_t) * C));
-  CUDA_CHECK(cudaMalloc(&ids_sorted, sizeof(uint32_t) * C));
   scan_bytes = scan_temp_bytes(umax);
-  sort_bytes = sort_pairs_temp_bytes(static_cast<int64_t>(C));
+  sort_bytes = 0;
+  if (C < rows) {  // evictions possible: LRU candidate lists of n_evict + umax <= 2 umax
+    cand_cap = 2 * umax;
+    CUDA_CHECK(cudaMalloc(&keys, sizeof(uint64_t) * cand_cap));
+    CUDA_CHECK(cudaMalloc(&keys_sorted, sizeof(uint64_t) * cand_cap));
+    CUDA_CHECK(cudaMalloc(&ids, sizeof(uint32_t) * cand_cap));
+    CUDA_CHECK(cudaMalloc(&ids_sorted, sizeof(uint32_t) * cand_cap));
+    sort_bytes = sort_pairs_temp_bytes(cand_cap);
+  }
   CUDA_CHECK(cudaMalloc(&temp, std::max(scan_bytes, sort_bytes)));
   CUDA_CHECK(cudaMalloc(&counters, sizeof(int32_t) * kCntWords));
   CUDA_CHECK(cudaMemset(counters, 0, sizeof(int32_t) * kCntWords));
@@ -529,6 +691,7 @@ void CacheLane::release() {
                   static_cast<void*>(steps), static_cast<void*>(slot_feat),
                   static_cast<void*>(last_use), static_cast<void*>(admit_seq),
                   static_cast<void*>(mark), static_cast<void*>(free_stack),
+                  static_cast<void*>(slot_host), static_cast<void*>(hist),
                   static_cast<void*>(index), static_cast<void*>(flag), static_cast<void*>(rank),
                   static_cast<void*>(own_k_set[0]), static_cast<void*>(own_slot_set[0]),
                   static_cast<void*>(own_k_set[1]), static_cast<void*>(own_slot_set[1]),
@@ -539,8 +702,7 @@ void CacheLane::release() {
                   static_cast<void*>(ids), static_cast<void*>(ids_sorted), temp,
                   static_cast<void*>(counters)})
     if (p) cudaFree(p);
-  if (host_rows) cudaFreeHost(host_rows);
-  if (host_steps) cudaFreeHost(host_steps);
+  host.release();
   *this = CacheLane();
 }
 
@@ -583,39 +745,63 @@ void CacheLane::probe(const uint32_t* d_gids, int32_t cap, uint32_t W, int32_t t
   CUDA_LAUNCH_CHECK();
 }
 
-void CacheLane::victim_keys(int32_t t, bool count_old, cudaStream_t s) {
-  victim_keys_kernel<<<ceil_div(C, 256), 256, 0, s>>>(static_cast<uint32_t>(C), slot_feat, mark, t,
-                                                      last_use, admit_seq, keys, ids,
-                                                      count_old ? counters + kCntOld : nullptr);
+void CacheLane::victim_select(int32_t t, int32_t n_evict, cudaStream_t s) {
+  const int64_t nbins = static_cast<int64_t>(t) + 1;
+  if (nbins > hist_cap) {  // bins = steps so far (grows geometrically; rare)
+    int64_t cap2 = std::max<int64_t>(4096, hist_cap);
+    while (cap2 < nbins) cap2 *= 2;
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    if (hist) CUDA_CHECK(cudaFree(hist));
+    CUDA_CHECK(cudaMalloc(&hist, sizeof(uint32_t) * cap2));
+    hist_cap = cap2;
+  }
+  CUDA_CHECK(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * nbins, s));
+  const int grid = static_cast<int>(std::min<int64_t>(ceil_div(static_cast<int64_t>(C), 256), 148 * 8));
+  lru_hist_kernel<<<grid, 256, 0, s>>>(static_cast<uint32_t>(C), slot_feat, mark, t, last_use, hist);
+  CUDA_LAUNCH_CHECK();
+  lru_select_kernel<<<1, 1024, 0, s>>>(hist, static_cast<int32_t>(nbins), n_evict, t, counters);
   CUDA_LAUNCH_CHECK();
 }
 
-void CacheLane::evict(int32_t n_evict, uint32_t W, int32_t t, cudaStream_t s, bool keys_ready) {
+void CacheLane::victim_sort(int32_t t, int32_t n_evict, cudaStream_t s) {
+  const int64_t bound = std::min<int64_t>(cand_cap, static_cast<int64_t>(n_evict) + umax);
+  CUDA_CHECK(cudaMemsetAsync(keys, 0xFF, sizeof(uint64_t) * bound, s));
+  const int grid = static_cast<int>(std::min<int64_t>(ceil_div(static_cast<int64_t>(C), 256), 148 * 8));
+  lru_collect_kernel<<<grid, 256, 0, s>>>(static_cast<uint32_t>(C), slot_feat, mark, t, last_use,
+                                          admit_seq, counters, bound, keys, ids);
+  CUDA_LAUNCH_CHECK();
+  sort_pairs_u64_u32(temp, sort_bytes, keys, keys_sorted, ids, ids_sorted, bound, 64, s);
+}
+
+void CacheLane::evict(int32_t n_evict, uint32_t W, int32_t t, cudaStream_t s, bool selected) {
   if (n_evict <= 0) return;
-  if (!keys_ready) victim_keys(t, false, s);
-  sort_pairs_u64_u32(temp, sort_bytes, keys, keys_sorted, ids, ids_sorted,
-                     static_cast<int64_t>(C), 64, s);
+  if (!selected) victim_select(t, n_evict, s);
+  victim_sort(t, n_evict, s);
   evict_kernel<<<ceil_div(static_cast<int64_t>(n_evict) * 32, 256), 256, 0, s>>>(
-      n_evict, keys_sorted, ids_sorted, slot_feat, W, d, emb, mom, vel, steps, host_rows,
-      host_steps, index, free_stack, counters + kCntFreeTop, counters + kCntError);
+      n_evict, keys_sorted, ids_sorted, slot_feat, W, d, emb, mom, vel, steps, host.tab(),
+      slot_host, counters + kCntHostNext, index, free_stack, counters + kCntFreeTop,
+      counters + kCntError);
   CUDA_LAUNCH_CHECK();
 }
 
 bool CacheLane::swap_supported() const { return (d & 3) == 0 && 3 * (d / 4) <= 64; }
 
 void CacheLane::evict_admit(int32_t n_evict, int32_t n_work, uint32_t W, uint64_t seed, int32_t t,
-                            cudaStream_t s, bool keys_ready) {
+                            cudaStream_t s, bool selected) {
+  if (n_evict > 0) {  // every victim may need a new host slot
+    host.ensure(host.hi + static_cast<uint64_t>(n_evict), s);
+    host.hi += static_cast<uint64_t>(n_evict);
+  }
   if (n_evict <= 0 || !swap_supported()) {
-    evict(n_evict, W, t, s, keys_ready);
+    evict(n_evict, W, t, s, selected);
     admit(n_work, n_evict, W, seed, t, s);
     return;
   }
-  if (!keys_ready) victim_keys(t, false, s);
-  sort_pairs_u64_u32(temp, sort_bytes, keys, keys_sorted, ids, ids_sorted,
-                     static_cast<int64_t>(C), 64, s);
+  if (!selected) victim_select(t, n_evict, s);
+  victim_sort(t, n_evict, s);
   swap_kernel<<<ceil_div(static_cast<int64_t>(n_work) * 32, 256), 256, 0, s>>>(
       counters, n_evict, keys_sorted, ids_sorted, work_j, work_f, work_w, W, d / 4, free_stack,
-      index, reinterpret_cast<float4*>(host_rows), host_steps, seed, fnv1a64("embed"),
+      index, host.tab(), slot_host, counters + kCntHostNext, seed, fnv1a64("embed"),
       reinterpret_cast<float4*>(emb), reinterpret_cast<float4*>(mom),
       reinterpret_cast<float4*>(vel), steps, slot_feat, last_use, admit_seq, mark, t, own_slot,
       counters + kCntFromHost, counters + kCntError);
@@ -629,7 +815,7 @@ void CacheLane::admit(int32_t n_bound, int32_t n_evict, uint32_t W, uint64_t see
   if (n_bound > 0) {
     admit_kernel<<<ceil_div(ceil_div(static_cast<int64_t>(n_bound), kAdmitRows) * 32, 256), 256, 0,
                    s>>>(counters, n_evict, work_j, work_f, work_w, W, d, free_stack, index,
-                        host_rows, host_steps, seed, fnv1a64("embed"), emb, mom, vel, steps,
+                        host.tab(), slot_host, seed, fnv1a64("embed"), emb, mom, vel, steps,
                         slot_feat, last_use, admit_seq, mark, t, own_slot,
                         counters + kCntFromHost);
     CUDA_LAUNCH_CHECK();

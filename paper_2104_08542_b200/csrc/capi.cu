@@ -582,6 +582,27 @@ int sfctr_trainer_cache_slots(sfctr_trainer* t, int32_t lane, uint64_t* feature,
   });
 }
 
+int sfctr_trainer_cache_slots_range(sfctr_trainer* t, int32_t lane, uint64_t first, uint64_t count,
+                                    uint64_t* feature, int64_t* last_use, uint64_t* admit_seq) {
+  return guarded([&] {
+    SFB_CHECK(lane >= 0 && lane < t->t->lanes(), "lane out of range");
+    t->t->cache_slots(lane, feature, last_use, admit_seq, first, count);
+  });
+}
+
+int sfctr_trainer_peek_rows(sfctr_trainer* t, int64_t n, const uint64_t* features, float* rows,
+                            int64_t* steps) {
+  return guarded([&] {
+    SFB_CHECK(n >= 0 && (n == 0 || features), "features");
+    t->t->peek_rows(n, features, rows, steps);
+  });
+}
+
+int sfctr_trainer_dense_state(sfctr_trainer* t, float* params, float* m, float* v,
+                              int64_t* step) {
+  return guarded([&] { t->t->dense_state(params, m, v, step); });
+}
+
 int sfctr_trainer_free_count(sfctr_trainer* t, int32_t lane, uint64_t* out) {
   return guarded([&] {
     SFB_CHECK(lane >= 0 && lane < t->t->lanes(), "lane out of range");

@@ -104,9 +104,15 @@ __device__ __forceinline__ int64_t idiv(int64_t a, int b) {
 }
 #endif
 
-// Slot / index sentinels of the device MixCache.
-constexpr uint32_t kEmpty = 0xFFFFFFFFu;   // slot_feature of a free slot
-constexpr uint32_t kNever = 0xFFFFFFFFu;   // index[r]: row never touched (lazy init on admit)
-constexpr uint32_t kOnHost = 0xFFFFFFFEu;  // index[r]: row lives in the pinned host table
+// Slot / index sentinels of the device MixCache. index[r] of owned row r is a cache slot
+// (< kHostBit: capacities stay below 2^31), kNever, or kHostBit | h: the row lives in host
+// slot h of the pinned host pool (HostStore, host_store.hpp:61-92).
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;     // slot_feature of a free slot
+constexpr uint32_t kNever = 0xFFFFFFFFu;     // index[r]: row never touched (lazy init on admit)
+constexpr uint32_t kHostBit = 0x80000000u;   // index[r] = kHostBit | host slot
+constexpr uint32_t kNoHost = 0xFFFFFFFFu;    // slot_host[s]: the row has no host slot yet
+__host__ __device__ inline bool on_host(uint32_t where) {
+  return (where & kHostBit) && where != kNever;
+}
 
 }  // namespace sfb

@@ -668,15 +668,20 @@ __global__ void zero_rows_dev_kernel(float4* __restrict__ p, const int32_t* __re
   }
 }
 
-// ADAM: the owner's sum goes straight into the lazy Adam update of its cache slot (same
-// math as sparse_adam_v4, embed.cu) instead of being written to gown and read back.
-template <bool ADAM>
-__global__ void __launch_bounds__(256, 5) owner_reduce_dev_kernel(
+// The owner's sum goes straight into the lazy Adam update of its cache slot (same math as
+// sparse_adam_v4, embed.cu) instead of being written to gown and read back.
+//
+// Deferred FM term of the owner's OWN rows: -scale * B[r] * E[r] with E[r] the row this rank
+// pushed into its own receive table in the forward, i.e. emb[own_slot[j]] before this
+// update. It is taken from the cache row loaded here, never from E: after the gradient
+// barrier a faster peer may already be storing its step t+1 forward rows into E (the
+// owner-major block offsets move between steps), so E is not read past that barrier.
+__global__ void __launch_bounds__(256, 5) owner_reduce_adam_dev_kernel(
     const uint32_t* __restrict__ own_k, const int32_t* __restrict__ n_ptr,
     const uint32_t* __restrict__ tm, const Cnt8* __restrict__ sscan,
     const int32_t* __restrict__ totals, uint32_t W, uint32_t me, const uint32_t* __restrict__ lpos,
     const float4* __restrict__ dE, const float4* __restrict__ recvbuf, int d4,
-    float4* __restrict__ g, FmDefer fm, OwnerAdam a) {
+    const float* __restrict__ fmB, float fm_scale, OwnerAdam a) {
   const int64_t n = static_cast<int64_t>(*n_ptr) * d4;
   uint32_t soff[8];  // start of source w's block in my receive buffer
   uint32_t run = 0;
@@ -696,20 +701,14 @@ __global__ void __launch_bounds__(256, 5) owner_reduce_dev_kernel(
     const int64_t j = idiv(i, d4);
     const int c = static_cast<int>(i - j * d4);
     const uint32_t k = __ldg(own_k + j);
-    uint32_t s = 0;
-    if constexpr (ADAM) s = __ldg(a.own_slot + j);
+    const uint32_t s = __ldg(a.own_slot + j);
     const uint32_t m = __ldg(tm + k);
     const int64_t lr = ((m >> me) & 1u) ? static_cast<int64_t>(__ldg(lpos + k)) : 0;
-    int t = 0;
-    int64_t o = 0;
-    float4 mm, vv, e;
-    if constexpr (ADAM) {
-      t = __ldg(a.steps + s) + 1;
-      o = static_cast<int64_t>(s) * 3 * d4 + c;  // [emb | m | v] rows
-      mm = a.mom[o];
-      vv = a.vel[o];
-      e = a.emb[o];
-    }
+    const int t = __ldg(a.steps + s) + 1;
+    const int64_t o = static_cast<int64_t>(s) * 3 * d4 + c;  // [emb | m | v] rows
+    float4 mm = a.mom[o];
+    float4 vv = a.vel[o];
+    float4 e = a.emb[o];
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int w = 0; w < 8; ++w) {  // fixed source order (same as owner_reduce_kernel);
@@ -718,7 +717,13 @@ __global__ void __launch_bounds__(256, 5) owner_reduce_dev_kernel(
       float4 v;
       if (w == static_cast<int>(me)) {
         v = dE[lr * d4 + c];
-        if (fm.B) v = with_fm(v, fm, lr, c, d4);
+        if (fmB) {
+          const float kk = fm_scale * __ldg(fmB + lr);
+          v.x -= kk * e.x;
+          v.y -= kk * e.y;
+          v.z -= kk * e.z;
+          v.w -= kk * e.w;
+        }
       } else {
         v = __ldg(recvbuf + static_cast<int64_t>(soff[w] + __ldg(&sscan[j].c[w])) * d4 + c);
       }
@@ -727,20 +732,17 @@ __global__ void __launch_bounds__(256, 5) owner_reduce_dev_kernel(
       acc.z += v.z;
       acc.w += v.w;
     }
-    if constexpr (ADAM) {  // update_sparse, lazy per-row step count
-      const float c1 = __ldg(a.bc1 + t), c2 = __ldg(a.bc2 + t);
+    // update_sparse, lazy per-row step count
+    const float c1 = __ldg(a.bc1 + t), c2 = __ldg(a.bc2 + t);
 #define SFB_ADAM(X)                                   \
   mm.X = a.b1 * mm.X + a.omb1 * acc.X;                \
   vv.X = a.b2 * vv.X + a.omb2 * acc.X * acc.X;        \
   e.X -= a.lr * (mm.X / c1) / (sqrtf(vv.X / c2) + a.eps);
-      SFB_ADAM(x) SFB_ADAM(y) SFB_ADAM(z) SFB_ADAM(w)
+    SFB_ADAM(x) SFB_ADAM(y) SFB_ADAM(z) SFB_ADAM(w)
 #undef SFB_ADAM
-      a.mom[o] = mm;
-      a.vel[o] = vv;
-      a.emb[o] = e;
-    } else {
-      g[i] = acc;
-    }
+    a.mom[o] = mm;
+    a.vel[o] = vv;
+    a.emb[o] = e;
   }
 }
 
@@ -795,36 +797,19 @@ void Exchange::backward_send_dev(const float* dE, cudaStream_t s, const float* E
   CUDA_LAUNCH_CHECK();
 }
 
-void Exchange::backward_reduce_dev(const uint32_t* d_own_k, int32_t n_bound, const int32_t* d_n_own,
-                                   const float* dE, cudaStream_t s, const float* E, const float* B,
-                                   float fm_scale) {
-  const int d4 = d / 4;
-  owner_reduce_dev_kernel<false><<<std::max(1, std::min(ceil_div(static_cast<int64_t>(n_bound) * d4, 512),
-                                                 148 * 16)),
-                            256, 0, s>>>(d_own_k, d_n_own, tm, sscan, totals, W, me, lpos,
-                                         reinterpret_cast<const float4*>(dE),
-                                         reinterpret_cast<const float4*>(buf), d4,
-                                         reinterpret_cast<float4*>(gown),
-                                         FmDefer{reinterpret_cast<const float4*>(E), B, fm_scale},
-                                         OwnerAdam{});
-  CUDA_LAUNCH_CHECK();
-}
-
 void Exchange::backward_reduce_adam_dev(const uint32_t* d_own_k, int32_t n_bound,
                                         const int32_t* d_n_own, const float* dE, cudaStream_t s,
-                                        const float* E, const float* B, float fm_scale,
-                                        const AdamRows& ar) {
+                                        const float* B, float fm_scale, const AdamRows& ar) {
   const int d4 = d / 4;
   OwnerAdam a{reinterpret_cast<float4*>(ar.emb), reinterpret_cast<float4*>(ar.mom),
               reinterpret_cast<float4*>(ar.vel), ar.own_slot, ar.steps, ar.bc1, ar.bc2, ar.lr,
               ar.b1, ar.b2, ar.omb1, ar.omb2, ar.eps};
-  owner_reduce_dev_kernel<true><<<std::max(1, std::min(ceil_div(static_cast<int64_t>(n_bound) * d4, 256),
-                                                       148 * 15)),
-                                  256, 0, s>>>(d_own_k, d_n_own, tm, sscan, totals, W, me, lpos,
-                                               reinterpret_cast<const float4*>(dE),
-                                               reinterpret_cast<const float4*>(buf), d4, nullptr,
-                                               FmDefer{reinterpret_cast<const float4*>(E), B, fm_scale},
-                                               a);
+  owner_reduce_adam_dev_kernel<<<std::max(1, std::min(ceil_div(static_cast<int64_t>(n_bound) * d4, 256),
+                                                      148 * 15)),
+                                 256, 0, s>>>(d_own_k, d_n_own, tm, sscan, totals, W, me, lpos,
+                                              reinterpret_cast<const float4*>(dE),
+                                              reinterpret_cast<const float4*>(buf), d4, B,
+                                              fm_scale, a);
   CUDA_LAUNCH_CHECK();
 }
 

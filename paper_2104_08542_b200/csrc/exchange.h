@@ -98,9 +98,6 @@ struct Exchange {
   // r; both the push to the owners and the owner's reduction add it
   void backward_send_dev(const float* dE, cudaStream_t s, const float* E = nullptr,
                          const float* B = nullptr, float fm_scale = 0.f);
-  void backward_reduce_dev(const uint32_t* d_own_k, int32_t n_bound, const int32_t* d_n_own,
-                           const float* dE, cudaStream_t s, const float* E = nullptr,
-                           const float* B = nullptr, float fm_scale = 0.f);
   // the owner's reduction fused with the lazy Adam update of its rows (no gown round trip)
   struct AdamRows {
     float *emb, *mom, *vel;
@@ -109,9 +106,11 @@ struct Exchange {
     const float *bc1, *bc2;
     float lr, b1, b2, omb1, omb2, eps;
   };
+  // B != nullptr: add the deferred FM term of the owner's own rows, taken from the cache
+  // row itself (E is not read: peers may already be filling it for the next step)
   void backward_reduce_adam_dev(const uint32_t* d_own_k, int32_t n_bound, const int32_t* d_n_own,
-                                const float* dE, cudaStream_t s, const float* E, const float* B,
-                                float fm_scale, const AdamRows& ar);
+                                const float* dE, cudaStream_t s, const float* B, float fm_scale,
+                                const AdamRows& ar);
   // dE[0 : local rows) = 0 (and B[0 : local rows) when given), row count read on the device
   void zero_local_dev(float* dE, cudaStream_t s, float* B = nullptr);
   bool device_driven() const { return p2p && !copy_engine; }

@@ -59,7 +59,7 @@ void validate_config(const sfctr_config& c) {  // config.cpp:55-78 + device limi
   require(c.strategy == SFCTR_STRATEGY_CACHE,
           "the device path implements the cache strategy (host/prefetch are simulator-only)");
   require(c.vocabulary_size < 0xFFFFFFF0ull, "vocab must fit 32-bit device feature ids");
-  require(c.cache_capacity < 0xFFFFFFF0ull, "cache-capacity must fit 32-bit slots");
+  require(c.cache_capacity < 0x7FFFFFF0ull, "cache-capacity must fit 31-bit slots");
   require(static_cast<int64_t>(c.num_workers) * c.batch_size_per_worker * c.num_fields <
               (1ll << 31),
           "global batch ids must fit 31 bits");
@@ -208,13 +208,11 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
   tower_fused_ = !tower_simt_ && tower_fused_supported(d_) && tf && tf[0] == '1';
 
   const uint64_t owned_rows = (cfg_.vocabulary_size + W_ - 1) / W_;
-  const uint64_t host_rows = cfg_.host_table_rows ? cfg_.host_table_rows : owned_rows;
-  if (host_rows < owned_rows)
-    fail(kConfig, "host_rows must cover ceil(vocab / workers) rows (direct-mapped host table)");
   lane_.resize(lanes_);
   const int64_t umax = std::min<int64_t>(n_global_, static_cast<int64_t>(cfg_.vocabulary_size));
+  // host_rows: host-pool slots pinned up front per lane (the pool grows on demand)
   for (int l = 0; l < lanes_; ++l)
-    lane_[l].init(cfg_.cache_capacity, d_, owned_rows, host_rows, umax);
+    lane_[l].init(cfg_.cache_capacity, d_, owned_rows, cfg_.host_table_rows, umax);
   free_lb_.assign(lanes_, static_cast<int64_t>(cfg_.cache_capacity));
   if (world_ > 1 && cfg_.sync_mode == SFCTR_SYNC_ALLTOALL) {
     if (lanes_ != 1) fail(kConfig, "sync=alltoall needs one worker per process");
@@ -625,12 +623,12 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
     // are older than t-1 those victims are all among them and eviction overlaps step t-1.
     // Otherwise the manager waits for step t-1 to finish first. Either way the victims,
     // and so every result, equal sequential mode's.
-    bool keys_ready = false;
+    bool selected = false;
     if (piped && train_pending_[k ^ 1]) {
       bool any = false;
       for (int l = 0; l < lanes_; ++l)
         if (n_work[l] > lane_[l].free_top) {
-          lane_[l].victim_keys(t, /*count_old=*/true, sm);
+          lane_[l].victim_select(t, n_work[l] - lane_[l].free_top, sm);
           CUDA_CHECK(cudaMemcpyAsync(h_counts_ + kCntWords * l + kCntOld,
                                      lane_[l].counters + kCntOld, sizeof(int32_t),
                                      cudaMemcpyDeviceToHost, sm));
@@ -638,7 +636,7 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
         }
       if (any) {
         CUDA_CHECK(cudaStreamSynchronize(sm));
-        keys_ready = true;
+        selected = true;
         bool wait = false;
         for (int l = 0; l < lanes_; ++l)
           wait |= n_work[l] - lane_[l].free_top > h_counts_[kCntWords * l + kCntOld];
@@ -651,7 +649,7 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
     for (int l = 0; l < lanes_; ++l) {
       CacheLane& L = lane_[l];
       const int32_t n_evict = std::max<int32_t>(0, n_work[l] - L.free_top);
-      L.evict_admit(n_evict, n_work[l], Wu, cfg_.seed, t, sm, keys_ready);
+      L.evict_admit(n_evict, n_work[l], Wu, cfg_.seed, t, sm, selected && n_evict > 0);
       free_lb_[l] = static_cast<int64_t>(L.free_top) + n_evict - n_work[l];
       led_[0] += static_cast<int64_t>(n_work[l]) * d_ * 12;
       led_[1] += static_cast<int64_t>(n_evict) * d_ * 12;
@@ -881,7 +879,7 @@ void Trainer::train(int64_t step, const uint8_t* d_labels, float* d_loss) {
                           static_cast<float>(1.0 - cfg_.adam_beta2),
                           static_cast<float>(cfg_.adam_epsilon)};
     xch_.backward_reduce_adam_dev(lane_[0].own_k, n_own[0], snap_cnt(0) + kCntOwned, d_dG_, s,
-                                  xfm ? d_G_ : nullptr, xfm ? d_B_ : nullptr, emb_scale, ar);
+                                  xfm ? d_B_ : nullptr, emb_scale, ar);
   }
   for (int l = 0; l < lanes_ && !fused_adam; ++l)
     sparse_adam(a2a_ ? nullptr : lane_[l].own_k, lane_[l].own_slot, n_own[l],
@@ -1114,68 +1112,184 @@ void Trainer::logits(float* out) {
   CUDA_CHECK(cudaMemcpy(out, d_logits_, sizeof(float) * lanes_ * b_, cudaMemcpyDeviceToHost));
 }
 
-void Trainer::cache_slots(int lane, uint64_t* feature, int64_t* last_use, uint64_t* admit_seq) {
+void Trainer::cache_slots(int lane, uint64_t* feature, int64_t* last_use, uint64_t* admit_seq,
+                          uint64_t first, uint64_t count) {
   sync_all();
   const CacheLane& L = lane_.at(lane);
-  std::vector<uint32_t> f(L.C);
-  std::vector<int32_t> lu(L.C);
-  CUDA_CHECK(cudaMemcpy(f.data(), L.slot_feat, sizeof(uint32_t) * L.C, cudaMemcpyDeviceToHost));
-  CUDA_CHECK(cudaMemcpy(lu.data(), L.last_use, sizeof(int32_t) * L.C, cudaMemcpyDeviceToHost));
+  if (first > L.C) first = L.C;
+  if (count > L.C - first) count = L.C - first;
+  std::vector<uint32_t> f(count);
+  std::vector<int32_t> lu(count);
+  CUDA_CHECK(cudaMemcpy(f.data(), L.slot_feat + first, sizeof(uint32_t) * count,
+                        cudaMemcpyDeviceToHost));
+  CUDA_CHECK(cudaMemcpy(lu.data(), L.last_use + first, sizeof(int32_t) * count,
+                        cudaMemcpyDeviceToHost));
   if (admit_seq)
-    CUDA_CHECK(cudaMemcpy(admit_seq, L.admit_seq, sizeof(uint64_t) * L.C, cudaMemcpyDeviceToHost));
-  for (uint64_t i = 0; i < L.C; ++i) {
+    CUDA_CHECK(cudaMemcpy(admit_seq, L.admit_seq + first, sizeof(uint64_t) * count,
+                          cudaMemcpyDeviceToHost));
+  for (uint64_t i = 0; i < count; ++i) {
     if (feature) feature[i] = f[i] == kEmpty ? ~0ull : f[i];
     if (last_use) last_use[i] = lu[i];
   }
 }
 
+namespace {
+__global__ void gather_u32_kernel(const uint32_t* __restrict__ src, const uint64_t* __restrict__ idx,
+                                  int64_t n, uint32_t* __restrict__ out) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) out[i] = src[idx[i]];
+}
+// rows [n x 3d] and step counts of cache slots `slots` (one warp per row)
+__global__ void gather_slot_rows_kernel(const uint32_t* __restrict__ slots, int64_t n, int d3,
+                                        const float* __restrict__ emb,
+                                        const int32_t* __restrict__ steps, float* __restrict__ rows,
+                                        int32_t* __restrict__ out_steps) {
+  const int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= n) return;
+  const uint32_t s = slots[w];
+  for (int c = lane; c < d3; c += 32) rows[w * d3 + c] = emb[static_cast<size_t>(s) * d3 + c];
+  if (lane == 0) out_steps[w] = steps[s];
+}
+}  // namespace
+
+// Current state of owned rows wherever they live (cache slot or host pool): the index
+// entries of the rows are gathered on the device, cache rows by a gather kernel (never a
+// copy of the whole cache), host rows straight from the pinned slabs. kNever rows are
+// reported through `never` (nullptr: a LogicError, as HostStore::peek of an absent row).
+void Trainer::read_rows(int lane, const uint64_t* rows_idx, int64_t n, float* rows, int64_t* steps,
+                        bool* never) {
+  const CacheLane& L = lane_.at(lane);
+  const int d3 = 3 * d_;
+  if (n <= 0) return;
+  uint64_t* d_idx = nullptr;
+  uint32_t* d_where = nullptr;
+  CUDA_CHECK(cudaMalloc(&d_idx, sizeof(uint64_t) * n));
+  CUDA_CHECK(cudaMalloc(&d_where, sizeof(uint32_t) * n));
+  std::vector<uint32_t> where(n);
+  CUDA_CHECK(cudaMemcpy(d_idx, rows_idx, sizeof(uint64_t) * n, cudaMemcpyHostToDevice));
+  gather_u32_kernel<<<ceil_div(n, 256), 256>>>(L.index, d_idx, n, d_where);
+  CUDA_LAUNCH_CHECK();
+  CUDA_CHECK(cudaMemcpy(where.data(), d_where, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost));
+  std::vector<uint32_t> slots;
+  std::vector<int64_t> pos;
+  for (int64_t i = 0; i < n; ++i) {
+    const uint32_t w = where[i];
+    if (never) never[i] = w == kNever;
+    if (w == kNever) {
+      if (!never)
+        fail(kLogic, "row " + std::to_string(rows_idx[i] * W_ + lane0_ + lane) +
+                         " was never touched (HostStore::peek of an absent feature)");
+      if (rows) std::memset(rows + i * d3, 0, sizeof(float) * d3);
+      if (steps) steps[i] = 0;
+    } else if (on_host(w)) {
+      const uint32_t h = w & ~kHostBit;
+      if (rows) std::memcpy(rows + i * d3, L.host.row_host(h), sizeof(float) * d3);
+      if (steps) steps[i] = L.host.step_host(h);
+    } else {
+      slots.push_back(w);
+      pos.push_back(i);
+    }
+  }
+  if (!slots.empty()) {
+    const int64_t m = static_cast<int64_t>(slots.size());
+    uint32_t* d_slots = nullptr;
+    float* d_rows = nullptr;
+    int32_t* d_st = nullptr;
+    CUDA_CHECK(cudaMalloc(&d_slots, sizeof(uint32_t) * m));
+    CUDA_CHECK(cudaMalloc(&d_rows, sizeof(float) * m * d3));
+    CUDA_CHECK(cudaMalloc(&d_st, sizeof(int32_t) * m));
+    CUDA_CHECK(cudaMemcpy(d_slots, slots.data(), sizeof(uint32_t) * m, cudaMemcpyHostToDevice));
+    gather_slot_rows_kernel<<<ceil_div(m * 32, 256), 256>>>(d_slots, m, d3, L.emb, L.steps, d_rows,
+                                                            d_st);
+    CUDA_LAUNCH_CHECK();
+    std::vector<float> hr(static_cast<size_t>(m) * d3);
+    std::vector<int32_t> hs(m);
+    CUDA_CHECK(cudaMemcpy(hr.data(), d_rows, sizeof(float) * m * d3, cudaMemcpyDeviceToHost));
+    CUDA_CHECK(cudaMemcpy(hs.data(), d_st, sizeof(int32_t) * m, cudaMemcpyDeviceToHost));
+    for (int64_t q = 0; q < m; ++q) {
+      if (rows) std::memcpy(rows + pos[q] * d3, hr.data() + q * d3, sizeof(float) * d3);
+      if (steps) steps[pos[q]] = hs[q];
+    }
+    cudaFree(d_slots);
+    cudaFree(d_rows);
+    cudaFree(d_st);
+  }
+  cudaFree(d_idx);
+  cudaFree(d_where);
+}
+
+void Trainer::peek_rows(int64_t n, const uint64_t* features, float* rows, int64_t* steps) {
+  sync_all();
+  std::vector<std::vector<uint64_t>> idx(lanes_);
+  std::vector<std::vector<int64_t>> at(lanes_);
+  for (int64_t i = 0; i < n; ++i) {
+    const uint64_t f = features[i];
+    if (f >= cfg_.vocabulary_size) fail(kLogic, "feature id >= vocabulary size");
+    const int l = static_cast<int>(f % W_) - lane0_;
+    if (l < 0 || l >= lanes_)
+      fail(kLogic, "feature " + std::to_string(f) + " is owned by worker " +
+                       std::to_string(f % W_) + ", not by this process");
+    idx[l].push_back(f / W_);
+    at[l].push_back(i);
+  }
+  const int d3 = 3 * d_;
+  for (int l = 0; l < lanes_; ++l) {
+    const int64_t m = static_cast<int64_t>(idx[l].size());
+    if (!m) continue;
+    std::vector<float> r(rows ? static_cast<size_t>(m) * d3 : 0);
+    std::vector<int64_t> st(m);
+    read_rows(l, idx[l].data(), m, rows ? r.data() : nullptr, st.data(), nullptr);
+    for (int64_t q = 0; q < m; ++q) {
+      if (rows) std::memcpy(rows + at[l][q] * d3, r.data() + q * d3, sizeof(float) * d3);
+      if (steps) steps[at[l][q]] = st[q];
+    }
+  }
+}
+
 int64_t Trainer::snapshot(uint64_t* features, float* rows, int64_t* steps) {
   sync_all();
-  struct Src {
-    int lane;
-    uint32_t where;  // slot or kOnHost
-    uint64_t r;
-  };
-  std::map<uint64_t, Src> all;
+  // every touched owned row (index entry != kNever), sorted by feature
+  std::vector<std::pair<uint64_t, std::pair<int, uint64_t>>> all;  // feature -> (lane, row)
   for (int l = 0; l < lanes_; ++l) {
     const CacheLane& L = lane_[l];
     std::vector<uint32_t> idx(L.rows);
     CUDA_CHECK(cudaMemcpy(idx.data(), L.index, sizeof(uint32_t) * L.rows, cudaMemcpyDeviceToHost));
-    for (uint64_t r = 0; r < L.rows; ++r) {
-      if (idx[r] == kNever) continue;
-      all[r * W_ + (lane0_ + l)] = Src{l, idx[r], r};
-    }
+    for (uint64_t r = 0; r < L.rows; ++r)
+      if (idx[r] != kNever) all.push_back({r * W_ + (lane0_ + l), {l, r}});
   }
+  std::sort(all.begin(), all.end());
   if (!features) return static_cast<int64_t>(all.size());
   const int d3 = 3 * d_;
-  std::vector<std::vector<float>> ce(lanes_);
-  std::vector<std::vector<int32_t>> cs(lanes_);
-  if (rows || steps)
-    for (int l = 0; l < lanes_; ++l) {
-      const CacheLane& L = lane_[l];
-      const size_t cd = static_cast<size_t>(L.C) * d_ * 3;  // [emb | m | v] per slot
-      ce[l].resize(cd);
-      cs[l].resize(L.C);
-      CUDA_CHECK(cudaMemcpy(ce[l].data(), L.emb, sizeof(float) * cd, cudaMemcpyDeviceToHost));
-      CUDA_CHECK(cudaMemcpy(cs[l].data(), L.steps, sizeof(int32_t) * L.C, cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < all.size(); ++i) features[i] = all[i].first;
+  if (rows || steps) {
+    std::vector<std::vector<uint64_t>> idx(lanes_);
+    std::vector<std::vector<int64_t>> at(lanes_);
+    for (size_t i = 0; i < all.size(); ++i) {
+      idx[all[i].second.first].push_back(all[i].second.second);
+      at[all[i].second.first].push_back(static_cast<int64_t>(i));
     }
-  int64_t i = 0;
-  for (const auto& [f, src] : all) {
-    features[i] = f;
-    const CacheLane& L = lane_[src.lane];
-    if (rows) {
-      float* o = rows + static_cast<size_t>(i) * d3;
-      if (src.where == kOnHost) {
-        std::memcpy(o, L.host_rows + src.r * d3, sizeof(float) * d3);
-      } else {
-        std::memcpy(o, ce[src.lane].data() + static_cast<size_t>(src.where) * d3,
-                    sizeof(float) * d3);
+    for (int l = 0; l < lanes_; ++l) {
+      const int64_t m = static_cast<int64_t>(idx[l].size());
+      if (!m) continue;
+      std::vector<float> r(rows ? static_cast<size_t>(m) * d3 : 0);
+      std::vector<int64_t> st(m);
+      read_rows(l, idx[l].data(), m, rows ? r.data() : nullptr, st.data(), nullptr);
+      for (int64_t q = 0; q < m; ++q) {
+        if (rows) std::memcpy(rows + at[l][q] * d3, r.data() + q * d3, sizeof(float) * d3);
+        if (steps) steps[at[l][q]] = st[q];
       }
     }
-    if (steps) steps[i] = src.where == kOnHost ? L.host_steps[src.r] : cs[src.lane][src.where];
-    ++i;
   }
-  return i;
+  return static_cast<int64_t>(all.size());
+}
+
+void Trainer::dense_state(float* p, float* m, float* v, int64_t* step) {
+  sync_all();
+  if (p) CUDA_CHECK(cudaMemcpy(p, d_dense_, sizeof(float) * P_, cudaMemcpyDeviceToHost));
+  if (m) CUDA_CHECK(cudaMemcpy(m, d_dense_m_, sizeof(float) * P_, cudaMemcpyDeviceToHost));
+  if (v) CUDA_CHECK(cudaMemcpy(v, d_dense_v_, sizeof(float) * P_, cudaMemcpyDeviceToHost));
+  if (step) *step = dense_steps_;
 }
 
 void Trainer::get_dense(float* w1, float* b1, float* w2, float* b2) {

@@ -46,7 +46,13 @@ class Trainer {
   int rows() const { return lanes_ * cfg_.batch_size_per_worker; }
 
   void logits(float* out);
-  void cache_slots(int lane, uint64_t* feature, int64_t* last_use, uint64_t* admit_seq);
+  // slots [first, first + count) of a lane (clamped to the capacity)
+  void cache_slots(int lane, uint64_t* feature, int64_t* last_use, uint64_t* admit_seq,
+                   uint64_t first = 0, uint64_t count = ~0ull);
+  // HostStore::peek over this process's features: [emb | m | v] + adam step per feature
+  void peek_rows(int64_t n, const uint64_t* features, float* rows, int64_t* steps);
+  // dense parameters and their Adam moments [P] = W1 | b1 | w2 | b2, and the dense step
+  void dense_state(float* p, float* m, float* v, int64_t* step);
   uint64_t free_count(int lane);
   int64_t snapshot(uint64_t* features, float* rows, int64_t* steps);
   void get_dense(float* w1, float* b1, float* w2, float* b2);
@@ -66,6 +72,9 @@ class Trainer {
 
  private:
   void ensure_bias_tables(int64_t t_max);
+  // rows of one lane by owned-row index (see peek_rows)
+  void read_rows(int lane, const uint64_t* rows_idx, int64_t n, float* rows, int64_t* steps,
+                 bool* never);
   void phase(const char* name, cudaStream_t s = nullptr);
   void sync_all();
   void finish_phases();

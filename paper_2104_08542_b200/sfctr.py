@@ -174,6 +174,10 @@ SIGNATURES = [
     ("sfctr_trainer_stream", P, [P]),
     ("sfctr_trainer_logits", C.c_int, [P, f32p]),
     ("sfctr_trainer_cache_slots", C.c_int, [P, C.c_int32, u64p, i64p, u64p]),
+    ("sfctr_trainer_cache_slots_range", C.c_int,
+     [P, C.c_int32, C.c_uint64, C.c_uint64, u64p, i64p, u64p]),
+    ("sfctr_trainer_peek_rows", C.c_int, [P, C.c_int64, u64p, P, P]),
+    ("sfctr_trainer_dense_state", C.c_int, [P, P, P, P, C.POINTER(C.c_int64)]),
     ("sfctr_trainer_free_count", C.c_int, [P, C.c_int32, C.POINTER(C.c_uint64)]),
     ("sfctr_trainer_snapshot", C.c_int, [P, C.POINTER(C.c_int64), P, P, P]),
     ("sfctr_trainer_get_dense", C.c_int, [P, f32p, f32p, f32p, f32p]),
@@ -417,13 +421,39 @@ class Trainer:
         _check(lib().sfctr_trainer_logits(self._h, out))
         return out
 
-    def cache_slots(self, lane=0):
+    def cache_slots(self, lane=0, first=0, count=None):
+        """CacheBuffer::slots() of a local lane (slot -> feature, last_use, admit_seq);
+        first / count select a slot range (large caches)."""
         C_ = self.config.cache_capacity
-        f = np.zeros(C_, np.uint64)
-        lu = np.zeros(C_, np.int64)
-        seq = np.zeros(C_, np.uint64)
-        _check(lib().sfctr_trainer_cache_slots(self._h, lane, f, lu, seq))
-        return f, lu, seq
+        if count is None and first == 0:
+            f = np.zeros(C_, np.uint64)
+            lu = np.zeros(C_, np.int64)
+            seq = np.zeros(C_, np.uint64)
+            _check(lib().sfctr_trainer_cache_slots(self._h, lane, f, lu, seq))
+            return f, lu, seq
+        n = max(0, min(C_ - first, C_ if count is None else count))
+        f = np.zeros(max(n, 1), np.uint64)
+        lu = np.zeros(max(n, 1), np.int64)
+        seq = np.zeros(max(n, 1), np.uint64)
+        _check(lib().sfctr_trainer_cache_slots_range(self._h, lane, first, n, f, lu, seq))
+        return f[:n], lu[:n], seq[:n]
+
+    def peek_rows(self, features):
+        """HostStore::peek for features owned by this process: (rows [n, 3d] fp32 =
+        emb|m|v, adam steps [n])."""
+        f = np.ascontiguousarray(features, np.uint64).ravel()
+        rows = np.zeros((max(f.size, 1), 3 * self.dim), np.float32)
+        st = np.zeros(max(f.size, 1), np.int64)
+        _check(lib().sfctr_trainer_peek_rows(self._h, f.size, f, _ptr(rows), _ptr(st)))
+        return rows[:f.size], st[:f.size]
+
+    def dense_state(self):
+        """(params, m, v) each [P] = W1 | b1 | w2 | b2 (fp32), and the dense Adam step."""
+        P_ = self.fields * self.dim * self.hidden + 2 * self.hidden + 1
+        p, m, v = (np.zeros(P_, np.float32) for _ in range(3))
+        st = C.c_int64(0)
+        _check(lib().sfctr_trainer_dense_state(self._h, _ptr(p), _ptr(m), _ptr(v), C.byref(st)))
+        return p, m, v, st.value
 
     def free_count(self, lane=0):
         n = C.c_uint64(0)

@@ -67,6 +67,8 @@ def main():
         ("mini_w4", 4, 26, 256, 100_000, 7, 1.2, [0, 1, 5]),
         ("cfg2_w1", 1, 39, 8192, 33_800_000, 7, 1.05, [0]),
         ("cfg2_w2", 2, 39, 8192, 33_800_000, 7, 1.05, [0]),
+        ("cfg2_w4", 4, 39, 8192, 33_800_000, 7, 1.05, [0]),
+        ("cfg2_w8", 8, 39, 8192, 33_800_000, 7, 1.05, [0]),
         ("cfg3_s2", 8, 26, 1024, 1_000_000, 7, 2.0, [0]),
     ]
     for name, W, F, b, vocab, seed, zipf, steps in cases:

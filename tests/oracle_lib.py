@@ -84,6 +84,16 @@ def oracle():
     _sig(L, "orc_sim_dense", None, [C.c_void_p, f64p, f64p, f64p, f64p])
     _sig(L, "orc_sim_set_dense", None, [C.c_void_p, f64p, f64p, f64p, f64p])
     _sig(L, "orc_sim_ledger", None, [C.c_void_p, i64p])
+    _sig(L, "orc_sim_get_rows", C.c_int64, [C.c_void_p, C.c_int64, u64p, C.c_void_p, C.c_void_p])
+    _sig(L, "orc_sim_set_rows", C.c_int, [C.c_void_p, C.c_int64, u64p, C.c_void_p, C.c_void_p])
+    _sig(L, "orc_sim_keep_grads", None, [C.c_void_p, C.c_int])
+    _sig(L, "orc_sim_last_grads", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                            C.c_void_p, C.c_void_p, C.c_void_p,
+                                            C.POINTER(C.c_int64)])
+    _sig(L, "orc_sim_get_dense_state", None,
+         [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)])
+    _sig(L, "orc_sim_set_dense_state", None,
+         [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)])
     _sig(L, "orc_sim_last_unique", C.c_int64, [C.c_void_p])
     _sig(L, "orc_dense_init", None, [C.c_uint64, C.c_int, C.c_int, f64p, f64p, f64p, f64p])
     _sig(L, "orc_model_fwd_bwd", C.c_double,
