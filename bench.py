@@ -60,6 +60,12 @@ def parse():
     p.add_argument("--inflight", type=int, default=3, choices=[1, 2, 3],
                    help="e2e arm (pipelined): submitted steps whose loss is not yet read")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-mixcache", action="store_true",
+                   help="skip the MixCache-over-PCIe sub-lines (mixcache_small, cfg4)")
+    p.add_argument("--only-mixcache", action="store_true",
+                   help="run the MixCache sub-lines only (development)")
+    p.add_argument("--cfg4-cache-frac", type=float, default=0.10,
+                   help="cfg4 hot cache as a fraction of HBM (BASELINE configs[3]: 10-50 %%)")
     p.add_argument("--cpu-rows", type=int, default=2048, help="rows per CPU-baseline step")
     p.add_argument("--cpu-steps", type=int, default=3)
     return p.parse_args()
@@ -397,6 +403,102 @@ def run_ours(args, D):
     return out
 
 
+def run_cache_line(name, vocab, dim, fields, batch, zipf, cache, host_reserve, steps, max_fill,
+                   dev=0):
+    """MixCache over the pinned host pool (PCIe): one GPU, a cache smaller than the touched
+    table, so every step evicts LRU rows to the host and refills the ones that come back.
+    Fills the cache first (device-resident batches until steps evict), then times `steps`
+    steps on the trainer stream (CUDA events) and a second pass with per-phase events for
+    the eviction + admission time: fill / write-back GB/s against PCIe Gen5 x16."""
+    import torch
+
+    import paper_2104_08542_b200 as sb
+    cfg = sb.Config(num_workers=1, batch_size_per_worker=batch, num_fields=fields,
+                    embedding_dim=dim, vocabulary_size=vocab, cache_capacity=cache,
+                    hidden_dim=64, zipf_exponent=zipf, seed=7)
+    cfg.apply("mode", "pipelined")
+    cfg.apply("host_rows", str(host_reserve))
+    t0 = time.time()
+    tr = sb.Trainer(cfg, device=dev)
+    gen = sb.SyntheticGenerator(cfg, device=dev)
+    setup_s = time.time() - t0
+    n = batch * fields
+    ring = 64
+    d_feat = torch.empty((ring, n), dtype=torch.int64, device=f"cuda:{dev}")
+    d_lab = torch.empty((ring, batch), dtype=torch.uint8, device=f"cuda:{dev}")
+
+    def fill_ring(s0):
+        for i in range(ring):
+            gen.generate_device(s0 + i, 0, batch, d_feat[i].data_ptr(), d_lab[i].data_ptr())
+        torch.cuda.synchronize()
+
+    # fill: until steps evict (the cache is full) for a few steps in a row
+    s = 0
+    t0 = time.time()
+    evicting = 0
+    while s < max_fill and evicting < 3:
+        fill_ring(s)
+        for i in range(ring):
+            tr.step_device(s + i, d_feat[i].data_ptr(), d_lab[i].data_ptr())
+        tr.synchronize()
+        s += ring
+        evicting = evicting + 1 if tr.stats()["evicted"] > 0 else 0
+    fill_s = time.time() - t0
+    stream = torch.cuda.ExternalStream(tr.stream, device=f"cuda:{dev}")
+    fill_ring(s)
+    K = min(steps, ring // 2)
+    st0 = tr.stats()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for i in range(K):
+        tr.step_device(s + i, d_feat[i].data_ptr(), d_lab[i].data_ptr())
+    ev1.record(stream)
+    ev1.synchronize()
+    ms = ev0.elapsed_time(ev1) / K
+    tr.synchronize()
+    st1 = tr.stats()
+    tot = {k: st1[k] - st0[k] for k in st1 if k.startswith("total")}
+    tr.set_timing(True)
+    for i in range(K, 2 * K):
+        tr.step_device(s + i, d_feat[i].data_ptr(), d_lab[i].data_ptr())
+    tr.synchronize()
+    ph = {k: v / K for k, v in tr.phase_times()}
+    tr.set_timing(False)
+    st2 = tr.stats()
+    tot2 = {k: st2[k] - st1[k] for k in st2 if k.startswith("total")}
+    ev = tot["total_evicted"] / K
+    fh = tot["total_filled_from_host"] / K
+    row_b = (3 * dim + 1) * 4
+    d2h, h2d = ev * row_b, fh * row_b
+    # eviction + admission: LRU select (histogram) + candidate sort + the fused write-back /
+    # refill / lazy-init kernel (the rest of manage_evict_admit)
+    ea = sum(ph.get(k, 0.0) for k in ("evict_select", "evict_sort", "manage_evict_admit"))
+    ev2 = tot2["total_evicted"] / K
+    fh2 = tot2["total_filled_from_host"] / K
+    pcie_ea = (ev2 + fh2) * row_b
+    tr.close()
+    return {"name": name, "value": round(batch / (ms / 1e3), 1), "unit": "samples/s",
+            "ms_per_step": round(ms, 4), "steps": K,
+            "config": {"vocab": vocab, "dim": dim, "fields": fields, "batch": batch, "zipf": zipf,
+                       "cache_slots": cache, "cache_gb": round(cache * (12 * dim + 32) / 1e9, 2),
+                       "host_pool_reserved_rows": host_reserve, "mode": "pipelined"},
+            "fill": {"steps": s, "seconds": round(fill_s, 1)},
+            "per_step": {"unique": round(tot["total_unique"] / K, 1),
+                         "misses": round(tot["total_working"] / K, 1),
+                         "evictions": round(ev, 1), "refills_from_host": round(fh, 1),
+                         "pcie_d2h_bytes": int(d2h), "pcie_h2d_bytes": int(h2d)},
+            "pcie": {"evict_admit_ms": round(ea, 4),
+                     "gbs": round(pcie_ea / (ea / 1e3) / 1e9, 2) if ea else None,
+                     "writeback_gbs": round(ev2 * row_b / (ea / 1e3) / 1e9, 2) if ea else None,
+                     "fill_gbs": round(fh2 * row_b / (ea / 1e3) / 1e9, 2) if ea else None,
+                     "step_gbs": round((d2h + h2d) / (ms / 1e3) / 1e9, 2),
+                     "peak_gbs": 64.0,
+                     "peak_source": "PCIe Gen5 x16 nominal per direction; 44-56 GB/s measured "
+                                    "(profiles/r01s2_pcie_microbench.txt)"},
+            "phases_ms": {k: round(v, 4) for k, v in ph.items()}}
+
+
 def cpu_sample(args, workers, rows_total, steps, threads):
     """The oracle port (fp64 reference semantics) on host cores: rows_total rows/step."""
     import ctypes as C
@@ -474,7 +576,28 @@ def main():
             print(json.dumps(out), flush=True)
         D.close()
         return
-    out = run_ours(args, D)
+    out = run_ours(args, D) if not args.only_mixcache else {}
+    if D.world == 1 and not args.no_mixcache:
+        # MixCache regimes over PCIe (north_star (2)): the paper's 0.5 GB cache at cfg2, and
+        # BASELINE configs[3] (1B rows x d=32) with a hot cache of a fraction of HBM
+        import torch
+        sub = {}
+        try:
+            sub["mixcache_small"] = run_cache_line(
+                "mixcache_small: cfg2 with a 2^19-slot (0.5 GB) cache", args.vocab, args.dim,
+                args.fields, args.batch, args.zipf, 524288, 16_000_000, 20, 64 * 4)
+        except Exception as e:  # noqa: BLE001
+            sub["mixcache_small"] = {"error": str(e)[:300]}
+        try:
+            hbm = torch.cuda.get_device_properties(0).total_memory
+            slots = int(args.cfg4_cache_frac * hbm / (12 * 32 + 32))
+            sub["cfg4"] = run_cache_line(
+                f"cfg4 (BASELINE configs[3]): 1B rows x d=32, F=26, b=8192, hot cache "
+                f"{args.cfg4_cache_frac:.0%} of HBM", 1_000_000_000, 32, 26, 8192, 1.05, slots,
+                12_000_000, 20, 64 * 40)
+        except Exception as e:  # noqa: BLE001
+            sub["cfg4"] = {"error": str(e)[:300]}
+        out["mixcache_lines"] = sub
     if D.rank == 0:
         if D.world == 1 and not args.no_cpu_baseline:
             threads = os.cpu_count() or 1

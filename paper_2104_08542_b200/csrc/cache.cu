@@ -124,49 +124,104 @@ __global__ void mark_window_kernel(const uint32_t* __restrict__ gids,
 
 // LRU histogram over last_use of the eligible slots (occupied && !needed_soon; pins are
 // implied by BSP stream order: batch t-1's update has completed before manage(t) runs, and
-// the pipelined manager checks counters[kCntOld] before evicting). Slots admitted together
-// sit next to each other (LIFO free stack), so a warp's eligible lanes mostly share one
-// last_use: one atomic per distinct value per warp (match_any).
-__global__ void lru_hist_kernel(uint32_t C, const uint32_t* __restrict__ slot_feat,
-                                const int32_t* __restrict__ mark, int32_t t,
-                                const int32_t* __restrict__ last_use, uint32_t* __restrict__ hist) {
+// the pipelined manager checks counters[kCntOld] before evicting), in two levels so the
+// bins always fit shared memory: level 1 bins last_use >> shift over [0, t]; level 2 (when
+// shift > 0) counts the 2^shift steps of the threshold's coarse bin exactly. Each block
+// owns a contiguous chunk of slots and a shared-memory histogram (lanes of a warp with the
+// same value merge through match_any: slots admitted together sit next to each other), and
+// flushes its non-zero bins with one global atomic each: same-address global atomics from
+// every warp were the bottleneck of a single global histogram.
+// base_bin: level 2 restricts to [cnt[kCntSelB] << base_shift, + nbins); count_old also
+// counts the eligible slots last used before step t-1 (pipelined eviction safety).
+constexpr int kHistBins = 8192;  // shared-memory bins per level
+__global__ void __launch_bounds__(1024) lru_hist_kernel(
+    uint32_t C, const uint32_t* __restrict__ slot_feat, const int32_t* __restrict__ mark, int32_t t,
+    const int32_t* __restrict__ last_use, uint32_t* __restrict__ hist, int nbins, int shift,
+    int32_t* __restrict__ cnt, int base_shift, bool level2) {
+  __shared__ uint32_t sh[kHistBins];
+  __shared__ uint32_t old_blk;
+  for (int i = threadIdx.x; i < nbins; i += blockDim.x) sh[i] = 0;
+  if (threadIdx.x == 0) old_blk = 0;
+  __syncthreads();
+  const int32_t base = level2 ? (cnt[kCntSelB] << base_shift) : 0;
   const int lane = threadIdx.x & 31;
-  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
-  for (uint64_t w0 = ((blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5) * 32;
-       w0 < C; w0 += nwarps * 32) {
-    const uint64_t s = w0 + lane;
-    bool el = false;
-    int32_t lu = 0;
-    if (s < C) {
-      el = slot_feat[s] != kEmpty && mark[s] != t;
-      if (el) lu = last_use[s];
+  // 4 slots per thread per round (16 B loads of slot_feat / mark / last_use, issued before
+  // any use): the pass streams 12 B per slot at HBM rate instead of one dependent chain
+  const uint64_t C4 = (static_cast<uint64_t>(C) + 3) >> 2;
+  const uint64_t chunk = (C4 + gridDim.x - 1) / gridDim.x;
+  const uint64_t q0 = blockIdx.x * chunk, q1 = q0 + chunk < C4 ? q0 + chunk : C4;
+  uint32_t old = 0;
+  for (uint64_t qw = q0 + (threadIdx.x & ~31u); qw < q1; qw += blockDim.x) {
+    const uint64_t q = qw + lane;
+    uint4 f = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    int4 mk = make_int4(t, t, t, t), lu = make_int4(0, 0, 0, 0);
+    if (q < q1) {
+      if (4 * q + 3 < C) {
+        f = __ldcs(reinterpret_cast<const uint4*>(slot_feat) + q);
+        mk = __ldcs(reinterpret_cast<const int4*>(mark) + q);
+        lu = __ldcs(reinterpret_cast<const int4*>(last_use) + q);
+      } else {
+        uint32_t* fp = &f.x;
+        int* mp = &mk.x;
+        int* lp = &lu.x;
+        for (int e = 0; e < 4 && 4 * q + e < C; ++e) {
+          fp[e] = slot_feat[4 * q + e];
+          mp[e] = mark[4 * q + e];
+          lp[e] = last_use[4 * q + e];
+        }
+      }
     }
-    const unsigned act = __ballot_sync(0xFFFFFFFFu, el);
-    if (el) {
-      const unsigned peers = __match_any_sync(act, lu);
-      if (lane == __ffs(peers) - 1) atomicAdd(hist + lu, static_cast<uint32_t>(__popc(peers)));
+    const uint32_t fa[4] = {f.x, f.y, f.z, f.w};
+    const int32_t ma[4] = {mk.x, mk.y, mk.z, mk.w}, la[4] = {lu.x, lu.y, lu.z, lu.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      int bin = -1;
+      if (fa[e] != kEmpty && ma[e] != t) {
+        old += la[e] < t - 1;
+        const int32_t b = (la[e] - base) >> shift;
+        if (la[e] >= base && b < nbins) bin = b;
+      }
+      const unsigned act = __ballot_sync(0xFFFFFFFFu, bin >= 0);
+      if (bin >= 0) {
+        const unsigned peers = __match_any_sync(act, bin);
+        if (lane == __ffs(peers) - 1) atomicAdd(sh + bin, static_cast<uint32_t>(__popc(peers)));
+      }
     }
   }
+  if (!level2) {
+    for (int off = 16; off > 0; off >>= 1) old += __shfl_xor_sync(0xFFFFFFFFu, old, off);
+    if (lane == 0 && old) atomicAdd(&old_blk, old);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nbins; i += blockDim.x)
+    if (sh[i]) atomicAdd(hist + i, sh[i]);
+  if (threadIdx.x == 0 && old_blk) atomicAdd(cnt + kCntOld, static_cast<int32_t>(old_blk));
 }
 
-// One block: the threshold step T = min{T : #(last_use <= T) >= n_evict} (t when fewer
-// eligible slots exist: the capacity deadlock is then flagged by the eviction kernel), and
-// #(last_use < t-1) for the pipelined manager.
+// One block: the bin B = min{B : #(bins <= B) >= need} of a level's histogram, with need =
+// n_evict (level 1) or n_evict - #(below the coarse bin) (level 2); the last bin when fewer
+// eligible slots exist (the eviction kernel then flags the capacity deadlock). Level 1
+// writes B and #(bins < B) (kCntSelB / kCntSelBelow) and, when it is final (shift 0), the
+// threshold step kCntSelT; level 2 writes kCntSelT = (coarse bin << shift) + B.
 __global__ void __launch_bounds__(1024) lru_select_kernel(const uint32_t* __restrict__ hist,
                                                           int32_t nbins, int32_t n_evict,
-                                                          int32_t t, int32_t* __restrict__ cnt) {
+                                                          int32_t* __restrict__ cnt, int shift,
+                                                          bool level2) {
   __shared__ uint64_t part[1024];
   __shared__ int32_t found;
+  __shared__ uint64_t found_below;
   const int tid = threadIdx.x;
+  const uint64_t need =
+      static_cast<uint64_t>(n_evict) - (level2 ? static_cast<uint64_t>(cnt[kCntSelBelow]) : 0);
   const int per = (nbins + 1023) / 1024;
   const int lo = min(nbins, tid * per), hi = min(nbins, lo + per);
-  uint64_t sum = 0, old = 0;
-  for (int i = lo; i < hi; ++i) {
-    sum += hist[i];
-    if (i < t - 1) old += hist[i];
-  }
+  uint64_t sum = 0;
+  for (int i = lo; i < hi; ++i) sum += hist[i];
   part[tid] = sum;
-  if (tid == 0) found = t;
+  if (tid == 0) {
+    found = nbins - 1;
+    found_below = 0;
+  }
   __syncthreads();
   for (int off = 1; off < 1024; off <<= 1) {  // inclusive scan of the chunk sums
     const uint64_t v = tid >= off ? part[tid - off] : 0;
@@ -175,27 +230,27 @@ __global__ void __launch_bounds__(1024) lru_select_kernel(const uint32_t* __rest
     __syncthreads();
   }
   const uint64_t before = tid ? part[tid - 1] : 0;
-  if (before < static_cast<uint64_t>(n_evict) && part[tid] >= static_cast<uint64_t>(n_evict)) {
+  if (tid == 1023 && part[1023] < need) found_below = part[1023] - (nbins ? hist[nbins - 1] : 0);
+  if (before < need && part[tid] >= need) {
     uint64_t run = before;
     for (int i = lo; i < hi; ++i) {
-      run += hist[i];
-      if (run >= static_cast<uint64_t>(n_evict)) {
+      if (run + hist[i] >= need) {
         found = i;
+        found_below = run;
         break;
       }
+      run += hist[i];
     }
   }
-  // old: reduce the per-thread counts
   __syncthreads();
-  part[tid] = old;
-  __syncthreads();
-  for (int off = 512; off > 0; off >>= 1) {
-    if (tid < off) part[tid] += part[tid + off];
-    __syncthreads();
-  }
   if (tid == 0) {
-    cnt[kCntSelT] = found;
-    cnt[kCntOld] = static_cast<int32_t>(part[0] < 0x7FFFFFFFull ? part[0] : 0x7FFFFFFFull);
+    if (level2) {
+      cnt[kCntSelT] = (cnt[kCntSelB] << shift) + found;
+    } else {
+      cnt[kCntSelB] = found;
+      cnt[kCntSelBelow] = static_cast<int32_t>(found_below);
+      if (shift == 0) cnt[kCntSelT] = found;
+    }
     cnt[kCntSelN] = 0;
   }
 }
@@ -211,27 +266,59 @@ __global__ void lru_collect_kernel(uint32_t C, const uint32_t* __restrict__ slot
                                    uint64_t* __restrict__ keys, uint32_t* __restrict__ ids) {
   const int lane = threadIdx.x & 31;
   const int32_t T = cnt[kCntSelT];
-  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
-  for (uint64_t w0 = ((blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5) * 32;
-       w0 < C; w0 += nwarps * 32) {
-    const uint64_t s = w0 + lane;
-    bool take = false;
-    int32_t lu = 0;
-    if (s < C && slot_feat[s] != kEmpty && mark[s] != t) {
-      lu = last_use[s];
-      take = lu <= T;
-    }
-    const unsigned m = __ballot_sync(0xFFFFFFFFu, take);
-    if (!m) continue;
-    int32_t base = 0;
-    if (lane == __ffs(m) - 1) base = atomicAdd(cnt + kCntSelN, __popc(m));
-    base = __shfl_sync(0xFFFFFFFFu, base, __ffs(m) - 1);
-    if (take) {
-      const int64_t pos = base + __popc(m & ((1u << lane) - 1u));
-      if (pos < cap) {
-        keys[pos] = (static_cast<uint64_t>(lu + 1) << 40) | (admit_seq[s] & ((1ull << 40) - 1));
-        ids[pos] = static_cast<uint32_t>(s);
+  const uint64_t C4 = (static_cast<uint64_t>(C) + 3) >> 2;
+  const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  // 4 slots per thread per round, as in lru_hist_kernel
+  for (uint64_t qw = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) & ~31ull;
+       qw < C4; qw += nthreads) {
+    const uint64_t q = qw + lane;
+    uint4 f = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    int4 mk = make_int4(t, t, t, t), lu = make_int4(0, 0, 0, 0);
+    if (q < C4) {
+      if (4 * q + 3 < C) {
+        f = __ldcs(reinterpret_cast<const uint4*>(slot_feat) + q);
+        mk = __ldcs(reinterpret_cast<const int4*>(mark) + q);
+        lu = __ldcs(reinterpret_cast<const int4*>(last_use) + q);
+      } else {
+        uint32_t* fp = &f.x;
+        int* mp = &mk.x;
+        int* lp = &lu.x;
+        for (int e = 0; e < 4 && 4 * q + e < C; ++e) {
+          fp[e] = slot_feat[4 * q + e];
+          mp[e] = mark[4 * q + e];
+          lp[e] = last_use[4 * q + e];
+        }
       }
+    }
+    const uint32_t fa[4] = {f.x, f.y, f.z, f.w};
+    const int32_t ma[4] = {mk.x, mk.y, mk.z, mk.w}, la[4] = {lu.x, lu.y, lu.z, lu.w};
+    uint32_t take = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (fa[e] != kEmpty && ma[e] != t && la[e] <= T) take |= 1u << e;
+    const int mine = __popc(take);
+    // warp-inclusive scan of the per-thread candidate counts
+    int incl = mine;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int v = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+      if (lane >= off) incl += v;
+    }
+    const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    if (!total) continue;
+    int32_t base = 0;
+    if (lane == 31) base = atomicAdd(cnt + kCntSelN, total);
+    base = __shfl_sync(0xFFFFFFFFu, base, 31);
+    int64_t pos = base + incl - mine;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (!((take >> e) & 1u)) continue;
+      const uint64_t sl = 4 * q + e;
+      if (pos < cap) {
+        keys[pos] = (static_cast<uint64_t>(la[e] + 1) << 40) | (admit_seq[sl] & ((1ull << 40) - 1));
+        ids[pos] = static_cast<uint32_t>(sl);
+      }
+      ++pos;
     }
   }
 }
@@ -558,6 +645,7 @@ __global__ void fill_u32(uint32_t* p, uint64_t n, uint32_t v) {
 
 void HostPool::init(int dim, uint64_t owned_rows, uint64_t reserve_rows) {
   d = dim;
+  CUDA_CHECK(cudaGetDevice(&dev));
   // slab_rows = 2^shift: the largest power of two with slab_rows * 12d <= 256 MB, but no
   // larger than the owned shard needs (small tables get small slabs)
   const uint64_t row_bytes = 12ull * static_cast<uint64_t>(dim);
@@ -573,51 +661,109 @@ void HostPool::init(int dim, uint64_t owned_rows, uint64_t reserve_rows) {
   if (reserve_rows) ensure(reserve_rows, nullptr);
 }
 
-void HostPool::ensure(uint64_t slots, cudaStream_t s) {
-  if (slots <= cap) return;
+std::pair<float*, int32_t*> HostPool::alloc_slab() {
   const uint64_t slab_rows = 1ull << shift;
-  const size_t first = rows_h.size();
-  while (cap < slots) {
-    if (rows_h.size() >= static_cast<size_t>(kMaxSlabs) || cap + slab_rows > (1ull << 31) - 1)
-      fail(kRun, "host pool exhausted: " + std::to_string(cap) + " evicted rows per worker");
-    float* r = nullptr;
-    int32_t* st = nullptr;
-    const size_t rb = sizeof(float) * slab_rows * 3 * d;
-    if (cudaHostAlloc(reinterpret_cast<void**>(&r), rb, cudaHostAllocMapped | cudaHostAllocPortable) !=
-            cudaSuccess ||
-        cudaHostAlloc(reinterpret_cast<void**>(&st), sizeof(int32_t) * slab_rows,
-                      cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
-      cudaGetLastError();
-      if (r) cudaFreeHost(r);
-      fail(kRun, "cannot pin " + std::to_string(rb >> 20) + " MiB more for the host pool (" +
-                     std::to_string(cap) + " evicted rows held)");
-    }
-    float* rd = nullptr;
-    int32_t* sd = nullptr;
-    CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&rd), r, 0));
-    CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&sd), st, 0));
-    h_rows_tab[rows_h.size()] = rd;
-    h_steps_tab[rows_h.size()] = sd;
-    rows_h.push_back(r);
-    steps_h.push_back(st);
-    cap += slab_rows;
+  float* r = nullptr;
+  int32_t* st = nullptr;
+  if (cudaHostAlloc(reinterpret_cast<void**>(&r), sizeof(float) * slab_rows * 3 * d,
+                    cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
+      cudaHostAlloc(reinterpret_cast<void**>(&st), sizeof(int32_t) * slab_rows,
+                    cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    if (r) cudaFreeHost(r);
+    return {nullptr, nullptr};
   }
-  const size_t n = rows_h.size() - first;
-  CUDA_CHECK(cudaMemcpyAsync(d_rows + first, h_rows_tab + first, sizeof(float*) * n,
-                             cudaMemcpyHostToDevice, s));
-  CUDA_CHECK(cudaMemcpyAsync(d_steps + first, h_steps_tab + first, sizeof(int32_t*) * n,
-                             cudaMemcpyHostToDevice, s));
-  if (!s) CUDA_CHECK(cudaStreamSynchronize(nullptr));
+  return {r, st};
+}
+
+void HostPool::prefetch() {
+  {
+    std::lock_guard<std::mutex> g(mu);
+    if (filler_failed || static_cast<int>(spares.size()) >= kAhead) return;
+  }
+  if (filler.joinable()) {  // a previous round finished (or is finishing): reap it
+    filler.join();
+  }
+  filler = std::thread([this] {
+    cudaSetDevice(dev);
+    for (;;) {
+      {
+        std::lock_guard<std::mutex> g(mu);
+        if (static_cast<int>(spares.size()) >= kAhead) return;
+      }
+      auto slab = alloc_slab();
+      std::lock_guard<std::mutex> g(mu);
+      if (!slab.first) {
+        filler_failed = true;
+        return;
+      }
+      spares.push_back(slab);
+    }
+  });
+}
+
+void HostPool::ensure(uint64_t slots, cudaStream_t s) {
+  const uint64_t slab_rows = 1ull << shift;
+  if (slots > cap) {
+    const size_t first = rows_h.size();
+    while (cap < slots) {
+      if (rows_h.size() >= static_cast<size_t>(kMaxSlabs) || cap + slab_rows > (1ull << 31) - 1)
+        fail(kRun, "host pool exhausted: " + std::to_string(cap) + " evicted rows per worker");
+      std::pair<float*, int32_t*> slab{nullptr, nullptr};
+      {
+        std::lock_guard<std::mutex> g(mu);
+        if (!spares.empty()) {
+          slab = spares.back();
+          spares.pop_back();
+        }
+      }
+      if (!slab.first) slab = alloc_slab();
+      if (!slab.first)
+        fail(kRun, "cannot pin " + std::to_string((sizeof(float) * slab_rows * 3 * d) >> 20) +
+                       " MiB more for the host pool (" + std::to_string(cap) +
+                       " evicted rows held)");
+      float* rd = nullptr;
+      int32_t* sd = nullptr;
+      CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&rd), slab.first, 0));
+      CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&sd), slab.second, 0));
+      h_rows_tab[rows_h.size()] = rd;
+      h_steps_tab[rows_h.size()] = sd;
+      rows_h.push_back(slab.first);
+      steps_h.push_back(slab.second);
+      cap += slab_rows;
+    }
+    const size_t n = rows_h.size() - first;
+    CUDA_CHECK(cudaMemcpyAsync(d_rows + first, h_rows_tab + first, sizeof(float*) * n,
+                               cudaMemcpyHostToDevice, s));
+    CUDA_CHECK(cudaMemcpyAsync(d_steps + first, h_steps_tab + first, sizeof(int32_t*) * n,
+                               cudaMemcpyHostToDevice, s));
+    if (!s) CUDA_CHECK(cudaStreamSynchronize(nullptr));
+  }
+  if (cap - std::min(cap, slots) < static_cast<uint64_t>(kAhead) * slab_rows) prefetch();
 }
 
 void HostPool::release() {
+  if (filler.joinable()) filler.join();
+  for (auto& p : spares) {
+    cudaFreeHost(p.first);
+    cudaFreeHost(p.second);
+  }
+  spares.clear();
   for (float* p : rows_h) cudaFreeHost(p);
   for (int32_t* p : steps_h) cudaFreeHost(p);
   if (d_rows) cudaFree(d_rows);
   if (d_steps) cudaFree(d_steps);
   if (h_rows_tab) cudaFreeHost(h_rows_tab);
   if (h_steps_tab) cudaFreeHost(h_steps_tab);
-  *this = HostPool();
+  rows_h.clear();
+  steps_h.clear();
+  d = shift = dev = 0;
+  cap = hi = 0;
+  d_rows = nullptr;
+  d_steps = nullptr;
+  h_rows_tab = nullptr;
+  h_steps_tab = nullptr;
+  filler_failed = false;
 }
 
 void CacheLane::init(uint64_t capacity, int dim, uint64_t owned_rows, uint64_t host_reserve,
@@ -710,7 +856,7 @@ void CacheLane::select_owned(const uint32_t* d_gids, const int32_t* d_U, int32_t
                              uint32_t w, uint32_t* vsi_first, cudaStream_t s) {
   if (cap <= 0) return;
   if (W == 1) {  // a single worker owns every unique: own_k = identity, count = U
-    own_all_kernel<<<std::max(1, std::min(ceil_div(cap, 256), 148 * 8)), 256, 0, s>>>(
+    own_all_kernel<<<std::max(1, std::min(ceil_div(cap, 256), num_sms() * 8)), 256, 0, s>>>(
         d_U, own_k, counters + kCntOwned, d_gids, vsi_first);
     CUDA_LAUNCH_CHECK();
     return;
@@ -746,27 +892,33 @@ void CacheLane::probe(const uint32_t* d_gids, int32_t cap, uint32_t W, int32_t t
 }
 
 void CacheLane::victim_select(int32_t t, int32_t n_evict, cudaStream_t s) {
-  const int64_t nbins = static_cast<int64_t>(t) + 1;
-  if (nbins > hist_cap) {  // bins = steps so far (grows geometrically; rare)
-    int64_t cap2 = std::max<int64_t>(4096, hist_cap);
-    while (cap2 < nbins) cap2 *= 2;
-    CUDA_CHECK(cudaStreamSynchronize(s));
-    if (hist) CUDA_CHECK(cudaFree(hist));
-    CUDA_CHECK(cudaMalloc(&hist, sizeof(uint32_t) * cap2));
-    hist_cap = cap2;
+  if (!hist) CUDA_CHECK(cudaMalloc(&hist, sizeof(uint32_t) * 2 * kHistBins));
+  // level 1: last_use >> shift over [0, t] in at most kHistBins bins
+  int shift = 0;
+  while ((static_cast<int64_t>(t) >> shift) + 1 > kHistBins) ++shift;
+  const int nb1 = static_cast<int>((static_cast<int64_t>(t) >> shift) + 1);
+  CUDA_CHECK(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 2 * kHistBins, s));
+  CUDA_CHECK(cudaMemsetAsync(counters + kCntOld, 0, sizeof(int32_t), s));
+  const int grid = std::max(1, std::min<int>(ceil_div(static_cast<int64_t>(C), 16384), 2 * num_sms()));
+  lru_hist_kernel<<<grid, 1024, 0, s>>>(static_cast<uint32_t>(C), slot_feat, mark, t, last_use,
+                                        hist, nb1, shift, counters, 0, false);
+  CUDA_LAUNCH_CHECK();
+  lru_select_kernel<<<1, 1024, 0, s>>>(hist, nb1, n_evict, counters, shift, false);
+  CUDA_LAUNCH_CHECK();
+  if (shift > 0) {  // level 2: the 2^shift steps of the coarse bin, exactly
+    lru_hist_kernel<<<grid, 1024, 0, s>>>(static_cast<uint32_t>(C), slot_feat, mark, t, last_use,
+                                          hist + kHistBins, 1 << shift, 0, counters, shift, true);
+    CUDA_LAUNCH_CHECK();
+    lru_select_kernel<<<1, 1024, 0, s>>>(hist + kHistBins, 1 << shift, n_evict, counters, shift,
+                                         true);
+    CUDA_LAUNCH_CHECK();
   }
-  CUDA_CHECK(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * nbins, s));
-  const int grid = static_cast<int>(std::min<int64_t>(ceil_div(static_cast<int64_t>(C), 256), 148 * 8));
-  lru_hist_kernel<<<grid, 256, 0, s>>>(static_cast<uint32_t>(C), slot_feat, mark, t, last_use, hist);
-  CUDA_LAUNCH_CHECK();
-  lru_select_kernel<<<1, 1024, 0, s>>>(hist, static_cast<int32_t>(nbins), n_evict, t, counters);
-  CUDA_LAUNCH_CHECK();
 }
 
 void CacheLane::victim_sort(int32_t t, int32_t n_evict, cudaStream_t s) {
   const int64_t bound = std::min<int64_t>(cand_cap, static_cast<int64_t>(n_evict) + umax);
   CUDA_CHECK(cudaMemsetAsync(keys, 0xFF, sizeof(uint64_t) * bound, s));
-  const int grid = static_cast<int>(std::min<int64_t>(ceil_div(static_cast<int64_t>(C), 256), 148 * 8));
+  const int grid = static_cast<int>(std::min<int64_t>(ceil_div(static_cast<int64_t>(C), 1024), num_sms() * 8));
   lru_collect_kernel<<<grid, 256, 0, s>>>(static_cast<uint32_t>(C), slot_feat, mark, t, last_use,
                                           admit_seq, counters, bound, keys, ids);
   CUDA_LAUNCH_CHECK();
@@ -787,9 +939,9 @@ void CacheLane::evict(int32_t n_evict, uint32_t W, int32_t t, cudaStream_t s, bo
 bool CacheLane::swap_supported() const { return (d & 3) == 0 && 3 * (d / 4) <= 64; }
 
 void CacheLane::evict_admit(int32_t n_evict, int32_t n_work, uint32_t W, uint64_t seed, int32_t t,
-                            cudaStream_t s, bool selected) {
-  if (n_evict > 0) {  // every victim may need a new host slot
-    host.ensure(host.hi + static_cast<uint64_t>(n_evict), s);
+                            cudaStream_t s, bool selected, const PhaseHook& hook) {
+  if (n_evict > 0) {  // every victim may need a new host slot (host.hi: exact as of the
+    host.ensure(host.hi + static_cast<uint64_t>(n_evict), s);  // last host wait)
     host.hi += static_cast<uint64_t>(n_evict);
   }
   if (n_evict <= 0 || !swap_supported()) {
@@ -798,7 +950,9 @@ void CacheLane::evict_admit(int32_t n_evict, int32_t n_work, uint32_t W, uint64_
     return;
   }
   if (!selected) victim_select(t, n_evict, s);
+  hook("evict_select");
   victim_sort(t, n_evict, s);
+  hook("evict_sort");
   swap_kernel<<<ceil_div(static_cast<int64_t>(n_work) * 32, 256), 256, 0, s>>>(
       counters, n_evict, keys_sorted, ids_sorted, work_j, work_f, work_w, W, d / 4, free_stack,
       index, host.tab(), slot_host, counters + kCntHostNext, seed, fnv1a64("embed"),

@@ -2,6 +2,9 @@
 // table (see cache.cu for the policy and the reference lines it follows).
 #pragma once
 
+#include <mutex>
+#include <thread>
+#include <utility>
 #include <vector>
 
 #include "ops.h"
@@ -24,6 +27,8 @@ enum {
   kCntHostNext = 9,  // host slots handed out by the host pool (first evictions)
   kCntSelT = 10,     // LRU select: threshold step T (victims have last_use <= T)
   kCntSelN = 11,     // LRU select: candidates collected (last_use <= T)
+  kCntSelB = 12,     // LRU select: coarse (level-1) bin of the threshold
+  kCntSelBelow = 13, // LRU select: eligible slots below the coarse bin
   kCntWords = 16
 };
 
@@ -48,8 +53,18 @@ struct HostTab {
 // the first time it is evicted (pull_parameters_to_host) and keeps it: refills read it,
 // later write-backs of the same feature reuse it. Only evicted rows cost host memory.
 struct HostPool {
+  HostPool() = default;
+  HostPool(HostPool&& o) noexcept { *this = std::move(o); }
+  HostPool& operator=(HostPool&& o) noexcept {  // moved only while idle (no filler running)
+    d = o.d; shift = o.shift; dev = o.dev; cap = o.cap; hi = o.hi;
+    rows_h = std::move(o.rows_h); steps_h = std::move(o.steps_h);
+    d_rows = o.d_rows; d_steps = o.d_steps; h_rows_tab = o.h_rows_tab; h_steps_tab = o.h_steps_tab;
+    spares = std::move(o.spares); filler_failed = o.filler_failed;
+    o.d_rows = nullptr; o.d_steps = nullptr; o.h_rows_tab = nullptr; o.h_steps_tab = nullptr;
+    return *this;
+  }
   static constexpr int kMaxSlabs = 4096;
-  int d = 0, shift = 0;
+  int d = 0, shift = 0, dev = 0;
   uint64_t cap = 0;  // host slots allocated (slabs x slab_rows)
   uint64_t hi = 0;   // upper bound of the slots handed out (the device counter kCntHostNext)
   std::vector<float*> rows_h;
@@ -58,6 +73,17 @@ struct HostPool {
   int32_t** d_steps = nullptr;
   float** h_rows_tab = nullptr;  // pinned mirrors: append-only sources of the async uploads
   int32_t** h_steps_tab = nullptr;
+  // Pinning a 256 MB slab takes ~100 ms (page pinning runs at a few GB/s): while the pool
+  // is within kAhead slabs of its high-water mark, a background thread pins spare slabs
+  // ahead so the step that needs one takes it ready instead of stalling the manager stage.
+  // (At eviction rates above the pinning rate only the up-front reservation helps.)
+  static constexpr int kAhead = 4;
+  std::thread filler;
+  std::mutex mu;
+  std::vector<std::pair<float*, int32_t*>> spares;  // guarded by mu
+  bool filler_failed = false;                        // guarded by mu
+  std::pair<float*, int32_t*> alloc_slab();  // (rows, steps) pinned + mapped, or nulls
+  void prefetch();
   // slab_rows = 2^shift: about 256 MB per slab, smaller for small tables
   void init(int dim, uint64_t owned_rows, uint64_t reserve_rows);
   // grows the pool to at least `slots` host slots; new slab pointers are uploaded on s
@@ -92,8 +118,7 @@ struct CacheLane {
   uint32_t* index = nullptr;      // [rows] slot | kHostBit | host slot | kNever
   uint32_t* slot_host = nullptr;  // [C] host slot of the slot's row (kNoHost: none yet)
   HostPool host;                  // evicted rows (pinned, mapped host slabs)
-  uint32_t* hist = nullptr;       // LRU histogram: eligible slots per last_use step
-  int64_t hist_cap = 0;
+  uint32_t* hist = nullptr;       // LRU histograms (two levels of kHistBins)
 
   // per-step scratch; own_k / own_slot are read by the training stage, so they come in
   // two sets (step parity) and the manager of step t+1 fills one while step t trains
@@ -146,7 +171,7 @@ struct CacheLane {
   // eviction step (host-known n_evict / n_work): write-back and admission fused per slot
   // (swap_kernel) when the row fits the register staging, else evict() then admit()
   void evict_admit(int32_t n_evict, int32_t n_work, uint32_t W, uint64_t seed, int32_t t,
-                   cudaStream_t s, bool selected);
+                   cudaStream_t s, bool selected, const PhaseHook& hook = {});
   bool swap_supported() const;
 };
 

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -49,6 +50,20 @@ extern thread_local int64_t g_launches;
   } while (0)
 
 inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+// SM count of the current device (148 on B200), read once per device: grids are sized in
+// waves of it rather than a hard-coded count (MIG slices and other parts differ)
+inline int num_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+  if (!cache[dev]) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) n = 0;
+    cache[dev] = n > 0 ? n : 148;
+  }
+  return cache[dev];
+}
 
 // ---------------- rng.hpp:27-56 (host + device) ----------------
 constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ull;
@@ -103,6 +118,48 @@ __device__ __forceinline__ int64_t idiv(int64_t a, int b) {
                            : a / b;
 }
 #endif
+
+#ifdef __CUDACC__
+// NVLink flag barrier between the W ranks of one box (peer[w] = rank w's flag words, mapped
+// over CUDA IPC): rank `me` stores `epoch` into slot me of every peer's words (release,
+// system scope) and waits until every peer's store into its own slot has arrived (acquire).
+// Spinning backs off with __nanosleep. A peer that does not arrive within timeout_ns (global
+// timer) makes the barrier give up and raise *abort_flag instead of trapping: the host
+// reports a RunError at its next check, and a peer that is merely slow (host-side work,
+// a debugger) no longer takes down every other rank's CUDA context.
+__device__ inline void flag_barrier_wait(uint64_t* const* peer, int W, int me, uint64_t epoch,
+                                         uint64_t timeout_ns, int32_t* abort_flag) {
+  const int w = threadIdx.x;
+  if (w >= W || w == me) return;
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(peer[w] + me), "l"(epoch) : "memory");
+  const uint64_t* mine = peer[me] + w;
+  uint64_t v = 0, t0 = 0, now = 0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  unsigned ns = 32;
+  for (;;) {
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
+    if (v >= epoch) break;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (now - t0 > timeout_ns) {
+      if (abort_flag) atomicExch(abort_flag, 1);
+      break;
+    }
+    __nanosleep(ns);
+    if (ns < 2048) ns <<= 1;
+  }
+}
+#endif
+
+// barrier timeout: SFCTR_BARRIER_TIMEOUT_S seconds (default 600)
+inline uint64_t barrier_timeout_ns() {
+  static const uint64_t ns = [] {
+    double s = 600;
+    if (const char* e = std::getenv("SFCTR_BARRIER_TIMEOUT_S")) s = std::atof(e);
+    if (!(s > 0)) s = 600;
+    return static_cast<uint64_t>(s * 1e9);
+  }();
+  return ns;
+}
 
 // Slot / index sentinels of the device MixCache. index[r] of owned row r is a cache slot
 // (< kHostBit: capacities stay below 2^31), kNever, or kHostBit | h: the row lives in host

@@ -302,7 +302,7 @@ void CriteoTable::enqueue_chunk(int k, size_t n) {
   nl_write_kernel<<<tiles, kTileThreads, 0, s>>>(d_buf[k], N, tile_off, d_nlpos, d_rowline);
   CUDA_LAUNCH_CHECK();
   // tile_off[tiles] = (lines << 32 | rows) of the chunk
-  parse_kernel<<<148 * 8, 256, 0, s>>>(d_buf[k], d_nlpos, d_rowline, tile_off + tiles, d_state,
+  parse_kernel<<<num_sms() * 8, 256, 0, s>>>(d_buf[k], d_nlpos, d_rowline, tile_off + tiles, d_state,
                                        cap_rows, vocab, d_feat, d_lab,
                                        reinterpret_cast<unsigned long long*>(d_state + 2));
   CUDA_LAUNCH_CHECK();

@@ -303,7 +303,7 @@ int fm_sq_parts(int d) { return (d & 3) == 0 ? d / 4 : d; }
 
 // grid for the count-bounded grid-stride kernels: one resident wave of 256-thread CTAs
 // (148 SMs x 8), fewer when the bound is small; the device count ends the loops
-static int wave_grid(int64_t n_bound) { return std::max(1, std::min(ceil_div(n_bound, 256), 148 * 8)); }
+static int wave_grid(int64_t n_bound) { return std::max(1, std::min(ceil_div(n_bound, 256), num_sms() * 8)); }
 
 void gather_cache(const uint32_t* own_k, const uint32_t* own_slot, int32_t n_own,
                   const int32_t* d_n_own, const float* emb, int d, float* G, float* dG_zero,
@@ -400,7 +400,7 @@ void sparse_adam(const uint32_t* own_k /* gradient row index, or null = j */,
       if (b <= 0) CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sparse_adam_v4, 256, 0));
       return std::max(1, b);
     }();
-    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 148 * per_sm)));
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), num_sms() * per_sm)));
     sparse_adam_v4<<<grid, 256, 0, s>>>(
         own_k, own_slot, d_n_own, n_own, d / 4, reinterpret_cast<const float4*>(dG),
         reinterpret_cast<float4*>(emb), reinterpret_cast<float4*>(mom),

@@ -327,7 +327,7 @@ void Exchange::plan(const uint32_t* d_vid, int64_t n_global, int64_t per_worker,
   touch_mark_kernel<<<ceil_div(n_global, 256), 256, 0, s>>>(d_vid, n_global, per_worker, tb8);
   CUDA_LAUNCH_CHECK();
   hook("plan_mark");
-  touch_pack_kernel<<<std::max(1, std::min(ceil_div(c, 256), 148 * 8)), 256, 0, s>>>(d_U, tb8, tm);
+  touch_pack_kernel<<<std::max(1, std::min(ceil_div(c, 256), num_sms() * 8)), 256, 0, s>>>(d_U, tb8, tm);
   CUDA_LAUNCH_CHECK();
   hook("plan_touch");
   // receive plan (y = 0, over the uniques) and send plan (y = 1, over my owned uniques)
@@ -342,7 +342,7 @@ void Exchange::plan(const uint32_t* d_vid, int64_t n_global, int64_t per_worker,
   hook("plan_rank");
   // every peer's layout (peer-store transport)
   CUDA_CHECK(cudaMemsetAsync(totals + 16, 0, sizeof(int32_t) * 64, s));
-  count_matrix_kernel<<<std::min(ceil_div(c, 256), 148 * 4), 256, 0, s>>>(d_uniq, d_U, c, tm, W,
+  count_matrix_kernel<<<std::min(ceil_div(c, 256), num_sms() * 4), 256, 0, s>>>(d_uniq, d_U, c, tm, W,
                                                                            totals + 16);
   CUDA_LAUNCH_CHECK();
   offsets_kernel<<<1, 1, 0, s>>>(totals, me, offs);
@@ -754,7 +754,7 @@ void Exchange::forward_dev(const uint32_t* d_own_k, const uint32_t* d_own_slot, 
   for (int w = 0; w < W; ++w) pr.E[w] = reinterpret_cast<float4*>(peer_E[w]);
   static const int fwd_blocks = [] {  // experiment switch: SFCTR_FWD_PUSH_BLOCKS
     const char* e = std::getenv("SFCTR_FWD_PUSH_BLOCKS");
-    return e ? std::max(1, atoi(e)) : 148 * 2;
+    return e ? std::max(1, atoi(e)) : num_sms() * 2;
   }();
   // SFCTR_FWD_STAGED=1: pack per destination, then block pushes (measured slower at cfg2:
   // 93.5 vs 80 us at N = 4, the pack's HBM pass costs more than the pushes gain)
@@ -773,13 +773,13 @@ void Exchange::forward_dev(const uint32_t* d_own_k, const uint32_t* d_own_slot, 
   // the staging rows live in buf: it is free until the backward, which peers only start
   // after this step's forward barrier
   pack_fwd_kernel<<<std::max(1, std::min(ceil_div(static_cast<int64_t>(n_bound) * (d / 4), 256),
-                                         148 * 16)),
+                                         num_sms() * 16)),
                     256, 0, s>>>(d_own_k, d_own_slot, d_n_own, tm, sscan, W, me, offs,
                                  reinterpret_cast<const float4*>(emb), d / 4,
                                  reinterpret_cast<float4*>(peer_E[me]),
                                  reinterpret_cast<float4*>(buf));
   CUDA_LAUNCH_CHECK();
-  push_fwd_kernel<<<dim3(148, W), 256, 0, s>>>(reinterpret_cast<const float4*>(buf), d / 4, me,
+  push_fwd_kernel<<<dim3(num_sms(), W), 256, 0, s>>>(reinterpret_cast<const float4*>(buf), d / 4, me,
                                                 totals, offs, pr);
   CUDA_LAUNCH_CHECK();
 }
@@ -791,7 +791,7 @@ void Exchange::backward_send_dev(const float* dE, cudaStream_t s, const float* E
   // one wave of writers per destination: more concurrent NVLink writers congest the switch
   // (microbench/nvlink_push.cu: 569 GB/s out per GPU with 148 CTAs per peer at W = 4,
   // 444 GB/s with 592, 406 GB/s with 1184)
-  push_blocks_p2p_dev_kernel<<<dim3(148, W), 256, 0, s>>>(
+  push_blocks_p2p_dev_kernel<<<dim3(num_sms(), W), 256, 0, s>>>(
       reinterpret_cast<const float4*>(dE), d / 4, me, totals, offs, pr,
       FmDefer{reinterpret_cast<const float4*>(E), B, fm_scale});
   CUDA_LAUNCH_CHECK();
@@ -805,7 +805,7 @@ void Exchange::backward_reduce_adam_dev(const uint32_t* d_own_k, int32_t n_bound
               reinterpret_cast<float4*>(ar.vel), ar.own_slot, ar.steps, ar.bc1, ar.bc2, ar.lr,
               ar.b1, ar.b2, ar.omb1, ar.omb2, ar.eps};
   owner_reduce_adam_dev_kernel<<<std::max(1, std::min(ceil_div(static_cast<int64_t>(n_bound) * d4, 256),
-                                                      148 * 15)),
+                                                      num_sms() * 15)),
                                  256, 0, s>>>(d_own_k, d_n_own, tm, sscan, totals, W, me, lpos,
                                               reinterpret_cast<const float4*>(dE),
                                               reinterpret_cast<const float4*>(buf), d4, B,
@@ -814,7 +814,7 @@ void Exchange::backward_reduce_adam_dev(const uint32_t* d_own_k, int32_t n_bound
 }
 
 void Exchange::zero_local_dev(float* dE, cudaStream_t s, float* B) {
-  zero_rows_dev_kernel<<<148 * 8, 256, 0, s>>>(reinterpret_cast<float4*>(dE), offs, d / 4, B);
+  zero_rows_dev_kernel<<<num_sms() * 8, 256, 0, s>>>(reinterpret_cast<float4*>(dE), offs, d / 4, B);
   CUDA_LAUNCH_CHECK();
 }
 
@@ -888,23 +888,12 @@ namespace {
 struct PeerFlags {
   uint64_t* peer[8];  // every rank's flag words (mine included)
 };
-// NVLink flag barrier: rank me stores epoch into slot me of every peer's flags (release,
-// system scope) and waits until every peer's store into its own slot has arrived (acquire).
-// The peer stores being published were made by the previous kernel on this stream, which
-// ended every block with __threadfence_system(). A peer that never arrives (crashed rank)
-// traps after ~20 s instead of hanging the GPU.
-__global__ void flag_barrier_kernel(PeerFlags pf, int W, int me, uint64_t epoch) {
-  const int w = threadIdx.x;
-  if (w >= W || w == me) return;
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(pf.peer[w] + me), "l"(epoch) : "memory");
-  const uint64_t* mine = pf.peer[me] + w;
-  uint64_t v = 0;
-  long long t0 = clock64();
-  for (;;) {
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
-    if (v >= epoch) break;
-    if (clock64() - t0 > 40ll * 1000 * 1000 * 1000) __trap();
-  }
+// NVLink flag barrier (flag_barrier_wait, common.cuh). The peer stores being published were
+// made by the previous kernel on this stream, which ended every block with
+// __threadfence_system().
+__global__ void flag_barrier_kernel(PeerFlags pf, int W, int me, uint64_t epoch,
+                                    uint64_t timeout_ns, int32_t* abort_flag) {
+  flag_barrier_wait(pf.peer, W, me, epoch, timeout_ns, abort_flag);
 }
 }  // namespace
 
@@ -914,7 +903,7 @@ void Exchange::barrier(ncclComm_t comm, cudaStream_t s) {
   if (flags && !nccl_barrier) {
     PeerFlags pf{};
     for (int w = 0; w < W; ++w) pf.peer[w] = peer_flags[w];
-    flag_barrier_kernel<<<1, 32, 0, s>>>(pf, W, me, ++epoch);
+    flag_barrier_kernel<<<1, 32, 0, s>>>(pf, W, me, ++epoch, barrier_timeout_ns(), abort_flag);
     CUDA_LAUNCH_CHECK();
     return;
   }
@@ -950,7 +939,7 @@ int64_t Exchange::forward(const uint32_t* d_own_k, const uint32_t* d_own_slot, i
                                    cudaMemcpyDeviceToDevice, s));
       }
     } else if (n_own > 0) {
-      push_rows_p2p_kernel<<<std::min(ceil_div(static_cast<int64_t>(n_own) * 32, 256), 148 * 8),
+      push_rows_p2p_kernel<<<std::min(ceil_div(static_cast<int64_t>(n_own) * 32, 256), num_sms() * 8),
                              256, 0, s>>>(
           d_own_k, d_own_slot, n_own, tm, sscan, W, reinterpret_cast<const float4*>(emb), d4, pr);
       CUDA_LAUNCH_CHECK();
@@ -1014,7 +1003,7 @@ int64_t Exchange::backward_send(const float* dE, ncclComm_t comm, cudaStream_t s
         bytes += pb.rows[o] * d * 4;
       }
       if (most > 0) {
-        push_blocks_p2p_kernel<<<dim3(std::min(ceil_div(most * d4, 256), 148 * 2), W), 256, 0,
+        push_blocks_p2p_kernel<<<dim3(std::min(ceil_div(most * d4, 256), num_sms() * 2), W), 256, 0,
                                  s>>>(reinterpret_cast<const float4*>(dE), d4, pb);
         CUDA_LAUNCH_CHECK();
       }

@@ -46,6 +46,7 @@ struct Exchange {
   uint64_t* flags = nullptr;               // [8] NVLink flag barrier: slot w = rank w's epoch
   uint64_t* peer_flags[8] = {};
   uint64_t epoch = 0;
+  int32_t* abort_flag = nullptr;           // device word raised by a timed-out barrier
   bool nccl_barrier = false;               // SFCTR_NCCL_BARRIER=1: all-reduce barrier instead
   std::vector<int64_t> roff_all, boff_all;  // [w*8+o]: rank w's E block of owner o;
                                             // [o*8+w]: owner o's buf block of source w

@@ -18,11 +18,11 @@ struct PeerIds {
   uint32_t* dst[8];
 };
 
+// vec (host-decided): n and off multiples of 4 and `in` 16-byte aligned
 __global__ void __launch_bounds__(256) push_ids_kernel(const uint64_t* __restrict__ in, int64_t n,
                                                        uint64_t limit, int32_t* __restrict__ bad,
-                                                       PeerIds pd, int W, int64_t off) {
+                                                       PeerIds pd, int W, int64_t off, bool vec) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  const bool vec = (n & 3) == 0 && (off & 3) == 0;
   if (vec) {  // 4 ids per thread: two 16 B loads, one 16 B store per destination
     const int64_t n4 = n >> 2;
     for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < n4; q += stride) {
@@ -56,19 +56,33 @@ struct PeerFlags {
   uint64_t* peer[8];
 };
 
-// same protocol as the exchange's flag barrier (exchange.cu), on its own flags and epochs
-__global__ void id_barrier_kernel(PeerFlags pf, int W, int me, uint64_t epoch) {
+// The exchange's flag barrier protocol (flag_barrier_wait, common.cuh) on its own flags and
+// epochs, with one addition: bit 63 of the published word carries this rank's bad-id flag
+// (an id >= vocab in its batch), so every rank leaves the barrier knowing whether ANY rank
+// saw one and gates the step the same way (Trainer::prepare: no state moves).
+constexpr uint64_t kBadBit = 1ull << 63;
+__global__ void id_barrier_kernel(PeerFlags pf, int W, int me, uint64_t epoch, uint64_t timeout_ns,
+                                  int32_t* abort_flag, int32_t* bad) {
   const int w = threadIdx.x;
   if (w >= W || w == me) return;
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(pf.peer[w] + me), "l"(epoch) : "memory");
+  const uint64_t word = epoch | (*bad ? kBadBit : 0ull);
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(pf.peer[w] + me), "l"(word) : "memory");
   const uint64_t* mine = pf.peer[me] + w;
-  uint64_t v = 0;
-  const long long t0 = clock64();
+  uint64_t v = 0, t0 = 0, now = 0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  unsigned ns = 32;
   for (;;) {
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
-    if (v >= epoch) break;
-    if (clock64() - t0 > 40ll * 1000 * 1000 * 1000) __trap();
+    if ((v & ~kBadBit) >= epoch) break;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (now - t0 > timeout_ns) {
+      if (abort_flag) atomicExch(abort_flag, 1);
+      return;
+    }
+    __nanosleep(ns);
+    if (ns < 2048) ns <<= 1;
   }
+  if (v & kBadBit) atomicExch(bad, 1);
 }
 
 }  // namespace
@@ -96,6 +110,9 @@ void IdGather::release() {
 }
 
 bool IdGather::setup_p2p(ncclComm_t comm, cudaStream_t s) {
+  // the peer tables hold 8 ranks (one NVSwitch box): larger worlds keep the NCCL
+  // all-gather (W is the same on every rank, so all of them return here together)
+  if (W > 8) return false;
   int dev = 0;
   CUDA_CHECK(cudaGetDevice(&dev));
   int* d_x = nullptr;
@@ -155,13 +172,15 @@ const uint32_t* IdGather::gather(const uint64_t* d_ids, uint64_t limit, int32_t*
                                  cudaStream_t s) {
   PeerIds pd{};
   for (int w = 0; w < W; ++w) pd.dst[w] = peer_gids[k][w];
-  const int64_t units = (n & 3) == 0 ? n / 4 : n;
-  push_ids_kernel<<<std::max(1, std::min(ceil_div(units, 256), 148 * 2)), 256, 0, s>>>(
-      d_ids, n, limit, d_bad, pd, W, static_cast<int64_t>(me) * n);
+  const bool vec = (n & 3) == 0 && ((static_cast<int64_t>(me) * n) & 3) == 0 &&
+                   (reinterpret_cast<uintptr_t>(d_ids) & 15) == 0;
+  const int64_t units = vec ? n / 4 : n;
+  push_ids_kernel<<<std::max(1, std::min(ceil_div(units, 256), num_sms() * 2)), 256, 0, s>>>(
+      d_ids, n, limit, d_bad, pd, W, static_cast<int64_t>(me) * n, vec);
   CUDA_LAUNCH_CHECK();
   PeerFlags pf{};
   for (int w = 0; w < W; ++w) pf.peer[w] = peer_flags[w];
-  id_barrier_kernel<<<1, 32, 0, s>>>(pf, W, me, ++epoch);
+  id_barrier_kernel<<<1, 32, 0, s>>>(pf, W, me, ++epoch, barrier_timeout_ns(), abort_flag, d_bad);
   CUDA_LAUNCH_CHECK();
   return gids[k];
 }

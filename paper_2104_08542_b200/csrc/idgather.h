@@ -18,6 +18,7 @@ struct IdGather {
   uint64_t* flags = nullptr;           // flag-barrier words, slot w = rank w's epoch
   uint64_t* peer_flags[8] = {};
   uint64_t epoch = 0;
+  int32_t* abort_flag = nullptr;       // device word raised by a timed-out barrier (trainer's)
 
   void init(int W, int me, int64_t n);
   void release();

@@ -58,13 +58,6 @@ struct DxScatter {
 };
 
 // Optional callback between the tower's stages (the trainer records a phase event there).
-struct PhaseHook {
-  void (*fn)(void* ctx, const char* name) = nullptr;
-  void* ctx = nullptr;
-  void operator()(const char* name) const {
-    if (fn) fn(ctx, name);
-  }
-};
 
 // ---------------- tower.cu — DeepFM-lite ----------------
 struct TowerBufs {

@@ -10,6 +10,15 @@
 
 namespace sfb {
 
+// per-phase timing callback (Trainer::phase): records a named CUDA event on the stream
+struct PhaseHook {
+  void (*fn)(void* ctx, const char* name) = nullptr;
+  void* ctx = nullptr;
+  void operator()(const char* name) const {
+    if (fn) fn(ctx, name);
+  }
+};
+
 // ---------------- generator.cu — SyntheticGenerator (generator.cpp:32-115) ----------------
 struct GenTables {
   int fields = 0;

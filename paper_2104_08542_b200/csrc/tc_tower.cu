@@ -292,7 +292,7 @@ void launch_dx_gemm(const TowerTC& tc_, const float* dh_hi, const float* dh_lo, 
 
 // split-K factor so that tiles * splits ~ one wave of 148 SMs, no empty split
 void split_k(int tiles, int nkb, int* splits, int* kps) {
-  int s = std::max(1, std::min(nkb, 148 / std::max(1, tiles)));
+  int s = std::max(1, std::min(nkb, num_sms() / std::max(1, tiles)));
   *kps = (nkb + s - 1) / s;
   *splits = (nkb + *kps - 1) / *kps;
 }

@@ -296,7 +296,7 @@ void TowerBufs::init(int rc, int k, int h, int dim) {
   CUDA_CHECK(cudaMalloc(&lossr, sizeof(float) * rc));
   // row splits so that (K tiles x H tiles x splits) fills ~2 waves of 148 SMs
   const int kt = ceil_div(K, TB), ht = ceil_div(H, TB);
-  splits = std::max(1, std::min(ceil_div(rc, BK), (2 * 148 + kt * ht - 1) / (kt * ht)));
+  splits = std::max(1, std::min(ceil_div(rc, BK), (2 * num_sms() + kt * ht - 1) / (kt * ht)));
   CUDA_CHECK(cudaMalloc(&part, sizeof(float) * static_cast<size_t>(splits) * K * H));
   // kSgChunks chunks, or one per 8 rows when the tensor-core head writes them
   CUDA_CHECK(cudaMalloc(&sg_part, sizeof(float) * std::max(256, (rows_cap + 7) / 8) * (2 * h + 2)));

@@ -100,6 +100,8 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
   CUDA_CHECK(cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking,
                                           pipelined_ ? prio_hi : prio_lo));
   if (const char* e = std::getenv("SFCTR_NO_FREE_STEPS")) no_free_steps_ = e[0] == '1';
+  CUDA_CHECK(cudaMalloc(&d_err_, sizeof(int32_t) * 4));
+  CUDA_CHECK(cudaMemset(d_err_, 0, sizeof(int32_t) * 4));
   mstream_ = stream_;
   if (pipelined_) {
     CUDA_CHECK(cudaStreamCreateWithPriority(&mstream_, cudaStreamNonBlocking, prio_lo));
@@ -119,6 +121,7 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
     if (!(ni && ni[0] == '1')) {
       idg_.init(world_, rank_, n_local_);
       if (!idg_.setup_p2p(comm_, stream_)) idg_.release();
+      idg_.abort_flag = d_err_;
     }
     CUDA_CHECK(cudaEventCreateWithFlags(&dense_ready_, cudaEventDisableTiming));
     CUDA_CHECK(cudaEventCreateWithFlags(&dense_done_, cudaEventDisableTiming));
@@ -196,6 +199,7 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
     CUDA_CHECK(cudaEventCreateWithFlags(&loss_ev_[q], cudaEventDisableTiming));
   CUDA_CHECK(cudaMalloc(&d_acc_, sizeof(int64_t) * 8));
   CUDA_CHECK(cudaMemset(d_acc_, 0, sizeof(int64_t) * 8));
+
   CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_acc_), sizeof(int64_t) * 8, 0));
   tower_.init(b_, K_, H_, d_);
   towertc_.init(b_, K_, H_, d_);
@@ -220,6 +224,7 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
     if (d_ % 4) fail(kConfig, "sync=alltoall needs dim % 4 == 0");
     a2a_ = true;
     xch_.init(W_, rank_, umax, d_);
+    xch_.abort_flag = d_err_;
     CUDA_CHECK(cudaMalloc(&d_lvid_, sizeof(uint32_t) * n_local_));
     CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_totals_),
                              sizeof(int32_t) * Exchange::kTotals, 0));
@@ -266,6 +271,7 @@ Trainer::~Trainer() {
                   static_cast<void*>(d_dense_v_), static_cast<void*>(d_grads_),
                   static_cast<void*>(d_bc1_),
                   static_cast<void*>(d_bc2_), static_cast<void*>(d_acc_),
+                  static_cast<void*>(d_err_),
                   })
     if (p) cudaFree(p);
   if (h_acc_) cudaFreeHost(h_acc_);
@@ -339,11 +345,20 @@ struct TailArgs {
   const int32_t* U;
   int W, d;
   int64_t P;
+  const int32_t* bad;  // sticky bad-id flag: the step moves no state
+  int32_t* gated;      // steps skipped that way
 };
 
 __global__ void tail_kernel(TailArgs a) {
   const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  if (*a.bad) {
+    if (tid == 0) {
+      *a.gated += 1;
+      *a.loss_out = __int_as_float(0x7fc00000);  // NaN: the step did not run
+    }
+    return;
+  }
   for (int64_t i = tid; i < a.n; i += stride) {
     const float gi = a.g[i] * a.gs;
     const float mi = a.b1 * a.m[i] + a.omb1 * gi;
@@ -454,6 +469,30 @@ __global__ void snap_kernel(SnapArgs a) {
   if (i == 0) a.out[0] = *a.U;
   if (i < kCntWords * a.lanes) a.out[1 + i] = a.cnt[i / kCntWords][i % kCntWords];
 }
+// Bad-id gate (sticky flag d_scalars_[1]): a batch with an id >= vocab moves no state. The
+// VSI table was already reset behind the batch (select_owned); here the step is left with
+// no uniques and no owned rows, so probe / admission / exchange / update_sparse / the
+// dense update do nothing, and every position is pointed at table row 0 (own_slot[0] = 0,
+// lpos[0] = 0 after the plan) so the training stage reads valid memory and discards it.
+struct GatePtrs {
+  uint32_t* own_slot[8];
+};
+__global__ void bad_id_gate_kernel(const int32_t* __restrict__ bad, int32_t* U, LaneCounters cnt,
+                                   int lanes, uint32_t* __restrict__ vid, int64_t n, GatePtrs gp) {
+  if (!*bad) return;
+  const int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  for (int64_t i = i0; i < n; i += static_cast<int64_t>(gridDim.x) * blockDim.x) vid[i] = 0;
+  if (i0 == 0) {
+    *U = 0;
+    for (int l = 0; l < lanes; ++l) {
+      const_cast<int32_t*>(cnt.c[l])[kCntOwned] = 0;
+      gp.own_slot[l][0] = 0;
+    }
+  }
+}
+__global__ void bad_id_gate_plan_kernel(const int32_t* __restrict__ bad, uint32_t* lpos) {
+  if (*bad) lpos[0] = 0;
+}
 }  // namespace
 
 // Host-Manager stage of step t (Algorithm 1 l.2-7; manager_get + pull_parameters_to_host +
@@ -518,6 +557,8 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
     ids_to_u32(d_features, d_ids32_, n_local_, cfg_.vocabulary_size, d_scalars_ + 1, sm);
     if (world_ > 1) {
       NCCL_CHECK(ncclAllGather(d_ids32_, d_gids_, static_cast<size_t>(n_local_), ncclUint32, mcomm_, sm));
+      // every rank gates the step when any rank saw an id >= vocab
+      NCCL_CHECK(ncclAllReduce(d_scalars_ + 1, d_scalars_ + 1, 1, ncclInt32, ncclMax, mcomm_, sm));
       gids = d_gids_;
       stats_.nvlink_bytes += n_local_ * 4;
     }
@@ -537,6 +578,17 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
     lane_[l].select_owned(d_uniq_, d_scalars_ + 0, cap, Wu, static_cast<uint32_t>(lane0_ + l),
                           l == 0 ? vsi_.d_first : nullptr, sm);
   }
+  {
+    LaneCounters lc{};
+    GatePtrs gp{};
+    for (int l = 0; l < lanes_; ++l) {
+      lc.c[l] = lane_[l].counters;
+      gp.own_slot[l] = lane_[l].own_slot;
+    }
+    bad_id_gate_kernel<<<std::max(1, std::min(ceil_div(n_global_, 256), num_sms() * 4)), 256, 0,
+                         sm>>>(d_scalars_ + 1, d_scalars_ + 0, lc, lanes_, d_vid_, n_global_, gp);
+    CUDA_LAUNCH_CHECK();
+  }
   // window batches t+1..t+L-1 (needed_soon), one at a time through the window scratch
   const int nwin = cfg_.lookahead_depth - 1;
   for (int j = 0; j < nwin; ++j) {
@@ -545,6 +597,7 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
     const uint32_t* wg = d_ids32_;
     if (world_ > 1) {
       NCCL_CHECK(ncclAllGather(d_ids32_, d_gids_, static_cast<size_t>(n_local_), ncclUint32, mcomm_, sm));
+      NCCL_CHECK(ncclAllReduce(d_scalars_ + 1, d_scalars_ + 1, 1, ncclInt32, ncclMax, mcomm_, sm));
       wg = d_gids_;
     }
     vsi_device(vsi_, wg, n_global_, d_wuniq_, d_wvid_, d_scalars_ + 2, sm);
@@ -577,6 +630,8 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
                           h->tr->phase(n, h->s);
                         },
                         &hc});
+    bad_id_gate_plan_kernel<<<1, 1, 0, sm>>>(d_scalars_ + 1, xch_.lpos);
+    CUDA_LAUNCH_CHECK();
     if (!free_step)
       CUDA_CHECK(cudaMemcpyAsync(h_totals_, xch_.totals, sizeof(int32_t) * Exchange::kTotals,
                                  cudaMemcpyDeviceToHost, sm));
@@ -591,7 +646,7 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
                                  sizeof(int32_t) * kCntWords, cudaMemcpyDeviceToHost, sm));
     CUDA_CHECK(cudaStreamSynchronize(sm));
     U = h_scalars_[0];
-    if (h_scalars_[1]) fail(kLogic, "feature id >= vocabulary size in the batch", step);
+    if (h_scalars_[1]) raise_bad_id(step);
     stats_.unique = U;
     for (int l = 0; l < lanes_; ++l) {
       CacheLane& L = lane_[l];
@@ -599,6 +654,7 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
       n_own[l] = hc[kCntOwned];
       L.free_top = hc[kCntFreeTop];
       std::memcpy(&L.next_seq, hc + kCntSeq, sizeof(uint64_t));
+      L.host.hi = static_cast<uint64_t>(hc[kCntHostNext]);  // host slots handed out so far
     }
     // capacity check before any state moves (push_parameters_to_cache deadlock)
     for (int l = 0; l < lanes_; ++l) {
@@ -646,10 +702,16 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
         }
       }
     }
+    std::pair<Trainer*, cudaStream_t> hook_ctx{this, sm};
     for (int l = 0; l < lanes_; ++l) {
       CacheLane& L = lane_[l];
       const int32_t n_evict = std::max<int32_t>(0, n_work[l] - L.free_top);
-      L.evict_admit(n_evict, n_work[l], Wu, cfg_.seed, t, sm, selected && n_evict > 0);
+      L.evict_admit(n_evict, n_work[l], Wu, cfg_.seed, t, sm, selected && n_evict > 0,
+                    PhaseHook{[](void* c, const char* nm) {
+                                auto* h = static_cast<std::pair<Trainer*, cudaStream_t>*>(c);
+                                h->first->phase(nm, h->second);
+                              },
+                              &hook_ctx});
       free_lb_[l] = static_cast<int64_t>(L.free_top) + n_evict - n_work[l];
       led_[0] += static_cast<int64_t>(n_work[l]) * d_ * 12;
       led_[1] += static_cast<int64_t>(n_evict) * d_ * 12;
@@ -781,7 +843,7 @@ void Trainer::train(int64_t step, const uint8_t* d_labels, float* d_loss) {
   if (zero_in_gather) {
   } else if (xdev) {  // cleared by the manager stage
   } else if (free_step && d_ % 4 == 0)
-    zero_rows_kernel<<<148 * 8, 256, 0, s>>>(reinterpret_cast<float4*>(d_dG_), snap + 0,
+    zero_rows_kernel<<<num_sms() * 8, 256, 0, s>>>(reinterpret_cast<float4*>(d_dG_), snap + 0,
                                              d_ / 4, n_global_ * (d_ / 4));
   else
     CUDA_CHECK(cudaMemsetAsync(d_dG_, 0, sizeof(float) * table_rows * d_, s));
@@ -937,7 +999,9 @@ void Trainer::train(int64_t step, const uint8_t* d_labels, float* d_loss) {
     a.W = W_;
     a.d = d_;
     a.P = static_cast<int64_t>(P_);
-    tail_kernel<<<148 * 8, 256, 0, s>>>(a);  // one pass over the dense parameters and the rows
+    a.bad = d_scalars_ + 1;
+    a.gated = d_err_ + 1;
+    tail_kernel<<<num_sms() * 8, 256, 0, s>>>(a);  // one pass over the dense parameters and the rows
     CUDA_LAUNCH_CHECK();
     w1_split_ready_ = a.w_hi != nullptr;
   }
@@ -974,13 +1038,26 @@ void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_
 // Folds the deferred device counters in: capacity errors flagged by kernels
 // and the number of admissions that read a row back from the host table
 // (cumulative on the device; the delta covers every step since the last call).
+void Trainer::raise_bad_id(int64_t step) {
+  sync_all();
+  int32_t gated = 0;
+  CUDA_CHECK(cudaMemcpy(&gated, d_err_ + 1, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  CUDA_CHECK(cudaMemset(d_err_ + 1, 0, sizeof(int32_t)));
+  CUDA_CHECK(cudaMemset(d_scalars_ + 1, 0, sizeof(int32_t)));
+  dense_steps_ -= gated;  // the gated steps did not update the dense parameters
+  fail(kLogic, "feature id >= vocabulary size in the batch (no state was changed)", step);
+}
+
 void Trainer::check_device_errors(int64_t step) {
+  int32_t err[2] = {0, 0};
+  CUDA_CHECK(cudaMemcpy(err, d_err_, sizeof(err), cudaMemcpyDeviceToHost));
+  if (err[0])
+    fail(kRun, "a peer rank did not arrive at an NVLink barrier within SFCTR_BARRIER_TIMEOUT_S (" +
+                   std::to_string(barrier_timeout_ns() / 1000000000ull) + " s)",
+         step);
   int32_t bad = 0;
   CUDA_CHECK(cudaMemcpy(&bad, d_scalars_ + 1, sizeof(int32_t), cudaMemcpyDeviceToHost));
-  if (bad) {
-    CUDA_CHECK(cudaMemset(d_scalars_ + 1, 0, sizeof(int32_t)));
-    fail(kLogic, "feature id >= vocabulary size in the batch", step);
-  }
+  if (bad) raise_bad_id(step);
   int64_t cum = 0;
   for (int l = 0; l < lanes_; ++l) {
     int32_t c[kCntWords];

@@ -79,6 +79,9 @@ class Trainer {
   void sync_all();
   void finish_phases();
   void check_device_errors(int64_t step);
+  // clears the sticky bad-id flag, rolls the host's dense step back over the gated steps
+  // and raises the reference-style LogicError
+  [[noreturn]] void raise_bad_id(int64_t step);
   // waits for the stream, folds the device-side totals of host-wait-free steps into the
   // host ledger / stats, refreshes the per-step counters and the free-stack copies
   void refresh();
@@ -185,6 +188,10 @@ class Trainer {
   // each free one); d_acc_ accumulates their totals: U, owned, working, interworker bytes
   std::vector<int64_t> free_lb_;
   int64_t* d_acc_ = nullptr;
+  // [0] a flag barrier timed out (a peer never arrived), [1] steps gated by a bad id:
+  // after an id >= vocab is seen (d_scalars_[1], sticky until the host reports it) every
+  // step runs with no owned rows and skips the dense update, so no state moves
+  int32_t* d_err_ = nullptr;
   int64_t* h_acc_ = nullptr;
   bool acc_pending_ = false;    // d_acc_ holds steps not folded into the host totals yet
   bool last_step_free_ = false; // the last step skipped the host wait

@@ -174,7 +174,7 @@ void vsi_device(VsiScratch& v, const uint32_t* d_ids, int64_t n, uint32_t* d_gid
   vsi_emit_kernel<<<grid, 256, 0, s>>>(d_ids, n, v.d_first, v.d_rank, d_gids, d_vids, d_unique);
   CUDA_LAUNCH_CHECK();
   if (reset) {
-    vsi_reset_kernel<<<std::min(grid, 148 * 8), 256, 0, s>>>(d_gids, d_unique, v.d_first);
+    vsi_reset_kernel<<<std::min(grid, num_sms() * 8), 256, 0, s>>>(d_gids, d_unique, v.d_first);
     CUDA_LAUNCH_CHECK();
   }
 }

@@ -1,8 +1,14 @@
-"""Multi-GPU parity (NCCL path): W ranks, one per GPU, vs the CPU oracle running
-the same W-worker system. Both sync schemes — the reference's all-reduce of
-the common embedding / gradients and the owner-routed all-to-all — must give
-bit-exact cache slot tables, Adam step counts and ledger, and fp32-tolerance
-losses and rows (same bars as tests/test_gpu_parity.py). Skipped with < 2 GPUs."""
+"""Multi-GPU parity (NCCL / NVLink path): W ranks, one per GPU, vs the CPU oracle running
+the same W-worker system.
+
+* test_multi_rank_parity (tests/mp_parity_worker.py): cfg2 dimensions (d = 80, F = 39,
+  b = 1024 per GPU, 33.8M vocab), 10 steps, both sync schemes (the reference's all-reduce
+  and the owner-routed exchange), both run modes, with and without LRU evictions, at
+  W = 2 and 4; every step compared from identical state (tests/parity_util.py bars).
+* test_multi_rank_overlap (tests/mp_overlap_worker.py): steps kept in flight (the
+  pipelined manager of step t+1 overlapping step t's training across ranks), the
+  fallback transports, final state against the oracle's multi-step trajectory.
+Skipped with fewer GPUs than ranks."""
 import os
 import socket
 import subprocess
@@ -24,14 +30,35 @@ def _port():
     return p
 
 
+@pytest.mark.parametrize("n", [2, 4])
+@pytest.mark.parametrize("sync,mode,cache", [("allreduce", "sequential", 40000),
+                                             ("alltoall", "sequential", 40000),
+                                             ("allreduce", "pipelined", 40000),
+                                             ("alltoall", "pipelined", 40000),
+                                             ("alltoall", "pipelined", 200000)])
+def test_multi_rank_parity(n, sync, mode, cache):
+    if sb.device_count() < n:
+        pytest.skip(f"needs >= {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           os.path.join(ROOT, "tests", "mp_parity_worker.py"), "--sync", sync, "--mode", mode,
+           "--cache", str(cache)]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    print(out.stdout[-6000:], out.stderr[-3000:])
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert "parity ok" in out.stdout
+
+
 @pytest.mark.skipif(sb.device_count() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("sync,mode", [("allreduce", "sequential"), ("alltoall", "sequential"),
-                                       ("allreduce", "pipelined"), ("alltoall", "pipelined")])
-def test_two_rank_parity(sync, mode):
+@pytest.mark.parametrize("sync", ["allreduce", "alltoall"])
+def test_multi_rank_overlap(sync):
+    """Three steps in flight per rank: step t+1's manager stage overlaps step t's training
+    (and the peers' pushes of step t+1 race this rank's step-t reduction)."""
     n = min(sb.device_count(), 4)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
-           os.path.join(ROOT, "tests", "mp_parity_worker.py"), "--sync", sync, "--mode", mode]
+           os.path.join(ROOT, "tests", "mp_overlap_worker.py"), "--sync", sync, "--mode",
+           "pipelined"]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     print(out.stdout[-3000:], out.stderr[-3000:])
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
@@ -49,7 +76,7 @@ def test_two_rank_parity_fallback_transports(env):
     n = min(sb.device_count(), 4)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
-           os.path.join(ROOT, "tests", "mp_parity_worker.py"), "--sync", "alltoall",
+           os.path.join(ROOT, "tests", "mp_overlap_worker.py"), "--sync", "alltoall",
            "--mode", "pipelined"]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
                          env={**os.environ, **env})

@@ -301,6 +301,56 @@ def test_feature_out_of_vocab_is_a_logic_error():
         tr.step(0, np.array([1, 2, 3, 100], np.uint64), np.zeros(2, np.uint8))
 
 
+@pytest.mark.parametrize("mode", ["sequential", "pipelined"])
+def test_out_of_vocab_moves_no_state(mode):
+    """An id >= vocab is a LogicError that leaves every piece of state as it was, also when
+    the step was enqueued without a host wait (device inputs, host-wait-free steps: the
+    error surfaces at the next synchronising call). Training then continues exactly like a
+    trainer that never saw the bad batch."""
+    import torch
+    cfg = sb.Config(num_workers=1, batch_size_per_worker=64, num_fields=6, embedding_dim=8,
+                    vocabulary_size=5000, cache_capacity=5000, hidden_dim=16)
+    cfg.apply("mode", mode)
+    gen = sb.SyntheticGenerator(cfg)
+    batches = [gen.generate(t) for t in range(4)]
+    ref = sb.Trainer(cfg)
+    tr = sb.Trainer(cfg)
+    for t in range(2):
+        ref.step(t, *batches[t])
+        tr.step(t, *batches[t])
+    before = tr.snapshot(), tr.dense_state()
+    bad = batches[2][0].copy()
+    bad[17] = cfg.vocabulary_size + 3
+    # host-wait-free device step: enqueued, the error comes at synchronize()
+    d_f = torch.from_numpy(bad.view(np.int64)).cuda()
+    d_y = torch.from_numpy(batches[2][1]).cuda()
+    tr.step_device(2, d_f.data_ptr(), d_y.data_ptr())
+    with pytest.raises(sb.LogicError):
+        tr.synchronize()
+    after = tr.snapshot(), tr.dense_state()
+    for a, b in zip(before[0], after[0]):
+        assert np.array_equal(a, b)
+    for a, b in zip(before[1][:3], after[1][:3]):
+        assert np.array_equal(a, b)
+    assert before[1][3] == after[1][3]
+    # host-buffer step: raises at once, nothing moves either
+    with pytest.raises(sb.LogicError):
+        tr.step(2, bad, batches[2][1])
+    for a, b in zip(before[0], tr.snapshot()):
+        assert np.array_equal(a, b)
+    # continues like the reference trainer
+    for t in (2, 3):
+        l1 = ref.step(t, *batches[t])
+        l2 = tr.step(t, *batches[t])
+        assert abs(l1 - l2) <= 1e-6 * abs(l1)
+    fr, rr, sr = ref.snapshot()
+    ft, rt, st = tr.snapshot()
+    assert np.array_equal(fr, ft) and np.array_equal(sr, st)
+    assert np.max(np.abs(rr - rt)) <= 1e-6
+    ref.close()
+    tr.close()
+
+
 def test_worker_count_invariance_device():
     """SPEC acceptance 4 on the device: W in {1,2,4} on the same global batches."""
     snaps = []
