@@ -66,7 +66,8 @@ def parse():
                    help="run the MixCache sub-lines only (development)")
     p.add_argument("--cfg4-cache-frac", type=float, default=0.10,
                    help="cfg4 hot cache as a fraction of HBM (BASELINE configs[3]: 10-50 %%)")
-    p.add_argument("--cpu-rows", type=int, default=2048, help="rows per CPU-baseline step")
+    p.add_argument("--cpu-rows", type=int, default=8192,
+                   help="rows per CPU-baseline step (default: the full cfg2 batch per GPU)")
     p.add_argument("--cpu-steps", type=int, default=3)
     return p.parse_args()
 
@@ -103,7 +104,7 @@ class Clocks:
     REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
                "sw_power_cap": 0x4}
 
-    def __init__(self, indices, period_s=0.005):
+    def __init__(self, indices, period_s=0.001):
         self.indices, self.period = list(indices), period_s
         self.proc = None
 
@@ -134,7 +135,8 @@ class Clocks:
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(self.mx) if self.mx else None, "reasons": sorted(reasons),
                 "samples": len(sm), "gpus": len(self.indices),
-                "sampler": "nvml 5 ms, separate process"}
+                "sampler": "nvml every 1 ms in a separate process, from the start of the value "
+                           "region through the phase pass and the e2e region"}
 
 
 def phase_bytes(name, U, Uw, n, b, d, F, H, Ntot, fused_scatter=False, xrecv=0):
@@ -227,7 +229,6 @@ def run_ours(args, D):
     ev1.synchronize()
     torch.cuda.synchronize()
     dev_ms = ev0.elapsed_time(ev1)
-    clk = clocks.stop() if clocks else None
     tr.synchronize()  # deferred device counters
     st1 = tr.stats()
     tot = {k2: st1[k2] - st0[k2] for k2 in st1 if k2.startswith("total")}
@@ -281,6 +282,9 @@ def run_ours(args, D):
             losses.append(tr.step(s, hf[s], hl[s]))
     torch.cuda.synchronize()
     e2e_s = D.max(time.perf_counter() - w0)
+    # the sampler ran from the start of the `value` region through the phase pass and the
+    # e2e region (the value region alone is a few ms, shorter than NVML's update period)
+    clk = clocks.stop() if clocks else None
     D.barrier()
 
     rows_global = world * args.batch
