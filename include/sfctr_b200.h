@@ -290,6 +290,63 @@ int sfctr_trainer_phase_times(sfctr_trainer* t, int32_t max_phases, char* names 
                               float* ms, int32_t* n_phases);
 
 /* ---------------------------------------------------------------------
+ * Standalone device MixCache of ONE worker — CacheBuffer (cache_buffer.hpp:40-86) with its
+ * HostStore (host_store.hpp:61-92, a lazy pinned host pool of evicted rows) and the manager
+ * step, for callers that drive the cache themselves. The worker owns
+ * features f < key_space with f % num_workers == worker (shard_owner); rows
+ * are [emb | m | v] (dim each, fp32) + adam_steps, lazily initialised with
+ * initial_embedding(seed, f, dim) on first admission (HostStore::get_or_init).
+ *
+ * Batched operations take HOST arrays of n features and apply in list order with the
+ * reference's one-at-a-time semantics: they stop at the first feature the reference
+ * would throw on and return SFCTR_ERR_LOGIC with its message (cache_buffer.cpp), the
+ * preceding features having taken effect. n <= max_batch per call.
+ * ------------------------------------------------------------------- */
+typedef struct sfctr_cache sfctr_cache;
+/* CacheBuffer(capacity, dim) + HostStore(seed, dim); host_reserve pins host-pool rows up
+ * front (the pool grows on demand) */
+int sfctr_cache_create(uint64_t capacity, int32_t dim, uint64_t seed, uint64_t key_space,
+                       int32_t num_workers, int32_t worker, int64_t max_batch,
+                       uint64_t host_reserve, int device, sfctr_cache** out);
+void sfctr_cache_destroy(sfctr_cache* c);
+/* admit(f, host.take(f), step) (cache_buffer.cpp:38-53): needed_soon set, unpinned;
+ * slots (nullable) [n] receive the SlotIds */
+int sfctr_cache_admit(sfctr_cache* c, int64_t n, const uint64_t* features, int64_t step,
+                      uint64_t* slots);
+/* host.put(f, evict(f)) (cache_buffer.cpp:55-67): non-resident / pinned / needed_soon is
+ * SFCTR_ERR_LOGIC */
+int sfctr_cache_evict(sfctr_cache* c, int64_t n, const uint64_t* features);
+int sfctr_cache_touch(sfctr_cache* c, int64_t n, const uint64_t* features, int64_t step);
+/* pin (pinned != 0) / unpin */
+int sfctr_cache_pin(sfctr_cache* c, int64_t n, const uint64_t* features, int32_t pinned);
+int sfctr_cache_set_needed_soon(sfctr_cache* c, int64_t n, const uint64_t* features,
+                                int32_t value);
+/* slot_of: SlotId per feature, -1 when not resident (resident() == slot >= 0) */
+int sfctr_cache_slot_of(sfctr_cache* c, int64_t n, const uint64_t* features, int64_t* slots);
+int sfctr_cache_free_count(sfctr_cache* c, uint64_t* out);
+/* slots(): per slot feature (UINT64_MAX = free), last_use, admit_seq, pinned, needed_soon
+ * (any pointer may be NULL) */
+int sfctr_cache_slots(sfctr_cache* c, uint64_t* feature, int64_t* last_use, uint64_t* admit_seq,
+                      uint8_t* pinned, uint8_t* needed_soon);
+/* capacity, occupied, free, pinned, needed_soon; and occupancy_diagnostics() text */
+int sfctr_cache_occupancy(sfctr_cache* c, uint64_t out[5]);
+int sfctr_cache_occupancy_diagnostics(sfctr_cache* c, char* buf, size_t cap);
+/* HostStore::peek / slot(s).entry: rows [n*3d] (emb|m|v) + steps [n], cache or host */
+int sfctr_cache_peek(sfctr_cache* c, int64_t n, const uint64_t* features, float* rows,
+                     int64_t* steps);
+/* One manager step for this worker (manager_get + pull_parameters_to_host +
+ * push_parameters_to_cache): global_ids [n_global] = the step's
+ * DedupBatch::global_ids (all workers'; the owned ones are taken in order), window_ids
+ * [n_window] = every feature of the lookahead batches t..t+L-1 (duplicates allowed, may
+ * be empty). needed_soon := resident window features; hits touched; misses admitted in
+ * global_ids order after evicting the LRU (last_use, admit_seq) slots that are neither
+ * pinned nor needed_soon. Capacity shortfall is SFCTR_ERR_RUN before anything moves.
+ * Steps must increase. out (nullable) [5]: owned, hits, admitted, evicted, refilled from
+ * the host pool. */
+int sfctr_cache_prepare(sfctr_cache* c, int64_t step, int64_t n_global, const uint64_t* global_ids,
+                        int64_t n_window, const uint64_t* window_ids, int64_t out[5]);
+
+/* ---------------------------------------------------------------------
  * DeepFM-lite forward_backward on the device, standalone:
  * x [rows, F*d] fp32 host, labels [rows]; dense params as above. Outputs
  * (host, any may be NULL): loss (mean BCE), logits [rows], dx [rows, F*d]

@@ -13,6 +13,7 @@
 
 #include "sfctr/batch.hpp"
 #include "sfctr/error.hpp"
+#include "sfctr/host_store.hpp"
 #include "sfctr_b200.h"
 
 namespace sfctr {
@@ -117,6 +118,87 @@ inline DedupBatch virtual_sparse_id(const RawBatch& batch, int num_workers, int 
   for (int w = 0; w < num_workers; ++w) d.worker_row_ranges.push_back({rr[2 * w], rr[2 * w + 1]});
   return d;
 }
+
+// CacheBuffer (cache_buffer.hpp:40-86) of one worker with its HostStore and the manager
+// step, on the device: the reference's member functions, SlotId / FeatureId / ParamEntry
+// in and out, the reference's exceptions. evict() returns the evicted entry (fp32 state
+// widened to the reference's fp64 ParamEntry) after it went to the host pool.
+class CacheBuffer {
+ public:
+  CacheBuffer(std::uint64_t capacity, int dim, std::uint64_t seed, std::uint64_t key_space,
+              int num_workers = 1, int worker = 0, std::int64_t max_batch = 1 << 16,
+              int device = 0)
+      : dim_(dim), capacity_(capacity) {
+    check(sfctr_cache_create(capacity, dim, seed, key_space, num_workers, worker, max_batch, 0,
+                             device, &c_));
+  }
+  ~CacheBuffer() { sfctr_cache_destroy(c_); }
+  CacheBuffer(const CacheBuffer&) = delete;
+  CacheBuffer& operator=(const CacheBuffer&) = delete;
+
+  std::uint64_t capacity() const { return capacity_; }
+  std::size_t free_count() const {
+    std::uint64_t n = 0;
+    check(sfctr_cache_free_count(c_, &n));
+    return static_cast<std::size_t>(n);
+  }
+  std::size_t occupied_count() const { return capacity_ - free_count(); }
+  bool resident(FeatureId f) const { return raw_slot(f) >= 0; }
+  SlotId slot_of(FeatureId f) const {  // cache_buffer.cpp:31-35
+    const std::int64_t s = raw_slot(f);
+    if (s < 0) throw LogicError("feature " + std::to_string(f.value) + " not resident");
+    return SlotId{static_cast<std::uint64_t>(s)};
+  }
+  SlotId admit(FeatureId f, std::int64_t step) {  // admit(f, host.take(f), step)
+    std::uint64_t slot = 0;
+    check(sfctr_cache_admit(c_, 1, &f.value, step, &slot));
+    return SlotId{slot};
+  }
+  ParamEntry evict(FeatureId f) {  // host.put(f, evict(f)); returns the entry
+    check(sfctr_cache_evict(c_, 1, &f.value));
+    std::vector<float> row(3 * static_cast<std::size_t>(dim_));
+    std::int64_t steps = 0;
+    check(sfctr_cache_peek(c_, 1, &f.value, row.data(), &steps));
+    ParamEntry e(dim_);
+    for (std::size_t i = 0; i < row.size(); ++i) e.data[i] = row[i];
+    e.adam_steps = steps;
+    return e;
+  }
+  void touch(FeatureId f, std::int64_t step) { check(sfctr_cache_touch(c_, 1, &f.value, step)); }
+  void pin(FeatureId f) { check(sfctr_cache_pin(c_, 1, &f.value, 1)); }
+  void unpin(FeatureId f) { check(sfctr_cache_pin(c_, 1, &f.value, 0)); }
+  void set_needed_soon(FeatureId f, bool value) {
+    check(sfctr_cache_set_needed_soon(c_, 1, &f.value, value ? 1 : 0));
+  }
+  std::string occupancy_diagnostics() const {
+    char buf[256];
+    check(sfctr_cache_occupancy_diagnostics(c_, buf, sizeof(buf)));
+    return buf;
+  }
+  // manager_get + pull + push for this worker: owned, hits, admitted,
+  // evicted, refilled
+  std::vector<std::int64_t> prepare(std::int64_t step, const std::vector<FeatureId>& global_ids,
+                                    const std::vector<FeatureId>& window = {}) {
+    std::vector<std::uint64_t> g(global_ids.size()), w(window.size());
+    for (std::size_t i = 0; i < g.size(); ++i) g[i] = global_ids[i].value;
+    for (std::size_t i = 0; i < w.size(); ++i) w[i] = window[i].value;
+    std::vector<std::int64_t> out(5);
+    check(sfctr_cache_prepare(c_, step, static_cast<std::int64_t>(g.size()), g.data(),
+                              static_cast<std::int64_t>(w.size()), w.data(), out.data()));
+    return out;
+  }
+  sfctr_cache* handle() { return c_; }
+
+ private:
+  std::int64_t raw_slot(FeatureId f) const {
+    std::int64_t s = -1;
+    check(sfctr_cache_slot_of(c_, 1, &f.value, &s));
+    return s;
+  }
+  int dim_;
+  std::uint64_t capacity_;
+  sfctr_cache* c_ = nullptr;
+};
 
 // HostStore + CacheBuffer per worker + worker ops: one BSP step per call.
 class Trainer {

@@ -137,7 +137,7 @@ constexpr int kHistBins = 8192;  // shared-memory bins per level
 __global__ void __launch_bounds__(1024) lru_hist_kernel(
     uint32_t C, const uint32_t* __restrict__ slot_feat, const int32_t* __restrict__ mark, int32_t t,
     const int32_t* __restrict__ last_use, uint32_t* __restrict__ hist, int nbins, int shift,
-    int32_t* __restrict__ cnt, int base_shift, bool level2) {
+    int32_t* __restrict__ cnt, int base_shift, bool level2, const uint8_t* __restrict__ pin) {
   __shared__ uint32_t sh[kHistBins];
   __shared__ uint32_t old_blk;
   for (int i = threadIdx.x; i < nbins; i += blockDim.x) sh[i] = 0;
@@ -171,8 +171,11 @@ __global__ void __launch_bounds__(1024) lru_hist_kernel(
         }
       }
     }
-    const uint32_t fa[4] = {f.x, f.y, f.z, f.w};
+    uint32_t fa[4] = {f.x, f.y, f.z, f.w};
     const int32_t ma[4] = {mk.x, mk.y, mk.z, mk.w}, la[4] = {lu.x, lu.y, lu.z, lu.w};
+    if (pin && q < q1)  // standalone CacheBuffer: pinned slots are not evictable
+      for (int e = 0; e < 4; ++e)
+        if (4 * q + e < C && pin[4 * q + e]) fa[e] = kEmpty;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       int bin = -1;
@@ -249,6 +252,7 @@ __global__ void __launch_bounds__(1024) lru_select_kernel(const uint32_t* __rest
     } else {
       cnt[kCntSelB] = found;
       cnt[kCntSelBelow] = static_cast<int32_t>(found_below);
+      cnt[kCntSelTotal] = static_cast<int32_t>(part[1023] < 0x7FFFFFFFull ? part[1023] : 0x7FFFFFFFull);
       if (shift == 0) cnt[kCntSelT] = found;
     }
     cnt[kCntSelN] = 0;
@@ -263,7 +267,8 @@ __global__ void lru_collect_kernel(uint32_t C, const uint32_t* __restrict__ slot
                                    const int32_t* __restrict__ last_use,
                                    const uint64_t* __restrict__ admit_seq,
                                    int32_t* __restrict__ cnt, int64_t cap,
-                                   uint64_t* __restrict__ keys, uint32_t* __restrict__ ids) {
+                                   uint64_t* __restrict__ keys, uint32_t* __restrict__ ids,
+                                   const uint8_t* __restrict__ pin) {
   const int lane = threadIdx.x & 31;
   const int32_t T = cnt[kCntSelT];
   const uint64_t C4 = (static_cast<uint64_t>(C) + 3) >> 2;
@@ -290,8 +295,11 @@ __global__ void lru_collect_kernel(uint32_t C, const uint32_t* __restrict__ slot
         }
       }
     }
-    const uint32_t fa[4] = {f.x, f.y, f.z, f.w};
+    uint32_t fa[4] = {f.x, f.y, f.z, f.w};
     const int32_t ma[4] = {mk.x, mk.y, mk.z, mk.w}, la[4] = {lu.x, lu.y, lu.z, lu.w};
+    if (pin && q < C4)
+      for (int e = 0; e < 4; ++e)
+        if (4 * q + e < C && pin[4 * q + e]) fa[e] = kEmpty;
     uint32_t take = 0;
 #pragma unroll
     for (int e = 0; e < 4; ++e)
@@ -817,7 +825,7 @@ void CacheLane::init(uint64_t capacity, int dim, uint64_t owned_rows, uint64_t h
   CUDA_CHECK(cudaMalloc(&work_w, sizeof(uint32_t) * umax));
   scan_bytes = scan_temp_bytes(umax);
   sort_bytes = 0;
-  if (C < rows) {  // evictions possible: LRU candidate lists of n_evict + umax <= 2 umax
+  {  // LRU candidate lists of n_evict + umax <= 2 umax (also the explicit eviction lists)
     cand_cap = 2 * umax;
     CUDA_CHECK(cudaMalloc(&keys, sizeof(uint64_t) * cand_cap));
     CUDA_CHECK(cudaMalloc(&keys_sorted, sizeof(uint64_t) * cand_cap));
@@ -891,7 +899,7 @@ void CacheLane::probe(const uint32_t* d_gids, int32_t cap, uint32_t W, int32_t t
   CUDA_LAUNCH_CHECK();
 }
 
-void CacheLane::victim_select(int32_t t, int32_t n_evict, cudaStream_t s) {
+void CacheLane::victim_select(int32_t t, int32_t n_evict, cudaStream_t s, const uint8_t* pinned) {
   if (!hist) CUDA_CHECK(cudaMalloc(&hist, sizeof(uint32_t) * 2 * kHistBins));
   // level 1: last_use >> shift over [0, t] in at most kHistBins bins
   int shift = 0;
@@ -901,13 +909,14 @@ void CacheLane::victim_select(int32_t t, int32_t n_evict, cudaStream_t s) {
   CUDA_CHECK(cudaMemsetAsync(counters + kCntOld, 0, sizeof(int32_t), s));
   const int grid = std::max(1, std::min<int>(ceil_div(static_cast<int64_t>(C), 16384), 2 * num_sms()));
   lru_hist_kernel<<<grid, 1024, 0, s>>>(static_cast<uint32_t>(C), slot_feat, mark, t, last_use,
-                                        hist, nb1, shift, counters, 0, false);
+                                        hist, nb1, shift, counters, 0, false, pinned);
   CUDA_LAUNCH_CHECK();
   lru_select_kernel<<<1, 1024, 0, s>>>(hist, nb1, n_evict, counters, shift, false);
   CUDA_LAUNCH_CHECK();
   if (shift > 0) {  // level 2: the 2^shift steps of the coarse bin, exactly
     lru_hist_kernel<<<grid, 1024, 0, s>>>(static_cast<uint32_t>(C), slot_feat, mark, t, last_use,
-                                          hist + kHistBins, 1 << shift, 0, counters, shift, true);
+                                          hist + kHistBins, 1 << shift, 0, counters, shift, true,
+                                          pinned);
     CUDA_LAUNCH_CHECK();
     lru_select_kernel<<<1, 1024, 0, s>>>(hist + kHistBins, 1 << shift, n_evict, counters, shift,
                                          true);
@@ -915,20 +924,21 @@ void CacheLane::victim_select(int32_t t, int32_t n_evict, cudaStream_t s) {
   }
 }
 
-void CacheLane::victim_sort(int32_t t, int32_t n_evict, cudaStream_t s) {
+void CacheLane::victim_sort(int32_t t, int32_t n_evict, cudaStream_t s, const uint8_t* pinned) {
   const int64_t bound = std::min<int64_t>(cand_cap, static_cast<int64_t>(n_evict) + umax);
   CUDA_CHECK(cudaMemsetAsync(keys, 0xFF, sizeof(uint64_t) * bound, s));
   const int grid = static_cast<int>(std::min<int64_t>(ceil_div(static_cast<int64_t>(C), 1024), num_sms() * 8));
   lru_collect_kernel<<<grid, 256, 0, s>>>(static_cast<uint32_t>(C), slot_feat, mark, t, last_use,
-                                          admit_seq, counters, bound, keys, ids);
+                                          admit_seq, counters, bound, keys, ids, pinned);
   CUDA_LAUNCH_CHECK();
   sort_pairs_u64_u32(temp, sort_bytes, keys, keys_sorted, ids, ids_sorted, bound, 64, s);
 }
 
-void CacheLane::evict(int32_t n_evict, uint32_t W, int32_t t, cudaStream_t s, bool selected) {
+void CacheLane::evict(int32_t n_evict, uint32_t W, int32_t t, cudaStream_t s, bool selected,
+                      const uint8_t* pinned) {
   if (n_evict <= 0) return;
-  if (!selected) victim_select(t, n_evict, s);
-  victim_sort(t, n_evict, s);
+  if (!selected) victim_select(t, n_evict, s, pinned);
+  victim_sort(t, n_evict, s, pinned);
   evict_kernel<<<ceil_div(static_cast<int64_t>(n_evict) * 32, 256), 256, 0, s>>>(
       n_evict, keys_sorted, ids_sorted, slot_feat, W, d, emb, mom, vel, steps, host.tab(),
       slot_host, counters + kCntHostNext, index, free_stack, counters + kCntFreeTop,
@@ -939,19 +949,20 @@ void CacheLane::evict(int32_t n_evict, uint32_t W, int32_t t, cudaStream_t s, bo
 bool CacheLane::swap_supported() const { return (d & 3) == 0 && 3 * (d / 4) <= 64; }
 
 void CacheLane::evict_admit(int32_t n_evict, int32_t n_work, uint32_t W, uint64_t seed, int32_t t,
-                            cudaStream_t s, bool selected, const PhaseHook& hook) {
+                            cudaStream_t s, bool selected, const PhaseHook& hook,
+                            const uint8_t* pinned) {
   if (n_evict > 0) {  // every victim may need a new host slot (host.hi: exact as of the
     host.ensure(host.hi + static_cast<uint64_t>(n_evict), s);  // last host wait)
     host.hi += static_cast<uint64_t>(n_evict);
   }
   if (n_evict <= 0 || !swap_supported()) {
-    evict(n_evict, W, t, s, selected);
+    evict(n_evict, W, t, s, selected, pinned);
     admit(n_work, n_evict, W, seed, t, s);
     return;
   }
-  if (!selected) victim_select(t, n_evict, s);
+  if (!selected) victim_select(t, n_evict, s, pinned);
   hook("evict_select");
-  victim_sort(t, n_evict, s);
+  victim_sort(t, n_evict, s, pinned);
   hook("evict_sort");
   swap_kernel<<<ceil_div(static_cast<int64_t>(n_work) * 32, 256), 256, 0, s>>>(
       counters, n_evict, keys_sorted, ids_sorted, work_j, work_f, work_w, W, d / 4, free_stack,
@@ -975,6 +986,87 @@ void CacheLane::admit(int32_t n_bound, int32_t n_evict, uint32_t W, uint64_t see
     CUDA_LAUNCH_CHECK();
   }
   advance_kernel<<<1, 1, 0, s>>>(counters, n_evict);
+  CUDA_LAUNCH_CHECK();
+}
+
+// ---- explicit CacheBuffer operations (the standalone device CacheBuffer, cachebuf.cu) ----
+namespace {
+// err = min over offending positions of (i << 8 | code): 1 already resident, 2 not resident,
+// 3 pinned, 4 inside the lookahead window (cache_buffer.cpp:39,57-61). mode 0: admit (must
+// not be resident), 1: must be resident, 2: evict (resident, unpinned, not needed_soon)
+__global__ void check_list_kernel(const uint64_t* __restrict__ feats, int32_t n, uint32_t W,
+                                  const uint32_t* __restrict__ index, uint32_t C,
+                                  const uint8_t* __restrict__ pinned,
+                                  const int32_t* __restrict__ mark, int32_t epoch, int mode,
+                                  unsigned long long* __restrict__ err) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t s = index[static_cast<uint32_t>(feats[i]) / W];
+  unsigned long long code = 0;
+  if (mode == 0) {
+    if (s < C) code = 1;
+  } else if (s >= C) {
+    code = 2;
+  } else if (mode == 2) {
+    if (pinned && pinned[s]) code = 3;
+    else if (mark[s] == epoch) code = 4;
+  }
+  if (code) atomicMin(err, (static_cast<unsigned long long>(i) << 8) | code);
+}
+__global__ void admit_list_prep_kernel(const uint64_t* __restrict__ feats, int32_t n, uint32_t W,
+                                       const uint32_t* __restrict__ index,
+                                       uint32_t* __restrict__ work_j, uint32_t* __restrict__ work_f,
+                                       uint32_t* __restrict__ work_w, int32_t* __restrict__ cnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) cnt[kCntWorking] = n;
+  if (i >= n) return;
+  const uint32_t f = static_cast<uint32_t>(feats[i]);
+  work_j[i] = static_cast<uint32_t>(i);
+  work_f[i] = f;
+  work_w[i] = index[f / W];  // host slot / kNever (checked: not resident)
+}
+// the slots of `feats` in order as the "sorted" victims of evict_kernel
+__global__ void evict_list_prep_kernel(const uint64_t* __restrict__ feats, int32_t n, uint32_t W,
+                                       const uint32_t* __restrict__ index,
+                                       uint64_t* __restrict__ keys, uint32_t* __restrict__ ids,
+                                       int32_t* __restrict__ cnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) cnt[kCntWorking] = 0;
+  if (i >= n) return;
+  keys[i] = 0;
+  ids[i] = index[static_cast<uint32_t>(feats[i]) / W];
+}
+}  // namespace
+
+void CacheLane::check_list(const uint64_t* d_feats, int32_t n, uint32_t W, const uint8_t* pinned,
+                           int32_t epoch, int mode, unsigned long long* d_err, cudaStream_t s) {
+  if (n <= 0) return;
+  check_list_kernel<<<ceil_div(n, 256), 256, 0, s>>>(d_feats, n, W, index, static_cast<uint32_t>(C),
+                                                     pinned, mark, epoch, mode, d_err);
+  CUDA_LAUNCH_CHECK();
+}
+
+void CacheLane::admit_list(const uint64_t* d_feats, int32_t n, uint32_t W, uint64_t seed,
+                           int32_t t, cudaStream_t s) {
+  if (n <= 0) return;
+  admit_list_prep_kernel<<<ceil_div(n, 256), 256, 0, s>>>(d_feats, n, W, index, work_j, work_f,
+                                                          work_w, counters);
+  CUDA_LAUNCH_CHECK();
+  admit(n, 0, W, seed, t, s);
+}
+
+void CacheLane::evict_list(const uint64_t* d_feats, int32_t n, uint32_t W, cudaStream_t s) {
+  if (n <= 0) return;
+  host.ensure(host.hi + static_cast<uint64_t>(n), s);
+  host.hi += static_cast<uint64_t>(n);
+  evict_list_prep_kernel<<<ceil_div(n, 256), 256, 0, s>>>(d_feats, n, W, index, keys_sorted,
+                                                          ids_sorted, counters);
+  CUDA_LAUNCH_CHECK();
+  evict_kernel<<<ceil_div(static_cast<int64_t>(n) * 32, 256), 256, 0, s>>>(
+      n, keys_sorted, ids_sorted, slot_feat, W, d, emb, mom, vel, steps, host.tab(), slot_host,
+      counters + kCntHostNext, index, free_stack, counters + kCntFreeTop, counters + kCntError);
+  CUDA_LAUNCH_CHECK();
+  advance_kernel<<<1, 1, 0, s>>>(counters, n);
   CUDA_LAUNCH_CHECK();
 }
 

@@ -29,6 +29,7 @@ enum {
   kCntSelN = 11,     // LRU select: candidates collected (last_use <= T)
   kCntSelB = 12,     // LRU select: coarse (level-1) bin of the threshold
   kCntSelBelow = 13, // LRU select: eligible slots below the coarse bin
+  kCntSelTotal = 14, // LRU select: eligible slots in total
   kCntWords = 16
 };
 
@@ -157,13 +158,16 @@ struct CacheLane {
   // (occupied && !needed_soon) over last_use, then the threshold step T with
   // #(last_use < T) < n_evict <= #(last_use <= T) (counters[kCntSelT]), and the count of
   // eligible slots last used before step t-1 (counters[kCntOld], pipelined eviction safety)
-  void victim_select(int32_t t, int32_t n_evict, cudaStream_t s);
+  // pinned (nullable): per-slot pin flags of a standalone CacheBuffer (cachebuf.cu); the
+  // trainer's pins are implied by stream order
+  void victim_select(int32_t t, int32_t n_evict, cudaStream_t s, const uint8_t* pinned = nullptr);
   // collects the candidates (last_use <= T) and sorts them by (last_use, admit_seq): the
   // first n_evict are the victims, oldest first
-  void victim_sort(int32_t t, int32_t n_evict, cudaStream_t s);
+  void victim_sort(int32_t t, int32_t n_evict, cudaStream_t s, const uint8_t* pinned = nullptr);
   // victims go on top of the device free stack; n_evict is host-known (sync steps only);
   // selected: victim_select already ran for this step
-  void evict(int32_t n_evict, uint32_t W, int32_t t, cudaStream_t s, bool selected = false);
+  void evict(int32_t n_evict, uint32_t W, int32_t t, cudaStream_t s, bool selected = false,
+             const uint8_t* pinned = nullptr);
   // admits counters[kCntWorking] rows (device count, <= n_bound) from the device free
   // stack, then advances the device free-stack height (+ n_evict - n_work) and admit_seq
   void admit(int32_t n_bound, int32_t n_evict, uint32_t W, uint64_t seed, int32_t t,
@@ -171,8 +175,20 @@ struct CacheLane {
   // eviction step (host-known n_evict / n_work): write-back and admission fused per slot
   // (swap_kernel) when the row fits the register staging, else evict() then admit()
   void evict_admit(int32_t n_evict, int32_t n_work, uint32_t W, uint64_t seed, int32_t t,
-                   cudaStream_t s, bool selected, const PhaseHook& hook = {});
+                   cudaStream_t s, bool selected, const PhaseHook& hook = {},
+                   const uint8_t* pinned = nullptr);
   bool swap_supported() const;
+  // Explicit CacheBuffer operations on a device list of n <= umax owned features (the
+  // standalone DeviceCache, cachebuf.cu). check_list: *d_err = min (i << 8 | code) over the
+  // offending positions (1 already resident, 2 not resident, 3 pinned, 4 needed_soon, i.e.
+  // mark == epoch); mode 0 admit, 1 resident, 2 evict. admit_list / evict_list expect a
+  // checked list: admissions pop the LIFO free list in list order, evictions push their
+  // slots in list order (cache_buffer.cpp:41-42,64).
+  void check_list(const uint64_t* d_feats, int32_t n, uint32_t W, const uint8_t* pinned,
+                  int32_t epoch, int mode, unsigned long long* d_err, cudaStream_t s);
+  void admit_list(const uint64_t* d_feats, int32_t n, uint32_t W, uint64_t seed, int32_t t,
+                  cudaStream_t s);
+  void evict_list(const uint64_t* d_feats, int32_t n, uint32_t W, cudaStream_t s);
 };
 
 }  // namespace sfb

@@ -11,6 +11,7 @@
 #include <sstream>
 #include <string>
 
+#include "cachebuf.h"
 #include "criteo.h"
 #include "trainer.h"
 
@@ -151,6 +152,10 @@ struct sfctr_vsi {
 
 struct sfctr_trainer {
   std::unique_ptr<sfb::Trainer> t;
+};
+
+struct sfctr_cache {
+  std::unique_ptr<sfb::DeviceCache> c;
 };
 
 extern "C" {
@@ -527,6 +532,72 @@ int sfctr_trainer_create(const sfctr_config* cfg, int32_t rank, int32_t world,
 }
 
 void sfctr_trainer_destroy(sfctr_trainer* t) { delete t; }
+
+// ---- standalone device CacheBuffer + HostStore + manager (cachebuf.h) ----
+int sfctr_cache_create(uint64_t capacity, int32_t dim, uint64_t seed, uint64_t key_space,
+                       int32_t num_workers, int32_t worker, int64_t max_batch,
+                       uint64_t host_reserve, int device, sfctr_cache** out) {
+  return guarded([&] {
+    SFB_CHECK(out != nullptr, "out");
+    auto* c = new sfctr_cache;
+    try {
+      c->c = std::make_unique<sfb::DeviceCache>(capacity, dim, seed, key_space, num_workers,
+                                                worker, max_batch, host_reserve, device);
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+void sfctr_cache_destroy(sfctr_cache* c) { delete c; }
+int sfctr_cache_admit(sfctr_cache* c, int64_t n, const uint64_t* features, int64_t step,
+                      uint64_t* slots) {
+  return guarded([&] { c->c->admit(n, features, step, slots); });
+}
+int sfctr_cache_evict(sfctr_cache* c, int64_t n, const uint64_t* features) {
+  return guarded([&] { c->c->evict(n, features); });
+}
+int sfctr_cache_touch(sfctr_cache* c, int64_t n, const uint64_t* features, int64_t step) {
+  return guarded([&] { c->c->touch(n, features, step); });
+}
+int sfctr_cache_pin(sfctr_cache* c, int64_t n, const uint64_t* features, int32_t pinned) {
+  return guarded([&] { c->c->pin(n, features, pinned != 0); });
+}
+int sfctr_cache_set_needed_soon(sfctr_cache* c, int64_t n, const uint64_t* features,
+                                int32_t value) {
+  return guarded([&] { c->c->set_needed_soon(n, features, value != 0); });
+}
+int sfctr_cache_slot_of(sfctr_cache* c, int64_t n, const uint64_t* features, int64_t* slots) {
+  return guarded([&] { c->c->slot_of(n, features, slots); });
+}
+int sfctr_cache_free_count(sfctr_cache* c, uint64_t* out) {
+  return guarded([&] { *out = c->c->free_count(); });
+}
+int sfctr_cache_slots(sfctr_cache* c, uint64_t* feature, int64_t* last_use, uint64_t* admit_seq,
+                      uint8_t* pinned, uint8_t* needed_soon) {
+  return guarded([&] { c->c->slots(feature, last_use, admit_seq, pinned, needed_soon); });
+}
+int sfctr_cache_occupancy(sfctr_cache* c, uint64_t out[5]) {
+  return guarded([&] { c->c->occupancy(out); });
+}
+int sfctr_cache_occupancy_diagnostics(sfctr_cache* c, char* buf, size_t cap) {
+  return guarded([&] {
+    const std::string d = c->c->occupancy_diagnostics();
+    if (buf && cap) {
+      std::strncpy(buf, d.c_str(), cap - 1);
+      buf[cap - 1] = 0;
+    }
+  });
+}
+int sfctr_cache_peek(sfctr_cache* c, int64_t n, const uint64_t* features, float* rows,
+                     int64_t* steps) {
+  return guarded([&] { c->c->peek(n, features, rows, steps); });
+}
+int sfctr_cache_prepare(sfctr_cache* c, int64_t step, int64_t n_global, const uint64_t* global_ids,
+                        int64_t n_window, const uint64_t* window_ids, int64_t out[5]) {
+  return guarded([&] { c->c->prepare(step, n_global, global_ids, n_window, window_ids, out); });
+}
 
 int sfctr_trainer_step(sfctr_trainer* t, int64_t step, const uint64_t* features,
                        const uint8_t* labels, const uint64_t* window, double* loss) {

@@ -186,6 +186,21 @@ SIGNATURES = [
     ("sfctr_trainer_stats", C.c_int, [P, C.POINTER(StepStats)]),
     ("sfctr_trainer_set_timing", C.c_int, [P, C.c_int]),
     ("sfctr_trainer_phase_times", C.c_int, [P, C.c_int32, C.c_char_p, f32p, C.POINTER(C.c_int32)]),
+    ("sfctr_cache_create", C.c_int, [C.c_uint64, C.c_int32, C.c_uint64, C.c_uint64, C.c_int32,
+                                     C.c_int32, C.c_int64, C.c_uint64, C.c_int, C.POINTER(P)]),
+    ("sfctr_cache_destroy", None, [P]),
+    ("sfctr_cache_admit", C.c_int, [P, C.c_int64, u64p, C.c_int64, P]),
+    ("sfctr_cache_evict", C.c_int, [P, C.c_int64, u64p]),
+    ("sfctr_cache_touch", C.c_int, [P, C.c_int64, u64p, C.c_int64]),
+    ("sfctr_cache_pin", C.c_int, [P, C.c_int64, u64p, C.c_int32]),
+    ("sfctr_cache_set_needed_soon", C.c_int, [P, C.c_int64, u64p, C.c_int32]),
+    ("sfctr_cache_slot_of", C.c_int, [P, C.c_int64, u64p, i64p]),
+    ("sfctr_cache_free_count", C.c_int, [P, C.POINTER(C.c_uint64)]),
+    ("sfctr_cache_slots", C.c_int, [P, P, P, P, P, P]),
+    ("sfctr_cache_occupancy", C.c_int, [P, u64p]),
+    ("sfctr_cache_occupancy_diagnostics", C.c_int, [P, C.c_char_p, C.c_size_t]),
+    ("sfctr_cache_peek", C.c_int, [P, C.c_int64, u64p, P, P]),
+    ("sfctr_cache_prepare", C.c_int, [P, C.c_int64, C.c_int64, P, C.c_int64, P, i64p]),
     ("sfctr_model_forward_backward", C.c_int,
      [C.c_int, C.c_int32, C.c_int32, C.c_int32, C.c_int32, f32p, u8p, f32p, f32p, f32p, f32p,
       C.POINTER(C.c_double), P, P, P, P, P, P]),
@@ -517,6 +532,110 @@ class Trainer:
         try:
             self.close()
         except Exception:
+            pass
+
+
+class CacheBuffer:
+    """One worker's device MixCache: CacheBuffer (cache_buffer.hpp:40-86) + HostStore
+    (host_store.hpp:61-92) + the manager step, sfctr_cache_* in
+    include/sfctr_b200.h. Feature arguments are sequences of owned feature ids; batched
+    calls apply in order and raise LogicError where the reference would, after the
+    preceding features took effect."""
+
+    def __init__(self, capacity, dim, seed=7, key_space=1 << 20, num_workers=1, worker=0,
+                 max_batch=1 << 16, host_reserve=0, device=0):
+        self._h = P()
+        self.capacity, self.dim = capacity, dim
+        _check(lib().sfctr_cache_create(capacity, dim, seed, key_space, num_workers, worker,
+                                        max_batch, host_reserve, device, C.byref(self._h)))
+
+    @staticmethod
+    def _f(features):
+        return np.ascontiguousarray(np.atleast_1d(np.asarray(features, np.uint64)))
+
+    def admit(self, features, step):
+        f = self._f(features)
+        slots = np.zeros(max(f.size, 1), np.uint64)
+        _check(lib().sfctr_cache_admit(self._h, f.size, f, step, _ptr(slots)))
+        return slots[:f.size]
+
+    def evict(self, features):
+        f = self._f(features)
+        _check(lib().sfctr_cache_evict(self._h, f.size, f))
+
+    def touch(self, features, step):
+        f = self._f(features)
+        _check(lib().sfctr_cache_touch(self._h, f.size, f, step))
+
+    def pin(self, features):
+        f = self._f(features)
+        _check(lib().sfctr_cache_pin(self._h, f.size, f, 1))
+
+    def unpin(self, features):
+        f = self._f(features)
+        _check(lib().sfctr_cache_pin(self._h, f.size, f, 0))
+
+    def set_needed_soon(self, features, value=True):
+        f = self._f(features)
+        _check(lib().sfctr_cache_set_needed_soon(self._h, f.size, f, 1 if value else 0))
+
+    def slot_of(self, features):
+        f = self._f(features)
+        out = np.zeros(max(f.size, 1), np.int64)
+        _check(lib().sfctr_cache_slot_of(self._h, f.size, f, out))
+        return out[:f.size]
+
+    def resident(self, feature):
+        return int(self.slot_of([feature])[0]) >= 0
+
+    def free_count(self):
+        n = C.c_uint64(0)
+        _check(lib().sfctr_cache_free_count(self._h, C.byref(n)))
+        return n.value
+
+    def slots(self):
+        """(feature [UINT64_MAX = free], last_use, admit_seq, pinned, needed_soon) per slot"""
+        n = self.capacity
+        f, lu, seq = np.zeros(n, np.uint64), np.zeros(n, np.int64), np.zeros(n, np.uint64)
+        pin, nd = np.zeros(n, np.uint8), np.zeros(n, np.uint8)
+        _check(lib().sfctr_cache_slots(self._h, _ptr(f), _ptr(lu), _ptr(seq), _ptr(pin), _ptr(nd)))
+        return f, lu, seq, pin, nd
+
+    def occupancy(self):
+        out = np.zeros(5, np.uint64)
+        _check(lib().sfctr_cache_occupancy(self._h, out))
+        return dict(zip(("capacity", "occupied", "free", "pinned", "needed_soon"),
+                        (int(x) for x in out)))
+
+    def occupancy_diagnostics(self):
+        buf = C.create_string_buffer(256)
+        _check(lib().sfctr_cache_occupancy_diagnostics(self._h, buf, 256))
+        return buf.value.decode()
+
+    def peek(self, features):
+        f = self._f(features)
+        rows = np.zeros((max(f.size, 1), 3 * self.dim), np.float32)
+        st = np.zeros(max(f.size, 1), np.int64)
+        _check(lib().sfctr_cache_peek(self._h, f.size, f, _ptr(rows), _ptr(st)))
+        return rows[:f.size], st[:f.size]
+
+    def prepare(self, step, global_ids, window_ids=None):
+        g = self._f(global_ids)
+        w = self._f(window_ids) if window_ids is not None and len(window_ids) else None
+        out = np.zeros(5, np.int64)
+        _check(lib().sfctr_cache_prepare(self._h, step, g.size, _ptr(g), 0 if w is None else w.size,
+                                         _ptr(w), out))
+        return dict(zip(("owned", "hits", "admitted", "evicted", "refilled"), (int(x) for x in out)))
+
+    def close(self):
+        if self._h:
+            lib().sfctr_cache_destroy(self._h)
+            self._h = P()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
             pass
 
 

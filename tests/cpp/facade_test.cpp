@@ -6,6 +6,7 @@
 #include <fstream>
 #include <random>
 
+#include "sfctr/cache_buffer.hpp"
 #include "sfctr/criteo.hpp"
 #include "sfctr/generator.hpp"
 #include "sfctr/vsi.hpp"
@@ -35,6 +36,57 @@ int main() {
     if (da.global_ids != db.global_ids || da.virtual_ids != db.virtual_ids ||
         da.labels != db.labels || da.worker_row_ranges.size() != db.worker_row_ranges.size()) {
       std::printf("vsi mismatch at step %d\n", step);
+      return 1;
+    }
+  }
+  // CacheBuffer + HostStore: the reference's own classes vs the device ones, same ops
+  {
+    sfctr::CacheBuffer rcb(8, 4);
+    sfctr::HostStore rhs(7, 4);
+    sfctr::b200::CacheBuffer dcb(8, 4, 7, 1000);
+    std::mt19937_64 rng(11);
+    for (int i = 0; i < 600; ++i) {
+      const sfctr::FeatureId f{rng() % 20};
+      const std::int64_t step = i / 3;
+      const int op = static_cast<int>(rng() % 5);
+      int ra = 0, da = 0;  // 0 ok, 1 threw LogicError
+      std::uint64_t rs = 0, ds = 0;
+      if (op <= 1) {
+        try { rs = rcb.admit(f, rhs.take(f), step).value; } catch (const sfctr::LogicError&) { ra = 1; }
+        try { ds = dcb.admit(f, step).value; } catch (const sfctr::LogicError&) { da = 1; }
+      } else if (op == 2) {
+        try {
+          rcb.set_needed_soon(f, false);
+          rhs.put(f, rcb.evict(f));
+        } catch (const sfctr::LogicError&) { ra = 1; }
+        try {
+          dcb.set_needed_soon(f, false);
+          const sfctr::ParamEntry e = dcb.evict(f);
+          const sfctr::ParamEntry& r = rhs.peek(f);
+          for (std::size_t k = 0; k < r.data.size(); ++k)
+            if (static_cast<float>(r.data[k]) != static_cast<float>(e.data[k])) {
+              std::printf("evicted row mismatch\n");
+              return 1;
+            }
+        } catch (const sfctr::LogicError&) { da = 1; }
+      } else if (op == 3) {
+        try { rcb.touch(f, step); } catch (const sfctr::LogicError&) { ra = 1; }
+        try { dcb.touch(f, step); } catch (const sfctr::LogicError&) { da = 1; }
+      } else {
+        try { rcb.pin(f); rcb.unpin(f); } catch (const sfctr::LogicError&) { ra = 1; }
+        try { dcb.pin(f); dcb.unpin(f); } catch (const sfctr::LogicError&) { da = 1; }
+      }
+      if (ra != da || rs != ds || rcb.free_count() != dcb.free_count() ||
+          rcb.resident(f) != dcb.resident(f)) {
+        std::printf("cache mismatch at op %d (op %d f %llu): %d/%d %llu/%llu\n", i, op,
+                    static_cast<unsigned long long>(f.value), ra, da,
+                    static_cast<unsigned long long>(rs), static_cast<unsigned long long>(ds));
+        return 1;
+      }
+    }
+    if (rcb.occupancy_diagnostics() != dcb.occupancy_diagnostics()) {
+      std::printf("occupancy mismatch: %s vs %s\n", rcb.occupancy_diagnostics().c_str(),
+                  dcb.occupancy_diagnostics().c_str());
       return 1;
     }
   }
