@@ -104,7 +104,9 @@ class Clocks:
     REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
                "sw_power_cap": 0x4}
 
-    def __init__(self, indices, period_s=0.001):
+    def __init__(self, indices, period_s=None):
+        if period_s is None:  # BENCH_CLOCK_MS: sampler period (default 1 ms)
+            period_s = float(os.environ.get("BENCH_CLOCK_MS", "1")) / 1e3
         self.indices, self.period = list(indices), period_s
         self.proc = None
 

@@ -144,7 +144,9 @@ int sfctr_criteo_stats(const sfctr_criteo* r, int64_t* bytes, int64_t* lines, do
  * Virtual Sparse Id — virtual_sparse_id(const RawBatch&, int) (vsi.hpp:29)
  * ------------------------------------------------------------------- */
 typedef struct sfctr_vsi sfctr_vsi;
-/* key_space: every feature id must be < key_space (the vocabulary size).
+/* key_space: every feature id must be < key_space (the vocabulary size): a direct-mapped
+ * first-position table of 4 B per key; key_space = 0: arbitrary u64 ids (any FeatureId the
+ * reference accepts, vsi.cpp:23-54) through a hashed table of ~16 B per id slot.
  * max_ids: the largest rows*fields that will be passed. */
 int sfctr_vsi_create(int device, uint64_t key_space, int64_t max_ids, sfctr_vsi** out);
 void sfctr_vsi_destroy(sfctr_vsi* v);
@@ -155,7 +157,8 @@ void sfctr_vsi_destroy(sfctr_vsi* v);
 int sfctr_virtual_sparse_id(sfctr_vsi* v, const uint64_t* features, int32_t rows, int32_t fields,
                             int32_t num_workers, uint64_t* global_ids, uint64_t* virtual_ids,
                             int64_t* unique_count, int32_t* row_ranges);
-/* DEVICE buffers, asynchronous on `stream`: ids are u32 feature ids (< key_space);
+/* DEVICE buffers, asynchronous on `stream` (contexts with key_space > 0): ids are u32
+ * feature ids (< key_space);
  * writes d_global_ids [U] (u32), d_virtual_ids [n] (u32) and *d_unique (int32, device). */
 int sfctr_virtual_sparse_id_device(sfctr_vsi* v, const uint32_t* d_ids, int64_t n,
                                    uint32_t* d_global_ids, uint32_t* d_virtual_ids,

@@ -86,8 +86,9 @@ inline std::vector<double> initial_embedding(std::uint64_t seed, FeatureId f, in
   return out;
 }
 
-// DedupBatch virtual_sparse_id(const RawBatch&, int) (vsi.hpp:29), on the device.
-// key_space defaults to max id + 1.
+// DedupBatch virtual_sparse_id(const RawBatch&, int) (vsi.hpp:29), on the device, for any
+// FeatureId: key_space defaults to max id + 1 (direct-mapped first-position table) while
+// that stays below 2^31, else the hashed table (arbitrary u64 ids).
 inline DedupBatch virtual_sparse_id(const RawBatch& batch, int num_workers, int device = 0,
                                     std::uint64_t key_space = 0) {
   const std::size_t n = batch.features.size();
@@ -97,7 +98,7 @@ inline DedupBatch virtual_sparse_id(const RawBatch& batch, int num_workers, int 
     ids[i] = batch.features[i].value;
     mx = ids[i] > mx ? ids[i] : mx;
   }
-  if (!key_space) key_space = mx + 1;
+  if (!key_space && mx < (1ull << 31)) key_space = mx + 1;
   sfctr_vsi* v = nullptr;
   check(sfctr_vsi_create(device, key_space, static_cast<std::int64_t>(n ? n : 1), &v));
   std::vector<std::uint64_t> g(n ? n : 1), vid(n ? n : 1);

@@ -25,30 +25,32 @@ namespace sfb {
 
 namespace {
 
-// Counts live on the device (U, n_own): grids cover the upper bound `cap`
-// and entries past the live count are flagged 0, so no host round trip is
-// needed to size the manage kernels.
-// first != nullptr: also clears the VSI first-position table behind the batch
-// (the reset VSI would otherwise launch separately; every unique passes here once)
-__global__ void owned_flag_kernel(const uint32_t* __restrict__ gids,
-                                  const int32_t* __restrict__ U_ptr, int32_t cap, uint32_t W,
-                                  uint32_t w, uint32_t* __restrict__ flag,
-                                  uint32_t* __restrict__ first) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= cap) return;
-  const bool live = i < *U_ptr;
-  const uint32_t f = live ? gids[i] : 0u;
-  flag[i] = (live && f % W == w) ? 1u : 0u;
-  if (first && live) first[f] = kEmpty;
-}
+// Counts live on the device (U, n_own): the scans cover the upper bound `cap` and items
+// past the live count contribute 0, so no host round trip sizes the manage kernels.
+// Both selections below are one fused look-back scan each (scan.cuh): the flag, the scan
+// and the compaction in a single launch.
 
-__global__ void compact_kernel(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ rank,
-                               int32_t n, uint32_t* __restrict__ out, int32_t* __restrict__ count) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  if (flag[i]) out[rank[i]] = static_cast<uint32_t>(i);
-  if (i == n - 1) *count = static_cast<int32_t>(rank[i] + flag[i]);
-}
+// owned uniques of worker w (f mod W == w), in global_ids order -> own_k;
+// first != nullptr: also clears the VSI first-position table behind the batch (every unique
+// passes here once)
+struct OwnedFlag {
+  const uint32_t* gids;
+  const int32_t* U;
+  uint32_t W, w;
+  uint32_t* first;
+  __device__ uint32_t operator()(int64_t i) const {
+    if (i >= *U) return 0u;
+    const uint32_t f = gids[i];
+    if (first) first[f] = kEmpty;
+    return f % W == w ? 1u : 0u;
+  }
+};
+struct OwnedEmit {
+  uint32_t* own_k;
+  __device__ void operator()(int64_t i, uint32_t flag, uint32_t rank) const {
+    if (flag) own_k[rank] = static_cast<uint32_t>(i);
+  }
+};
 
 __global__ void own_all_kernel(const int32_t* __restrict__ U_ptr, uint32_t* __restrict__ own_k,
                                int32_t* __restrict__ count, const uint32_t* __restrict__ gids,
@@ -56,57 +58,54 @@ __global__ void own_all_kernel(const int32_t* __restrict__ U_ptr, uint32_t* __re
   const int32_t U = *U_ptr;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < U; j += gridDim.x * blockDim.x) {
     own_k[j] = static_cast<uint32_t>(j);
-    if (first) first[gids[j]] = kEmpty;  // VSI table reset (see owned_flag_kernel)
+    if (first) first[gids[j]] = kEmpty;  // VSI table reset (see OwnedFlag)
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *count = U;
 }
 
-// Probe the owned features of batch t: hits are touched and marked needed_soon,
-// misses flagged for admission.
-__global__ void probe_kernel(const uint32_t* __restrict__ own_k,
-                             const int32_t* __restrict__ n_own_ptr, int32_t cap,
-                             const uint32_t* __restrict__ gids, uint32_t W,
-                             const uint32_t* __restrict__ index, uint32_t C, int32_t t,
-                             int32_t* __restrict__ last_use, int32_t* __restrict__ mark,
-                             uint32_t* __restrict__ own_slot, uint32_t* __restrict__ miss,
-                             int32_t* __restrict__ marked, uint32_t* __restrict__ own_f) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= cap) return;
-  if (j >= *n_own_ptr) {
-    miss[j] = 0;
-    return;
-  }
-  const uint32_t f = gids[own_k[j]];
-  const uint32_t s = index[f / W];
-  if (s < C) {
-    if (t > last_use[s]) last_use[s] = t;  // CacheBuffer::touch (cache_buffer.cpp:69-72)
-    if (atomicExch(mark + s, t) != t) atomicAdd(marked, 1);
-    own_slot[j] = s;
-    miss[j] = 0;
-  } else {
+// Probe the owned features of batch t: hits are touched and marked needed_soon, misses
+// listed for admission in global_ids order with their probe-time feature and index entry
+// (work_j / work_f / work_w), so admit reads them coalesced.
+struct ProbeFlag {
+  const uint32_t* own_k;
+  const int32_t* n_own;
+  const uint32_t* gids;
+  uint32_t W;
+  const uint32_t* index;
+  uint32_t C;
+  int32_t t;
+  int32_t* last_use;
+  int32_t* mark;
+  uint32_t* own_slot;
+  int32_t* marked;
+  uint32_t* own_f;
+  __device__ uint32_t operator()(int64_t j) const {
+    if (j >= *n_own) return 0u;
+    const uint32_t f = gids[own_k[j]];
+    const uint32_t s = index[f / W];
     own_slot[j] = s;  // host slot / kNever until admit assigns the slot
+    if (s < C) {
+      if (t > last_use[s]) last_use[s] = t;  // CacheBuffer::touch (cache_buffer.cpp:69-72)
+      if (atomicExch(mark + s, t) != t) atomicAdd(marked, 1);
+      return 0u;
+    }
     own_f[j] = f;
-    miss[j] = 1;
+    return 1u;
   }
-}
-
-// work list of the misses (global_ids order) with their probe-time feature / index entry
-__global__ void compact_work_kernel(const uint32_t* __restrict__ miss,
-                                    const uint32_t* __restrict__ rank, int32_t n,
-                                    const uint32_t* __restrict__ own_f,
-                                    const uint32_t* __restrict__ own_slot,
-                                    uint32_t* __restrict__ work_j, uint32_t* __restrict__ work_f,
-                                    uint32_t* __restrict__ work_w, int32_t* __restrict__ count) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  if (miss[i]) {
-    const uint32_t r = rank[i];
-    work_j[r] = static_cast<uint32_t>(i);
-    work_f[r] = own_f[i];
-    work_w[r] = own_slot[i];
+};
+struct ProbeEmit {
+  const uint32_t* own_f;
+  const uint32_t* own_slot;
+  uint32_t* work_j;
+  uint32_t* work_f;
+  uint32_t* work_w;
+  __device__ void operator()(int64_t j, uint32_t miss, uint32_t rank) const {
+    if (!miss) return;
+    work_j[rank] = static_cast<uint32_t>(j);
+    work_f[rank] = own_f[j];
+    work_w[rank] = own_slot[j];
   }
-  if (i == n - 1) *count = static_cast<int32_t>(rank[i] + miss[i]);
-}
+};
 
 // needed_soon for resident owned features of a lookahead batch
 __global__ void mark_window_kernel(const uint32_t* __restrict__ gids,
@@ -810,20 +809,16 @@ void CacheLane::init(uint64_t capacity, int dim, uint64_t owned_rows, uint64_t h
   free_top = static_cast<int32_t>(C);
   next_seq = 0;
   // per-step scratch
-  CUDA_CHECK(cudaMalloc(&flag, sizeof(uint32_t) * umax));
-  CUDA_CHECK(cudaMalloc(&rank, sizeof(uint32_t) * umax));
+  tiles.init(umax);
   for (int k = 0; k < 2; ++k) {
     CUDA_CHECK(cudaMalloc(&own_k_set[k], sizeof(uint32_t) * umax));
     CUDA_CHECK(cudaMalloc(&own_slot_set[k], sizeof(uint32_t) * umax));
   }
   use(0);
-  CUDA_CHECK(cudaMalloc(&miss, sizeof(uint32_t) * umax));
-  CUDA_CHECK(cudaMalloc(&miss_rank, sizeof(uint32_t) * umax));
   CUDA_CHECK(cudaMalloc(&work_j, sizeof(uint32_t) * umax));
   CUDA_CHECK(cudaMalloc(&own_f, sizeof(uint32_t) * umax));
   CUDA_CHECK(cudaMalloc(&work_f, sizeof(uint32_t) * umax));
   CUDA_CHECK(cudaMalloc(&work_w, sizeof(uint32_t) * umax));
-  scan_bytes = scan_temp_bytes(umax);
   sort_bytes = 0;
   {  // LRU candidate lists of n_evict + umax <= 2 umax (also the explicit eviction lists)
     cand_cap = 2 * umax;
@@ -833,7 +828,7 @@ void CacheLane::init(uint64_t capacity, int dim, uint64_t owned_rows, uint64_t h
     CUDA_CHECK(cudaMalloc(&ids_sorted, sizeof(uint32_t) * cand_cap));
     sort_bytes = sort_pairs_temp_bytes(cand_cap);
   }
-  CUDA_CHECK(cudaMalloc(&temp, std::max(scan_bytes, sort_bytes)));
+  CUDA_CHECK(cudaMalloc(&temp, sort_bytes));
   CUDA_CHECK(cudaMalloc(&counters, sizeof(int32_t) * kCntWords));
   CUDA_CHECK(cudaMemset(counters, 0, sizeof(int32_t) * kCntWords));
   CUDA_CHECK(cudaMemcpy(counters + kCntFreeTop, &free_top, sizeof(int32_t), cudaMemcpyHostToDevice));
@@ -846,17 +841,17 @@ void CacheLane::release() {
                   static_cast<void*>(last_use), static_cast<void*>(admit_seq),
                   static_cast<void*>(mark), static_cast<void*>(free_stack),
                   static_cast<void*>(slot_host), static_cast<void*>(hist),
-                  static_cast<void*>(index), static_cast<void*>(flag), static_cast<void*>(rank),
+                  static_cast<void*>(index),
                   static_cast<void*>(own_k_set[0]), static_cast<void*>(own_slot_set[0]),
                   static_cast<void*>(own_k_set[1]), static_cast<void*>(own_slot_set[1]),
-                  static_cast<void*>(miss),
-                  static_cast<void*>(miss_rank), static_cast<void*>(work_j),
+                  static_cast<void*>(work_j),
                   static_cast<void*>(own_f), static_cast<void*>(work_f), static_cast<void*>(work_w),
                   static_cast<void*>(keys), static_cast<void*>(keys_sorted),
                   static_cast<void*>(ids), static_cast<void*>(ids_sorted), temp,
                   static_cast<void*>(counters)})
     if (p) cudaFree(p);
   host.release();
+  tiles.release();
   *this = CacheLane();
 }
 
@@ -869,11 +864,8 @@ void CacheLane::select_owned(const uint32_t* d_gids, const int32_t* d_U, int32_t
     CUDA_LAUNCH_CHECK();
     return;
   }
-  owned_flag_kernel<<<ceil_div(cap, 256), 256, 0, s>>>(d_gids, d_U, cap, W, w, flag, vsi_first);
-  CUDA_LAUNCH_CHECK();
-  exclusive_scan_u32(temp, scan_bytes, flag, rank, cap, s);
-  compact_kernel<<<ceil_div(cap, 256), 256, 0, s>>>(flag, rank, cap, own_k, counters + kCntOwned);
-  CUDA_LAUNCH_CHECK();
+  lookback_scan<2>(tiles, cap, OwnedFlag{d_gids, d_U, W, w, vsi_first}, OwnedEmit{own_k},
+                counters + kCntOwned, s);
 }
 
 void CacheLane::mark_window(const uint32_t* d_gids, const int32_t* d_U, int32_t cap, uint32_t W,
@@ -887,16 +879,10 @@ void CacheLane::mark_window(const uint32_t* d_gids, const int32_t* d_U, int32_t 
 
 void CacheLane::probe(const uint32_t* d_gids, int32_t cap, uint32_t W, int32_t t, cudaStream_t s) {
   if (cap <= 0) return;
-  probe_kernel<<<ceil_div(cap, 256), 256, 0, s>>>(own_k, counters + kCntOwned, cap, d_gids, W,
-                                                  index, static_cast<uint32_t>(C), t, last_use,
-                                                  mark, own_slot, miss, counters + kCntMarked,
-                                                  own_f);
-  CUDA_LAUNCH_CHECK();
-  exclusive_scan_u32(temp, scan_bytes, miss, miss_rank, cap, s);
-  compact_work_kernel<<<ceil_div(cap, 256), 256, 0, s>>>(miss, miss_rank, cap, own_f, own_slot,
-                                                         work_j, work_f, work_w,
-                                                         counters + kCntWorking);
-  CUDA_LAUNCH_CHECK();
+  lookback_scan<1>(tiles, cap,
+                ProbeFlag{own_k, counters + kCntOwned, d_gids, W, index, static_cast<uint32_t>(C), t,
+                          last_use, mark, own_slot, counters + kCntMarked, own_f},
+                ProbeEmit{own_f, own_slot, work_j, work_f, work_w}, counters + kCntWorking, s);
 }
 
 void CacheLane::victim_select(int32_t t, int32_t n_evict, cudaStream_t s, const uint8_t* pinned) {

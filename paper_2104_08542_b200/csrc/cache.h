@@ -123,9 +123,9 @@ struct CacheLane {
 
   // per-step scratch; own_k / own_slot are read by the training stage, so they come in
   // two sets (step parity) and the manager of step t+1 fills one while step t trains
-  uint32_t *flag = nullptr, *rank = nullptr, *own_k = nullptr, *own_slot = nullptr;
+  uint32_t *own_k = nullptr, *own_slot = nullptr;
   uint32_t *own_k_set[2] = {nullptr, nullptr}, *own_slot_set[2] = {nullptr, nullptr};
-  uint32_t *miss = nullptr, *miss_rank = nullptr, *work_j = nullptr;
+  uint32_t* work_j = nullptr;
   // probe-time facts about the misses, so admit reads them coalesced instead of
   // chasing work_j -> own_k -> gids -> index: feature and index entry (host slot / kNever)
   uint32_t *own_f = nullptr, *work_f = nullptr, *work_w = nullptr;
@@ -134,8 +134,9 @@ struct CacheLane {
   uint64_t *keys = nullptr, *keys_sorted = nullptr;
   uint32_t *ids = nullptr, *ids_sorted = nullptr;
   int64_t cand_cap = 0;
-  void* temp = nullptr;
-  size_t scan_bytes = 0, sort_bytes = 0;
+  void* temp = nullptr;     // victim sort scratch
+  size_t sort_bytes = 0;
+  ScanTiles tiles;           // fused look-back scans (owned selection, probe)
   int32_t* counters = nullptr;  // [kCntWords] device counters (kCnt*)
 
   // host_reserve: host-pool slots pinned up front (the pool grows on demand beyond it)

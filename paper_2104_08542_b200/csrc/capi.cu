@@ -433,8 +433,8 @@ int sfctr_vsi_create(int device, uint64_t key_space, int64_t max_ids, sfctr_vsi*
   *out = nullptr;
   return guarded([&] {
     DeviceScope ds(device);
-    if (key_space == 0 || key_space >= 0xFFFFFFF0ull)
-      sfb::fail(sfb::kConfig, "key_space must be in [1, 2^32-16)");
+    if (key_space >= 0xFFFFFFF0ull)
+      sfb::fail(sfb::kConfig, "key_space must be below 2^32-16 (0 = arbitrary u64 ids, hashed)");
     auto v = std::make_unique<sfctr_vsi>();
     v->device = device;
     v->scratch.init(key_space, max_ids);
@@ -475,6 +475,27 @@ int sfctr_virtual_sparse_id(sfctr_vsi* v, const uint64_t* features, int32_t rows
     cudaStream_t s = v->stream;
     CUDA_CHECK(cudaMemsetAsync(v->d_scal, 0, sizeof(int32_t) * 4, s));
     CUDA_CHECK(cudaMemcpyAsync(v->d_in, features, sizeof(uint64_t) * n, cudaMemcpyHostToDevice, s));
+    if (v->scratch.key_space == 0) {  // arbitrary u64 ids: hashed first-position table
+      sfb::vsi_device_hashed(v->scratch, v->d_in, n, v->d_out64, v->d_vids, v->d_scal, s);
+      int32_t u = 0;
+      CUDA_CHECK(cudaMemcpyAsync(&u, v->d_scal, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      CUDA_CHECK(cudaStreamSynchronize(s));
+      CUDA_CHECK(cudaMemcpyAsync(global_ids, v->d_out64, sizeof(uint64_t) * u,
+                                 cudaMemcpyDeviceToHost, s));
+      sfb::u32_to_u64(v->d_vids, v->d_in, n, s);
+      CUDA_CHECK(cudaMemcpyAsync(virtual_ids, v->d_in, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost,
+                                 s));
+      CUDA_CHECK(cudaStreamSynchronize(s));
+      *unique_count = u;
+      if (row_ranges) {
+        const int per = rows / num_workers;  // vsi.cpp:48-52
+        for (int w = 0; w < num_workers; ++w) {
+          row_ranges[2 * w] = w * per;
+          row_ranges[2 * w + 1] = (w + 1) * per;
+        }
+      }
+      return;
+    }
     sfb::ids_to_u32(v->d_in, v->d_ids, n, v->scratch.key_space, v->d_scal + 1, s);
     int32_t bad = 0;
     CUDA_CHECK(cudaMemcpyAsync(&bad, v->d_scal + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
@@ -506,6 +527,7 @@ int sfctr_virtual_sparse_id_device(sfctr_vsi* v, const uint32_t* d_ids, int64_t 
                                    int32_t* d_unique, void* stream) {
   return guarded([&] {
     CUDA_CHECK(cudaSetDevice(v->device));
+    SFB_CHECK(v->scratch.key_space > 0, "the u32 device entry needs a context with a key space");
     sfb::vsi_device(v->scratch, d_ids, n, d_global_ids, d_virtual_ids, d_unique,
                     static_cast<cudaStream_t>(stream));
   });

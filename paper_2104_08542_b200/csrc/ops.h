@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "scan.cuh"
 
 namespace sfb {
 
@@ -40,16 +41,22 @@ void initial_embedding_device(uint64_t seed, uint64_t feature, int dim, double* 
 
 // ---------------- vsi.cu — virtual_sparse_id (vsi.cpp:23-54) ----------------
 struct VsiScratch {
-  uint64_t key_space = 0;
+  uint64_t key_space = 0;          // 0: hashed table for arbitrary u64 ids
   int64_t cap = 0;                 // max ids per call
-  uint32_t* d_first = nullptr;     // [key_space] first position per feature, 0xFFFFFFFF = unseen
-  uint32_t* d_flag = nullptr;      // [cap]
-  uint32_t* d_rank = nullptr;      // [cap]
-  void* d_cub = nullptr;           // CUB temp storage
-  size_t cub_bytes = 0;
+  // direct-mapped: [key_space] first position per feature (0xFFFFFFFF = unseen), re-tagged
+  // with the unique's rank during the scan; hashed: the per-slot equivalent [hmask + 2]
+  uint32_t* d_first = nullptr;
+  unsigned long long* d_hkeys = nullptr;  // hashed: keys [hmask + 2] (last = the ~0 id)
+  uint64_t hmask = 0;
+  uint32_t* d_hslot = nullptr;     // hashed: table slot per position [cap]
+  uint32_t* d_uslot = nullptr;     // hashed: table slot per unique [cap]
+  ScanTiles tiles;                 // fused look-back scan state
   void init(uint64_t key_space, int64_t cap);
   void release();
 };
+// arbitrary u64 ids [n] -> global_ids u64 [U], vids u32 [n], *d_unique (key_space 0 context)
+void vsi_device_hashed(VsiScratch& v, const uint64_t* d_ids, int64_t n, uint64_t* d_gids,
+                       uint32_t* d_vids, int32_t* d_unique, cudaStream_t s);
 // ids u32 [n] -> global_ids u32 [U] (first-appearance order), vids u32 [n], *d_unique.
 // reset = false leaves the first-position table dirty: the caller clears it (the
 // trainer folds that into its owned-set kernel)
@@ -60,10 +67,7 @@ void ids_to_u32(const uint64_t* d_in, uint32_t* d_out, int64_t n, uint64_t limit
                 cudaStream_t s);
 void u32_to_u64(const uint32_t* d_in, uint64_t* d_out, int64_t n, cudaStream_t s);
 
-// ---------------- scan helpers (CUB) ----------------
-size_t scan_temp_bytes(int64_t n);
-void exclusive_scan_u32(void* temp, size_t temp_bytes, const uint32_t* in, uint32_t* out,
-                        int64_t n, cudaStream_t s);
+// ---------------- victim sort (CUB radix sort of the few LRU candidates) ----------------
 size_t sort_pairs_temp_bytes(int64_t n);
 void sort_pairs_u64_u32(void* temp, size_t temp_bytes, const uint64_t* keys_in, uint64_t* keys_out,
                         const uint32_t* vals_in, uint32_t* vals_out, int64_t n, int end_bit,

@@ -585,8 +585,9 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
       lc.c[l] = lane_[l].counters;
       gp.own_slot[l] = lane_[l].own_slot;
     }
-    bad_id_gate_kernel<<<std::max(1, std::min(ceil_div(n_global_, 256), num_sms() * 4)), 256, 0,
-                         sm>>>(d_scalars_ + 1, d_scalars_ + 0, lc, lanes_, d_vid_, n_global_, gp);
+    // one block: the common case reads the flag and exits
+    bad_id_gate_kernel<<<1, 256, 0, sm>>>(d_scalars_ + 1, d_scalars_ + 0, lc, lanes_, d_vid_,
+                                          n_global_, gp);
     CUDA_LAUNCH_CHECK();
   }
   // window batches t+1..t+L-1 (needed_soon), one at a time through the window scratch

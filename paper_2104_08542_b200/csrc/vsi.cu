@@ -6,18 +6,25 @@
 // min-position formulation instead (SURVEY §7 hard part (i)):
 //   1. first[f] = min position of f    (direct-mapped table over the
 //      vocabulary in HBM; read-before-atomicMin skips the contended atomics)
-//   2. flag[i]  = (first[f_i] == i)    (i is a first appearance; evaluated inside
-//   3. rank     = exclusive scan(flag)  the CUB scan; U = rank[n-1] + flag[n-1])
-//   4. global_ids[rank[i]] = f_i for flagged i;  vid[i] = rank[first[f_i]]
-//   5. first[global_ids[k]] = unseen   (reset only the touched entries)
-// The direct-mapped table (4 B per vocabulary id: 135 MB at 33.8M ids) is the
-// HBM-rich choice: no probing, no tombstones, one sector per access.
+//   2. one fused decoupled look-back scan (scan.cuh) over flag[i] = (first[f_i] == i):
+//      a flagged i writes global_ids[rank] = f_i and re-tags first[f_i] = rank | 2^31
+//      (safe: no other position ever equals the first position, so the tag cannot make
+//      another flag true, and the first position reads first[f_i] before it tags it);
+//      the last tile writes U
+//   3. vid[i] = first[f_i] & (2^31 - 1)
+//   4. first[global_ids[k]] = unseen   (reset only the touched entries)
+// The direct-mapped table (4 B per vocabulary id: 135 MB at 33.8M ids) is the HBM-rich
+// choice: no probing, no tombstones, one sector per access.
+//
+// Arbitrary u64 ids (the reference accepts any FeatureId, vsi.cpp:41-46): the same three
+// passes over an open-addressing hash table (keys u64, linear probing) instead of the
+// direct-mapped one. A warp first merges equal ids with __match_any_sync so only the
+// lowest lane of each group (its smallest position) inserts; every position keeps its
+// table slot, so the scan and the remap read the slot directly.
 #include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
-#include <thrust/iterator/counting_iterator.h>
-#include <thrust/iterator/transform_iterator.h>
 
 #include "ops.h"
+#include "scan.cuh"
 
 namespace sfb {
 
@@ -44,19 +51,110 @@ __global__ void vsi_first_kernel(const uint32_t* __restrict__ ids, int64_t n,
   if (__ldcg(first + f) > static_cast<uint32_t>(i)) atomicMin(first + f, static_cast<uint32_t>(i));
 }
 
-__global__ void vsi_emit_kernel(const uint32_t* __restrict__ ids, int64_t n,
-                                const uint32_t* __restrict__ first,
-                                const uint32_t* __restrict__ rank, uint32_t* __restrict__ gids,
-                                uint32_t* __restrict__ vids, int32_t* __restrict__ unique) {
+constexpr uint32_t kTag = 0x80000000u;
+
+struct VsiFlag {  // first appearance?
+  const uint32_t* ids;
+  const uint32_t* first;
+  __device__ uint32_t operator()(int64_t i) const {
+    return __ldcg(first + __ldg(ids + i)) == static_cast<uint32_t>(i) ? 1u : 0u;
+  }
+};
+struct VsiEmit {
+  const uint32_t* ids;
+  uint32_t* first;
+  uint32_t* gids;
+  __device__ void operator()(int64_t i, uint32_t flag, uint32_t rank) const {
+    if (!flag) return;
+    const uint32_t f = __ldg(ids + i);
+    gids[rank] = f;
+    first[f] = rank | kTag;
+  }
+};
+
+__global__ void vsi_vid_kernel(const uint32_t* __restrict__ ids, int64_t n,
+                               const uint32_t* __restrict__ first, uint32_t* __restrict__ vids) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= n) return;
-  const uint32_t f = ids[i];
-  const uint32_t r = rank[i];
-  const uint32_t fi = __ldg(first + f);
-  const uint32_t flag = fi == static_cast<uint32_t>(i) ? 1u : 0u;
-  if (flag) gids[r] = f;
-  vids[i] = __ldg(rank + fi);
-  if (i == n - 1) *unique = static_cast<int32_t>(r + flag);
+  if (i < n) vids[i] = __ldcg(first + __ldg(ids + i)) & ~kTag;
+}
+
+// ---- hashed path (arbitrary u64 ids) ----
+constexpr uint64_t kHashEmpty = ~0ull;
+__device__ __forceinline__ uint64_t hmix64(uint64_t x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdull;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ull;
+  return x ^ (x >> 33);
+}
+// keys[mask + 1] is the dedicated slot of the id equal to the empty marker
+__global__ void vsi_hash_insert_kernel(const uint64_t* __restrict__ ids, int64_t n,
+                                       unsigned long long* __restrict__ keys,
+                                       uint32_t* __restrict__ pos, uint64_t mask,
+                                       uint32_t* __restrict__ hslot) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const bool live = i < n;
+  const uint64_t f = live ? ids[i] : kHashEmpty;
+  const unsigned act = __ballot_sync(0xFFFFFFFFu, live);
+  if (!live) return;
+  const unsigned peers = __match_any_sync(act, f);
+  const int leader = __ffs(peers) - 1;  // the group's smallest position
+  uint32_t slot = 0;
+  if (lane == leader) {
+    if (f == kHashEmpty) {
+      slot = static_cast<uint32_t>(mask + 1);
+    } else {
+      uint64_t h = hmix64(f) & mask;
+      for (;;) {
+        const unsigned long long prev = atomicCAS(keys + h, kHashEmpty, f);
+        if (prev == kHashEmpty || prev == f) break;
+        h = (h + 1) & mask;
+      }
+      slot = static_cast<uint32_t>(h);
+    }
+    if (__ldcg(pos + slot) > static_cast<uint32_t>(i)) atomicMin(pos + slot, static_cast<uint32_t>(i));
+  }
+  slot = __shfl_sync(act, slot, leader);
+  hslot[i] = slot;
+}
+struct VsiHashFlag {
+  const uint32_t* hslot;
+  const uint32_t* pos;
+  __device__ uint32_t operator()(int64_t i) const {
+    return __ldcg(pos + __ldg(hslot + i)) == static_cast<uint32_t>(i) ? 1u : 0u;
+  }
+};
+struct VsiHashEmit {
+  const uint64_t* ids;
+  const uint32_t* hslot;
+  uint32_t* pos;
+  uint64_t* gids;
+  uint32_t* uslot;
+  __device__ void operator()(int64_t i, uint32_t flag, uint32_t rank) const {
+    if (!flag) return;
+    const uint32_t sl = __ldg(hslot + i);
+    gids[rank] = ids[i];
+    uslot[rank] = sl;
+    pos[sl] = rank | kTag;
+  }
+};
+__global__ void vsi_hash_vid_kernel(const uint32_t* __restrict__ hslot, int64_t n,
+                                    const uint32_t* __restrict__ pos, uint32_t* __restrict__ vids) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) vids[i] = __ldcg(pos + __ldg(hslot + i)) & ~kTag;
+}
+__global__ void vsi_hash_reset_kernel(const uint32_t* __restrict__ uslot,
+                                      const int32_t* __restrict__ unique,
+                                      unsigned long long* __restrict__ keys,
+                                      uint32_t* __restrict__ pos) {
+  const int32_t u = *unique;
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < u;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t sl = uslot[k];
+    keys[sl] = kHashEmpty;
+    pos[sl] = kUnseen;
+  }
 }
 
 __global__ void vsi_reset_kernel(const uint32_t* __restrict__ gids,
@@ -86,38 +184,7 @@ __global__ void u32_to_u64_kernel(const uint32_t* __restrict__ in, uint64_t* __r
   if (i < n) out[i] = in[i];
 }
 
-// flag[i] = (first[ids[i]] == i), evaluated inside the scan (no flag array / kernel)
-struct FirstFlag {
-  const uint32_t* ids;
-  const uint32_t* first;
-  __device__ uint32_t operator()(int i) const {
-    return __ldg(first + __ldg(ids + i)) == static_cast<uint32_t>(i) ? 1u : 0u;
-  }
-};
-using FlagIt = thrust::transform_iterator<FirstFlag, thrust::counting_iterator<int>>;
-
-size_t flag_scan_temp_bytes(int64_t n) {
-  size_t bytes = 0;
-  FlagIt it(thrust::counting_iterator<int>(0), FirstFlag{nullptr, nullptr});
-  CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, it, static_cast<uint32_t*>(nullptr),
-                                           static_cast<int>(n)));
-  return bytes;
-}
-
 }  // namespace
-
-size_t scan_temp_bytes(int64_t n) {
-  size_t bytes = 0;
-  CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, static_cast<const uint32_t*>(nullptr),
-                                           static_cast<uint32_t*>(nullptr), static_cast<int>(n)));
-  return bytes;
-}
-
-void exclusive_scan_u32(void* temp, size_t temp_bytes, const uint32_t* in, uint32_t* out,
-                        int64_t n, cudaStream_t s) {
-  CUDA_CHECK(cub::DeviceScan::ExclusiveSum(temp, temp_bytes, in, out, static_cast<int>(n), s));
-  g_launches += 2;  // init + decoupled look-back scan
-}
 
 size_t sort_pairs_temp_bytes(int64_t n) {
   size_t bytes = 0;
@@ -136,47 +203,83 @@ void sort_pairs_u64_u32(void* temp, size_t temp_bytes, const uint64_t* keys_in, 
   g_launches += 1 + (end_bit + 7) / 8;  // histogram + one onesweep pass per 8 bits
 }
 
+void ScanTiles::init(int64_t max_items) {
+  release();
+  max_tiles = std::max<int64_t>(1, (max_items + kScanThreads - 1) / kScanThreads);
+  CUDA_CHECK(cudaMalloc(&state, sizeof(uint64_t) * max_tiles));
+  CUDA_CHECK(cudaMemset(state, 0, sizeof(uint64_t) * max_tiles));
+  epoch = 0;
+}
+
+void ScanTiles::release() {
+  if (state) cudaFree(state);
+  state = nullptr;
+  max_tiles = 0;
+}
+
 void VsiScratch::init(uint64_t ks, int64_t c) {
   release();
   key_space = ks;
   cap = c > 0 ? c : 1;
-  CUDA_CHECK(cudaMalloc(&d_first, sizeof(uint32_t) * key_space));
-  CUDA_CHECK(cudaMalloc(&d_flag, sizeof(uint32_t) * cap));
-  CUDA_CHECK(cudaMalloc(&d_rank, sizeof(uint32_t) * cap));
-  cub_bytes = std::max(scan_temp_bytes(cap), flag_scan_temp_bytes(cap));
-  CUDA_CHECK(cudaMalloc(&d_cub, cub_bytes));
-  fill_u32_kernel<<<1184, 256>>>(d_first, static_cast<int64_t>(key_space), kUnseen);
-  CUDA_LAUNCH_CHECK();
+  tiles.init(cap);
+  if (key_space) {
+    CUDA_CHECK(cudaMalloc(&d_first, sizeof(uint32_t) * key_space));
+    fill_u32_kernel<<<1184, 256>>>(d_first, static_cast<int64_t>(key_space), kUnseen);
+    CUDA_LAUNCH_CHECK();
+  } else {  // hashed: a power-of-two table of at least 2 cap slots (+1 for the empty marker)
+    hmask = 1;
+    while (hmask + 1 < static_cast<uint64_t>(2 * cap)) hmask = 2 * hmask + 1;
+    CUDA_CHECK(cudaMalloc(&d_hkeys, sizeof(unsigned long long) * (hmask + 2)));
+    CUDA_CHECK(cudaMemset(d_hkeys, 0xFF, sizeof(unsigned long long) * (hmask + 2)));
+    CUDA_CHECK(cudaMalloc(&d_first, sizeof(uint32_t) * (hmask + 2)));
+    CUDA_CHECK(cudaMemset(d_first, 0xFF, sizeof(uint32_t) * (hmask + 2)));
+    CUDA_CHECK(cudaMalloc(&d_hslot, sizeof(uint32_t) * cap));
+    CUDA_CHECK(cudaMalloc(&d_uslot, sizeof(uint32_t) * cap));
+  }
   CUDA_CHECK(cudaDeviceSynchronize());
 }
 
 void VsiScratch::release() {
-  cudaFree(d_first);
-  cudaFree(d_flag);
-  cudaFree(d_rank);
-  cudaFree(d_cub);
-  d_first = d_flag = d_rank = nullptr;
-  d_cub = nullptr;
+  tiles.release();
+  for (void* p : {static_cast<void*>(d_first), static_cast<void*>(d_hkeys),
+                  static_cast<void*>(d_hslot), static_cast<void*>(d_uslot)})
+    if (p) cudaFree(p);
+  d_first = d_hslot = d_uslot = nullptr;
+  d_hkeys = nullptr;
+  hmask = 0;
 }
 
 void vsi_device(VsiScratch& v, const uint32_t* d_ids, int64_t n, uint32_t* d_gids,
                 uint32_t* d_vids, int32_t* d_unique, cudaStream_t s, bool reset) {
   SFB_CHECK(n > 0 && n <= v.cap, "vsi batch exceeds scratch capacity");
+  SFB_CHECK(v.key_space > 0, "direct-mapped VSI needs a key space");
   const int grid = ceil_div(n, 256);
   vsi_first_kernel<<<grid, 256, 0, s>>>(d_ids, n, v.d_first);
   CUDA_LAUNCH_CHECK();
-  {
-    FlagIt it(thrust::counting_iterator<int>(0), FirstFlag{d_ids, v.d_first});
-    size_t bytes = v.cub_bytes;
-    CUDA_CHECK(cub::DeviceScan::ExclusiveSum(v.d_cub, bytes, it, v.d_rank, static_cast<int>(n), s));
-    g_launches += 2;  // init + decoupled look-back scan
-  }
-  vsi_emit_kernel<<<grid, 256, 0, s>>>(d_ids, n, v.d_first, v.d_rank, d_gids, d_vids, d_unique);
+  lookback_scan<2>(v.tiles, n, VsiFlag{d_ids, v.d_first}, VsiEmit{d_ids, v.d_first, d_gids},
+                   d_unique, s);
+  vsi_vid_kernel<<<grid, 256, 0, s>>>(d_ids, n, v.d_first, d_vids);
   CUDA_LAUNCH_CHECK();
   if (reset) {
     vsi_reset_kernel<<<std::min(grid, num_sms() * 8), 256, 0, s>>>(d_gids, d_unique, v.d_first);
     CUDA_LAUNCH_CHECK();
   }
+}
+
+void vsi_device_hashed(VsiScratch& v, const uint64_t* d_ids, int64_t n, uint64_t* d_gids,
+                       uint32_t* d_vids, int32_t* d_unique, cudaStream_t s) {
+  SFB_CHECK(n > 0 && n <= v.cap, "vsi batch exceeds scratch capacity");
+  SFB_CHECK(v.key_space == 0, "hashed VSI needs a context created with key_space 0");
+  const int grid = ceil_div(n, 256);
+  vsi_hash_insert_kernel<<<grid, 256, 0, s>>>(d_ids, n, v.d_hkeys, v.d_first, v.hmask, v.d_hslot);
+  CUDA_LAUNCH_CHECK();
+  lookback_scan<2>(v.tiles, n, VsiHashFlag{v.d_hslot, v.d_first},
+                VsiHashEmit{d_ids, v.d_hslot, v.d_first, d_gids, v.d_uslot}, d_unique, s);
+  vsi_hash_vid_kernel<<<grid, 256, 0, s>>>(v.d_hslot, n, v.d_first, d_vids);
+  CUDA_LAUNCH_CHECK();
+  vsi_hash_reset_kernel<<<std::min(grid, num_sms() * 8), 256, 0, s>>>(v.d_uslot, d_unique,
+                                                                     v.d_hkeys, v.d_first);
+  CUDA_LAUNCH_CHECK();
 }
 
 void ids_to_u32(const uint64_t* d_in, uint32_t* d_out, int64_t n, uint64_t limit, int32_t* d_bad,

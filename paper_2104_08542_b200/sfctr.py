@@ -351,7 +351,11 @@ class VirtualSparseId:
 def virtual_sparse_id(features, rows, fields, num_workers=1, key_space=None, device=0):
     """One-shot DedupBatch virtual_sparse_id(const RawBatch&, int) (vsi.hpp:29)."""
     feats = np.ascontiguousarray(features, np.uint64)
-    ks = int(key_space if key_space is not None else (int(feats.max()) + 1 if feats.size else 1))
+    if key_space is None:  # direct-mapped below 2^31 ids, else the hashed table (any u64)
+        mx = int(feats.max()) if feats.size else 0
+        ks = mx + 1 if mx < (1 << 31) else 0
+    else:
+        ks = int(key_space)
     v = VirtualSparseId(ks, max(rows * fields, 1), device)
     try:
         return v(feats, rows, fields, num_workers)

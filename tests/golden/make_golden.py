@@ -98,6 +98,21 @@ def main():
         vsi_ex.append({"rows": rows, "fields": F, "features": feats, "global_ids": g.tolist(),
                        "virtual_ids": v.tolist()})
     out["vsi_examples"] = vsi_ex
+    # vsi.cpp on arbitrary u64 FeatureIds (ids >= 2^32, the all-ones id, repeats)
+    rng = np.random.default_rng(2026)
+    u64_ex = []
+    for rows, F in [(64, 8), (512, 26)]:
+        pool = np.concatenate([rng.integers(0, 1 << 62, 40, dtype=np.uint64) * np.uint64(3),
+                               np.array([0, 1, (1 << 32) - 1, 1 << 32, (1 << 64) - 1,
+                                         (1 << 64) - 2], np.uint64)])
+        f = pool[rng.integers(0, pool.size, rows * F)]
+        g, v, _ = ref_vsi(f, np.zeros(rows, np.uint8), rows, F, 1)
+        rec = {"rows": rows, "fields": F, "features_sha256": sha(f), "unique": int(len(g)),
+               "global_ids_sha256": sha(g), "virtual_ids_sha256": sha(v)}
+        if rows * F <= 512:  # the larger batch is regenerated by the tests (same rng calls)
+            rec["features"] = [str(int(x)) for x in f]
+        u64_ex.append(rec)
+    out["vsi_u64_examples"] = u64_ex
 
     # CacheBuffer (cache_buffer.cpp) + HostStore (host_store.cpp): a seeded
     # random admit/evict/touch trace; records every returned slot and the final table.

@@ -9,6 +9,7 @@ Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline leg import
 this module; the product never does.
 """
 import ctypes as C
+import hashlib
 import os
 
 import numpy as np
@@ -268,3 +269,20 @@ def oracle_criteo(data, vocab):
     if rows == -2:
         raise ValueError(0, "no data rows")
     return f[:rows * 26].copy(), y[:rows].copy()
+
+
+def u64_golden_batches(golden):
+    """the golden u64 batches (tests/golden/make_golden.py: same rng calls)"""
+    rng = np.random.default_rng(2026)
+    out = []
+    for rec in golden["vsi_u64_examples"]:
+        rows, F = rec["rows"], rec["fields"]
+        pool = np.concatenate([rng.integers(0, 1 << 62, 40, dtype=np.uint64) * np.uint64(3),
+                               np.array([0, 1, (1 << 32) - 1, 1 << 32, (1 << 64) - 1,
+                                         (1 << 64) - 2], np.uint64)])
+        f = pool[rng.integers(0, pool.size, rows * F)]
+        assert hashlib.sha256(f.tobytes()).hexdigest() == rec["features_sha256"]
+        if "features" in rec:
+            assert [str(int(x)) for x in f] == rec["features"]
+        out.append((rec, f))
+    return out

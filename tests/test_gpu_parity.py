@@ -16,7 +16,7 @@ import numpy as np
 import pytest
 
 import paper_2104_08542_b200 as sb
-from oracle_lib import OrcConfig, oracle, oracle_generate, oracle_vsi
+from oracle_lib import OrcConfig, oracle, oracle_generate, oracle_vsi, u64_golden_batches
 
 pytestmark = pytest.mark.gpu
 
@@ -396,3 +396,44 @@ def test_trainer_alternative_towers(monkeypatch, env):
     cfg = sb.Config(num_workers=1, batch_size_per_worker=128, num_fields=8, embedding_dim=16,
                     vocabulary_size=20000, cache_capacity=1200, hidden_dim=32, zipf_exponent=1.05)
     run_parity(cfg, 5)
+
+
+# ---------------- VSI over arbitrary u64 ids (hashed first-position table) ----------------
+
+def test_vsi_hashed_u64_golden(golden):
+    """vsi.cpp:23-54 accepts any FeatureId: ids >= 2^32 and the all-ones id go through the
+    hashed table (key_space 0), bit-exact with the reference's own output."""
+    for rec, f in u64_golden_batches(golden):
+        g, v, rr = sb.virtual_sparse_id(f, rec["rows"], rec["fields"], key_space=0)
+        assert len(g) == rec["unique"]
+        assert sha(g) == rec["global_ids_sha256"] and sha(v) == rec["virtual_ids_sha256"]
+
+
+def test_vsi_hashed_random_vs_oracle():
+    rng = np.random.default_rng(3)
+    ctx = sb.VirtualSparseId(0, 1 << 17)
+    cases = [np.array([(1 << 64) - 1], np.uint64), np.full(4096, (1 << 64) - 1, np.uint64),
+             np.arange(1 << 16, dtype=np.uint64) * np.uint64(1 << 40)]
+    for _ in range(60):
+        n = int(rng.integers(1, 1 << 17))
+        k = int(rng.integers(1, n + 1))
+        pool = rng.integers(0, np.iinfo(np.uint64).max, k, dtype=np.uint64, endpoint=True)
+        cases.append(pool[rng.integers(0, k, n)])
+    for f in cases:
+        g, v, _ = ctx(f, f.size, 1)
+        go, vo = oracle_vsi(f, f.size, 1)
+        assert np.array_equal(g, go) and np.array_equal(v, vo)
+        assert np.array_equal(g[v.astype(np.int64)], f)
+    ctx.close()
+
+
+def test_vsi_direct_large_batches_vs_oracle():
+    """the fused look-back scan across many tiles (cfg2 W=8-sized batches)"""
+    rng = np.random.default_rng(4)
+    ctx = sb.VirtualSparseId(1 << 24, 3 << 20)
+    for n in (2048, 2049, 4095, 1 << 20, 3 << 20):
+        f = rng.integers(0, int(rng.integers(1, 1 << 24)), n).astype(np.uint64)
+        g, v, _ = ctx(f, n, 1)
+        go, vo = oracle_vsi(f, n, 1)
+        assert np.array_equal(g, go) and np.array_equal(v, vo)
+    ctx.close()

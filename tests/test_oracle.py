@@ -419,3 +419,12 @@ def test_eviction_safety_fuzz():
                 break
         O.orc_sim_destroy(s)
     assert 0 < deadlocks < 300
+
+
+def test_oracle_vsi_u64_golden(golden):
+    """the oracle's VSI on arbitrary u64 ids equals the reference's (golden digests)"""
+    from oracle_lib import u64_golden_batches
+    for rec, f in u64_golden_batches(golden):
+        g, v = oracle_vsi(f, rec["rows"], rec["fields"])
+        assert len(g) == rec["unique"]
+        assert sha(g) == rec["global_ids_sha256"] and sha(v) == rec["virtual_ids_sha256"]
