@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define SFCTR_B200_ABI_VERSION 1
+#define SFCTR_B200_ABI_VERSION 2
 
 typedef enum sfctr_status {
   SFCTR_OK = 0,
@@ -50,6 +50,9 @@ enum { SFCTR_SYNC_ALLREDUCE = 0, SFCTR_SYNC_ALLTOALL = 1 };
 /* RunMode (config.hpp:30): pipelined overlaps the manager stage of step t+1 with the
  * training of step t; results are identical to sequential. */
 enum { SFCTR_MODE_SEQUENTIAL = 0, SFCTR_MODE_PIPELINED = 1 };
+/* DataSource (config.hpp:33-36, config key `data`: synthetic | criteo:<path>) */
+enum { SFCTR_DATA_SYNTHETIC = 0, SFCTR_DATA_CRITEO = 1 };
+#define SFCTR_PATH_MAX 1024
 
 typedef struct sfctr_config {
   /* reference fields, config.hpp:44-71 (same defaults) */
@@ -73,6 +76,12 @@ typedef struct sfctr_config {
   uint64_t host_table_rows;      /* (host_rows) host-pool rows pinned up front per worker (the pool
                                     of evicted rows grows on demand beyond it); 0 = none */
   int32_t run_mode;              /* (mode) sequential | pipelined — RunMode, config.hpp:30 */
+  /* reference fields, config.hpp:69-71 */
+  int32_t data_source;           /* (data) synthetic | criteo:<path> */
+  char criteo_path[SFCTR_PATH_MAX];
+  /* (deterministic) 1: fixed-order gradient sums (segment sum in ascending position order
+   * per unique, no atomics): bit-identical results run to run. Slower. */
+  int32_t deterministic;
 } sfctr_config;
 
 void sfctr_config_default(sfctr_config* cfg);
@@ -139,6 +148,20 @@ int sfctr_criteo_read_batch_device(sfctr_criteo* r, int64_t step, int32_t row0, 
                                    uint64_t* d_features, uint8_t* d_labels, void* stream);
 /* bytes and lines parsed; device span of the ingest, first chunk copy to last parse (ms) */
 int sfctr_criteo_stats(const sfctr_criteo* r, int64_t* bytes, int64_t* lines, double* parse_ms);
+
+/* ---------------------------------------------------------------------
+ * Batch source — the pipeline's data loader over the configured DataSource (config key
+ * `data`, config.cpp:146-154): the SyntheticGenerator or the CriteoReader (criteo_path),
+ * same read interface (rows [row0, row0+nrows) of global batch `step`).
+ * ------------------------------------------------------------------- */
+typedef struct sfctr_batch_source sfctr_batch_source;
+int sfctr_batch_source_create(const sfctr_config* cfg, int device, sfctr_batch_source** out);
+void sfctr_batch_source_destroy(sfctr_batch_source* b);
+int sfctr_batch_source_read(sfctr_batch_source* b, int64_t step, int32_t row0, int32_t nrows,
+                            uint64_t* features, uint8_t* labels);
+int sfctr_batch_source_read_device(sfctr_batch_source* b, int64_t step, int32_t row0,
+                                   int32_t nrows, uint64_t* d_features, uint8_t* d_labels,
+                                   void* stream);
 
 /* ---------------------------------------------------------------------
  * Virtual Sparse Id — virtual_sparse_id(const RawBatch&, int) (vsi.hpp:29)

@@ -89,9 +89,22 @@ void apply_entry(sfctr_config& c, const std::string& key, const std::string& val
   else if (key == "epsilon") c.adam_epsilon = parse_double(key, value);
   else if (key == "zipf") c.zipf_exponent = parse_double(key, value);
   else if (key == "hidden") c.hidden_dim = parse_int(key, value);
-  else if (key == "data") {
-    if (value != "synthetic")
-      sfb::fail(sfb::kConfig, "config key 'data': only 'synthetic' is on the device path");
+  else if (key == "data") {  // config.cpp:146-154
+    if (value == "synthetic") {
+      c.data_source = SFCTR_DATA_SYNTHETIC;
+      c.criteo_path[0] = 0;
+    } else if (value.rfind("criteo:", 0) == 0) {
+      const std::string path = value.substr(7);
+      if (path.size() >= SFCTR_PATH_MAX) sfb::fail(sfb::kConfig, "config key 'data': path too long");
+      c.data_source = SFCTR_DATA_CRITEO;
+      std::memcpy(c.criteo_path, path.c_str(), path.size() + 1);
+    } else {
+      sfb::fail(sfb::kConfig, "config key 'data': expected 'synthetic' or 'criteo:<path>'");
+    }
+  } else if (key == "deterministic") {
+    if (value == "1" || value == "true") c.deterministic = 1;
+    else if (value == "0" || value == "false") c.deterministic = 0;
+    else sfb::fail(sfb::kConfig, "config key 'deterministic': expected 0 or 1");
   } else if (key == "sync") {
     if (value == "allreduce") c.sync_mode = SFCTR_SYNC_ALLREDUCE;
     else if (value == "alltoall") c.sync_mode = SFCTR_SYNC_ALLTOALL;
@@ -154,6 +167,11 @@ struct sfctr_trainer {
   std::unique_ptr<sfb::Trainer> t;
 };
 
+struct sfctr_batch_source {  // the configured DataSource behind one read interface
+  sfctr_generator* gen = nullptr;
+  sfctr_criteo* criteo = nullptr;
+};
+
 struct sfctr_cache {
   std::unique_ptr<sfb::DeviceCache> c;
 };
@@ -184,6 +202,9 @@ void sfctr_config_default(sfctr_config* c) {  // config.hpp:44-71
   c->sync_mode = SFCTR_SYNC_ALLREDUCE;
   c->host_table_rows = 0;
   c->run_mode = SFCTR_MODE_SEQUENTIAL;
+  c->data_source = SFCTR_DATA_SYNTHETIC;
+  c->criteo_path[0] = 0;
+  c->deterministic = 0;
 }
 
 int sfctr_config_validate(const sfctr_config* c) {
@@ -426,6 +447,41 @@ int sfctr_initial_embedding(uint64_t seed, uint64_t feature, int32_t dim, int de
     CUDA_CHECK(cudaMemcpy(out, d, sizeof(double) * dim, cudaMemcpyDeviceToHost));
     cudaFree(d);
   });
+}
+
+// ---------------- batch source (config key `data`) ----------------
+int sfctr_batch_source_create(const sfctr_config* cfg, int device, sfctr_batch_source** out) {
+  *out = nullptr;
+  return guarded([&] {
+    sfb::validate_config(*cfg);
+    auto b = std::make_unique<sfctr_batch_source>();
+    int st = 0;
+    if (cfg->data_source == SFCTR_DATA_CRITEO)
+      st = sfctr_criteo_open(cfg->criteo_path, cfg, device, &b->criteo);
+    else
+      st = sfctr_generator_create(cfg, device, &b->gen);
+    if (st) sfb::fail(st, g_err);
+    *out = b.release();
+  });
+}
+void sfctr_batch_source_destroy(sfctr_batch_source* b) {
+  if (!b) return;
+  if (b->gen) sfctr_generator_destroy(b->gen);
+  if (b->criteo) sfctr_criteo_destroy(b->criteo);
+  delete b;
+}
+int sfctr_batch_source_read(sfctr_batch_source* b, int64_t step, int32_t row0, int32_t nrows,
+                            uint64_t* features, uint8_t* labels) {
+  return b->criteo ? sfctr_criteo_read_batch(b->criteo, step, row0, nrows, features, labels)
+                   : sfctr_generator_generate(b->gen, step, row0, nrows, features, labels);
+}
+int sfctr_batch_source_read_device(sfctr_batch_source* b, int64_t step, int32_t row0,
+                                   int32_t nrows, uint64_t* d_features, uint8_t* d_labels,
+                                   void* stream) {
+  return b->criteo ? sfctr_criteo_read_batch_device(b->criteo, step, row0, nrows, d_features,
+                                                    d_labels, stream)
+                   : sfctr_generator_generate_device(b->gen, step, row0, nrows, d_features,
+                                                     d_labels, stream);
 }
 
 // ---------------- VSI ----------------

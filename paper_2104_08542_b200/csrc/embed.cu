@@ -2,6 +2,8 @@
 // the backward scatter-add are HBM-bound byte movers, so every kernel moves
 // 128-bit vectors with consecutive threads on consecutive 16 B of one
 // embedding row (d=80 -> 20 lanes cover a 320 B row; rows are 16 B aligned).
+#include <cub/device/device_radix_sort.cuh>
+
 #include "kernels.h"
 
 namespace sfb {
@@ -379,6 +381,98 @@ void segment_sum(const uint32_t* vid, int32_t n, int F, int d, int ldx, const fl
     SFB_CHECK(!Bsum, "segment_sum: deferred FM term needs d % 4 == 0");
     segment_sum_s<<<ceil_div(m, 256), 256, 0, s>>>(vid, n, F, d, ldx, dX, G, fm_s, gz, scale, dG);
   }
+  CUDA_LAUNCH_CHECK();
+}
+
+namespace {
+__global__ void iota_u32_kernel(uint32_t* p, int32_t n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = static_cast<uint32_t>(i);
+}
+struct SegStartFlag {
+  const uint32_t* v;
+  __device__ uint32_t operator()(int64_t i) const { return i == 0 || v[i] != v[i - 1] ? 1u : 0u; }
+};
+struct SegStartEmit {
+  uint32_t* starts;
+  __device__ void operator()(int64_t i, uint32_t flag, uint32_t rank) const {
+    if (flag) starts[rank] = static_cast<uint32_t>(i);
+  }
+};
+// one warp per segment (unique row v), positions in ascending order, columns over lanes
+__global__ void segment_sum_csr_kernel(const uint32_t* __restrict__ vid_sorted,
+                                       const uint32_t* __restrict__ pos_sorted,
+                                       const uint32_t* __restrict__ starts,
+                                       const int32_t* __restrict__ count, int32_t n, int F, int d,
+                                       int ldx, const float* __restrict__ dX,
+                                       const float* __restrict__ G, const float* __restrict__ fm_s,
+                                       const float* __restrict__ gz, float scale,
+                                       float* __restrict__ dG) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nseg = *count;
+  const int64_t wstride = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t sg = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; sg < nseg;
+       sg += wstride) {
+    const uint32_t q0 = starts[sg];
+    const uint32_t q1 = sg + 1 < nseg ? starts[sg + 1] : static_cast<uint32_t>(n);
+    const int64_t v = vid_sorted[q0];
+    for (int c0 = 0; c0 < d; c0 += 32) {
+      const int c = c0 + lane;
+      if (c >= d) break;
+      const float gv = G[v * d + c];
+      float acc = 0.f;
+      for (uint32_t q = q0; q < q1; ++q) {
+        const uint32_t p = pos_sorted[q];
+        const uint32_t r = p / static_cast<uint32_t>(F), f = p - r * static_cast<uint32_t>(F);
+        acc += dX[static_cast<int64_t>(r) * ldx + static_cast<int64_t>(f) * d + c] +
+               scale * gz[r] * (fm_s[static_cast<int64_t>(r) * d + c] - gv);
+      }
+      dG[v * d + c] += acc;
+    }
+  }
+}
+}  // namespace
+
+void SegCsr::init(int64_t n) {
+  release();
+  cap = std::max<int64_t>(n, 1);
+  CUDA_CHECK(cudaMalloc(&pos_in, sizeof(uint32_t) * cap));
+  CUDA_CHECK(cudaMalloc(&vid_out, sizeof(uint32_t) * cap));
+  CUDA_CHECK(cudaMalloc(&pos_out, sizeof(uint32_t) * cap));
+  CUDA_CHECK(cudaMalloc(&starts, sizeof(uint32_t) * (cap + 1)));
+  CUDA_CHECK(cudaMalloc(&count, sizeof(int32_t)));
+  CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, static_cast<const uint32_t*>(nullptr),
+                                             static_cast<uint32_t*>(nullptr),
+                                             static_cast<const uint32_t*>(nullptr),
+                                             static_cast<uint32_t*>(nullptr), static_cast<int>(cap)));
+  CUDA_CHECK(cudaMalloc(&temp, temp_bytes));
+  tiles.init(cap);
+}
+
+void SegCsr::release() {
+  for (void* p : {static_cast<void*>(pos_in), static_cast<void*>(vid_out),
+                  static_cast<void*>(pos_out), static_cast<void*>(starts),
+                  static_cast<void*>(count), temp})
+    if (p) cudaFree(p);
+  tiles.release();
+  *this = SegCsr();
+}
+
+void segment_sum_csr(SegCsr& cs, const uint32_t* vid, int32_t n, int F, int d, int ldx,
+                     const float* dX, const float* G, const float* fm_s, const float* gz,
+                     float scale, float* dG, int vid_bits, cudaStream_t s) {
+  if (n <= 0) return;
+  SFB_CHECK(n <= cs.cap, "segment_sum_csr: batch exceeds scratch");
+  iota_u32_kernel<<<ceil_div(n, 256), 256, 0, s>>>(cs.pos_in, n);
+  CUDA_LAUNCH_CHECK();
+  size_t tb = cs.temp_bytes;
+  // LSD radix sort is stable: each unique's positions stay in ascending order
+  CUDA_CHECK(cub::DeviceRadixSort::SortPairs(cs.temp, tb, vid, cs.vid_out, cs.pos_in, cs.pos_out, n,
+                                             0, std::max(1, std::min(32, vid_bits)), s));
+  g_launches += 1 + (vid_bits + 7) / 8;
+  lookback_scan<8>(cs.tiles, n, SegStartFlag{cs.vid_out}, SegStartEmit{cs.starts}, cs.count, s);
+  segment_sum_csr_kernel<<<num_sms() * 8, 256, 0, s>>>(cs.vid_out, cs.pos_out, cs.starts, cs.count,
+                                                       n, F, d, ldx, dX, G, fm_s, gz, scale, dG);
   CUDA_LAUNCH_CHECK();
 }
 

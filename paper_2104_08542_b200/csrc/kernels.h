@@ -33,6 +33,23 @@ void fm_sums(const float* X, int32_t rows, int F, int d, int ldx, float* fm_s, f
 void segment_sum(const uint32_t* vid, int32_t n, int F, int d, int ldx, const float* dX,
                  const float* G, const float* fm_s, const float* gz, float scale, float* dG,
                  cudaStream_t s, float* Bsum = nullptr);
+// Deterministic segment sum (config key deterministic): the lane's positions are sorted
+// stably by vid, then one warp per unique sums its positions' gradients in ascending
+// position order and adds the sum to dG[v] (no atomics: lanes run in stream order), so
+// every run of the same inputs produces bit-identical gradients.
+struct SegCsr {
+  int64_t cap = 0;
+  uint32_t *pos_in = nullptr, *vid_out = nullptr, *pos_out = nullptr, *starts = nullptr;
+  int32_t* count = nullptr;
+  void* temp = nullptr;
+  size_t temp_bytes = 0;
+  ScanTiles tiles;
+  void init(int64_t n);
+  void release();
+};
+void segment_sum_csr(SegCsr& cs, const uint32_t* vid, int32_t n, int F, int d, int ldx,
+                     const float* dX, const float* G, const float* fm_s, const float* gz,
+                     float scale, float* dG, int vid_bits, cudaStream_t s);
 // dX[r, k] += scale * gz[r] * (fm_s[r, k % d] - X[r, k]) (FM part, standalone model op)
 void fm_grad_add(const float* X, int32_t rows, int F, int d, int ldx, const float* fm_s,
                  const float* gz, float scale, float* dX, cudaStream_t s);

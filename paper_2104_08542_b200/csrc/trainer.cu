@@ -67,6 +67,13 @@ void validate_config(const sfctr_config& c) {  // config.cpp:55-78 + device limi
           "sync must be allreduce or alltoall");
   require(c.run_mode == SFCTR_MODE_SEQUENTIAL || c.run_mode == SFCTR_MODE_PIPELINED,
           "mode must be pipelined or sequential");
+  if (c.data_source == SFCTR_DATA_CRITEO) {  // config.cpp:74-77
+    require(c.criteo_path[0] != 0, "criteo data source needs a file path");
+    require(c.num_fields == 26, "criteo format has 26 categorical fields; set fields=26");
+  } else {
+    require(c.data_source == SFCTR_DATA_SYNTHETIC, "data must be synthetic or criteo:<path>");
+  }
+  require(c.deterministic == 0 || c.deterministic == 1, "deterministic must be 0 or 1");
 }
 
 Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nccl_id, int device)
@@ -209,7 +216,9 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
   // fused gather/GEMM/scatter tower (SFCTR_TOWER_FUSED=1): X / dX never touch HBM,
   // but on B200 the streamed path below is faster today (profiles/), so it is opt-in
   const char* tf = std::getenv("SFCTR_TOWER_FUSED");
-  tower_fused_ = !tower_simt_ && tower_fused_supported(d_) && tf && tf[0] == '1';
+  det_ = cfg_.deterministic != 0;
+  tower_fused_ = !tower_simt_ && !det_ && tower_fused_supported(d_) && tf && tf[0] == '1';
+  if (det_) csr_.init(static_cast<int64_t>(b_) * F_);
 
   const uint64_t owned_rows = (cfg_.vocabulary_size + W_ - 1) / W_;
   lane_.resize(lanes_);
@@ -244,6 +253,7 @@ Trainer::~Trainer() {
   if (mstream_) cudaStreamSynchronize(mstream_);
   if (stream_) cudaStreamSynchronize(stream_);
   for (auto& l : lane_) l.release();
+  csr_.release();
   tower_.release();
   towertc_.release();
   xch_.release();
@@ -790,7 +800,7 @@ void Trainer::train(int64_t step, const uint8_t* d_labels, float* d_loss) {
   // same G row as emb[slot]): the scatter pass then does not re-gather G per position
   // (the owner-routed exchange over peer stores defers it too: the push to the owner and the
   // owner's reduction add it per local row, see FmDefer in exchange.cu)
-  const bool defer_fm = (zero_in_gather || (xdev && d_ % 4 == 0)) && !tower_fused_;
+  const bool defer_fm = (zero_in_gather || (xdev && d_ % 4 == 0)) && !tower_fused_ && !det_;
   // ... and the segment sum then runs inside the tower's dX GEMM epilogue (dX never hits HBM)
   const bool fuse_scatter = defer_fm && !tower_simt_ && H_ <= 64 && dx_scatter_fits(F_, d_);
   // ... and the forward reads the cache rows in place (own_k is the identity at W = 1, so
@@ -882,7 +892,13 @@ void Trainer::train(int64_t step, const uint8_t* d_labels, float* d_loss) {
                                            this},
                                 fuse_scatter ? &sc : nullptr);
     phase(tower_simt_ ? "tower" : "tower_reduce", s);
-    if (!fuse_scatter) {
+    if (det_) {  // fixed-order (CSR) segment sum: bit-identical run to run
+      int bits = 1;
+      while (bits < 32 && (1ll << bits) < n_global_) ++bits;
+      segment_sum_csr(csr_, vid, b_ * F_, F_, d_, ldx_, d_dX_, d_G_, d_fm_s_, tower_.gz, emb_scale,
+                      d_dG_, bits, s);
+      phase("segment_sum", s);
+    } else if (!fuse_scatter) {
       segment_sum(vid, b_ * F_, F_, d_, ldx_, d_dX_, d_G_, d_fm_s_, tower_.gz, emb_scale, d_dG_, s,
                   defer_fm ? d_B_ : nullptr);
       phase("segment_sum", s);

@@ -177,6 +177,8 @@ class Trainer {
   int32_t* h_totals_ = nullptr;   // pinned [16] exchange plan totals
   int ldx_ = 0;
   bool tower_simt_ = false;
+  bool det_ = false;              // deterministic: fixed-order segment sums (segment_sum_csr)
+  SegCsr csr_;
   bool tower_fused_ = false;
   bool w1_split_ready_ = false;  // towertc_ holds the tf32 parts of the current W1
   int64_t dense_steps_ = 0;

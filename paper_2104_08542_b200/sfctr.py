@@ -80,6 +80,9 @@ class Config(C.Structure):
         ("sync_mode", C.c_int32),
         ("host_table_rows", C.c_uint64),
         ("run_mode", C.c_int32),
+        ("data_source", C.c_int32),
+        ("criteo_path", C.c_char * 1024),
+        ("deterministic", C.c_int32),
     ]
 
     def __init__(self, **kw):
@@ -146,6 +149,10 @@ SIGNATURES = [
     ("sfctr_generator_generate_device", C.c_int, [P, C.c_int64, C.c_int32, C.c_int32, P, P, P]),
     ("sfctr_generator_shard_start", C.c_uint64, [P, C.c_int32]),
     ("sfctr_initial_embedding", C.c_int, [C.c_uint64, C.c_uint64, C.c_int32, C.c_int, f64p]),
+    ("sfctr_batch_source_create", C.c_int, [P, C.c_int, C.POINTER(P)]),
+    ("sfctr_batch_source_destroy", None, [P]),
+    ("sfctr_batch_source_read", C.c_int, [P, C.c_int64, C.c_int32, C.c_int32, u64p, u8p]),
+    ("sfctr_batch_source_read_device", C.c_int, [P, C.c_int64, C.c_int32, C.c_int32, P, P, P]),
     ("sfctr_vsi_create", C.c_int, [C.c_int, C.c_uint64, C.c_int64, C.POINTER(P)]),
     ("sfctr_vsi_destroy", None, [P]),
     ("sfctr_virtual_sparse_id", C.c_int,
@@ -310,6 +317,39 @@ class SyntheticGenerator:
 
 
 # ---------------- VSI ----------------
+
+class BatchSource:
+    """The configured DataSource (config key `data`, config.cpp:146-154): the synthetic
+    generator or the Criteo TSV at criteo_path, one read interface."""
+
+    def __init__(self, config: Config, device: int = 0):
+        self._h = P()
+        self.fields = config.num_fields
+        self.global_rows = config.num_workers * config.batch_size_per_worker
+        _check(lib().sfctr_batch_source_create(C.byref(config), device, C.byref(self._h)))
+
+    def read(self, step, row0=0, nrows=None):
+        n = self.global_rows if nrows is None else nrows
+        f = np.zeros(n * self.fields, np.uint64)
+        y = np.zeros(n, np.uint8)
+        _check(lib().sfctr_batch_source_read(self._h, step, row0, n, f, y))
+        return f, y
+
+    def read_device(self, step, row0, nrows, d_features, d_labels, stream=None):
+        _check(lib().sfctr_batch_source_read_device(self._h, step, row0, nrows, d_features,
+                                                    d_labels, stream))
+
+    def close(self):
+        if self._h:
+            lib().sfctr_batch_source_destroy(self._h)
+            self._h = P()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
 
 class VirtualSparseId:
     """Device context for virtual_sparse_id (vsi.hpp:29)."""

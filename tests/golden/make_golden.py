@@ -163,7 +163,9 @@ def main():
     out["config_checks"] = [[k, v, R.ref_config_check(k.encode(), v.encode(), 1)]
                             for k, v in [("workers", "8"), ("workers", "0"), ("dim", "-3"),
                                          ("zipf", "abc"), ("bogus", "1"), ("vocab", "33800000"),
-                                         ("beta1", "1.0"), ("lookahead", "2")]]
+                                         ("beta1", "1.0"), ("lookahead", "2"),
+                                         ("data", "synthetic"), ("data", "criteo:/tmp/day_0.tsv"),
+                                         ("data", "criteo:"), ("data", "parquet:/x")]]
 
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(out, fh, indent=1)

@@ -22,6 +22,8 @@ def main():
     ap.add_argument("--sync", default="allreduce")
     ap.add_argument("--steps", type=int, default=6)
     ap.add_argument("--mode", default="sequential")
+    ap.add_argument("--deterministic", action="store_true")
+    ap.add_argument("--dump", default="", help="rank 0 saves the merged final state (npz)")
     args = ap.parse_args()
     import torch
     import torch.distributed as td
@@ -37,6 +39,8 @@ def main():
                     zipf_exponent=1.05)
     cfg.apply("sync", args.sync)
     cfg.apply("mode", args.mode)
+    if args.deterministic:
+        cfg.apply("deterministic", "1")
     nid = dist.nccl_id_for(D, sb.nccl_unique_id)
     tr = sb.Trainer(cfg, rank=D.rank, world=W, nccl_id=nid, device=D.local_rank)
     gen = sb.SyntheticGenerator(cfg, device=D.local_rank)
@@ -94,6 +98,9 @@ def main():
         df = np.concatenate([g[2] for g in gathered])[order]
         dr = np.concatenate([g[3] for g in gathered])[order]
         ds = np.concatenate([g[4] for g in gathered])[order]
+        if args.dump:
+            np.savez(args.dump, features=df, rows=dr, steps=ds,
+                     losses=np.array([g[1] for g in gathered]))
         n_orc = O.orc_sim_snapshot(sim, None, None, None)
         of = np.zeros(n_orc, np.uint64)
         orows = np.zeros((n_orc, 3 * cfg.embedding_dim))

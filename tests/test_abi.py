@@ -10,6 +10,7 @@ import pytest
 
 import paper_2104_08542_b200 as sb
 from paper_2104_08542_b200 import sfctr
+from oracle_lib import ref, ref_available
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HEADER = os.path.join(ROOT, "include", "sfctr_b200.h")
@@ -32,7 +33,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_abi_version():
-    assert sfctr.lib().sfctr_abi_version() == 1
+    assert sfctr.lib().sfctr_abi_version() == 2
 
 
 def test_config_defaults_match_reference():
@@ -89,3 +90,42 @@ def test_no_silent_cpu_fallback():
         sb.SyntheticGenerator(cfg)
     with pytest.raises(sb.CudaError):
         sb.initial_embedding(7, 0, 4)
+
+
+def test_data_source_config_key():
+    """config key `data` (config.cpp:146-154) and its validation (config.cpp:74-77), with the
+    reference's messages; `deterministic` is a B200 key."""
+    c = sb.Config()
+    c.apply("data", "criteo:/data/day_0.tsv")
+    assert c.data_source == 1 and c.criteo_path == b"/data/day_0.tsv"
+    c.validate()
+    c.apply("fields", "25")
+    with pytest.raises(sb.ConfigError, match="criteo format has 26 categorical fields; set fields=26"):
+        c.validate()
+    c.apply("data", "synthetic")
+    assert c.data_source == 0 and c.criteo_path == b""
+    c.validate()
+    with pytest.raises(sb.ConfigError, match="expected 'synthetic' or 'criteo:<path>'"):
+        sb.Config().apply("data", "parquet:/x")
+    c = sb.Config()
+    c.apply("data", "criteo:")
+    with pytest.raises(sb.ConfigError, match="criteo data source needs a file path"):
+        c.validate()
+    c = sb.Config()
+    c.apply("deterministic", "1")
+    assert c.deterministic == 1
+    with pytest.raises(sb.ConfigError):
+        c.apply("deterministic", "maybe")
+
+
+@pytest.mark.skipif(not ref_available(), reason="oracle/_ref not built")
+def test_data_source_messages_match_reference():
+    R = ref()
+    for key, value in (("data", "parquet:/x"), ("data", "criteo:")):
+        assert R.ref_config_check(key.encode(), value.encode(), 1) == 1
+        want = R.ref_last_error().decode()
+        c = sb.Config()
+        with pytest.raises(sb.ConfigError) as e:
+            c.apply(key, value)
+            c.validate()
+        assert str(e.value) == want, (str(e.value), want)

@@ -185,3 +185,34 @@ def test_device_entry_points_exported():
               "sfctr_criteo_token_hash", "sfctr_criteo_destroy"):
         assert hasattr(lib, n)
     assert os.path.exists(os.path.join(os.path.dirname(sb.__file__), "libsfctr_b200.so"))
+
+
+@pytest.mark.gpu
+def test_batch_source_data_key(tmp_path):
+    """config key data=criteo:<path> feeds the trainer through the batch source (the
+    reference's pipeline data loader); data=synthetic is the generator, bit for bit."""
+    data = make_criteo_tsv(3000, seed=4)
+    p = tmp_path / "day.tsv"
+    p.write_bytes(data)
+    cfg = sb.Config(num_workers=2, batch_size_per_worker=256, num_fields=26, embedding_dim=8,
+                    vocabulary_size=50000, cache_capacity=20000, hidden_dim=16)
+    cfg.apply("data", f"criteo:{p}")
+    src = sb.BatchSource(cfg)
+    rd = sb.CriteoReader(str(p), cfg)
+    for step in (0, 5, 11):
+        f1, y1 = src.read(step)
+        f2, y2 = rd.read_batch(step)
+        assert np.array_equal(f1, f2) and np.array_equal(y1, y2)
+    tr = sb.Trainer(cfg)
+    for step in range(3):
+        loss = tr.step(step, *src.read(step))
+        assert np.isfinite(loss)
+    tr.close()
+    src.close()
+    cfg.apply("data", "synthetic")
+    src = sb.BatchSource(cfg)
+    gen = sb.SyntheticGenerator(cfg)
+    f1, y1 = src.read(3, 256, 256)
+    f2, y2 = gen.generate(3, 256, 256)
+    assert np.array_equal(f1, f2) and np.array_equal(y1, y2)
+    src.close()

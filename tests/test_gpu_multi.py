@@ -14,6 +14,7 @@ import socket
 import subprocess
 import sys
 
+import numpy as np
 import pytest
 
 import paper_2104_08542_b200 as sb
@@ -83,3 +84,24 @@ def test_two_rank_parity_fallback_transports(env):
     print(out.stdout[-3000:], out.stderr[-3000:])
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
     assert "parity ok" in out.stdout
+
+
+@pytest.mark.skipif(sb.device_count() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("sync", ["allreduce", "alltoall"])
+def test_multi_rank_deterministic(sync, tmp_path):
+    """deterministic=1 across ranks: two launches of the same in-flight run give
+    bit-identical final rows, moments, step counts and losses (fixed-order segment sums,
+    fixed source order in the owner reduction, NCCL's fixed reduction order)."""
+    n = min(sb.device_count(), 4)
+    dumps = []
+    for k in range(2):
+        dump = str(tmp_path / f"run{k}.npz")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", "--master-port",
+               str(_port()), os.path.join(ROOT, "tests", "mp_overlap_worker.py"), "--sync", sync,
+               "--mode", "pipelined", "--deterministic", "--dump", dump]
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+        assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+        dumps.append(np.load(dump))
+    for key in ("features", "rows", "steps", "losses"):
+        assert np.array_equal(dumps[0][key], dumps[1][key]), key

@@ -437,3 +437,35 @@ def test_vsi_direct_large_batches_vs_oracle():
         go, vo = oracle_vsi(f, n, 1)
         assert np.array_equal(g, go) and np.array_equal(v, vo)
     ctx.close()
+
+
+# ---------------- deterministic mode (fixed-order gradient sums) ----------------
+
+@pytest.mark.parametrize("mode", ["sequential", "pipelined"])
+def test_deterministic_runs_are_bit_identical(mode):
+    """deterministic=1: the segment sum adds each unique's positions in ascending order (no
+    atomics), so two runs of the same batches give bit-identical losses, rows, moments,
+    step counts and dense parameters; and it stays within the oracle's
+    parity bars. Two in-process lanes (the lanes' sums are added in lane order) and LRU
+    evictions included."""
+    cfg = sb.Config(num_workers=2, batch_size_per_worker=512, num_fields=12, embedding_dim=16,
+                    vocabulary_size=200_000, cache_capacity=4500, hidden_dim=32,
+                    zipf_exponent=1.05)
+    cfg.apply("deterministic", "1")
+    cfg.apply("mode", mode)
+    gen = sb.SyntheticGenerator(cfg)
+    batches = [gen.generate(t) for t in range(8)]
+    runs = []
+    for _ in range(2):
+        tr = sb.Trainer(cfg)
+        losses = [tr.step(t, *batches[t]) for t in range(8)]
+        runs.append((losses, tr.snapshot(), tr.dense_state()))
+        assert tr.ledger()["swap_events"] > 0
+        tr.close()
+    (l1, s1, d1), (l2, s2, d2) = runs
+    assert l1 == l2
+    for a, b in zip(s1, s2):
+        assert np.array_equal(a, b)
+    for a, b in zip(d1[:3], d2[:3]):
+        assert np.array_equal(a, b)
+    run_parity(cfg, 6)
