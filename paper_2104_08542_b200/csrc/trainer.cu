@@ -628,7 +628,10 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
   const int64_t bound = lane_[0].umax;
   const bool xdev = a2a_ && xch_.device_driven();
   bool free_step = (world_ == 1 || xdev) && !no_free_steps_;
-  for (int l = 0; l < lanes_ && free_step; ++l) free_step = free_lb_[l] >= bound;
+  // A lane whose cache holds its whole owned shard (C >= owned rows) can never run out of
+  // slots: every admission is a non-resident owned row, so no step needs the host check
+  for (int l = 0; l < lanes_ && free_step; ++l)
+    free_step = lane_[l].C >= lane_[l].rows || free_lb_[l] >= bound;
   if (a2a_) {  // exchange plan (touched masks, send/receive positions), device only
     struct HookCtx {
       Trainer* tr;
