@@ -119,7 +119,8 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc, const float* X, int ld
                                float* dX, float emb_scale, float* grads, bool accumulate,
                                cudaStream_t s,
                                bool w1_split_ready = false, const PhaseHook& hook = {},
-                               const DxScatter* scatter = nullptr);
+                               const DxScatter* scatter = nullptr,
+                               const PhaseHook& after_dx = {});  // called once GEMM2 is queued
 // whether the fused dX scatter (tc_dx.cuh) fits: d % 4 == 0 and its smem tables
 bool dx_scatter_fits(int F, int d);
 // Fused path (tc_fused.cuh): X = G[vid] is gathered straight into the GEMM

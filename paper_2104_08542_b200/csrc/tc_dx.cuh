@@ -53,6 +53,7 @@ struct DxParams {
   float* dG;            // [rows x d] gradient table (red.add)
   float* Bsum;          // [rows] deferred FM coefficients (red.add)
   int F, d;
+  int exp;              // experiment: 1 = no global reductions, 2 = no FM-sum loads
 };
 
 // smem for the scatter epilogue: value tile [128 x 68] f32, vid [128 x F] u32, gz [128]
@@ -70,7 +71,10 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
 
 // SCATTER runs kDxScatterWarps epilogue warps (several per TMEM lane quarter): the scatter is bound by how
 // many red.global.add instructions are in flight per SM
-constexpr int kDxScatterWarps = 16;  // 4 per TMEM lane quarter
+#ifndef SFB_DX_EW
+#define SFB_DX_EW 16
+#endif
+constexpr int kDxScatterWarps = SFB_DX_EW;  // 4 per TMEM lane quarter
 template <bool SCATTER>
 constexpr int dx_threads() { return SCATTER ? 64 + 32 * kDxScatterWarps : 192; }
 
@@ -84,8 +88,7 @@ __global__ void __launch_bounds__(dx_threads<SCATTER>(), 1)
   using L = DxLayout;
   constexpr int BS = L::B_STAGES;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* smem = smem_1024(smem_raw);
   uint8_t* a_s = smem;
   uint8_t* b_s = smem + L::A_BYTES;
   uint8_t* out_s = b_s + BS * L::B_STAGE;  // TMA-store staging, or the scatter tables
@@ -252,7 +255,7 @@ __global__ void __launch_bounds__(dx_threads<SCATTER>(), 1)
       for (int u8 = 0; u8 < NB; ++u8) {
         const int rr = 2 * EW * u8 + 2 * ew + (lane >> 4);
         ok[u8] = r0 + rr < p.M && col < p.N;
-        fm[u8] = ok[u8] ? __ldg(reinterpret_cast<const float4*>(
+        fm[u8] = ok[u8] && p.exp != 2 ? __ldg(reinterpret_cast<const float4*>(
                               p.fm_s + static_cast<int64_t>(r0 + rr) * d + cc))
                         : make_float4(0.f, 0.f, 0.f, 0.f);
       }
@@ -285,6 +288,7 @@ __global__ void __launch_bounds__(dx_threads<SCATTER>(), 1)
         const float k = p.scale * g;
         const uint32_t u = vid_s[rr * F + f];
         float* dstg = p.dG + static_cast<int64_t>(u) * d + cc;
+        if (p.exp == 1) continue;
         asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dstg),
                      "f"(p.scale * a.x + k * fm[u8].x), "f"(p.scale * a.y + k * fm[u8].y),
                      "f"(p.scale * a.z + k * fm[u8].z), "f"(p.scale * a.w + k * fm[u8].w));

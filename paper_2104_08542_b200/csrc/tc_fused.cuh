@@ -85,8 +85,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   using L = Layout<BN>;
   constexpr int ST = L::STAGES;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* smem = smem_1024(smem_raw);
   uint64_t* fullB = reinterpret_cast<uint64_t*>(smem + ST * L::STAGE_BYTES);
   uint64_t* readyA = fullB + ST;
   uint64_t* empty = readyA + ST;
@@ -269,8 +268,7 @@ __global__ void __launch_bounds__(192, 1)
   using L = Layout<BN, 2>;
   constexpr int ST = L::STAGES;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* smem = smem_1024(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * L::STAGE_BYTES);
   uint64_t* empty = full + ST;
   uint64_t* tmem_full = empty + ST;
@@ -438,8 +436,7 @@ __global__ void __launch_bounds__(192, 1)
   using L = Layout<BN>;
   constexpr int ST = L::STAGES;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* smem = smem_1024(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * L::STAGE_BYTES);
   uint64_t* ready = full + ST;
   uint64_t* empty = ready + ST;

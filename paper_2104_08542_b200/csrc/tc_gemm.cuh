@@ -23,6 +23,16 @@
 namespace sfb {
 namespace tc {
 
+// The dynamic shared memory rounded up to 1024 B (SWIZZLE_128B operands need it) by pointer
+// arithmetic on the shared array itself: an integer round trip through uintptr_t loses the
+// address space, and every access through the result becomes a generic LD.E / ST.E instead
+// of LDS / STS.
+__device__ __forceinline__ uint8_t* smem_1024(uint8_t* raw) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(raw));
+  return raw + ((1024u - (a & 1023u)) & 1023u);
+}
+
+
 constexpr int BM = 128;
 constexpr int BKE = 32;                  // K elements per block (128 B)
 constexpr int A_BYTES = BM * BKE * 4;    // 16 KB
@@ -224,8 +234,7 @@ __global__ void __launch_bounds__(192, 1)
   using L = Layout<BN, MAXST>;
   constexpr int ST = L::STAGES;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* smem = smem_1024(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * L::STAGE_BYTES);
   uint64_t* ready = full + ST;
   uint64_t* empty = ready + ST;
@@ -449,8 +458,7 @@ __global__ void __launch_bounds__(192, 1)
   using L = DecLayout<BN>;
   constexpr int RS = kRawStages, OS = kOpStages;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* smem = smem_1024(smem_raw);
   uint8_t* raw = smem;
   uint8_t* ops = smem + L::RAW_BYTES;
   uint64_t* raw_full = reinterpret_cast<uint64_t*>(ops + OS * L::OP_BYTES);

@@ -256,7 +256,11 @@ void launch_dx_gemm(const TowerTC& tc_, const float* dh_hi, const float* dh_lo, 
   p.n_tiles = (K + 63) / 64;
   p.tiles = ((rows + 127) / 128) * p.n_tiles;
   p.scale = scale;
-  const int grid = std::min(p.tiles, sm_count());
+  static const int dx_grid = [] {  // experiment switch: SFCTR_DX_GRID (CTAs of GEMM2)
+    const char* e = std::getenv("SFCTR_DX_GRID");
+    return e ? std::max(1, atoi(e)) : 0;
+  }();
+  const int grid = std::min(p.tiles, dx_grid ? dx_grid : sm_count());
   if (sc) {
     p.vid = sc->vid;
     p.remap = sc->remap;
@@ -266,6 +270,11 @@ void launch_dx_gemm(const TowerTC& tc_, const float* dh_hi, const float* dh_lo, 
     p.Bsum = sc->Bsum;
     p.F = sc->F;
     p.d = sc->d;
+    static const int dx_exp = [] {
+      const char* e = std::getenv("SFCTR_DX_EXP");
+      return e ? atoi(e) : 0;
+    }();
+    p.exp = dx_exp;
     auto kern = tc::gemm_dx_persistent_kernel<true>;
     const int smem = 1024 + tc::DxLayout::A_BYTES + tc::DxLayout::B_STAGES * tc::DxLayout::B_STAGE +
                      ((tc::dx_scatter_bytes(p.F, p.d) + 15) & ~15) + 256;
@@ -529,7 +538,7 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc_, const float* X, int l
                                float* dX, float emb_scale, float* grads, bool accumulate,
                                cudaStream_t s, bool w1_split_ready,
                                const PhaseHook& hook,
-                               const DxScatter* scatter) {
+                               const DxScatter* scatter, const PhaseHook& after_dx) {
   const int K = F * d, H = t.H;
   SFB_CHECK(rows <= t.rows_cap && rows <= tc_.rows_cap && K == tc_.K && ldx == tc_.ldk,
             "tower buffers too small");
@@ -609,6 +618,7 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc_, const float* X, int l
                                                        p, s);
   }
   hook("tower_gemm2");
+  after_dx("dx");  // the caller may start what needs only dX / the scattered gradients
   // ---- GEMM3: dW1 partials = X^T dh (A = X MN-major, B = dh hi/lo MN-major)
   const int nkb3 = (rows + tc::BKE - 1) / tc::BKE;
   const int mt3 = (K + 127) / 128;

@@ -84,8 +84,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
   constexpr int RA = kTsARing, RB = kTsBRing, TS = kTsStages;
   constexpr int BN = 64;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* smem = smem_1024(smem_raw);
   uint8_t* a_ring = smem;
   uint8_t* b_ring = smem + RA * L::A_RAW;
   uint64_t* a_full = reinterpret_cast<uint64_t*>(b_ring + RB * L::B_STAGE);

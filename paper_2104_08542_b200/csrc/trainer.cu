@@ -107,6 +107,11 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
   CUDA_CHECK(cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking,
                                           pipelined_ ? prio_hi : prio_lo));
   if (const char* e = std::getenv("SFCTR_NO_FREE_STEPS")) no_free_steps_ = e[0] == '1';
+  if (const char* e = std::getenv("SFCTR_NO_UPDATE_FORK")) no_update_fork_ = e[0] == '1';
+  CUDA_CHECK(cudaStreamCreateWithPriority(&ustream_, cudaStreamNonBlocking,
+                                          pipelined_ ? prio_hi : prio_lo));
+  CUDA_CHECK(cudaEventCreateWithFlags(&dx_done_, cudaEventDisableTiming));
+  CUDA_CHECK(cudaEventCreateWithFlags(&upd_done_, cudaEventDisableTiming));
   CUDA_CHECK(cudaMalloc(&d_err_, sizeof(int32_t) * 4));
   CUDA_CHECK(cudaMemset(d_err_, 0, sizeof(int32_t) * 4));
   mstream_ = stream_;
@@ -296,6 +301,12 @@ Trainer::~Trainer() {
   for (cudaEvent_t e : {dense_ready_, dense_done_})
     if (e) cudaEventDestroy(e);
   if (dstream_) cudaStreamDestroy(dstream_);
+  if (ustream_) {
+    cudaStreamSynchronize(ustream_);
+    cudaStreamDestroy(ustream_);
+  }
+  for (cudaEvent_t e : {dx_done_, upd_done_})
+    if (e) cudaEventDestroy(e);
   if (mcomm_ && mcomm_ != comm_) ncclCommDestroy(mcomm_);
   if (comm_) ncclCommDestroy(comm_);
   if (mstream_ && mstream_ != stream_) cudaStreamDestroy(mstream_);
@@ -784,6 +795,8 @@ void Trainer::train(int64_t step, const uint8_t* d_labels, float* d_loss) {
   const bool free_step = prep_.free_step, xdev = prep_.xdev;
   const int32_t U = prep_.U;
   const std::vector<int32_t> n_own = prep_.n_own;
+  prep_n_own0_ = n_own[0];
+  prep_k_ = k;
   int32_t* snap = d_snap_[k];
   auto snap_cnt = [&](int l) { return snap + 1 + kCntWords * l; };
   prep_.step = -1;
@@ -862,6 +875,31 @@ void Trainer::train(int64_t step, const uint8_t* d_labels, float* d_loss) {
   else
     CUDA_CHECK(cudaMemsetAsync(d_dG_, 0, sizeof(float) * table_rows * d_, s));
   const float emb_scale = 1.f / static_cast<float>(W_);
+  // Row update overlapped with dW1: once the dX GEMM has scattered every embedding gradient
+  // (fused scatter, one lane), the row update only needs those gradients, so it runs on
+  // ustream_ while GEMM3 and its reduction run here; the tail waits for it.
+  const bool fork_update = fuse_scatter && !timing_ && !no_update_fork_ && lanes_ == 1 &&
+                           !tower_fused_ && !tower_simt_ && (world_ == 1 || xdev);
+  if (fork_update) ensure_bias_tables(steps_done_ + 2);  // may synchronise: before the fork
+  struct ForkCtx {
+    Trainer* tr;
+    cudaStream_t s;
+    int k;
+    bool defer_fm;
+    float scale;
+  } fork_ctx{this, s, k, defer_fm, emb_scale};
+  const PhaseHook after_dx =
+      fork_update ? PhaseHook{[](void* c, const char*) {
+                                auto* f = static_cast<ForkCtx*>(c);
+                                Trainer* t = f->tr;
+                                CUDA_CHECK(cudaEventRecord(t->dx_done_, f->s));
+                                CUDA_CHECK(cudaStreamWaitEvent(t->ustream_, t->dx_done_));
+                                t->launch_row_update(t->ustream_, f->k, t->a2a_, f->defer_fm,
+                                                     f->scale, t->d_dG_);
+                                CUDA_CHECK(cudaEventRecord(t->upd_done_, t->ustream_));
+                              },
+                              &fork_ctx}
+                  : PhaseHook{};
   for (int l = 0; l < lanes_; ++l) {
     const uint32_t* vid = a2a_ && !remap_local
                               ? d_lvid_
@@ -893,7 +931,7 @@ void Trainer::train(int64_t step, const uint8_t* d_labels, float* d_loss) {
                                              static_cast<Trainer*>(c)->phase(n);
                                            },
                                            this},
-                                fuse_scatter ? &sc : nullptr);
+                                fuse_scatter ? &sc : nullptr, after_dx);
     phase(tower_simt_ ? "tower" : "tower_reduce", s);
     if (det_) {  // fixed-order (CSR) segment sum: bit-identical run to run
       int bits = 1;
@@ -922,7 +960,9 @@ void Trainer::train(int64_t step, const uint8_t* d_labels, float* d_loss) {
   }
   const float* grad_rows = d_dG_;
   bool fused_adam = false;  // owner reduction + sparse Adam fused (owner-routed, peer stores)
-  if (a2a_) {
+  if (fork_update) {
+    // the row update is on ustream_ (push + barrier + owner reduction + Adam at W > 1)
+  } else if (a2a_) {
     const bool xfm = xdev && defer_fm;
     if (xdev)
       xch_.backward_send_dev(d_dG_, s, xfm ? d_G_ : nullptr, xfm ? d_B_ : nullptr, emb_scale);
@@ -951,7 +991,9 @@ void Trainer::train(int64_t step, const uint8_t* d_labels, float* d_loss) {
 
   // ---- update_sparse (l.14) + dense Adam
   ensure_bias_tables(steps_done_ + 2);
-  if (fused_adam) {
+  if (fork_update) {
+    CUDA_CHECK(cudaStreamWaitEvent(s, upd_done_));
+  } else if (fused_adam) {
     const bool xfm = defer_fm;
     Exchange::AdamRows ar{lane_[0].emb, lane_[0].mom, lane_[0].vel, lane_[0].own_slot,
                           lane_[0].steps, d_bc1_, d_bc2_,
@@ -963,7 +1005,7 @@ void Trainer::train(int64_t step, const uint8_t* d_labels, float* d_loss) {
     xch_.backward_reduce_adam_dev(lane_[0].own_k, n_own[0], snap_cnt(0) + kCntOwned, d_dG_, s,
                                   xfm ? d_B_ : nullptr, emb_scale, ar);
   }
-  for (int l = 0; l < lanes_ && !fused_adam; ++l)
+  for (int l = 0; l < lanes_ && !fused_adam && !fork_update; ++l)
     sparse_adam(a2a_ ? nullptr : lane_[l].own_k, lane_[l].own_slot, n_own[l],
                 snap_cnt(l) + kCntOwned, grad_rows, d_,
                 lane_[l].emb,
@@ -1047,6 +1089,36 @@ void Trainer::train(int64_t step, const uint8_t* d_labels, float* d_loss) {
   stats_.total_nvlink_bytes += stats_.nvlink_bytes;
   stats_.total_kernel_launches += stats_.kernel_launches;
   stats_.total_pinned_waits += stats_.pinned_waits;
+}
+
+// The row update of one lane (W = 1: sparse Adam over the scattered gradients; owner-routed
+// peer stores: push the partial gradient rows to their owners, flag barrier, fused owner
+// reduction + Adam) on stream us.
+void Trainer::launch_row_update(cudaStream_t us, int k, bool a2a, bool defer_fm, float emb_scale,
+                                const float* grad_rows) {
+  (void)k;
+  const int32_t n_bound = prep_n_own0_;
+  const int32_t* n_own_dev = d_snap_[prep_k_] + 1 + kCntOwned;
+  if (a2a) {
+    xch_.backward_send_dev(d_dG_, us, defer_fm ? d_G_ : nullptr, defer_fm ? d_B_ : nullptr,
+                           emb_scale);
+    xch_.barrier(comm_, us);
+    Exchange::AdamRows ar{lane_[0].emb, lane_[0].mom, lane_[0].vel, lane_[0].own_slot,
+                          lane_[0].steps, d_bc1_, d_bc2_,
+                          static_cast<float>(cfg_.learning_rate),
+                          static_cast<float>(cfg_.adam_beta1), static_cast<float>(cfg_.adam_beta2),
+                          static_cast<float>(1.0 - cfg_.adam_beta1),
+                          static_cast<float>(1.0 - cfg_.adam_beta2),
+                          static_cast<float>(cfg_.adam_epsilon)};
+    xch_.backward_reduce_adam_dev(lane_[0].own_k, n_bound, n_own_dev, d_dG_, us,
+                                  defer_fm ? d_B_ : nullptr, emb_scale, ar);
+    return;
+  }
+  sparse_adam(lane_[0].own_k, lane_[0].own_slot, n_bound, n_own_dev, grad_rows, d_, lane_[0].emb,
+              lane_[0].mom, lane_[0].vel, lane_[0].steps, d_bc1_, d_bc2_,
+              static_cast<float>(cfg_.learning_rate), static_cast<float>(cfg_.adam_beta1),
+              static_cast<float>(cfg_.adam_beta2), static_cast<float>(cfg_.adam_epsilon), us,
+              /*inc_steps=*/false, defer_fm ? d_B_ : nullptr, emb_scale);
 }
 
 void Trainer::step_device(int64_t step, const uint64_t* d_features, const uint8_t* d_labels,

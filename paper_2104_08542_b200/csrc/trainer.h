@@ -113,6 +113,16 @@ class Trainer {
   ncclComm_t mcomm_ = nullptr;       // manager-stage communicator (id all-gather)
   IdGather idg_;                     // NVLink peer-store id all-gather (world > 1)
   cudaStream_t dstream_ = nullptr;   // dense-gradient all-reduce, overlapping the row exchange
+  // sparse update stream: once the dX GEMM has scattered the embedding gradients, the row
+  // update (sparse Adam, or at W > 1 the gradient push + owner reduction + Adam) runs here
+  // while the training stream computes dW1 (GEMM3) and its reduction
+  cudaStream_t ustream_ = nullptr;
+  cudaEvent_t dx_done_ = nullptr, upd_done_ = nullptr;
+  void launch_row_update(cudaStream_t us, int k, bool a2a, bool defer_fm, float emb_scale,
+                         const float* grad_rows);
+  bool no_update_fork_ = false;  // SFCTR_NO_UPDATE_FORK=1: the update stays on the training stream
+  int32_t prep_n_own0_ = 0;      // the training step's owned-count bound and parity set
+  int prep_k_ = 0;
   cudaEvent_t dense_ready_ = nullptr, dense_done_ = nullptr;
   cudaEvent_t prep_done_[2] = {}, train_done_[2] = {};
   bool prep_recorded_[2] = {false, false};
