@@ -865,7 +865,7 @@ void CacheLane::select_owned(const uint32_t* d_gids, const int32_t* d_U, int32_t
     return;
   }
   lookback_scan<2>(tiles, cap, OwnedFlag{d_gids, d_U, W, w, vsi_first}, OwnedEmit{own_k},
-                counters + kCntOwned, s);
+                   counters + kCntOwned, s, d_U);
 }
 
 void CacheLane::mark_window(const uint32_t* d_gids, const int32_t* d_U, int32_t cap, uint32_t W,
@@ -882,7 +882,8 @@ void CacheLane::probe(const uint32_t* d_gids, int32_t cap, uint32_t W, int32_t t
   lookback_scan<1>(tiles, cap,
                 ProbeFlag{own_k, counters + kCntOwned, d_gids, W, index, static_cast<uint32_t>(C), t,
                           last_use, mark, own_slot, counters + kCntMarked, own_f},
-                ProbeEmit{own_f, own_slot, work_j, work_f, work_w}, counters + kCntWorking, s);
+                ProbeEmit{own_f, own_slot, work_j, work_f, work_w}, counters + kCntWorking, s,
+                counters + kCntOwned);
 }
 
 void CacheLane::victim_select(int32_t t, int32_t n_evict, cudaStream_t s, const uint8_t* pinned) {

@@ -47,11 +47,14 @@ struct VsiScratch {
   // with the unique's rank during the scan; hashed: the per-slot equivalent [hmask + 2]
   uint32_t* d_first = nullptr;
   unsigned long long* d_hkeys = nullptr;  // hashed: keys [hmask + 2] (last = the ~0 id)
+  uint32_t* d_hkeys32 = nullptr;          // hashed32: u32 keys [hmask + 2]
+  bool hashed32 = false;  // u32 ids through an L2-resident hashed table (no vocab-sized table)
   uint64_t hmask = 0;
   uint32_t* d_hslot = nullptr;     // hashed: table slot per position [cap]
   uint32_t* d_uslot = nullptr;     // hashed: table slot per unique [cap]
   ScanTiles tiles;                 // fused look-back scan state
-  void init(uint64_t key_space, int64_t cap);
+  // hash32: u32 ids below key_space through the hashed table (always reset behind a batch)
+  void init(uint64_t key_space, int64_t cap, bool hash32 = false);
   void release();
 };
 // arbitrary u64 ids [n] -> global_ids u64 [U], vids u32 [n], *d_unique (key_space 0 context)

@@ -52,13 +52,22 @@ __global__ void __launch_bounds__(kScanThreads) lookback_scan_kernel(int64_t n, 
                                                                      EmitFn emit,
                                                                      uint64_t* __restrict__ state,
                                                                      uint32_t epoch,
-                                                                     int32_t* __restrict__ total) {
+                                                                     int32_t* __restrict__ total,
+                                                                     const int32_t* __restrict__ live) {
   __shared__ uint32_t warp_sum[kScanThreads / 32];
   __shared__ uint32_t tile_prefix;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   constexpr int64_t kScanTile = kScanThreads * kScanItems;
   const int64_t tile = blockIdx.x;
   const int64_t base = tile * kScanTile;
+  // live (device count, nullable): items [live, n) are empty; tiles past the last live one
+  // exit at once (no successor reads their state) and the last live tile writes the total
+  if (live) {
+    const int64_t nl = min(n, static_cast<int64_t>(max(0, *live)));
+    if (base >= nl && tile > 0) return;
+    n = nl;
+  }
+  const int64_t last_tile = n > 0 ? (n - 1) / kScanTile : 0;
   uint32_t v[kScanItems], ex[kScanItems];
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
@@ -129,13 +138,14 @@ __global__ void __launch_bounds__(kScanThreads) lookback_scan_kernel(int64_t n, 
     const int64_t i = base + k * kScanThreads + tid;
     if (i < n) emit(i, v[k], pfx + ex[k]);
   }
-  if (total && tile == gridDim.x - 1 && tid == 0) *total = static_cast<int32_t>(pfx + run);
+  if (total && tile == last_tile && tid == 0) *total = static_cast<int32_t>(pfx + run);
 }
 
-// launches the fused scan over n items (n >= 1) on stream s, kItems items per thread
+// launches the fused scan over n items (n >= 1) on stream s, kItems items per thread;
+// live (nullable): a device count <= n of the items that exist (the grid covers n)
 template <int kItems = kScanItemsMax, typename ValueFn, typename EmitFn>
 void lookback_scan(ScanTiles& st, int64_t n, ValueFn value, EmitFn emit, int32_t* total,
-                   cudaStream_t s) {
+                   cudaStream_t s, const int32_t* live = nullptr) {
   static_assert(kItems >= 1 && kItems <= kScanItemsMax, "items per thread");
   const int64_t tiles = (n + kScanThreads * kItems - 1) / (kScanThreads * kItems);
   SFB_CHECK(tiles <= st.max_tiles, "scan larger than its tile state");
@@ -144,7 +154,7 @@ void lookback_scan(ScanTiles& st, int64_t n, ValueFn value, EmitFn emit, int32_t
     st.epoch = 1;
   }
   lookback_scan_kernel<kItems><<<static_cast<int>(tiles), kScanThreads, 0, s>>>(
-      n, value, emit, st.state, st.epoch, total);
+      n, value, emit, st.state, st.epoch, total, live);
   CUDA_LAUNCH_CHECK();
 }
 #endif

@@ -36,6 +36,9 @@ __global__ void dense_init_kernel(float* p, int64_t n, uint64_t stream_seed, dou
 }
 }  // namespace
 
+// default VSI table: the hashed one (L2-resident at every shipped size)
+bool vsi_hash_default() { return true; }
+
 void validate_config(const sfctr_config& c) {  // config.cpp:55-78 + device limits
   auto require = [](bool ok, const char* msg) {
     if (!ok) fail(kConfig, msg);
@@ -139,7 +142,13 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
     CUDA_CHECK(cudaEventCreateWithFlags(&dense_done_, cudaEventDisableTiming));
   }
 
-  vsi_.init(cfg_.vocabulary_size, n_global_);
+  // VSI first-position table: hashed (2 x the global batch, L2-resident) or direct-mapped
+  // over the vocabulary (SFCTR_VSI_HASH=0|1 overrides the default)
+  {
+    bool hash = vsi_hash_default();
+    if (const char* e = std::getenv("SFCTR_VSI_HASH")) hash = e[0] == '1';
+    vsi_.init(cfg_.vocabulary_size, n_global_, hash);
+  }
   if (lanes_ > 8) fail(kConfig, "at most 8 worker lanes per process");
   for (int k = 0; k < 2; ++k) {  // per-step-parity sets (see trainer.h)
     CUDA_CHECK(cudaMalloc(&d_in_feat_set_[k], sizeof(uint64_t) * n_local_));
@@ -597,7 +606,7 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
     CUDA_CHECK(cudaMemsetAsync(lane_[l].counters + 3, 0, sizeof(int32_t) * 2, sm));
     CUDA_CHECK(cudaMemsetAsync(lane_[l].counters + kCntOld, 0, sizeof(int32_t), sm));
     lane_[l].select_owned(d_uniq_, d_scalars_ + 0, cap, Wu, static_cast<uint32_t>(lane0_ + l),
-                          l == 0 ? vsi_.d_first : nullptr, sm);
+                          l == 0 && !vsi_.hashed32 ? vsi_.d_first : nullptr, sm);
   }
   {
     LaneCounters lc{};

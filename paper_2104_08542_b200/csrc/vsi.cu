@@ -78,8 +78,14 @@ __global__ void vsi_vid_kernel(const uint32_t* __restrict__ ids, int64_t n,
   if (i < n) vids[i] = __ldcg(first + __ldg(ids + i)) & ~kTag;
 }
 
-// ---- hashed path (arbitrary u64 ids) ----
-constexpr uint64_t kHashEmpty = ~0ull;
+// ---- hashed path (arbitrary u64 ids, or u32 ids with an L2-resident table) ----
+// KeyT = unsigned long long (any FeatureId) or uint32_t (device ids below the vocabulary: a
+// table of 2 x cap slots fits in L2, where the direct-mapped table over the vocabulary does
+// not, so its random accesses are L2 hits instead of DRAM sectors)
+template <typename KeyT>
+__device__ __forceinline__ KeyT hash_empty() {
+  return static_cast<KeyT>(~0ull);
+}
 __device__ __forceinline__ uint64_t hmix64(uint64_t x) {
   x ^= x >> 33;
   x *= 0xff51afd7ed558ccdull;
@@ -88,27 +94,31 @@ __device__ __forceinline__ uint64_t hmix64(uint64_t x) {
   return x ^ (x >> 33);
 }
 // keys[mask + 1] is the dedicated slot of the id equal to the empty marker
-__global__ void vsi_hash_insert_kernel(const uint64_t* __restrict__ ids, int64_t n,
-                                       unsigned long long* __restrict__ keys,
-                                       uint32_t* __restrict__ pos, uint64_t mask,
-                                       uint32_t* __restrict__ hslot) {
+template <typename KeyT, typename IdT>
+__global__ void vsi_hash_insert_kernel(const IdT* __restrict__ ids, int64_t n,
+                                       KeyT* __restrict__ keys, uint32_t* __restrict__ pos,
+                                       uint64_t mask, uint32_t* __restrict__ hslot) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const bool live = i < n;
-  const uint64_t f = live ? ids[i] : kHashEmpty;
+  const KeyT f = live ? static_cast<KeyT>(ids[i]) : hash_empty<KeyT>();
   const unsigned act = __ballot_sync(0xFFFFFFFFu, live);
   if (!live) return;
   const unsigned peers = __match_any_sync(act, f);
   const int leader = __ffs(peers) - 1;  // the group's smallest position
   uint32_t slot = 0;
   if (lane == leader) {
-    if (f == kHashEmpty) {
+    if (f == hash_empty<KeyT>()) {
       slot = static_cast<uint32_t>(mask + 1);
     } else {
-      uint64_t h = hmix64(f) & mask;
+      uint64_t h = hmix64(static_cast<uint64_t>(f)) & mask;
       for (;;) {
-        const unsigned long long prev = atomicCAS(keys + h, kHashEmpty, f);
-        if (prev == kHashEmpty || prev == f) break;
+        const KeyT cur = __ldcg(keys + h);  // read first: repeated ids skip the CAS
+        if (cur == f) break;
+        if (cur == hash_empty<KeyT>()) {
+          const KeyT prev = atomicCAS(keys + h, hash_empty<KeyT>(), f);
+          if (prev == hash_empty<KeyT>() || prev == f) break;
+        }
         h = (h + 1) & mask;
       }
       slot = static_cast<uint32_t>(h);
@@ -125,11 +135,12 @@ struct VsiHashFlag {
     return __ldcg(pos + __ldg(hslot + i)) == static_cast<uint32_t>(i) ? 1u : 0u;
   }
 };
+template <typename IdT>
 struct VsiHashEmit {
-  const uint64_t* ids;
+  const IdT* ids;
   const uint32_t* hslot;
   uint32_t* pos;
-  uint64_t* gids;
+  IdT* gids;
   uint32_t* uslot;
   __device__ void operator()(int64_t i, uint32_t flag, uint32_t rank) const {
     if (!flag) return;
@@ -144,15 +155,15 @@ __global__ void vsi_hash_vid_kernel(const uint32_t* __restrict__ hslot, int64_t 
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i < n) vids[i] = __ldcg(pos + __ldg(hslot + i)) & ~kTag;
 }
+template <typename KeyT>
 __global__ void vsi_hash_reset_kernel(const uint32_t* __restrict__ uslot,
-                                      const int32_t* __restrict__ unique,
-                                      unsigned long long* __restrict__ keys,
+                                      const int32_t* __restrict__ unique, KeyT* __restrict__ keys,
                                       uint32_t* __restrict__ pos) {
   const int32_t u = *unique;
   for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < u;
        k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const uint32_t sl = uslot[k];
-    keys[sl] = kHashEmpty;
+    keys[sl] = hash_empty<KeyT>();
     pos[sl] = kUnseen;
   }
 }
@@ -217,12 +228,22 @@ void ScanTiles::release() {
   max_tiles = 0;
 }
 
-void VsiScratch::init(uint64_t ks, int64_t c) {
+void VsiScratch::init(uint64_t ks, int64_t c, bool hash32) {
   release();
   key_space = ks;
   cap = c > 0 ? c : 1;
+  hashed32 = hash32 && ks > 0;
   tiles.init(cap);
-  if (key_space) {
+  if (hashed32) {  // u32 keys in a table of at least 2 cap slots (+1 for the empty marker)
+    hmask = 1;
+    while (hmask + 1 < static_cast<uint64_t>(2 * cap)) hmask = 2 * hmask + 1;
+    CUDA_CHECK(cudaMalloc(&d_hkeys32, sizeof(uint32_t) * (hmask + 2)));
+    CUDA_CHECK(cudaMemset(d_hkeys32, 0xFF, sizeof(uint32_t) * (hmask + 2)));
+    CUDA_CHECK(cudaMalloc(&d_first, sizeof(uint32_t) * (hmask + 2)));
+    CUDA_CHECK(cudaMemset(d_first, 0xFF, sizeof(uint32_t) * (hmask + 2)));
+    CUDA_CHECK(cudaMalloc(&d_hslot, sizeof(uint32_t) * cap));
+    CUDA_CHECK(cudaMalloc(&d_uslot, sizeof(uint32_t) * cap));
+  } else if (key_space) {
     CUDA_CHECK(cudaMalloc(&d_first, sizeof(uint32_t) * key_space));
     fill_u32_kernel<<<1184, 256>>>(d_first, static_cast<int64_t>(key_space), kUnseen);
     CUDA_LAUNCH_CHECK();
@@ -242,11 +263,13 @@ void VsiScratch::init(uint64_t ks, int64_t c) {
 void VsiScratch::release() {
   tiles.release();
   for (void* p : {static_cast<void*>(d_first), static_cast<void*>(d_hkeys),
-                  static_cast<void*>(d_hslot), static_cast<void*>(d_uslot)})
+                  static_cast<void*>(d_hkeys32), static_cast<void*>(d_hslot),
+                  static_cast<void*>(d_uslot)})
     if (p) cudaFree(p);
-  d_first = d_hslot = d_uslot = nullptr;
+  d_first = d_hslot = d_uslot = d_hkeys32 = nullptr;
   d_hkeys = nullptr;
   hmask = 0;
+  hashed32 = false;
 }
 
 void vsi_device(VsiScratch& v, const uint32_t* d_ids, int64_t n, uint32_t* d_gids,
@@ -254,6 +277,20 @@ void vsi_device(VsiScratch& v, const uint32_t* d_ids, int64_t n, uint32_t* d_gid
   SFB_CHECK(n > 0 && n <= v.cap, "vsi batch exceeds scratch capacity");
   SFB_CHECK(v.key_space > 0, "direct-mapped VSI needs a key space");
   const int grid = ceil_div(n, 256);
+  if (v.hashed32) {  // L2-resident hashed table; always reset behind the batch
+    vsi_hash_insert_kernel<uint32_t, uint32_t><<<grid, 256, 0, s>>>(d_ids, n, v.d_hkeys32,
+                                                                    v.d_first, v.hmask, v.d_hslot);
+    CUDA_LAUNCH_CHECK();
+    lookback_scan<2>(v.tiles, n, VsiHashFlag{v.d_hslot, v.d_first},
+                     VsiHashEmit<uint32_t>{d_ids, v.d_hslot, v.d_first, d_gids, v.d_uslot},
+                     d_unique, s);
+    vsi_hash_vid_kernel<<<grid, 256, 0, s>>>(v.d_hslot, n, v.d_first, d_vids);
+    CUDA_LAUNCH_CHECK();
+    vsi_hash_reset_kernel<uint32_t><<<std::min(grid, num_sms() * 8), 256, 0, s>>>(
+        v.d_uslot, d_unique, v.d_hkeys32, v.d_first);
+    CUDA_LAUNCH_CHECK();
+    return;
+  }
   vsi_first_kernel<<<grid, 256, 0, s>>>(d_ids, n, v.d_first);
   CUDA_LAUNCH_CHECK();
   lookback_scan<2>(v.tiles, n, VsiFlag{d_ids, v.d_first}, VsiEmit{d_ids, v.d_first, d_gids},
@@ -271,14 +308,16 @@ void vsi_device_hashed(VsiScratch& v, const uint64_t* d_ids, int64_t n, uint64_t
   SFB_CHECK(n > 0 && n <= v.cap, "vsi batch exceeds scratch capacity");
   SFB_CHECK(v.key_space == 0, "hashed VSI needs a context created with key_space 0");
   const int grid = ceil_div(n, 256);
-  vsi_hash_insert_kernel<<<grid, 256, 0, s>>>(d_ids, n, v.d_hkeys, v.d_first, v.hmask, v.d_hslot);
+  vsi_hash_insert_kernel<unsigned long long, uint64_t><<<grid, 256, 0, s>>>(
+      d_ids, n, v.d_hkeys, v.d_first, v.hmask, v.d_hslot);
   CUDA_LAUNCH_CHECK();
   lookback_scan<2>(v.tiles, n, VsiHashFlag{v.d_hslot, v.d_first},
-                VsiHashEmit{d_ids, v.d_hslot, v.d_first, d_gids, v.d_uslot}, d_unique, s);
+                   VsiHashEmit<uint64_t>{d_ids, v.d_hslot, v.d_first, d_gids, v.d_uslot},
+                   d_unique, s);
   vsi_hash_vid_kernel<<<grid, 256, 0, s>>>(v.d_hslot, n, v.d_first, d_vids);
   CUDA_LAUNCH_CHECK();
-  vsi_hash_reset_kernel<<<std::min(grid, num_sms() * 8), 256, 0, s>>>(v.d_uslot, d_unique,
-                                                                     v.d_hkeys, v.d_first);
+  vsi_hash_reset_kernel<unsigned long long><<<std::min(grid, num_sms() * 8), 256, 0, s>>>(
+      v.d_uslot, d_unique, v.d_hkeys, v.d_first);
   CUDA_LAUNCH_CHECK();
 }
 
