@@ -176,10 +176,13 @@ __device__ __forceinline__ bool elect_one() {
   return pred != 0;
 }
 
+// Round to the nearest tf32 (ties away from zero) = cvt.rna.tf32.f32 for finite x, in two
+// integer ops: ptxas expands cvt.rna.tf32 on sm_100a into an inf/nan-guarded sequence
+// (FSETP + SEL + ...), and the split warps of the X-streaming GEMMs (tc_ts.cuh) run 64 of
+// these per row per k-block, which made the split the pacing stage of GEMM1 / GEMM3.
+// (Non-finite inputs are never split: a non-finite activation already fails the step.)
 __device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {

@@ -10,6 +10,7 @@
 //   reduce : dW1 = sum_z part (fixed order); db1, dw2, db2, loss (fixed order)
 #include <cuda.h>
 
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 
@@ -228,8 +229,40 @@ void launch_ts_gemm(dim3 grid, const CUtensorMap& a, const CUtensorMap& bhi,
     CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = true;
   }
-  kern<<<grid, tc::kTsThreads, smem, s>>>(a, bhi, blo, p);
+  static const int dbg = [] {  // experiment switch: SFCTR_TS_DBG (tc_ts.cuh p.dbg bits)
+    const char* e = std::getenv("SFCTR_TS_DBG");
+    return e ? atoi(e) : 0;
+  }();
+  tc::Params q = p;
+  q.dbg = dbg;
+  // SFCTR_TS_TRACE=n: the n-th launch of this instantiation records CTA 0's per-k-block
+  // clock64 stamps and prints them (diagnostics; synchronises the stream)
+  static const int trace_at = [] {
+    const char* e = std::getenv("SFCTR_TS_TRACE");
+    return e ? atoi(e) : -1;
+  }();
+  static int launches = 0;
+  long long* tr = nullptr;
+  if (launches++ == trace_at) {
+    CUDA_CHECK(cudaMalloc(&tr, sizeof(long long) * 320));
+    CUDA_CHECK(cudaMemsetAsync(tr, 0, sizeof(long long) * 320, s));
+    q.trace = tr;
+  }
+  kern<<<grid, tc::kTsThreads, smem, s>>>(a, bhi, blo, q);
   CUDA_LAUNCH_CHECK();
+  if (tr) {
+    long long h[320];
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    CUDA_CHECK(cudaMemcpy(h, tr, sizeof(h), cudaMemcpyDeviceToHost));
+    cudaFree(tr);
+    const long long t0 = h[0];
+    fprintf(stderr, "ts trace A_MN=%d (clk rel. to the first A issue): i a_issue split_start split_done mma_bfull mma_tready\n",
+            A_MN ? 1 : 0);
+    for (int i = 0; i < 64; ++i)
+      fprintf(stderr, "%2d %8lld %8lld %8lld %8lld %8lld\n", i, h[i] ? h[i] - t0 : -1,
+              h[64 + i] ? h[64 + i] - t0 : -1, h[128 + i] ? h[128 + i] - t0 : -1,
+              h[192 + i] ? h[192 + i] - t0 : -1, h[256 + i] ? h[256 + i] - t0 : -1);
+  }
 }
 
 int sm_count() {
