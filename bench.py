@@ -325,9 +325,12 @@ def run_ours(args, D):
         kernels["tower_total"] = {"ms": round(tower_ms, 4), "tf32_flops": fl,
                                   "tflops": round(fl / (tower_ms / 1e3) / 1e12, 2)}
     traffic = {}
-    try:  # DRAM bytes per launch from the committed ncu --set full capture (profiles/)
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            traffic = json.load(fh).get("dram_bytes_per_launch", {})
+    try:  # DRAM bytes per launch from the committed ncu --set full capture (profiles/): a
+        # one-GPU capture (ncu never wraps a multi-rank command), so it describes N = 1 only;
+        # at N > 1 the dominant kernel is the fused owner reduction + Adam, never captured
+        if world == 1:
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+                traffic = json.load(fh).get("dram_bytes_per_launch", {})
     except Exception:
         pass
     # dominant kernel = the largest single-kernel phase with an algorithmic model
@@ -337,10 +340,15 @@ def run_ours(args, D):
     if dom:
         r = kernels[dom]
         if "bytes" in r:
-            roofline = {"kernel": dom, "bound": "hbm", "achieved": r["gbs"], "peak": peaks["hbm_gbs"],
+            roofline = {"kernel": dom if world == 1 or dom != "sparse_adam"
+                        else "owner_reduce_adam (fused owner reduction + sparse Adam)",
+                        "bound": "hbm", "achieved": r["gbs"], "peak": peaks["hbm_gbs"],
                         "unit": "GB/s", "frac": r["frac_hbm"], "traffic": traffic.get(dom),
                         "algorithmic_bytes": r["bytes"],
                         "peak_source": peak_kind + " (copy GB/s, MEASURED_PEAKS.json)"}
+            if world > 1:
+                roofline["traffic_note"] = ("null: ncu never wraps a multi-rank command; the "
+                                            "committed capture is N = 1 (profiles/ncu_traffic.json)")
         else:
             roofline = {"kernel": dom, "bound": "tensor", "achieved": r["tflops"],
                         "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
