@@ -349,6 +349,25 @@ void Exchange::plan(const uint32_t* d_vid, int64_t n_global, int64_t per_worker,
   CUDA_LAUNCH_CHECK();
 }
 
+void Exchange::plan_send(const uint32_t* d_own_k, const int32_t* d_n_own, const int32_t* d_zero,
+                         cudaStream_t s) {
+  const int c = static_cast<int>(cap);
+  const int ntiles = ceil_div(c, kTile);
+  plan_count_kernel<<<dim3(ntiles, 2), 256, 0, s>>>(d_own_k, d_zero, d_own_k, d_n_own, c, tm, W, me,
+                                                    ntiles, tile_cnt);
+  CUDA_LAUNCH_CHECK();
+  plan_scan_tiles_kernel<<<1, 512, 0, s>>>(tile_cnt, ntiles, tile_off, totals);
+  CUDA_LAUNCH_CHECK();
+  plan_rank_kernel<<<dim3(ntiles, 2), 256, 0, s>>>(d_own_k, d_zero, d_own_k, d_n_own, c, tm, W, me,
+                                                   ntiles, tile_off, totals, sscan, lpos);
+  CUDA_LAUNCH_CHECK();
+}
+
+void Exchange::plan_offsets(cudaStream_t s) {
+  offsets_kernel<<<1, 1, 0, s>>>(totals, me, offs);
+  CUDA_LAUNCH_CHECK();
+}
+
 void Exchange::local_vids(const uint32_t* d_vid_mine, int64_t n, uint32_t* d_lvid, cudaStream_t s) {
   lvid_kernel<<<ceil_div(n, 256), 256, 0, s>>>(d_vid_mine, n, lpos, d_lvid);
   CUDA_LAUNCH_CHECK();

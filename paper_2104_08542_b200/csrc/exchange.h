@@ -83,6 +83,12 @@ struct Exchange {
   void plan(const uint32_t* d_vid, int64_t n_global, int64_t per_worker, const uint32_t* d_uniq,
             const int32_t* d_U, const uint32_t* d_own_k, const int32_t* d_n_own, cudaStream_t s,
             const PhaseHook& hook = PhaseHook{});
+  // the send plan alone (sscan, totals[8..16)) over my owned uniques with tm already filled
+  // (owner-sharded manager, shardplan.cu): the receive plan is left empty
+  void plan_send(const uint32_t* d_own_k, const int32_t* d_n_own, const int32_t* d_zero,
+                 cudaStream_t s);
+  // the layout offsets (offs) from totals
+  void plan_offsets(cudaStream_t s);
   void set_counts(const int32_t* h_totals);  // after the step's host wait
   void local_vids(const uint32_t* d_vid_mine, int64_t n, uint32_t* d_lvid, cudaStream_t s);
   int64_t local_rows() const { return recv_off.empty() ? 0 : recv_off[8]; }

@@ -1,0 +1,483 @@
+// Owner-sharded manager stage (see shardplan.h). Per step, on the manager stream:
+//   1. route: every local position p (global index me*n + i) sends (f, p) to owner f mod W
+//      by peer stores into the owner's region for this source (warp-aggregated cursors);
+//      flag barrier B1 also delivers the pair counts (and the bad-id bit)
+//   2. dedup: the owner inserts the pairs it received into a hashed table (match_any merges
+//      a warp's equal ids first): min global position and touched-by-rank mask per feature
+//   3. order: a flag at every owned unique's first global position, one fused look-back scan
+//      over the W*n positions -> owned uniques in global first-appearance order (= the
+//      global_ids order of vsi.cpp:41-46 filtered by owner, as the replicated VSI produces
+//      it), the touched masks by owned index, own_k = identity
+//   4. plan: ranks of each owned unique among those each rank touches (Exchange::plan_send,
+//      the replicated path's own kernels), my column of the count matrix published to every
+//      rank with my unique count; flag barrier B2
+//   5. layout: every rank's receive blocks from the full matrix (offs), the global unique
+//      count, my own rows' local-table positions (lpos)
+//   6. write-back: the owner stores, for every pair it received, the local-table row of that
+//      position into its source's lvid (peer stores); flag barrier B3
+// The result is bit-for-bit the replicated manager's plan: the same owners, the same
+// first-appearance order per owner, the same block layout of every rank's local table.
+#include "shardplan.h"
+
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "scan.cuh"
+
+namespace sfb {
+
+namespace {
+
+constexpr uint32_t kUnseenPos = 0xFFFFFFFFu;
+constexpr uint32_t kEmptyKey = 0xFFFFFFFFu;
+constexpr uint32_t kTagOwned = 0x80000000u;
+constexpr uint64_t kBadBit = 1ull << 63;
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdull;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ull;
+  return x ^ (x >> 33);
+}
+
+struct PeerPairs {
+  uint64_t* dst[8];  // every rank's pair buffer
+};
+
+// 1. route (f, p) to owner f mod W: region `me` of the owner's buffer, warp-aggregated slots
+__global__ void __launch_bounds__(256) route_pairs_kernel(const uint64_t* __restrict__ ids,
+                                                          int64_t n, uint64_t vocab, int W, int me,
+                                                          int32_t* __restrict__ bad,
+                                                          int32_t* __restrict__ cursor,
+                                                          PeerPairs pp) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t n_round = (n + 31) & ~31ll;
+  bool saw_bad = false;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n_round;
+       i += stride) {
+    const bool live = i < n;
+    uint64_t a = live ? ids[i] : 0;
+    if (live && a >= vocab) {  // gated step: the position still routes (as feature 0)
+      saw_bad = true;
+      a = 0;
+    }
+    const uint32_t f = static_cast<uint32_t>(a);
+    const int o = live ? static_cast<int>(f % static_cast<uint32_t>(W)) : -1;
+    const uint64_t pair = (static_cast<uint64_t>(f) << 32) |
+                          static_cast<uint32_t>(static_cast<int64_t>(me) * n + i);
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {  // static destination index: pp stays in the param space
+      if (w >= W) break;
+      const unsigned m = __ballot_sync(0xFFFFFFFFu, o == w);
+      if (!m) continue;
+      const int leader = __ffs(m) - 1;
+      int base = 0;
+      if (lane == leader) base = atomicAdd(cursor + w, __popc(m));
+      base = __shfl_sync(0xFFFFFFFFu, base, leader);
+      if (o == w)
+        pp.dst[w][static_cast<int64_t>(me) * n + base + __popc(m & ((1u << lane) - 1u))] = pair;
+    }
+  }
+  if (saw_bad) *bad = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) __threadfence_system();
+}
+
+struct PeerInts {
+  int32_t* p[8];
+};
+struct PeerFlagsS {
+  uint64_t* p[8];
+};
+
+// The step's two small publications, then the flag barrier (common.cuh's protocol; bit 63 of
+// the published word carries the bad-id flag to every rank). Thread x writes rank x's inbox:
+//   kind 0 (B1): inbox[72 + me] = pairs I routed to owner x (cursor[x])
+//   kind 1 (B2): inbox[w * 8 + me] = rows of mine rank w touches (send totals[8 + w]) for
+//                every w, inbox[64 + me] = my owned unique count
+//   kind 2 (B3): nothing (the lvid write-back precedes it)
+__global__ void publish_barrier_kernel(int kind, PeerInts inbox, const int32_t* __restrict__ cursor,
+                                       const int32_t* __restrict__ totals,
+                                       const int32_t* __restrict__ n_own, PeerFlagsS pf, int W,
+                                       int me, uint64_t epoch, uint64_t timeout_ns,
+                                       int32_t* abort_flag, int32_t* bad) {
+  const int x = threadIdx.x;
+  if (x < W) {
+    int32_t* dst = inbox.p[x];
+    if (kind == 0) {
+      dst[72 + me] = cursor[x];
+    } else if (kind == 1) {
+      for (int w = 0; w < W; ++w) dst[w * 8 + me] = totals[8 + w];
+      dst[64 + me] = *n_own;
+    }
+  }
+  __threadfence_system();
+  __syncwarp();
+  if (x >= W || x == me) return;
+  const uint64_t word = epoch | (bad && *bad ? kBadBit : 0ull);
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(pf.p[x] + me), "l"(word) : "memory");
+  const uint64_t* mine = pf.p[me] + x;
+  uint64_t v = 0, t0 = 0, now = 0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  unsigned ns = 32;
+  for (;;) {
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
+    if ((v & ~kBadBit) >= epoch) break;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (now - t0 > timeout_ns) {
+      if (abort_flag) atomicExch(abort_flag, 1);
+      return;
+    }
+    __nanosleep(ns);
+    if (ns < 2048) ns <<= 1;
+  }
+  if ((v & kBadBit) && bad) atomicExch(bad, 1);
+}
+
+// 2. dedup the received pairs; blockIdx.y = source region r (inbox[72 + r] pairs)
+__global__ void __launch_bounds__(256) dedup_pairs_kernel(const uint64_t* __restrict__ pairs,
+                                                          int64_t n,
+                                                          const int32_t* __restrict__ inbox,
+                                                          uint32_t* __restrict__ keys,
+                                                          uint32_t* __restrict__ pos,
+                                                          uint32_t* __restrict__ tmask,
+                                                          uint64_t mask,
+                                                          uint32_t* __restrict__ hslot) {
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.y;
+  const int64_t cnt = inbox[72 + r];
+  const uint64_t* src = pairs + static_cast<int64_t>(r) * n;
+  uint32_t* hs = hslot + static_cast<int64_t>(r) * n;
+  const uint32_t bit = 1u << r;
+  for (int64_t i0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) & ~31ll;
+       i0 < cnt; i0 += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = i0 + lane;
+    const bool live = i < cnt;
+    const unsigned act = __ballot_sync(0xFFFFFFFFu, live);
+    if (live) {
+      const uint64_t pr = src[i];
+      const uint32_t f = static_cast<uint32_t>(pr >> 32), p = static_cast<uint32_t>(pr);
+      const unsigned peers = __match_any_sync(act, f);
+      const int leader = __ffs(peers) - 1;
+      // the group's smallest position (a region's pairs are not in position order)
+      uint32_t pmin = p;
+      for (unsigned m = peers; m; m &= m - 1) {
+        const uint32_t o = __shfl_sync(peers, p, __ffs(m) - 1);
+        pmin = o < pmin ? o : pmin;
+      }
+      uint32_t slot = 0;
+      if (lane == leader) {
+        uint64_t h = mix64(f) & mask;
+        for (;;) {
+          const uint32_t cur = __ldcg(keys + h);
+          if (cur == f) break;
+          if (cur == kEmptyKey) {
+            const uint32_t prev = atomicCAS(keys + h, kEmptyKey, f);
+            if (prev == kEmptyKey || prev == f) break;
+          }
+          h = (h + 1) & mask;
+        }
+        slot = static_cast<uint32_t>(h);
+        if (__ldcg(pos + slot) > pmin) atomicMin(pos + slot, pmin);
+        if (!(__ldcg(tmask + slot) & bit)) atomicOr(tmask + slot, bit);
+      }
+      hs[i] = __shfl_sync(peers, slot, leader);
+    }
+  }
+}
+
+// 3a. flag the first global position of every owned unique (blockIdx.y = source region)
+__global__ void __launch_bounds__(256) first_flags_kernel(const uint64_t* __restrict__ pairs,
+                                                          int64_t n,
+                                                          const int32_t* __restrict__ inbox,
+                                                          const uint32_t* __restrict__ hslot,
+                                                          const uint32_t* __restrict__ pos,
+                                                          uint32_t* __restrict__ at_pos) {
+  const int r = blockIdx.y;
+  const int64_t cnt = inbox[72 + r];
+  const int64_t off = static_cast<int64_t>(r) * n;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < cnt;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t p = static_cast<uint32_t>(pairs[off + i]);
+    const uint32_t sl = hslot[off + i];
+    if (pos[sl] == p) at_pos[p] = sl + 1;
+  }
+}
+
+// 3b. owned uniques in global first-appearance order (fused look-back scan over positions)
+struct FirstFlag {
+  const uint32_t* at_pos;
+  __device__ uint32_t operator()(int64_t p) const { return at_pos[p] ? 1u : 0u; }
+};
+struct FirstEmit {
+  uint32_t* at_pos;
+  const uint32_t* keys;
+  uint32_t* pos;
+  const uint32_t* tmask;
+  uint32_t* owned;
+  uint32_t* own_k;
+  uint32_t* tm;
+  uint32_t* uslot;
+  __device__ void operator()(int64_t p, uint32_t flag, uint32_t rank) const {
+    if (!flag) return;
+    const uint32_t sl = at_pos[p] - 1;
+    at_pos[p] = 0;  // clean for the next step
+    owned[rank] = keys[sl];
+    own_k[rank] = rank;
+    tm[rank] = tmask[sl];
+    uslot[rank] = sl;
+    pos[sl] = rank | kTagOwned;  // the slot now names its owned index
+  }
+};
+
+// 5. the count matrix (every owner's column arrived with B2), my receive totals, U
+__global__ void finalize_kernel(const int32_t* __restrict__ inbox, int W, int me,
+                                int32_t* __restrict__ totals, int32_t* __restrict__ U_global) {
+  const int t = threadIdx.x;
+  if (t < 64) totals[16 + t] = (t / 8 < W && t % 8 < W) ? inbox[t] : 0;  // cnt[w][o]
+  if (t < 8) totals[t] = t < W ? inbox[me * 8 + t] : 0;                   // rows from owner t
+  if (t == 0) {
+    int32_t u = 0;
+    for (int o = 0; o < W; ++o) u += inbox[64 + o];
+    *U_global = u;
+  }
+}
+
+// my own rows' local-table rows by owned index (the owner reduction reads its own partial
+// gradients at lpos[own_k[j]], own_k = identity here)
+__global__ void own_lpos_kernel(const int32_t* __restrict__ n_own, const uint32_t* __restrict__ tm,
+                                const Cnt8* __restrict__ sscan, const int32_t* __restrict__ offs,
+                                int me, uint32_t* __restrict__ lpos) {
+  const int32_t cnt = *n_own;
+  const uint32_t base = static_cast<uint32_t>(offs[Exchange::kOffRoff + me * 8 + me]);
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < cnt; j += gridDim.x * blockDim.x)
+    lpos[j] = ((tm[j] >> me) & 1u) ? base + sscan[j].c[me] : 0xFFFFFFFFu;
+}
+
+struct PeerLvid {
+  uint32_t* p[8];
+};
+
+// 6. every received pair's local-table row, stored into its source's lvid: rank r's block of
+// my rows starts at roff[r][me]; owned index j is row sscan[j].c[r] of that block
+__global__ void __launch_bounds__(256) writeback_kernel(const uint64_t* __restrict__ pairs,
+                                                        int64_t n, int me,
+                                                        const int32_t* __restrict__ inbox,
+                                                        const uint32_t* __restrict__ hslot,
+                                                        const uint32_t* __restrict__ pos,
+                                                        const Cnt8* __restrict__ sscan,
+                                                        const int32_t* __restrict__ offs,
+                                                        PeerLvid pl) {
+  const int r = blockIdx.y;
+  const int64_t cnt = inbox[72 + r];
+  const int64_t off = static_cast<int64_t>(r) * n;
+  const uint32_t roff = static_cast<uint32_t>(offs[Exchange::kOffRoff + r * 8 + me]);
+  uint32_t* dst = nullptr;
+#pragma unroll
+  for (int w = 0; w < 8; ++w)
+    if (w == r) dst = pl.p[w];
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < cnt;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t p = static_cast<uint32_t>(pairs[off + i]);
+    const uint32_t j = pos[hslot[off + i]] & ~kTagOwned;
+    dst[p - static_cast<uint32_t>(off)] = roff + sscan[j].c[r];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) __threadfence_system();
+}
+
+// 7. clear the hashed table behind the batch
+__global__ void reset_table_kernel(const uint32_t* __restrict__ uslot,
+                                   const int32_t* __restrict__ n_own, uint32_t* __restrict__ keys,
+                                   uint32_t* __restrict__ pos, uint32_t* __restrict__ tmask) {
+  const int32_t cnt = *n_own;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < cnt; j += gridDim.x * blockDim.x) {
+    const uint32_t sl = uslot[j];
+    keys[sl] = kEmptyKey;
+    pos[sl] = kUnseenPos;
+    tmask[sl] = 0;
+  }
+}
+
+}  // namespace
+
+void ShardPlan::init(int W_, int me_, int64_t n_, int64_t cap_) {
+  release();
+  W = W_;
+  me = me_;
+  n = n_;
+  cap = cap_;
+  CUDA_CHECK(cudaMalloc(&pairs, sizeof(uint64_t) * W * n));
+  CUDA_CHECK(cudaMalloc(&inbox, sizeof(int32_t) * kInbox));
+  CUDA_CHECK(cudaMemset(inbox, 0, sizeof(int32_t) * kInbox));
+  for (auto& l : lvid) CUDA_CHECK(cudaMalloc(&l, sizeof(uint32_t) * n));
+  CUDA_CHECK(cudaMalloc(&cursor, sizeof(int32_t) * 16));
+  hmask = 1;
+  while (hmask + 1 < static_cast<uint64_t>(2 * cap)) hmask = 2 * hmask + 1;
+  CUDA_CHECK(cudaMalloc(&hkeys, sizeof(uint32_t) * (hmask + 2)));
+  CUDA_CHECK(cudaMemset(hkeys, 0xFF, sizeof(uint32_t) * (hmask + 2)));
+  CUDA_CHECK(cudaMalloc(&hpos, sizeof(uint32_t) * (hmask + 2)));
+  CUDA_CHECK(cudaMemset(hpos, 0xFF, sizeof(uint32_t) * (hmask + 2)));
+  CUDA_CHECK(cudaMalloc(&hmask_bits, sizeof(uint32_t) * (hmask + 2)));
+  CUDA_CHECK(cudaMemset(hmask_bits, 0, sizeof(uint32_t) * (hmask + 2)));
+  CUDA_CHECK(cudaMalloc(&hslot, sizeof(uint32_t) * W * n));
+  CUDA_CHECK(cudaMalloc(&at_pos, sizeof(uint32_t) * W * n));
+  CUDA_CHECK(cudaMemset(at_pos, 0, sizeof(uint32_t) * W * n));
+  CUDA_CHECK(cudaMalloc(&uslot, sizeof(uint32_t) * cap));
+  CUDA_CHECK(cudaMalloc(&zero, sizeof(int32_t)));
+  CUDA_CHECK(cudaMemset(zero, 0, sizeof(int32_t)));
+  tiles.init(static_cast<int64_t>(W) * n);
+}
+
+void ShardPlan::release() {
+  if (ready)
+    for (int w = 0; w < W; ++w) {
+      if (w == me) continue;
+      for (void* p : {static_cast<void*>(peer_pairs[w]), static_cast<void*>(peer_inbox[w]),
+                      static_cast<void*>(peer_lvid[0][w]), static_cast<void*>(peer_lvid[1][w]),
+                      static_cast<void*>(peer_flags[w])})
+        if (p) cudaIpcCloseMemHandle(p);
+    }
+  for (void* p : {static_cast<void*>(pairs), static_cast<void*>(inbox),
+                  static_cast<void*>(lvid[0]), static_cast<void*>(lvid[1]),
+                  static_cast<void*>(flags), static_cast<void*>(cursor),
+                  static_cast<void*>(hkeys), static_cast<void*>(hpos),
+                  static_cast<void*>(hmask_bits), static_cast<void*>(hslot),
+                  static_cast<void*>(at_pos), static_cast<void*>(uslot),
+                  static_cast<void*>(zero)})
+    if (p) cudaFree(p);
+  tiles.release();
+  *this = ShardPlan();
+}
+
+bool ShardPlan::setup_p2p(ncclComm_t comm, cudaStream_t s) {
+  if (W > 8) return false;
+  int dev = 0;
+  CUDA_CHECK(cudaGetDevice(&dev));
+  int* d_x = nullptr;
+  CUDA_CHECK(cudaMalloc(&d_x, sizeof(int) * (W + 1)));
+  CUDA_CHECK(cudaMemcpyAsync(d_x + me, &dev, sizeof(int), cudaMemcpyHostToDevice, s));
+  NCCL_CHECK(ncclAllGather(d_x + me, d_x, 1, ncclInt32, comm, s));
+  std::vector<int> devs(W);
+  CUDA_CHECK(cudaMemcpyAsync(devs.data(), d_x, sizeof(int) * W, cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  int ok = 1;
+  for (int w = 0; w < W; ++w) {
+    if (w == me) continue;
+    int can = 0;
+    if (cudaDeviceCanAccessPeer(&can, dev, devs[w]) != cudaSuccess || !can) ok = 0;
+  }
+  cudaGetLastError();
+  CUDA_CHECK(cudaMemcpyAsync(d_x + W, &ok, sizeof(int), cudaMemcpyHostToDevice, s));
+  NCCL_CHECK(ncclAllReduce(d_x + W, d_x + W, 1, ncclInt32, ncclMin, comm, s));
+  CUDA_CHECK(cudaMemcpyAsync(&ok, d_x + W, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  cudaFree(d_x);
+  if (!ok) return false;
+  CUDA_CHECK(cudaMalloc(&flags, sizeof(uint64_t) * 8));
+  CUDA_CHECK(cudaMemset(flags, 0, sizeof(uint64_t) * 8));
+  constexpr int kH = 5;
+  cudaIpcMemHandle_t mine[kH];
+  CUDA_CHECK(cudaIpcGetMemHandle(&mine[0], pairs));
+  CUDA_CHECK(cudaIpcGetMemHandle(&mine[1], inbox));
+  CUDA_CHECK(cudaIpcGetMemHandle(&mine[2], lvid[0]));
+  CUDA_CHECK(cudaIpcGetMemHandle(&mine[3], lvid[1]));
+  CUDA_CHECK(cudaIpcGetMemHandle(&mine[4], flags));
+  const size_t hb = sizeof(mine);
+  uint8_t* d_h = nullptr;
+  CUDA_CHECK(cudaMalloc(&d_h, hb * W));
+  CUDA_CHECK(cudaMemcpyAsync(d_h + hb * me, mine, hb, cudaMemcpyHostToDevice, s));
+  NCCL_CHECK(ncclAllGather(d_h + hb * me, d_h, hb, ncclUint8, comm, s));
+  std::vector<cudaIpcMemHandle_t> all(kH * W);
+  CUDA_CHECK(cudaMemcpyAsync(all.data(), d_h, hb * W, cudaMemcpyDeviceToHost, s));
+  CUDA_CHECK(cudaStreamSynchronize(s));
+  cudaFree(d_h);
+  for (int w = 0; w < W; ++w) {
+    if (w == me) {
+      peer_pairs[w] = pairs;
+      peer_inbox[w] = inbox;
+      peer_lvid[0][w] = lvid[0];
+      peer_lvid[1][w] = lvid[1];
+      peer_flags[w] = flags;
+      continue;
+    }
+    void* p[kH] = {};
+    for (int q = 0; q < kH; ++q)
+      CUDA_CHECK(cudaIpcOpenMemHandle(&p[q], all[kH * w + q], cudaIpcMemLazyEnablePeerAccess));
+    peer_pairs[w] = static_cast<uint64_t*>(p[0]);
+    peer_inbox[w] = static_cast<int32_t*>(p[1]);
+    peer_lvid[0][w] = static_cast<uint32_t*>(p[2]);
+    peer_lvid[1][w] = static_cast<uint32_t*>(p[3]);
+    peer_flags[w] = static_cast<uint64_t*>(p[4]);
+  }
+  ready = true;
+  return true;
+}
+
+void ShardPlan::run(const uint64_t* d_ids, uint64_t vocab, int32_t* d_bad, int k, Exchange& xch,
+                    uint32_t* owned_uniq, uint32_t* own_k, int32_t* d_n_own, int32_t* d_U_global,
+                    cudaStream_t s, const PhaseHook& hook) {
+  PeerPairs pp{};
+  PeerInts pi{};
+  PeerFlagsS pf{};
+  PeerLvid pl{};
+  for (int w = 0; w < W; ++w) {
+    pp.dst[w] = peer_pairs[w];
+    pi.p[w] = peer_inbox[w];
+    pf.p[w] = peer_flags[w];
+    pl.p[w] = peer_lvid[k][w];
+  }
+  const uint64_t tmo = barrier_timeout_ns();
+  const int64_t total = static_cast<int64_t>(W) * n;
+  const int gx = static_cast<int>(std::max<int64_t>(
+      1, std::min<int64_t>(ceil_div(n, 256), num_sms() * 8 / W)));  // per source region
+  // 1. route + B1 (pair counts into every owner's inbox[72 + me], the bad-id bit)
+  CUDA_CHECK(cudaMemsetAsync(cursor, 0, sizeof(int32_t) * 8, s));
+  route_pairs_kernel<<<static_cast<int>(std::max<int64_t>(
+                           1, std::min<int64_t>(ceil_div(n, 256), num_sms() * 4))),
+                       256, 0, s>>>(d_ids, n, vocab, W, me, d_bad, cursor, pp);
+  CUDA_LAUNCH_CHECK();
+  publish_barrier_kernel<<<1, 32, 0, s>>>(0, pi, cursor, nullptr, nullptr, pf, W, me, ++epoch,
+                                          tmo, abort_flag, d_bad);
+  CUDA_LAUNCH_CHECK();
+  hook("shard_route");
+  // 2. dedup, 3. first positions -> owned uniques in global first-appearance order
+  dedup_pairs_kernel<<<dim3(gx, W), 256, 0, s>>>(pairs, n, inbox, hkeys, hpos, hmask_bits, hmask,
+                                                 hslot);
+  CUDA_LAUNCH_CHECK();
+  first_flags_kernel<<<dim3(gx, W), 256, 0, s>>>(pairs, n, inbox, hslot, hpos, at_pos);
+  CUDA_LAUNCH_CHECK();
+  lookback_scan<8>(tiles, total, FirstFlag{at_pos},
+                   FirstEmit{at_pos, hkeys, hpos, hmask_bits, owned_uniq, own_k, xch.tm, uslot},
+                   d_n_own, s);
+  hook("shard_dedup");
+  // 4. send plan over my owned uniques, my column of the count matrix + my count; B2
+  xch.plan_send(own_k, d_n_own, zero, s);
+  publish_barrier_kernel<<<1, 32, 0, s>>>(1, pi, nullptr, xch.totals, d_n_own, pf, W, me, ++epoch,
+                                          tmo, abort_flag, nullptr);
+  CUDA_LAUNCH_CHECK();
+  // 5. layout
+  finalize_kernel<<<1, 64, 0, s>>>(inbox, W, me, xch.totals, d_U_global);
+  CUDA_LAUNCH_CHECK();
+  xch.plan_offsets(s);
+  own_lpos_kernel<<<std::max(1, std::min(ceil_div(cap, 256), num_sms() * 4)), 256, 0, s>>>(
+      d_n_own, xch.tm, xch.sscan, xch.offs, me, xch.lpos);
+  CUDA_LAUNCH_CHECK();
+  hook("shard_plan");
+  // 6. write-back, table reset, B3 (every rank's lvid complete)
+  writeback_kernel<<<dim3(gx, W), 256, 0, s>>>(pairs, n, me, inbox, hslot, hpos, xch.sscan,
+                                               xch.offs, pl);
+  CUDA_LAUNCH_CHECK();
+  reset_table_kernel<<<std::max(1, std::min(ceil_div(cap, 256), num_sms() * 4)), 256, 0, s>>>(
+      uslot, d_n_own, hkeys, hpos, hmask_bits);
+  CUDA_LAUNCH_CHECK();
+  publish_barrier_kernel<<<1, 32, 0, s>>>(2, pi, nullptr, nullptr, nullptr, pf, W, me, ++epoch,
+                                          tmo, abort_flag, nullptr);
+  CUDA_LAUNCH_CHECK();
+  hook("shard_writeback");
+}
+
+}  // namespace sfb

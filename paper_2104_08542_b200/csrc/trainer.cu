@@ -257,6 +257,16 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
     xch_.copy_engine = ce && ce[0] == '1';
     const char* nb = std::getenv("SFCTR_NCCL_BARRIER");
     xch_.nccl_barrier = nb && nb[0] == '1';
+    // owner-sharded manager stage (same decision on every rank: the environment and the
+    // collectively agreed peer access)
+    const char* sh = std::getenv("SFCTR_SHARD_MANAGER");
+    if (xch_.device_driven() && !xch_.nccl_barrier && cfg_.lookahead_depth == 1 &&
+        !(sh && sh[0] == '0')) {
+      shard_.init(W_, rank_, n_local_, umax);
+      shard_.abort_flag = d_err_;
+      sharded_ = shard_.setup_p2p(comm_, stream_);
+      if (!sharded_) shard_.release();
+    }
   }
   ensure_bias_tables(1024);
   CUDA_CHECK(cudaStreamSynchronize(stream_));
@@ -270,6 +280,7 @@ Trainer::~Trainer() {
   csr_.release();
   tower_.release();
   towertc_.release();
+  shard_.release();
   xch_.release();
   if (d_lvid_) cudaFree(d_lvid_);
   if (h_totals_) cudaFreeHost(h_totals_);
@@ -579,8 +590,31 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
   // [1] (bad-id flag) is sticky until a host check has seen it
   CUDA_CHECK(cudaMemsetAsync(d_scalars_, 0, sizeof(int32_t), sm));
   CUDA_CHECK(cudaMemsetAsync(d_scalars_ + 2, 0, sizeof(int32_t) * 6, sm));
+  const int32_t cap = static_cast<int32_t>(lane_[0].umax);
+  for (int l = 0; l < lanes_; ++l) {
+    // per-step counters; kCntFromHost (index 2), kCntFreeTop and kCntSeq carry over
+    CUDA_CHECK(cudaMemsetAsync(lane_[l].counters, 0, sizeof(int32_t) * 2, sm));
+    CUDA_CHECK(cudaMemsetAsync(lane_[l].counters + 3, 0, sizeof(int32_t) * 2, sm));
+    CUDA_CHECK(cudaMemsetAsync(lane_[l].counters + kCntOld, 0, sizeof(int32_t), sm));
+  }
+  struct HookCtx {
+    Trainer* tr;
+    cudaStream_t s;
+  } hctx{this, sm};
+  const PhaseHook mhook{[](void* c, const char* n) {
+                          auto* h = static_cast<HookCtx*>(c);
+                          h->tr->phase(n, h->s);
+                        },
+                        &hctx};
   const uint32_t* gids = d_ids32_;
-  if (world_ > 1 && idg_.p2p) {  // u64 -> u32 + peer stores into every rank's buffer
+  if (sharded_) {
+    // ids routed to their owners; each owner's uniques in global first-appearance order
+    // (own_k = identity, d_uniq_ = the owned features), the exchange plan and every rank's
+    // local-table rows (shard_.lvid[k]); U (all ranks) lands in d_scalars_[0]
+    shard_.run(d_features, cfg_.vocabulary_size, d_scalars_ + 1, k, xch_, d_uniq_, lane_[0].own_k,
+               lane_[0].counters + kCntOwned, d_scalars_ + 0, sm, mhook);
+    stats_.nvlink_bytes += n_local_ * 12;  // pairs out, local rows back
+  } else if (world_ > 1 && idg_.p2p) {  // u64 -> u32 + peer stores into every rank's buffer
     gids = idg_.gather(d_features, cfg_.vocabulary_size, d_scalars_ + 1, k, sm);
     stats_.nvlink_bytes += n_local_ * 4;
   } else {
@@ -593,21 +627,17 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
       stats_.nvlink_bytes += n_local_ * 4;
     }
   }
-  phase("ids_allgather", sm);
-  vsi_device(vsi_, gids, n_global_, d_uniq_, d_vid_, d_scalars_ + 0, sm, /*reset=*/false);
-  phase("vsi", sm);
+  if (!sharded_) {
+    phase("ids_allgather", sm);
+    vsi_device(vsi_, gids, n_global_, d_uniq_, d_vid_, d_scalars_ + 0, sm, /*reset=*/false);
+    phase("vsi", sm);
+  }
   // ---- Host-Manager: MixCache per lane (Algorithm 1 l.4-7). The unique and
   // owned counts stay on the device (grids cover the batch-size bound), so the
   // step waits on the host only once, after the probe.
-  const int32_t cap = static_cast<int32_t>(lane_[0].umax);
-  for (int l = 0; l < lanes_; ++l) {
-    // per-step counters; kCntFromHost (index 2), kCntFreeTop and kCntSeq carry over
-    CUDA_CHECK(cudaMemsetAsync(lane_[l].counters, 0, sizeof(int32_t) * 2, sm));
-    CUDA_CHECK(cudaMemsetAsync(lane_[l].counters + 3, 0, sizeof(int32_t) * 2, sm));
-    CUDA_CHECK(cudaMemsetAsync(lane_[l].counters + kCntOld, 0, sizeof(int32_t), sm));
+  for (int l = 0; l < lanes_ && !sharded_; ++l)
     lane_[l].select_owned(d_uniq_, d_scalars_ + 0, cap, Wu, static_cast<uint32_t>(lane0_ + l),
                           l == 0 && !vsi_.hashed32 ? vsi_.d_first : nullptr, sm);
-  }
   {
     LaneCounters lc{};
     GatePtrs gp{};
@@ -616,8 +646,9 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
       gp.own_slot[l] = lane_[l].own_slot;
     }
     // one block: the common case reads the flag and exits
-    bad_id_gate_kernel<<<1, 256, 0, sm>>>(d_scalars_ + 1, d_scalars_ + 0, lc, lanes_, d_vid_,
-                                          n_global_, gp);
+    bad_id_gate_kernel<<<1, 256, 0, sm>>>(d_scalars_ + 1, d_scalars_ + 0, lc, lanes_,
+                                          sharded_ ? shard_.lvid[k] : d_vid_,
+                                          sharded_ ? n_local_ : n_global_, gp);
     CUDA_LAUNCH_CHECK();
   }
   // window batches t+1..t+L-1 (needed_soon), one at a time through the window scratch
@@ -653,19 +684,12 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
   for (int l = 0; l < lanes_ && free_step; ++l)
     free_step = lane_[l].C >= lane_[l].rows || free_lb_[l] >= bound;
   if (a2a_) {  // exchange plan (touched masks, send/receive positions), device only
-    struct HookCtx {
-      Trainer* tr;
-      cudaStream_t s;
-    } hc{this, sm};
-    xch_.plan(d_vid_, n_global_, static_cast<int64_t>(b_) * F_, d_uniq_, d_scalars_ + 0,
-              lane_[0].own_k, lane_[0].counters + kCntOwned, sm,
-              PhaseHook{[](void* c, const char* n) {
-                          auto* h = static_cast<HookCtx*>(c);
-                          h->tr->phase(n, h->s);
-                        },
-                        &hc});
-    bad_id_gate_plan_kernel<<<1, 1, 0, sm>>>(d_scalars_ + 1, xch_.lpos);
-    CUDA_LAUNCH_CHECK();
+    if (!sharded_) {  // (the sharded stage built it with the ids)
+      xch_.plan(d_vid_, n_global_, static_cast<int64_t>(b_) * F_, d_uniq_, d_scalars_ + 0,
+                lane_[0].own_k, lane_[0].counters + kCntOwned, sm, mhook);
+      bad_id_gate_plan_kernel<<<1, 1, 0, sm>>>(d_scalars_ + 1, xch_.lpos);
+      CUDA_LAUNCH_CHECK();
+    }
     if (!free_step)
       CUDA_CHECK(cudaMemcpyAsync(h_totals_, xch_.totals, sizeof(int32_t) * Exchange::kTotals,
                                  cudaMemcpyDeviceToHost, sm));
@@ -832,7 +856,8 @@ void Trainer::train(int64_t step, const uint8_t* d_labels, float* d_loss) {
   // unique k's row is emb[own_slot[k]]): G is never materialised
   const bool direct_emb = defer_fm && zero_in_gather;
   // owner-routed: positions index the local table through lpos (no lvid pass)
-  const bool remap_local = a2a_ && fuse_scatter && d_ % 4 == 0;
+  // (the sharded manager stage wrote every position's local row already: shard_.lvid[k])
+  const bool remap_local = a2a_ && fuse_scatter && d_ % 4 == 0 && !sharded_;
   if (a2a_) {
     if (!free_step) {
       xch_.set_counts(h_totals_);
@@ -851,7 +876,7 @@ void Trainer::train(int64_t step, const uint8_t* d_labels, float* d_loss) {
     table_rows = free_step ? static_cast<size_t>(n_global_) : static_cast<size_t>(xch_.local_rows());
     // with the fused scatter the forward gather and the dX epilogue look the local row up
     // themselves (vid -> lpos[vid]); otherwise the local row of every position is materialised
-    if (!remap_local)
+    if (!remap_local && !sharded_)
       xch_.local_vids(d_vid_ + static_cast<size_t>(lane0_) * b_ * F_, n_local_, d_lvid_, s);
   } else {
     if (world_ > 1) CUDA_CHECK(cudaMemsetAsync(d_G_, 0, sizeof(float) * ud, s));
@@ -910,7 +935,8 @@ void Trainer::train(int64_t step, const uint8_t* d_labels, float* d_loss) {
                               &fork_ctx}
                   : PhaseHook{};
   for (int l = 0; l < lanes_; ++l) {
-    const uint32_t* vid = a2a_ && !remap_local
+    const uint32_t* vid = sharded_ ? shard_.lvid[k]
+                          : a2a_ && !remap_local
                               ? d_lvid_
                               : d_vid_ + static_cast<size_t>(lane0_ + l) * b_ * F_;
     const uint32_t* remap = remap_local ? xch_.lpos : nullptr;

@@ -10,6 +10,7 @@
 #include "cache.h"
 #include "exchange.h"
 #include "idgather.h"
+#include "shardplan.h"
 #include "kernels.h"
 
 namespace sfb {
@@ -184,6 +185,11 @@ class Trainer {
   bool a2a_ = false;              // owner-routed all-to-all sync (world > 1)
   Exchange xch_;
   uint32_t* d_lvid_ = nullptr;    // [n_local] local-table rows of this process's positions
+  // owner-sharded manager stage (shardplan.h): ids routed to their owners instead of the
+  // all-gather + replicated VSI + replicated plan (alltoall over peer stores, lookahead 1;
+  // SFCTR_SHARD_MANAGER=0 keeps the replicated stage)
+  ShardPlan shard_;
+  bool sharded_ = false;
   int32_t* h_totals_ = nullptr;   // pinned [16] exchange plan totals
   int ldx_ = 0;
   bool tower_simt_ = false;

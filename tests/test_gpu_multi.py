@@ -66,6 +66,24 @@ def test_multi_rank_overlap(sync):
     assert "parity ok" in out.stdout
 
 
+@pytest.mark.parametrize("n", [2, 4])
+def test_multi_rank_parity_replicated_manager(n):
+    """The owner-routed exchange with the replicated manager stage (every rank all-gathers
+    the ids and runs VSI + the plan over the global batch; SFCTR_SHARD_MANAGER=0) instead
+    of the owner-sharded one (the default): same per-step parity bars."""
+    if sb.device_count() < n:
+        pytest.skip(f"needs >= {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           os.path.join(ROOT, "tests", "mp_parity_worker.py"), "--sync", "alltoall", "--mode",
+           "pipelined", "--cache", "40000"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT,
+                         env={**os.environ, "SFCTR_SHARD_MANAGER": "0"})
+    print(out.stdout[-6000:], out.stderr[-3000:])
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert "parity ok" in out.stdout
+
+
 @pytest.mark.skipif(sb.device_count() < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("env", [{"SFCTR_NO_P2P": "1", "SFCTR_NCCL_IDS": "1"},
                                  {"SFCTR_NCCL_BARRIER": "1"},
