@@ -30,6 +30,8 @@ import time
 
 import numpy as np
 
+os.environ.setdefault("SFCTR_PHASE_GATE_US", "1500")  # read by the trainer in its phase pass
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -248,7 +250,9 @@ def run_ours(args, D):
     loss_dev = float(d_loss.item())
 
     # ---- per-phase breakdown: K more device-resident steps with phase events (the trainer
-    # issues both stages on one stream while timing, so each phase time is its own)
+    # issues both stages on one stream while timing, so each phase time is its own; a
+    # SFCTR_PHASE_GATE_US hold at the head of every step lets the host enqueue the whole
+    # step first, so a phase's time is device time, not the host's issue time)
     tr.set_timing(True)
     D.barrier()
     for i in range(K):
@@ -358,7 +362,7 @@ def run_ours(args, D):
     sync = None
     if world > 1:
         sync_ms = sum(v for k2, v in phase_ms.items()
-                      if k2.startswith(("allreduce", "exchange")) or k2 == "ids_allgather")
+                      if k2.startswith(("allreduce", "exchange", "shard_")) or k2 == "ids_allgather")
         nv = per_step.get("nvlink_bytes", 0)
         # all-reduce: NCCL bus bytes = 2(W-1)/W x payload; all-to-all: every byte
         # this rank sends crosses NVLink once

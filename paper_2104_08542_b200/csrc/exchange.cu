@@ -213,28 +213,42 @@ __device__ __forceinline__ void plan_count_tile(const uint32_t* __restrict__ key
 }
 
 // warp p scans plane p over the tiles (exclusive), totals[p] = plane total
-// two tables at once (receive plan, send plan): warp q < 16 scans plane q % 8 of table q / 8
+// two tables at once (receive plan, send plan): warp q < 16 scans plane q % 8 of table q / 8.
+// Only the tiles holding live elements (live0 / live1: the tables' element counts) are
+// scanned (the others rank nothing), four 32-tile chunks' loads in flight at a time.
 __global__ void plan_scan_tiles_kernel(const uint32_t* __restrict__ tile_cnt_all, int ntiles,
                                        uint32_t* __restrict__ tile_off_all,
-                                       int32_t* __restrict__ totals_all) {
+                                       int32_t* __restrict__ totals_all,
+                                       const int32_t* __restrict__ live0,
+                                       const int32_t* __restrict__ live1) {
   const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (q >= 16) return;
   const int p = q & 7;
   const uint32_t* tile_cnt = tile_cnt_all + (q >> 3) * ntiles * 8;
   uint32_t* tile_off = tile_off_all + (q >> 3) * ntiles * 8;
   int32_t* totals = totals_all + (q >> 3) * 8;
+  const int32_t live = max(0, *((q >> 3) ? live1 : live0));
+  const int nt = min(ntiles, (live + kTile - 1) / kTile);
   uint32_t carry = 0;
-  for (int t0 = 0; t0 < ntiles; t0 += 32) {
-    const int t = t0 + lane;
-    const uint32_t v = t < ntiles ? tile_cnt[t * 8 + p] : 0u;
-    uint32_t x = v;
+  for (int t0 = 0; t0 < nt; t0 += 128) {
+    uint32_t v[4];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
-      if (lane >= o) x += y;
+    for (int u = 0; u < 4; ++u) {
+      const int t = t0 + u * 32 + lane;
+      v[u] = t < nt ? tile_cnt[t * 8 + p] : 0u;
     }
-    if (t < ntiles) tile_off[t * 8 + p] = carry + x - v;
-    carry += __shfl_sync(0xFFFFFFFFu, x, 31);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int t = t0 + u * 32 + lane;
+      uint32_t x = v[u];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (t < nt) tile_off[t * 8 + p] = carry + x - v[u];
+      carry += __shfl_sync(0xFFFFFFFFu, x, 31);
+    }
   }
   if (lane == 0) totals[p] = static_cast<int32_t>(carry);
 }
@@ -334,7 +348,7 @@ void Exchange::plan(const uint32_t* d_vid, int64_t n_global, int64_t per_worker,
   plan_count_kernel<<<dim3(ntiles, 2), 256, 0, s>>>(d_uniq, d_U, d_own_k, d_n_own, c, tm, W, me,
                                                     ntiles, tile_cnt);
   CUDA_LAUNCH_CHECK();
-  plan_scan_tiles_kernel<<<1, 512, 0, s>>>(tile_cnt, ntiles, tile_off, totals);
+  plan_scan_tiles_kernel<<<1, 512, 0, s>>>(tile_cnt, ntiles, tile_off, totals, d_U, d_n_own);
   CUDA_LAUNCH_CHECK();
   plan_rank_kernel<<<dim3(ntiles, 2), 256, 0, s>>>(d_uniq, d_U, d_own_k, d_n_own, c, tm, W, me,
                                                    ntiles, tile_off, totals, sscan, lpos);
@@ -356,7 +370,7 @@ void Exchange::plan_send(const uint32_t* d_own_k, const int32_t* d_n_own, const 
   plan_count_kernel<<<dim3(ntiles, 2), 256, 0, s>>>(d_own_k, d_zero, d_own_k, d_n_own, c, tm, W, me,
                                                     ntiles, tile_cnt);
   CUDA_LAUNCH_CHECK();
-  plan_scan_tiles_kernel<<<1, 512, 0, s>>>(tile_cnt, ntiles, tile_off, totals);
+  plan_scan_tiles_kernel<<<1, 512, 0, s>>>(tile_cnt, ntiles, tile_off, totals, d_zero, d_n_own);
   CUDA_LAUNCH_CHECK();
   plan_rank_kernel<<<dim3(ntiles, 2), 256, 0, s>>>(d_own_k, d_zero, d_own_k, d_n_own, c, tm, W, me,
                                                    ntiles, tile_off, totals, sscan, lpos);
@@ -368,8 +382,9 @@ void Exchange::plan_offsets(cudaStream_t s) {
   CUDA_LAUNCH_CHECK();
 }
 
-void Exchange::local_vids(const uint32_t* d_vid_mine, int64_t n, uint32_t* d_lvid, cudaStream_t s) {
-  lvid_kernel<<<ceil_div(n, 256), 256, 0, s>>>(d_vid_mine, n, lpos, d_lvid);
+void Exchange::local_vids(const uint32_t* d_vid_mine, int64_t n, uint32_t* d_lvid, cudaStream_t s,
+                          const uint32_t* table) {
+  lvid_kernel<<<ceil_div(n, 256), 256, 0, s>>>(d_vid_mine, n, table ? table : lpos, d_lvid);
   CUDA_LAUNCH_CHECK();
 }
 

@@ -90,7 +90,9 @@ struct Exchange {
   // the layout offsets (offs) from totals
   void plan_offsets(cudaStream_t s);
   void set_counts(const int32_t* h_totals);  // after the step's host wait
-  void local_vids(const uint32_t* d_vid_mine, int64_t n, uint32_t* d_lvid, cudaStream_t s);
+  // d_lvid[i] = table[d_vid_mine[i]], table = lpos by default
+  void local_vids(const uint32_t* d_vid_mine, int64_t n, uint32_t* d_lvid, cudaStream_t s,
+                  const uint32_t* table = nullptr);
   int64_t local_rows() const { return recv_off.empty() ? 0 : recv_off[8]; }
   // returns the bytes this rank sent
   // with the peer-store transport the caller may defer the barrier (do_barrier = false)

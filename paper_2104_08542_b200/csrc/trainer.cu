@@ -453,6 +453,26 @@ __global__ void zero_rows_kernel(float4* __restrict__ p, const int32_t* __restri
 
 }  // namespace
 
+namespace {
+// phase pass only: hold the stream for `ns` so the host enqueues the whole step behind it and
+// every phase time is device time, not the host's issue time (SFCTR_PHASE_GATE_US)
+__global__ void phase_gate_kernel(uint64_t ns) {
+  uint64_t t0 = 0, t = 0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(1000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+uint64_t phase_gate_ns() {
+  static const uint64_t ns = [] {
+    const char* e = std::getenv("SFCTR_PHASE_GATE_US");
+    return e ? static_cast<uint64_t>(std::max(0.0, std::atof(e)) * 1e3) : 0ull;
+  }();
+  return ns;
+}
+}  // namespace
+
 void Trainer::phase(const char* name, cudaStream_t s) {
   if (!timing_) return;
   if (!s) s = stream_;
@@ -569,6 +589,10 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
   if (a2a_) xch_.use(k);
   int32_t* snap = d_snap_[k];
   auto snap_cnt = [&](int l) { return snap + 1 + kCntWords * l; };
+  if (timing_ && phase_gate_ns()) {
+    phase_gate_kernel<<<1, 1, 0, sm>>>(phase_gate_ns());
+    CUDA_LAUNCH_CHECK();
+  }
   phase("start", sm);
   if (sm != sw) phase("start", sw);
   {  // per-step fields restart, running totals carry over
@@ -610,7 +634,8 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
   if (sharded_) {
     // ids routed to their owners; each owner's uniques in global first-appearance order
     // (own_k = identity, d_uniq_ = the owned features), the exchange plan and every rank's
-    // local-table rows (shard_.lvid[k]); U (all ranks) lands in d_scalars_[0]
+    // position -> local-table row map (shard_.index(k) into shard_.rows(k)); U (all ranks)
+    // lands in d_scalars_[0]
     shard_.run(d_features, cfg_.vocabulary_size, d_scalars_ + 1, k, xch_, d_uniq_, lane_[0].own_k,
                lane_[0].counters + kCntOwned, d_scalars_ + 0, sm, mhook);
     stats_.nvlink_bytes += n_local_ * 12;  // pairs out, local rows back
@@ -647,8 +672,7 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
     }
     // one block: the common case reads the flag and exits
     bad_id_gate_kernel<<<1, 256, 0, sm>>>(d_scalars_ + 1, d_scalars_ + 0, lc, lanes_,
-                                          sharded_ ? shard_.lvid[k] : d_vid_,
-                                          sharded_ ? n_local_ : n_global_, gp);
+                                          d_vid_, sharded_ ? 0 : n_global_, gp);
     CUDA_LAUNCH_CHECK();
   }
   // window batches t+1..t+L-1 (needed_soon), one at a time through the window scratch
@@ -855,9 +879,9 @@ void Trainer::train(int64_t step, const uint8_t* d_labels, float* d_loss) {
   // ... and the forward reads the cache rows in place (own_k is the identity at W = 1, so
   // unique k's row is emb[own_slot[k]]): G is never materialised
   const bool direct_emb = defer_fm && zero_in_gather;
-  // owner-routed: positions index the local table through lpos (no lvid pass)
-  // (the sharded manager stage wrote every position's local row already: shard_.lvid[k])
-  const bool remap_local = a2a_ && fuse_scatter && d_ % 4 == 0 && !sharded_;
+  // owner-routed: positions index the local table through lpos (no lvid pass); with the
+  // sharded manager stage through the owners' replies (row = rows(k)[index(k)[i]])
+  const bool remap_local = a2a_ && fuse_scatter && d_ % 4 == 0;
   if (a2a_) {
     if (!free_step) {
       xch_.set_counts(h_totals_);
@@ -876,7 +900,9 @@ void Trainer::train(int64_t step, const uint8_t* d_labels, float* d_loss) {
     table_rows = free_step ? static_cast<size_t>(n_global_) : static_cast<size_t>(xch_.local_rows());
     // with the fused scatter the forward gather and the dX epilogue look the local row up
     // themselves (vid -> lpos[vid]); otherwise the local row of every position is materialised
-    if (!remap_local && !sharded_)
+    if (!remap_local && sharded_)
+      xch_.local_vids(shard_.index(k), n_local_, d_lvid_, s, shard_.rows(k));
+    else if (!remap_local)
       xch_.local_vids(d_vid_ + static_cast<size_t>(lane0_) * b_ * F_, n_local_, d_lvid_, s);
   } else {
     if (world_ > 1) CUDA_CHECK(cudaMemsetAsync(d_G_, 0, sizeof(float) * ud, s));
@@ -935,11 +961,10 @@ void Trainer::train(int64_t step, const uint8_t* d_labels, float* d_loss) {
                               &fork_ctx}
                   : PhaseHook{};
   for (int l = 0; l < lanes_; ++l) {
-    const uint32_t* vid = sharded_ ? shard_.lvid[k]
-                          : a2a_ && !remap_local
-                              ? d_lvid_
-                              : d_vid_ + static_cast<size_t>(lane0_ + l) * b_ * F_;
-    const uint32_t* remap = remap_local ? xch_.lpos : nullptr;
+    const uint32_t* vid = a2a_ && !remap_local ? d_lvid_
+                          : sharded_            ? shard_.index(k)
+                                                : d_vid_ + static_cast<size_t>(lane0_ + l) * b_ * F_;
+    const uint32_t* remap = !remap_local ? nullptr : sharded_ ? shard_.rows(k) : xch_.lpos;
     const uint8_t* lab = d_labels + static_cast<size_t>(l) * b_;
     if (tower_fused_) {  // gather -> GEMM -> scatter-add, X / dX never materialised
       tower_forward_backward_fused(tower_, towertc_, d_G_, static_cast<int64_t>(table_rows), vid,
