@@ -359,7 +359,7 @@ void Exchange::plan(const uint32_t* d_vid, int64_t n_global, int64_t per_worker,
   count_matrix_kernel<<<std::min(ceil_div(c, 256), num_sms() * 4), 256, 0, s>>>(d_uniq, d_U, c, tm, W,
                                                                            totals + 16);
   CUDA_LAUNCH_CHECK();
-  offsets_kernel<<<1, 1, 0, s>>>(totals, me, offs);
+  offsets_kernel<<<1, 32, 0, s>>>(totals, me, offs);
   CUDA_LAUNCH_CHECK();
 }
 
@@ -378,7 +378,7 @@ void Exchange::plan_send(const uint32_t* d_own_k, const int32_t* d_n_own, const 
 }
 
 void Exchange::plan_offsets(cudaStream_t s) {
-  offsets_kernel<<<1, 1, 0, s>>>(totals, me, offs);
+  offsets_kernel<<<1, 32, 0, s>>>(totals, me, offs);
   CUDA_LAUNCH_CHECK();
 }
 
@@ -499,27 +499,38 @@ __global__ void push_block_p2p_kernel(const float4* __restrict__ dE, int64_t src
 
 namespace {
 
-// the host's set_counts, on the device (one thread): every rank's receive layout
+// the host's set_counts, on the device: every rank's receive layout (the totals staged in
+// shared memory, then thread w builds row w of roff, thread 8 + o column o of boff)
 __global__ void offsets_kernel(const int32_t* __restrict__ totals, int me, int32_t* __restrict__ offs) {
-  const int32_t* cnt = totals + 16;  // cnt[w][o]
-  int32_t* roff = offs + Exchange::kOffRoff;
-  int32_t* boff = offs + Exchange::kOffBoff;
-  int32_t* recv_off = offs + Exchange::kOffRecv;
-  int32_t* send_off = offs + Exchange::kOffSend;
-  for (int w = 0; w < 8; ++w) {
-    roff[w * 8] = 0;
-    for (int o = 1; o < 8; ++o) roff[w * 8 + o] = roff[w * 8 + o - 1] + cnt[w * 8 + o - 1];
-  }
-  for (int o = 0; o < 8; ++o) {
-    boff[o * 8] = 0;
-    for (int w = 1; w < 8; ++w)
-      boff[o * 8 + w] = boff[o * 8 + w - 1] + (w - 1 == o ? 0 : cnt[(w - 1) * 8 + o]);
-  }
-  recv_off[0] = 0;
-  send_off[0] = 0;
-  for (int o = 0; o < 8; ++o) {
-    recv_off[o + 1] = recv_off[o] + totals[o];
-    send_off[o + 1] = send_off[o] + (o == me ? 0 : totals[8 + o]);
+  __shared__ int32_t t[Exchange::kTotals];
+  for (int i = threadIdx.x; i < Exchange::kTotals; i += blockDim.x) t[i] = totals[i];
+  __syncthreads();
+  const int32_t* cnt = t + 16;  // cnt[w][o]
+  const int x = threadIdx.x;
+  if (x < 8) {
+    int32_t* roff = offs + Exchange::kOffRoff + x * 8;
+    int32_t run = 0;
+    for (int o = 0; o < 8; ++o) {
+      roff[o] = run;
+      run += cnt[x * 8 + o];
+    }
+  } else if (x < 16) {
+    const int o = x - 8;
+    int32_t* boff = offs + Exchange::kOffBoff + o * 8;
+    int32_t run = 0;
+    for (int w = 0; w < 8; ++w) {
+      boff[w] = run;
+      if (w != o) run += cnt[w * 8 + o];
+    }
+  } else if (x == 16) {
+    int32_t* recv_off = offs + Exchange::kOffRecv;
+    int32_t* send_off = offs + Exchange::kOffSend;
+    recv_off[0] = 0;
+    send_off[0] = 0;
+    for (int o = 0; o < 8; ++o) {
+      recv_off[o + 1] = recv_off[o] + t[o];
+      send_off[o + 1] = send_off[o] + (o == me ? 0 : t[8 + o]);
+    }
   }
 }
 

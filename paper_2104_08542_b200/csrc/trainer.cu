@@ -361,6 +361,23 @@ struct LaneCounters {
   const int32_t* c[8];
 };
 
+struct StepClear {
+  int32_t* scalars;
+  int32_t* cnt[8];
+  int lanes;
+};
+// scalars[0] and [2, 8) ([1], the bad-id flag, is sticky until a host check has seen it);
+// per lane counters [0, 2), [3, 5) and kCntOld
+__global__ void step_clear_kernel(StepClear a) {
+  const int t = threadIdx.x;
+  if (t < 8 && t != 1) a.scalars[t] = 0;
+  const int l = t / 8, q = t % 8;
+  if (l < a.lanes) {
+    const int idx = q < 2 ? q : q < 4 ? q + 1 : q == 4 ? kCntOld : -1;
+    if (idx >= 0) a.cnt[l][idx] = 0;
+  }
+}
+
 // The step's tail in one launch: dense Adam over the P dense parameters (same math as
 // dense_adam, tower.cu), the per-row Adam step counts of the rows sparse_adam just
 // updated, the loss, and (host-wait-free steps) the step totals.
@@ -612,15 +629,17 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
   // ==== manager stage (stream sm) ====
   // ---- Data-Loader: ids to u32, all-gather the global batch, VSI (Algorithm 1 l.2-3)
   // [1] (bad-id flag) is sticky until a host check has seen it
-  CUDA_CHECK(cudaMemsetAsync(d_scalars_, 0, sizeof(int32_t), sm));
-  CUDA_CHECK(cudaMemsetAsync(d_scalars_ + 2, 0, sizeof(int32_t) * 6, sm));
-  const int32_t cap = static_cast<int32_t>(lane_[0].umax);
-  for (int l = 0; l < lanes_; ++l) {
-    // per-step counters; kCntFromHost (index 2), kCntFreeTop and kCntSeq carry over
-    CUDA_CHECK(cudaMemsetAsync(lane_[l].counters, 0, sizeof(int32_t) * 2, sm));
-    CUDA_CHECK(cudaMemsetAsync(lane_[l].counters + 3, 0, sizeof(int32_t) * 2, sm));
-    CUDA_CHECK(cudaMemsetAsync(lane_[l].counters + kCntOld, 0, sizeof(int32_t), sm));
+  // per-step scalars and per-lane counters cleared in one launch (kCntFromHost (index 2),
+  // kCntFreeTop and kCntSeq carry over)
+  {
+    StepClear sc{};
+    sc.scalars = d_scalars_;
+    for (int l = 0; l < lanes_; ++l) sc.cnt[l] = lane_[l].counters;
+    sc.lanes = lanes_;
+    step_clear_kernel<<<1, 64, 0, sm>>>(sc);
+    CUDA_LAUNCH_CHECK();
   }
+  const int32_t cap = static_cast<int32_t>(lane_[0].umax);
   struct HookCtx {
     Trainer* tr;
     cudaStream_t s;

@@ -105,6 +105,24 @@ def test_two_rank_parity_fallback_transports(env):
 
 
 @pytest.mark.skipif(sb.device_count() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("sync,env", [("alltoall", {}), ("alltoall", {"SFCTR_SHARD_MANAGER": "0"}),
+                                      ("allreduce", {})])
+def test_multi_rank_out_of_vocab(sync, env):
+    """An id >= vocab on one rank gates the step on every rank (sharded manager: the bad-id
+    bit rides the routing barrier; replicated: the id all-gather's reduction): LogicError
+    everywhere, no state moves, training continues like a run that never saw the batch."""
+    n = min(sb.device_count(), 4)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           os.path.join(ROOT, "tests", "mp_oov_worker.py"), "--sync", sync]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
+                         env={**os.environ, **env})
+    print(out.stdout[-3000:], out.stderr[-3000:])
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert "oov ok" in out.stdout
+
+
+@pytest.mark.skipif(sb.device_count() < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("sync", ["allreduce", "alltoall"])
 def test_multi_rank_deterministic(sync, tmp_path):
     """deterministic=1 across ranks: two launches of the same in-flight run give
