@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 namespace sfb {
 
@@ -147,6 +148,43 @@ __device__ inline void flag_barrier_wait(uint64_t* const* peer, int W, int me, u
     __nanosleep(ns);
     if (ns < 2048) ns <<= 1;
   }
+}
+#endif
+
+// Programmatic dependent launch (PDL) between consecutive kernels of the training stream:
+// a kernel launched with launch_pdl() may start (prologue: barrier init, TMEM allocation,
+// tensor-map prefetch) while its predecessor drains; pdl_wait() blocks until the predecessor
+// has completed and its writes are visible, so it must precede every read of the
+// predecessor's outputs. pdl_trigger() lets the successor launch before this grid exits.
+// Both are no-ops for a kernel launched without the attribute. SFCTR_NO_PDL=1 disables it.
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+#endif
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SFCTR_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+#ifdef __CUDACC__
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 #endif
 

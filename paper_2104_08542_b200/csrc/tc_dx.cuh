@@ -130,6 +130,7 @@ __global__ void __launch_bounds__(dx_threads<SCATTER>(), 1)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  pdl_wait();  // dh (head) / vid, gz, fm_s are read below
   const uint32_t tmem = *tmem_holder;
 
   if (warp == 0) {

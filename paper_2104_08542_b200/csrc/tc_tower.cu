@@ -95,6 +95,7 @@ __global__ void head_tc_kernel(int rows, int H, int d, int sq_parts, const float
                                float* __restrict__ lossr, float* __restrict__ dh_hi,
                                float* __restrict__ dh_lo, int ldh, float* __restrict__ sg_part) {
   __shared__ float sg[8][2 * 64 + 2];
+  pdl_wait();  // GEMM1's partials
   const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   if (r >= rows) {  // (rows % 8 != 0) this warp's row contributes nothing
@@ -248,7 +249,7 @@ void launch_ts_gemm(dim3 grid, const CUtensorMap& a, const CUtensorMap& bhi,
     CUDA_CHECK(cudaMemsetAsync(tr, 0, sizeof(long long) * 320, s));
     q.trace = tr;
   }
-  kern<<<grid, tc::kTsThreads, smem, s>>>(a, bhi, blo, q);
+  launch_pdl(kern, grid, dim3(tc::kTsThreads), smem, s, a, bhi, blo, q);
   CUDA_LAUNCH_CHECK();
   if (tr) {
     long long h[320];
@@ -316,7 +317,7 @@ void launch_dx_gemm(const TowerTC& tc_, const float* dh_hi, const float* dh_lo, 
       CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       configured = smem;
     }
-    kern<<<grid, tc::dx_threads<true>(), smem, s>>>(ah, al, bh, bl, bh, p);
+    launch_pdl(kern, dim3(grid), dim3(tc::dx_threads<true>()), smem, s, ah, al, bh, bl, bh, p);
     CUDA_LAUNCH_CHECK();
     return;
   }
@@ -328,7 +329,7 @@ void launch_dx_gemm(const TowerTC& tc_, const float* dh_hi, const float* dh_lo, 
     CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = true;
   }
-  kern<<<grid, 192, smem, s>>>(ah, al, bh, bl, out, p);
+  launch_pdl(kern, dim3(grid), dim3(192), smem, s, ah, al, bh, bl, out, p);
   CUDA_LAUNCH_CHECK();
 }
 
@@ -614,10 +615,11 @@ void tower_forward_backward_tc(TowerBufs& t, TowerTC& tc_, const float* X, int l
   }
   hook("tower_gemm1");
   // ---- head
-  head_tc_kernel<<<ceil_div(static_cast<int64_t>(rows) * 32, 256), 256, 0, s>>>(
-      rows, H, d, fm_sq_parts(d), tc_.part1, s1, static_cast<long long>(rows) * H, b1, w2, b2p,
-      fm_s, fm_sqp, labels, 1.f / rows, logits, t.act, t.dh, t.gz, t.lossr, tc_.dh_hi, tc_.dh_lo,
-      tc_.ldh, H <= 64 ? t.sg_part : nullptr);
+  launch_pdl(head_tc_kernel, dim3(ceil_div(static_cast<int64_t>(rows) * 32, 256)), dim3(256), 0, s,
+             rows, H, d, fm_sq_parts(d), static_cast<const float*>(tc_.part1), s1,
+             static_cast<long long>(rows) * H, b1, w2, b2p, static_cast<const float*>(fm_s),
+             static_cast<const float*>(fm_sqp), labels, 1.f / rows, logits, t.act, t.dh, t.gz,
+             t.lossr, tc_.dh_hi, tc_.dh_lo, tc_.ldh, H <= 64 ? t.sg_part : nullptr);
   CUDA_LAUNCH_CHECK();
   hook("tower_head");
   // ---- GEMM2: dX = scale dh W1^T (A = dh hi/lo, B = W1 hi/lo, both K-major; the FM

@@ -30,8 +30,14 @@
 namespace sfb {
 namespace tc {
 
-constexpr int kTsARing = 8;   // raw A tiles (smem)
-constexpr int kTsBRing = 4;   // B hi/lo tiles (smem)
+#ifndef SFB_TS_ARING
+#define SFB_TS_ARING 8
+#endif
+#ifndef SFB_TS_BRING
+#define SFB_TS_BRING 4
+#endif
+constexpr int kTsARing = SFB_TS_ARING;  // raw A tiles (smem)
+constexpr int kTsBRing = SFB_TS_BRING;  // B hi/lo tiles (smem)
 constexpr int kTsStages = 6;  // TMEM A stages: 128 accumulator columns + 6 x 64 = 512
 constexpr int kTsThreads = 352;  // 11 warps: A producer, MMA, 8 split/epilogue, B producer
 
@@ -137,6 +143,10 @@ __global__ void __launch_bounds__(kTsThreads, 1)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // PDL: the predecessor's outputs (X / dh) are read only after it has completed. No early
+  // trigger: successors launched early sit on SM slots the concurrent row update needs
+  // (measured: -8 % at cfg2 N = 1 with a trigger here and in the dX GEMM)
+  pdl_wait();
   const uint32_t tmem = *tmem_holder;  // accumulator: columns [0, 128)
   auto a_col = [&](int s) { return tmem + 128u + static_cast<uint32_t>(s) * 64u; };  // hi | lo
 

@@ -426,6 +426,7 @@ __global__ void tower_reduce_kernel(const float* __restrict__ part3, int splits,
                                     int chunks, int H, float inv_rows, float* __restrict__ g_db1,
                                     float* __restrict__ g_dw2, float* __restrict__ g_db2,
                                     float* __restrict__ g_loss, int accumulate) {
+  pdl_wait();  // GEMM3 partials
   if (static_cast<int>(blockIdx.x) < nb) {
     const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (i >= kh) return;
@@ -467,9 +468,9 @@ void tower_reduce(const float* part3, int splits, int64_t kh, float* g_w1, Tower
                   int chunks, int rows, int H, float* g_b1, float* g_w2, float* g_b2,
                   float* g_loss, bool accumulate, cudaStream_t s) {
   const int nb = ceil_div(kh, 256);
-  tower_reduce_kernel<<<nb + 2 * H + 2, 256, 0, s>>>(part3, splits, kh, g_w1, nb, t.sg_part, chunks,
-                                                     H, 1.f / rows, g_b1, g_w2, g_b2, g_loss,
-                                                     accumulate ? 1 : 0);
+  launch_pdl(tower_reduce_kernel, dim3(nb + 2 * H + 2), dim3(256), 0, s, part3, splits, kh, g_w1,
+             nb, static_cast<const float*>(t.sg_part), chunks, H, 1.f / rows, g_b1, g_w2, g_b2,
+             g_loss, accumulate ? 1 : 0);
   CUDA_LAUNCH_CHECK();
 }
 
