@@ -403,10 +403,13 @@ __global__ void admit_kernel(const int32_t* __restrict__ counters, int32_t n_evi
   const int32_t n_work = counters[kCntWorking];
   const int32_t free_top = counters[kCntFreeTop] + n_evict;
   const uint64_t seq0 = *reinterpret_cast<const uint64_t*>(counters + kCntSeq);
-  const int64_t i0 =
-      ((blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5) * kAdmitRows;
   const int lane = threadIdx.x & 31;
-  if (i0 >= n_work) return;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  // grid-stride over warps: the grid is capped (mgr_grid) so the manager stage never fills an
+  // SM that a persistent training kernel is about to need
+  for (int64_t wi = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+       wi * kAdmitRows < n_work; wi += nwarps) {
+  const int64_t i0 = wi * kAdmitRows;
   const int64_t mi = i0 + lane;
   const bool mine = lane < kAdmitRows && mi < n_work;
   uint32_t my_f = 0, my_s = 0, my_where = kNever;
@@ -475,6 +478,7 @@ __global__ void admit_kernel(const int32_t* __restrict__ counters, int32_t n_evi
         vel[so + c] = 0.f;
       }
     }
+  }
   }
 }
 
@@ -859,7 +863,7 @@ void CacheLane::select_owned(const uint32_t* d_gids, const int32_t* d_U, int32_t
                              uint32_t w, uint32_t* vsi_first, cudaStream_t s) {
   if (cap <= 0) return;
   if (W == 1) {  // a single worker owns every unique: own_k = identity, count = U
-    own_all_kernel<<<std::max(1, std::min(ceil_div(cap, 256), num_sms() * 8)), 256, 0, s>>>(
+    own_all_kernel<<<mgr_grid(ceil_div(cap, 256)), 256, 0, s>>>(
         d_U, own_k, counters + kCntOwned, d_gids, vsi_first);
     CUDA_LAUNCH_CHECK();
     return;
@@ -965,8 +969,8 @@ void CacheLane::evict_admit(int32_t n_evict, int32_t n_work, uint32_t W, uint64_
 void CacheLane::admit(int32_t n_bound, int32_t n_evict, uint32_t W, uint64_t seed, int32_t t,
                       cudaStream_t s) {
   if (n_bound > 0) {
-    admit_kernel<<<ceil_div(ceil_div(static_cast<int64_t>(n_bound), kAdmitRows) * 32, 256), 256, 0,
-                   s>>>(counters, n_evict, work_j, work_f, work_w, W, d, free_stack, index,
+    admit_kernel<<<mgr_grid(ceil_div(ceil_div(static_cast<int64_t>(n_bound), kAdmitRows) * 32, 256)),
+                   256, 0, s>>>(counters, n_evict, work_j, work_f, work_w, W, d, free_stack, index,
                         host.tab(), slot_host, seed, fnv1a64("embed"), emb, mom, vel, steps,
                         slot_feat, last_use, admit_seq, mark, t, own_slot,
                         counters + kCntFromHost);

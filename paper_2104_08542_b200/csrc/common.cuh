@@ -6,6 +6,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <stdexcept>
@@ -187,6 +188,20 @@ void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cu
   CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 #endif
+
+// Grid of a manager-stage kernel (grid-stride loops inside): at most SFCTR_MGR_CTAS_PER_SM
+// CTAs per SM when set (default 0 = uncapped). Measured at cfg2 N = 1: a cap of 2 made the
+// step slower (25.9 vs 27.5 M samples/s): the capped CTAs live longer and the block
+// scheduler packs them onto a subset of SMs, which then cannot take a persistent training
+// GEMM CTA. The training GEMMs take their work items dynamically instead (tc_ts.cuh).
+inline int mgr_grid(int64_t want) {
+  static const int per = [] {
+    const char* e = std::getenv("SFCTR_MGR_CTAS_PER_SM");
+    return e ? std::max(0, std::atoi(e)) : 0;
+  }();
+  const int64_t cap = per > 0 ? static_cast<int64_t>(num_sms()) * per : want;
+  return static_cast<int>(std::max<int64_t>(1, std::min(want, cap)));
+}
 
 // barrier timeout: SFCTR_BARRIER_TIMEOUT_S seconds (default 600)
 inline uint64_t barrier_timeout_ns() {

@@ -328,7 +328,8 @@ void gather_cache(const uint32_t* own_k, const uint32_t* own_slot, int32_t n_own
 void zero_rows_b(const int32_t* d_n, int32_t n_bound, int d, float* dG, float* B, cudaStream_t s) {
   SFB_CHECK((d & 3) == 0, "zero_rows_b needs d % 4 == 0");
   if (n_bound <= 0) return;
-  zero_rows_b_kernel<<<wave_grid(static_cast<int64_t>(n_bound) * (d / 4)), 256, 0, s>>>(
+  // manager stage: a capped grid (mgr_grid), not a full wave of resident CTAs
+  zero_rows_b_kernel<<<mgr_grid(ceil_div(static_cast<int64_t>(n_bound) * (d / 4), 256)), 256, 0, s>>>(
       d_n, d / 4, reinterpret_cast<float4*>(dG), B);
   CUDA_LAUNCH_CHECK();
 }

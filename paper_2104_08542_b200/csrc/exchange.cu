@@ -859,7 +859,8 @@ void Exchange::backward_reduce_adam_dev(const uint32_t* d_own_k, int32_t n_bound
 }
 
 void Exchange::zero_local_dev(float* dE, cudaStream_t s, float* B) {
-  zero_rows_dev_kernel<<<num_sms() * 8, 256, 0, s>>>(reinterpret_cast<float4*>(dE), offs, d / 4, B);
+  zero_rows_dev_kernel<<<mgr_grid(num_sms() * 8), 256, 0, s>>>(reinterpret_cast<float4*>(dE), offs,
+                                                                d / 4, B);
   CUDA_LAUNCH_CHECK();
 }
 

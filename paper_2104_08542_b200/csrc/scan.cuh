@@ -58,87 +58,88 @@ __global__ void __launch_bounds__(kScanThreads) lookback_scan_kernel(int64_t n, 
   __shared__ uint32_t tile_prefix;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   constexpr int64_t kScanTile = kScanThreads * kScanItems;
-  const int64_t tile = blockIdx.x;
-  const int64_t base = tile * kScanTile;
   // live (device count, nullable): items [live, n) are empty; tiles past the last live one
   // exit at once (no successor reads their state) and the last live tile writes the total
-  if (live) {
-    const int64_t nl = min(n, static_cast<int64_t>(max(0, *live)));
-    if (base >= nl && tile > 0) return;
-    n = nl;
-  }
-  const int64_t last_tile = n > 0 ? (n - 1) / kScanTile : 0;
-  uint32_t v[kScanItems], ex[kScanItems];
+  if (live) n = min(n, static_cast<int64_t>(max(0, *live)));
+  const int64_t ntiles = n > 0 ? (n + kScanTile - 1) / kScanTile : 1;
+  const int64_t last_tile = ntiles - 1;
+  // persistent: CTA b scans tiles b, b + G, b + 2G, ... in order (G = gridDim.x, capped by
+  // mgr_grid); a tile's look-back only waits on lower tiles, which their CTAs reach first
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t base = tile * kScanTile;
+    uint32_t v[kScanItems], ex[kScanItems];
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    const int64_t i = base + k * kScanThreads + tid;
-    v[k] = i < n ? value(i) : 0u;
-  }
-  uint32_t run = 0;  // tile-local running total (uniform)
-#pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    uint32_t x = v[k];
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, off);
-      if (lane >= off) x += y;
+    for (int k = 0; k < kScanItems; ++k) {
+      const int64_t i = base + k * kScanThreads + tid;
+      v[k] = i < n ? value(i) : 0u;
     }
-    if (lane == 31) warp_sum[wid] = x;
-    __syncthreads();
-    uint32_t before = 0, all = 0;
+    uint32_t run = 0;  // tile-local running total (uniform)
 #pragma unroll
-    for (int w = 0; w < kScanThreads / 32; ++w) {
-      const uint32_t s = warp_sum[w];
-      before += w < wid ? s : 0u;
-      all += s;
-    }
-    ex[k] = run + before + x - v[k];
-    run += all;
-    __syncthreads();
-  }
-  using namespace scan_detail;
-  if (tile == 0) {
-    if (tid == 0) {
-      publish(state, epoch, kPre, run);
-      tile_prefix = 0;
-    }
-  } else if (wid == 0) {
-    if (lane == 0) publish(state + tile, epoch, kAgg, run);
-    uint32_t excl = 0;
-    int64_t look = tile - 1;
-    for (;;) {
-      const int64_t t = look - lane;
-      uint64_t w = t >= 0 ? peek(state + t)
-                          : ((static_cast<uint64_t>(epoch) << 34) | (kPre << 32));
-      uint64_t st = (w >> 34) == epoch ? ((w >> 32) & 3u) : 0u;
-      while (__any_sync(0xFFFFFFFFu, st == 0)) {  // a predecessor has not published yet
-        if (st == 0) {
-          w = peek(state + t);
-          st = (w >> 34) == epoch ? ((w >> 32) & 3u) : 0u;
-        }
+    for (int k = 0; k < kScanItems; ++k) {
+      uint32_t x = v[k];
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, off);
+        if (lane >= off) x += y;
       }
-      const unsigned pre = __ballot_sync(0xFFFFFFFFu, st == kPre);
-      const int stop = pre ? __ffs(pre) - 1 : 31;  // closest predecessor with a full prefix
-      uint32_t val = lane <= stop ? static_cast<uint32_t>(w) : 0u;
+      if (lane == 31) warp_sum[wid] = x;
+      __syncthreads();
+      uint32_t before = 0, all = 0;
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) val += __shfl_xor_sync(0xFFFFFFFFu, val, off);
-      excl += val;
-      if (pre) break;
-      look -= 32;
+      for (int w = 0; w < kScanThreads / 32; ++w) {
+        const uint32_t s = warp_sum[w];
+        before += w < wid ? s : 0u;
+        all += s;
+      }
+      ex[k] = run + before + x - v[k];
+      run += all;
+      __syncthreads();
     }
-    if (lane == 0) {
-      publish(state + tile, epoch, kPre, excl + run);
-      tile_prefix = excl;
-    }
-  }
-  __syncthreads();
-  const uint32_t pfx = tile_prefix;
+    using namespace scan_detail;
+    if (tile == 0) {
+      if (tid == 0) {
+        publish(state, epoch, kPre, run);
+        tile_prefix = 0;
+      }
+    } else if (wid == 0) {
+      if (lane == 0) publish(state + tile, epoch, kAgg, run);
+      uint32_t excl = 0;
+      int64_t look = tile - 1;
+      for (;;) {
+        const int64_t t = look - lane;
+        uint64_t w = t >= 0 ? peek(state + t)
+                            : ((static_cast<uint64_t>(epoch) << 34) | (kPre << 32));
+        uint64_t st = (w >> 34) == epoch ? ((w >> 32) & 3u) : 0u;
+        while (__any_sync(0xFFFFFFFFu, st == 0)) {  // a predecessor has not published yet
+          if (st == 0) {
+            w = peek(state + t);
+            st = (w >> 34) == epoch ? ((w >> 32) & 3u) : 0u;
+          }
+        }
+        const unsigned pre = __ballot_sync(0xFFFFFFFFu, st == kPre);
+        const int stop = pre ? __ffs(pre) - 1 : 31;  // closest predecessor with a full prefix
+        uint32_t val = lane <= stop ? static_cast<uint32_t>(w) : 0u;
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    const int64_t i = base + k * kScanThreads + tid;
-    if (i < n) emit(i, v[k], pfx + ex[k]);
+        for (int off = 16; off > 0; off >>= 1) val += __shfl_xor_sync(0xFFFFFFFFu, val, off);
+        excl += val;
+        if (pre) break;
+        look -= 32;
+      }
+      if (lane == 0) {
+        publish(state + tile, epoch, kPre, excl + run);
+        tile_prefix = excl;
+      }
+    }
+    __syncthreads();
+    const uint32_t pfx = tile_prefix;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      const int64_t i = base + k * kScanThreads + tid;
+      if (i < n) emit(i, v[k], pfx + ex[k]);
+    }
+    if (total && tile == last_tile && tid == 0) *total = static_cast<int32_t>(pfx + run);
+    __syncthreads();  // warp_sum / tile_prefix are reused by the next tile
   }
-  if (total && tile == last_tile && tid == 0) *total = static_cast<int32_t>(pfx + run);
 }
 
 // launches the fused scan over n items (n >= 1) on stream s, kItems items per thread;
@@ -153,7 +154,7 @@ void lookback_scan(ScanTiles& st, int64_t n, ValueFn value, EmitFn emit, int32_t
     CUDA_CHECK(cudaMemsetAsync(st.state, 0, sizeof(uint64_t) * st.max_tiles, s));
     st.epoch = 1;
   }
-  lookback_scan_kernel<kItems><<<static_cast<int>(tiles), kScanThreads, 0, s>>>(
+  lookback_scan_kernel<kItems><<<mgr_grid(tiles), kScanThreads, 0, s>>>(
       n, value, emit, st.state, st.epoch, total, live);
   CUDA_LAUNCH_CHECK();
 }

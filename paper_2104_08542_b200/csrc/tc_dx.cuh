@@ -54,6 +54,7 @@ struct DxParams {
   float* Bsum;          // [rows] deferred FM coefficients (red.add)
   int F, d;
   int exp;              // experiment: 1 = no global reductions, 2 = no FM-sum loads
+  unsigned long long* cta_trace;  // profiling (nullable): per-CTA [start, end] globaltimer
 };
 
 // smem for the scatter epilogue: value tile [128 x 68] f32, vid [128 x F] u32, gz [128]
@@ -103,6 +104,7 @@ __global__ void __launch_bounds__(dx_threads<SCATTER>(), 1)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (p.cta_trace && threadIdx.x == 0) p.cta_trace[2 * blockIdx.x] = global_ns();
   const int t0 = static_cast<int>(static_cast<long long>(blockIdx.x) * p.tiles / gridDim.x);
   const int t1 = static_cast<int>(static_cast<long long>(blockIdx.x + 1) * p.tiles / gridDim.x);
 
@@ -342,6 +344,7 @@ __global__ void __launch_bounds__(dx_threads<SCATTER>(), 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (p.cta_trace && threadIdx.x == 0) p.cta_trace[2 * blockIdx.x + 1] = global_ns();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));

@@ -62,6 +62,7 @@ struct Params {
   // the MMAs, bit2 skip the A loads, bit3 skip the B loads
   int dbg = 0;
   long long* trace = nullptr;  // profiling: per-k-block clock64 stamps of CTA 0 (scratch only)
+  unsigned long long* cta_trace = nullptr;  // profiling: per-CTA [start, end] globaltimer
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -87,6 +88,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 
 __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {

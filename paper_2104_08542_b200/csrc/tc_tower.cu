@@ -12,7 +12,9 @@
 
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <mutex>
+#include <vector>
 
 #include "kernels.h"
 #include "tc_fused.cuh"
@@ -220,6 +222,55 @@ void launch_gemm(dim3 grid, const CUtensorMap& a, const CUtensorMap& alo, const 
   CUDA_LAUNCH_CHECK();
 }
 
+// SFCTR_CTA_TRACE=n: launch n of a call site records every CTA's [start, end] globaltimer
+// (ns); launch n + 20 prints the spread (first start .. last start, first end .. last end),
+// synchronising once (diagnostics: how late persistent CTAs start next to the manager stage)
+struct CtaTrace {
+  const char* name;
+  int launches = 0;
+  unsigned long long* buf = nullptr;
+  int grid = 0;
+  unsigned long long* arm(int g) {
+    static const int at = [] {
+      const char* e = std::getenv("SFCTR_CTA_TRACE");
+      return e ? atoi(e) : -1;
+    }();
+    const int i = launches++;
+    if (at < 0) return nullptr;
+    if (i == 0) CUDA_CHECK(cudaMalloc(&buf, sizeof(unsigned long long) * 2 * 1024));
+    if (i == at) {
+      grid = g;
+      return buf;
+    }
+    if (i == at + 20 && grid) {
+      std::vector<unsigned long long> h(2 * grid);
+      CUDA_CHECK(cudaDeviceSynchronize());  // the host runs steps ahead of the device
+      CUDA_CHECK(cudaMemcpy(h.data(), buf, sizeof(unsigned long long) * 2 * grid,
+                            cudaMemcpyDeviceToHost));
+      unsigned long long s0 = ~0ull, s1 = 0, e0 = ~0ull, e1 = 0;
+      for (int c = 0; c < grid; ++c) {
+        s0 = std::min(s0, h[2 * c]);
+        s1 = std::max(s1, h[2 * c]);
+        e0 = std::min(e0, h[2 * c + 1]);
+        e1 = std::max(e1, h[2 * c + 1]);
+      }
+      fprintf(stderr, "cta trace %s grid %d: start spread %.2f us, end spread %.2f us, span %.2f us\n",
+              name, grid, (s1 - s0) * 1e-3, (e1 - e0) * 1e-3, (e1 - s0) * 1e-3);
+      std::vector<double> st(grid);
+      for (int c = 0; c < grid; ++c) st[c] = (h[2 * c] - s0) * 1e-3;
+      std::vector<double> so = st;
+      std::sort(so.begin(), so.end());
+      fprintf(stderr, "  start pct (us) p10 %.2f p50 %.2f p75 %.2f p90 %.2f p95 %.2f max %.2f; late (>5us) CTAs:",
+              so[grid / 10], so[grid / 2], so[3 * grid / 4], so[9 * grid / 10], so[19 * grid / 20],
+              so[grid - 1]);
+      for (int c = 0; c < grid; ++c)
+        if (st[c] > 5) fprintf(stderr, " %d(%.1f,dur %.1f)", c, st[c], (h[2 * c + 1] - h[2 * c]) * 1e-3);
+      fprintf(stderr, "\n");
+    }
+    return nullptr;
+  }
+};
+
 template <bool A_MN, bool B_MN>
 void launch_ts_gemm(dim3 grid, const CUtensorMap& a, const CUtensorMap& bhi,
                     const CUtensorMap& blo, const tc::Params& p, cudaStream_t s) {
@@ -249,6 +300,9 @@ void launch_ts_gemm(dim3 grid, const CUtensorMap& a, const CUtensorMap& bhi,
     CUDA_CHECK(cudaMemsetAsync(tr, 0, sizeof(long long) * 320, s));
     q.trace = tr;
   }
+  const int items = static_cast<int>(grid.x * grid.y * grid.z);
+  static CtaTrace ct{A_MN ? "gemm3" : "gemm1"};
+  q.cta_trace = ct.arm(items);
   launch_pdl(kern, grid, dim3(tc::kTsThreads), smem, s, a, bhi, blo, q);
   CUDA_LAUNCH_CHECK();
   if (tr) {
@@ -317,6 +371,8 @@ void launch_dx_gemm(const TowerTC& tc_, const float* dh_hi, const float* dh_lo, 
       CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       configured = smem;
     }
+    static CtaTrace ct{"gemm2"};
+    p.cta_trace = ct.arm(grid);
     launch_pdl(kern, dim3(grid), dim3(tc::dx_threads<true>()), smem, s, ah, al, bh, bl, bh, p);
     CUDA_LAUNCH_CHECK();
     return;

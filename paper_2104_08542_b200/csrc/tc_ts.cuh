@@ -106,15 +106,18 @@ __global__ void __launch_bounds__(kTsThreads, 1)
   auto b_lo = [&](int s) { return b_ring + s * L::B_STAGE + L::B_PART; };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
-  const int kb0 = blockIdx.z * p.k_blocks_per_split;
+  const int bx = blockIdx.x, by = blockIdx.y, bz = blockIdx.z;
+  const int m0 = bx * BM, n0 = by * BN;
+  const int kb0 = bz * p.k_blocks_per_split;
   const int kb1 = min(p.num_k_blocks, kb0 + p.k_blocks_per_split);
   const int nkb = kb1 - kb0;
   // CTAs sharing a B tile start at different k-blocks so they do not all read
   // the same L2 lines at the same moment
-  const int rot = nkb > 0 ? static_cast<int>((blockIdx.x * 5u) % static_cast<unsigned>(nkb)) : 0;
+  const int rot = nkb > 0 ? static_cast<int>((bx * 5u) % static_cast<unsigned>(nkb)) : 0;
   auto kblk = [&](int i) { const int j = i + rot; return kb0 + (j >= nkb ? j - nkb : j); };
-  const bool tr = p.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+  const bool tr = p.trace && bx == 0 && by == 0 && bz == 0;
+  const int cta = (bz * gridDim.y + by) * gridDim.x + bx;
+  if (p.cta_trace && threadIdx.x == 0) p.cta_trace[2 * cta] = global_ns();
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < RA; ++s) {
@@ -299,7 +302,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
       for (int r = w2; r < BM; r += 8) {
         const int m = m0 + r;
         if (m >= p.M) break;
-        float* o = p.out + blockIdx.z * p.split_stride + static_cast<long long>(m) * p.ldo;
+        float* o = p.out + bz * p.split_stride + static_cast<long long>(m) * p.ldo;
 #pragma unroll
         for (int c = lane; c < BN; c += 32) {
           const int n = n0 + c;
@@ -310,6 +313,7 @@ __global__ void __launch_bounds__(kTsThreads, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (p.cta_trace && threadIdx.x == 0) p.cta_trace[2 * cta + 1] = global_ns();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));

@@ -45,10 +45,12 @@ __global__ void fill_u32_kernel(uint32_t* p, int64_t n, uint32_t v) {
 // which removes the contended atomics on hot ids.
 __global__ void vsi_first_kernel(const uint32_t* __restrict__ ids, int64_t n,
                                  uint32_t* __restrict__ first) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= n) return;
-  const uint32_t f = __ldg(ids + i);
-  if (__ldcg(first + f) > static_cast<uint32_t>(i)) atomicMin(first + f, static_cast<uint32_t>(i));
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t f = __ldg(ids + i);
+    if (__ldcg(first + f) > static_cast<uint32_t>(i))
+      atomicMin(first + f, static_cast<uint32_t>(i));
+  }
 }
 
 constexpr uint32_t kTag = 0x80000000u;
@@ -74,8 +76,9 @@ struct VsiEmit {
 
 __global__ void vsi_vid_kernel(const uint32_t* __restrict__ ids, int64_t n,
                                const uint32_t* __restrict__ first, uint32_t* __restrict__ vids) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i < n) vids[i] = __ldcg(first + __ldg(ids + i)) & ~kTag;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    vids[i] = __ldcg(first + __ldg(ids + i)) & ~kTag;
 }
 
 // ---- hashed path (arbitrary u64 ids, or u32 ids with an L2-resident table) ----
@@ -98,12 +101,15 @@ template <typename KeyT, typename IdT>
 __global__ void vsi_hash_insert_kernel(const IdT* __restrict__ ids, int64_t n,
                                        KeyT* __restrict__ keys, uint32_t* __restrict__ pos,
                                        uint64_t mask, uint32_t* __restrict__ hslot) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const int lane = threadIdx.x & 31;
+  // grid-stride in warp-aligned steps (the ballot / match below need whole warps)
+  for (int64_t i0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) & ~31ll;
+       i0 < n; i0 += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  const int64_t i = i0 + lane;
   const bool live = i < n;
   const KeyT f = live ? static_cast<KeyT>(ids[i]) : hash_empty<KeyT>();
   const unsigned act = __ballot_sync(0xFFFFFFFFu, live);
-  if (!live) return;
+  if (!live) continue;
   const unsigned peers = __match_any_sync(act, f);
   const int leader = __ffs(peers) - 1;  // the group's smallest position
   uint32_t slot = 0;
@@ -127,6 +133,7 @@ __global__ void vsi_hash_insert_kernel(const IdT* __restrict__ ids, int64_t n,
   }
   slot = __shfl_sync(act, slot, leader);
   hslot[i] = slot;
+  }
 }
 struct VsiHashFlag {
   const uint32_t* hslot;
@@ -152,8 +159,9 @@ struct VsiHashEmit {
 };
 __global__ void vsi_hash_vid_kernel(const uint32_t* __restrict__ hslot, int64_t n,
                                     const uint32_t* __restrict__ pos, uint32_t* __restrict__ vids) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i < n) vids[i] = __ldcg(pos + __ldg(hslot + i)) & ~kTag;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    vids[i] = __ldcg(pos + __ldg(hslot + i)) & ~kTag;
 }
 template <typename KeyT>
 __global__ void vsi_hash_reset_kernel(const uint32_t* __restrict__ uslot,
@@ -178,14 +186,15 @@ __global__ void vsi_reset_kernel(const uint32_t* __restrict__ gids,
 
 __global__ void ids_to_u32_kernel(const uint64_t* __restrict__ in, uint32_t* __restrict__ out,
                                   int64_t n, uint64_t limit, int32_t* bad) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= n) return;
-  const uint64_t v = in[i];
-  if (v >= limit) {
-    *bad = 1;
-    out[i] = 0;
-  } else {
-    out[i] = static_cast<uint32_t>(v);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t v = in[i];
+    if (v >= limit) {
+      *bad = 1;
+      out[i] = 0;
+    } else {
+      out[i] = static_cast<uint32_t>(v);
+    }
   }
 }
 
@@ -276,7 +285,7 @@ void vsi_device(VsiScratch& v, const uint32_t* d_ids, int64_t n, uint32_t* d_gid
                 uint32_t* d_vids, int32_t* d_unique, cudaStream_t s, bool reset) {
   SFB_CHECK(n > 0 && n <= v.cap, "vsi batch exceeds scratch capacity");
   SFB_CHECK(v.key_space > 0, "direct-mapped VSI needs a key space");
-  const int grid = ceil_div(n, 256);
+  const int grid = mgr_grid(ceil_div(n, 256));  // manager stage: capped, grid-stride kernels
   if (v.hashed32) {  // L2-resident hashed table; always reset behind the batch
     vsi_hash_insert_kernel<uint32_t, uint32_t><<<grid, 256, 0, s>>>(d_ids, n, v.d_hkeys32,
                                                                     v.d_first, v.hmask, v.d_hslot);
@@ -286,7 +295,7 @@ void vsi_device(VsiScratch& v, const uint32_t* d_ids, int64_t n, uint32_t* d_gid
                      d_unique, s);
     vsi_hash_vid_kernel<<<grid, 256, 0, s>>>(v.d_hslot, n, v.d_first, d_vids);
     CUDA_LAUNCH_CHECK();
-    vsi_hash_reset_kernel<uint32_t><<<std::min(grid, num_sms() * 8), 256, 0, s>>>(
+    vsi_hash_reset_kernel<uint32_t><<<grid, 256, 0, s>>>(
         v.d_uslot, d_unique, v.d_hkeys32, v.d_first);
     CUDA_LAUNCH_CHECK();
     return;
@@ -298,7 +307,7 @@ void vsi_device(VsiScratch& v, const uint32_t* d_ids, int64_t n, uint32_t* d_gid
   vsi_vid_kernel<<<grid, 256, 0, s>>>(d_ids, n, v.d_first, d_vids);
   CUDA_LAUNCH_CHECK();
   if (reset) {
-    vsi_reset_kernel<<<std::min(grid, num_sms() * 8), 256, 0, s>>>(d_gids, d_unique, v.d_first);
+    vsi_reset_kernel<<<grid, 256, 0, s>>>(d_gids, d_unique, v.d_first);
     CUDA_LAUNCH_CHECK();
   }
 }
@@ -307,7 +316,7 @@ void vsi_device_hashed(VsiScratch& v, const uint64_t* d_ids, int64_t n, uint64_t
                        uint32_t* d_vids, int32_t* d_unique, cudaStream_t s) {
   SFB_CHECK(n > 0 && n <= v.cap, "vsi batch exceeds scratch capacity");
   SFB_CHECK(v.key_space == 0, "hashed VSI needs a context created with key_space 0");
-  const int grid = ceil_div(n, 256);
+  const int grid = mgr_grid(ceil_div(n, 256));
   vsi_hash_insert_kernel<unsigned long long, uint64_t><<<grid, 256, 0, s>>>(
       d_ids, n, v.d_hkeys, v.d_first, v.hmask, v.d_hslot);
   CUDA_LAUNCH_CHECK();
@@ -316,7 +325,7 @@ void vsi_device_hashed(VsiScratch& v, const uint64_t* d_ids, int64_t n, uint64_t
                    d_unique, s);
   vsi_hash_vid_kernel<<<grid, 256, 0, s>>>(v.d_hslot, n, v.d_first, d_vids);
   CUDA_LAUNCH_CHECK();
-  vsi_hash_reset_kernel<unsigned long long><<<std::min(grid, num_sms() * 8), 256, 0, s>>>(
+  vsi_hash_reset_kernel<unsigned long long><<<grid, 256, 0, s>>>(
       v.d_uslot, d_unique, v.d_hkeys, v.d_first);
   CUDA_LAUNCH_CHECK();
 }
@@ -324,7 +333,7 @@ void vsi_device_hashed(VsiScratch& v, const uint64_t* d_ids, int64_t n, uint64_t
 void ids_to_u32(const uint64_t* d_in, uint32_t* d_out, int64_t n, uint64_t limit, int32_t* d_bad,
                 cudaStream_t s) {
   if (n <= 0) return;
-  ids_to_u32_kernel<<<ceil_div(n, 256), 256, 0, s>>>(d_in, d_out, n, limit, d_bad);
+  ids_to_u32_kernel<<<mgr_grid(ceil_div(n, 256)), 256, 0, s>>>(d_in, d_out, n, limit, d_bad);
   CUDA_LAUNCH_CHECK();
 }
 
