@@ -107,19 +107,27 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
   CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   // the training stage is the step's critical path: in pipelined mode its CTAs are
   // scheduled ahead of the manager stage's (which only has to finish within the step)
-  CUDA_CHECK(cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking,
-                                          pipelined_ ? prio_hi : prio_lo));
+  // SFCTR_STREAM_PRIO (experiment): "train" (default) = training stream high, manager low;
+  // "same" = both low; "manager" = manager high, training low
+  int prio_train = pipelined_ ? prio_hi : prio_lo, prio_mgr = prio_lo;
+  if (const char* e = std::getenv("SFCTR_STREAM_PRIO")) {
+    if (std::string(e) == "same") prio_train = prio_lo;
+    if (std::string(e) == "manager" && pipelined_) {
+      prio_train = prio_lo;
+      prio_mgr = prio_hi;
+    }
+  }
+  CUDA_CHECK(cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking, prio_train));
   if (const char* e = std::getenv("SFCTR_NO_FREE_STEPS")) no_free_steps_ = e[0] == '1';
   if (const char* e = std::getenv("SFCTR_NO_UPDATE_FORK")) no_update_fork_ = e[0] == '1';
-  CUDA_CHECK(cudaStreamCreateWithPriority(&ustream_, cudaStreamNonBlocking,
-                                          pipelined_ ? prio_hi : prio_lo));
+  CUDA_CHECK(cudaStreamCreateWithPriority(&ustream_, cudaStreamNonBlocking, prio_train));
   CUDA_CHECK(cudaEventCreateWithFlags(&dx_done_, cudaEventDisableTiming));
   CUDA_CHECK(cudaEventCreateWithFlags(&upd_done_, cudaEventDisableTiming));
   CUDA_CHECK(cudaMalloc(&d_err_, sizeof(int32_t) * 4));
   CUDA_CHECK(cudaMemset(d_err_, 0, sizeof(int32_t) * 4));
   mstream_ = stream_;
   if (pipelined_) {
-    CUDA_CHECK(cudaStreamCreateWithPriority(&mstream_, cudaStreamNonBlocking, prio_lo));
+    CUDA_CHECK(cudaStreamCreateWithPriority(&mstream_, cudaStreamNonBlocking, prio_mgr));
     CUDA_CHECK(cudaStreamCreateWithFlags(&cstream_, cudaStreamNonBlocking));
     for (auto& e : in_ready_) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
@@ -274,6 +282,11 @@ Trainer::Trainer(const sfctr_config& cfg, int rank, int world, const uint8_t* nc
 
 Trainer::~Trainer() {
   cudaSetDevice(dev_);
+  try {
+    dump_stamps();
+  } catch (...) {
+  }
+  if (d_stamps_) cudaFree(d_stamps_);
   if (mstream_) cudaStreamSynchronize(mstream_);
   if (stream_) cudaStreamSynchronize(stream_);
   for (auto& l : lane_) l.release();
@@ -471,6 +484,19 @@ __global__ void zero_rows_kernel(float4* __restrict__ p, const int32_t* __restri
 }  // namespace
 
 namespace {
+// SFCTR_STEP_TRACE=n: globaltimer stamps of the last n steps' stage boundaries (diagnostics)
+__global__ void stamp_kernel(unsigned long long* p) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *p = t;
+}
+int step_trace_n() {
+  static const int n = [] {
+    const char* e = std::getenv("SFCTR_STEP_TRACE");
+    return e ? std::max(0, std::atoi(e)) : 0;
+  }();
+  return n;
+}
 // phase pass only: hold the stream for `ns` so the host enqueues the whole step behind it and
 // every phase time is device time, not the host's issue time (SFCTR_PHASE_GATE_US)
 __global__ void phase_gate_kernel(uint64_t ns) {
@@ -489,6 +515,42 @@ uint64_t phase_gate_ns() {
   return ns;
 }
 }  // namespace
+
+void Trainer::stamp(int64_t step, int slot, cudaStream_t s) {
+  const int n = step_trace_n();
+  if (n <= 0) return;
+  if (!d_stamps_) {
+    CUDA_CHECK(cudaMalloc(&d_stamps_, sizeof(unsigned long long) * 4 * n));
+    CUDA_CHECK(cudaMemset(d_stamps_, 0, sizeof(unsigned long long) * 4 * n));
+  }
+  stamp_kernel<<<1, 1, 0, s>>>(d_stamps_ + (step % n) * 4 + slot);
+  CUDA_CHECK(cudaGetLastError());
+  last_stamped_ = step;
+}
+
+void Trainer::dump_stamps() {
+  const int n = step_trace_n();
+  if (n <= 0 || !d_stamps_) return;
+  std::vector<unsigned long long> h(4 * n);
+  CUDA_CHECK(cudaDeviceSynchronize());
+  CUDA_CHECK(cudaMemcpy(h.data(), d_stamps_, sizeof(unsigned long long) * 4 * n,
+                        cudaMemcpyDeviceToHost));
+  // steps last_stamped_ - n + 1 .. last_stamped_, in order
+  fprintf(stderr, "step trace (us, rel. to the first manager start): step mgr_start mgr_end "
+                  "train_start train_end | train_wait_for_mgr train_gap_after_prev\n");
+  const int64_t first = std::max<int64_t>(0, last_stamped_ - n + 1);
+  const unsigned long long t0 = h[(first % n) * 4];
+  unsigned long long prev_end = 0;
+  for (int64_t st = first; st <= last_stamped_; ++st) {
+    const unsigned long long* r = h.data() + (st % n) * 4;
+    auto us = [&](unsigned long long t) { return t ? (static_cast<double>(t) - t0) * 1e-3 : -1.0; };
+    fprintf(stderr, "%5lld %9.1f %9.1f %9.1f %9.1f | %7.1f %7.1f\n", static_cast<long long>(st),
+            us(r[0]), us(r[1]), us(r[2]), us(r[3]),
+            r[2] > r[1] ? (static_cast<double>(r[2]) - r[1]) * 1e-3 : 0.0,
+            prev_end && r[2] > prev_end ? (static_cast<double>(r[2]) - prev_end) * 1e-3 : 0.0);
+    prev_end = r[3];
+  }
+}
 
 void Trainer::phase(const char* name, cudaStream_t s) {
   if (!timing_) return;
@@ -612,6 +674,7 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
   }
   phase("start", sm);
   if (sm != sw) phase("start", sw);
+  stamp(step, 0, sm);
   {  // per-step fields restart, running totals carry over
     sfctr_step_stats next{};
     next.total_steps = stats_.total_steps;
@@ -844,6 +907,7 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
   else if (xdev)
     xch_.zero_local_dev(d_dG_, sm, d_ % 4 == 0 && !tower_fused_ ? d_B_ : nullptr);
   phase("manage_evict_admit", sm);
+  stamp(step, 1, sm);
   if (sm != sw) {
     CUDA_CHECK(cudaEventRecord(prep_done_[k], sm));
     prep_recorded_[k] = true;
@@ -877,6 +941,7 @@ void Trainer::train(int64_t step, const uint8_t* d_labels, float* d_loss) {
   auto snap_cnt = [&](int l) { return snap + 1 + kCntWords * l; };
   prep_.step = -1;
   if (sm != sw) CUDA_CHECK(cudaStreamWaitEvent(sw, prep_done_[k]));
+  stamp(step, 2, sw);
   (void)t;
 
   // ==== training stage (stream sw) ====
@@ -1147,6 +1212,7 @@ void Trainer::train(int64_t step, const uint8_t* d_labels, float* d_loss) {
     w1_split_ready_ = a.w_hi != nullptr;
   }
   phase("dense_adam", s);
+  stamp(step, 3, s);
   if (pipelined_) {
     CUDA_CHECK(cudaEventRecord(train_done_[k], sw));
     train_pending_[k] = true;

@@ -190,6 +190,11 @@ class Trainer {
   // SFCTR_SHARD_MANAGER=0 keeps the replicated stage)
   ShardPlan shard_;
   bool sharded_ = false;
+  // SFCTR_STEP_TRACE diagnostics: stage-boundary stamps, printed at destruction
+  unsigned long long* d_stamps_ = nullptr;
+  int64_t last_stamped_ = -1;
+  void stamp(int64_t step, int slot, cudaStream_t s);
+  void dump_stamps();
   int32_t* h_totals_ = nullptr;   // pinned [16] exchange plan totals
   int ldx_ = 0;
   bool tower_simt_ = false;
