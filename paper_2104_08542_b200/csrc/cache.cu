@@ -55,6 +55,7 @@ struct OwnedEmit {
 __global__ void own_all_kernel(const int32_t* __restrict__ U_ptr, uint32_t* __restrict__ own_k,
                                int32_t* __restrict__ count, const uint32_t* __restrict__ gids,
                                uint32_t* __restrict__ first) {
+  pdl_wait();
   const int32_t U = *U_ptr;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < U; j += gridDim.x * blockDim.x) {
     own_k[j] = static_cast<uint32_t>(j);
@@ -113,6 +114,7 @@ __global__ void mark_window_kernel(const uint32_t* __restrict__ gids,
                                    uint32_t w, const uint32_t* __restrict__ index, uint32_t C,
                                    int32_t t, int32_t* __restrict__ mark,
                                    int32_t* __restrict__ marked) {
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= cap || i >= *U_ptr) return;
   const uint32_t f = gids[i];
@@ -137,6 +139,7 @@ __global__ void __launch_bounds__(1024) lru_hist_kernel(
     uint32_t C, const uint32_t* __restrict__ slot_feat, const int32_t* __restrict__ mark, int32_t t,
     const int32_t* __restrict__ last_use, uint32_t* __restrict__ hist, int nbins, int shift,
     int32_t* __restrict__ cnt, int base_shift, bool level2, const uint8_t* __restrict__ pin) {
+  pdl_wait();
   __shared__ uint32_t sh[kHistBins];
   __shared__ uint32_t old_blk;
   for (int i = threadIdx.x; i < nbins; i += blockDim.x) sh[i] = 0;
@@ -209,6 +212,7 @@ __global__ void __launch_bounds__(1024) lru_select_kernel(const uint32_t* __rest
                                                           int32_t nbins, int32_t n_evict,
                                                           int32_t* __restrict__ cnt, int shift,
                                                           bool level2) {
+  pdl_wait();
   __shared__ uint64_t part[1024];
   __shared__ int32_t found;
   __shared__ uint64_t found_below;
@@ -268,6 +272,7 @@ __global__ void lru_collect_kernel(uint32_t C, const uint32_t* __restrict__ slot
                                    int32_t* __restrict__ cnt, int64_t cap,
                                    uint64_t* __restrict__ keys, uint32_t* __restrict__ ids,
                                    const uint8_t* __restrict__ pin) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int32_t T = cnt[kCntSelT];
   const uint64_t C4 = (static_cast<uint64_t>(C) + 3) >> 2;
@@ -341,6 +346,7 @@ __global__ void evict_kernel(int32_t n_evict, const uint64_t* __restrict__ sorte
                              uint32_t* __restrict__ slot_host, int32_t* __restrict__ host_next,
                              uint32_t* __restrict__ index, uint32_t* __restrict__ free_stack,
                              const int32_t* __restrict__ free_top_ptr, int32_t* __restrict__ err) {
+  pdl_wait();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= n_evict) return;
@@ -400,6 +406,7 @@ __global__ void admit_kernel(const int32_t* __restrict__ counters, int32_t n_evi
                              uint64_t* __restrict__ admit_seq,
                              int32_t* __restrict__ mark, int32_t t,
                              uint32_t* __restrict__ own_slot, int32_t* __restrict__ n_from_host) {
+  pdl_wait();
   const int32_t n_work = counters[kCntWorking];
   const int32_t free_top = counters[kCntFreeTop] + n_evict;
   const uint64_t seq0 = *reinterpret_cast<const uint64_t*>(counters + kCntSeq);
@@ -502,6 +509,7 @@ __global__ void __launch_bounds__(256) swap_kernel(
     int32_t* __restrict__ last_use, uint64_t* __restrict__ admit_seq,
     int32_t* __restrict__ mark, int32_t t, uint32_t* __restrict__ own_slot,
     int32_t* __restrict__ n_from_host, int32_t* __restrict__ err) {
+  pdl_wait();
   __shared__ __align__(128) float4 wb_stage[8][64];   // per warp: the victim row (<= 64 chunks)
   __shared__ __align__(128) float4 adm_stage[8][64];  // per warp: the refilled host row
   __shared__ __align__(8) uint64_t adm_bar[8];
@@ -641,6 +649,7 @@ __global__ void init_lane_kernel(uint32_t C, uint32_t* slot_feat, int32_t* last_
 
 // device free-stack height and admit_seq after this step's evictions and admissions
 __global__ void advance_kernel(int32_t* counters, int32_t n_evict) {
+  pdl_wait();
   const int32_t n_work = counters[kCntWorking];
   counters[kCntFreeTop] += n_evict - n_work;
   *reinterpret_cast<uint64_t*>(counters + kCntSeq) += static_cast<uint64_t>(n_work);
@@ -863,8 +872,7 @@ void CacheLane::select_owned(const uint32_t* d_gids, const int32_t* d_U, int32_t
                              uint32_t w, uint32_t* vsi_first, cudaStream_t s) {
   if (cap <= 0) return;
   if (W == 1) {  // a single worker owns every unique: own_k = identity, count = U
-    own_all_kernel<<<mgr_grid(ceil_div(cap, 256)), 256, 0, s>>>(
-        d_U, own_k, counters + kCntOwned, d_gids, vsi_first);
+    launch_pdl(own_all_kernel, dim3(mgr_grid(ceil_div(cap, 256))), dim3(256), 0, s, d_U, own_k, counters + kCntOwned, d_gids, vsi_first);
     CUDA_LAUNCH_CHECK();
     return;
   }
@@ -875,7 +883,7 @@ void CacheLane::select_owned(const uint32_t* d_gids, const int32_t* d_U, int32_t
 void CacheLane::mark_window(const uint32_t* d_gids, const int32_t* d_U, int32_t cap, uint32_t W,
                             uint32_t w, int32_t t, cudaStream_t s) {
   if (cap <= 0) return;
-  mark_window_kernel<<<ceil_div(cap, 256), 256, 0, s>>>(d_gids, d_U, cap, W, w, index,
+  launch_pdl(mark_window_kernel, dim3(ceil_div(cap, 256)), dim3(256), 0, s, d_gids, d_U, cap, W, w, index,
                                                         static_cast<uint32_t>(C), t, mark,
                                                         counters + kCntMarked);
   CUDA_LAUNCH_CHECK();
@@ -899,17 +907,17 @@ void CacheLane::victim_select(int32_t t, int32_t n_evict, cudaStream_t s, const 
   CUDA_CHECK(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 2 * kHistBins, s));
   CUDA_CHECK(cudaMemsetAsync(counters + kCntOld, 0, sizeof(int32_t), s));
   const int grid = std::max(1, std::min<int>(ceil_div(static_cast<int64_t>(C), 16384), 2 * num_sms()));
-  lru_hist_kernel<<<grid, 1024, 0, s>>>(static_cast<uint32_t>(C), slot_feat, mark, t, last_use,
+  launch_pdl(lru_hist_kernel, dim3(grid), dim3(1024), 0, s, static_cast<uint32_t>(C), slot_feat, mark, t, last_use,
                                         hist, nb1, shift, counters, 0, false, pinned);
   CUDA_LAUNCH_CHECK();
-  lru_select_kernel<<<1, 1024, 0, s>>>(hist, nb1, n_evict, counters, shift, false);
+  launch_pdl(lru_select_kernel, dim3(1), dim3(1024), 0, s, hist, nb1, n_evict, counters, shift, false);
   CUDA_LAUNCH_CHECK();
   if (shift > 0) {  // level 2: the 2^shift steps of the coarse bin, exactly
-    lru_hist_kernel<<<grid, 1024, 0, s>>>(static_cast<uint32_t>(C), slot_feat, mark, t, last_use,
+    launch_pdl(lru_hist_kernel, dim3(grid), dim3(1024), 0, s, static_cast<uint32_t>(C), slot_feat, mark, t, last_use,
                                           hist + kHistBins, 1 << shift, 0, counters, shift, true,
                                           pinned);
     CUDA_LAUNCH_CHECK();
-    lru_select_kernel<<<1, 1024, 0, s>>>(hist + kHistBins, 1 << shift, n_evict, counters, shift,
+    launch_pdl(lru_select_kernel, dim3(1), dim3(1024), 0, s, hist + kHistBins, 1 << shift, n_evict, counters, shift,
                                          true);
     CUDA_LAUNCH_CHECK();
   }
@@ -919,7 +927,7 @@ void CacheLane::victim_sort(int32_t t, int32_t n_evict, cudaStream_t s, const ui
   const int64_t bound = std::min<int64_t>(cand_cap, static_cast<int64_t>(n_evict) + umax);
   CUDA_CHECK(cudaMemsetAsync(keys, 0xFF, sizeof(uint64_t) * bound, s));
   const int grid = static_cast<int>(std::min<int64_t>(ceil_div(static_cast<int64_t>(C), 1024), num_sms() * 8));
-  lru_collect_kernel<<<grid, 256, 0, s>>>(static_cast<uint32_t>(C), slot_feat, mark, t, last_use,
+  launch_pdl(lru_collect_kernel, dim3(grid), dim3(256), 0, s, static_cast<uint32_t>(C), slot_feat, mark, t, last_use,
                                           admit_seq, counters, bound, keys, ids, pinned);
   CUDA_LAUNCH_CHECK();
   sort_pairs_u64_u32(temp, sort_bytes, keys, keys_sorted, ids, ids_sorted, bound, 64, s);
@@ -930,8 +938,7 @@ void CacheLane::evict(int32_t n_evict, uint32_t W, int32_t t, cudaStream_t s, bo
   if (n_evict <= 0) return;
   if (!selected) victim_select(t, n_evict, s, pinned);
   victim_sort(t, n_evict, s, pinned);
-  evict_kernel<<<ceil_div(static_cast<int64_t>(n_evict) * 32, 256), 256, 0, s>>>(
-      n_evict, keys_sorted, ids_sorted, slot_feat, W, d, emb, mom, vel, steps, host.tab(),
+  launch_pdl(evict_kernel, dim3(ceil_div(static_cast<int64_t>(n_evict) * 32, 256)), dim3(256), 0, s, n_evict, keys_sorted, ids_sorted, slot_feat, W, d, emb, mom, vel, steps, host.tab(),
       slot_host, counters + kCntHostNext, index, free_stack, counters + kCntFreeTop,
       counters + kCntError);
   CUDA_LAUNCH_CHECK();
@@ -955,28 +962,26 @@ void CacheLane::evict_admit(int32_t n_evict, int32_t n_work, uint32_t W, uint64_
   hook("evict_select");
   victim_sort(t, n_evict, s, pinned);
   hook("evict_sort");
-  swap_kernel<<<ceil_div(static_cast<int64_t>(n_work) * 32, 256), 256, 0, s>>>(
-      counters, n_evict, keys_sorted, ids_sorted, work_j, work_f, work_w, W, d / 4, free_stack,
+  launch_pdl(swap_kernel, dim3(ceil_div(static_cast<int64_t>(n_work) * 32, 256)), dim3(256), 0, s, counters, n_evict, keys_sorted, ids_sorted, work_j, work_f, work_w, W, d / 4, free_stack,
       index, host.tab(), slot_host, counters + kCntHostNext, seed, fnv1a64("embed"),
       reinterpret_cast<float4*>(emb), reinterpret_cast<float4*>(mom),
       reinterpret_cast<float4*>(vel), steps, slot_feat, last_use, admit_seq, mark, t, own_slot,
       counters + kCntFromHost, counters + kCntError);
   CUDA_LAUNCH_CHECK();
-  advance_kernel<<<1, 1, 0, s>>>(counters, n_evict);
+  launch_pdl(advance_kernel, dim3(1), dim3(1), 0, s, counters, n_evict);
   CUDA_LAUNCH_CHECK();
 }
 
 void CacheLane::admit(int32_t n_bound, int32_t n_evict, uint32_t W, uint64_t seed, int32_t t,
                       cudaStream_t s) {
   if (n_bound > 0) {
-    admit_kernel<<<mgr_grid(ceil_div(ceil_div(static_cast<int64_t>(n_bound), kAdmitRows) * 32, 256)),
-                   256, 0, s>>>(counters, n_evict, work_j, work_f, work_w, W, d, free_stack, index,
+    launch_pdl(admit_kernel, dim3(mgr_grid(ceil_div(ceil_div(static_cast<int64_t>(n_bound), kAdmitRows) * 32, 256))), dim3(256), 0, s, counters, n_evict, work_j, work_f, work_w, W, d, free_stack, index,
                         host.tab(), slot_host, seed, fnv1a64("embed"), emb, mom, vel, steps,
                         slot_feat, last_use, admit_seq, mark, t, own_slot,
                         counters + kCntFromHost);
     CUDA_LAUNCH_CHECK();
   }
-  advance_kernel<<<1, 1, 0, s>>>(counters, n_evict);
+  launch_pdl(advance_kernel, dim3(1), dim3(1), 0, s, counters, n_evict);
   CUDA_LAUNCH_CHECK();
 }
 
@@ -1053,11 +1058,10 @@ void CacheLane::evict_list(const uint64_t* d_feats, int32_t n, uint32_t W, cudaS
   evict_list_prep_kernel<<<ceil_div(n, 256), 256, 0, s>>>(d_feats, n, W, index, keys_sorted,
                                                           ids_sorted, counters);
   CUDA_LAUNCH_CHECK();
-  evict_kernel<<<ceil_div(static_cast<int64_t>(n) * 32, 256), 256, 0, s>>>(
-      n, keys_sorted, ids_sorted, slot_feat, W, d, emb, mom, vel, steps, host.tab(), slot_host,
+  launch_pdl(evict_kernel, dim3(ceil_div(static_cast<int64_t>(n) * 32, 256)), dim3(256), 0, s, n, keys_sorted, ids_sorted, slot_feat, W, d, emb, mom, vel, steps, host.tab(), slot_host,
       counters + kCntHostNext, index, free_stack, counters + kCntFreeTop, counters + kCntError);
   CUDA_LAUNCH_CHECK();
-  advance_kernel<<<1, 1, 0, s>>>(counters, n);
+  launch_pdl(advance_kernel, dim3(1), dim3(1), 0, s, counters, n);
   CUDA_LAUNCH_CHECK();
 }
 

@@ -20,6 +20,7 @@ __global__ void gather_cache_v4(const uint32_t* __restrict__ own_k,
                                 const int32_t* __restrict__ n_ptr, int32_t n_bound, int d4,
                                 const float4* __restrict__ emb, float4* __restrict__ G,
                                 float4* __restrict__ dG_zero, float* __restrict__ B_zero) {
+  pdl_wait();
   const int32_t n_own = n_ptr ? *n_ptr : n_bound;
   const int64_t n = static_cast<int64_t>(n_own) * d4;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -36,6 +37,7 @@ __global__ void gather_cache_v4(const uint32_t* __restrict__ own_k,
 // one worker without a materialised G: only dG[0:U) and B[0:U) need clearing
 __global__ void zero_rows_b_kernel(const int32_t* __restrict__ n_ptr, int d4,
                                    float4* __restrict__ dG, float* __restrict__ B) {
+  pdl_wait();
   const int64_t n = static_cast<int64_t>(*n_ptr) * d4;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -70,6 +72,7 @@ __global__ void __launch_bounds__(256, 5) gather_instances_v4(
     const uint32_t* __restrict__ vid, int32_t rows, int F, int d4, const float4* __restrict__ G,
     float4* __restrict__ X, float4* __restrict__ fm_s, float* __restrict__ fm_sqp,
     const uint32_t* __restrict__ slot_of, int g4) {
+  pdl_wait();
   // g4: row stride of G in float4 (d/4 for a common table, 3d/4 for the cache rows)
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const int64_t p = i >> 1;
@@ -260,6 +263,7 @@ __global__ void sparse_adam_v4(const uint32_t* __restrict__ own_k,
                                const float* __restrict__ bc2, float lr, float b1, float b2,
                                float omb1, float omb2, float eps, const float* __restrict__ Bsum,
                                float fm_scale) {
+  pdl_wait();
   const int32_t n_own = n_ptr ? *n_ptr : n_bound;
   const int64_t n = static_cast<int64_t>(n_own) * d4;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -314,7 +318,7 @@ void gather_cache(const uint32_t* own_k, const uint32_t* own_slot, int32_t n_own
   if (n_own <= 0) return;
   if ((d & 3) == 0) {
     const int64_t n = static_cast<int64_t>(n_own) * (d / 4);
-    gather_cache_v4<<<wave_grid(n), 256, 0, s>>>(own_k, own_slot, d_n_own, n_own, d / 4,
+    launch_pdl(gather_cache_v4, dim3(wave_grid(n)), dim3(256), 0, s, own_k, own_slot, d_n_own, n_own, d / 4,
                                                      reinterpret_cast<const float4*>(emb),
                                                      reinterpret_cast<float4*>(G),
                                                      reinterpret_cast<float4*>(dG_zero), B_zero);
@@ -329,8 +333,7 @@ void zero_rows_b(const int32_t* d_n, int32_t n_bound, int d, float* dG, float* B
   SFB_CHECK((d & 3) == 0, "zero_rows_b needs d % 4 == 0");
   if (n_bound <= 0) return;
   // manager stage: a capped grid (mgr_grid), not a full wave of resident CTAs
-  zero_rows_b_kernel<<<mgr_grid(ceil_div(static_cast<int64_t>(n_bound) * (d / 4), 256)), 256, 0, s>>>(
-      d_n, d / 4, reinterpret_cast<float4*>(dG), B);
+  launch_pdl(zero_rows_b_kernel, dim3(mgr_grid(ceil_div(static_cast<int64_t>(n_bound) * (d / 4), 256))), dim3(256), 0, s, d_n, d / 4, reinterpret_cast<float4*>(dG), B);
   CUDA_LAUNCH_CHECK();
 }
 
@@ -341,8 +344,7 @@ void gather_instances(const uint32_t* vid, int32_t rows, int F, int d, int ldx, 
   SFB_CHECK(!slot_of || (d & 3) == 0, "gather_instances: slot indirection needs d % 4 == 0");
   if ((d & 3) == 0) {
     const int64_t n = static_cast<int64_t>(rows) * (d / 4) * 2;  // two threads per chunk
-    gather_instances_v4<<<ceil_div(n, 256), 256, 0, s>>>(
-        vid, rows, F, d / 4, reinterpret_cast<const float4*>(G), reinterpret_cast<float4*>(X),
+    launch_pdl(gather_instances_v4, dim3(ceil_div(n, 256)), dim3(256), 0, s, vid, rows, F, d / 4, reinterpret_cast<const float4*>(G), reinterpret_cast<float4*>(X),
         reinterpret_cast<float4*>(fm_s), fm_sqp, slot_of, (g_ld ? g_ld : d) / 4);
   } else {
     const int64_t n = static_cast<int64_t>(rows) * d;
@@ -496,8 +498,7 @@ void sparse_adam(const uint32_t* own_k /* gradient row index, or null = j */,
       return std::max(1, b);
     }();
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), num_sms() * per_sm)));
-    sparse_adam_v4<<<grid, 256, 0, s>>>(
-        own_k, own_slot, d_n_own, n_own, d / 4, reinterpret_cast<const float4*>(dG),
+    launch_pdl(sparse_adam_v4, dim3(grid), dim3(256), 0, s, own_k, own_slot, d_n_own, n_own, d / 4, reinterpret_cast<const float4*>(dG),
         reinterpret_cast<float4*>(emb), reinterpret_cast<float4*>(mom),
         reinterpret_cast<float4*>(vel), steps, bc1, bc2, lr, beta1, beta2, omb1, omb2, eps, Bsum,
         fm_scale);

@@ -26,6 +26,7 @@ namespace {
 // (The atomicOr formulation ran at ~20 G positions/s, bound by L2 atomics.)
 __global__ void touch_mark_kernel(const uint32_t* __restrict__ vid, int64_t n, int64_t per_worker,
                                   uint8_t* __restrict__ tb8) {
+  pdl_wait();
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= n) return;
   tb8[static_cast<int64_t>(__ldg(vid + i)) * 8 + idiv(i, static_cast<int>(per_worker))] = 1;
@@ -33,6 +34,7 @@ __global__ void touch_mark_kernel(const uint32_t* __restrict__ vid, int64_t n, i
 
 __global__ void touch_pack_kernel(const int32_t* __restrict__ U, uint8_t* __restrict__ tb8,
                                   uint32_t* __restrict__ tm) {
+  pdl_wait();
   const int32_t n = *U;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
     uint64_t* row = reinterpret_cast<uint64_t*>(tb8) + k;
@@ -47,6 +49,7 @@ __global__ void touch_pack_kernel(const int32_t* __restrict__ U, uint8_t* __rest
 
 __global__ void lvid_kernel(const uint32_t* __restrict__ vid, int64_t n,
                             const uint32_t* __restrict__ lpos, uint32_t* __restrict__ lvid) {
+  pdl_wait();
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i < n) lvid[i] = lpos[vid[i]];
 }
@@ -221,6 +224,7 @@ __global__ void plan_scan_tiles_kernel(const uint32_t* __restrict__ tile_cnt_all
                                        int32_t* __restrict__ totals_all,
                                        const int32_t* __restrict__ live0,
                                        const int32_t* __restrict__ live1) {
+  pdl_wait();
   const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (q >= 16) return;
   const int p = q & 7;
@@ -314,6 +318,7 @@ __global__ void __launch_bounds__(256) plan_count_kernel(
     const uint32_t* __restrict__ own_k, const int32_t* __restrict__ n_own, int cap,
     const uint32_t* __restrict__ tm, uint32_t W, uint32_t me, int ntiles,
     uint32_t* __restrict__ tile_cnt) {
+  pdl_wait();
   if (blockIdx.y == 0) plan_count_tile<false>(uniq, U, cap, tm, W, me, tile_cnt);
   else plan_count_tile<true>(own_k, n_own, cap, tm, W, me, tile_cnt + ntiles * 8);
 }
@@ -324,6 +329,7 @@ __global__ void __launch_bounds__(256) plan_rank_kernel(
     const uint32_t* __restrict__ tm, uint32_t W, uint32_t me, int ntiles,
     const uint32_t* __restrict__ tile_off, const int32_t* __restrict__ totals,
     Cnt8* __restrict__ sscan, uint32_t* __restrict__ lpos) {
+  pdl_wait();
   if (blockIdx.y == 0)
     plan_rank_tile<false>(uniq, U, cap, tm, W, me, tile_off, totals, nullptr, lpos);
   else
@@ -338,28 +344,28 @@ void Exchange::plan(const uint32_t* d_vid, int64_t n_global, int64_t per_worker,
                     const int32_t* d_n_own, cudaStream_t s, const PhaseHook& hook) {
   const int c = static_cast<int>(cap);
   const int ntiles = ceil_div(c, kTile);
-  touch_mark_kernel<<<ceil_div(n_global, 256), 256, 0, s>>>(d_vid, n_global, per_worker, tb8);
+  launch_pdl(touch_mark_kernel, dim3(ceil_div(n_global, 256)), dim3(256), 0, s, d_vid, n_global, per_worker, tb8);
   CUDA_LAUNCH_CHECK();
   hook("plan_mark");
-  touch_pack_kernel<<<std::max(1, std::min(ceil_div(c, 256), num_sms() * 8)), 256, 0, s>>>(d_U, tb8, tm);
+  launch_pdl(touch_pack_kernel, dim3(std::max(1, std::min(ceil_div(c, 256), num_sms() * 8))), dim3(256), 0, s, d_U, tb8, tm);
   CUDA_LAUNCH_CHECK();
   hook("plan_touch");
   // receive plan (y = 0, over the uniques) and send plan (y = 1, over my owned uniques)
-  plan_count_kernel<<<dim3(ntiles, 2), 256, 0, s>>>(d_uniq, d_U, d_own_k, d_n_own, c, tm, W, me,
+  launch_pdl(plan_count_kernel, dim3(dim3(ntiles, 2)), dim3(256), 0, s, d_uniq, d_U, d_own_k, d_n_own, c, tm, W, me,
                                                     ntiles, tile_cnt);
   CUDA_LAUNCH_CHECK();
-  plan_scan_tiles_kernel<<<1, 512, 0, s>>>(tile_cnt, ntiles, tile_off, totals, d_U, d_n_own);
+  launch_pdl(plan_scan_tiles_kernel, dim3(1), dim3(512), 0, s, tile_cnt, ntiles, tile_off, totals, d_U, d_n_own);
   CUDA_LAUNCH_CHECK();
-  plan_rank_kernel<<<dim3(ntiles, 2), 256, 0, s>>>(d_uniq, d_U, d_own_k, d_n_own, c, tm, W, me,
+  launch_pdl(plan_rank_kernel, dim3(dim3(ntiles, 2)), dim3(256), 0, s, d_uniq, d_U, d_own_k, d_n_own, c, tm, W, me,
                                                    ntiles, tile_off, totals, sscan, lpos);
   CUDA_LAUNCH_CHECK();
   hook("plan_rank");
   // every peer's layout (peer-store transport)
   CUDA_CHECK(cudaMemsetAsync(totals + 16, 0, sizeof(int32_t) * 64, s));
-  count_matrix_kernel<<<std::min(ceil_div(c, 256), num_sms() * 4), 256, 0, s>>>(d_uniq, d_U, c, tm, W,
+  launch_pdl(count_matrix_kernel, dim3(std::min(ceil_div(c, 256), num_sms() * 4)), dim3(256), 0, s, d_uniq, d_U, c, tm, W,
                                                                            totals + 16);
   CUDA_LAUNCH_CHECK();
-  offsets_kernel<<<1, 32, 0, s>>>(totals, me, offs);
+  launch_pdl(offsets_kernel, dim3(1), dim3(32), 0, s, totals, me, offs);
   CUDA_LAUNCH_CHECK();
 }
 
@@ -367,24 +373,24 @@ void Exchange::plan_send(const uint32_t* d_own_k, const int32_t* d_n_own, const 
                          cudaStream_t s) {
   const int c = static_cast<int>(cap);
   const int ntiles = ceil_div(c, kTile);
-  plan_count_kernel<<<dim3(ntiles, 2), 256, 0, s>>>(d_own_k, d_zero, d_own_k, d_n_own, c, tm, W, me,
+  launch_pdl(plan_count_kernel, dim3(dim3(ntiles, 2)), dim3(256), 0, s, d_own_k, d_zero, d_own_k, d_n_own, c, tm, W, me,
                                                     ntiles, tile_cnt);
   CUDA_LAUNCH_CHECK();
-  plan_scan_tiles_kernel<<<1, 512, 0, s>>>(tile_cnt, ntiles, tile_off, totals, d_zero, d_n_own);
+  launch_pdl(plan_scan_tiles_kernel, dim3(1), dim3(512), 0, s, tile_cnt, ntiles, tile_off, totals, d_zero, d_n_own);
   CUDA_LAUNCH_CHECK();
-  plan_rank_kernel<<<dim3(ntiles, 2), 256, 0, s>>>(d_own_k, d_zero, d_own_k, d_n_own, c, tm, W, me,
+  launch_pdl(plan_rank_kernel, dim3(dim3(ntiles, 2)), dim3(256), 0, s, d_own_k, d_zero, d_own_k, d_n_own, c, tm, W, me,
                                                    ntiles, tile_off, totals, sscan, lpos);
   CUDA_LAUNCH_CHECK();
 }
 
 void Exchange::plan_offsets(cudaStream_t s) {
-  offsets_kernel<<<1, 32, 0, s>>>(totals, me, offs);
+  launch_pdl(offsets_kernel, dim3(1), dim3(32), 0, s, totals, me, offs);
   CUDA_LAUNCH_CHECK();
 }
 
 void Exchange::local_vids(const uint32_t* d_vid_mine, int64_t n, uint32_t* d_lvid, cudaStream_t s,
                           const uint32_t* table) {
-  lvid_kernel<<<ceil_div(n, 256), 256, 0, s>>>(d_vid_mine, n, table ? table : lpos, d_lvid);
+  launch_pdl(lvid_kernel, dim3(ceil_div(n, 256)), dim3(256), 0, s, d_vid_mine, n, table ? table : lpos, d_lvid);
   CUDA_LAUNCH_CHECK();
 }
 
@@ -415,6 +421,7 @@ __global__ void count_matrix_kernel(const uint32_t* __restrict__ uniq,
                                     const int32_t* __restrict__ U, int cap,
                                     const uint32_t* __restrict__ tm, uint32_t W,
                                     int32_t* __restrict__ cnt) {
+  pdl_wait();
   __shared__ int32_t c[64];
   if (threadIdx.x < 64) c[threadIdx.x] = 0;
   __syncthreads();
@@ -502,6 +509,7 @@ namespace {
 // the host's set_counts, on the device: every rank's receive layout (the totals staged in
 // shared memory, then thread w builds row w of roff, thread 8 + o column o of boff)
 __global__ void offsets_kernel(const int32_t* __restrict__ totals, int me, int32_t* __restrict__ offs) {
+  pdl_wait();
   __shared__ int32_t t[Exchange::kTotals];
   for (int i = threadIdx.x; i < Exchange::kTotals; i += blockDim.x) t[i] = totals[i];
   __syncthreads();
@@ -543,6 +551,7 @@ __global__ void __launch_bounds__(256) push_rows_p2p_dev_kernel(
     const int32_t* __restrict__ n_ptr, const uint32_t* __restrict__ tm,
     const Cnt8* __restrict__ sscan, uint32_t W, uint32_t me, const int32_t* __restrict__ offs,
     const float4* __restrict__ emb, int d4, PeerRows pr) {
+  pdl_wait();
   const int64_t n = static_cast<int64_t>(*n_ptr) * d4;
   uint32_t e_off[8];
 #pragma unroll
@@ -671,6 +680,7 @@ __global__ void push_blocks_p2p_dev_kernel(const float4* __restrict__ dE, int d4
                                            const int32_t* __restrict__ totals,
                                            const int32_t* __restrict__ offs, PeerRows pr,
                                            FmDefer fm) {
+  pdl_wait();
   const int o = blockIdx.y;
   if (o != static_cast<int>(me)) {
     const int64_t n = static_cast<int64_t>(totals[o]) * d4;
@@ -702,6 +712,7 @@ __global__ void push_blocks_p2p_dev_kernel(const float4* __restrict__ dE, int d4
 
 __global__ void zero_rows_dev_kernel(float4* __restrict__ p, const int32_t* __restrict__ offs,
                                      int d4, float* __restrict__ B) {
+  pdl_wait();
   const int64_t n = static_cast<int64_t>(offs[Exchange::kOffRecv + 8]) * d4;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -727,6 +738,7 @@ __global__ void __launch_bounds__(256, 5) owner_reduce_adam_dev_kernel(
     const int32_t* __restrict__ totals, uint32_t W, uint32_t me, const uint32_t* __restrict__ lpos,
     const float4* __restrict__ dE, const float4* __restrict__ recvbuf, int d4,
     const float* __restrict__ fmB, float fm_scale, OwnerAdam a) {
+  pdl_wait();
   const int64_t n = static_cast<int64_t>(*n_ptr) * d4;
   uint32_t soff[8];  // start of source w's block in my receive buffer
   uint32_t run = 0;
@@ -808,9 +820,8 @@ void Exchange::forward_dev(const uint32_t* d_own_k, const uint32_t* d_own_slot, 
     return !(e && e[0] == '1');
   }();
   if (fused) {
-    push_rows_p2p_dev_kernel<<<std::max(1, std::min(ceil_div(static_cast<int64_t>(n_bound) * (d / 4), 512),
-                                                    fwd_blocks)),
-                               256, 0, s>>>(d_own_k, d_own_slot, d_n_own, tm, sscan, W, me, offs,
+    launch_pdl(push_rows_p2p_dev_kernel, dim3(std::max(1, std::min(ceil_div(static_cast<int64_t>(n_bound) * (d / 4), 512),
+                                                    fwd_blocks))), dim3(256), 0, s, d_own_k, d_own_slot, d_n_own, tm, sscan, W, me, offs,
                                             reinterpret_cast<const float4*>(emb), d / 4, pr);
     CUDA_LAUNCH_CHECK();
     return;
@@ -836,8 +847,7 @@ void Exchange::backward_send_dev(const float* dE, cudaStream_t s, const float* E
   // one wave of writers per destination: more concurrent NVLink writers congest the switch
   // (microbench/nvlink_push.cu: 569 GB/s out per GPU with 148 CTAs per peer at W = 4,
   // 444 GB/s with 592, 406 GB/s with 1184)
-  push_blocks_p2p_dev_kernel<<<dim3(num_sms(), W), 256, 0, s>>>(
-      reinterpret_cast<const float4*>(dE), d / 4, me, totals, offs, pr,
+  launch_pdl(push_blocks_p2p_dev_kernel, dim3(dim3(num_sms(), W)), dim3(256), 0, s, reinterpret_cast<const float4*>(dE), d / 4, me, totals, offs, pr,
       FmDefer{reinterpret_cast<const float4*>(E), B, fm_scale});
   CUDA_LAUNCH_CHECK();
 }
@@ -849,9 +859,8 @@ void Exchange::backward_reduce_adam_dev(const uint32_t* d_own_k, int32_t n_bound
   OwnerAdam a{reinterpret_cast<float4*>(ar.emb), reinterpret_cast<float4*>(ar.mom),
               reinterpret_cast<float4*>(ar.vel), ar.own_slot, ar.steps, ar.bc1, ar.bc2, ar.lr,
               ar.b1, ar.b2, ar.omb1, ar.omb2, ar.eps};
-  owner_reduce_adam_dev_kernel<<<std::max(1, std::min(ceil_div(static_cast<int64_t>(n_bound) * d4, 256),
-                                                      num_sms() * 15)),
-                                 256, 0, s>>>(d_own_k, d_n_own, tm, sscan, totals, W, me, lpos,
+  launch_pdl(owner_reduce_adam_dev_kernel, dim3(std::max(1, std::min(ceil_div(static_cast<int64_t>(n_bound) * d4, 256),
+                                                      num_sms() * 15))), dim3(256), 0, s, d_own_k, d_n_own, tm, sscan, totals, W, me, lpos,
                                               reinterpret_cast<const float4*>(dE),
                                               reinterpret_cast<const float4*>(buf), d4, B,
                                               fm_scale, a);
@@ -859,7 +868,7 @@ void Exchange::backward_reduce_adam_dev(const uint32_t* d_own_k, int32_t n_bound
 }
 
 void Exchange::zero_local_dev(float* dE, cudaStream_t s, float* B) {
-  zero_rows_dev_kernel<<<mgr_grid(num_sms() * 8), 256, 0, s>>>(reinterpret_cast<float4*>(dE), offs,
+  launch_pdl(zero_rows_dev_kernel, dim3(mgr_grid(num_sms() * 8)), dim3(256), 0, s, reinterpret_cast<float4*>(dE), offs,
                                                                 d / 4, B);
   CUDA_LAUNCH_CHECK();
 }
@@ -939,6 +948,7 @@ struct PeerFlags {
 // __threadfence_system().
 __global__ void flag_barrier_kernel(PeerFlags pf, int W, int me, uint64_t epoch,
                                     uint64_t timeout_ns, int32_t* abort_flag) {
+  pdl_wait();
   flag_barrier_wait(pf.peer, W, me, epoch, timeout_ns, abort_flag);
 }
 }  // namespace
@@ -949,7 +959,7 @@ void Exchange::barrier(ncclComm_t comm, cudaStream_t s) {
   if (flags && !nccl_barrier) {
     PeerFlags pf{};
     for (int w = 0; w < W; ++w) pf.peer[w] = peer_flags[w];
-    flag_barrier_kernel<<<1, 32, 0, s>>>(pf, W, me, ++epoch, barrier_timeout_ns(), abort_flag);
+    launch_pdl(flag_barrier_kernel, dim3(1), dim3(32), 0, s, pf, W, me, ++epoch, barrier_timeout_ns(), abort_flag);
     CUDA_LAUNCH_CHECK();
     return;
   }

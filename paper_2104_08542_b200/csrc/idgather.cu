@@ -22,6 +22,7 @@ struct PeerIds {
 __global__ void __launch_bounds__(256) push_ids_kernel(const uint64_t* __restrict__ in, int64_t n,
                                                        uint64_t limit, int32_t* __restrict__ bad,
                                                        PeerIds pd, int W, int64_t off, bool vec) {
+  pdl_wait();
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   if (vec) {  // 4 ids per thread: two 16 B loads, one 16 B store per destination
     const int64_t n4 = n >> 2;
@@ -63,6 +64,7 @@ struct PeerFlags {
 constexpr uint64_t kBadBit = 1ull << 63;
 __global__ void id_barrier_kernel(PeerFlags pf, int W, int me, uint64_t epoch, uint64_t timeout_ns,
                                   int32_t* abort_flag, int32_t* bad) {
+  pdl_wait();
   const int w = threadIdx.x;
   if (w >= W || w == me) return;
   const uint64_t word = epoch | (*bad ? kBadBit : 0ull);
@@ -175,12 +177,11 @@ const uint32_t* IdGather::gather(const uint64_t* d_ids, uint64_t limit, int32_t*
   const bool vec = (n & 3) == 0 && ((static_cast<int64_t>(me) * n) & 3) == 0 &&
                    (reinterpret_cast<uintptr_t>(d_ids) & 15) == 0;
   const int64_t units = vec ? n / 4 : n;
-  push_ids_kernel<<<std::max(1, std::min(ceil_div(units, 256), num_sms() * 2)), 256, 0, s>>>(
-      d_ids, n, limit, d_bad, pd, W, static_cast<int64_t>(me) * n, vec);
+  launch_pdl(push_ids_kernel, dim3(std::max(1, std::min(ceil_div(units, 256), num_sms() * 2))), dim3(256), 0, s, d_ids, n, limit, d_bad, pd, W, static_cast<int64_t>(me) * n, vec);
   CUDA_LAUNCH_CHECK();
   PeerFlags pf{};
   for (int w = 0; w < W; ++w) pf.peer[w] = peer_flags[w];
-  id_barrier_kernel<<<1, 32, 0, s>>>(pf, W, me, ++epoch, barrier_timeout_ns(), abort_flag, d_bad);
+  launch_pdl(id_barrier_kernel, dim3(1), dim3(32), 0, s, pf, W, me, ++epoch, barrier_timeout_ns(), abort_flag, d_bad);
   CUDA_LAUNCH_CHECK();
   return gids[k];
 }

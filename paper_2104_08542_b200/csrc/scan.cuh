@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(kScanThreads) lookback_scan_kernel(int64_t n, 
                                                                      const int32_t* __restrict__ live) {
   __shared__ uint32_t warp_sum[kScanThreads / 32];
   __shared__ uint32_t tile_prefix;
+  pdl_wait();  // launched with launch_pdl: the producer of the scanned values must be done
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   constexpr int64_t kScanTile = kScanThreads * kScanItems;
   // live (device count, nullable): items [live, n) are empty; tiles past the last live one
@@ -154,8 +155,8 @@ void lookback_scan(ScanTiles& st, int64_t n, ValueFn value, EmitFn emit, int32_t
     CUDA_CHECK(cudaMemsetAsync(st.state, 0, sizeof(uint64_t) * st.max_tiles, s));
     st.epoch = 1;
   }
-  lookback_scan_kernel<kItems><<<mgr_grid(tiles), kScanThreads, 0, s>>>(
-      n, value, emit, st.state, st.epoch, total, live);
+  launch_pdl(lookback_scan_kernel<kItems, ValueFn, EmitFn>, dim3(mgr_grid(tiles)),
+             dim3(kScanThreads), 0, s, n, value, emit, st.state, st.epoch, total, live);
   CUDA_LAUNCH_CHECK();
 }
 #endif

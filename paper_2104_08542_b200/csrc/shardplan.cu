@@ -63,6 +63,7 @@ __global__ void __launch_bounds__(256) route_pairs_kernel(const uint64_t* __rest
                                                           int32_t* __restrict__ bad,
                                                           int32_t* __restrict__ cursor,
                                                           PeerPairs pp, uint32_t* __restrict__ rix) {
+  pdl_wait();
   __shared__ uint32_t wc[kRouteItems][8][8];  // [item][warp][owner]: counts -> offsets
   __shared__ uint32_t bbase[8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -140,6 +141,7 @@ __global__ void publish_barrier_kernel(int kind, PeerInts inbox, const int32_t* 
                                        const int32_t* __restrict__ n_own, PeerFlagsS pf, int W,
                                        int me, uint64_t epoch, uint64_t timeout_ns,
                                        int32_t* abort_flag, int32_t* bad) {
+  pdl_wait();
   const int x = threadIdx.x;
   if (x < W) {
     int32_t* dst = inbox.p[x];
@@ -182,6 +184,7 @@ __global__ void __launch_bounds__(256) dedup_pairs_kernel(const uint64_t* __rest
                                                           uint32_t* __restrict__ tmask,
                                                           uint64_t mask,
                                                           uint32_t* __restrict__ hslot) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int r = blockIdx.y;
   const int64_t cnt = inbox[72 + r];
@@ -233,6 +236,7 @@ __global__ void __launch_bounds__(256) first_bits_kernel(const uint64_t* __restr
                                                          const uint32_t* __restrict__ hslot,
                                                          const uint32_t* __restrict__ pos,
                                                          uint32_t* __restrict__ bits) {
+  pdl_wait();
   const int r = blockIdx.y;
   const int64_t cnt = inbox[72 + r];
   const int64_t off = static_cast<int64_t>(r) * n;
@@ -263,6 +267,7 @@ __global__ void __launch_bounds__(256) first_emit_kernel(
     const uint32_t* __restrict__ keys, const uint32_t* __restrict__ tmask,
     uint32_t* __restrict__ owned, uint32_t* __restrict__ own_k, uint32_t* __restrict__ tm,
     uint32_t* __restrict__ uslot) {
+  pdl_wait();
   const int r = blockIdx.y;
   const int64_t cnt = inbox[72 + r];
   const int64_t off = static_cast<int64_t>(r) * n;
@@ -304,6 +309,7 @@ __global__ void __launch_bounds__(256) reply_kernel(int64_t n, int W, int me,
                                                     int32_t* __restrict__ totals,
                                                     int32_t* __restrict__ U_global,
                                                     PeerReply pr) {
+  pdl_wait();
   const int r = blockIdx.y;
   if (r == W) {
     uint32_t base = 0;  // roff[me][me]
@@ -347,6 +353,7 @@ __global__ void reset_table_kernel(const uint32_t* __restrict__ uslot,
                                    uint32_t* __restrict__ pos, uint32_t* __restrict__ tmask,
                                    int32_t* __restrict__ cursor, uint32_t* __restrict__ bits,
                                    int64_t nwords) {
+  pdl_wait();
   const int32_t cnt = *n_own;
   if (blockIdx.x == 0 && threadIdx.x < 8) cursor[threadIdx.x] = 0;
   for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < nwords;
@@ -497,43 +504,41 @@ void ShardPlan::run(const uint64_t* d_ids, uint64_t vocab, int32_t* d_bad, int k
   const int gx = static_cast<int>(std::max<int64_t>(
       1, std::min<int64_t>(ceil_div(n, 256), num_sms() * 8 / W)));  // per source region
   // 1. route + B1 (pair counts into every owner's inbox[72 + me], the bad-id bit)
-  route_pairs_kernel<<<static_cast<int>(std::max<int64_t>(1, ceil_div(n, 256 * kRouteItems))),
-                       256, 0, s>>>(d_ids, n, vocab, W, me, d_bad, cursor, pp, rix + k * n);
+  launch_pdl(route_pairs_kernel, dim3(static_cast<int>(std::max<int64_t>(1, ceil_div(n, 256 * kRouteItems)))), dim3(256), 0, s, d_ids, n, vocab, W, me, d_bad, cursor, pp, rix + k * n);
   CUDA_LAUNCH_CHECK();
   hook("shard_route");
-  publish_barrier_kernel<<<1, 32, 0, s>>>(0, pi, cursor, nullptr, nullptr, pf, W, me, ++epoch,
+  launch_pdl(publish_barrier_kernel, dim3(1), dim3(32), 0, s, 0, pi, cursor, nullptr, nullptr, pf, W, me, ++epoch,
                                           tmo, abort_flag, d_bad);
   CUDA_LAUNCH_CHECK();
   hook("shard_b1");
   // 2. dedup, 3. first positions -> owned uniques in global first-appearance order
-  dedup_pairs_kernel<<<dim3(gx, W), 256, 0, s>>>(prs, n, ibx, hkeys, hpos, hmask_bits, hmask,
+  launch_pdl(dedup_pairs_kernel, dim3(dim3(gx, W)), dim3(256), 0, s, prs, n, ibx, hkeys, hpos, hmask_bits, hmask,
                                                  hslot);
   CUDA_LAUNCH_CHECK();
   hook("shard_dedup");
-  first_bits_kernel<<<dim3(gx, W), 256, 0, s>>>(prs, n, ibx, hslot, hpos, bits);
+  launch_pdl(first_bits_kernel, dim3(dim3(gx, W)), dim3(256), 0, s, prs, n, ibx, hslot, hpos, bits);
   CUDA_LAUNCH_CHECK();
   hook("shard_first");
   lookback_scan<4>(tiles, nwords, WordCount{bits}, WordPrefix{wpre}, d_n_own, s);
   hook("shard_scan");
-  first_emit_kernel<<<dim3(gx, W), 256, 0, s>>>(prs, n, ibx, hslot, hpos, bits, wpre, hkeys,
+  launch_pdl(first_emit_kernel, dim3(dim3(gx, W)), dim3(256), 0, s, prs, n, ibx, hslot, hpos, bits, wpre, hkeys,
                                                 hmask_bits, owned_uniq, own_k, xch.tm, uslot);
   CUDA_LAUNCH_CHECK();
   hook("shard_emit");
   // 4. send plan over my owned uniques, my column of the count matrix + my count; B2
   xch.plan_send(own_k, d_n_own, zero, s);
   hook("shard_plan");
-  publish_barrier_kernel<<<1, 32, 0, s>>>(1, pi, nullptr, xch.totals, d_n_own, pf, W, me, ++epoch,
+  launch_pdl(publish_barrier_kernel, dim3(1), dim3(32), 0, s, 1, pi, nullptr, xch.totals, d_n_own, pf, W, me, ++epoch,
                                           tmo, abort_flag, nullptr);
   CUDA_LAUNCH_CHECK();
   hook("shard_b2");
   // 5 + 6. layout + replies, then the table reset (no barrier after the replies, see top)
-  reply_kernel<<<dim3(gx, W + 1), 256, 0, s>>>(n, W, me, ibx, hslot, hpos, xch.sscan, xch.tm,
+  launch_pdl(reply_kernel, dim3(dim3(gx, W + 1)), dim3(256), 0, s, n, W, me, ibx, hslot, hpos, xch.sscan, xch.tm,
                                                d_n_own, xch.lpos, xch.totals, d_U_global, pr);
   CUDA_LAUNCH_CHECK();
   hook("shard_reply");
   xch.plan_offsets(s);
-  reset_table_kernel<<<std::max(1, std::min(ceil_div(cap, 256), num_sms() * 4)), 256, 0, s>>>(
-      uslot, d_n_own, hkeys, hpos, hmask_bits, cursor, bits, nwords);
+  launch_pdl(reset_table_kernel, dim3(std::max(1, std::min(ceil_div(cap, 256), num_sms() * 4))), dim3(256), 0, s, uslot, d_n_own, hkeys, hpos, hmask_bits, cursor, bits, nwords);
   CUDA_LAUNCH_CHECK();
   hook("shard_reset");
 }

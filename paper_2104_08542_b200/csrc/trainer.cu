@@ -382,6 +382,7 @@ struct StepClear {
 // scalars[0] and [2, 8) ([1], the bad-id flag, is sticky until a host check has seen it);
 // per lane counters [0, 2), [3, 5) and kCntOld
 __global__ void step_clear_kernel(StepClear a) {
+  pdl_wait();
   const int t = threadIdx.x;
   if (t < 8 && t != 1) a.scalars[t] = 0;
   const int l = t / 8, q = t % 8;
@@ -421,6 +422,7 @@ struct TailArgs {
 };
 
 __global__ void tail_kernel(TailArgs a) {
+  pdl_wait();
   const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   if (*a.bad) {
@@ -484,6 +486,7 @@ __global__ void zero_rows_kernel(float4* __restrict__ p, const int32_t* __restri
 }  // namespace
 
 namespace {
+__global__ void empty_kernel() { pdl_wait(); }
 // SFCTR_STEP_TRACE=n: globaltimer stamps of the last n steps' stage boundaries (diagnostics)
 __global__ void stamp_kernel(unsigned long long* p) {
   unsigned long long t;
@@ -605,6 +608,7 @@ struct SnapArgs {
   int32_t* out;
 };
 __global__ void snap_kernel(SnapArgs a) {
+  pdl_wait();
   const int i = threadIdx.x;
   if (i == 0) a.out[0] = *a.U;
   if (i < kCntWords * a.lanes) a.out[1 + i] = a.cnt[i / kCntWords][i % kCntWords];
@@ -619,6 +623,7 @@ struct GatePtrs {
 };
 __global__ void bad_id_gate_kernel(const int32_t* __restrict__ bad, int32_t* U, LaneCounters cnt,
                                    int lanes, uint32_t* __restrict__ vid, int64_t n, GatePtrs gp) {
+  pdl_wait();
   if (!*bad) return;
   const int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   for (int64_t i = i0; i < n; i += static_cast<int64_t>(gridDim.x) * blockDim.x) vid[i] = 0;
@@ -631,6 +636,7 @@ __global__ void bad_id_gate_kernel(const int32_t* __restrict__ bad, int32_t* U, 
   }
 }
 __global__ void bad_id_gate_plan_kernel(const int32_t* __restrict__ bad, uint32_t* lpos) {
+  pdl_wait();
   if (*bad) lpos[0] = 0;
 }
 }  // namespace
@@ -699,7 +705,7 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
     sc.scalars = d_scalars_;
     for (int l = 0; l < lanes_; ++l) sc.cnt[l] = lane_[l].counters;
     sc.lanes = lanes_;
-    step_clear_kernel<<<1, 64, 0, sm>>>(sc);
+    launch_pdl(step_clear_kernel, dim3(1), dim3(64), 0, sm, sc);
     CUDA_LAUNCH_CHECK();
   }
   const int32_t cap = static_cast<int32_t>(lane_[0].umax);
@@ -753,7 +759,7 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
       gp.own_slot[l] = lane_[l].own_slot;
     }
     // one block: the common case reads the flag and exits
-    bad_id_gate_kernel<<<1, 256, 0, sm>>>(d_scalars_ + 1, d_scalars_ + 0, lc, lanes_,
+    launch_pdl(bad_id_gate_kernel, dim3(1), dim3(256), 0, sm, d_scalars_ + 1, d_scalars_ + 0, lc, lanes_,
                                           d_vid_, sharded_ ? 0 : n_global_, gp);
     CUDA_LAUNCH_CHECK();
   }
@@ -793,7 +799,7 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
     if (!sharded_) {  // (the sharded stage built it with the ids)
       xch_.plan(d_vid_, n_global_, static_cast<int64_t>(b_) * F_, d_uniq_, d_scalars_ + 0,
                 lane_[0].own_k, lane_[0].counters + kCntOwned, sm, mhook);
-      bad_id_gate_plan_kernel<<<1, 1, 0, sm>>>(d_scalars_ + 1, xch_.lpos);
+      launch_pdl(bad_id_gate_plan_kernel, dim3(1), dim3(1), 0, sm, d_scalars_ + 1, xch_.lpos);
       CUDA_LAUNCH_CHECK();
     }
     if (!free_step)
@@ -897,7 +903,7 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
     for (int l = 0; l < lanes_; ++l) sa.cnt[l] = lane_[l].counters;
     sa.lanes = lanes_;
     sa.out = snap;
-    snap_kernel<<<1, 1 + kCntWords * 8, 0, sm>>>(sa);
+    launch_pdl(snap_kernel, dim3(1), dim3(1 + kCntWords * 8), 0, sm, sa);
     CUDA_LAUNCH_CHECK();
   }
   // Clear this step's gradient table (its parity set) here, off the training stage's path:
@@ -907,6 +913,17 @@ void Trainer::prepare(int64_t step, const uint64_t* d_features, const uint64_t* 
   else if (xdev)
     xch_.zero_local_dev(d_dG_, sm, d_ % 4 == 0 && !tower_fused_ ? d_B_ : nullptr);
   phase("manage_evict_admit", sm);
+  {  // experiment: SFCTR_MGR_EXTRA=k empty kernels on the manager stream (boundary cost)
+    static const int extra = [] {
+      const char* e = std::getenv("SFCTR_MGR_EXTRA");
+      return e ? std::atoi(e) : 0;
+    }();
+    static const bool extra_pdl = std::getenv("SFCTR_MGR_EXTRA_PDL") != nullptr;
+    for (int q = 0; q < extra; ++q) {
+      if (extra_pdl) launch_pdl(empty_kernel, dim3(1), dim3(32), 0, sm);
+      else empty_kernel<<<1, 32, 0, sm>>>();
+    }
+  }
   stamp(step, 1, sm);
   if (sm != sw) {
     CUDA_CHECK(cudaEventRecord(prep_done_[k], sm));
@@ -1207,7 +1224,7 @@ void Trainer::train(int64_t step, const uint8_t* d_labels, float* d_loss) {
     a.P = static_cast<int64_t>(P_);
     a.bad = d_scalars_ + 1;
     a.gated = d_err_ + 1;
-    tail_kernel<<<num_sms() * 8, 256, 0, s>>>(a);  // one pass over the dense parameters and the rows
+    launch_pdl(tail_kernel, dim3(num_sms() * 8), dim3(256), 0, s, a);  // one pass over the dense parameters and the rows
     CUDA_LAUNCH_CHECK();
     w1_split_ready_ = a.w_hi != nullptr;
   }

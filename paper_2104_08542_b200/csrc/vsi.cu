@@ -45,6 +45,7 @@ __global__ void fill_u32_kernel(uint32_t* p, int64_t n, uint32_t v) {
 // which removes the contended atomics on hot ids.
 __global__ void vsi_first_kernel(const uint32_t* __restrict__ ids, int64_t n,
                                  uint32_t* __restrict__ first) {
+  pdl_wait();
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const uint32_t f = __ldg(ids + i);
@@ -76,6 +77,7 @@ struct VsiEmit {
 
 __global__ void vsi_vid_kernel(const uint32_t* __restrict__ ids, int64_t n,
                                const uint32_t* __restrict__ first, uint32_t* __restrict__ vids) {
+  pdl_wait();
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
     vids[i] = __ldcg(first + __ldg(ids + i)) & ~kTag;
@@ -101,6 +103,7 @@ template <typename KeyT, typename IdT>
 __global__ void vsi_hash_insert_kernel(const IdT* __restrict__ ids, int64_t n,
                                        KeyT* __restrict__ keys, uint32_t* __restrict__ pos,
                                        uint64_t mask, uint32_t* __restrict__ hslot) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   // grid-stride in warp-aligned steps (the ballot / match below need whole warps)
   for (int64_t i0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) & ~31ll;
@@ -159,6 +162,7 @@ struct VsiHashEmit {
 };
 __global__ void vsi_hash_vid_kernel(const uint32_t* __restrict__ hslot, int64_t n,
                                     const uint32_t* __restrict__ pos, uint32_t* __restrict__ vids) {
+  pdl_wait();
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
     vids[i] = __ldcg(pos + __ldg(hslot + i)) & ~kTag;
@@ -167,6 +171,7 @@ template <typename KeyT>
 __global__ void vsi_hash_reset_kernel(const uint32_t* __restrict__ uslot,
                                       const int32_t* __restrict__ unique, KeyT* __restrict__ keys,
                                       uint32_t* __restrict__ pos) {
+  pdl_wait();
   const int32_t u = *unique;
   for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < u;
        k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -178,6 +183,7 @@ __global__ void vsi_hash_reset_kernel(const uint32_t* __restrict__ uslot,
 
 __global__ void vsi_reset_kernel(const uint32_t* __restrict__ gids,
                                  const int32_t* __restrict__ unique, uint32_t* __restrict__ first) {
+  pdl_wait();
   const int32_t u = *unique;
   for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < u;
        k += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -186,6 +192,7 @@ __global__ void vsi_reset_kernel(const uint32_t* __restrict__ gids,
 
 __global__ void ids_to_u32_kernel(const uint64_t* __restrict__ in, uint32_t* __restrict__ out,
                                   int64_t n, uint64_t limit, int32_t* bad) {
+  pdl_wait();
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const uint64_t v = in[i];
@@ -287,27 +294,26 @@ void vsi_device(VsiScratch& v, const uint32_t* d_ids, int64_t n, uint32_t* d_gid
   SFB_CHECK(v.key_space > 0, "direct-mapped VSI needs a key space");
   const int grid = mgr_grid(ceil_div(n, 256));  // manager stage: capped, grid-stride kernels
   if (v.hashed32) {  // L2-resident hashed table; always reset behind the batch
-    vsi_hash_insert_kernel<uint32_t, uint32_t><<<grid, 256, 0, s>>>(d_ids, n, v.d_hkeys32,
+    launch_pdl(vsi_hash_insert_kernel<uint32_t, uint32_t>, dim3(grid), dim3(256), 0, s, d_ids, n, v.d_hkeys32,
                                                                     v.d_first, v.hmask, v.d_hslot);
     CUDA_LAUNCH_CHECK();
     lookback_scan<2>(v.tiles, n, VsiHashFlag{v.d_hslot, v.d_first},
                      VsiHashEmit<uint32_t>{d_ids, v.d_hslot, v.d_first, d_gids, v.d_uslot},
                      d_unique, s);
-    vsi_hash_vid_kernel<<<grid, 256, 0, s>>>(v.d_hslot, n, v.d_first, d_vids);
+    launch_pdl(vsi_hash_vid_kernel, dim3(grid), dim3(256), 0, s, v.d_hslot, n, v.d_first, d_vids);
     CUDA_LAUNCH_CHECK();
-    vsi_hash_reset_kernel<uint32_t><<<grid, 256, 0, s>>>(
-        v.d_uslot, d_unique, v.d_hkeys32, v.d_first);
+    launch_pdl(vsi_hash_reset_kernel<uint32_t>, dim3(grid), dim3(256), 0, s, v.d_uslot, d_unique, v.d_hkeys32, v.d_first);
     CUDA_LAUNCH_CHECK();
     return;
   }
-  vsi_first_kernel<<<grid, 256, 0, s>>>(d_ids, n, v.d_first);
+  launch_pdl(vsi_first_kernel, dim3(grid), dim3(256), 0, s, d_ids, n, v.d_first);
   CUDA_LAUNCH_CHECK();
   lookback_scan<2>(v.tiles, n, VsiFlag{d_ids, v.d_first}, VsiEmit{d_ids, v.d_first, d_gids},
                    d_unique, s);
-  vsi_vid_kernel<<<grid, 256, 0, s>>>(d_ids, n, v.d_first, d_vids);
+  launch_pdl(vsi_vid_kernel, dim3(grid), dim3(256), 0, s, d_ids, n, v.d_first, d_vids);
   CUDA_LAUNCH_CHECK();
   if (reset) {
-    vsi_reset_kernel<<<grid, 256, 0, s>>>(d_gids, d_unique, v.d_first);
+    launch_pdl(vsi_reset_kernel, dim3(grid), dim3(256), 0, s, d_gids, d_unique, v.d_first);
     CUDA_LAUNCH_CHECK();
   }
 }
@@ -317,23 +323,21 @@ void vsi_device_hashed(VsiScratch& v, const uint64_t* d_ids, int64_t n, uint64_t
   SFB_CHECK(n > 0 && n <= v.cap, "vsi batch exceeds scratch capacity");
   SFB_CHECK(v.key_space == 0, "hashed VSI needs a context created with key_space 0");
   const int grid = mgr_grid(ceil_div(n, 256));
-  vsi_hash_insert_kernel<unsigned long long, uint64_t><<<grid, 256, 0, s>>>(
-      d_ids, n, v.d_hkeys, v.d_first, v.hmask, v.d_hslot);
+  launch_pdl(vsi_hash_insert_kernel<unsigned long long, uint64_t>, dim3(grid), dim3(256), 0, s, d_ids, n, v.d_hkeys, v.d_first, v.hmask, v.d_hslot);
   CUDA_LAUNCH_CHECK();
   lookback_scan<2>(v.tiles, n, VsiHashFlag{v.d_hslot, v.d_first},
                    VsiHashEmit<uint64_t>{d_ids, v.d_hslot, v.d_first, d_gids, v.d_uslot},
                    d_unique, s);
-  vsi_hash_vid_kernel<<<grid, 256, 0, s>>>(v.d_hslot, n, v.d_first, d_vids);
+  launch_pdl(vsi_hash_vid_kernel, dim3(grid), dim3(256), 0, s, v.d_hslot, n, v.d_first, d_vids);
   CUDA_LAUNCH_CHECK();
-  vsi_hash_reset_kernel<unsigned long long><<<grid, 256, 0, s>>>(
-      v.d_uslot, d_unique, v.d_hkeys, v.d_first);
+  launch_pdl(vsi_hash_reset_kernel<unsigned long long>, dim3(grid), dim3(256), 0, s, v.d_uslot, d_unique, v.d_hkeys, v.d_first);
   CUDA_LAUNCH_CHECK();
 }
 
 void ids_to_u32(const uint64_t* d_in, uint32_t* d_out, int64_t n, uint64_t limit, int32_t* d_bad,
                 cudaStream_t s) {
   if (n <= 0) return;
-  ids_to_u32_kernel<<<mgr_grid(ceil_div(n, 256)), 256, 0, s>>>(d_in, d_out, n, limit, d_bad);
+  launch_pdl(ids_to_u32_kernel, dim3(mgr_grid(ceil_div(n, 256))), dim3(256), 0, s, d_in, d_out, n, limit, d_bad);
   CUDA_LAUNCH_CHECK();
 }
 
