@@ -284,9 +284,11 @@ Trainer::~Trainer() {
   cudaSetDevice(dev_);
   try {
     dump_stamps();
+    dump_phase_stamps();
   } catch (...) {
   }
   if (d_stamps_) cudaFree(d_stamps_);
+  if (d_pst_) cudaFree(d_pst_);
   if (mstream_) cudaStreamSynchronize(mstream_);
   if (stream_) cudaStreamSynchronize(stream_);
   for (auto& l : lane_) l.release();
@@ -555,8 +557,65 @@ void Trainer::dump_stamps() {
   }
 }
 
+// SFCTR_PHASE_STAMPS=n: outside the phase pass, every phase boundary also writes a
+// globaltimer stamp (one 1-thread kernel each, so the run is perturbed by their launches);
+// the destructor prints the mean device time per phase and stream over the last steps
+// (diagnostics: the stage breakdown while both stages run concurrently)
+void Trainer::phase_stamp(const char* name, cudaStream_t s) {
+  static const int cap = [] {
+    const char* e = std::getenv("SFCTR_PHASE_STAMPS");
+    return e ? std::max(0, std::atoi(e)) : 0;
+  }();
+  if (cap <= 0) return;
+  if (!d_pst_) {
+    CUDA_CHECK(cudaMalloc(&d_pst_, sizeof(unsigned long long) * cap));
+    pst_cap_ = cap;
+  }
+  const int64_t i = pst_n_++;
+  stamp_kernel<<<1, 1, 0, s>>>(d_pst_ + i % cap);
+  CUDA_CHECK(cudaGetLastError());
+  if (static_cast<int64_t>(pst_names_.size()) < cap) {
+    pst_names_.emplace_back(name);
+    pst_streams_.push_back(s);
+  } else {
+    pst_names_[i % cap] = name;
+    pst_streams_[i % cap] = s;
+  }
+}
+
+void Trainer::dump_phase_stamps() {
+  if (!d_pst_ || pst_n_ < 2) return;
+  const int cap = pst_cap_;
+  std::vector<unsigned long long> h(cap);
+  CUDA_CHECK(cudaDeviceSynchronize());
+  CUDA_CHECK(cudaMemcpy(h.data(), d_pst_, sizeof(unsigned long long) * cap, cudaMemcpyDeviceToHost));
+  const int64_t first = std::max<int64_t>(0, pst_n_ - cap);
+  std::map<std::pair<cudaStream_t, std::string>, std::pair<double, int>> acc;
+  std::map<cudaStream_t, unsigned long long> last;
+  for (int64_t i = first; i < pst_n_; ++i) {
+    const int q = static_cast<int>(i % cap);
+    const cudaStream_t st = pst_streams_[q];
+    const std::string& nm = pst_names_[q];
+    auto it = last.find(st);
+    if (it != last.end() && nm != "start") {
+      auto& a = acc[{st, nm}];
+      a.first += (static_cast<double>(h[q]) - it->second) * 1e-3;
+      a.second += 1;
+    }
+    last[st] = h[q];
+  }
+  fprintf(stderr, "phase stamps (mean us per occurrence, concurrent run):\n");
+  for (const auto& kv : acc)
+    fprintf(stderr, "  %s %-24s %8.2f  (n=%d)\n",
+            kv.first.first == mstream_ ? "mgr  " : kv.first.first == ustream_ ? "upd  " : "train",
+            kv.first.second.c_str(), kv.second.first / kv.second.second, kv.second.second);
+}
+
 void Trainer::phase(const char* name, cudaStream_t s) {
-  if (!timing_) return;
+  if (!timing_) {
+    phase_stamp(name, s ? s : stream_);
+    return;
+  }
   if (!s) s = stream_;
   cudaEvent_t e;
   CUDA_CHECK(cudaEventCreate(&e));

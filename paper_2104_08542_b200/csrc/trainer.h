@@ -3,6 +3,7 @@
 
 #include <nccl.h>
 
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -195,6 +196,13 @@ class Trainer {
   int64_t last_stamped_ = -1;
   void stamp(int64_t step, int slot, cudaStream_t s);
   void dump_stamps();
+  unsigned long long* d_pst_ = nullptr;  // SFCTR_PHASE_STAMPS ring
+  int pst_cap_ = 0;
+  int64_t pst_n_ = 0;
+  std::vector<std::string> pst_names_;
+  std::vector<cudaStream_t> pst_streams_;
+  void phase_stamp(const char* name, cudaStream_t s);
+  void dump_phase_stamps();
   int32_t* h_totals_ = nullptr;   // pinned [16] exchange plan totals
   int ldx_ = 0;
   bool tower_simt_ = false;
