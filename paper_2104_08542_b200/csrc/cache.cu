@@ -85,13 +85,19 @@ struct ProbeFlag {
     const uint32_t f = gids[own_k[j]];
     const uint32_t s = index[f / W];
     own_slot[j] = s;  // host slot / kNever until admit assigns the slot
+    bool newly_marked = false;
     if (s < C) {
       if (t > last_use[s]) last_use[s] = t;  // CacheBuffer::touch (cache_buffer.cpp:69-72)
-      if (atomicExch(mark + s, t) != t) atomicAdd(marked, 1);
-      return 0u;
+      newly_marked = atomicExch(mark + s, t) != t;
+    } else {
+      own_f[j] = f;
     }
-    own_f[j] = f;
-    return 1u;
+    // one counter atomic per group of converged lanes, not per hit: ~100 k hits per step
+    // on a single address were serialised at one L2 slice
+    const unsigned am = __activemask();
+    const unsigned bal = __ballot_sync(am, newly_marked);
+    if (bal && (threadIdx.x & 31) == __ffs(am) - 1) atomicAdd(marked, __popc(bal));
+    return s < C ? 0u : 1u;
   }
 };
 struct ProbeEmit {
@@ -116,11 +122,16 @@ __global__ void mark_window_kernel(const uint32_t* __restrict__ gids,
                                    int32_t* __restrict__ marked) {
   pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= cap || i >= *U_ptr) return;
-  const uint32_t f = gids[i];
-  if (f % W != w) return;
-  const uint32_t s = index[f / W];
-  if (s < C && atomicExch(mark + s, t) != t) atomicAdd(marked, 1);
+  bool newly = false;
+  if (i < cap && i < *U_ptr) {
+    const uint32_t f = gids[i];
+    if (f % W == w) {
+      const uint32_t s = index[f / W];
+      newly = s < C && atomicExch(mark + s, t) != t;
+    }
+  }
+  const unsigned bal = __ballot_sync(0xFFFFFFFFu, newly);  // one counter atomic per warp
+  if (bal && (threadIdx.x & 31) == 0) atomicAdd(marked, __popc(bal));
 }
 
 // LRU histogram over last_use of the eligible slots (occupied && !needed_soon; pins are
