@@ -186,20 +186,15 @@ __device__ __forceinline__ uint32_t plan_mask(int i, const uint32_t* __restrict_
 }
 
 template <bool SEND>
-__device__ __forceinline__ void plan_count_tile(const uint32_t* __restrict__ keys,
-                                                         const int32_t* __restrict__ live, int cap,
-                                                         const uint32_t* __restrict__ tm,
-                                                         uint32_t W, uint32_t me,
-                                                         uint32_t* __restrict__ tile_cnt) {
+__device__ __forceinline__ void plan_count_tile(int tile, const uint32_t* __restrict__ keys,
+                                                const int32_t* __restrict__ live, int cap,
+                                                const uint32_t* __restrict__ tm, uint32_t W,
+                                                uint32_t me, uint32_t* __restrict__ tile_cnt) {
   __shared__ uint32_t wc[8][8];  // [warp][plane]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (blockIdx.x * kTile >= *live) {  // tile past the live count: nothing to rank
-    if (threadIdx.x < 8) tile_cnt[blockIdx.x * 8 + threadIdx.x] = 0;
-    return;
-  }
   uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int r = 0; r < 4; ++r) {
-    const int i = blockIdx.x * kTile + r * 256 + threadIdx.x;
+    const int i = tile * kTile + r * 256 + threadIdx.x;
     const uint32_t m = i < cap ? plan_mask<SEND>(i, keys, live, tm, W, me) : 0u;
 #pragma unroll
     for (int p = 0; p < 8; ++p) acc[p] += __popc(__ballot_sync(0xFFFFFFFFu, (m >> p) & 1u));
@@ -211,8 +206,9 @@ __device__ __forceinline__ void plan_count_tile(const uint32_t* __restrict__ key
   if (threadIdx.x < 8) {
     uint32_t s = 0;
     for (int w = 0; w < 8; ++w) s += wc[w][threadIdx.x];
-    tile_cnt[blockIdx.x * 8 + threadIdx.x] = s;
+    tile_cnt[tile * 8 + threadIdx.x] = s;
   }
+  __syncthreads();  // wc is reused by the CTA's next tile
 }
 
 // warp p scans plane p over the tiles (exclusive), totals[p] = plane total
@@ -258,7 +254,7 @@ __global__ void plan_scan_tiles_kernel(const uint32_t* __restrict__ tile_cnt_all
 }
 
 template <bool SEND>
-__device__ __forceinline__ void plan_rank_tile(const uint32_t* __restrict__ keys,
+__device__ __forceinline__ void plan_rank_tile(int tile, const uint32_t* __restrict__ keys,
                                                         const int32_t* __restrict__ live, int cap,
                                                         const uint32_t* __restrict__ tm,
                                                         uint32_t W, uint32_t me,
@@ -268,11 +264,10 @@ __device__ __forceinline__ void plan_rank_tile(const uint32_t* __restrict__ keys
                                                         uint32_t* __restrict__ lpos) {
   __shared__ uint32_t wc[4][8][8];  // [round][warp][plane] -> exclusive offsets in tile order
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (blockIdx.x * kTile >= *live) return;  // no live element in this tile
   const unsigned lt = (1u << lane) - 1u;
   uint32_t m[4], pre[4][8];
   for (int r = 0; r < 4; ++r) {
-    const int i = blockIdx.x * kTile + r * 256 + threadIdx.x;
+    const int i = tile * kTile + r * 256 + threadIdx.x;
     m[r] = i < cap ? plan_mask<SEND>(i, keys, live, tm, W, me) : 0u;
 #pragma unroll
     for (int p = 0; p < 8; ++p) {
@@ -284,7 +279,7 @@ __device__ __forceinline__ void plan_rank_tile(const uint32_t* __restrict__ keys
   __syncthreads();
   if (threadIdx.x < 8) {  // plane p: exclusive prefix over (round, warp) in tile order
     const int p = threadIdx.x;
-    uint32_t run = tile_off[blockIdx.x * 8 + p];
+    uint32_t run = tile_off[tile * 8 + p];
     for (int rr = 0; rr < 4; ++rr)
       for (int w = 0; w < 8; ++w) {
         const uint32_t c = wc[rr][w][p];
@@ -294,7 +289,7 @@ __device__ __forceinline__ void plan_rank_tile(const uint32_t* __restrict__ keys
   }
   __syncthreads();
   for (int r = 0; r < 4; ++r) {
-    const int i = blockIdx.x * kTile + r * 256 + threadIdx.x;
+    const int i = tile * kTile + r * 256 + threadIdx.x;
     if (i >= cap) continue;
     Cnt8 out{};
 #pragma unroll
@@ -310,17 +305,25 @@ __device__ __forceinline__ void plan_rank_tile(const uint32_t* __restrict__ keys
       lpos[i] = 0xFFFFFFFFu;
     }
   }
+  __syncthreads();  // wc is reused by the CTA's next tile
 }
 
+
 // blockIdx.y = 0: receive plan over the uniques; 1: send plan over my owned uniques
+// (send_only: blockIdx.y = 0 is the send plan). Persistent over the table's tiles; tiles past
+// the live count are neither counted nor ranked (the tile scan stops at the last live one)
 __global__ void __launch_bounds__(256) plan_count_kernel(
     const uint32_t* __restrict__ uniq, const int32_t* __restrict__ U,
     const uint32_t* __restrict__ own_k, const int32_t* __restrict__ n_own, int cap,
     const uint32_t* __restrict__ tm, uint32_t W, uint32_t me, int ntiles,
-    uint32_t* __restrict__ tile_cnt) {
+    uint32_t* __restrict__ tile_cnt, int send_only) {
   pdl_wait();
-  if (blockIdx.y == 0) plan_count_tile<false>(uniq, U, cap, tm, W, me, tile_cnt);
-  else plan_count_tile<true>(own_k, n_own, cap, tm, W, me, tile_cnt + ntiles * 8);
+  const bool send = send_only || blockIdx.y == 1;
+  const int32_t live = send ? *n_own : *U;
+  for (int tile = blockIdx.x; tile < ntiles && tile * kTile < live; tile += gridDim.x) {
+    if (send) plan_count_tile<true>(tile, own_k, n_own, cap, tm, W, me, tile_cnt + ntiles * 8);
+    else plan_count_tile<false>(tile, uniq, U, cap, tm, W, me, tile_cnt);
+  }
 }
 
 __global__ void __launch_bounds__(256) plan_rank_kernel(
@@ -328,13 +331,17 @@ __global__ void __launch_bounds__(256) plan_rank_kernel(
     const uint32_t* __restrict__ own_k, const int32_t* __restrict__ n_own, int cap,
     const uint32_t* __restrict__ tm, uint32_t W, uint32_t me, int ntiles,
     const uint32_t* __restrict__ tile_off, const int32_t* __restrict__ totals,
-    Cnt8* __restrict__ sscan, uint32_t* __restrict__ lpos) {
+    Cnt8* __restrict__ sscan, uint32_t* __restrict__ lpos, int send_only) {
   pdl_wait();
-  if (blockIdx.y == 0)
-    plan_rank_tile<false>(uniq, U, cap, tm, W, me, tile_off, totals, nullptr, lpos);
-  else
-    plan_rank_tile<true>(own_k, n_own, cap, tm, W, me, tile_off + ntiles * 8, totals, sscan,
-                         nullptr);
+  const bool send = send_only || blockIdx.y == 1;
+  const int32_t live = send ? *n_own : *U;
+  for (int tile = blockIdx.x; tile < ntiles && tile * kTile < live; tile += gridDim.x) {
+    if (send)
+      plan_rank_tile<true>(tile, own_k, n_own, cap, tm, W, me, tile_off + ntiles * 8, totals,
+                           sscan, nullptr);
+    else
+      plan_rank_tile<false>(tile, uniq, U, cap, tm, W, me, tile_off, totals, nullptr, lpos);
+  }
 }
 
 }  // namespace
@@ -351,13 +358,14 @@ void Exchange::plan(const uint32_t* d_vid, int64_t n_global, int64_t per_worker,
   CUDA_LAUNCH_CHECK();
   hook("plan_touch");
   // receive plan (y = 0, over the uniques) and send plan (y = 1, over my owned uniques)
-  launch_pdl(plan_count_kernel, dim3(dim3(ntiles, 2)), dim3(256), 0, s, d_uniq, d_U, d_own_k, d_n_own, c, tm, W, me,
-                                                    ntiles, tile_cnt);
+  const int gx = std::max(1, std::min(ntiles, num_sms() * 4));  // persistent over the tiles
+  launch_pdl(plan_count_kernel, dim3(gx, 2), dim3(256), 0, s, d_uniq, d_U, d_own_k, d_n_own, c,
+             tm, W, me, ntiles, tile_cnt, 0);
   CUDA_LAUNCH_CHECK();
   launch_pdl(plan_scan_tiles_kernel, dim3(1), dim3(512), 0, s, tile_cnt, ntiles, tile_off, totals, d_U, d_n_own);
   CUDA_LAUNCH_CHECK();
-  launch_pdl(plan_rank_kernel, dim3(dim3(ntiles, 2)), dim3(256), 0, s, d_uniq, d_U, d_own_k, d_n_own, c, tm, W, me,
-                                                   ntiles, tile_off, totals, sscan, lpos);
+  launch_pdl(plan_rank_kernel, dim3(gx, 2), dim3(256), 0, s, d_uniq, d_U, d_own_k, d_n_own, c, tm,
+             W, me, ntiles, tile_off, totals, sscan, lpos, 0);
   CUDA_LAUNCH_CHECK();
   hook("plan_rank");
   // every peer's layout (peer-store transport)
@@ -373,13 +381,14 @@ void Exchange::plan_send(const uint32_t* d_own_k, const int32_t* d_n_own, const 
                          cudaStream_t s) {
   const int c = static_cast<int>(cap);
   const int ntiles = ceil_div(c, kTile);
-  launch_pdl(plan_count_kernel, dim3(dim3(ntiles, 2)), dim3(256), 0, s, d_own_k, d_zero, d_own_k, d_n_own, c, tm, W, me,
-                                                    ntiles, tile_cnt);
+  const int gx = std::max(1, std::min(ntiles, num_sms() * 4));  // persistent, send table only
+  launch_pdl(plan_count_kernel, dim3(gx, 1), dim3(256), 0, s, d_own_k, d_zero, d_own_k, d_n_own,
+             c, tm, W, me, ntiles, tile_cnt, 1);
   CUDA_LAUNCH_CHECK();
   launch_pdl(plan_scan_tiles_kernel, dim3(1), dim3(512), 0, s, tile_cnt, ntiles, tile_off, totals, d_zero, d_n_own);
   CUDA_LAUNCH_CHECK();
-  launch_pdl(plan_rank_kernel, dim3(dim3(ntiles, 2)), dim3(256), 0, s, d_own_k, d_zero, d_own_k, d_n_own, c, tm, W, me,
-                                                   ntiles, tile_off, totals, sscan, lpos);
+  launch_pdl(plan_rank_kernel, dim3(gx, 1), dim3(256), 0, s, d_own_k, d_zero, d_own_k, d_n_own,
+             c, tm, W, me, ntiles, tile_off, totals, sscan, lpos, 1);
   CUDA_LAUNCH_CHECK();
 }
 
