@@ -883,7 +883,8 @@ void CacheLane::select_owned(const uint32_t* d_gids, const int32_t* d_U, int32_t
                              uint32_t w, uint32_t* vsi_first, cudaStream_t s) {
   if (cap <= 0) return;
   if (W == 1) {  // a single worker owns every unique: own_k = identity, count = U
-    launch_pdl(own_all_kernel, dim3(mgr_grid(ceil_div(cap, 256))), dim3(256), 0, s, d_U, own_k, counters + kCntOwned, d_gids, vsi_first);
+    launch_pdl(own_all_kernel, dim3(mgr_grid(std::min(ceil_div(cap, 256), num_sms() * 8))), dim3(256),
+               0, s, d_U, own_k, counters + kCntOwned, d_gids, vsi_first);
     CUDA_LAUNCH_CHECK();
     return;
   }

@@ -333,7 +333,8 @@ void zero_rows_b(const int32_t* d_n, int32_t n_bound, int d, float* dG, float* B
   SFB_CHECK((d & 3) == 0, "zero_rows_b needs d % 4 == 0");
   if (n_bound <= 0) return;
   // manager stage: a capped grid (mgr_grid), not a full wave of resident CTAs
-  launch_pdl(zero_rows_b_kernel, dim3(mgr_grid(ceil_div(static_cast<int64_t>(n_bound) * (d / 4), 256))), dim3(256), 0, s, d_n, d / 4, reinterpret_cast<float4*>(dG), B);
+  launch_pdl(zero_rows_b_kernel, dim3(mgr_grid(wave_grid(static_cast<int64_t>(n_bound) * (d / 4)))),
+             dim3(256), 0, s, d_n, d / 4, reinterpret_cast<float4*>(dG), B);
   CUDA_LAUNCH_CHECK();
 }
 

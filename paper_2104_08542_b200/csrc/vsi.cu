@@ -302,7 +302,7 @@ void vsi_device(VsiScratch& v, const uint32_t* d_ids, int64_t n, uint32_t* d_gid
                      d_unique, s);
     launch_pdl(vsi_hash_vid_kernel, dim3(grid), dim3(256), 0, s, v.d_hslot, n, v.d_first, d_vids);
     CUDA_LAUNCH_CHECK();
-    launch_pdl(vsi_hash_reset_kernel<uint32_t>, dim3(grid), dim3(256), 0, s, v.d_uslot, d_unique, v.d_hkeys32, v.d_first);
+    launch_pdl(vsi_hash_reset_kernel<uint32_t>, dim3(std::min(grid, num_sms() * 8)), dim3(256), 0, s, v.d_uslot, d_unique, v.d_hkeys32, v.d_first);
     CUDA_LAUNCH_CHECK();
     return;
   }
@@ -313,7 +313,7 @@ void vsi_device(VsiScratch& v, const uint32_t* d_ids, int64_t n, uint32_t* d_gid
   launch_pdl(vsi_vid_kernel, dim3(grid), dim3(256), 0, s, d_ids, n, v.d_first, d_vids);
   CUDA_LAUNCH_CHECK();
   if (reset) {
-    launch_pdl(vsi_reset_kernel, dim3(grid), dim3(256), 0, s, d_gids, d_unique, v.d_first);
+    launch_pdl(vsi_reset_kernel, dim3(std::min(grid, num_sms() * 8)), dim3(256), 0, s, d_gids, d_unique, v.d_first);
     CUDA_LAUNCH_CHECK();
   }
 }
@@ -330,7 +330,7 @@ void vsi_device_hashed(VsiScratch& v, const uint64_t* d_ids, int64_t n, uint64_t
                    d_unique, s);
   launch_pdl(vsi_hash_vid_kernel, dim3(grid), dim3(256), 0, s, v.d_hslot, n, v.d_first, d_vids);
   CUDA_LAUNCH_CHECK();
-  launch_pdl(vsi_hash_reset_kernel<unsigned long long>, dim3(grid), dim3(256), 0, s, v.d_uslot, d_unique, v.d_hkeys, v.d_first);
+  launch_pdl(vsi_hash_reset_kernel<unsigned long long>, dim3(std::min(grid, num_sms() * 8)), dim3(256), 0, s, v.d_uslot, d_unique, v.d_hkeys, v.d_first);
   CUDA_LAUNCH_CHECK();
 }
 
