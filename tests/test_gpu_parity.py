@@ -12,6 +12,8 @@ Bars (stated per test):
 import ctypes as C
 import hashlib
 
+import os
+
 import numpy as np
 import pytest
 
@@ -469,3 +471,26 @@ def test_deterministic_runs_are_bit_identical(mode):
     for a, b in zip(d1[:3], d2[:3]):
         assert np.array_equal(a, b)
     run_parity(cfg, 6)
+
+
+@pytest.mark.parametrize("mode", ["sequential", "pipelined"])
+def test_launch_switches_are_bit_identical(mode, tmp_path):
+    """The launch / scheduling switches change when kernels start, never what they compute:
+    programmatic dependent launch off (SFCTR_NO_PDL=1), the training stream at high priority
+    (SFCTR_STREAM_PRIO=train) and the row update not forked (SFCTR_NO_UPDATE_FORK=1) give
+    bit-identical losses, rows and dense state to the defaults (deterministic mode)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    worker = os.path.join(root, "tests", "launch_mode_worker.py")
+    outs = []
+    for k, env in enumerate([{}, {"SFCTR_NO_PDL": "1", "SFCTR_STREAM_PRIO": "train",
+                                  "SFCTR_NO_UPDATE_FORK": "1"}]):
+        out = str(tmp_path / f"run{k}.npz")
+        r = subprocess.run([sys.executable, worker, out, mode], capture_output=True, text=True,
+                           timeout=600, env={**os.environ, **env})
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+        outs.append(np.load(out))
+    for key in ("losses", "f", "r", "s", "p", "m", "v"):
+        assert np.array_equal(outs[0][key], outs[1][key]), key
+
