@@ -344,6 +344,87 @@ __global__ void __launch_bounds__(256) plan_rank_kernel(
   }
 }
 
+// The send plan of the owner-sharded manager in one kernel: its producer (shardplan.cu's
+// first-position emit) already counted the owned uniques per (1024-row tile, destination) in
+// tile_cnt, and own_k is the identity. Each CTA sums the counts of the tiles before its own
+// (at most a few hundred) instead of a separate tile scan; block 0 also writes the totals.
+__global__ void __launch_bounds__(256) send_rank_counted_kernel(
+    const int32_t* __restrict__ n_own_p, const uint32_t* __restrict__ tm, uint32_t W, int cap,
+    const uint32_t* __restrict__ tile_cnt, Cnt8* __restrict__ sscan, int32_t* __restrict__ totals) {
+  pdl_wait();
+  __shared__ uint32_t red[8][8];  // [warp][plane]
+  __shared__ uint32_t off[8];
+  __shared__ uint32_t wc[4][8][8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const uint32_t wm = W >= 32 ? 0xFFFFFFFFu : (1u << W) - 1u;
+  const int32_t n_own = *n_own_p;
+  const int nt = (n_own + kTile - 1) / kTile;
+  auto sum_tiles = [&](int limit) {  // off[p] = sum of tile_cnt[q][p] over q < limit
+    uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int q = threadIdx.x; q < limit; q += blockDim.x) {
+      const uint4 a = reinterpret_cast<const uint4*>(tile_cnt)[2 * q];
+      const uint4 b = reinterpret_cast<const uint4*>(tile_cnt)[2 * q + 1];
+      acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
+      acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
+    }
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      uint32_t v = acc[p];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+      if (lane == 0) red[warp][p] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 8) {
+      uint32_t v = 0;
+      for (int w = 0; w < 8; ++w) v += red[w][threadIdx.x];
+      off[threadIdx.x] = v;
+    }
+    __syncthreads();
+  };
+  if (blockIdx.x == 0) {
+    sum_tiles(nt);
+    if (threadIdx.x < 8) totals[8 + threadIdx.x] = static_cast<int32_t>(off[threadIdx.x]);
+    __syncthreads();
+  }
+  for (int tile = blockIdx.x; tile < nt; tile += gridDim.x) {
+    sum_tiles(tile);
+    uint32_t m[4], pre[4][8];
+    for (int r = 0; r < 4; ++r) {
+      const int i = tile * kTile + r * 256 + threadIdx.x;
+      m[r] = i < n_own ? (tm[i] & wm) : 0u;
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        const unsigned b = __ballot_sync(0xFFFFFFFFu, (m[r] >> p) & 1u);
+        pre[r][p] = __popc(b & lt);
+        if (lane == 0) wc[r][warp][p] = __popc(b);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < 8) {  // plane p: exclusive prefix over (round, warp) in tile order
+      const int p = threadIdx.x;
+      uint32_t run = off[p];
+      for (int rr = 0; rr < 4; ++rr)
+        for (int w = 0; w < 8; ++w) {
+          const uint32_t c = wc[rr][w][p];
+          wc[rr][w][p] = run;
+          run += c;
+        }
+    }
+    __syncthreads();
+    for (int r = 0; r < 4; ++r) {
+      const int i = tile * kTile + r * 256 + threadIdx.x;
+      if (i >= n_own || i >= cap) continue;
+      Cnt8 out{};
+#pragma unroll
+      for (int p = 0; p < 8; ++p) out.c[p] = wc[r][warp][p] + pre[r][p];
+      sscan[i] = out;
+    }
+    __syncthreads();  // wc / off are reused by the CTA's next tile
+  }
+}
+
 }  // namespace
 
 void Exchange::plan(const uint32_t* d_vid, int64_t n_global, int64_t per_worker,
@@ -389,6 +470,15 @@ void Exchange::plan_send(const uint32_t* d_own_k, const int32_t* d_n_own, const 
   CUDA_LAUNCH_CHECK();
   launch_pdl(plan_rank_kernel, dim3(gx, 1), dim3(256), 0, s, d_own_k, d_zero, d_own_k, d_n_own,
              c, tm, W, me, ntiles, tile_off, totals, sscan, lpos, 1);
+  CUDA_LAUNCH_CHECK();
+}
+
+void Exchange::send_plan_counted(const int32_t* d_n_own, cudaStream_t s) {
+  const int c = static_cast<int>(cap);
+  const int ntiles = ceil_div(c, kTile);
+  launch_pdl(send_rank_counted_kernel, dim3(std::max(1, std::min(ntiles, num_sms() * 4))),
+             dim3(256), 0, s, d_n_own, static_cast<const uint32_t*>(tm), static_cast<uint32_t>(W),
+             c, static_cast<const uint32_t*>(tile_cnt), sscan, totals);
   CUDA_LAUNCH_CHECK();
 }
 

@@ -87,6 +87,11 @@ struct Exchange {
   // (owner-sharded manager, shardplan.cu): the receive plan is left empty
   void plan_send(const uint32_t* d_own_k, const int32_t* d_n_own, const int32_t* d_zero,
                  cudaStream_t s);
+  // the send plan when the producer of the owned uniques already counted them per
+  // (1024-row tile, destination) into tile_cnt (zeroed before) and own_k is the identity:
+  // one kernel (shardplan.cu); writes sscan and totals[8..16)
+  void send_plan_counted(const int32_t* d_n_own, cudaStream_t s);
+  int tile_words() const { return 8 * ((static_cast<int>(cap) + 1023) / 1024); }
   // the layout offsets (offs) from totals
   void plan_offsets(cudaStream_t s);
   void set_counts(const int32_t* h_totals);  // after the step's host wait

@@ -10,9 +10,9 @@
 //      in global first-appearance order (= the
 //      global_ids order of vsi.cpp:41-46 filtered by owner, as the replicated VSI produces
 //      it), the touched masks by owned index, own_k = identity
-//   4. plan: ranks of each owned unique among those each rank touches (Exchange::plan_send,
-//      the replicated path's own kernels), my column of the count matrix published to every
-//      rank with my unique count; flag barrier B2
+//   4. plan: ranks of each owned unique among those each rank touches (one kernel,
+//      Exchange::send_plan_counted, over per-tile counts the emit of step 3 accumulated), my
+//      column of the count matrix published to every rank with my unique count; barrier B2
 //   5. layout: the full matrix, my receive totals, U, my own rows' local-table rows (lpos)
 //   6. reply: for every pair it received the owner stores the local-table row of that
 //      position into its source's reply buffer, contiguously (pair i of region r -> r's
@@ -235,9 +235,13 @@ __global__ void __launch_bounds__(256) first_bits_kernel(const uint64_t* __restr
                                                          const int32_t* __restrict__ inbox,
                                                          const uint32_t* __restrict__ hslot,
                                                          const uint32_t* __restrict__ pos,
-                                                         uint32_t* __restrict__ bits) {
+                                                         uint32_t* __restrict__ bits,
+                                                         uint32_t* __restrict__ tile_cnt,
+                                                         int tile_words) {
   pdl_wait();
   const int r = blockIdx.y;
+  if (blockIdx.x == 0 && blockIdx.y == 0)  // the send plan's per-tile counts (3c adds to them)
+    for (int q = threadIdx.x; q < tile_words; q += blockDim.x) tile_cnt[q] = 0;
   const int64_t cnt = inbox[72 + r];
   const int64_t off = static_cast<int64_t>(r) * n;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < cnt;
@@ -266,7 +270,7 @@ __global__ void __launch_bounds__(256) first_emit_kernel(
     const uint32_t* __restrict__ bits, const uint32_t* __restrict__ wpre,
     const uint32_t* __restrict__ keys, const uint32_t* __restrict__ tmask,
     uint32_t* __restrict__ owned, uint32_t* __restrict__ own_k, uint32_t* __restrict__ tm,
-    uint32_t* __restrict__ uslot) {
+    uint32_t* __restrict__ uslot, uint32_t* __restrict__ tile_cnt) {
   pdl_wait();
   const int r = blockIdx.y;
   const int64_t cnt = inbox[72 + r];
@@ -280,9 +284,12 @@ __global__ void __launch_bounds__(256) first_emit_kernel(
     const uint32_t rank = wpre[p >> 5] + __popc(bits[p >> 5] & ((1u << (p & 31)) - 1u));
     owned[rank] = keys[sl];
     own_k[rank] = rank;
-    tm[rank] = tmask[sl];
+    const uint32_t mk = tmask[sl];
+    tm[rank] = mk;
     uslot[rank] = sl;
     pos[sl] = rank | kTagOwned;  // the slot now names its owned index
+    // the send plan's count of owned uniques per (1024-row tile, destination rank)
+    for (uint32_t m = mk; m; m &= m - 1) atomicAdd(tile_cnt + (rank >> 10) * 8 + (__ffs(m) - 1), 1u);
   }
 }
 
@@ -516,17 +523,18 @@ void ShardPlan::run(const uint64_t* d_ids, uint64_t vocab, int32_t* d_bad, int k
                                                  hslot);
   CUDA_LAUNCH_CHECK();
   hook("shard_dedup");
-  launch_pdl(first_bits_kernel, dim3(dim3(gx, W)), dim3(256), 0, s, prs, n, ibx, hslot, hpos, bits);
+  launch_pdl(first_bits_kernel, dim3(dim3(gx, W)), dim3(256), 0, s, prs, n, ibx, hslot, hpos, bits,
+             xch.tile_cnt, xch.tile_words());
   CUDA_LAUNCH_CHECK();
   hook("shard_first");
   lookback_scan<4>(tiles, nwords, WordCount{bits}, WordPrefix{wpre}, d_n_own, s);
   hook("shard_scan");
   launch_pdl(first_emit_kernel, dim3(dim3(gx, W)), dim3(256), 0, s, prs, n, ibx, hslot, hpos, bits, wpre, hkeys,
-                                                hmask_bits, owned_uniq, own_k, xch.tm, uslot);
+                                                hmask_bits, owned_uniq, own_k, xch.tm, uslot, xch.tile_cnt);
   CUDA_LAUNCH_CHECK();
   hook("shard_emit");
   // 4. send plan over my owned uniques, my column of the count matrix + my count; B2
-  xch.plan_send(own_k, d_n_own, zero, s);
+  xch.send_plan_counted(d_n_own, s);
   hook("shard_plan");
   launch_pdl(publish_barrier_kernel, dim3(1), dim3(32), 0, s, 1, pi, nullptr, xch.totals, d_n_own, pf, W, me, ++epoch,
                                           tmo, abort_flag, nullptr);
