@@ -55,6 +55,7 @@ struct DxParams {
   int F, d;
   int exp;              // experiment: 1 = no global reductions, 2 = no FM-sum loads
   unsigned long long* cta_trace;  // profiling (nullable): per-CTA [start, end] globaltimer
+  long long* trace;               // profiling (nullable): CTA 0 per-tile clock64 stamps
 };
 
 // smem for the scatter epilogue: value tile [128 x 68] f32, vid [128 x F] u32, gz [128]
@@ -177,7 +178,9 @@ __global__ void __launch_bounds__(dx_threads<SCATTER>(), 1)
       }
       const int s = i % BS, buf = i & 1;
       mbar_wait(acc_empty + buf, ((i >> 1) & 1) ^ 1);
+      if (p.trace && blockIdx.x == 0 && lane == 0 && i < 32) p.trace[i] = clock64();
       mbar_wait(b_full + s, (i / BS) & 1);
+      if (p.trace && blockIdx.x == 0 && lane == 0 && i < 32) p.trace[32 + i] = clock64();
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (elect_one()) {
         const uint32_t d = tmem + static_cast<uint32_t>(buf) * 128u;
@@ -263,6 +266,8 @@ __global__ void __launch_bounds__(dx_threads<SCATTER>(), 1)
                         : make_float4(0.f, 0.f, 0.f, 0.f);
       }
       mbar_wait(acc_full + buf, (i >> 1) & 1);
+      const bool trc = p.trace && blockIdx.x == 0 && et == 0 && i < 32;
+      if (trc) p.trace[64 + i] = clock64();
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       // (1) accumulator -> value tile, thread = row
       const uint32_t trow = tmem + static_cast<uint32_t>(buf) * 128u + lane_off;
@@ -281,6 +286,7 @@ __global__ void __launch_bounds__(dx_threads<SCATTER>(), 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(acc_empty + buf);  // the MMA of the next tile may start
       asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");
+      if (trc) p.trace[96 + i] = clock64();
       // (2) half-warp per row: lane & 15 = 16 B chunk of the tile's 64 columns
 #pragma unroll
       for (int u8 = 0; u8 < NB; ++u8) {
@@ -297,7 +303,9 @@ __global__ void __launch_bounds__(dx_threads<SCATTER>(), 1)
                      "f"(p.scale * a.z + k * fm[u8].z), "f"(p.scale * a.w + k * fm[u8].w));
         if (cc == 0) atomicAdd(p.Bsum + u, g);
       }
+      if (trc) p.trace[128 + i] = clock64();
       asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");  // value tile / tables free
+      if (trc) p.trace[160 + i] = clock64();
     }
   } else {  // ---------------- epilogue
     const int q = warp & 3;

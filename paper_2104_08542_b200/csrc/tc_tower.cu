@@ -373,8 +373,33 @@ void launch_dx_gemm(const TowerTC& tc_, const float* dh_hi, const float* dh_lo, 
     }
     static CtaTrace ct{"gemm2"};
     p.cta_trace = ct.arm(grid);
+    // SFCTR_DX_TRACE=n: launch n records CTA 0's per-tile clock64 stamps and prints them
+    static const int dx_trace_at = [] {
+      const char* e = std::getenv("SFCTR_DX_TRACE");
+      return e ? atoi(e) : -1;
+    }();
+    static int dx_launches = 0;
+    long long* trbuf = nullptr;
+    if (dx_launches++ == dx_trace_at) {
+      CUDA_CHECK(cudaMalloc(&trbuf, sizeof(long long) * 192));
+      CUDA_CHECK(cudaMemsetAsync(trbuf, 0, sizeof(long long) * 192, s));
+      p.trace = trbuf;
+    }
     launch_pdl(kern, dim3(grid), dim3(tc::dx_threads<true>()), smem, s, ah, al, bh, bl, bh, p);
     CUDA_LAUNCH_CHECK();
+    if (trbuf) {
+      long long h[192];
+      CUDA_CHECK(cudaStreamSynchronize(s));
+      CUDA_CHECK(cudaMemcpy(h, trbuf, sizeof(h), cudaMemcpyDeviceToHost));
+      cudaFree(trbuf);
+      const long long t0 = h[0];
+      fprintf(stderr, "dx trace (clk rel. to the first MMA acc wait): i mma_acc_ok mma_b_ok epi_acc_full epi_drained epi_scattered epi_done\n");
+      for (int i = 0; i < 32; ++i)
+        fprintf(stderr, "%2d %8lld %8lld %8lld %8lld %8lld %8lld\n", i, h[i] ? h[i] - t0 : -1,
+                h[32 + i] ? h[32 + i] - t0 : -1, h[64 + i] ? h[64 + i] - t0 : -1,
+                h[96 + i] ? h[96 + i] - t0 : -1, h[128 + i] ? h[128 + i] - t0 : -1,
+                h[160 + i] ? h[160 + i] - t0 : -1);
+    }
     return;
   }
   const CUtensorMap out = tmap(dX, K, rows, ldx, 32, 128);
