@@ -53,9 +53,15 @@ struct DxParams {
   float* dG;            // [rows x d] gradient table (red.add)
   float* Bsum;          // [rows] deferred FM coefficients (red.add)
   int F, d;
-  int exp;              // experiment: 1 = no global reductions, 2 = no FM-sum loads
+  int exp;              // experiment: 1 = no global reductions, 2 = no FM-sum loads,
+                        // 3 = drain the accumulator only (no tile, no scatter)
   unsigned long long* cta_trace;  // profiling (nullable): per-CTA [start, end] globaltimer
   long long* trace;               // profiling (nullable): CTA 0 per-tile clock64 stamps
+  // SCATTER: the A operand (dh hi / lo, [rows x lda], pre-split) is written into TMEM by
+  // four A-writer warps once per 128-row tile and the MMAs read it from there (TS form)
+  const float* a_hi;
+  const float* a_lo;
+  int lda;
 };
 
 // smem for the scatter epilogue: value tile [128 x 68] f32, vid [128 x F] u32, gz [128]
@@ -78,7 +84,9 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
 #endif
 constexpr int kDxScatterWarps = SFB_DX_EW;  // 4 per TMEM lane quarter
 template <bool SCATTER>
-constexpr int dx_threads() { return SCATTER ? 64 + 32 * kDxScatterWarps : 192; }
+constexpr int dx_threads() { return SCATTER ? 64 + 32 * kDxScatterWarps + 128 : 192; }
+constexpr int kDxAWriter0 = 2 + kDxScatterWarps;  // first of the 4 A-writer warps (SCATTER)
+constexpr uint32_t kDxTmemA = 256;                 // TMEM column of A (SCATTER): hi [0,64), lo [64,128)
 
 template <bool SCATTER>
 __global__ void __launch_bounds__(dx_threads<SCATTER>(), 1)
@@ -110,7 +118,7 @@ __global__ void __launch_bounds__(dx_threads<SCATTER>(), 1)
   const int t1 = static_cast<int>(static_cast<long long>(blockIdx.x + 1) * p.tiles / gridDim.x);
 
   if (threadIdx.x == 0) {
-    mbar_init(a_full, 1);
+    mbar_init(a_full, SCATTER ? 4 : 1);  // SCATTER: the four A-writer warps
     mbar_init(a_empty, 1);
     for (int s = 0; s < BS; ++s) {
       mbar_init(b_full + s, 1);
@@ -126,8 +134,8 @@ __global__ void __launch_bounds__(dx_threads<SCATTER>(), 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmOut)) : "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
-        smem_u32(tmem_holder)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+        smem_u32(tmem_holder)), "n"(SCATTER ? 512 : 256));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -142,12 +150,14 @@ __global__ void __launch_bounds__(dx_threads<SCATTER>(), 1)
       for (int t = t0, i = 0; t < t1; ++t, ++i) {
         const int m = t / p.n_tiles, n = t - m * p.n_tiles;
         if (m != cur_m) {
-          if (gen > 0) mbar_wait(a_empty, (gen - 1) & 1);
-          mbar_expect_tx(a_full, L::A_BYTES);
+          if constexpr (!SCATTER) {  // (SCATTER: A goes to TMEM through the A-writer warps)
+            if (gen > 0) mbar_wait(a_empty, (gen - 1) & 1);
+            mbar_expect_tx(a_full, L::A_BYTES);
 #pragma unroll
-          for (int kb = 0; kb < 2; ++kb) {
-            tma_load_2d(&tmAhi, a_full, a_s + kb * L::A_PART, kb * BKE, m * BM);
-            tma_load_2d(&tmAlo, a_full, a_s + (2 + kb) * L::A_PART, kb * BKE, m * BM);
+            for (int kb = 0; kb < 2; ++kb) {
+              tma_load_2d(&tmAhi, a_full, a_s + kb * L::A_PART, kb * BKE, m * BM);
+              tma_load_2d(&tmAlo, a_full, a_s + (2 + kb) * L::A_PART, kb * BKE, m * BM);
+            }
           }
           cur_m = m;
           ++gen;
@@ -190,10 +200,16 @@ __global__ void __launch_bounds__(dx_threads<SCATTER>(), 1)
 #pragma unroll
           for (int kk = 0; kk < BKE / 8; ++kk) {
             const uint64_t bd = smem_desc(bs + 2 * kb * L::B_PART + kk * 32, 16, 1024);  // [hi; lo]
-            const uint64_t ah = smem_desc(as + kb * L::A_PART + kk * 32, 16, 1024);
-            const uint64_t al = smem_desc(as + (2 + kb) * L::A_PART + kk * 32, 16, 1024);
-            mma_tf32(d, ah, bd, id128, (kb > 0 || kk > 0) ? 1u : 0u);
-            mma_tf32(d, al, bd, id64, 1u);
+            if constexpr (SCATTER) {  // A from TMEM: no shared-memory A reads per tile
+              const uint32_t at = tmem + kDxTmemA + static_cast<uint32_t>(kb * 32 + kk * 8);
+              mma_tf32_ts(d, at, bd, id128, (kb > 0 || kk > 0) ? 1u : 0u);
+              mma_tf32_ts(d, at + 64u, bd, id64, 1u);
+            } else {
+              const uint64_t ah = smem_desc(as + kb * L::A_PART + kk * 32, 16, 1024);
+              const uint64_t al = smem_desc(as + (2 + kb) * L::A_PART + kk * 32, 16, 1024);
+              mma_tf32(d, ah, bd, id128, (kb > 0 || kk > 0) ? 1u : 0u);
+              mma_tf32(d, al, bd, id64, 1u);
+            }
           }
         }
         mma_commit(b_empty + s);
@@ -202,6 +218,42 @@ __global__ void __launch_bounds__(dx_threads<SCATTER>(), 1)
         if (t + 1 >= t1 || mn != m) mma_commit(a_empty);
       }
       __syncwarp();
+    }
+  } else if (SCATTER && warp >= kDxAWriter0) {  // ---------------- A writer (SCATTER)
+    // dh hi / lo rows of the current 128-row tile into TMEM columns [kDxTmemA, +128): warp
+    // (lane quarter q) writes rows 32 q .. 32 q + 31, thread = row; once per tile row, after
+    // the MMAs of the previous one have completed (a_empty)
+    const int q = warp & 3;
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    int cur_m = -1, gen = 0;
+    for (int t = t0; t < t1; ++t) {
+      const int m = t / p.n_tiles;
+      if (m == cur_m) continue;
+      if (gen > 0) mbar_wait(a_empty, (gen - 1) & 1);
+      const int row = m * BM + q * 32 + lane;
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+      for (int part = 0; part < 4; ++part) {  // hi k 0-31, hi k 32-63, lo k 0-31, lo k 32-63
+        const float* src = (part < 2 ? p.a_hi : p.a_lo) + static_cast<int64_t>(row) * p.lda +
+                           (part & 1) * 32;
+        float v[32];
+#pragma unroll
+        for (int k4 = 0; k4 < 8; ++k4) {
+          const float4 x = row < p.M ? __ldg(reinterpret_cast<const float4*>(src) + k4)
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+          v[4 * k4] = x.x;
+          v[4 * k4 + 1] = x.y;
+          v[4 * k4 + 2] = x.z;
+          v[4 * k4 + 3] = x.w;
+        }
+        tmem_st32(tmem + kDxTmemA + static_cast<uint32_t>(part * 32) + lane_off, v);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(a_full);
+      cur_m = m;
+      ++gen;
     }
   } else if constexpr (SCATTER) {  // ---------------- scatter epilogue (segment sum)
     const int q = warp & 3;
@@ -277,6 +329,10 @@ __global__ void __launch_bounds__(dx_threads<SCATTER>(), 1)
         tmem_ld16(trow + c0, v);
         tmem_ld16(trow + 64 + c0, w);
         float4* dst = reinterpret_cast<float4*>(tile + row * kDxTileStride + c0);
+        if (p.exp == 3) {  // experiment: drain only (no shared-memory tile, no scatter)
+          if (v[0] + w[0] == 12345.f) p.dG[0] = v[1];
+          continue;
+        }
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj)
           dst[jj] = make_float4(v[4 * jj] + w[4 * jj], v[4 * jj + 1] + w[4 * jj + 1],
@@ -289,7 +345,7 @@ __global__ void __launch_bounds__(dx_threads<SCATTER>(), 1)
       if (trc) p.trace[96 + i] = clock64();
       // (2) half-warp per row: lane & 15 = 16 B chunk of the tile's 64 columns
 #pragma unroll
-      for (int u8 = 0; u8 < NB; ++u8) {
+      for (int u8 = 0; u8 < NB && p.exp != 3; ++u8) {
         const int rr = 2 * EW * u8 + 2 * ew + (lane >> 4);
         if (!ok[u8]) continue;
         const float4 a = *reinterpret_cast<const float4*>(tile + rr * kDxTileStride + 4 * j);
@@ -355,7 +411,8 @@ __global__ void __launch_bounds__(dx_threads<SCATTER>(), 1)
   if (p.cta_trace && threadIdx.x == 0) p.cta_trace[2 * blockIdx.x + 1] = global_ns();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(SCATTER ? 512 : 256));
   }
 }
 

@@ -350,6 +350,9 @@ void launch_dx_gemm(const TowerTC& tc_, const float* dh_hi, const float* dh_lo, 
   }();
   const int grid = std::min(p.tiles, dx_grid ? dx_grid : sm_count());
   if (sc) {
+    p.a_hi = dh_hi;
+    p.a_lo = dh_lo;
+    p.lda = tc_.ldh;
     p.vid = sc->vid;
     p.remap = sc->remap;
     p.fm_s = sc->fm_s;
