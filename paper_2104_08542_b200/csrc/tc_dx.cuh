@@ -62,6 +62,8 @@ struct DxParams {
   const float* a_hi;
   const float* a_lo;
   int lda;
+  int epi;  // SCATTER epilogue: 0 = through a shared-memory value tile (half-warp per row),
+            // 1 = warp-local register transpose (no tile, no per-tile block barriers)
 };
 
 // smem for the scatter epilogue: value tile [128 x 68] f32, vid [128 x F] u32, gz [128]
@@ -272,6 +274,10 @@ __global__ void __launch_bounds__(dx_threads<SCATTER>(), 1)
       const int m = t / p.n_tiles, n = t - m * p.n_tiles;
       const int buf = i & 1;
       const int r0 = m * BM;
+      // epi 1 has no per-tile barrier: every warp must be past the previous tile row's
+      // scatter before its tables are restaged, and the staging done before they are read
+      if (p.epi == 1 && m != cur_m && cur_m >= 0)
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");
       if (m != cur_m) {  // stage this m-tile's vid / gz (the previous tile's scatter is done)
         // 8 independent loads in flight per thread (a plain loop is a chain of dependent
         // L2 round trips: ~10 per thread per m-tile, twice that with the remap)
@@ -299,6 +305,66 @@ __global__ void __launch_bounds__(dx_threads<SCATTER>(), 1)
         }
         if (et < BM) gz_s[et] = r0 + et < p.M ? __ldg(p.gz + r0 + et) : 0.f;
         cur_m = m;
+        if (p.epi == 1) asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");
+      }
+      if (p.epi == 1) {
+        // warp (q, h) owns rows 32 q .. 32 q + 31 and columns 16 h .. 16 h + 15 of the tile.
+        // After the TMEM drain (thread = row) a register transpose gives, for k = 0..3, lane l
+        // the 16 B chunk (l & 3) of row 8 k + (l >> 2): each red covers 8 rows x 64 B
+        const int cl = lane & 3;
+        const int col = n * 64 + 16 * h + 4 * cl;
+        const int f = col / d, cc = col - f * d;
+        float4 fmk[4];
+        bool okk[4];
+        int rrk[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          rrk[k] = q * 32 + 8 * k + (lane >> 2);
+          okk[k] = r0 + rrk[k] < p.M && col < p.N;
+          fmk[k] = okk[k] && p.exp != 2 ? __ldg(reinterpret_cast<const float4*>(
+                                             p.fm_s + static_cast<int64_t>(r0 + rrk[k]) * d + cc))
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        mbar_wait(acc_full + buf, (i >> 1) & 1);
+        const bool trc = p.trace && blockIdx.x == 0 && et == 0 && i < 32;
+        if (trc) p.trace[64 + i] = clock64();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t trow = tmem + static_cast<uint32_t>(buf) * 128u + lane_off;
+        float v[16], w[16];
+        tmem_ld16(trow + 16 * h, v);
+        tmem_ld16(trow + 64 + 16 * h, w);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) v[c] += w[c];
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_empty + buf);  // the MMA of the next tile may start
+        if (trc) p.trace[96 + i] = clock64();
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int src = 8 * k + (lane >> 2);
+          float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {  // the source row's chunk c; lane keeps c == cl
+            const float x0 = __shfl_sync(0xFFFFFFFFu, v[4 * c], src);
+            const float x1 = __shfl_sync(0xFFFFFFFFu, v[4 * c + 1], src);
+            const float x2 = __shfl_sync(0xFFFFFFFFu, v[4 * c + 2], src);
+            const float x3 = __shfl_sync(0xFFFFFFFFu, v[4 * c + 3], src);
+            if (c == cl) a = make_float4(x0, x1, x2, x3);
+          }
+          if (!okk[k] || p.exp == 1 || p.exp == 3) continue;
+          const int rr = rrk[k];
+          const float g = gz_s[rr];
+          const float kf = p.scale * g;
+          const uint32_t u = vid_s[rr * F + f];
+          float* dstg = p.dG + static_cast<int64_t>(u) * d + cc;
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dstg),
+                       "f"(p.scale * a.x + kf * fmk[k].x), "f"(p.scale * a.y + kf * fmk[k].y),
+                       "f"(p.scale * a.z + kf * fmk[k].z), "f"(p.scale * a.w + kf * fmk[k].w));
+          if (cc == 0) atomicAdd(p.Bsum + u, g);
+        }
+        if (trc) p.trace[128 + i] = clock64();
+        if (trc) p.trace[160 + i] = clock64();
+        continue;
       }
       // (0) this tile's FM sums (they do not depend on the accumulator): loads issued
       // before the wait, so their L2 latency overlaps the MMA / TMEM drain

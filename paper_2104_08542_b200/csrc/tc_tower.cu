@@ -366,6 +366,11 @@ void launch_dx_gemm(const TowerTC& tc_, const float* dh_hi, const float* dh_lo, 
       return e ? atoi(e) : 0;
     }();
     p.exp = dx_exp;
+    static const int dx_epi = [] {  // SFCTR_DX_EPI=0|1 (tc_dx.cuh DxParams::epi)
+      const char* e = std::getenv("SFCTR_DX_EPI");
+      return e ? atoi(e) : 1;
+    }();
+    p.epi = dx_epi;
     auto kern = tc::gemm_dx_persistent_kernel<true>;
     const int smem = 1024 + tc::DxLayout::A_BYTES + tc::DxLayout::B_STAGES * tc::DxLayout::B_STAGE +
                      ((tc::dx_scatter_bytes(p.F, p.d) + 15) & ~15) + 256;
