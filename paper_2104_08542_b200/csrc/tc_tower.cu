@@ -366,9 +366,12 @@ void launch_dx_gemm(const TowerTC& tc_, const float* dh_hi, const float* dh_lo, 
       return e ? atoi(e) : 0;
     }();
     p.exp = dx_exp;
-    static const int dx_epi = [] {  // SFCTR_DX_EPI=0|1 (tc_dx.cuh DxParams::epi)
+    // SFCTR_DX_EPI=0|1 (tc_dx.cuh DxParams::epi). 0 (default): the value-tile epilogue; 1,
+    // the register transpose, measured level on the step (+1 % e2e, within noise on value)
+    // but 2-3 us slower as a kernel alone
+    static const int dx_epi = [] {
       const char* e = std::getenv("SFCTR_DX_EPI");
-      return e ? atoi(e) : 1;
+      return e ? atoi(e) : 0;
     }();
     p.epi = dx_epi;
     auto kern = tc::gemm_dx_persistent_kernel<true>;
