@@ -62,6 +62,7 @@ struct DxParams {
   const float* a_hi;
   const float* a_lo;
   int lda;
+  int H;    // contraction length (<= 64): A columns >= H are written as zeros
   int epi;  // SCATTER epilogue: 0 = through a shared-memory value tile (half-warp per row),
             // 1 = warp-local register transpose (no tile, no per-tile block barriers)
 };
@@ -241,8 +242,17 @@ __global__ void __launch_bounds__(dx_threads<SCATTER>(), 1)
         float v[32];
 #pragma unroll
         for (int k4 = 0; k4 < 8; ++k4) {
-          const float4 x = row < p.M ? __ldg(reinterpret_cast<const float4*>(src) + k4)
-                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+          const int k = (part & 1) * 32 + 4 * k4;  // column of dh (contraction index)
+          float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (row < p.M) {
+            if (k + 4 <= p.H) {
+              x = __ldg(reinterpret_cast<const float4*>(src) + k4);
+            } else if (k < p.H) {  // the row's last partial group (H % 4 != 0)
+              x.x = __ldg(src + 4 * k4);
+              if (k + 1 < p.H) x.y = __ldg(src + 4 * k4 + 1);
+              if (k + 2 < p.H) x.z = __ldg(src + 4 * k4 + 2);
+            }
+          }
           v[4 * k4] = x.x;
           v[4 * k4 + 1] = x.y;
           v[4 * k4 + 2] = x.z;

@@ -353,6 +353,7 @@ void launch_dx_gemm(const TowerTC& tc_, const float* dh_hi, const float* dh_lo, 
     p.a_hi = dh_hi;
     p.a_lo = dh_lo;
     p.lda = tc_.ldh;
+    p.H = H;
     p.vid = sc->vid;
     p.remap = sc->remap;
     p.fm_s = sc->fm_s;
