@@ -102,8 +102,8 @@ __global__ void __launch_bounds__(dx_threads<SCATTER>(), 1)
   constexpr int BS = L::B_STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_1024(smem_raw);
-  uint8_t* a_s = smem;
-  uint8_t* b_s = smem + L::A_BYTES;
+  uint8_t* a_s = smem;  // SCATTER: A lives in TMEM, no shared-memory A region
+  uint8_t* b_s = smem + (SCATTER ? 0 : L::A_BYTES);
   uint8_t* out_s = b_s + BS * L::B_STAGE;  // TMA-store staging, or the scatter tables
   uint64_t* bars = reinterpret_cast<uint64_t*>(
       out_s + (SCATTER ? ((dx_scatter_bytes(p.F, p.d) + 15) & ~15) : L::OUT_BYTES));

@@ -376,7 +376,7 @@ void launch_dx_gemm(const TowerTC& tc_, const float* dh_hi, const float* dh_lo, 
     }();
     p.epi = dx_epi;
     auto kern = tc::gemm_dx_persistent_kernel<true>;
-    const int smem = 1024 + tc::DxLayout::A_BYTES + tc::DxLayout::B_STAGES * tc::DxLayout::B_STAGE +
+    const int smem = 1024 + tc::DxLayout::B_STAGES * tc::DxLayout::B_STAGE +  // (A in TMEM)
                      ((tc::dx_scatter_bytes(p.F, p.d) + 15) & ~15) + 256;
     static int configured = 0;
     if (smem > configured) {
