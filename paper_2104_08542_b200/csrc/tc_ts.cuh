@@ -3,10 +3,9 @@
 // Used for the tower's two X-streaming GEMMs (N = H = 64, K or M = the 3120-wide
 // activation): they are HBM streams of X with a skinny MMA, so the design goal is
 // bytes in flight, not MMA shape.
-//   * raw A tiles land by TMA in a deep smem ring (kTsARing x 16 KB) that is
-//     released as soon as the split warps have read a tile — not when the MMA is
-//     done — so ~7 tiles of X are always in flight per SM (Little's law at
-//     ~1.5 us loaded DRAM latency);
+//   * raw A tiles land by TMA in a smem ring (kTsARing x 16 KB) that is released as
+//     soon as the split warps have read a tile — not when the MMA is done — so ~5 tiles
+//     of X are always in flight per SM (Little's law at ~1.5 us loaded DRAM latency);
 //   * the split warps (thread = TMEM lane = A row; two warp groups taking alternate
 //     k-blocks) round the row to tf32 hi/lo in registers and write both parts
 //     straight into a TMEM stage (tcgen05.st);
@@ -30,14 +29,19 @@
 namespace sfb {
 namespace tc {
 
+// 6 raw A tiles: 161 KB of shared memory per CTA instead of 193 KB with 8, which leaves room
+// for the manager stage's CTAs beside the GEMM (+1.5 % at cfg2 N = 1; 6 tiles = ~2 us of
+// X in flight at ~700 clk per k-block still covers the loaded DRAM latency)
 #ifndef SFB_TS_ARING
-#define SFB_TS_ARING 8
+#define SFB_TS_ARING 6
 #endif
 #ifndef SFB_TS_BRING
 #define SFB_TS_BRING 4
 #endif
 constexpr int kTsARing = SFB_TS_ARING;  // raw A tiles (smem)
 constexpr int kTsBRing = SFB_TS_BRING;  // B hi/lo tiles (smem)
+// (odd ring depths crashed when tried: the two split groups take alternate k-blocks)
+static_assert(kTsARing % 2 == 0 && kTsBRing % 2 == 0, "ring depths must be even");
 constexpr int kTsStages = 6;  // TMEM A stages: 128 accumulator columns + 6 x 64 = 512
 constexpr int kTsThreads = 352;  // 11 warps: A producer, MMA, 8 split/epilogue, B producer
 
