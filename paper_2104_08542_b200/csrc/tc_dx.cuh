@@ -35,7 +35,10 @@ struct DxLayout {
   static constexpr int A_BYTES = 4 * A_PART;      // hi kb0, hi kb1, lo kb0, lo kb1
   static constexpr int B_PART = 64 * BKE * 4;     // 8 KB: 64 n x 32 k
   static constexpr int B_STAGE = 4 * B_PART;      // kb0 [hi; lo], kb1 [hi; lo]
-  static constexpr int B_STAGES = 3;
+#ifndef SFB_DX_BSTAGES
+#define SFB_DX_BSTAGES 3
+#endif
+  static constexpr int B_STAGES = SFB_DX_BSTAGES;
   static constexpr int OUT_BYTES = BM * 64 * 4;   // 32 KB staging (2 boxes of 32 columns)
   static constexpr int SMEM = 1024 + A_BYTES + B_STAGES * B_STAGE + OUT_BYTES + 256;
 };
