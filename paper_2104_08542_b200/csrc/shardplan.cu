@@ -6,10 +6,10 @@
 //   2. dedup: the owner inserts the pairs it received into a hashed table (match_any merges
 //      a warp's equal ids first): min global position and touched-by-rank mask per feature
 //   3. order: a bit at every owned unique's first global position, one fused look-back scan
-//      over the bitmap words, then each unique's rank among the set bits -> owned uniques
-//      in global first-appearance order (= the
-//      global_ids order of vsi.cpp:41-46 filtered by owner, as the replicated VSI produces
-//      it), the touched masks by owned index, own_k = identity
+//      over the bitmap words, then each unique's rank among the set bits -> owned uniques in
+//      global first-appearance order (= the global_ids order of vsi.cpp:41-46 filtered by
+//      owner, as the replicated VSI produces it), the touched masks by owned index,
+//      own_k = identity, and the send plan's per-(tile, destination) counts
 //   4. plan: ranks of each owned unique among those each rank touches (one kernel,
 //      Exchange::send_plan_counted, over per-tile counts the emit of step 3 accumulated), my
 //      column of the count matrix published to every rank with my unique count; barrier B2
