@@ -458,21 +458,6 @@ void Exchange::plan(const uint32_t* d_vid, int64_t n_global, int64_t per_worker,
   CUDA_LAUNCH_CHECK();
 }
 
-void Exchange::plan_send(const uint32_t* d_own_k, const int32_t* d_n_own, const int32_t* d_zero,
-                         cudaStream_t s) {
-  const int c = static_cast<int>(cap);
-  const int ntiles = ceil_div(c, kTile);
-  const int gx = std::max(1, std::min(ntiles, num_sms() * 4));  // persistent, send table only
-  launch_pdl(plan_count_kernel, dim3(gx, 1), dim3(256), 0, s, d_own_k, d_zero, d_own_k, d_n_own,
-             c, tm, W, me, ntiles, tile_cnt, 1);
-  CUDA_LAUNCH_CHECK();
-  launch_pdl(plan_scan_tiles_kernel, dim3(1), dim3(512), 0, s, tile_cnt, ntiles, tile_off, totals, d_zero, d_n_own);
-  CUDA_LAUNCH_CHECK();
-  launch_pdl(plan_rank_kernel, dim3(gx, 1), dim3(256), 0, s, d_own_k, d_zero, d_own_k, d_n_own,
-             c, tm, W, me, ntiles, tile_off, totals, sscan, lpos, 1);
-  CUDA_LAUNCH_CHECK();
-}
-
 void Exchange::send_plan_counted(const int32_t* d_n_own, cudaStream_t s) {
   const int c = static_cast<int>(cap);
   const int ntiles = ceil_div(c, kTile);

@@ -83,10 +83,6 @@ struct Exchange {
   void plan(const uint32_t* d_vid, int64_t n_global, int64_t per_worker, const uint32_t* d_uniq,
             const int32_t* d_U, const uint32_t* d_own_k, const int32_t* d_n_own, cudaStream_t s,
             const PhaseHook& hook = PhaseHook{});
-  // the send plan alone (sscan, totals[8..16)) over my owned uniques with tm already filled
-  // (owner-sharded manager, shardplan.cu): the receive plan is left empty
-  void plan_send(const uint32_t* d_own_k, const int32_t* d_n_own, const int32_t* d_zero,
-                 cudaStream_t s);
   // the send plan when the producer of the owned uniques already counted them per
   // (1024-row tile, destination) into tile_cnt (zeroed before) and own_k is the identity:
   // one kernel (shardplan.cu); writes sscan and totals[8..16)

@@ -406,8 +406,6 @@ void ShardPlan::init(int W_, int me_, int64_t n_, int64_t cap_) {
   CUDA_CHECK(cudaMalloc(&bits, sizeof(uint32_t) * nwords));
   CUDA_CHECK(cudaMemset(bits, 0, sizeof(uint32_t) * nwords));
   CUDA_CHECK(cudaMalloc(&uslot, sizeof(uint32_t) * cap));
-  CUDA_CHECK(cudaMalloc(&zero, sizeof(int32_t)));
-  CUDA_CHECK(cudaMemset(zero, 0, sizeof(int32_t)));
   tiles.init(nwords);
 }
 
@@ -424,7 +422,7 @@ void ShardPlan::release() {
                   static_cast<void*>(cursor), static_cast<void*>(hkeys), static_cast<void*>(hpos),
                   static_cast<void*>(hmask_bits), static_cast<void*>(hslot),
                   static_cast<void*>(wpre), static_cast<void*>(bits),
-                  static_cast<void*>(uslot), static_cast<void*>(zero)})
+                  static_cast<void*>(uslot)})
     if (p) cudaFree(p);
   tiles.release();
   *this = ShardPlan();

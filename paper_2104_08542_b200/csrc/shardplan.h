@@ -47,7 +47,6 @@ struct ShardPlan {
   uint32_t* wpre = nullptr;           // [nwords] set bits before each word
   int64_t nwords = 0;
   uint32_t* uslot = nullptr;          // [cap] slot per owned unique
-  int32_t* zero = nullptr;            // a device zero (empty receive plan)
   ScanTiles tiles;
   static constexpr int kInbox = 80;
 
