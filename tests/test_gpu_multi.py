@@ -8,6 +8,10 @@ the same W-worker system.
 * test_multi_rank_overlap (tests/mp_overlap_worker.py): steps kept in flight (the
   pipelined manager of step t+1 overlapping step t's training across ranks), the
   fallback transports, final state against the oracle's multi-step trajectory.
+* The owner-routed exchange runs the owner-sharded manager stage by default;
+  test_multi_rank_parity_replicated_manager keeps the replicated one covered, and
+  test_multi_rank_out_of_vocab (tests/mp_oov_worker.py) checks the bad-id gate across ranks
+  for the sharded, replicated and all-reduce paths.
 Skipped with fewer GPUs than ranks."""
 import os
 import socket
